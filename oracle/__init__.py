@@ -1,0 +1,194 @@
+"""CPU oracle for the BSN-TEM data-parallel step and the paper's ring allreduce.
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and the
+``cpu_baseline`` / ``--impl reference`` legs of ``bench.py`` may import this
+package.  The product package ``paper_1906_06496_b200`` never imports it, and
+the two share no code.
+
+The arithmetic lives in ``tem_oracle.cpp`` (plain C++, fp64 ground truth, fp32
+ring replay, ``-ffp-contract=off``); this module only builds it with g++ and
+marshals numpy arrays through ctypes.  Every function cites the passage it
+follows in the C++ source.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "tem_oracle.cpp")
+_LIB = os.path.join(_HERE, "libtem_oracle.so")
+_lock = threading.Lock()
+_lib = None
+
+SUM, MEAN = 0, 1
+
+
+def build(force: bool = False) -> str:
+    """Compile tem_oracle.cpp -> libtem_oracle.so (plain g++, no fast math)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call([
+            "g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math",
+            "-fno-unsafe-math-optimizations", "-shared", "-fPIC", _SRC, "-o", tmp,
+        ])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            L = ctypes.CDLL(_LIB)
+            i64, i32, f32 = ctypes.c_int64, ctypes.c_int, ctypes.c_float
+            P = ctypes.c_void_p
+            L.orc_kpad.restype = i64
+            L.orc_kpad.argtypes = [i64, i32, i32]
+            for fn in (L.orc_scatter_schedule, L.orc_gather_schedule):
+                fn.restype = i32
+                fn.argtypes = [i32, i32, i32, ctypes.POINTER(i32), ctypes.POINTER(i32)]
+            L.orc_ring_allreduce_f32.restype = i32
+            L.orc_ring_allreduce_f32.argtypes = [P, i32, i64, i32, P]
+            L.orc_ring_sgd_f32.restype = i32
+            L.orc_ring_sgd_f32.argtypes = [P, P, i32, i64, i32, f32]
+            L.orc_ring_chain_f32.restype = i32
+            L.orc_ring_chain_f32.argtypes = [P, i32, i64, i32, P]
+            L.orc_ps_allreduce_f32.restype = i32
+            L.orc_ps_allreduce_f32.argtypes = [P, i32, i64, i32, P]
+            L.orc_bf16_bits.restype = ctypes.c_uint16
+            L.orc_bf16_bits.argtypes = [f32]
+            L.orc_tem_num_params.restype = i64
+            L.orc_tem_num_params.argtypes = [i32, i32, i32]
+            L.orc_tem_fwd_bwd.restype = i32
+            L.orc_tem_fwd_bwd.argtypes = [i32, i32, i32, i32, i32, i32, P, P, P, P, P, P, P]
+            _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+# --------------------------------------------------------------------------- partition / schedules
+def kpad(K: int, N: int, V: int = 4) -> int:
+    """K_pad = roundup(K, N*V)."""
+    r = lib().orc_kpad(K, N, V)
+    if r < 0:
+        raise ValueError("invalid partition arguments")
+    return int(r)
+
+
+def scatter_schedule(rank: int, N: int, rnd: int):
+    """send (n-i)%N, receive (n-i-1)%N."""
+    s, r = ctypes.c_int(), ctypes.c_int()
+    if lib().orc_scatter_schedule(rank, N, rnd, ctypes.byref(s), ctypes.byref(r)):
+        raise ValueError("round out of range")
+    return s.value, r.value
+
+
+def gather_schedule(rank: int, N: int, rnd: int):
+    """P:152 with reading R10: send (n+1-k)%N, receive (n-k)%N."""
+    s, r = ctypes.c_int(), ctypes.c_int()
+    if lib().orc_gather_schedule(rank, N, rnd, ctypes.byref(s), ctypes.byref(r)):
+        raise ValueError("round out of range")
+    return s.value, r.value
+
+
+# --------------------------------------------------------------------------- ring / PS replay
+def ring_allreduce(grads: np.ndarray, op: int = SUM):
+    """Round-by-round ring replay.  grads: [N][K_pad] float32.
+
+    Returns (out [N][K_pad] float32, sent_elems [N] int64)."""
+    g = np.ascontiguousarray(grads, dtype=np.float32).copy()
+    N, K_pad = g.shape
+    sent = np.zeros(N, dtype=np.int64)
+    if lib().orc_ring_allreduce_f32(_ptr(g), N, K_pad, op, _ptr(sent)):
+        raise ValueError("invalid ring arguments")
+    return g, sent
+
+
+def ring_chain(grads: np.ndarray, op: int = SUM) -> np.ndarray:
+    """Per-element chain form: [K_pad] float32."""
+    g = np.ascontiguousarray(grads, dtype=np.float32)
+    N, K_pad = g.shape
+    out = np.empty(K_pad, dtype=np.float32)
+    if lib().orc_ring_chain_f32(_ptr(g), N, K_pad, op, _ptr(out)):
+        raise ValueError("invalid ring arguments")
+    return out
+
+
+def ring_sgd(grads: np.ndarray, params: np.ndarray, lr: float, op: int = MEAN) -> np.ndarray:
+    """Ring allreduce + owner SGD (fma(-lr, gbar, w)) + gather of weights.
+
+    grads [N][K_pad] f32; params [K_pad] f32 (identical on all ranks on entry).
+    Returns params after the step, [N][K_pad] float32."""
+    g = np.ascontiguousarray(grads, dtype=np.float32)
+    N, K_pad = g.shape
+    p = np.ascontiguousarray(np.broadcast_to(np.asarray(params, np.float32), (N, K_pad))).copy()
+    if lib().orc_ring_sgd_f32(_ptr(g), _ptr(p), N, K_pad, op, float(lr)):
+        raise ValueError("invalid ring arguments")
+    return p
+
+
+def ps_allreduce(grads: np.ndarray, op: int = SUM) -> np.ndarray:
+    """Parameter-server comparator (ascending-rank sum)."""
+    g = np.ascontiguousarray(grads, dtype=np.float32)
+    N, K = g.shape
+    out = np.empty(K, dtype=np.float32)
+    if lib().orc_ps_allreduce_f32(_ptr(g), N, K, op, _ptr(out)):
+        raise ValueError("invalid PS arguments")
+    return out
+
+
+def bf16_round(a: np.ndarray) -> np.ndarray:
+    """fp32 -> bf16 (RNE bit rule) -> fp32, elementwise (reading R8)."""
+    f = np.ascontiguousarray(a, dtype=np.float32).ravel()
+    L = lib()
+    bits = np.fromiter((L.orc_bf16_bits(float(v)) for v in f), dtype=np.uint32, count=f.size)
+    return (bits << 16).view(np.float32).reshape(np.shape(a))
+
+
+# --------------------------------------------------------------------------- TEM
+def num_params(Cin: int = 400, C: int = 512, Co: int = 3) -> int:
+    return int(lib().orc_tem_num_params(Cin, C, Co))
+
+
+def tem_fwd_bwd(x, params, labels, lam=(1.0, 1.0, 1.0), prec: int = 0, C: int = 512):
+    """BSN-TEM forward + weighted logistic loss + backward.
+
+    x [B][T][Cin], params flat (fp32 values, any float dtype), labels [B][Co][T].
+    prec 0 = fp64, 1 = bf16-operand emulation (reading R8).
+    Returns dict(loss [1+Co] f64, z [B][T][Co] f64, grad [K] f64)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    B, T, Cin = x.shape
+    labels = np.ascontiguousarray(labels, dtype=np.float64)
+    Co = labels.shape[1]
+    K = num_params(Cin, C, Co)
+    p = np.ascontiguousarray(np.asarray(params, dtype=np.float64)[:K])
+    assert p.size == K, (p.size, K)
+    lam = np.ascontiguousarray(lam, dtype=np.float64)
+    loss = np.zeros(1 + Co)
+    z = np.zeros((B, T, Co))
+    grad = np.zeros(K)
+    rc = lib().orc_tem_fwd_bwd(prec, B, T, Cin, C, Co, _ptr(x), _ptr(p), _ptr(labels), _ptr(lam),
+                               _ptr(loss), _ptr(z), _ptr(grad))
+    if rc:
+        raise ValueError("invalid TEM arguments")
+    return {"loss": loss, "z": z, "grad": grad}
+
+
+def param_slices(Cin: int = 400, C: int = 512, Co: int = 3):
+    """Flat gradient order [W1, b1, W2, b2, W3, b3] (SURVEY 8(c) layouts)."""
+    sizes = [("W1", C * 3 * Cin), ("b1", C), ("W2", C * 3 * C), ("b2", C), ("W3", Co * C), ("b3", Co)]
+    out, off = {}, 0
+    for name, n in sizes:
+        out[name] = slice(off, off + n)
+        off += n
+    return out
