@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""bench.py -- data-parallel BSN-TEM training throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c1] [--impl ours|reference]
+
+One "step" = one pass of the whole hot path over one batch per
+rank: conv1/conv2 forward, head + weighted logistic loss, backward, and the fused ring
+allreduce + mean + SGD (tem_step through the C ABI).  N > 1 runs under torchrun, one
+process per GPU (weak scaling: B per GPU fixed).  Rank 0 prints ONE JSON line.
+
+Timing: W untimed warm-up steps; then K timed steps, each bracketed by CUDA events on the
+launching stream, with a 256 MiB L2 flush (outside the events) between steps; barrier +
+synchronize on both sides of the timed region; the max over ranks is reported.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TEM train samples/sec at 1/2/4/8 B200; ring-allreduce bus GB/s vs NCCL"
+UNIT = "samples/s"
+WORKLOADS = {
+    "c1": dict(desc="configs[0]: BSN TEM (400->512->512->3 conv1d, T=100) one data-parallel SGD step, "
+                    "batch 4/rank, fp32", B=4, prec=0, dtype="f32"),
+    "c2": dict(desc="configs[1]: BSN TEM fp32 training, batch 16/GPU, synthetic ActivityNet-shaped "
+                    "features", B=16, prec=0, dtype="f32"),
+    "c3": dict(desc="configs[2]: BSN TEM bf16-operand/fp32-accumulate training, batch 256/GPU", B=256,
+               prec=1, dtype="bf16 operands, f32 accumulate"),
+}
+T, CIN, C = 100, 400, 512
+# Algorithmic FLOPs per sample of each kernel (dense count incl. zero-pad taps).
+FLOPS_PER_SAMPLE = {
+    "conv1_fwd": 2 * T * C * 3 * CIN,      # 122.88 M
+    "conv2_fwd": 2 * T * C * 3 * C,        # 157.29 M
+    "conv2_dgrad": 2 * T * C * 3 * C,      # 157.29 M
+    "conv2_wgrad": 2 * T * C * 3 * C,      # 157.29 M
+    "conv1_wgrad": 2 * T * C * 3 * CIN,    # 122.88 M
+}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(workload: dict, videos: int):
+    """The oracle as it stands (plain single-threaded C++, fp64 / bf16-emulated fp64) timed on a
+    bounded sample of the same workload: `videos` videos of forward+loss+backward, plus the
+    fp32 ring replay of the 1,403,395-element gradient at N=2."""
+    import numpy as np
+    import datagen
+    import oracle
+    oracle.lib()
+    x = datagen.features(videos, rank=0, batch_idx=0)
+    lab = datagen.labels(videos, rank=0, batch_idx=0)
+    p = datagen.init_params()
+    t0 = time.perf_counter()
+    oracle.tem_fwd_bwd(x, p, lab, prec=workload["prec"])
+    g = np.zeros((2, oracle.kpad(1403395, 2)), np.float32)
+    oracle.ring_sgd(g, np.zeros(g.shape[1], np.float32), 0.01)
+    dt = time.perf_counter() - t0
+    return {"value": videos / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{videos} videos ({'fp64' if workload['prec'] == 0 else 'bf16-emulated fp64'} "
+                      f"fwd+loss+bwd, T=100, 400->512->512->3) + fp32 ring/SGD replay of K=1403395 at N=2; "
+                      f"{dt:.1f} s single-threaded"}
+
+
+def run_reference(args, workload):
+    """--impl reference: the CPU oracle on this arm's config/metric/unit (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np
+    import datagen
+    import oracle
+    oracle.lib()
+    p = datagen.init_params()
+    per_step = 1  # one video of the workload per step: a bounded sample
+    x = datagen.features(per_step, rank=0, batch_idx=0)
+    lab = datagen.labels(per_step, rank=0, batch_idx=0)
+    for _ in range(args.warmup):
+        oracle.tem_fwd_bwd(x, p, lab, prec=workload["prec"])
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.tem_fwd_bwd(x, p, lab, prec=workload["prec"])
+    dt = time.perf_counter() - t0
+    v = per_step * args.steps / dt
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic", "config": {"workload": workload["desc"], "batch_per_gpu": workload["B"],
+                                           "seq_len": T, "parallelism": f"dp{args.gpus}"},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                            "sample": f"{per_step} video per step, {args.steps} steps, single-threaded "
+                                      f"C++ oracle ({'fp64' if workload['prec'] == 0 else 'bf16-emulated fp64'})"},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--pool", type=int, default=8, help="resident input batches per rank")
+    ap.add_argument("--cpu-videos", type=int, default=16)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--lr", type=float, default=0.01)
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, wl)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import datagen
+    from paper_1906_06496_b200 import tem
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            print(json.dumps({"error": "run N>1 under torchrun (one process per GPU)"}))
+            return 2
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    B, prec = wl["B"], wl["prec"]
+    sc = tem.SessionConfig(world_size=world, rank=rank, local_ranks=1, batch_per_rank=B, precision=prec,
+                           lr=args.lr)
+    t_init0 = time.perf_counter()
+    sess = tem.TemSession(sc, datagen.init_params(), device=local)
+    t_init = time.perf_counter() - t_init0
+
+    # resident input pool (HBM); rank r's shard of global batch k uses seeds (r, k)
+    xs, labs = [], []
+    for k in range(args.pool):
+        x = datagen.features(B, rank=rank, batch_idx=k)
+        lab = datagen.labels(B, rank=rank, batch_idx=k)
+        if prec == 1:
+            xs.append(torch.from_numpy(datagen.to_bf16_bits(x).view(np.int16)).to(dev))
+        else:
+            xs.append(torch.from_numpy(x).to(dev))
+        labs.append(torch.from_numpy(lab).to(dev))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    for i in range(args.warmup):
+        sess.step(xs[i % args.pool], labs[i % args.pool])
+    code, _ = sess.sync()
+    if code != 0:
+        raise tem.TemError(code, "warmup")
+
+    # ---------------- timed region (device value) ----------------
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    sess.timing_begin(args.steps)
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        sess.step(xs[i % args.pool], labs[i % args.pool])
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    slot_ms, nrec = sess.timing_end()
+    code, _ = sess.sync()
+    if code != 0:
+        raise tem.TemError(code, "timed steps")
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+    total_ms = float(tot.item())
+    ms_per_step = total_ms / args.steps
+    value = world * B * args.steps / (total_ms / 1e3)
+    launches = sess.launches_per_step()
+
+    # ---------------- end to end through the C ABI with host buffers ----------------
+    e2e = None
+    if not args.no_e2e:
+        if prec == 1:
+            xh = [torch.from_numpy(datagen.to_bf16_bits(datagen.features(B, rank=rank, batch_idx=k)).view(np.int16)).pin_memory()
+                  for k in range(2)]
+        else:
+            xh = [torch.from_numpy(datagen.features(B, rank=rank, batch_idx=k)).pin_memory() for k in range(2)]
+        lh = [torch.from_numpy(datagen.labels(B, rank=rank, batch_idx=k)).pin_memory() for k in range(2)]
+        loss_h = torch.zeros(4, dtype=torch.float32).pin_memory()
+        for i in range(2):
+            sess.step_host(xh[i], lh[i], loss_h)
+        torch.cuda.synchronize()
+        ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        barrier()
+        torch.cuda.synchronize()
+        for i in range(args.steps):
+            flush.zero_()
+            ev2[i][0].record(stream)
+            sess.step_host(xh[i % 2], lh[i % 2], loss_h)
+            ev2[i][1].record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        code, _ = sess.sync()
+        if code != 0:
+            raise tem.TemError(code, "e2e steps")
+        t2 = torch.tensor([sum(a.elapsed_time(b) for a, b in ev2)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * B * args.steps / (float(t2.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(xh[0].numel() * xh[0].element_size() + lh[0].numel() * 4),
+               "d2h_bytes_per_step": 16, "api": "tem_step_host"}
+
+    # ---------------- roofline of the dominant kernel ----------------
+    peaks, peak_src = load_peaks()
+    conv = {k: v for k, v in slot_ms.items() if k in FLOPS_PER_SAMPLE}
+    dom = max(conv, key=conv.get) if nrec else None
+    roof = None
+    if dom:
+        avg_s = conv[dom] / nrec / 1e3
+        achieved = FLOPS_PER_SAMPLE[dom] * B / avg_s / 1e12
+        kpath = sess.kernel_path()
+        if kpath.startswith("simt"):
+            peak = 148 * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12
+            roof = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": None,
+                    "peak_source": f"FP32 FMA: 148 SM x 128 lanes x 2 x {peaks['sm_max_mhz']:.0f} MHz "
+                                   f"(sm_max_mhz, {peak_src}) -- DESIGN.md 7"}
+        else:
+            key = "bf16_tflops_sustained"
+            bf16 = peaks.get(key, peaks.get("bf16_tflops"))
+            peak = bf16 if prec == 1 else bf16 / 2.0
+            roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                    "frac": achieved / peak, "traffic": None,
+                    "peak_source": f"{key} ({peak_src})" + ("" if prec == 1 else " x 1/2 (tf32:bf16 nominal ratio)")}
+        tr = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tr):
+            try:
+                t = json.load(open(tr)).get(f"{args.workload}/{kpath}/{dom}")
+                roof["traffic"] = t
+            except Exception:
+                pass
+        roof["share_of_step"] = conv[dom] / max(sum(slot_ms.values()), 1e-9)
+        roof["slot_ms_per_step"] = {k: v / max(nrec, 1) for k, v in slot_ms.items()}
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": wl["dtype"], "data": "synthetic (seeded ActivityNet-shaped features/labels, random-init weights)",
+        "config": {"workload": wl["desc"], "batch_per_gpu": B, "global_batch": B * world, "seq_len": T,
+                   "channels": "400->512->512->3", "parallelism": f"dp{world}",
+                   "exchange": "fused ring allreduce + mean + SGD (KR1)" if world > 1 else "N=1: owner SGD only",
+                   "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                   "kernel_path": sess.kernel_path()},
+        "gpu_launches": launches * args.steps,
+        "launches_per_step": launches,
+        "roofline": roof,
+        "e2e": e2e,
+        "clocks": clk,
+        "t3_init_s": t_init,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(wl, args.cpu_videos)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    sess.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

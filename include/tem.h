@@ -1,0 +1,184 @@
+/* ============================================================================
+ * tem.h -- C ABI of libtem.so: the data-parallel BSN-TEM training step of
+ * arXiv 1906.06496 with its ring allreduce, for NVIDIA B200 (sm_100a).
+ *
+ * Citations: "P:n" = PAPER.md line n; "S:n" = SPEC.md line n; "SURVEY 8(x)" =
+ * the hot-path scope table in SURVEY.md section 8.  Readings R1..R16 of the
+ * paper are listed in DESIGN.md section 3.
+ *
+ * Plain C: every pointer is a raw host or device address, every size a plain
+ * integer.  `stream` arguments are a cudaStream_t passed as void* (NULL = the
+ * legacy default stream).  No torch type appears here.
+ *
+ * Ownership.  The CALLER owns all device memory: parameters, the symmetric
+ * heap of every rank, the workspace, inputs and outputs.  The library borrows
+ * these pointers for the lifetime of the context and allocates no device
+ * memory itself; it heap-allocates only its opaque host-side context (and a
+ * 64-byte pinned, device-mapped status word through which kernels latch
+ * errors).
+ *
+ * Asynchrony and errors.  Calls enqueue work on `stream` and return after
+ * enqueue.  Host-detectable errors return immediately (INVALID_ARG, CUDA,
+ * STATE).  Errors detected on the device (PROTOCOL, TRANSPORT, NONFINITE) are
+ * latched in the context and returned by the NEXT call on that context (or by
+ * tem_shutdown / tem_sync); after such an error the contents of params / buf
+ * are unspecified.  No function throws, aborts or exits.
+ *
+ * Collective semantics.  With world_size N > 1 every rank calls
+ * tem_step / tem_exchange / ring_allreduce in the same order with equal
+ * arguments; calls on one context are not reentrant.
+ * ==========================================================================*/
+#ifndef TEM_H_
+#define TEM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TEM_OK = 0,
+    TEM_ERR_INVALID_ARG = 1, /* bad dims, N <= 0, pointer outside the symmetric heap   */
+    TEM_ERR_PROTOCOL = 2,    /* ranks disagree on K; detected via the ring's flags    */
+    TEM_ERR_TRANSPORT = 3,   /* a peer flag did not arrive within the spin bound     */
+    TEM_ERR_CUDA = 4,        /* a CUDA launch / API call failed                               */
+    TEM_ERR_NONFINITE = 5,   /* non-finite loss; tem_sync reports the step index      */
+    TEM_ERR_STATE = 6        /* call on a shut-down or NULL context                           */
+} tem_status;
+
+typedef enum { TEM_SUM = 0, TEM_MEAN = 1 } tem_reduce_op;
+typedef enum { TEM_FP32 = 0, TEM_BF16 = 1 } tem_precision;    /* BASELINE configs[1]/[2]   */
+
+#define TEM_MAX_RANKS 8
+
+typedef struct tem_ctx tem_ctx; /* opaque, owned by the library */
+
+typedef struct {
+    /* --- cluster (SPEC WorkerId / ClusterConfig; "N is the number of GPU") */
+    int32_t rank;        /* this process's first rank, 0 <= rank < world_size               */
+    int32_t world_size;  /* N, 1 <= N <= TEM_MAX_RANKS                                       */
+    int32_t device;      /* CUDA device ordinal                                              */
+    int32_t local_ranks; /* ranks driven by this process on `device`: 1 in production (one
+                            process per GPU); == world_size for the single-device emulation
+                            used by the tests, where the N ranks run as CTA groups of one
+                            cooperative launch over same-device "peer" heaps               */
+    /* --- model ("temporal network with 3 convolution layers"; shapes BASELINE.json)  */
+    int32_t batch_per_rank; /* B >= 0 videos per rank per step (P:113 data parallelism)     */
+    int32_t seq_len;        /* T >= 1 snippets per video (100 in the paper's setup)          */
+    int32_t c_in;           /* 400 two-stream feature dims; multiple of 16           */
+    int32_t c_hidden;       /* 512; multiple of 128, at most 512                             */
+    int32_t c_out;          /* 3: actionness, start, end (reading R4); must be 3             */
+    int32_t precision;      /* tem_precision: TEM_FP32 (fp32 operands, fp32 accumulate) or
+                               TEM_BF16 (bf16 operands, fp32 accumulate; reading R8)          */
+    float lr;               /* SGD step size >= 0 (S:272 vs S:278 resolved: 0 allowed)       */
+    float loss_weight[3];   /* lambda_action, lambda_start, lambda_end (reading R6)          */
+    /* --- symmetric memory (one heap per rank, all mapped in this process)                  */
+    void* const* peer_bufs; /* [world_size] base of each rank's heap as mapped here (for
+                               local_ranks == world_size all are on `device`)                 */
+    size_t sym_bytes;       /* capacity of each heap, >= tem_sym_bytes(cfg)                   */
+    int64_t max_allreduce_elems; /* largest K ring_allreduce will be called with (sizes the
+                                    staging area); 0 -> the TEM gradient size               */
+    /* --- workspace                                                                         */
+    void* workspace;        /* device, 256-byte aligned, >= tem_workspace_bytes(cfg)          */
+    size_t workspace_bytes;
+    /* --- ring tuning (0 = automatic)                                                       */
+    int32_t ring_channels;  /* G: CTAs per rank in the ring kernel                           */
+    int32_t ring_chunks;    /* C: pipelined sub-chunks per channel per block                 */
+} tem_config;
+
+/* --- sizes -----------------------------------------------------------------------------
+ * K      = c_hidden*3*c_in + c_hidden + c_hidden*3*c_hidden + c_hidden + 3*c_hidden + 3
+ *          (flat order [W1, b1, W2, b2, W3, b3]; W1 [c_hidden][3][c_in],
+ *          W2 [c_hidden][3][c_hidden], W3 [3][c_hidden]; reading R3)
+ * K_pad  = roundup(K, 4*world_size)  (N equal 16-byte aligned blocks)
+ * Return 0 on invalid cfg. */
+int64_t tem_num_params(const tem_config* cfg);
+int64_t tem_kpad(const tem_config* cfg, int64_t K);
+size_t tem_workspace_bytes(const tem_config* cfg);
+/* Per-rank symmetric heap layout (offsets are identical on every rank):
+ *   [0, 4*K_pad)                 params (fp32 master weights)
+ *   [off_user, off_user + 4*max) user region for ring_allreduce buffers
+ *   then the ring staging area and the flag area (library-private).
+ * The caller zero-fills the whole heap once before tem_init on every rank. */
+size_t tem_sym_bytes(const tem_config* cfg);
+size_t tem_sym_user_offset(const tem_config* cfg);
+
+/* --- lifecycle ---------------------------------------------------------------------------
+ * tem_init: validates cfg, lays out workspace and heap, and binds `params`, which must be
+ * the first 4*K_pad bytes of this rank's heap (peer_bufs[rank]) and hold the initial
+ * weights, bitwise identical on every rank ("all of GPUs have the same CNN model").
+ * For local_ranks > 1, params of rank r are peer_bufs[r]; `params` must equal
+ * peer_bufs[rank].  Returns INVALID_ARG / CUDA; *out = NULL on failure. */
+tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out);
+
+/* tem_step = tem_compute + tem_exchange: one synchronous data-parallel SGD step.
+ *   x       device, [local_ranks][B][T][c_in], fp32 (TEM_FP32) or bf16 bits (TEM_BF16),
+ *           row-major channels-last; rank r's shard of the global batch.
+ *   labels  device, [local_ranks][B][3][T] fp32 in [0,1] (channel 0 action, 1 start, 2 end).
+ *   loss_out device, [local_ranks][4] fp32: total, action, start, end -- the LOCAL batch
+ *           mean (reading R5/R6) of this step, before the update.
+ * After the call completes, params are bitwise identical on every rank because the
+ * ring's gather carries the updated weights. */
+tem_status tem_step(tem_ctx* ctx, const void* x, const float* labels, float* loss_out,
+                    void* stream);
+/* t1 of P:163 only: forward + loss + backward into the local gradient buffer. */
+tem_status tem_compute(tem_ctx* ctx, const void* x, const float* labels, float* loss_out,
+                       void* stream);
+/* t2 of P:163 only: ring allreduce (Mean) of the local gradients fused with the owner's
+ * SGD update w = fma(-lr, gbar, w) and the gather of the updated weights. */
+tem_status tem_exchange(tem_ctx* ctx, void* stream);
+/* tem_step with HOST buffers (pinned recommended): copies x and labels host->device into
+ * the workspace, runs the step, copies loss (local_ranks*4 floats) device->host, all on
+ * `stream`.  The end-to-end path a user calls. */
+tem_status tem_step_host(tem_ctx* ctx, const void* x_host, const float* labels_host,
+                         float* loss_host, void* stream);
+
+/* ring_allreduce: in-place allreduce of K fp32 elements.
+ *   buf   device; must be the user region of this rank's heap, i.e.
+ *         peer_bufs[rank] + tem_sym_user_offset(cfg) (the same offset on every rank);
+ *         for local_ranks > 1 every emulated rank's user region is reduced.
+ *   K     1 <= K <= max_allreduce_elems (equal on every rank, else PROTOCOL).  The partition
+ *         pads K to K_pad = roundup(K, 4N); elements >= K are neither read nor written.
+ *   op    TEM_SUM or TEM_MEAN (mean = s * fl(1/N), once, on the block owner; reading R11).
+ * Result is bitwise identical on every rank and equals the oracle's ring replay bit for bit:
+ * block b is summed along the chain g_b + g_{b+1} + ... + g_{b+N-1}. */
+tem_status ring_allreduce(tem_ctx* ctx, float* buf, int64_t K, int32_t op, void* stream);
+
+/* Parameter-server comparator: every rank pushes its buffer into
+ * rank 0's heap; rank 0 sums in ascending rank order, applies op, and pushes the
+ * result back to every rank.  Same buffer rules as ring_allreduce. */
+tem_status ps_allreduce(tem_ctx* ctx, float* buf, int64_t K, int32_t op, void* stream);
+
+/* Blocks until all work of ctx on `stream` is done; returns the latched device status.
+ * For NONFINITE, *bad_step (if non-NULL) receives the 0-based step index. */
+tem_status tem_sync(tem_ctx* ctx, void* stream, int64_t* bad_step);
+
+/* Collective teardown.  NULL is a no-op (returns TEM_OK).  Returns any latched error. */
+tem_status tem_shutdown(tem_ctx* ctx);
+
+/* --- introspection for tests and benchmarks (device pointers owned by the workspace) --- */
+float* tem_local_grad(tem_ctx* ctx, int32_t local_rank); /* [K_pad] fp32, last tem_compute */
+float* tem_logits(tem_ctx* ctx, int32_t local_rank);     /* [B][T][3] fp32 z, last compute */
+/* Number of kernels one tem_step / tem_exchange / ring_allreduce(K) enqueues. */
+int32_t tem_launches_per_step(tem_ctx* ctx);
+int32_t tem_launches_per_exchange(tem_ctx* ctx);
+const char* tem_status_string(int32_t status);
+/* Per-kernel timing for benchmarks (local_ranks == 1 only).  tem_timing_begin creates
+ * host-side CUDA events for up to max_steps subsequent tem_step / tem_step_host calls and
+ * brackets every kernel of each step with a start/stop event on the launching stream.
+ * tem_timing_end synchronises those events, writes the per-slot SUM over recorded steps
+ * (milliseconds) into sum_ms[tem_timing_slots()], the number of recorded steps into
+ * *steps, destroys the events and disables timing. */
+int32_t tem_timing_slots(tem_ctx* ctx);
+const char* tem_timing_slot_name(tem_ctx* ctx, int32_t slot);
+tem_status tem_timing_begin(tem_ctx* ctx, int32_t max_steps);
+tem_status tem_timing_end(tem_ctx* ctx, float* sum_ms, int32_t* steps);
+/* Kernel-path description (e.g. "simt-fp32", "tcgen05-bf16") for reports. */
+const char* tem_kernel_path(tem_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TEM_H_ */

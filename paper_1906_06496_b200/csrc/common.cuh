@@ -1,0 +1,68 @@
+// common.cuh -- device helpers private to libtem (never shared with oracle/).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/tem.h"
+
+#define TEM_DEV __device__ __forceinline__
+
+namespace tem {
+
+// Operand storage types.  fp32 path: float everywhere; bf16 path: bf16 operands
+// (reading R8), fp32 accumulate.
+TEM_DEV float to_f(float v) { return v; }
+TEM_DEV float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
+template <typename T> TEM_DEV T from_f(float v);
+template <> TEM_DEV float from_f<float>(float v) { return v; }
+template <> TEM_DEV __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+// Load 8 consecutive operand elements as floats (16B / 32B aligned).
+TEM_DEV void load8(const float* p, float* v) {
+    float4 a = *reinterpret_cast<const float4*>(p);
+    float4 b = *reinterpret_cast<const float4*>(p + 4);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+}
+TEM_DEV void load8(const __nv_bfloat16* p, float* v) {
+    uint4 u = *reinterpret_cast<const uint4*>(p);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        v[2 * i] = __uint_as_float(w[i] << 16);
+        v[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+    }
+}
+
+// ---- system-scope flag primitives (ring protocol, cross-GPU over NVLink) ----------------
+TEM_DEV uint64_t ld_acquire_sys(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+TEM_DEV void st_release_sys(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+TEM_DEV uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// L2-coherent 128-bit load (bypasses L1: data written by a peer GPU lands in our L2).
+TEM_DEV float4 ld_cg4(const float* p) { return __ldcg(reinterpret_cast<const float4*>(p)); }
+
+// Device-side error latch (host-mapped pinned word): first error wins.
+struct Status {
+    int32_t code;      // tem_status
+    int32_t pad;
+    int64_t step;      // step index for NONFINITE
+};
+TEM_DEV void latch(Status* s, int32_t code, int64_t step) {
+    if (atomicCAS(&s->code, 0, code) == 0) {
+        s->step = step;
+        __threadfence_system();
+    }
+}
+
+}  // namespace tem

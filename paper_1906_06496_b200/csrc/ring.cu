@@ -1,0 +1,353 @@
+// ring.cu -- KR1: the paper's ring allreduce over NVLink peer memory,
+// with the 1/N mean and the SGD update fused into the block owner (SURVEY 8(a)
+// rows a9-a12), plus the parameter-server comparator KP1.
+//
+// Protocol (one launch per rank per collective; grid = G channels x local ranks):
+//   * The gradient of K_pad elements is split into N equal blocks (row a9); each
+//     block into G*C pieces; channel g (a CTA) owns pieces g*C .. g*C+C-1 of every
+//     block, so the chain order of every element is independent of G and C.
+//   * Scatter round i = 0..N-2: rank n sends block s = (n-i) mod N.  The
+//     message is own[s] (+ the partial received from the left in round i-1), pushed
+//     with 128-bit stores straight into the right neighbour's staging slot i; then a
+//     release flag.  So block b is summed along g_b + g_{b+1} + ... + g_{b+N-1}
+//     (SURVEY 8(c) c.1), bit-identical to the oracle's round-by-round replay.
+//   * After round N-2, rank n owns block (n+1) mod N: it adds the last
+//     partial, applies mean (s * fl(1/N)) and, in SGD mode, w = fma(-lr, gbar, w),
+//     then pushes the RESULT into the right neighbour's destination buffer (gather
+//     round 0, fused).
+//   * Gather round k = 1..N-2 (reading R10): forward the block received in
+//     round k-1 (send (n+1-k) mod N) -- replace, never add.
+//   * Flags are 64-bit words [epoch:32 | K tag:31 | 0] in the receiver's heap, one per
+//     (phase, round, channel, chunk).  Epochs are per-channel counters that advance by
+//     one per collective on every rank, so no flag is ever reset.  A flag whose K tag
+//     differs from the receiver's K latches PROTOCOL (every rank sees a mismatch in the
+//     first round because K_pad and thus the tag differ).  A spin longer than spin_ns
+//     latches TRANSPORT and abandons the collective.
+// The same device code serves production (one process per GPU, peers over NVLink)
+// and the single-device emulation used by the tests (N ranks = N CTA groups of one
+// cooperative launch, "peer" heaps on the same device).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+
+namespace tem {
+namespace {
+
+constexpr int RING_THREADS = 512;
+
+TEM_DEV int modn(int a, int n) {
+    const int r = a % n;
+    return r < 0 ? r + n : r;
+}
+
+struct Piece {
+    int64_t v0, v1;  // vector (float4) range inside a block
+};
+TEM_DEV Piece piece_of(int64_t nvec, int G, int C, int g, int c) {
+    const int64_t q = (int64_t)g * C + c, GC = (int64_t)G * C;
+    return {q * nvec / GC, (q + 1) * nvec / GC};
+}
+
+TEM_DEV uint64_t flag_value(uint32_t epoch, int64_t K) {
+    return ((uint64_t)epoch << 32) | (uint64_t)((uint32_t)K & 0x7FFFFFFFu);
+}
+
+// Thread 0 waits for `flag` to reach `epoch`; returns false (CTA-uniform) on timeout.
+TEM_DEV bool wait_flag(const uint64_t* flag, uint32_t epoch, int64_t K, Status* st,
+                       uint64_t spin_ns, int* s_abort) {
+    if (threadIdx.x == 0) {
+        uint64_t v = ld_acquire_sys(flag);
+        if ((uint32_t)(v >> 32) < epoch) {
+            const uint64_t t0 = globaltimer();
+            do {
+                __nanosleep(64);
+                v = ld_acquire_sys(flag);
+                if ((uint32_t)(v >> 32) >= epoch) break;
+                if (globaltimer() - t0 > spin_ns) {
+                    latch(st, TEM_ERR_TRANSPORT, -1);
+                    *s_abort = 1;
+                    break;
+                }
+            } while (true);
+        }
+        if (!*s_abort && (uint32_t)v != ((uint32_t)K & 0x7FFFFFFFu)) latch(st, TEM_ERR_PROTOCOL, -1);
+    }
+    __syncthreads();
+    return *s_abort == 0;
+}
+
+TEM_DEV void signal_flag(uint64_t* flag, uint32_t epoch, int64_t K) {
+    __syncthreads();  // every thread's data stores precede thread 0's release (cumulative)
+    if (threadIdx.x == 0) st_release_sys(flag, flag_value(epoch, K));
+}
+
+TEM_DEV void store_shadow4(__nv_bfloat16* sh, int64_t e, float4 w) {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(w.x, w.y);
+    __nv_bfloat162 hi = __floats2bfloat162_rn(w.z, w.w);
+    uint2 u;
+    u.x = *reinterpret_cast<uint32_t*>(&lo);
+    u.y = *reinterpret_cast<uint32_t*>(&hi);
+    *reinterpret_cast<uint2*>(sh + e) = u;
+}
+
+// Masked vector helpers for ring_allreduce with K < K_pad (elements >= K untouched).
+TEM_DEV float4 ld4_masked(const float* p, int64_t e, int64_t K) {
+    if (e + 4 <= K) return *reinterpret_cast<const float4*>(p + e);
+    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (e + 0 < K) r.x = p[e + 0];
+    if (e + 1 < K) r.y = p[e + 1];
+    if (e + 2 < K) r.z = p[e + 2];
+    return r;
+}
+TEM_DEV float4 ldcg4_masked(const float* p, int64_t e, int64_t K) {
+    if (e + 4 <= K) return ld_cg4(p + e);
+    float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (e + 0 < K) r.x = __ldcg(p + e + 0);
+    if (e + 1 < K) r.y = __ldcg(p + e + 1);
+    if (e + 2 < K) r.z = __ldcg(p + e + 2);
+    return r;
+}
+TEM_DEV void st4_masked(float* p, int64_t e, int64_t K, float4 v) {
+    if (e + 4 <= K) {
+        *reinterpret_cast<float4*>(p + e) = v;
+        return;
+    }
+    if (e + 0 < K) p[e + 0] = v.x;
+    if (e + 1 < K) p[e + 1] = v.y;
+    if (e + 2 < K) p[e + 2] = v.z;
+}
+
+__global__ void __launch_bounds__(RING_THREADS) ring_kernel(const __grid_constant__ RingParams P) {
+    __shared__ uint32_t s_epoch;
+    __shared__ int s_abort;
+    const int l = blockIdx.y, g = blockIdx.x, tid = threadIdx.x;
+    const int N = P.N, n = P.rank_base + l, G = P.G, C = P.C;
+    const RingLocal& L = P.loc[l];
+    const int right = modn(n + 1, N);
+    char* heap_self = L.heaps[n];
+    char* heap_right = L.heaps[right];
+    const float* stage_self = reinterpret_cast<const float*>(heap_self + P.off_stage);
+    float* stage_right = reinterpret_cast<float*>(heap_right + P.off_stage);
+    const uint64_t* flags_self = reinterpret_cast<const uint64_t*>(heap_self + P.off_flags);
+    uint64_t* flags_right = reinterpret_cast<uint64_t*>(heap_right + P.off_flags);
+    float* dst_right = reinterpret_cast<float*>(heap_right + P.off_dst);
+    float* dst_self = L.dst_self;
+    const float* src = L.src;
+    const int64_t K = P.K, Bk = P.Kpad / N, nvec = Bk / 4;
+    const float inv_n = 1.0f / (float)N;
+    if (tid == 0) {
+        s_epoch = L.epochs[g] + 1;
+        s_abort = 0;
+    }
+    __syncthreads();
+    const uint32_t epoch = s_epoch;
+    // slot tied to (channel g, chunk c) forever: epochs of channel g only ever grow
+    auto fidx = [&](int phase, int round, int c) -> int64_t {
+        return (((int64_t)g * kMaxChunks + c) * 2 + phase) * (TEM_MAX_RANKS - 1) + round;
+    };
+
+    // ---------------- scatter: rounds 0..N-2 ----------------
+    for (int i = 0; i <= N - 2; ++i) {
+        const int s = modn(n - i, N);
+        for (int c = 0; c < C; ++c) {
+            const Piece pc = piece_of(nvec, G, C, g, c);
+            if (i > 0 && !wait_flag(flags_self + fidx(0, i - 1, c), epoch, K, P.status, P.spin_ns, &s_abort))
+                return;
+            for (int64_t v = pc.v0 + tid; v < pc.v1; v += RING_THREADS) {
+                const int64_t e = (int64_t)s * Bk + 4 * v;  // global element index
+                if (e >= K) continue;
+                float4 a = ld4_masked(src, e, K);
+                if (i > 0) {
+                    const float4 b = ld_cg4(stage_self + (int64_t)(i - 1) * Bk + 4 * v);
+                    a.x = a.x + b.x; a.y = a.y + b.y; a.z = a.z + b.z; a.w = a.w + b.w;
+                }
+                *reinterpret_cast<float4*>(stage_right + (int64_t)i * Bk + 4 * v) = a;
+            }
+            signal_flag(flags_right + fidx(0, i, c), epoch, K);
+        }
+    }
+    // ---------------- owner: last add, mean, SGD; gather round 0 fused ----------------
+    {
+        const int b = modn(n + 1, N);
+        for (int c = 0; c < C; ++c) {
+            const Piece pc = piece_of(nvec, G, C, g, c);
+            if (N > 1 && !wait_flag(flags_self + fidx(0, N - 2, c), epoch, K, P.status, P.spin_ns, &s_abort))
+                return;
+            for (int64_t v = pc.v0 + tid; v < pc.v1; v += RING_THREADS) {
+                const int64_t e = (int64_t)b * Bk + 4 * v;
+                if (e >= K) continue;
+                float4 a = ld4_masked(src, e, K);
+                if (N > 1) {
+                    const float4 r = ld_cg4(stage_self + (int64_t)(N - 2) * Bk + 4 * v);
+                    a.x = a.x + r.x; a.y = a.y + r.y; a.z = a.z + r.z; a.w = a.w + r.w;
+                }
+                if (P.op == TEM_MEAN) {
+                    a.x = a.x * inv_n; a.y = a.y * inv_n; a.z = a.z * inv_n; a.w = a.w * inv_n;
+                }
+                float4 out = a;
+                if (P.mode == 1) {
+                    const float4 w = *reinterpret_cast<const float4*>(dst_self + e);
+                    out.x = __fmaf_rn(-P.lr, a.x, w.x);
+                    out.y = __fmaf_rn(-P.lr, a.y, w.y);
+                    out.z = __fmaf_rn(-P.lr, a.z, w.z);
+                    out.w = __fmaf_rn(-P.lr, a.w, w.w);
+                    if (L.shadow) store_shadow4(L.shadow, e, out);
+                }
+                st4_masked(dst_self, e, K, out);
+                if (N > 1) st4_masked(dst_right, e, K, out);
+            }
+            if (N > 1) signal_flag(flags_right + fidx(1, 0, c), epoch, K);
+        }
+    }
+    // ---------------- gather rounds 1..N-2: forward what arrived ----------------
+    for (int k = 1; k <= N - 2; ++k) {
+        const int s = modn(n + 1 - k, N);
+        for (int c = 0; c < C; ++c) {
+            const Piece pc = piece_of(nvec, G, C, g, c);
+            if (!wait_flag(flags_self + fidx(1, k - 1, c), epoch, K, P.status, P.spin_ns, &s_abort)) return;
+            for (int64_t v = pc.v0 + tid; v < pc.v1; v += RING_THREADS) {
+                const int64_t e = (int64_t)s * Bk + 4 * v;
+                if (e >= K) continue;
+                const float4 a = ldcg4_masked(dst_self, e, K);
+                if (L.shadow) store_shadow4(L.shadow, e, a);
+                st4_masked(dst_right, e, K, a);
+            }
+            signal_flag(flags_right + fidx(1, k, c), epoch, K);
+        }
+    }
+    // ---------------- last gather round: receive block (n+2) mod N ----------------
+    if (N > 1) {
+        const int r = modn(n + 2, N);
+        for (int c = 0; c < C; ++c) {
+            const Piece pc = piece_of(nvec, G, C, g, c);
+            if (!wait_flag(flags_self + fidx(1, N - 2, c), epoch, K, P.status, P.spin_ns, &s_abort)) return;
+            if (L.shadow) {
+                for (int64_t v = pc.v0 + tid; v < pc.v1; v += RING_THREADS) {
+                    const int64_t e = (int64_t)r * Bk + 4 * v;
+                    store_shadow4(L.shadow, e, ld_cg4(dst_self + e));
+                }
+            }
+        }
+    }
+    if (tid == 0) L.epochs[g] = epoch;
+}
+
+// N = 1: the ring is the identity; the owner update alone.
+__global__ void sgd_single_kernel(const float* __restrict__ g, float* __restrict__ w,
+                                  __nv_bfloat16* __restrict__ shadow, int64_t n, int op, float lr) {
+    const int64_t nv = n / 4;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        float4 a = reinterpret_cast<const float4*>(g)[v];
+        if (op == TEM_MEAN) {  // fl(1/1) = 1: a * 1 is exact
+            a.x = a.x * 1.0f; a.y = a.y * 1.0f; a.z = a.z * 1.0f; a.w = a.w * 1.0f;
+        }
+        float4 x = reinterpret_cast<float4*>(w)[v];
+        x.x = __fmaf_rn(-lr, a.x, x.x);
+        x.y = __fmaf_rn(-lr, a.y, x.y);
+        x.z = __fmaf_rn(-lr, a.z, x.z);
+        x.w = __fmaf_rn(-lr, a.w, x.w);
+        reinterpret_cast<float4*>(w)[v] = x;
+        if (shadow) store_shadow4(shadow, 4 * v, x);
+    }
+}
+
+// KP1 parameter-server comparator: every rank pushes its buffer into
+// its slot of rank 0's heap; rank 0 sums slots in ascending rank order,
+// applies op, writes the result into every rank's buffer; then a release flag per
+// rank.  Channel g handles a contiguous slice of K.
+__global__ void __launch_bounds__(RING_THREADS) ps_kernel(const __grid_constant__ PsParams P) {
+    __shared__ uint32_t s_epoch;
+    __shared__ int s_abort;
+    const int l = blockIdx.y, g = blockIdx.x, tid = threadIdx.x;
+    const int N = P.N, n = P.rank_base + l, G = P.G;
+    const RingLocal& L = P.loc[l];
+    char* heap0 = L.heaps[0];
+    const int64_t K = P.K;
+    const int64_t Kv = (K + 3) / 4;
+    const int64_t v0 = g * Kv / G, v1 = (g + 1) * Kv / G;
+    const float inv_n = 1.0f / (float)N;
+    if (tid == 0) {
+        s_epoch = L.epochs[g] + 1;
+        s_abort = 0;
+    }
+    __syncthreads();
+    const uint32_t epoch = s_epoch;
+    // K_slot stride: slots hold K rounded up to 4
+    const int64_t slot_stride = Kv * 4;
+    // phase 0: push to server slot n (uplink: N*M)
+    {
+        float* slot = reinterpret_cast<float*>(heap0 + P.off_slots) + (int64_t)n * slot_stride;
+        for (int64_t v = v0 + tid; v < v1; v += RING_THREADS) {
+            const int64_t e = 4 * v;
+            st4_masked(slot, e, K, ld4_masked(L.src, e, K));
+        }
+        uint64_t* f = reinterpret_cast<uint64_t*>(heap0 + P.off_flags) + (int64_t)n * kMaxChannels + g;
+        signal_flag(f, epoch, K);
+    }
+    if (n == 0) {
+        // server: wait for all N pushes of this channel, then reduce in ascending rank order
+        for (int r = 0; r < N; ++r) {
+            const uint64_t* f = reinterpret_cast<const uint64_t*>(heap0 + P.off_flags) + (int64_t)r * kMaxChannels + g;
+            if (!wait_flag(f, epoch, K, P.status, P.spin_ns, &s_abort)) return;
+        }
+        const float* slots = reinterpret_cast<const float*>(heap0 + P.off_slots);
+        for (int64_t v = v0 + tid; v < v1; v += RING_THREADS) {
+            const int64_t e = 4 * v;
+            float4 a = ldcg4_masked(slots, e, K);
+            for (int r = 1; r < N; ++r) {
+                const float4 b = ldcg4_masked(slots + (int64_t)r * slot_stride, e, K);
+                a.x = a.x + b.x; a.y = a.y + b.y; a.z = a.z + b.z; a.w = a.w + b.w;
+            }
+            if (P.op == TEM_MEAN) {
+                a.x = a.x * inv_n; a.y = a.y * inv_n; a.z = a.z * inv_n; a.w = a.w * inv_n;
+            }
+            for (int r = 0; r < N; ++r)  // downlink broadcast
+                st4_masked(reinterpret_cast<float*>(L.heaps[r] + P.off_dst), e, K, a);
+        }
+        __syncthreads();
+        for (int r = 0; r < N; ++r) {
+            uint64_t* f = reinterpret_cast<uint64_t*>(L.heaps[r] + P.off_flags) + (int64_t)(TEM_MAX_RANKS + r) * kMaxChannels + g;
+            signal_flag(f, epoch, K);
+        }
+    }
+    // everybody: wait for the downlink of this channel
+    {
+        const uint64_t* f = reinterpret_cast<const uint64_t*>(L.heaps[n] + P.off_flags) + (int64_t)(TEM_MAX_RANKS + n) * kMaxChannels + g;
+        if (!wait_flag(f, epoch, K, P.status, P.spin_ns, &s_abort)) return;
+    }
+    if (tid == 0) L.epochs[g] = epoch;
+}
+
+}  // namespace
+
+cudaError_t launch_ring(const RingParams& p, cudaStream_t s) {
+    dim3 grid(p.G, p.nlocal), block(RING_THREADS);
+    if (p.nlocal > 1) {
+        // single-device emulation: CTAs of different emulated ranks wait on one another,
+        // so they must be co-resident -> cooperative launch (fails instead of hanging).
+        void* args[] = {const_cast<RingParams*>(&p)};
+        return cudaLaunchCooperativeKernel((const void*)ring_kernel, grid, block, args, 0, s);
+    }
+    ring_kernel<<<grid, block, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sgd_single(const float* g, float* w, __nv_bfloat16* shadow, int64_t n, int op,
+                              float lr, cudaStream_t s) {
+    sgd_single_kernel<<<296, 512, 0, s>>>(g, w, shadow, n, op, lr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ps(const PsParams& p, cudaStream_t s) {
+    dim3 grid(p.G, p.nlocal), block(RING_THREADS);
+    if (p.nlocal > 1) {
+        void* args[] = {const_cast<PsParams*>(&p)};
+        return cudaLaunchCooperativeKernel((const void*)ps_kernel, grid, block, args, 0, s);
+    }
+    ps_kernel<<<grid, block, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+}  // namespace tem

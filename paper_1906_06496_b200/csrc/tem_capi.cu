@@ -1,0 +1,564 @@
+// tem_capi.cu -- host side of the C ABI declared in include/tem.h.
+//
+// Validates configurations, lays out the caller-owned workspace and symmetric
+// heaps, and enqueues the kernels of tem_simt.cu / tem_umma.cu / ring.cu.  No
+// device memory is allocated here.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <new>
+
+#include "kernels.h"
+
+using namespace tem;
+
+namespace {
+
+constexpr size_t kAlign = 256;
+constexpr uint64_t kSpinNs = 20ull * 1000 * 1000 * 1000;  // 20 s flag-wait bound
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+int64_t roundup(int64_t x, int64_t q) { return (x + q - 1) / q * q; }
+
+struct HeapLayout {
+    size_t off_user, user_bytes, off_stage, off_ps, off_flags, off_psflags, total;
+};
+
+struct WsLayout {
+    size_t xp, h1, h2, dA2, dA1, z, grad, headpart, wpart, shadow, epochs, stepctr, xstage,
+        labstage, lossstage, per_rank;
+};
+
+bool cfg_valid(const tem_config* c) {
+    if (!c) return false;
+    if (c->world_size < 1 || c->world_size > TEM_MAX_RANKS) return false;
+    if (c->rank < 0 || c->rank >= c->world_size) return false;
+    if (!(c->local_ranks == 1 || (c->local_ranks == c->world_size && c->rank == 0))) return false;
+    if (c->batch_per_rank < 0 || c->seq_len < 1) return false;
+    if (c->c_in < 16 || c->c_in % 16 != 0) return false;
+    if (c->c_hidden < 128 || c->c_hidden % 128 != 0 || c->c_hidden > 512) return false;
+    if (c->c_out != 3) return false;
+    if (c->precision != TEM_FP32 && c->precision != TEM_BF16) return false;
+    if (!(c->lr >= 0.0f) || !isfinite(c->lr)) return false;
+    for (int o = 0; o < 3; ++o)
+        if (!isfinite(c->loss_weight[o])) return false;
+    if (c->max_allreduce_elems < 0) return false;
+    if (c->ring_channels < 0 || c->ring_channels > kMaxChannels) return false;
+    if (c->ring_chunks < 0 || c->ring_chunks > kMaxChunks) return false;
+    return true;
+}
+
+int64_t num_params(const tem_config* c) {
+    const int64_t C = c->c_hidden, Ci = c->c_in, Co = c->c_out;
+    return C * 3 * Ci + C + C * 3 * C + C + Co * C + Co;
+}
+
+Geom make_geom(const tem_config* c) {
+    Geom g;
+    g.B = c->batch_per_rank;
+    g.T = c->seq_len;
+    g.Cin = c->c_in;
+    g.C = c->c_hidden;
+    g.Co = c->c_out;
+    g.R = g.B * (g.T + 2);
+    g.prec = c->precision;
+    g.K = num_params(c);
+    g.Kpad = roundup(g.K, 4 * (int64_t)c->world_size);
+    g.off_W1 = 0;
+    g.off_b1 = g.off_W1 + (int64_t)g.C * 3 * g.Cin;
+    g.off_W2 = g.off_b1 + g.C;
+    g.off_b2 = g.off_W2 + (int64_t)g.C * 3 * g.C;
+    g.off_W3 = g.off_b2 + g.C;
+    g.off_b3 = g.off_W3 + (int64_t)g.Co * g.C;
+    return g;
+}
+
+int64_t max_ar(const tem_config* c) {
+    return c->max_allreduce_elems > 0 ? c->max_allreduce_elems : num_params(c);
+}
+
+HeapLayout heap_layout(const tem_config* c) {
+    HeapLayout h;
+    const int64_t N = c->world_size;
+    const int64_t kpad = roundup(num_params(c), 4 * N);
+    const int64_t kar = roundup(max_ar(c), 4 * N);
+    h.off_user = align_up((size_t)kpad * 4, 4096);
+    h.user_bytes = (size_t)kar * 4;
+    h.off_stage = align_up(h.off_user + h.user_bytes, 4096);
+    const size_t stage_bytes = (size_t)(kpad > kar ? kpad : kar) * 4;
+    h.off_ps = align_up(h.off_stage + stage_bytes, 4096);
+    const int64_t kps = roundup(num_params(c) > max_ar(c) ? num_params(c) : max_ar(c), 4);
+    h.off_flags = align_up(h.off_ps + (size_t)N * kps * 4, 4096);
+    const size_t ring_flags = (size_t)kMaxChannels * kMaxChunks * 2 * (TEM_MAX_RANKS - 1) * 8;
+    h.off_psflags = h.off_flags + ring_flags;
+    h.total = align_up(h.off_psflags + (size_t)2 * TEM_MAX_RANKS * kMaxChannels * 8, 4096);
+    return h;
+}
+
+WsLayout ws_layout(const tem_config* c) {
+    const Geom g = make_geom(c);
+    const size_t esz = g.prec == TEM_BF16 ? 2 : 4;
+    WsLayout w;
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        const size_t at = o;
+        o = align_up(o + bytes, kAlign);
+        return at;
+    };
+    const int S = simt_wgrad_splits(g);
+    const size_t wmax = (size_t)g.C * 3 * (g.Cin > g.C ? g.Cin : g.C) + g.C;
+    w.xp = take((size_t)g.R * g.Cin * esz);
+    w.h1 = take((size_t)g.R * g.C * esz);
+    w.h2 = take((size_t)g.R * g.C * 4);
+    w.dA2 = take((size_t)g.R * g.C * esz);
+    w.dA1 = take((size_t)g.R * g.C * esz);
+    w.z = take((size_t)g.B * g.T * 3 * 4);
+    w.grad = take((size_t)g.Kpad * 4);
+    w.headpart = take((size_t)g.B * (3 * g.C + 6) * 4);
+    w.wpart = take((size_t)S * wmax * 4);
+    w.shadow = take(g.prec == TEM_BF16 ? (size_t)g.Kpad * 2 : 0);
+    w.epochs = take((size_t)kMaxChannels * 4);
+    w.stepctr = take(8);
+    w.xstage = take((size_t)g.B * g.T * g.Cin * esz);
+    w.labstage = take((size_t)g.B * 3 * g.T * 4);
+    w.lossstage = take(4 * 4);
+    w.per_rank = o;
+    return w;
+}
+
+}  // namespace
+
+struct tem_ctx {
+    tem_config cfg;
+    void* peers[TEM_MAX_RANKS];
+    Geom g;
+    HeapLayout hl;
+    WsLayout wl;
+    int N, nlocal, rank;
+    int G, C;                  // ring channels / chunks for the TEM gradient
+    RankBufs rb[TEM_MAX_RANKS];
+    uint32_t* epochs[TEM_MAX_RANKS];
+    char* ws_base[TEM_MAX_RANKS];
+    Status* st_host;
+    Status* st_dev;
+    int launches_step, launches_exchange;
+    bool alive;
+    // per-kernel timing (tem_timing_*)
+    cudaEvent_t* tev;  // [max_steps][NUM_SLOTS*2]
+    int t_max, t_idx;
+};
+
+extern "C" {
+
+const char* tem_status_string(int32_t s) {
+    switch (s) {
+        case TEM_OK: return "TEM_OK";
+        case TEM_ERR_INVALID_ARG: return "TEM_ERR_INVALID_ARG";
+        case TEM_ERR_PROTOCOL: return "TEM_ERR_PROTOCOL";
+        case TEM_ERR_TRANSPORT: return "TEM_ERR_TRANSPORT";
+        case TEM_ERR_CUDA: return "TEM_ERR_CUDA";
+        case TEM_ERR_NONFINITE: return "TEM_ERR_NONFINITE";
+        case TEM_ERR_STATE: return "TEM_ERR_STATE";
+        default: return "TEM_ERR_UNKNOWN";
+    }
+}
+
+int64_t tem_num_params(const tem_config* cfg) { return cfg_valid(cfg) ? num_params(cfg) : 0; }
+
+int64_t tem_kpad(const tem_config* cfg, int64_t K) {
+    if (!cfg_valid(cfg) || K < 0) return 0;
+    return roundup(K, 4 * (int64_t)cfg->world_size);
+}
+
+size_t tem_workspace_bytes(const tem_config* cfg) {
+    if (!cfg_valid(cfg)) return 0;
+    return ws_layout(cfg).per_rank * (size_t)cfg->local_ranks;
+}
+
+size_t tem_sym_bytes(const tem_config* cfg) { return cfg_valid(cfg) ? heap_layout(cfg).total : 0; }
+
+size_t tem_sym_user_offset(const tem_config* cfg) { return cfg_valid(cfg) ? heap_layout(cfg).off_user : 0; }
+
+tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
+    if (!out) return TEM_ERR_INVALID_ARG;
+    *out = nullptr;
+    if (!cfg_valid(cfg) || !cfg->peer_bufs || !params || !cfg->workspace) return TEM_ERR_INVALID_ARG;
+    const HeapLayout hl = heap_layout(cfg);
+    const WsLayout wl = ws_layout(cfg);
+    if (cfg->sym_bytes < hl.total) return TEM_ERR_INVALID_ARG;
+    if (cfg->workspace_bytes < wl.per_rank * (size_t)cfg->local_ranks) return TEM_ERR_INVALID_ARG;
+    if (((uintptr_t)cfg->workspace) % kAlign) return TEM_ERR_INVALID_ARG;
+    for (int r = 0; r < cfg->world_size; ++r)
+        if (!cfg->peer_bufs[r] || ((uintptr_t)cfg->peer_bufs[r]) % 4096) return TEM_ERR_INVALID_ARG;
+    if ((void*)params != cfg->peer_bufs[cfg->rank]) return TEM_ERR_INVALID_ARG;
+    if (cudaSetDevice(cfg->device) != cudaSuccess) return TEM_ERR_CUDA;
+
+    tem_ctx* c = new (std::nothrow) tem_ctx();
+    if (!c) return TEM_ERR_CUDA;
+    c->cfg = *cfg;
+    for (int r = 0; r < cfg->world_size; ++r) c->peers[r] = cfg->peer_bufs[r];
+    c->cfg.peer_bufs = c->peers;
+    c->g = make_geom(cfg);
+    c->hl = hl;
+    c->wl = wl;
+    c->N = cfg->world_size;
+    c->nlocal = cfg->local_ranks;
+    c->rank = cfg->rank;
+    // ring geometry for the TEM gradient (identical on every rank: depends on cfg only)
+    c->G = cfg->ring_channels > 0 ? cfg->ring_channels : 16;
+    c->C = cfg->ring_chunks > 0 ? cfg->ring_chunks : 4;
+    if (c->nlocal > 1) {  // emulation: all CTAs of all emulated ranks must be co-resident
+        int dev_sms = 148;
+        cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
+        const int cap = dev_sms / c->nlocal;
+        if (c->G > cap) c->G = cap;
+    }
+    if (cudaHostAlloc((void**)&c->st_host, 64, cudaHostAllocMapped) != cudaSuccess) {
+        delete c;
+        return TEM_ERR_CUDA;
+    }
+    memset((void*)c->st_host, 0, 64);
+    if (cudaHostGetDevicePointer((void**)&c->st_dev, c->st_host, 0) != cudaSuccess) {
+        cudaFreeHost(c->st_host);
+        delete c;
+        return TEM_ERR_CUDA;
+    }
+    for (int l = 0; l < c->nlocal; ++l) {
+        char* base = (char*)cfg->workspace + wl.per_rank * l;
+        c->ws_base[l] = base;
+        RankBufs& b = c->rb[l];
+        b.params = (const float*)c->peers[c->rank + l];
+        b.xp = base + wl.xp;
+        b.h1 = base + wl.h1;
+        b.h2 = (float*)(base + wl.h2);
+        b.dA2 = base + wl.dA2;
+        b.dA1 = base + wl.dA1;
+        b.z = (float*)(base + wl.z);
+        b.grad = (float*)(base + wl.grad);
+        b.headpart = (float*)(base + wl.headpart);
+        b.wpart = (float*)(base + wl.wpart);
+        b.stepctr = (int64_t*)(base + wl.stepctr);
+        b.shadow = c->g.prec == TEM_BF16 ? (__nv_bfloat16*)(base + wl.shadow) : nullptr;
+        b.wop = b.shadow ? (const void*)b.shadow : (const void*)b.params;
+        c->epochs[l] = (uint32_t*)(base + wl.epochs);
+        cudaError_t e = cudaMemsetAsync(base, 0, wl.per_rank, 0);
+        if (e == cudaSuccess && b.shadow) e = launch_cast_shadow(b.params, b.shadow, c->g.Kpad, 0);
+        if (e != cudaSuccess) {
+            cudaFreeHost(c->st_host);
+            delete c;
+            return TEM_ERR_CUDA;
+        }
+    }
+    if (cudaStreamSynchronize(0) != cudaSuccess) {
+        cudaFreeHost(c->st_host);
+        delete c;
+        return TEM_ERR_CUDA;
+    }
+    c->launches_step = 0;
+    c->launches_exchange = 0;
+    c->alive = true;
+    *out = c;
+    return TEM_OK;
+}
+
+static tem_status check_ctx(tem_ctx* c) {
+    if (!c || !c->alive) return TEM_ERR_STATE;
+    const int32_t code = *(volatile int32_t*)&c->st_host->code;
+    if (code != 0) return (tem_status)code;
+    return TEM_OK;
+}
+
+static cudaEvent_t* timing_slot_events(tem_ctx* c) {
+    if (!c->tev || c->t_idx >= c->t_max || c->nlocal != 1) return nullptr;
+    return c->tev + (size_t)c->t_idx * NUM_SLOTS * 2;
+}
+
+static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, float* loss_out,
+                               cudaStream_t s, int* nl) {
+    const EvRec rec{timing_slot_events(c), s};
+    const Geom& g = c->g;
+    const size_t esz = g.prec == TEM_BF16 ? 2 : 4;
+    const float lam[3] = {c->cfg.loss_weight[0], c->cfg.loss_weight[1], c->cfg.loss_weight[2]};
+    for (int l = 0; l < c->nlocal; ++l) {
+        const char* xl = (const char*)x + (size_t)l * g.B * g.T * g.Cin * esz;
+        const float* labl = labels + (size_t)l * g.B * 3 * g.T;
+        rec.begin(SLOT_PREP);
+        if (launch_prep_x(g, xl, c->rb[l].xp, s) != cudaSuccess) return TEM_ERR_CUDA;
+        rec.end(SLOT_PREP);
+        ++*nl;
+        if (simt_compute(g, c->rb[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s) != cudaSuccess)
+            return TEM_ERR_CUDA;
+    }
+    return TEM_OK;
+}
+
+static RingLocal ring_local(tem_ctx* c, int l, const float* src, float* dst, __nv_bfloat16* shadow) {
+    RingLocal L;
+    L.src = src;
+    L.dst_self = dst;
+    L.shadow = shadow;
+    L.epochs = c->epochs[l];
+    for (int r = 0; r < TEM_MAX_RANKS; ++r) L.heaps[r] = r < c->N ? (char*)c->peers[r] : nullptr;
+    return L;
+}
+
+static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
+    const Geom& g = c->g;
+    const EvRec rec{timing_slot_events(c), s};
+    rec.begin(SLOT_EXCHANGE);
+    tem_status st = TEM_OK;
+    if (c->N == 1) {
+        for (int l = 0; l < c->nlocal; ++l) {
+            if (launch_sgd_single(c->rb[l].grad, (float*)c->rb[l].params, c->rb[l].shadow, g.Kpad,
+                                  TEM_MEAN, c->cfg.lr, s) != cudaSuccess)
+                return TEM_ERR_CUDA;
+            ++*nl;
+        }
+        rec.end(SLOT_EXCHANGE);
+        return st;
+    }
+    RingParams p;
+    memset(&p, 0, sizeof(p));
+    for (int l = 0; l < c->nlocal; ++l)
+        p.loc[l] = ring_local(c, l, c->rb[l].grad, (float*)c->rb[l].params, c->rb[l].shadow);
+    p.N = c->N;
+    p.rank_base = c->rank;
+    p.nlocal = c->nlocal;
+    p.G = c->G;
+    p.C = c->C;
+    p.op = TEM_MEAN;
+    p.mode = 1;
+    p.K = g.Kpad;
+    p.Kpad = g.Kpad;
+    p.lr = c->cfg.lr;
+    p.off_dst = 0;
+    p.off_stage = (int64_t)c->hl.off_stage;
+    p.off_flags = (int64_t)c->hl.off_flags;
+    p.status = c->st_dev;
+    p.spin_ns = kSpinNs;
+    if (launch_ring(p, s) != cudaSuccess) return TEM_ERR_CUDA;
+    rec.end(SLOT_EXCHANGE);
+    ++*nl;
+    return st;
+}
+
+tem_status tem_compute(tem_ctx* c, const void* x, const float* labels, float* loss_out, void* stream) {
+    tem_status st = check_ctx(c);
+    if (st != TEM_OK) return st;
+    if ((!x || !labels) && c->g.B > 0) return TEM_ERR_INVALID_ARG;
+    if (!loss_out) return TEM_ERR_INVALID_ARG;
+    int nl = 0;
+    st = compute_impl(c, x, labels, loss_out, (cudaStream_t)stream, &nl);
+    return st;
+}
+
+tem_status tem_exchange(tem_ctx* c, void* stream) {
+    tem_status st = check_ctx(c);
+    if (st != TEM_OK) return st;
+    int nl = 0;
+    st = exchange_impl(c, (cudaStream_t)stream, &nl);
+    c->launches_exchange = nl;
+    return st;
+}
+
+tem_status tem_step(tem_ctx* c, const void* x, const float* labels, float* loss_out, void* stream) {
+    tem_status st = check_ctx(c);
+    if (st != TEM_OK) return st;
+    if ((!x || !labels) && c->g.B > 0) return TEM_ERR_INVALID_ARG;
+    if (!loss_out) return TEM_ERR_INVALID_ARG;
+    int nl = 0;
+    st = compute_impl(c, x, labels, loss_out, (cudaStream_t)stream, &nl);
+    if (st != TEM_OK) return st;
+    int ne = 0;
+    st = exchange_impl(c, (cudaStream_t)stream, &ne);
+    c->launches_step = nl + ne;
+    c->launches_exchange = ne;
+    if (c->tev && c->t_idx < c->t_max) ++c->t_idx;
+    return st;
+}
+
+tem_status tem_step_host(tem_ctx* c, const void* x_host, const float* labels_host, float* loss_host,
+                         void* stream) {
+    tem_status st = check_ctx(c);
+    if (st != TEM_OK) return st;
+    if (!loss_host || ((!x_host || !labels_host) && c->g.B > 0)) return TEM_ERR_INVALID_ARG;
+    if (c->nlocal != 1) return TEM_ERR_INVALID_ARG;  // host path: one rank per process
+    cudaStream_t s = (cudaStream_t)stream;
+    const Geom& g = c->g;
+    const size_t esz = g.prec == TEM_BF16 ? 2 : 4;
+    char* base = c->ws_base[0];
+    void* xd = base + c->wl.xstage;
+    float* ld = (float*)(base + c->wl.labstage);
+    float* lossd = (float*)(base + c->wl.lossstage);
+    const size_t xb = (size_t)g.B * g.T * g.Cin * esz, lb = (size_t)g.B * 3 * g.T * 4;
+    if (xb && cudaMemcpyAsync(xd, x_host, xb, cudaMemcpyHostToDevice, s) != cudaSuccess) return TEM_ERR_CUDA;
+    if (lb && cudaMemcpyAsync(ld, labels_host, lb, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return TEM_ERR_CUDA;
+    st = tem_step(c, xd, ld, lossd, stream);
+    if (st != TEM_OK) return st;
+    if (cudaMemcpyAsync(loss_host, lossd, 16, cudaMemcpyDeviceToHost, s) != cudaSuccess) return TEM_ERR_CUDA;
+    return TEM_OK;
+}
+
+static int ar_channels(tem_ctx* c, int64_t kpad) {
+    // ~>= 2K float4 per channel per block piece set; same on every rank (depends on K, N, cfg)
+    int64_t nvec = kpad / c->N / 4;
+    int64_t G = nvec / 2048;
+    const int cap = c->cfg.ring_channels > 0 ? c->cfg.ring_channels : 32;
+    if (G > cap) G = cap;
+    if (G < 1) G = 1;
+    if (c->nlocal > 1) {
+        int dev_sms = 148;
+        cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->cfg.device);
+        if (G > dev_sms / c->nlocal) G = dev_sms / c->nlocal;
+    }
+    return (int)G;
+}
+
+tem_status ring_allreduce(tem_ctx* c, float* buf, int64_t K, int32_t op, void* stream) {
+    tem_status st = check_ctx(c);
+    if (st != TEM_OK) return st;
+    if (op != TEM_SUM && op != TEM_MEAN) return TEM_ERR_INVALID_ARG;
+    if (K < 1 || K > max_ar(&c->cfg)) return TEM_ERR_INVALID_ARG;
+    if ((char*)buf != (char*)c->peers[c->rank] + c->hl.off_user) return TEM_ERR_INVALID_ARG;
+    RingParams p;
+    memset(&p, 0, sizeof(p));
+    for (int l = 0; l < c->nlocal; ++l) {
+        float* ub = (float*)((char*)c->peers[c->rank + l] + c->hl.off_user);
+        p.loc[l] = ring_local(c, l, ub, ub, nullptr);
+    }
+    p.N = c->N;
+    p.rank_base = c->rank;
+    p.nlocal = c->nlocal;
+    p.Kpad = roundup(K, 4 * (int64_t)c->N);
+    p.G = ar_channels(c, p.Kpad);
+    p.C = c->cfg.ring_chunks > 0 ? c->cfg.ring_chunks : 4;
+    p.op = op;
+    p.mode = 0;
+    p.K = K;
+    p.lr = 0.f;
+    p.off_dst = (int64_t)c->hl.off_user;
+    p.off_stage = (int64_t)c->hl.off_stage;
+    p.off_flags = (int64_t)c->hl.off_flags;
+    p.status = c->st_dev;
+    p.spin_ns = kSpinNs;
+    if (launch_ring(p, (cudaStream_t)stream) != cudaSuccess) return TEM_ERR_CUDA;
+    return TEM_OK;
+}
+
+tem_status ps_allreduce(tem_ctx* c, float* buf, int64_t K, int32_t op, void* stream) {
+    tem_status st = check_ctx(c);
+    if (st != TEM_OK) return st;
+    if (op != TEM_SUM && op != TEM_MEAN) return TEM_ERR_INVALID_ARG;
+    if (K < 1 || K > max_ar(&c->cfg)) return TEM_ERR_INVALID_ARG;
+    if ((char*)buf != (char*)c->peers[c->rank] + c->hl.off_user) return TEM_ERR_INVALID_ARG;
+    PsParams p;
+    memset(&p, 0, sizeof(p));
+    for (int l = 0; l < c->nlocal; ++l) {
+        float* ub = (float*)((char*)c->peers[c->rank + l] + c->hl.off_user);
+        p.loc[l] = ring_local(c, l, ub, ub, nullptr);
+    }
+    p.N = c->N;
+    p.rank_base = c->rank;
+    p.nlocal = c->nlocal;
+    p.G = ar_channels(c, roundup(K, 4 * (int64_t)c->N));
+    p.op = op;
+    p.K = K;
+    p.off_dst = (int64_t)c->hl.off_user;
+    p.off_slots = (int64_t)c->hl.off_ps;
+    p.off_flags = (int64_t)c->hl.off_psflags;
+    p.status = c->st_dev;
+    p.spin_ns = kSpinNs;
+    if (launch_ps(p, (cudaStream_t)stream) != cudaSuccess) return TEM_ERR_CUDA;
+    return TEM_OK;
+}
+
+tem_status tem_sync(tem_ctx* c, void* stream, int64_t* bad_step) {
+    if (!c || !c->alive) return TEM_ERR_STATE;
+    if (cudaStreamSynchronize((cudaStream_t)stream) != cudaSuccess) return TEM_ERR_CUDA;
+    const int32_t code = *(volatile int32_t*)&c->st_host->code;
+    if (bad_step) *bad_step = *(volatile int64_t*)&c->st_host->step;
+    return (tem_status)code;
+}
+
+tem_status tem_shutdown(tem_ctx* c) {
+    if (!c) return TEM_OK;
+    if (!c->alive) return TEM_ERR_STATE;
+    tem_status st = TEM_OK;
+    if (cudaSetDevice(c->cfg.device) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+        st = TEM_ERR_CUDA;
+    const int32_t code = *(volatile int32_t*)&c->st_host->code;
+    if (st == TEM_OK && code != 0) st = (tem_status)code;
+    cudaFreeHost(c->st_host);
+    if (c->tev) {
+        for (size_t i = 0; i < (size_t)c->t_max * NUM_SLOTS * 2; ++i) cudaEventDestroy(c->tev[i]);
+        delete[] c->tev;
+    }
+    c->alive = false;
+    delete c;
+    return st;
+}
+
+float* tem_local_grad(tem_ctx* c, int32_t l) {
+    if (!c || !c->alive || l < 0 || l >= c->nlocal) return nullptr;
+    return c->rb[l].grad;
+}
+
+float* tem_logits(tem_ctx* c, int32_t l) {
+    if (!c || !c->alive || l < 0 || l >= c->nlocal) return nullptr;
+    return c->rb[l].z;
+}
+
+int32_t tem_timing_slots(tem_ctx* c) { return c ? NUM_SLOTS : 0; }
+
+const char* tem_timing_slot_name(tem_ctx* c, int32_t slot) { return c ? slot_name(slot) : "?"; }
+
+tem_status tem_timing_begin(tem_ctx* c, int32_t max_steps) {
+    if (!c || !c->alive) return TEM_ERR_STATE;
+    if (max_steps < 1 || c->nlocal != 1 || c->tev) return TEM_ERR_INVALID_ARG;
+    const size_t n = (size_t)max_steps * NUM_SLOTS * 2;
+    c->tev = new (std::nothrow) cudaEvent_t[n];
+    if (!c->tev) return TEM_ERR_CUDA;
+    for (size_t i = 0; i < n; ++i)
+        if (cudaEventCreate(&c->tev[i]) != cudaSuccess) return TEM_ERR_CUDA;
+    c->t_max = max_steps;
+    c->t_idx = 0;
+    return TEM_OK;
+}
+
+tem_status tem_timing_end(tem_ctx* c, float* sum_ms, int32_t* steps) {
+    if (!c || !c->alive) return TEM_ERR_STATE;
+    if (!c->tev) return TEM_ERR_INVALID_ARG;
+    tem_status st = TEM_OK;
+    for (int k = 0; k < NUM_SLOTS; ++k) sum_ms[k] = 0.f;
+    for (int i = 0; i < c->t_idx; ++i)
+        for (int k = 0; k < NUM_SLOTS; ++k) {
+            cudaEvent_t a = c->tev[((size_t)i * NUM_SLOTS + k) * 2], b = c->tev[((size_t)i * NUM_SLOTS + k) * 2 + 1];
+            if (cudaEventSynchronize(b) != cudaSuccess) { st = TEM_ERR_CUDA; continue; }
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, a, b) == cudaSuccess) sum_ms[k] += ms;
+            // slots never recorded this step (e.g. head with B = 0) report "not ready": skip
+            cudaGetLastError();
+        }
+    if (steps) *steps = c->t_idx;
+    const size_t n = (size_t)c->t_max * NUM_SLOTS * 2;
+    for (size_t i = 0; i < n; ++i) cudaEventDestroy(c->tev[i]);
+    delete[] c->tev;
+    c->tev = nullptr;
+    c->t_max = c->t_idx = 0;
+    return st;
+}
+
+int32_t tem_launches_per_step(tem_ctx* c) { return c ? c->launches_step : 0; }
+int32_t tem_launches_per_exchange(tem_ctx* c) { return c ? c->launches_exchange : 0; }
+
+const char* tem_kernel_path(tem_ctx* c) {
+    if (!c) return "none";
+    return c->g.prec == TEM_BF16 ? "simt-bf16" : "simt-fp32";
+}
+
+}  // extern "C"

@@ -1,0 +1,354 @@
+"""Thin Python binding of libtem.so (include/tem.h).
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels
+behind the C ABI.  torch is used for device memory, streams and process groups
+(symmetric-memory rendezvous for the peer heaps).  There is no fallback: if the
+library cannot be loaded, importing the binding raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _build
+
+TEM_OK, TEM_ERR_INVALID_ARG, TEM_ERR_PROTOCOL, TEM_ERR_TRANSPORT, TEM_ERR_CUDA, \
+    TEM_ERR_NONFINITE, TEM_ERR_STATE = range(7)
+TEM_SUM, TEM_MEAN = 0, 1
+TEM_FP32, TEM_BF16 = 0, 1
+MAX_RANKS = 8
+
+_P = ctypes.c_void_p
+
+
+class tem_config(ctypes.Structure):
+    _fields_ = [
+        ("rank", ctypes.c_int32), ("world_size", ctypes.c_int32), ("device", ctypes.c_int32),
+        ("local_ranks", ctypes.c_int32),
+        ("batch_per_rank", ctypes.c_int32), ("seq_len", ctypes.c_int32),
+        ("c_in", ctypes.c_int32), ("c_hidden", ctypes.c_int32), ("c_out", ctypes.c_int32),
+        ("precision", ctypes.c_int32),
+        ("lr", ctypes.c_float), ("loss_weight", ctypes.c_float * 3),
+        ("peer_bufs", ctypes.POINTER(ctypes.c_void_p)), ("sym_bytes", ctypes.c_size_t),
+        ("max_allreduce_elems", ctypes.c_int64),
+        ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
+        ("ring_channels", ctypes.c_int32), ("ring_chunks", ctypes.c_int32),
+    ]
+
+
+class TemError(RuntimeError):
+    def __init__(self, code: int, what: str = ""):
+        self.code = code
+        super().__init__(f"{what}: {status_string(code)} ({code})")
+
+
+_lib = None
+
+
+def lib():
+    """Load the in-tree libtem.so (building it with nvcc if stale).  Raises if it cannot."""
+    global _lib
+    if _lib is None:
+        path = _build.build()
+        L = ctypes.CDLL(path)
+        cp = ctypes.POINTER(tem_config)
+        L.tem_num_params.restype = ctypes.c_int64
+        L.tem_num_params.argtypes = [cp]
+        L.tem_kpad.restype = ctypes.c_int64
+        L.tem_kpad.argtypes = [cp, ctypes.c_int64]
+        for f in (L.tem_workspace_bytes, L.tem_sym_bytes, L.tem_sym_user_offset):
+            f.restype = ctypes.c_size_t
+            f.argtypes = [cp]
+        L.tem_init.restype = ctypes.c_int
+        L.tem_init.argtypes = [cp, _P, ctypes.POINTER(_P)]
+        for f in (L.tem_step, L.tem_compute):
+            f.restype = ctypes.c_int
+            f.argtypes = [_P, _P, _P, _P, _P]
+        L.tem_step_host.restype = ctypes.c_int
+        L.tem_step_host.argtypes = [_P, _P, _P, _P, _P]
+        L.tem_exchange.restype = ctypes.c_int
+        L.tem_exchange.argtypes = [_P, _P]
+        for f in (L.ring_allreduce, L.ps_allreduce):
+            f.restype = ctypes.c_int
+            f.argtypes = [_P, _P, ctypes.c_int64, ctypes.c_int32, _P]
+        L.tem_sync.restype = ctypes.c_int
+        L.tem_sync.argtypes = [_P, _P, ctypes.POINTER(ctypes.c_int64)]
+        L.tem_shutdown.restype = ctypes.c_int
+        L.tem_shutdown.argtypes = [_P]
+        for f in (L.tem_local_grad, L.tem_logits):
+            f.restype = _P
+            f.argtypes = [_P, ctypes.c_int32]
+        for f in (L.tem_launches_per_step, L.tem_launches_per_exchange):
+            f.restype = ctypes.c_int32
+            f.argtypes = [_P]
+        L.tem_status_string.restype = ctypes.c_char_p
+        L.tem_status_string.argtypes = [ctypes.c_int32]
+        L.tem_kernel_path.restype = ctypes.c_char_p
+        L.tem_kernel_path.argtypes = [_P]
+        L.tem_timing_slots.restype = ctypes.c_int32
+        L.tem_timing_slots.argtypes = [_P]
+        L.tem_timing_slot_name.restype = ctypes.c_char_p
+        L.tem_timing_slot_name.argtypes = [_P, ctypes.c_int32]
+        L.tem_timing_begin.restype = ctypes.c_int
+        L.tem_timing_begin.argtypes = [_P, ctypes.c_int32]
+        L.tem_timing_end.restype = ctypes.c_int
+        L.tem_timing_end.argtypes = [_P, ctypes.POINTER(ctypes.c_float), ctypes.POINTER(ctypes.c_int32)]
+        _lib = L
+    return _lib
+
+
+EXPORTS = ["tem_num_params", "tem_kpad", "tem_workspace_bytes", "tem_sym_bytes",
+           "tem_sym_user_offset", "tem_init", "tem_step", "tem_compute", "tem_exchange",
+           "tem_step_host", "ring_allreduce", "ps_allreduce", "tem_sync", "tem_shutdown",
+           "tem_local_grad", "tem_logits", "tem_launches_per_step", "tem_launches_per_exchange",
+           "tem_status_string", "tem_kernel_path", "tem_timing_slots", "tem_timing_slot_name",
+           "tem_timing_begin", "tem_timing_end"]
+
+
+def status_string(code: int) -> str:
+    return lib().tem_status_string(int(code)).decode()
+
+
+def _check(code: int, what: str):
+    if code != TEM_OK:
+        raise TemError(code, what)
+
+
+def _stream_ptr(stream: Optional[torch.cuda.Stream]):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+# ----------------------------------------------------------------------------- C-ABI mirrors
+def tem_num_params(cfg: tem_config) -> int:
+    return int(lib().tem_num_params(ctypes.byref(cfg)))
+
+
+def tem_kpad(cfg: tem_config, K: int) -> int:
+    return int(lib().tem_kpad(ctypes.byref(cfg), K))
+
+
+def tem_workspace_bytes(cfg: tem_config) -> int:
+    return int(lib().tem_workspace_bytes(ctypes.byref(cfg)))
+
+
+def tem_sym_bytes(cfg: tem_config) -> int:
+    return int(lib().tem_sym_bytes(ctypes.byref(cfg)))
+
+
+def tem_sym_user_offset(cfg: tem_config) -> int:
+    return int(lib().tem_sym_user_offset(ctypes.byref(cfg)))
+
+
+def tem_init(cfg: tem_config, params_ptr: int) -> int:
+    ctx = _P()
+    _check(lib().tem_init(ctypes.byref(cfg), _P(params_ptr), ctypes.byref(ctx)), "tem_init")
+    return ctx.value
+
+
+def tem_step(ctx: int, x_ptr: int, labels_ptr: int, loss_ptr: int, stream=None):
+    _check(lib().tem_step(_P(ctx), _P(x_ptr), _P(labels_ptr), _P(loss_ptr), _stream_ptr(stream)), "tem_step")
+
+
+def tem_compute(ctx: int, x_ptr: int, labels_ptr: int, loss_ptr: int, stream=None):
+    _check(lib().tem_compute(_P(ctx), _P(x_ptr), _P(labels_ptr), _P(loss_ptr), _stream_ptr(stream)),
+           "tem_compute")
+
+
+def tem_exchange(ctx: int, stream=None):
+    _check(lib().tem_exchange(_P(ctx), _stream_ptr(stream)), "tem_exchange")
+
+
+def tem_step_host(ctx: int, x_host_ptr: int, labels_host_ptr: int, loss_host_ptr: int, stream=None):
+    _check(lib().tem_step_host(_P(ctx), _P(x_host_ptr), _P(labels_host_ptr), _P(loss_host_ptr),
+                               _stream_ptr(stream)), "tem_step_host")
+
+
+def ring_allreduce(ctx: int, buf_ptr: int, K: int, op: int = TEM_SUM, stream=None):
+    _check(lib().ring_allreduce(_P(ctx), _P(buf_ptr), int(K), int(op), _stream_ptr(stream)), "ring_allreduce")
+
+
+def ps_allreduce(ctx: int, buf_ptr: int, K: int, op: int = TEM_SUM, stream=None):
+    _check(lib().ps_allreduce(_P(ctx), _P(buf_ptr), int(K), int(op), _stream_ptr(stream)), "ps_allreduce")
+
+
+def tem_sync(ctx: int, stream=None):
+    step = ctypes.c_int64(-1)
+    code = lib().tem_sync(_P(ctx), _stream_ptr(stream), ctypes.byref(step))
+    return int(code), int(step.value)
+
+
+def tem_shutdown(ctx: int):
+    _check(lib().tem_shutdown(_P(ctx)), "tem_shutdown")
+
+
+# ----------------------------------------------------------------------------- session helper
+@dataclass
+class SessionConfig:
+    world_size: int = 1
+    rank: int = 0
+    local_ranks: int = 1
+    batch_per_rank: int = 16
+    seq_len: int = 100
+    c_in: int = 400
+    c_hidden: int = 512
+    c_out: int = 3
+    precision: int = TEM_FP32
+    lr: float = 0.01
+    loss_weight: Sequence[float] = (1.0, 1.0, 1.0)
+    max_allreduce_elems: int = 0
+    ring_channels: int = 0
+    ring_chunks: int = 0
+
+
+class TemSession:
+    """Owns the device memory of one process's ranks and the library context.
+
+    * world_size == local_ranks (N = 1, or the single-device emulation): every rank's
+      heap is a plain device allocation on this GPU.
+    * local_ranks == 1 and world_size > 1 (one process per GPU): the heap comes from
+      torch symmetric memory; its rendezvous gives the peer pointers (NVLink P2P).
+    """
+
+    def __init__(self, sc: SessionConfig, params: np.ndarray, device: int | None = None, group=None):
+        L = lib()
+        self.sc = sc
+        self.device = torch.cuda.current_device() if device is None else device
+        self.dev = torch.device("cuda", self.device)
+        cfg = tem_config()
+        cfg.rank, cfg.world_size, cfg.device, cfg.local_ranks = sc.rank, sc.world_size, self.device, sc.local_ranks
+        cfg.batch_per_rank, cfg.seq_len = sc.batch_per_rank, sc.seq_len
+        cfg.c_in, cfg.c_hidden, cfg.c_out = sc.c_in, sc.c_hidden, sc.c_out
+        cfg.precision, cfg.lr = sc.precision, sc.lr
+        for i in range(3):
+            cfg.loss_weight[i] = float(sc.loss_weight[i])
+        cfg.max_allreduce_elems = sc.max_allreduce_elems
+        cfg.ring_channels, cfg.ring_chunks = sc.ring_channels, sc.ring_chunks
+        self.K = tem_num_params(cfg)
+        if self.K == 0:
+            raise TemError(TEM_ERR_INVALID_ARG, "config")
+        self.Kpad = tem_kpad(cfg, self.K)
+        self.sym_bytes = tem_sym_bytes(cfg)
+        self.user_off = tem_sym_user_offset(cfg)
+        self.ws_bytes = tem_workspace_bytes(cfg)
+        N = sc.world_size
+        self._symm = None
+        if sc.local_ranks == N:
+            self.heaps = [torch.zeros(self.sym_bytes + 4096, dtype=torch.uint8, device=self.dev)
+                          for _ in range(N)]
+            ptrs = [(h.data_ptr() + 4095) // 4096 * 4096 for h in self.heaps]
+            self.heap_off = [p - h.data_ptr() for p, h in zip(ptrs, self.heaps)]
+        else:
+            import torch.distributed as dist
+            import torch.distributed._symmetric_memory as symm_mem
+            grp = group if group is not None else dist.group.WORLD
+            t = symm_mem.empty(self.sym_bytes, dtype=torch.uint8, device=self.dev)
+            t.zero_()
+            hdl = symm_mem.rendezvous(t, grp)
+            self._symm = (t, hdl)
+            ptrs = list(hdl.buffer_ptrs)
+            if any(p % 4096 for p in ptrs):
+                raise TemError(TEM_ERR_INVALID_ARG, "symmetric heap not 4 KiB aligned")
+            self.heaps = [t]
+            self.heap_off = [0]
+            torch.cuda.synchronize(self.dev)
+            dist.barrier(group=grp)
+        self._ptr_arr = (ctypes.c_void_p * N)(*ptrs)
+        cfg.peer_bufs = ctypes.cast(self._ptr_arr, ctypes.POINTER(ctypes.c_void_p))
+        cfg.sym_bytes = self.sym_bytes
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.dev)
+        cfg.workspace, cfg.workspace_bytes = self.ws.data_ptr(), self.ws_bytes
+        self.cfg = cfg
+        p = np.zeros(self.Kpad, np.float32)
+        p[: min(params.size, self.Kpad)] = np.asarray(params, np.float32)[: self.Kpad]
+        pt = torch.from_numpy(p).to(self.dev)
+        for l in range(sc.local_ranks):
+            self.params(l).copy_(pt)
+        torch.cuda.synchronize(self.dev)
+        self.ctx = tem_init(cfg, ptrs[sc.rank])
+        self.loss = torch.zeros(sc.local_ranks, 4, dtype=torch.float32, device=self.dev)
+
+    # -- views into caller-owned memory
+    def _heap(self, l: int) -> torch.Tensor:
+        h = self.heaps[l]
+        return h[self.heap_off[l]: self.heap_off[l] + self.sym_bytes]
+
+    def params(self, l: int = 0) -> torch.Tensor:
+        return self._heap(l)[: 4 * self.Kpad].view(torch.float32)
+
+    def user(self, l: int = 0, K: int | None = None) -> torch.Tensor:
+        n = self.Kpad if K is None else K
+        return self._heap(l)[self.user_off: self.user_off + 4 * n].view(torch.float32)
+
+    def _ws_view(self, ptr: int, nbytes: int) -> torch.Tensor:
+        off = ptr - self.ws.data_ptr()
+        return self.ws[off: off + nbytes]
+
+    def local_grad(self, l: int = 0) -> torch.Tensor:
+        ptr = lib().tem_local_grad(_P(self.ctx), l)
+        return self._ws_view(ptr, 4 * self.Kpad).view(torch.float32)
+
+    def logits(self, l: int = 0) -> torch.Tensor:
+        ptr = lib().tem_logits(_P(self.ctx), l)
+        B, T = self.sc.batch_per_rank, self.sc.seq_len
+        return self._ws_view(ptr, 4 * B * T * 3).view(torch.float32).view(B, T, 3)
+
+    # -- calls
+    def step(self, x: torch.Tensor, labels: torch.Tensor, stream=None) -> torch.Tensor:
+        tem_step(self.ctx, x.data_ptr(), labels.data_ptr(), self.loss.data_ptr(), stream)
+        return self.loss
+
+    def compute(self, x: torch.Tensor, labels: torch.Tensor, stream=None) -> torch.Tensor:
+        tem_compute(self.ctx, x.data_ptr(), labels.data_ptr(), self.loss.data_ptr(), stream)
+        return self.loss
+
+    def exchange(self, stream=None):
+        tem_exchange(self.ctx, stream)
+
+    def allreduce(self, K: int, op: int = TEM_SUM, stream=None):
+        ring_allreduce(self.ctx, self.user(0).data_ptr(), K, op, stream)
+
+    def ps_allreduce(self, K: int, op: int = TEM_SUM, stream=None):
+        ps_allreduce(self.ctx, self.user(0).data_ptr(), K, op, stream)
+
+    def sync(self, stream=None):
+        return tem_sync(self.ctx, stream)
+
+    def launches_per_step(self) -> int:
+        return int(lib().tem_launches_per_step(_P(self.ctx)))
+
+    def launches_per_exchange(self) -> int:
+        return int(lib().tem_launches_per_exchange(_P(self.ctx)))
+
+    def timing_begin(self, max_steps: int):
+        _check(lib().tem_timing_begin(_P(self.ctx), int(max_steps)), "tem_timing_begin")
+
+    def timing_end(self) -> tuple[dict, int]:
+        n = int(lib().tem_timing_slots(_P(self.ctx)))
+        arr = (ctypes.c_float * n)()
+        steps = ctypes.c_int32(0)
+        _check(lib().tem_timing_end(_P(self.ctx), arr, ctypes.byref(steps)), "tem_timing_end")
+        names = [lib().tem_timing_slot_name(_P(self.ctx), k).decode() for k in range(n)]
+        return {names[k]: float(arr[k]) for k in range(n)}, int(steps.value)
+
+    def step_host(self, x_host: torch.Tensor, labels_host: torch.Tensor, loss_host: torch.Tensor, stream=None):
+        tem_step_host(self.ctx, x_host.data_ptr(), labels_host.data_ptr(), loss_host.data_ptr(), stream)
+
+    def kernel_path(self) -> str:
+        return lib().tem_kernel_path(_P(self.ctx)).decode()
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            ctx, self.ctx = self.ctx, None
+            tem_shutdown(ctx)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
