@@ -58,58 +58,76 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + clock-event (throttle) reasons polled through NVML every ~5 ms in a
+    background thread; stats are taken over the samples inside [mark_start, mark_stop]."""
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.t0 = self.t1 = None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    def _reasons(self):
+        nv = self.nv
+        for fn in ("nvmlDeviceGetCurrentClocksEventReasons", "nvmlDeviceGetCurrentClocksThrottleReasons"):
+            if hasattr(nv, fn):
+                try:
+                    return int(getattr(nv, fn)(self.h))
+                except Exception:
+                    pass
+        return 0
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                sm = float(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.samples.append((time.perf_counter(), sm, self._reasons()))
+            except Exception:
+                pass
+            time.sleep(0.005)
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
+        if self.ok:
+            self.th = threading.Thread(target=self._run, daemon=True)
+            self.th.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def mark_start(self):
+        self.t0 = time.perf_counter()
+
+    def mark_stop(self):
+        self.t1 = time.perf_counter()
 
     def stop(self):
-        if self.proc is None:
+        if not self.ok:
             return None
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        self.t.join(timeout=2)
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
-                continue
-            try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[5:9]):
-                if v.lower() == "active":
+        time.sleep(0.02)
+        self._stop.set()
+        self.th.join(timeout=2)
+        win = [x for x in self.samples if self.t0 is not None and self.t0 <= x[0] <= (self.t1 or 1e30)]
+        if not win:  # timed region shorter than one poll: nearest samples around it
+            win = sorted(self.samples, key=lambda x: abs(x[0] - (self.t0 or 0)))[:3]
+        if not win:
+            return None
+        reasons = set()
+        for _, _, r in win:
+            for bit, nm in self.REASONS.items():
+                if r & bit:
                     reasons.add(nm)
-        if not sm:
-            return None
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median([w[1] for w in win]), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(win), "source": "nvml"}
 
 
 def cpu_baseline(workload: dict, videos: int):
@@ -227,6 +245,8 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
+    clocks = ClockSampler(local)
+    clocks.start()
     for i in range(args.warmup):
         sess.step(xs[i % args.pool], labs[i % args.pool])
     code, _ = sess.sync()
@@ -235,10 +255,9 @@ def main():
 
     # ---------------- timed region (device value) ----------------
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    clocks = ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
-    clocks.start()
+    clocks.mark_start()
     sess.timing_begin(args.steps)
     for i in range(args.steps):
         flush.zero_()
@@ -246,6 +265,7 @@ def main():
         sess.step(xs[i % args.pool], labs[i % args.pool])
         ev[i][1].record(stream)
     torch.cuda.synchronize()
+    clocks.mark_stop()
     barrier()
     clk = clocks.stop()
     slot_ms, nrec = sess.timing_end()

@@ -161,6 +161,10 @@ tem_status tem_shutdown(tem_ctx* ctx);
 /* --- introspection for tests and benchmarks (device pointers owned by the workspace) --- */
 float* tem_local_grad(tem_ctx* ctx, int32_t local_rank); /* [K_pad] fp32, last tem_compute */
 float* tem_logits(tem_ctx* ctx, int32_t local_rank);     /* [B][T][3] fp32 z, last compute */
+/* ReLU decisions of the last tem_compute of local rank `local_rank`: writes
+ * out[layer][b][t][c] = 1[a_layer > 0] (uint8, layer 0 = conv1, 1 = conv2) into the
+ * caller's device buffer of 2*B*T*c_hidden bytes, on `stream` (reading R7b). */
+tem_status tem_relu_decisions(tem_ctx* ctx, int32_t local_rank, uint8_t* out, void* stream);
 /* Number of kernels one tem_step / tem_exchange / ring_allreduce(K) enqueues. */
 int32_t tem_launches_per_step(tem_ctx* ctx);
 int32_t tem_launches_per_exchange(tem_ctx* ctx);

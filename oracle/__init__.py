@@ -67,6 +67,9 @@ def lib():
             L.orc_tem_num_params.argtypes = [i32, i32, i32]
             L.orc_tem_fwd_bwd.restype = i32
             L.orc_tem_fwd_bwd.argtypes = [i32, i32, i32, i32, i32, i32, P, P, P, P, P, P, P]
+            L.orc_tem_fwd_bwd_ex.restype = i32
+            L.orc_tem_fwd_bwd_ex.argtypes = [i32, i32, i32, i32, i32, i32, P, P, P, P, P, P, P,
+                                             P, i64, ctypes.c_double, P, i64, P, P]
             _lib = L
     return _lib
 
@@ -160,12 +163,15 @@ def num_params(Cin: int = 400, C: int = 512, Co: int = 3) -> int:
     return int(lib().orc_tem_num_params(Cin, C, Co))
 
 
-def tem_fwd_bwd(x, params, labels, lam=(1.0, 1.0, 1.0), prec: int = 0, C: int = 512):
+def tem_fwd_bwd(x, params, labels, lam=(1.0, 1.0, 1.0), prec: int = 0, C: int = 512,
+                flips=(), kink_tau: float = 0.0, kinks_cap: int = 4096):
     """BSN-TEM forward + weighted logistic loss + backward.
 
     x [B][T][Cin], params flat (fp32 values, any float dtype), labels [B][Co][T].
     prec 0 = fp64, 1 = bf16-operand emulation (reading R8).
-    Returns dict(loss [1+Co] f64, z [B][T][Co] f64, grad [K] f64)."""
+    flips: indices layer*(B*T*C) + (b*T+t)*C + c of ReLU decisions to invert (reading R7b).
+    kink_tau > 0: also report pre-activations with |a| <= kink_tau * sum|terms|.
+    Returns dict(loss [1+Co] f64, z [B][T][Co] f64, grad [K] f64, kinks [n] int64)."""
     x = np.ascontiguousarray(x, dtype=np.float64)
     B, T, Cin = x.shape
     labels = np.ascontiguousarray(labels, dtype=np.float64)
@@ -177,11 +183,19 @@ def tem_fwd_bwd(x, params, labels, lam=(1.0, 1.0, 1.0), prec: int = 0, C: int = 
     loss = np.zeros(1 + Co)
     z = np.zeros((B, T, Co))
     grad = np.zeros(K)
-    rc = lib().orc_tem_fwd_bwd(prec, B, T, Cin, C, Co, _ptr(x), _ptr(p), _ptr(labels), _ptr(lam),
-                               _ptr(loss), _ptr(z), _ptr(grad))
+    fl = np.ascontiguousarray(np.sort(np.asarray(flips, dtype=np.int64)))
+    kinks = np.zeros(max(kinks_cap, 1), dtype=np.int64)
+    nk = np.zeros(1, dtype=np.int64)
+    dec = np.zeros(2 * B * T * C, dtype=np.uint8)
+    rc = lib().orc_tem_fwd_bwd_ex(prec, B, T, Cin, C, Co, _ptr(x), _ptr(p), _ptr(labels), _ptr(lam),
+                                  _ptr(loss), _ptr(z), _ptr(grad), _ptr(fl) if fl.size else None,
+                                  int(fl.size), float(kink_tau), _ptr(kinks), int(kinks_cap), _ptr(nk),
+                                  _ptr(dec))
     if rc:
         raise ValueError("invalid TEM arguments")
-    return {"loss": loss, "z": z, "grad": grad}
+    n = int(nk[0])
+    return {"loss": loss, "z": z, "grad": grad, "kinks": kinks[:min(n, kinks_cap)].copy(), "nkinks": n,
+            "decisions": dec}
 
 
 def param_slices(Cin: int = 400, C: int = 512, Co: int = 3):

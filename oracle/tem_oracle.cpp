@@ -28,6 +28,7 @@
 //   TEM backward   : central finite differences + torch.autograd float64
 //   DP equivalence : N ranks x B (mean) == 1 rank x N*B
 // ============================================================================
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -249,10 +250,32 @@ int64_t orc_tem_num_params(int Cin, int C, int Co) {
 
 static double softplus(double u) { return u > 0 ? u + std::log1p(std::exp(-u)) : std::log1p(std::exp(u)); }
 
-int orc_tem_fwd_bwd(int prec, int B, int T, int Cin, int C, int Co,
-                    const double* x, const double* params, const double* labels,
-                    const double* lambda, double* loss_out, double* z_out, double* grad_out) {
+// ReLU decisions (reading R7b).  The ReLU mask 1[a > 0] is a decision taken by
+// floating point: when |a| is within the rounding error of the accumulation, fp32
+// and fp64 may legitimately disagree.  The extended entry point therefore
+//   * reports every pre-activation with |a| <= kink_tau * S, S = |bias| + sum |w x|
+//     (the magnitude the rounding error scales with), as index
+//     layer*(B*T*C) + (b*T + t)*C + c  (layer 0 = a1, 1 = a2), and
+//   * accepts a sorted list `flips` of such indices whose decision is inverted.
+// With no flips it is exactly the plain definition.
+int orc_tem_fwd_bwd_ex(int prec, int B, int T, int Cin, int C, int Co,
+                       const double* x, const double* params, const double* labels,
+                       const double* lambda, double* loss_out, double* z_out, double* grad_out,
+                       const int64_t* flips, int64_t nflips, double kink_tau,
+                       int64_t* kinks_out, int64_t kinks_cap, int64_t* nkinks,
+                       uint8_t* decisions_out) {
     if (B < 0 || T < 1 || Cin < 1 || C < 1 || Co < 1 || (prec != 0 && prec != 1)) return 1;
+    if (nkinks) *nkinks = 0;
+    const int64_t layer_stride = (int64_t)B * T * C;
+    auto flipped = [&](int64_t idx) {
+        return nflips > 0 && std::binary_search(flips, flips + nflips, idx);
+    };
+    auto note_kink = [&](int64_t idx, double a, double S) {
+        if (kink_tau > 0 && std::fabs(a) <= kink_tau * S && nkinks) {
+            if (*nkinks < kinks_cap && kinks_out) kinks_out[*nkinks] = idx;
+            ++*nkinks;
+        }
+    };
     const int K3 = 3;
     const double* W1 = params;
     const double* b1 = W1 + (size_t)C * K3 * Cin;
@@ -280,35 +303,53 @@ int orc_tem_fwd_bwd(int prec, int B, int T, int Cin, int C, int Co,
 
     // a1: conv1 (row a1)
     std::vector<double> a1(BT * C), h1q(BT * C), a2(BT * C), h2(BT * C);
+    std::vector<char> d1(BT * C), d2(BT * C);  // ReLU decisions
     for (int b = 0; b < B; ++b)
         for (int t = 0; t < T; ++t)
             for (int o = 0; o < C; ++o) {
-                double acc = b1[o];
+                double acc = b1[o], S = std::fabs(b1[o]);
                 for (int j = 0; j < K3; ++j) {
                     const int tt = t + j - 1;
                     if (tt < 0 || tt >= T) continue;  // zero "same" padding
                     const double* wr = &W1q[((size_t)o * K3 + j) * Cin];
                     const double* xr = &xq[((size_t)b * T + tt) * Cin];
-                    for (int c = 0; c < Cin; ++c) acc += wr[c] * xr[c];
+                    for (int c = 0; c < Cin; ++c) {
+                        acc += wr[c] * xr[c];
+                        S += std::fabs(wr[c] * xr[c]);
+                    }
                 }
-                a1[((size_t)b * T + t) * C + o] = acc;
+                const size_t e = ((size_t)b * T + t) * C + o;
+                a1[e] = acc;
+                note_kink((int64_t)e, acc, S);
+                d1[e] = (char)((acc > 0) != flipped((int64_t)e));
             }
-    for (size_t e = 0; e < a1.size(); ++e) h1q[e] = op(a1[e] > 0 ? a1[e] : 0.0);
+    for (size_t e = 0; e < a1.size(); ++e) h1q[e] = op(d1[e] ? a1[e] : 0.0);
     // a2: conv2 (row a2)
     for (int b = 0; b < B; ++b)
         for (int t = 0; t < T; ++t)
             for (int o = 0; o < C; ++o) {
-                double acc = b2[o];
+                double acc = b2[o], S = std::fabs(b2[o]);
                 for (int j = 0; j < K3; ++j) {
                     const int tt = t + j - 1;
                     if (tt < 0 || tt >= T) continue;
                     const double* wr = &W2q[((size_t)o * K3 + j) * C];
                     const double* hr = &h1q[((size_t)b * T + tt) * C];
-                    for (int c = 0; c < C; ++c) acc += wr[c] * hr[c];
+                    for (int c = 0; c < C; ++c) {
+                        acc += wr[c] * hr[c];
+                        S += std::fabs(wr[c] * hr[c]);
+                    }
                 }
-                a2[((size_t)b * T + t) * C + o] = acc;
+                const size_t e = ((size_t)b * T + t) * C + o;
+                a2[e] = acc;
+                note_kink(layer_stride + (int64_t)e, acc, S);
+                d2[e] = (char)((acc > 0) != flipped(layer_stride + (int64_t)e));
             }
-    for (size_t e = 0; e < a2.size(); ++e) h2[e] = a2[e] > 0 ? a2[e] : 0.0;
+    for (size_t e = 0; e < a2.size(); ++e) h2[e] = d2[e] ? a2[e] : 0.0;
+    if (decisions_out)
+        for (size_t e = 0; e < BT * C; ++e) {
+            decisions_out[e] = (uint8_t)d1[e];
+            decisions_out[BT * C + e] = (uint8_t)d2[e];
+        }
     // z: conv3 k1 (row a3)
     std::vector<double> z(BT * Co), dz(BT * Co);
     for (size_t r = 0; r < BT; ++r)
@@ -352,7 +393,7 @@ int orc_tem_fwd_bwd(int prec, int B, int T, int Cin, int C, int Co,
         for (int c = 0; c < C; ++c) {
             double acc = 0.0;
             for (int o = 0; o < Co; ++o) acc += W3[(size_t)o * C + c] * dz[r * Co + o];
-            dA2q[r * C + c] = op(a2[r * C + c] > 0 ? acc : 0.0);
+            dA2q[r * C + c] = op(d2[r * C + c] ? acc : 0.0);
         }
     // conv2 wgrad (row a7)
     for (int b = 0; b < B; ++b)
@@ -381,7 +422,7 @@ int orc_tem_fwd_bwd(int prec, int B, int T, int Cin, int C, int Co,
                         acc += W2q[((size_t)o * K3 + j) * C + c] * dA2q[((size_t)b * T + ts) * C + o];
                 }
                 const size_t r = (size_t)b * T + t;
-                dA1q[r * C + c] = op(a1[r * C + c] > 0 ? acc : 0.0);
+                dA1q[r * C + c] = op(d1[r * C + c] ? acc : 0.0);
             }
     // conv1 wgrad (row a8); no dX (inputs are precomputed features)
     for (int b = 0; b < B; ++b)
@@ -398,6 +439,13 @@ int orc_tem_fwd_bwd(int prec, int B, int T, int Cin, int C, int Co,
                 }
             }
     return 0;
+}
+
+int orc_tem_fwd_bwd(int prec, int B, int T, int Cin, int C, int Co,
+                    const double* x, const double* params, const double* labels,
+                    const double* lambda, double* loss_out, double* z_out, double* grad_out) {
+    return orc_tem_fwd_bwd_ex(prec, B, T, Cin, C, Co, x, params, labels, lambda, loss_out, z_out,
+                              grad_out, nullptr, 0, 0.0, nullptr, 0, nullptr, nullptr);
 }
 
 }  // extern "C"

@@ -41,6 +41,7 @@ struct RankBufs {
 int simt_wgrad_splits(const Geom& g);
 cudaError_t launch_prep_x(const Geom& g, const void* x, void* xp, cudaStream_t s);
 cudaError_t launch_cast_shadow(const float* params, __nv_bfloat16* shadow, int64_t n, cudaStream_t s);
+cudaError_t launch_relu_decisions(const Geom& g, const RankBufs& b, uint8_t* out, cudaStream_t s);
 // Enqueue the whole forward + loss + backward; returns number of kernels launched via *nlaunch.
 // Kernel slots of one step (for tem_timing_*): every launch is bracketed by
 // ev[2*slot] / ev[2*slot+1] when ev != nullptr.

@@ -513,6 +513,14 @@ float* tem_logits(tem_ctx* c, int32_t l) {
     return c->rb[l].z;
 }
 
+tem_status tem_relu_decisions(tem_ctx* c, int32_t l, uint8_t* out, void* stream) {
+    if (!c || !c->alive) return TEM_ERR_STATE;
+    if (l < 0 || l >= c->nlocal || (!out && c->g.B > 0)) return TEM_ERR_INVALID_ARG;
+    if (c->g.B == 0) return TEM_OK;
+    return launch_relu_decisions(c->g, c->rb[l], out, (cudaStream_t)stream) == cudaSuccess ? TEM_OK
+                                                                                           : TEM_ERR_CUDA;
+}
+
 int32_t tem_timing_slots(tem_ctx* c) { return c ? NUM_SLOTS : 0; }
 
 const char* tem_timing_slot_name(tem_ctx* c, int32_t slot) { return c ? slot_name(slot) : "?"; }

@@ -496,6 +496,30 @@ cudaError_t launch_prep_x(const Geom& g, const void* x, void* xp, cudaStream_t s
     return cudaGetLastError();
 }
 
+template <typename T>
+__global__ void relu_decisions_kernel(const T* __restrict__ h1, const float* __restrict__ h2,
+                                      uint8_t* __restrict__ out, int B, int Tn, int C) {
+    const int64_t n = (int64_t)B * Tn * C;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e / C;
+        const int c = (int)(e - r * C);
+        const int64_t v = r / Tn, t = r - v * Tn;
+        const int64_t p = v * (Tn + 2) + t + 1;
+        out[e] = to_f(h1[p * C + c]) > 0.f ? 1 : 0;
+        out[n + e] = h2[p * C + c] > 0.f ? 1 : 0;
+    }
+}
+
+cudaError_t launch_relu_decisions(const Geom& g, const RankBufs& b, uint8_t* out, cudaStream_t s) {
+    if (g.prec == TEM_BF16)
+        relu_decisions_kernel<__nv_bfloat16><<<296, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(b.h1), b.h2,
+                                                                 out, g.B, g.T, g.C);
+    else
+        relu_decisions_kernel<float><<<296, 256, 0, s>>>(static_cast<const float*>(b.h1), b.h2, out, g.B, g.T, g.C);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_cast_shadow(const float* params, __nv_bfloat16* shadow, int64_t n, cudaStream_t s) {
     cast_shadow_kernel<<<296, 256, 0, s>>>(params, shadow, n);
     return cudaGetLastError();

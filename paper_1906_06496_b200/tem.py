@@ -90,6 +90,8 @@ def lib():
         L.tem_status_string.argtypes = [ctypes.c_int32]
         L.tem_kernel_path.restype = ctypes.c_char_p
         L.tem_kernel_path.argtypes = [_P]
+        L.tem_relu_decisions.restype = ctypes.c_int
+        L.tem_relu_decisions.argtypes = [_P, ctypes.c_int32, _P, _P]
         L.tem_timing_slots.restype = ctypes.c_int32
         L.tem_timing_slots.argtypes = [_P]
         L.tem_timing_slot_name.restype = ctypes.c_char_p
@@ -107,7 +109,7 @@ EXPORTS = ["tem_num_params", "tem_kpad", "tem_workspace_bytes", "tem_sym_bytes",
            "tem_step_host", "ring_allreduce", "ps_allreduce", "tem_sync", "tem_shutdown",
            "tem_local_grad", "tem_logits", "tem_launches_per_step", "tem_launches_per_exchange",
            "tem_status_string", "tem_kernel_path", "tem_timing_slots", "tem_timing_slot_name",
-           "tem_timing_begin", "tem_timing_end"]
+           "tem_timing_begin", "tem_timing_end", "tem_relu_decisions"]
 
 
 def status_string(code: int) -> str:
@@ -297,6 +299,13 @@ class TemSession:
         ptr = lib().tem_logits(_P(self.ctx), l)
         B, T = self.sc.batch_per_rank, self.sc.seq_len
         return self._ws_view(ptr, 4 * B * T * 3).view(torch.float32).view(B, T, 3)
+
+    def relu_decisions(self, l: int = 0) -> torch.Tensor:
+        B, T, C = self.sc.batch_per_rank, self.sc.seq_len, self.sc.c_hidden
+        out = torch.zeros(2 * B * T * C, dtype=torch.uint8, device=self.dev)
+        _check(lib().tem_relu_decisions(_P(self.ctx), l, _P(out.data_ptr()), _stream_ptr(None)),
+               "tem_relu_decisions")
+        return out
 
     # -- calls
     def step(self, x: torch.Tensor, labels: torch.Tensor, stream=None) -> torch.Tensor:

@@ -164,6 +164,49 @@ def test_finite_differences(orc):
     assert checked > 50
 
 
+def test_relu_decision_flips_match_autograd_with_explicit_masks(orc):
+    """Reading R7b: inverting chosen ReLU decisions equals an independent torch float64 model
+    whose ReLU is the mask (a > 0) XOR flip, differentiated by autograd."""
+    Cin, C, Co = 4, 6, 3
+    B, T = 2, 5
+    x, p, lab = tiny(B=B, T=T, seed=3)
+    lam = (2.0, 1.0, 1.0)
+    base = orc.tem_fwd_bwd(x, p, lab, lam, prec=0, C=C, kink_tau=1.0, kinks_cap=10 ** 5)
+    n = B * T * C
+    assert base["nkinks"] == 2 * n  # tau = 1 reports every pre-activation
+    rng = np.random.default_rng(0)
+    flips = np.sort(rng.choice(2 * n, 7, replace=False))
+    r = orc.tem_fwd_bwd(x, p, lab, lam, prec=0, C=C, flips=flips)
+    fl = np.zeros(2 * n, bool)
+    fl[flips] = True
+    F1 = torch.tensor(fl[:n].reshape(B, T, C)).permute(0, 2, 1)
+    F2 = torch.tensor(fl[n:].reshape(B, T, C)).permute(0, 2, 1)
+    P = {k: torch.tensor(v, dtype=torch.float64, requires_grad=True) for k, v in split(p, Cin, C, Co).items()}
+    xt = torch.tensor(x, dtype=torch.float64).permute(0, 2, 1)
+    a1 = F.conv1d(xt, P["W1"].permute(0, 2, 1), P["b1"], padding=1)
+    m1 = ((a1 > 0) ^ F1).double()
+    h1 = a1 * m1
+    a2 = F.conv1d(h1, P["W2"].permute(0, 2, 1), P["b2"], padding=1)
+    m2 = ((a2 > 0) ^ F2).double()
+    h2 = a2 * m2
+    dec = torch.cat([m1.permute(0, 2, 1).reshape(-1), m2.permute(0, 2, 1).reshape(-1)]).numpy().astype(np.uint8)
+    assert np.array_equal(r["decisions"], dec)
+    z = F.conv1d(h2, P["W3"].unsqueeze(-1), P["b3"])
+    b = (torch.tensor(lab, dtype=torch.float64) > 0.5).double()
+    lpos = b.sum(-1, keepdim=True)
+    w = (T / lpos.clamp(min=1)) * b + (T / (T - lpos).clamp(min=1)) * (1 - b)
+    L = (F.binary_cross_entropy_with_logits(z, b, weight=w, reduction="none").mean(-1)
+         * torch.tensor(lam, dtype=torch.float64)).sum(-1).mean()
+    L.backward()
+    grad = torch.cat([P[k].grad.reshape(-1) for k in ("W1", "b1", "W2", "b2", "W3", "b3")]).numpy()
+    assert np.allclose(r["grad"], grad, rtol=1e-10, atol=1e-12)
+    assert abs(r["loss"][0] - L.item()) < 1e-12
+    assert not np.allclose(r["grad"], base["grad"])  # the flips matter
+    # no flips and tau = 0: identical to the plain entry point
+    plain = orc.tem_fwd_bwd(x, p, lab, lam, prec=0, C=C)
+    assert np.array_equal(plain["grad"], base["grad"]) and plain["nkinks"] == 0
+
+
 def test_data_parallel_identity(orc):
     """N ranks x B with Mean == 1 rank x N*B (per-video alpha)."""
     Cin, C, Co = 4, 6, 3
