@@ -161,6 +161,11 @@ tem_status tem_shutdown(tem_ctx* ctx);
 /* --- introspection for tests and benchmarks (device pointers owned by the workspace) --- */
 float* tem_local_grad(tem_ctx* ctx, int32_t local_rank); /* [K_pad] fp32, last tem_compute */
 float* tem_logits(tem_ctx* ctx, int32_t local_rank);     /* [B][T][3] fp32 z, last compute */
+/* Device address and size of an internal workspace tensor of local rank `local_rank`, for
+ * tests: "xp", "h1", "h2", "dA2", "dA1" (halo-padded [B][T+2][C] rows in the path's operand
+ * type; h2 fp32), their residual planes "xp_lo", "h1_lo", "dA2_lo", "dA1_lo", and the weight
+ * operand copies "shadow", "shadow_lo" ([K_pad] bf16).  NULL / 0 if absent. */
+void* tem_debug_buffer(tem_ctx* ctx, int32_t local_rank, const char* name, int64_t* nbytes);
 /* ReLU decisions of the last tem_compute of local rank `local_rank`: writes
  * out[layer][b][t][c] = 1[a_layer > 0] (uint8, layer 0 = conv1, 1 = conv2) into the
  * caller's device buffer of 2*B*T*c_hidden bytes, on `stream` (reading R7b). */

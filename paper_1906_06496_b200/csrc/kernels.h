@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace tem {
@@ -16,26 +18,69 @@ struct Geom {
     int B, T, Cin, C, Co;
     int R;          // B*(T+2) padded rows
     int prec;       // TEM_FP32 / TEM_BF16
+    int path;       // PATH_SIMT / PATH_UMMA
+    int op_bf16;    // operand planes stored as bf16 (UMMA always; SIMT for TEM_BF16)
+    int split;      // hi/lo residual planes present (UMMA + TEM_FP32)
     int64_t K, Kpad;
     int64_t off_W1, off_b1, off_W2, off_b2, off_W3, off_b3;
 };
 
+// Kernel paths.  UMMA (default): tcgen05/TMA bf16 tensor-core GEMMs, one plane of bf16
+// operands (TEM_BF16) or hi/lo planes (TEM_FP32, 3-pass split).  SIMT: CUDA-core
+// reference path (fp32 or bf16 single-plane operands), kept for cross-checking.
+enum Path { PATH_SIMT = 0, PATH_UMMA = 1 };
+
 // Per-rank device buffers (all inside the caller's workspace except params).
+// Operand tensors ("hi" = the plane used by SIMT and by the 1-plane UMMA path; "_lo" =
+// residual plane x - bf16(x), present only on the UMMA fp32 path).
 struct RankBufs {
     const float* params;  // fp32 master weights [Kpad] (symmetric heap)
-    const void* wop;      // operand copy of the weights: params (fp32) or bf16 shadow
+    const void* wop;      // SIMT operand copy of the weights: params (fp32) or bf16 shadow
     void* xp;             // [R][Cin] operand type
     void* h1;             // [R][C]   operand type
     float* h2;            // [R][C]
     void* dA2;            // [R][C]   operand type
     void* dA1;            // [R][C]   operand type
+    void* xp_lo;
+    void* h1_lo;
+    void* dA2_lo;
+    void* dA1_lo;
     float* z;             // [B][T][3]
     float* grad;          // [Kpad] local gradient (flat order W1 b1 W2 b2 W3 b3 pad)
     float* headpart;      // [B][3C + 6]
     float* wpart;         // [S][max(C*3*Cin + C, C*3*C + C)]
     int64_t* stepctr;     // step counter for NONFINITE reporting
-    __nv_bfloat16* shadow;  // [Kpad] bf16 weights (TEM_BF16) or nullptr
+    __nv_bfloat16* shadow;     // [Kpad] bf16 weights (hi plane) or nullptr
+    __nv_bfloat16* shadow_lo;  // [Kpad] residual plane (UMMA fp32) or nullptr
 };
+
+// --- tcgen05 path (tem_umma.cu) ---------------------------------------------------------
+enum UmmaMode { FWD_ = 0, DGRAD_ = 1, WGRAD_ = 2 };
+struct UmmaParams {
+    CUtensorMap a[2];  // A operand, hi / lo planes
+    CUtensorMap b[2];  // B operand, hi / lo planes
+    int R, Tp;         // padded rows, T + 2
+    int Kc, cpb;       // FWD/DGRAD: channels per tap along K, k-blocks per tap
+    int Nout;          // output columns (row stride of outputs / mask)
+    const float* bias; // FWD
+    const void* mask;  // DGRAD: h1 (bf16 hi plane)
+    void* out_hi;      // FWD/DGRAD output plane (bf16) or fp32 (out_f32)
+    void* out_lo;      // residual plane or nullptr
+    int out_f32;
+    float* part;       // WGRAD split partials
+    int64_t part_stride;
+    int NW, Cin_w, cpj;  // WGRAD: 3*Cin, Cin, 64-wide chunks per tap
+    int ksplit_rows;
+};
+struct UmmaPlan {
+    UmmaParams conv1, conv2, dgrad, wgrad1, wgrad2;
+    int npass, bn_fwd, S, ksplit_rows;
+};
+int umma_wgrad_splits(const Geom& g);
+bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan);
+cudaError_t launch_prep_x_split(const Geom& g, const float* x, void* hi, void* lo, cudaStream_t s);
+cudaError_t launch_cast_shadow_split(const float* params, __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t n,
+                                     cudaStream_t s);
 
 // --- SIMT path (tem_simt.cu) ---------------------------------------------------------
 int simt_wgrad_splits(const Geom& g);
@@ -57,12 +102,21 @@ struct EvRec {
 cudaError_t simt_compute(const Geom& g, const RankBufs& b, const float* labels,
                          const float lam[3], float* loss_out, Status* status, int* nlaunch,
                          const EvRec& rec, cudaStream_t s);
+cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, const float* labels,
+                         const float lam[3], float* loss_out, Status* status, int* nlaunch,
+                         const EvRec& rec, cudaStream_t s);
+// head (conv3 + sigmoid + loss + dz + dA2) and its deterministic finalisation (rows a3-a5);
+// writes dA2 as b.dA2 (+ b.dA2_lo when present) in the operand type of the path.
+cudaError_t launch_head(const Geom& g, const RankBufs& b, const float* labels, const float lam[3],
+                        float* loss_out, Status* status, const EvRec& rec, cudaStream_t s, int* n);
+cudaError_t launch_reduce_splits(const float* part, float* dst, int64_t n, int S, cudaStream_t s);
 
 // --- ring / exchange (ring.cu) --------------------------------------------------------
 struct RingLocal {
     const float* src;       // contribution of this rank (local grads, or the user buffer)
     float* dst_self;        // result on this rank (params, or the user buffer)
-    __nv_bfloat16* shadow;  // bf16 copy of dst to refresh (TEM_BF16 weights) or nullptr
+    __nv_bfloat16* shadow;  // bf16 copy of dst to refresh (operand weights) or nullptr
+    __nv_bfloat16* shadow_lo;  // residual plane dst - bf16(dst) or nullptr
     uint32_t* epochs;       // [kMaxChannels] per-channel collective counters (workspace)
     char* heaps[TEM_MAX_RANKS];  // every rank's heap base as mapped in this process
 };
@@ -78,8 +132,8 @@ struct RingParams {
     uint64_t spin_ns;
 };
 cudaError_t launch_ring(const RingParams& p, cudaStream_t s);
-cudaError_t launch_sgd_single(const float* g, float* w, __nv_bfloat16* shadow, int64_t n,
-                              int op, float lr, cudaStream_t s);
+cudaError_t launch_sgd_single(const float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo,
+                              int64_t n, int op, float lr, cudaStream_t s);
 struct PsParams {
     RingLocal loc[TEM_MAX_RANKS];
     int N, rank_base, nlocal, G, op;

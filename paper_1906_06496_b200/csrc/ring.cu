@@ -82,13 +82,23 @@ TEM_DEV void signal_flag(uint64_t* flag, uint32_t epoch, int64_t K) {
     if (threadIdx.x == 0) st_release_sys(flag, flag_value(epoch, K));
 }
 
-TEM_DEV void store_shadow4(__nv_bfloat16* sh, int64_t e, float4 w) {
-    __nv_bfloat162 lo = __floats2bfloat162_rn(w.x, w.y);
-    __nv_bfloat162 hi = __floats2bfloat162_rn(w.z, w.w);
+// Refresh the operand copies of the weights: sh = bf16(w), and (3-pass fp32 path)
+// sl = bf16(w - bf16(w)).
+TEM_DEV void store_shadow4(__nv_bfloat16* sh, __nv_bfloat16* sl, int64_t e, float4 w) {
+    const __nv_bfloat162 a = __floats2bfloat162_rn(w.x, w.y);
+    const __nv_bfloat162 b = __floats2bfloat162_rn(w.z, w.w);
     uint2 u;
-    u.x = *reinterpret_cast<uint32_t*>(&lo);
-    u.y = *reinterpret_cast<uint32_t*>(&hi);
+    u.x = *reinterpret_cast<const uint32_t*>(&a);
+    u.y = *reinterpret_cast<const uint32_t*>(&b);
     *reinterpret_cast<uint2*>(sh + e) = u;
+    if (sl) {
+        const __nv_bfloat162 c = __floats2bfloat162_rn(w.x - __low2float(a), w.y - __high2float(a));
+        const __nv_bfloat162 d = __floats2bfloat162_rn(w.z - __low2float(b), w.w - __high2float(b));
+        uint2 v;
+        v.x = *reinterpret_cast<const uint32_t*>(&c);
+        v.y = *reinterpret_cast<const uint32_t*>(&d);
+        *reinterpret_cast<uint2*>(sl + e) = v;
+    }
 }
 
 // Masked vector helpers for ring_allreduce with K < K_pad (elements >= K untouched).
@@ -192,7 +202,7 @@ __global__ void __launch_bounds__(RING_THREADS) ring_kernel(const __grid_constan
                     out.y = __fmaf_rn(-P.lr, a.y, w.y);
                     out.z = __fmaf_rn(-P.lr, a.z, w.z);
                     out.w = __fmaf_rn(-P.lr, a.w, w.w);
-                    if (L.shadow) store_shadow4(L.shadow, e, out);
+                    if (L.shadow) store_shadow4(L.shadow, L.shadow_lo, e, out);
                 }
                 st4_masked(dst_self, e, K, out);
                 if (N > 1) st4_masked(dst_right, e, K, out);
@@ -210,7 +220,7 @@ __global__ void __launch_bounds__(RING_THREADS) ring_kernel(const __grid_constan
                 const int64_t e = (int64_t)s * Bk + 4 * v;
                 if (e >= K) continue;
                 const float4 a = ldcg4_masked(dst_self, e, K);
-                if (L.shadow) store_shadow4(L.shadow, e, a);
+                if (L.shadow) store_shadow4(L.shadow, L.shadow_lo, e, a);
                 st4_masked(dst_right, e, K, a);
             }
             signal_flag(flags_right + fidx(1, k, c), epoch, K);
@@ -225,7 +235,7 @@ __global__ void __launch_bounds__(RING_THREADS) ring_kernel(const __grid_constan
             if (L.shadow) {
                 for (int64_t v = pc.v0 + tid; v < pc.v1; v += RING_THREADS) {
                     const int64_t e = (int64_t)r * Bk + 4 * v;
-                    store_shadow4(L.shadow, e, ld_cg4(dst_self + e));
+                    store_shadow4(L.shadow, L.shadow_lo, e, ld_cg4(dst_self + e));
                 }
             }
         }
@@ -235,7 +245,8 @@ __global__ void __launch_bounds__(RING_THREADS) ring_kernel(const __grid_constan
 
 // N = 1: the ring is the identity; the owner update alone.
 __global__ void sgd_single_kernel(const float* __restrict__ g, float* __restrict__ w,
-                                  __nv_bfloat16* __restrict__ shadow, int64_t n, int op, float lr) {
+                                  __nv_bfloat16* __restrict__ shadow, __nv_bfloat16* __restrict__ shadow_lo,
+                                  int64_t n, int op, float lr) {
     const int64_t nv = n / 4;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv;
          v += (int64_t)gridDim.x * blockDim.x) {
@@ -249,7 +260,7 @@ __global__ void sgd_single_kernel(const float* __restrict__ g, float* __restrict
         x.z = __fmaf_rn(-lr, a.z, x.z);
         x.w = __fmaf_rn(-lr, a.w, x.w);
         reinterpret_cast<float4*>(w)[v] = x;
-        if (shadow) store_shadow4(shadow, 4 * v, x);
+        if (shadow) store_shadow4(shadow, shadow_lo, 4 * v, x);
     }
 }
 
@@ -334,9 +345,9 @@ cudaError_t launch_ring(const RingParams& p, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_sgd_single(const float* g, float* w, __nv_bfloat16* shadow, int64_t n, int op,
-                              float lr, cudaStream_t s) {
-    sgd_single_kernel<<<296, 512, 0, s>>>(g, w, shadow, n, op, lr);
+cudaError_t launch_sgd_single(const float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo,
+                              int64_t n, int op, float lr, cudaStream_t s) {
+    sgd_single_kernel<<<296, 512, 0, s>>>(g, w, shadow, shadow_lo, n, op, lr);
     return cudaGetLastError();
 }
 

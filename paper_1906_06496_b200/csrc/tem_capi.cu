@@ -11,6 +11,7 @@
 #include <string.h>
 
 #include <new>
+#include <stdlib.h>
 
 #include "kernels.h"
 
@@ -29,8 +30,8 @@ struct HeapLayout {
 };
 
 struct WsLayout {
-    size_t xp, h1, h2, dA2, dA1, z, grad, headpart, wpart, shadow, epochs, stepctr, xstage,
-        labstage, lossstage, per_rank;
+    size_t xp, h1, h2, dA2, dA1, xp_lo, h1_lo, dA2_lo, dA1_lo, z, grad, headpart, wpart, shadow,
+        shadow_lo, epochs, stepctr, xstage, labstage, lossstage, per_rank;
 };
 
 bool cfg_valid(const tem_config* c) {
@@ -57,8 +58,15 @@ int64_t num_params(const tem_config* c) {
     return C * 3 * Ci + C + C * 3 * C + C + Co * C + Co;
 }
 
+int env_path() {
+    const char* e = getenv("TEM_KERNEL_PATH");
+    if (e && (strcmp(e, "simt") == 0 || strcmp(e, "SIMT") == 0)) return PATH_SIMT;
+    return PATH_UMMA;
+}
+
 Geom make_geom(const tem_config* c) {
     Geom g;
+    g.path = env_path();
     g.B = c->batch_per_rank;
     g.T = c->seq_len;
     g.Cin = c->c_in;
@@ -66,6 +74,8 @@ Geom make_geom(const tem_config* c) {
     g.Co = c->c_out;
     g.R = g.B * (g.T + 2);
     g.prec = c->precision;
+    g.op_bf16 = (g.path == PATH_UMMA || g.prec == TEM_BF16) ? 1 : 0;
+    g.split = (g.path == PATH_UMMA && g.prec == TEM_FP32) ? 1 : 0;
     g.K = num_params(c);
     g.Kpad = roundup(g.K, 4 * (int64_t)c->world_size);
     g.off_W1 = 0;
@@ -101,7 +111,8 @@ HeapLayout heap_layout(const tem_config* c) {
 
 WsLayout ws_layout(const tem_config* c) {
     const Geom g = make_geom(c);
-    const size_t esz = g.prec == TEM_BF16 ? 2 : 4;
+    const size_t esz = g.op_bf16 ? 2 : 4;       // operand plane element size
+    const size_t xsz = g.prec == TEM_BF16 ? 2 : 4;  // caller's x element size
     WsLayout w;
     size_t o = 0;
     auto take = [&](size_t bytes) {
@@ -109,21 +120,27 @@ WsLayout ws_layout(const tem_config* c) {
         o = align_up(o + bytes, kAlign);
         return at;
     };
-    const int S = simt_wgrad_splits(g);
+    const int S = simt_wgrad_splits(g) > umma_wgrad_splits(g) ? simt_wgrad_splits(g) : umma_wgrad_splits(g);
     const size_t wmax = (size_t)g.C * 3 * (g.Cin > g.C ? g.Cin : g.C) + g.C;
     w.xp = take((size_t)g.R * g.Cin * esz);
     w.h1 = take((size_t)g.R * g.C * esz);
     w.h2 = take((size_t)g.R * g.C * 4);
     w.dA2 = take((size_t)g.R * g.C * esz);
     w.dA1 = take((size_t)g.R * g.C * esz);
+    const size_t lo = g.split ? 1 : 0;
+    w.xp_lo = take(lo * g.R * g.Cin * esz);
+    w.h1_lo = take(lo * g.R * g.C * esz);
+    w.dA2_lo = take(lo * g.R * g.C * esz);
+    w.dA1_lo = take(lo * g.R * g.C * esz);
     w.z = take((size_t)g.B * g.T * 3 * 4);
     w.grad = take((size_t)g.Kpad * 4);
     w.headpart = take((size_t)g.B * (3 * g.C + 6) * 4);
     w.wpart = take((size_t)S * wmax * 4);
-    w.shadow = take(g.prec == TEM_BF16 ? (size_t)g.Kpad * 2 : 0);
+    w.shadow = take(g.op_bf16 ? (size_t)g.Kpad * 2 : 0);
+    w.shadow_lo = take(lo * (size_t)g.Kpad * 2);
     w.epochs = take((size_t)kMaxChannels * 4);
     w.stepctr = take(8);
-    w.xstage = take((size_t)g.B * g.T * g.Cin * esz);
+    w.xstage = take((size_t)g.B * g.T * g.Cin * xsz);
     w.labstage = take((size_t)g.B * 3 * g.T * 4);
     w.lossstage = take(4 * 4);
     w.per_rank = o;
@@ -141,6 +158,7 @@ struct tem_ctx {
     int N, nlocal, rank;
     int G, C;                  // ring channels / chunks for the TEM gradient
     RankBufs rb[TEM_MAX_RANKS];
+    UmmaPlan* plan[TEM_MAX_RANKS];
     uint32_t* epochs[TEM_MAX_RANKS];
     char* ws_base[TEM_MAX_RANKS];
     Status* st_host;
@@ -242,12 +260,23 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
         b.headpart = (float*)(base + wl.headpart);
         b.wpart = (float*)(base + wl.wpart);
         b.stepctr = (int64_t*)(base + wl.stepctr);
-        b.shadow = c->g.prec == TEM_BF16 ? (__nv_bfloat16*)(base + wl.shadow) : nullptr;
+        b.xp_lo = c->g.split ? base + wl.xp_lo : nullptr;
+        b.h1_lo = c->g.split ? base + wl.h1_lo : nullptr;
+        b.dA2_lo = c->g.split ? base + wl.dA2_lo : nullptr;
+        b.dA1_lo = c->g.split ? base + wl.dA1_lo : nullptr;
+        b.shadow = c->g.op_bf16 ? (__nv_bfloat16*)(base + wl.shadow) : nullptr;
+        b.shadow_lo = c->g.split ? (__nv_bfloat16*)(base + wl.shadow_lo) : nullptr;
         b.wop = b.shadow ? (const void*)b.shadow : (const void*)b.params;
+        c->plan[l] = nullptr;
         c->epochs[l] = (uint32_t*)(base + wl.epochs);
         cudaError_t e = cudaMemsetAsync(base, 0, wl.per_rank, 0);
-        if (e == cudaSuccess && b.shadow) e = launch_cast_shadow(b.params, b.shadow, c->g.Kpad, 0);
+        if (e == cudaSuccess && b.shadow) e = launch_cast_shadow_split(b.params, b.shadow, b.shadow_lo, c->g.Kpad, 0);
+        if (e == cudaSuccess && c->g.path == PATH_UMMA) {
+            c->plan[l] = new (std::nothrow) UmmaPlan();
+            if (!c->plan[l] || !umma_plan(c->g, b, c->plan[l])) e = cudaErrorInvalidValue;
+        }
         if (e != cudaSuccess) {
+            for (int q = 0; q <= l; ++q) delete c->plan[q];
             cudaFreeHost(c->st_host);
             delete c;
             return TEM_ERR_CUDA;
@@ -281,26 +310,33 @@ static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, f
                                cudaStream_t s, int* nl) {
     const EvRec rec{timing_slot_events(c), s};
     const Geom& g = c->g;
-    const size_t esz = g.prec == TEM_BF16 ? 2 : 4;
+    const size_t esz = g.prec == TEM_BF16 ? 2 : 4;  // caller's x element size
     const float lam[3] = {c->cfg.loss_weight[0], c->cfg.loss_weight[1], c->cfg.loss_weight[2]};
     for (int l = 0; l < c->nlocal; ++l) {
         const char* xl = (const char*)x + (size_t)l * g.B * g.T * g.Cin * esz;
         const float* labl = labels + (size_t)l * g.B * 3 * g.T;
         rec.begin(SLOT_PREP);
-        if (launch_prep_x(g, xl, c->rb[l].xp, s) != cudaSuccess) return TEM_ERR_CUDA;
+        cudaError_t e = g.split ? launch_prep_x_split(g, (const float*)xl, c->rb[l].xp, c->rb[l].xp_lo, s)
+                                : launch_prep_x(g, xl, c->rb[l].xp, s);
         rec.end(SLOT_PREP);
+        if (e != cudaSuccess) return TEM_ERR_CUDA;
         ++*nl;
-        if (simt_compute(g, c->rb[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s) != cudaSuccess)
-            return TEM_ERR_CUDA;
+        if (g.path == PATH_UMMA && g.B > 0)
+            e = umma_compute(g, c->rb[l], *c->plan[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s);
+        else
+            e = simt_compute(g, c->rb[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s);
+        if (e != cudaSuccess) return TEM_ERR_CUDA;
     }
     return TEM_OK;
 }
 
-static RingLocal ring_local(tem_ctx* c, int l, const float* src, float* dst, __nv_bfloat16* shadow) {
+static RingLocal ring_local(tem_ctx* c, int l, const float* src, float* dst, __nv_bfloat16* shadow,
+                            __nv_bfloat16* shadow_lo) {
     RingLocal L;
     L.src = src;
     L.dst_self = dst;
     L.shadow = shadow;
+    L.shadow_lo = shadow_lo;
     L.epochs = c->epochs[l];
     for (int r = 0; r < TEM_MAX_RANKS; ++r) L.heaps[r] = r < c->N ? (char*)c->peers[r] : nullptr;
     return L;
@@ -313,7 +349,7 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
     tem_status st = TEM_OK;
     if (c->N == 1) {
         for (int l = 0; l < c->nlocal; ++l) {
-            if (launch_sgd_single(c->rb[l].grad, (float*)c->rb[l].params, c->rb[l].shadow, g.Kpad,
+            if (launch_sgd_single(c->rb[l].grad, (float*)c->rb[l].params, c->rb[l].shadow, c->rb[l].shadow_lo, g.Kpad,
                                   TEM_MEAN, c->cfg.lr, s) != cudaSuccess)
                 return TEM_ERR_CUDA;
             ++*nl;
@@ -324,7 +360,7 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
     RingParams p;
     memset(&p, 0, sizeof(p));
     for (int l = 0; l < c->nlocal; ++l)
-        p.loc[l] = ring_local(c, l, c->rb[l].grad, (float*)c->rb[l].params, c->rb[l].shadow);
+        p.loc[l] = ring_local(c, l, c->rb[l].grad, (float*)c->rb[l].params, c->rb[l].shadow, c->rb[l].shadow_lo);
     p.N = c->N;
     p.rank_base = c->rank;
     p.nlocal = c->nlocal;
@@ -429,7 +465,7 @@ tem_status ring_allreduce(tem_ctx* c, float* buf, int64_t K, int32_t op, void* s
     memset(&p, 0, sizeof(p));
     for (int l = 0; l < c->nlocal; ++l) {
         float* ub = (float*)((char*)c->peers[c->rank + l] + c->hl.off_user);
-        p.loc[l] = ring_local(c, l, ub, ub, nullptr);
+        p.loc[l] = ring_local(c, l, ub, ub, nullptr, nullptr);
     }
     p.N = c->N;
     p.rank_base = c->rank;
@@ -460,7 +496,7 @@ tem_status ps_allreduce(tem_ctx* c, float* buf, int64_t K, int32_t op, void* str
     memset(&p, 0, sizeof(p));
     for (int l = 0; l < c->nlocal; ++l) {
         float* ub = (float*)((char*)c->peers[c->rank + l] + c->hl.off_user);
-        p.loc[l] = ring_local(c, l, ub, ub, nullptr);
+        p.loc[l] = ring_local(c, l, ub, ub, nullptr, nullptr);
     }
     p.N = c->N;
     p.rank_base = c->rank;
@@ -494,6 +530,7 @@ tem_status tem_shutdown(tem_ctx* c) {
     const int32_t code = *(volatile int32_t*)&c->st_host->code;
     if (st == TEM_OK && code != 0) st = (tem_status)code;
     cudaFreeHost(c->st_host);
+    for (int l = 0; l < c->nlocal; ++l) delete c->plan[l];
     if (c->tev) {
         for (size_t i = 0; i < (size_t)c->t_max * NUM_SLOTS * 2; ++i) cudaEventDestroy(c->tev[i]);
         delete[] c->tev;
@@ -511,6 +548,27 @@ float* tem_local_grad(tem_ctx* c, int32_t l) {
 float* tem_logits(tem_ctx* c, int32_t l) {
     if (!c || !c->alive || l < 0 || l >= c->nlocal) return nullptr;
     return c->rb[l].z;
+}
+
+void* tem_debug_buffer(tem_ctx* c, int32_t l, const char* name, int64_t* nbytes) {
+    if (nbytes) *nbytes = 0;
+    if (!c || !c->alive || l < 0 || l >= c->nlocal || !name) return nullptr;
+    const Geom& g = c->g;
+    const RankBufs& b = c->rb[l];
+    const int64_t esz = g.op_bf16 ? 2 : 4;
+    const int64_t act = (int64_t)g.R * g.C * esz, xin = (int64_t)g.R * g.Cin * esz;
+    struct Item { const char* n; const void* p; int64_t bytes; };
+    const Item items[] = {
+        {"xp", b.xp, xin}, {"h1", b.h1, act}, {"h2", b.h2, (int64_t)g.R * g.C * 4}, {"dA2", b.dA2, act},
+        {"dA1", b.dA1, act}, {"xp_lo", b.xp_lo, xin}, {"h1_lo", b.h1_lo, act}, {"dA2_lo", b.dA2_lo, act},
+        {"dA1_lo", b.dA1_lo, act}, {"shadow", b.shadow, g.Kpad * 2}, {"shadow_lo", b.shadow_lo, g.Kpad * 2}};
+    for (const Item& it : items)
+        if (strcmp(it.n, name) == 0) {
+            if (!it.p) return nullptr;
+            if (nbytes) *nbytes = it.bytes;
+            return const_cast<void*>(it.p);
+        }
+    return nullptr;
 }
 
 tem_status tem_relu_decisions(tem_ctx* c, int32_t l, uint8_t* out, void* stream) {
@@ -566,6 +624,7 @@ int32_t tem_launches_per_exchange(tem_ctx* c) { return c ? c->launches_exchange 
 
 const char* tem_kernel_path(tem_ctx* c) {
     if (!c) return "none";
+    if (c->g.path == PATH_UMMA) return c->g.prec == TEM_BF16 ? "tcgen05-bf16" : "tcgen05-bf16x3-fp32";
     return c->g.prec == TEM_BF16 ? "simt-bf16" : "simt-fp32";
 }
 

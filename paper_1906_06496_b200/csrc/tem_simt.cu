@@ -253,7 +253,7 @@ template <typename TOp>
 __global__ void __launch_bounds__(256) head_kernel(
     const float* __restrict__ h2, const float* __restrict__ W3, const float* __restrict__ b3,
     const float* __restrict__ labels, float lam0, float lam1, float lam2, TOp* __restrict__ dA2,
-    float* __restrict__ z_out, float* __restrict__ part, int B, int Tn, int C) {
+    TOp* __restrict__ dA2_lo, float* __restrict__ z_out, float* __restrict__ part, int B, int Tn, int C) {
     extern __shared__ __align__(16) float sm[];
     float* sW3 = sm;                 // [3][C]
     float* sacc = sm + 3 * C;        // [8][3][C]
@@ -320,7 +320,10 @@ __global__ void __launch_bounds__(256) head_kernel(
             float d = sW3[c] * dz[0];
             d = fmaf(sW3[C + c], dz[1], d);
             d = fmaf(sW3[2 * C + c], dz[2], d);
-            dA2[p * C + c] = from_f<TOp>(h[q] > 0.f ? d : 0.f);
+            const float dv = h[q] > 0.f ? d : 0.f;
+            const TOp dh = from_f<TOp>(dv);
+            dA2[p * C + c] = dh;
+            if (dA2_lo) dA2_lo[p * C + c] = from_f<TOp>(dv - to_f(dh));
 #pragma unroll
             for (int o = 0; o < 3; ++o) wacc[o][q] = fmaf(dz[o], h[q], wacc[o][q]);
         }
@@ -329,6 +332,7 @@ __global__ void __launch_bounds__(256) head_kernel(
     for (int i = tid; i < 2 * C; i += blockDim.x) {
         const size_t p = (size_t)v * Tp + (i < C ? 0 : Tp - 1);
         dA2[p * C + (i % C)] = from_f<TOp>(0.f);
+        if (dA2_lo) dA2_lo[p * C + (i % C)] = from_f<TOp>(0.f);
     }
 #pragma unroll
     for (int o = 0; o < 3; ++o)
@@ -423,20 +427,10 @@ cudaError_t conv_launches(const Geom& g, const RankBufs& b, const float* labels,
     rec.end(SLOT_CONV2);
     ++n;
     // a3-a5: head
-    const size_t hsm = (size_t)(3 * g.C + 8 * 3 * g.C) * sizeof(float);
-    cudaFuncSetAttribute(head_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-    if (g.B > 0) {
-        rec.begin(SLOT_HEAD);
-        head_kernel<T><<<g.B, 256, hsm, s>>>(b.h2, b.params + g.off_W3, b.params + g.off_b3, labels,
-                                             lam[0], lam[1], lam[2], dA2, b.z, b.headpart, g.B, g.T, g.C);
-        rec.end(SLOT_HEAD);
-        ++n;
+    {
+        cudaError_t e = launch_head(g, b, labels, lam, loss_out, status, rec, s, &n);
+        if (e != cudaSuccess) return e;
     }
-    rec.begin(SLOT_HEADFIN);
-    head_finalize_kernel<<<(3 * g.C + 3 + 255) / 256, 256, 0, s>>>(
-        b.headpart, b.grad + g.off_W3, loss_out, g.B, g.C, lam[0], lam[1], lam[2], status, b.stepctr);
-    rec.end(SLOT_HEADFIN);
-    ++n;
     // a6: conv2 dgrad -> dA1
     rec.begin(SLOT_DGRAD);
     simt_conv_kernel<DGRAD, T, T, T><<<dim3((R + BM - 1) / BM, (g.C + BN - 1) / BN), blk, 0, s>>>(
@@ -455,7 +449,7 @@ cudaError_t conv_launches(const Geom& g, const RankBufs& b, const float* labels,
     {
         const int64_t nn = (int64_t)g.C * 3 * g.C + g.C;
         rec.begin(SLOT_RED2);
-        reduce_splits_kernel<<<296, 256, 0, s>>>(b.wpart, b.grad + g.off_W2, nn, S_eff);
+        launch_reduce_splits(b.wpart, b.grad + g.off_W2, nn, S_eff, s);
         rec.end(SLOT_RED2);
         ++n;
     }
@@ -467,7 +461,7 @@ cudaError_t conv_launches(const Geom& g, const RankBufs& b, const float* labels,
     {
         const int64_t nn = (int64_t)g.C * 3 * g.Cin + g.C;
         rec.begin(SLOT_RED1);
-        reduce_splits_kernel<<<296, 256, 0, s>>>(b.wpart, b.grad + g.off_W1, nn, S_eff);
+        launch_reduce_splits(b.wpart, b.grad + g.off_W1, nn, S_eff, s);
         rec.end(SLOT_RED1);
         ++n;
     }
@@ -476,6 +470,39 @@ cudaError_t conv_launches(const Geom& g, const RankBufs& b, const float* labels,
 }
 
 }  // namespace
+
+cudaError_t launch_head(const Geom& g, const RankBufs& b, const float* labels, const float lam[3],
+                        float* loss_out, Status* status, const EvRec& rec, cudaStream_t s, int* n) {
+    const size_t hsm = (size_t)(3 * g.C + 8 * 3 * g.C) * sizeof(float);
+    if (g.B > 0) {
+        rec.begin(SLOT_HEAD);
+        if (g.prec == TEM_BF16 || b.dA2_lo) {
+            auto k = head_kernel<__nv_bfloat16>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+            k<<<g.B, 256, hsm, s>>>(b.h2, b.params + g.off_W3, b.params + g.off_b3, labels, lam[0], lam[1], lam[2],
+                                    static_cast<__nv_bfloat16*>(b.dA2), static_cast<__nv_bfloat16*>(b.dA2_lo), b.z,
+                                    b.headpart, g.B, g.T, g.C);
+        } else {
+            auto k = head_kernel<float>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+            k<<<g.B, 256, hsm, s>>>(b.h2, b.params + g.off_W3, b.params + g.off_b3, labels, lam[0], lam[1], lam[2],
+                                    static_cast<float*>(b.dA2), nullptr, b.z, b.headpart, g.B, g.T, g.C);
+        }
+        rec.end(SLOT_HEAD);
+        ++*n;
+    }
+    rec.begin(SLOT_HEADFIN);
+    head_finalize_kernel<<<(3 * g.C + 3 + 255) / 256, 256, 0, s>>>(
+        b.headpart, b.grad + g.off_W3, loss_out, g.B, g.C, lam[0], lam[1], lam[2], status, b.stepctr);
+    rec.end(SLOT_HEADFIN);
+    ++*n;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_splits(const float* part, float* dst, int64_t n, int S, cudaStream_t s) {
+    reduce_splits_kernel<<<296, 256, 0, s>>>(part, dst, n, S);
+    return cudaGetLastError();
+}
 
 int simt_wgrad_splits(const Geom& g) {
     const int tiles = (g.C / BM) * ((3 * g.Cin + BN - 1) / BN);
@@ -512,7 +539,7 @@ __global__ void relu_decisions_kernel(const T* __restrict__ h1, const float* __r
 }
 
 cudaError_t launch_relu_decisions(const Geom& g, const RankBufs& b, uint8_t* out, cudaStream_t s) {
-    if (g.prec == TEM_BF16)
+    if (g.op_bf16)
         relu_decisions_kernel<__nv_bfloat16><<<296, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(b.h1), b.h2,
                                                                  out, g.B, g.T, g.C);
     else

@@ -90,6 +90,8 @@ def lib():
         L.tem_status_string.argtypes = [ctypes.c_int32]
         L.tem_kernel_path.restype = ctypes.c_char_p
         L.tem_kernel_path.argtypes = [_P]
+        L.tem_debug_buffer.restype = _P
+        L.tem_debug_buffer.argtypes = [_P, ctypes.c_int32, ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64)]
         L.tem_relu_decisions.restype = ctypes.c_int
         L.tem_relu_decisions.argtypes = [_P, ctypes.c_int32, _P, _P]
         L.tem_timing_slots.restype = ctypes.c_int32
@@ -109,7 +111,7 @@ EXPORTS = ["tem_num_params", "tem_kpad", "tem_workspace_bytes", "tem_sym_bytes",
            "tem_step_host", "ring_allreduce", "ps_allreduce", "tem_sync", "tem_shutdown",
            "tem_local_grad", "tem_logits", "tem_launches_per_step", "tem_launches_per_exchange",
            "tem_status_string", "tem_kernel_path", "tem_timing_slots", "tem_timing_slot_name",
-           "tem_timing_begin", "tem_timing_end", "tem_relu_decisions"]
+           "tem_timing_begin", "tem_timing_end", "tem_relu_decisions", "tem_debug_buffer"]
 
 
 def status_string(code: int) -> str:
@@ -299,6 +301,18 @@ class TemSession:
         ptr = lib().tem_logits(_P(self.ctx), l)
         B, T = self.sc.batch_per_rank, self.sc.seq_len
         return self._ws_view(ptr, 4 * B * T * 3).view(torch.float32).view(B, T, 3)
+
+    def debug_buffer(self, name: str, l: int = 0):
+        """Internal workspace tensor as a torch view (bf16/fp32 per the path), or None."""
+        nb = ctypes.c_int64(0)
+        ptr = lib().tem_debug_buffer(_P(self.ctx), l, name.encode(), ctypes.byref(nb))
+        if not ptr:
+            return None
+        raw = self._ws_view(ptr, nb.value)
+        if name == "h2":
+            return raw.view(torch.float32)
+        elem = 2 if self.kernel_path().startswith("tcgen05") or self.sc.precision == TEM_BF16 else 4
+        return raw.view(torch.bfloat16 if elem == 2 else torch.float32)
 
     def relu_decisions(self, l: int = 0) -> torch.Tensor:
         B, T, C = self.sc.batch_per_rank, self.sc.seq_len, self.sc.c_hidden

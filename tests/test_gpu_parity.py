@@ -125,9 +125,9 @@ def test_tem_step_emulated_ranks(tem, orc, N, B, prec):
         ref = oracle_with_gpu_decisions(orc, s, r, x[r], p, lab[r], lam, prec)
         check_tensors(orc, grads[r][:s.K], s.logits(r).cpu().numpy(), loss[r].cpu().numpy(), ref, TOL[prec])
     if prec == 1:  # bf16 shadow refreshed from the new weights: next step sees them
+        w1 = s.params(0).cpu().numpy().copy()  # weights after step 1 = inputs of step 2
         loss2 = s.step(xd, ld)
         assert s.sync()[0] == 0
-        w1 = s.params(0).cpu().numpy()
         ref2 = orc.tem_fwd_bwd(x[0], w1, lab[0], lam, prec=1)
         assert rel_err(loss2[0].cpu().numpy(), ref2["loss"]) <= TOL[1]
     s.close()
@@ -280,12 +280,17 @@ def test_empty_batch_and_lr_zero(tem, orc):
 
 
 def test_nonfinite_latched(tem):
+    """a non-finite loss latches NONFINITE with its step index.  (NaN features would
+    not do: ReLU maps NaN pre-activations to 0 -- the comparison a > 0 is false.)"""
     s, p = session(tem, 1, 2, 0)
-    x = torch.full((1, 2, 100, 400), float("nan"), device="cuda")
-    lab = torch.zeros(1, 2, 3, 100, device="cuda")
+    x = torch.from_numpy(datagen.features(2)).cuda()[None]
+    lab = torch.from_numpy(datagen.labels(2)).cuda()[None]
+    s.step(x, lab)
+    assert s.sync()[0] == 0
+    s.params(0)[s.K - 1] = float("nan")  # b3[end] -> z[:, :, 2] = NaN at step 1
     s.step(x, lab)
     code, step = s.sync()
-    assert code == tem.TEM_ERR_NONFINITE and step == 0
+    assert code == tem.TEM_ERR_NONFINITE and step == 1
     with pytest.raises(tem.TemError):
         s.step(x, lab)
     s.ctx = None  # context is poisoned; shutdown would report the latched error
