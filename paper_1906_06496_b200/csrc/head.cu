@@ -1,0 +1,251 @@
+// head.cu -- the TEM head and its deterministic reduction.
+//
+// head_rows_kernel, grid (B videos, HS row-splits), 8 warps, one snippet row per warp
+// iteration:
+//   z_o  = b3[o] + sum_c W3[o][c] h2[c]                           (conv3, k = 1)
+//   p_o  = sigmoid(z_o); b = [g > 0.5]; alpha+/- = T / max(l+/-, 1) per video and channel
+//   L_o += alpha+ b log p + alpha- (1-b) log(1-p), log p = -softplus(-z), log(1-p) = -softplus(z)
+//   dz_o = lambda_o / (B T) * (alpha- (1-b) p - alpha+ b (1-p))    (row a4)
+//   dA2  = 1[h2 > 0] * (W3^T dz), stored in the operand format of the path (row a5)
+// and per-CTA partials of dW3 = sum dz h2^T, db3 = sum dz, L_o, and db2 = sum dA2 (the
+// bias gradient of conv2 sums the same rounded operand the conv2 weight gradient uses).
+// head_reduce_kernel sums the partials in a fixed order (two levels, the last CTA to
+// finish does the second level) into the gradient and the four loss outputs, and latches
+// NONFINITE.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "kernels.h"
+
+namespace tem {
+namespace {
+
+constexpr int HEAD_WARPS = 8;
+
+TEM_DEV float softplusf(float u) { return u > 0.f ? u + log1pf(expf(-u)) : log1pf(expf(u)); }
+
+template <typename TOp>
+__global__ void __launch_bounds__(256) head_rows_kernel(
+    const float* __restrict__ h2, const float* __restrict__ W3, const float* __restrict__ b3,
+    const float* __restrict__ labels, float lam0, float lam1, float lam2, TOp* __restrict__ dA2,
+    TOp* __restrict__ dA2_lo, float* __restrict__ z_out, float* __restrict__ part, int B, int Tn, int C,
+    int HS) {
+    extern __shared__ __align__(16) float sm[];
+    float* sW3 = sm;           // [3][C]
+    float* sacc = sm + 3 * C;  // [8][4C]: dW3 (3C) then db2 (C) per warp
+    __shared__ float s_ap[3], s_an[3], s_misc[HEAD_WARPS][6];
+    __shared__ int s_cnt[3];
+    const int v = blockIdx.x, hs = blockIdx.y, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int Tp = Tn + 2;
+    const int t0 = (int)((int64_t)hs * Tn / HS), t1 = (int)((int64_t)(hs + 1) * Tn / HS);
+    const float lam[3] = {lam0, lam1, lam2};
+    for (int i = tid; i < 3 * C; i += blockDim.x) sW3[i] = W3[i];
+    if (tid < 3) s_cnt[tid] = 0;
+    __syncthreads();
+    for (int i = tid; i < 3 * Tn; i += blockDim.x) {  // l+ per channel (reading R5: strict >)
+        const float g = labels[(size_t)v * 3 * Tn + i];
+        if (g > 0.5f) atomicAdd(&s_cnt[i / Tn], 1);
+    }
+    __syncthreads();
+    if (tid < 3) {
+        const int lp = s_cnt[tid], ln = Tn - lp;
+        s_ap[tid] = (float)Tn / (float)(lp > 1 ? lp : 1);
+        s_an[tid] = (float)Tn / (float)(ln > 1 ? ln : 1);
+    }
+    __syncthreads();
+    const int NQ = C / 32;  // <= 16
+    float wacc[3][16], bacc[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        bacc[q] = 0.f;
+#pragma unroll
+        for (int o = 0; o < 3; ++o) wacc[o][q] = 0.f;
+    }
+    float lsum[3] = {0.f, 0.f, 0.f}, dbs[3] = {0.f, 0.f, 0.f};
+    const float inv_bt = 1.0f / ((float)B * (float)Tn);
+    for (int t = t0 + warp; t < t1; t += HEAD_WARPS) {
+        const size_t p = (size_t)v * Tp + t + 1;
+        float h[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) h[q] = (q < NQ) ? h2[p * C + lane + 32 * q] : 0.f;
+        float z[3];
+#pragma unroll
+        for (int o = 0; o < 3; ++o) {
+            float s = 0.f;
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                if (q < NQ) s = fmaf(sW3[o * C + lane + 32 * q], h[q], s);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+            z[o] = s + b3[o];
+        }
+        float dz[3];
+#pragma unroll
+        for (int o = 0; o < 3; ++o) {
+            const float g = labels[((size_t)v * 3 + o) * Tn + t];
+            const float bt = g > 0.5f ? 1.f : 0.f;
+            const float logp = -softplusf(-z[o]), log1mp = -softplusf(z[o]);
+            lsum[o] += s_ap[o] * bt * logp + s_an[o] * (1.f - bt) * log1mp;
+            const float pr = 1.f / (1.f + expf(-z[o]));
+            dz[o] = lam[o] * inv_bt * (s_an[o] * (1.f - bt) * pr - s_ap[o] * bt * (1.f - pr));
+            dbs[o] += dz[o];
+        }
+        if (lane == 0) {
+            float* zo = z_out + ((size_t)v * Tn + t) * 3;
+            zo[0] = z[0];
+            zo[1] = z[1];
+            zo[2] = z[2];
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            if (q >= NQ) continue;
+            const int c = lane + 32 * q;
+            float d = sW3[c] * dz[0];
+            d = fmaf(sW3[C + c], dz[1], d);
+            d = fmaf(sW3[2 * C + c], dz[2], d);
+            const float dv = h[q] > 0.f ? d : 0.f;
+            const TOp dh = from_f<TOp>(dv);
+            float stored = to_f(dh);
+            dA2[p * C + c] = dh;
+            if (dA2_lo) {
+                const TOp dl = from_f<TOp>(dv - stored);
+                dA2_lo[p * C + c] = dl;
+                stored += to_f(dl);
+            }
+            bacc[q] += stored;
+#pragma unroll
+            for (int o = 0; o < 3; ++o) wacc[o][q] = fmaf(dz[o], h[q], wacc[o][q]);
+        }
+    }
+    if (hs == 0) {  // zero the two halo rows of this video
+        for (int i = tid; i < 2 * C; i += blockDim.x) {
+            const size_t p = (size_t)v * Tp + (i < C ? 0 : Tp - 1);
+            dA2[p * C + (i % C)] = from_f<TOp>(0.f);
+            if (dA2_lo) dA2_lo[p * C + (i % C)] = from_f<TOp>(0.f);
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        if (q >= NQ) continue;
+#pragma unroll
+        for (int o = 0; o < 3; ++o) sacc[(size_t)warp * 4 * C + o * C + lane + 32 * q] = wacc[o][q];
+        sacc[(size_t)warp * 4 * C + 3 * C + lane + 32 * q] = bacc[q];
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int o = 0; o < 3; ++o) {
+            s_misc[warp][o] = lsum[o];
+            s_misc[warp][3 + o] = dbs[o];
+        }
+    }
+    __syncthreads();
+    // partial row layout: [dW3 (3C)][db3 (3)][L (3)][db2 (C)]
+    float* dst = part + ((size_t)v * HS + hs) * (4 * C + 6);
+    for (int i = tid; i < 4 * C; i += blockDim.x) {
+        float s = sacc[i];
+        for (int w = 1; w < HEAD_WARPS; ++w) s += sacc[(size_t)w * 4 * C + i];
+        dst[i < 3 * C ? i : i + 6] = s;
+    }
+    if (tid < 3) {
+        float l = s_misc[0][tid], d = s_misc[0][3 + tid];
+        for (int w = 1; w < HEAD_WARPS; ++w) {
+            l += s_misc[w][tid];
+            d += s_misc[w][3 + tid];
+        }
+        dst[3 * C + tid] = d;
+        dst[3 * C + 3 + tid] = -l / (float)Tn;
+    }
+}
+
+// Two-level fixed-order reduction of the P = B*HS partial rows (n = 4C+6 entries each).
+// Level 1: CTA (x, y) sums rows [y*P/G, (y+1)*P/G) of entries x*256.. into lvl1[y].
+// Level 2: the last CTA to finish sums lvl1[0..G) in order and writes the outputs.
+__global__ void head_reduce_kernel(const float* __restrict__ part, int P, int C, float* __restrict__ lvl1,
+                                   unsigned* __restrict__ counter, float* __restrict__ gW3,
+                                   float* __restrict__ gb2, float* __restrict__ loss_out, int B, float lam0,
+                                   float lam1, float lam2, Status* status, int64_t* stepctr) {
+    const int n = 4 * C + 6;
+    const int G = gridDim.y;
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r0 = (int)((int64_t)blockIdx.y * P / G), r1 = (int)((int64_t)(blockIdx.y + 1) * P / G);
+    if (e < n) {
+        float s = 0.f;
+        for (int r = r0; r < r1; ++r) s += part[(size_t)r * n + e];
+        lvl1[(size_t)blockIdx.y * n + e] = s;
+    }
+    __threadfence();
+    __syncthreads();
+    __shared__ unsigned s_last;
+    if (threadIdx.x == 0) {
+        const unsigned total = gridDim.x * gridDim.y;
+        s_last = (atomicAdd(counter, 1u) == total - 1) ? 1u : 0u;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    __shared__ float s_L[3];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        float s = 0.f;
+        for (int g = 0; g < G; ++g) s += __ldcg(&lvl1[(size_t)g * n + i]);
+        if (i < 3 * C + 3) gW3[i] = s;                 // dW3 then db3 (contiguous in the flat order)
+        else if (i < 3 * C + 6) s_L[i - 3 * C - 3] = s;  // sum over videos of L_o
+        else gb2[i - 3 * C - 6] = s;                   // db2
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        *counter = 0u;
+        float L[3];
+        for (int o = 0; o < 3; ++o) L[o] = B > 0 ? s_L[o] / (float)B : 0.f;
+        const float tot = lam0 * L[0] + lam1 * L[1] + lam2 * L[2];
+        loss_out[0] = tot;
+        loss_out[1] = L[0];
+        loss_out[2] = L[1];
+        loss_out[3] = L[2];
+        const int64_t step = *stepctr;
+        *stepctr = step + 1;
+        if (!isfinite(tot)) latch(status, TEM_ERR_NONFINITE, step);
+    }
+}
+
+}  // namespace
+
+int head_splits(const Geom& g) { return g.T >= 32 ? 4 : 1; }
+int head_groups(const Geom& g) {
+    const int P = g.B * head_splits(g);
+    return P >= 256 ? 32 : (P >= 32 ? 8 : 1);
+}
+
+cudaError_t launch_head(const Geom& g, const RankBufs& b, const float* labels, const float lam[3],
+                        float* loss_out, Status* status, const EvRec& rec, cudaStream_t s, int* n) {
+    const int HS = head_splits(g);
+    const size_t hsm = (size_t)(3 * g.C + HEAD_WARPS * 4 * g.C) * sizeof(float);
+    if (g.B > 0) {
+        rec.begin(SLOT_HEAD);
+        const dim3 grid(g.B, HS);
+        if (g.op_bf16) {
+            auto k = head_rows_kernel<__nv_bfloat16>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+            k<<<grid, 256, hsm, s>>>(b.h2, b.params + g.off_W3, b.params + g.off_b3, labels, lam[0], lam[1], lam[2],
+                                     static_cast<__nv_bfloat16*>(b.dA2), static_cast<__nv_bfloat16*>(b.dA2_lo),
+                                     b.z, b.headpart, g.B, g.T, g.C, HS);
+        } else {
+            auto k = head_rows_kernel<float>;
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+            k<<<grid, 256, hsm, s>>>(b.h2, b.params + g.off_W3, b.params + g.off_b3, labels, lam[0], lam[1], lam[2],
+                                     static_cast<float*>(b.dA2), nullptr, b.z, b.headpart, g.B, g.T, g.C, HS);
+        }
+        rec.end(SLOT_HEAD);
+        ++*n;
+    }
+    rec.begin(SLOT_HEADFIN);
+    const int nent = 4 * g.C + 6;
+    head_reduce_kernel<<<dim3((nent + 255) / 256, head_groups(g)), 256, 0, s>>>(
+        b.headpart, g.B * HS, g.C, b.headlvl1, b.counter, b.grad + g.off_W3, b.grad + g.off_b2, loss_out, g.B,
+        lam[0], lam[1], lam[2], status, b.stepctr);
+    rec.end(SLOT_HEADFIN);
+    ++*n;
+    return cudaGetLastError();
+}
+
+}  // namespace tem

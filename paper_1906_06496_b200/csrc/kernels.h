@@ -47,7 +47,10 @@ struct RankBufs {
     void* dA1_lo;
     float* z;             // [B][T][3]
     float* grad;          // [Kpad] local gradient (flat order W1 b1 W2 b2 W3 b3 pad)
-    float* headpart;      // [B][3C + 6]
+    float* headpart;      // [B*HS][4C + 6] head partials (dW3, db3, L, db2)
+    float* headlvl1;      // [32][4C + 6] first-level sums
+    unsigned* counter;    // last-CTA ticket of the head reduction (self-resetting)
+    float* bpart;         // [m-tiles][C] conv1 bias-gradient partials (tcgen05 DGRAD epilogue)
     float* wpart;         // [S][max(C*3*Cin + C, C*3*C + C)]
     int64_t* stepctr;     // step counter for NONFINITE reporting
     __nv_bfloat16* shadow;     // [Kpad] bf16 weights (hi plane) or nullptr
@@ -67,6 +70,7 @@ struct UmmaParams {
     void* out_hi;      // FWD/DGRAD output plane (bf16) or fp32 (out_f32)
     void* out_lo;      // residual plane or nullptr
     int out_f32;
+    float* bsum;       // DGRAD: per-m-tile column sums of the stored dA1 [m-tiles][Nout] or nullptr
     float* part;       // WGRAD split partials
     int64_t part_stride;
     int NW, Cin_w, cpj;  // WGRAD: 3*Cin, Cin, 64-wide chunks per tap
@@ -84,6 +88,7 @@ cudaError_t launch_cast_shadow_split(const float* params, __nv_bfloat16* hi, __n
 
 // --- SIMT path (tem_simt.cu) ---------------------------------------------------------
 int simt_wgrad_splits(const Geom& g);
+int head_splits(const Geom& g);
 cudaError_t launch_prep_x(const Geom& g, const void* x, void* xp, cudaStream_t s);
 cudaError_t launch_cast_shadow(const float* params, __nv_bfloat16* shadow, int64_t n, cudaStream_t s);
 cudaError_t launch_relu_decisions(const Geom& g, const RankBufs& b, uint8_t* out, cudaStream_t s);

@@ -30,7 +30,7 @@ struct HeapLayout {
 };
 
 struct WsLayout {
-    size_t xp, h1, h2, dA2, dA1, xp_lo, h1_lo, dA2_lo, dA1_lo, z, grad, headpart, wpart, shadow,
+    size_t xp, h1, h2, dA2, dA1, xp_lo, h1_lo, dA2_lo, dA1_lo, z, grad, headpart, headlvl1, counter, bpart, wpart, shadow,
         shadow_lo, epochs, stepctr, xstage, labstage, lossstage, per_rank;
 };
 
@@ -134,7 +134,10 @@ WsLayout ws_layout(const tem_config* c) {
     w.dA1_lo = take(lo * g.R * g.C * esz);
     w.z = take((size_t)g.B * g.T * 3 * 4);
     w.grad = take((size_t)g.Kpad * 4);
-    w.headpart = take((size_t)g.B * (3 * g.C + 6) * 4);
+    w.headpart = take((size_t)g.B * head_splits(g) * (4 * g.C + 6) * 4);
+    w.headlvl1 = take((size_t)32 * (4 * g.C + 6) * 4);
+    w.counter = take(64);
+    w.bpart = take((size_t)((g.R + 127) / 128) * g.C * 4);
     w.wpart = take((size_t)S * wmax * 4);
     w.shadow = take(g.op_bf16 ? (size_t)g.Kpad * 2 : 0);
     w.shadow_lo = take(lo * (size_t)g.Kpad * 2);
@@ -258,6 +261,9 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
         b.z = (float*)(base + wl.z);
         b.grad = (float*)(base + wl.grad);
         b.headpart = (float*)(base + wl.headpart);
+        b.headlvl1 = (float*)(base + wl.headlvl1);
+        b.counter = (unsigned*)(base + wl.counter);
+        b.bpart = (float*)(base + wl.bpart);
         b.wpart = (float*)(base + wl.wpart);
         b.stepctr = (int64_t*)(base + wl.stepctr);
         b.xp_lo = c->g.split ? base + wl.xp_lo : nullptr;

@@ -244,156 +244,6 @@ __global__ void cast_shadow_kernel(const float* __restrict__ w, __nv_bfloat16* _
         s[i] = __float2bfloat16_rn(w[i]);
 }
 
-TEM_DEV float softplusf(float u) { return u > 0.f ? u + log1pf(expf(-u)) : log1pf(expf(u)); }
-
-// Fused head, one CTA per video (rows a3-a5): z = b3 + W3 h2; p = sigmoid(z);
-// weighted logistic loss with per-video class weights; dz; dA2 = 1[h2>0] W3^T dz;
-// per-video partials of dW3, db3 and L_o.  8 warps, warp w handles t = w, w+8, ...
-template <typename TOp>
-__global__ void __launch_bounds__(256) head_kernel(
-    const float* __restrict__ h2, const float* __restrict__ W3, const float* __restrict__ b3,
-    const float* __restrict__ labels, float lam0, float lam1, float lam2, TOp* __restrict__ dA2,
-    TOp* __restrict__ dA2_lo, float* __restrict__ z_out, float* __restrict__ part, int B, int Tn, int C) {
-    extern __shared__ __align__(16) float sm[];
-    float* sW3 = sm;                 // [3][C]
-    float* sacc = sm + 3 * C;        // [8][3][C]
-    __shared__ float s_ap[3], s_an[3], s_misc[8][6];
-    __shared__ int s_cnt[3];
-    const int v = blockIdx.x, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int Tp = Tn + 2;
-    const float lam[3] = {lam0, lam1, lam2};
-    for (int i = tid; i < 3 * C; i += blockDim.x) sW3[i] = W3[i];
-    if (tid < 3) s_cnt[tid] = 0;
-    __syncthreads();
-    // label statistics: l+ per channel (b_t = [g_t > 0.5], reading R5)
-    for (int i = tid; i < 3 * Tn; i += blockDim.x) {
-        const float g = labels[(size_t)v * 3 * Tn + i];
-        if (g > 0.5f) atomicAdd(&s_cnt[i / Tn], 1);
-    }
-    __syncthreads();
-    if (tid < 3) {
-        const int lp = s_cnt[tid], ln = Tn - lp;
-        s_ap[tid] = (float)Tn / (float)(lp > 1 ? lp : 1);
-        s_an[tid] = (float)Tn / (float)(ln > 1 ? ln : 1);
-    }
-    __syncthreads();
-    const int NQ = C / 32;  // <= 16
-    float wacc[3][16];
-#pragma unroll
-    for (int o = 0; o < 3; ++o)
-#pragma unroll
-        for (int q = 0; q < 16; ++q) wacc[o][q] = 0.f;
-    float lsum[3] = {0.f, 0.f, 0.f}, dbs[3] = {0.f, 0.f, 0.f};
-    const float inv_bt = 1.0f / ((float)B * (float)Tn);
-    for (int t = warp; t < Tn; t += 8) {
-        const size_t p = (size_t)v * Tp + t + 1;
-        float h[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) h[q] = (q < NQ) ? h2[p * C + lane + 32 * q] : 0.f;
-        float z[3];
-#pragma unroll
-        for (int o = 0; o < 3; ++o) {
-            float s = 0.f;
-#pragma unroll
-            for (int q = 0; q < 16; ++q)
-                if (q < NQ) s = fmaf(sW3[o * C + lane + 32 * q], h[q], s);
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-            z[o] = s + b3[o];
-        }
-        float dz[3];
-#pragma unroll
-        for (int o = 0; o < 3; ++o) {
-            const float g = labels[((size_t)v * 3 + o) * Tn + t];
-            const float bt = g > 0.5f ? 1.f : 0.f;
-            const float logp = -softplusf(-z[o]), log1mp = -softplusf(z[o]);
-            lsum[o] += s_ap[o] * bt * logp + s_an[o] * (1.f - bt) * log1mp;
-            const float pr = 1.f / (1.f + expf(-z[o]));
-            dz[o] = lam[o] * inv_bt * (s_an[o] * (1.f - bt) * pr - s_ap[o] * bt * (1.f - pr));
-            dbs[o] += dz[o];
-        }
-        if (lane < 3) z_out[((size_t)v * Tn + t) * 3 + lane] = z[lane];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            if (q >= NQ) continue;
-            const int c = lane + 32 * q;
-            float d = sW3[c] * dz[0];
-            d = fmaf(sW3[C + c], dz[1], d);
-            d = fmaf(sW3[2 * C + c], dz[2], d);
-            const float dv = h[q] > 0.f ? d : 0.f;
-            const TOp dh = from_f<TOp>(dv);
-            dA2[p * C + c] = dh;
-            if (dA2_lo) dA2_lo[p * C + c] = from_f<TOp>(dv - to_f(dh));
-#pragma unroll
-            for (int o = 0; o < 3; ++o) wacc[o][q] = fmaf(dz[o], h[q], wacc[o][q]);
-        }
-    }
-    // zero halo rows of dA2
-    for (int i = tid; i < 2 * C; i += blockDim.x) {
-        const size_t p = (size_t)v * Tp + (i < C ? 0 : Tp - 1);
-        dA2[p * C + (i % C)] = from_f<TOp>(0.f);
-        if (dA2_lo) dA2_lo[p * C + (i % C)] = from_f<TOp>(0.f);
-    }
-#pragma unroll
-    for (int o = 0; o < 3; ++o)
-#pragma unroll
-        for (int q = 0; q < 16; ++q)
-            if (q < NQ) sacc[((size_t)warp * 3 + o) * C + lane + 32 * q] = wacc[o][q];
-    if (lane == 0) {
-#pragma unroll
-        for (int o = 0; o < 3; ++o) {
-            s_misc[warp][o] = lsum[o];
-            s_misc[warp][3 + o] = dbs[o];
-        }
-    }
-    __syncthreads();
-    float* dst = part + (size_t)v * (3 * C + 6);
-    for (int i = tid; i < 3 * C; i += blockDim.x) {
-        float s = sacc[i];
-        for (int w = 1; w < 8; ++w) s += sacc[(size_t)w * 3 * C + i];
-        dst[i] = s;
-    }
-    if (tid < 3) {
-        float l = s_misc[0][tid], d = s_misc[0][3 + tid];
-        for (int w = 1; w < 8; ++w) {
-            l += s_misc[w][tid];
-            d += s_misc[w][3 + tid];
-        }
-        dst[3 * C + tid] = d;                // db3 partial
-        dst[3 * C + 3 + tid] = -l / (float)Tn;  // L_o of this video
-    }
-}
-
-// Sum the per-video head partials in ascending video order into the gradient
-// (dW3, db3) and the loss outputs; latch NONFINITE.
-__global__ void head_finalize_kernel(const float* __restrict__ part, float* __restrict__ gW3,
-                                     float* __restrict__ loss_out, int B, int C, float lam0,
-                                     float lam1, float lam2, Status* status, int64_t* stepctr) {
-    const int n = 3 * C + 3;
-    const int stride = 3 * C + 6;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        float s = 0.f;
-        for (int v = 0; v < B; ++v) s += part[(size_t)v * stride + i];
-        gW3[i] = s;  // [W3 (3C)][b3 (3)] contiguous in the flat order
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        float L[3];
-        for (int o = 0; o < 3; ++o) {
-            float s = 0.f;
-            for (int v = 0; v < B; ++v) s += part[(size_t)v * stride + 3 * C + 3 + o];
-            L[o] = B > 0 ? s / (float)B : 0.f;
-        }
-        const float tot = lam0 * L[0] + lam1 * L[1] + lam2 * L[2];
-        loss_out[0] = tot;
-        loss_out[1] = L[0];
-        loss_out[2] = L[1];
-        loss_out[3] = L[2];
-        const int64_t step = *stepctr;
-        *stepctr = step + 1;
-        if (!isfinite(tot)) latch(status, TEM_ERR_NONFINITE, step);
-    }
-}
-
 template <typename T>
 cudaError_t conv_launches(const Geom& g, const RankBufs& b, const float* labels, const float lam[3],
                           float* loss_out, Status* status, int* nl, const EvRec& rec, cudaStream_t s) {
@@ -409,10 +259,7 @@ cudaError_t conv_launches(const Geom& g, const RankBufs& b, const float* labels,
     int n = 0;
     if (g.B == 0) {  // empty shard: zero gradient, zero loss (the update is then a no-op)
         cudaMemsetAsync(b.grad, 0, (size_t)g.Kpad * sizeof(float), s);
-        head_finalize_kernel<<<(3 * g.C + 3 + 255) / 256, 256, 0, s>>>(
-            b.headpart, b.grad + g.off_W3, loss_out, 0, g.C, lam[0], lam[1], lam[2], status, b.stepctr);
-        *nl += 1;
-        return cudaGetLastError();
+        return launch_head(g, b, labels, lam, loss_out, status, rec, s, nl);
     }
     // a1: conv1 + bias + ReLU -> h1
     rec.begin(SLOT_CONV1);
@@ -470,34 +317,6 @@ cudaError_t conv_launches(const Geom& g, const RankBufs& b, const float* labels,
 }
 
 }  // namespace
-
-cudaError_t launch_head(const Geom& g, const RankBufs& b, const float* labels, const float lam[3],
-                        float* loss_out, Status* status, const EvRec& rec, cudaStream_t s, int* n) {
-    const size_t hsm = (size_t)(3 * g.C + 8 * 3 * g.C) * sizeof(float);
-    if (g.B > 0) {
-        rec.begin(SLOT_HEAD);
-        if (g.prec == TEM_BF16 || b.dA2_lo) {
-            auto k = head_kernel<__nv_bfloat16>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-            k<<<g.B, 256, hsm, s>>>(b.h2, b.params + g.off_W3, b.params + g.off_b3, labels, lam[0], lam[1], lam[2],
-                                    static_cast<__nv_bfloat16*>(b.dA2), static_cast<__nv_bfloat16*>(b.dA2_lo), b.z,
-                                    b.headpart, g.B, g.T, g.C);
-        } else {
-            auto k = head_kernel<float>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-            k<<<g.B, 256, hsm, s>>>(b.h2, b.params + g.off_W3, b.params + g.off_b3, labels, lam[0], lam[1], lam[2],
-                                    static_cast<float*>(b.dA2), nullptr, b.z, b.headpart, g.B, g.T, g.C);
-        }
-        rec.end(SLOT_HEAD);
-        ++*n;
-    }
-    rec.begin(SLOT_HEADFIN);
-    head_finalize_kernel<<<(3 * g.C + 3 + 255) / 256, 256, 0, s>>>(
-        b.headpart, b.grad + g.off_W3, loss_out, g.B, g.C, lam[0], lam[1], lam[2], status, b.stepctr);
-    rec.end(SLOT_HEADFIN);
-    ++*n;
-    return cudaGetLastError();
-}
 
 cudaError_t launch_reduce_splits(const float* part, float* dst, int64_t n, int S, cudaStream_t s) {
     reduce_splits_kernel<<<296, 256, 0, s>>>(part, dst, n, S);

@@ -40,7 +40,8 @@ struct Cfg {
     static constexpr uint32_t A_BYTES = BM * BK * 2;
     static constexpr uint32_t B_BYTES = BN * BK * 2;
     static constexpr uint32_t STAGE_BYTES = NPL * (A_BYTES + B_BYTES);
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
+                                     4 * BN * 4 /*epilogue column sums*/;
     static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
 };
 
@@ -76,6 +77,33 @@ TEM_DEV void store16_planes(__nv_bfloat16* hi, __nv_bfloat16* lo, const float (&
     }
 }
 
+// Column sums of a 32-row x 16-column register tile (one row per lane): a reduce-scatter
+// over the warp in a fixed order.  Returns, in lanes L and L^1, the 32-row sum of
+// column ((L>>4)&1)*8 + ((L>>3)&1)*4 + ((L>>2)&1)*2 + ((L>>1)&1).
+TEM_DEV float warp_colsum16(const float (&v)[16], int lane, int* col) {
+    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
+    float a[8], b[4], c[2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const float keep = b4 ? v[i + 8] : v[i], send = b4 ? v[i] : v[i + 8];
+        a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float keep = b3 ? a[i + 4] : a[i], send = b3 ? a[i] : a[i + 4];
+        b[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const float keep = b2 ? b[i + 2] : b[i], send = b2 ? b[i] : b[i + 2];
+        c[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+    }
+    float d = (b1 ? c[1] : c[0]) + __shfl_xor_sync(0xffffffffu, b1 ? c[0] : c[1], 2);
+    d += __shfl_xor_sync(0xffffffffu, d, 1);
+    *col = (b4 ? 8 : 0) + (b3 ? 4 : 0) + (b2 ? 2 : 0) + (b1 ? 1 : 0);
+    return d;
+}
+
 template <int MODE, int BN, int NPASS, int STAGES>
 __global__ void __launch_bounds__(NTHREADS, 1) umma_conv_kernel(const __grid_constant__ UmmaParams P) {
     using C_ = Cfg<BN, NPASS, STAGES>;
@@ -86,6 +114,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_conv_kernel(const __grid_con
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+    float* csum = reinterpret_cast<float*>(smem + STAGES * C_::STAGE_BYTES + 256);  // [4][BN]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.x * BM;
@@ -207,10 +236,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_conv_kernel(const __grid_con
 #pragma unroll
             for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
             if (MODE == FWD_ || MODE == DGRAD_) {
-                if (row >= P.R) continue;
-                const int n = ntile * BN + c16 * 16;
-                if (n >= P.Nout) continue;
-                const bool halo = halo_row(row, P.Tp);
+                const int n = ntile * BN + c16 * 16;  // Nout is a multiple of BN
+                const bool valid = row < P.R;
+                const bool halo = !valid || halo_row(row, P.Tp);
                 if (MODE == FWD_) {
 #pragma unroll
                     for (int i = 0; i < 16; ++i) {
@@ -218,18 +246,36 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_conv_kernel(const __grid_con
                         v[i] = (!halo && t > 0.f) ? t : 0.f;
                     }
                 } else {
-                    const uint4* mk = reinterpret_cast<const uint4*>(
-                        static_cast<const __nv_bfloat16*>(P.mask) + (size_t)row * P.Nout + n);
-                    const uint4 m0v = mk[0], m1v = mk[1];
-                    const uint32_t mw[8] = {m0v.x, m0v.y, m0v.z, m0v.w, m1v.x, m1v.y, m1v.z, m1v.w};
+                    uint32_t mw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                    if (!halo) {
+                        const uint4* mk = reinterpret_cast<const uint4*>(
+                            static_cast<const __nv_bfloat16*>(P.mask) + (size_t)row * P.Nout + n);
+                        const uint4 m0v = mk[0], m1v = mk[1];
+                        mw[0] = m0v.x; mw[1] = m0v.y; mw[2] = m0v.z; mw[3] = m0v.w;
+                        mw[4] = m1v.x; mw[5] = m1v.y; mw[6] = m1v.z; mw[7] = m1v.w;
+                    }
 #pragma unroll
                     for (int i = 0; i < 8; ++i) {
                         const bool p0 = __uint_as_float(mw[i] << 16) > 0.f;
                         const bool p1 = __uint_as_float(mw[i] & 0xFFFF0000u) > 0.f;
-                        v[2 * i] = (!halo && p0) ? v[2 * i] : 0.f;
-                        v[2 * i + 1] = (!halo && p1) ? v[2 * i + 1] : 0.f;
+                        v[2 * i] = p0 ? v[2 * i] : 0.f;
+                        v[2 * i + 1] = p1 ? v[2 * i + 1] : 0.f;
+                    }
+                    if (P.bsum) {
+                        // bias gradient of conv1 (row a8): column sums of the STORED operand
+                        // (bf16(v) [+ bf16(v - bf16(v))]), reduced over this CTA's 128 rows
+                        float sv[16];
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const float h = __bfloat162float(__float2bfloat16_rn(v[i]));
+                            sv[i] = P.out_lo ? h + __bfloat162float(__float2bfloat16_rn(v[i] - h)) : h;
+                        }
+                        int col;
+                        const float cs = warp_colsum16(sv, lane, &col);
+                        if ((lane & 1) == 0) csum[q * BN + c16 * 16 + col] = cs;
                     }
                 }
+                if (!valid) continue;
                 if (P.out_f32) {
                     float4* d = reinterpret_cast<float4*>(static_cast<float*>(P.out_hi) + (size_t)row * P.Nout + n);
 #pragma unroll
@@ -256,6 +302,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_conv_kernel(const __grid_con
                     for (int i = 0; i < 16; ++i)
                         if (c + i < P.Cin_w) dst[i] = v[i];
                 }
+            }
+        }
+        if (MODE == DGRAD_ && P.bsum) {
+            // combine the 4 row-quarters in a fixed order -> bsum[m-tile][n]
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            const int et = threadIdx.x - 64;  // 0..127
+            for (int cidx = et; cidx < BN; cidx += 128) {
+                const float s = ((csum[cidx] + csum[BN + cidx]) + csum[2 * BN + cidx]) + csum[3 * BN + cidx];
+                P.bsum[(size_t)blockIdx.x * P.Nout + ntile * BN + cidx] = s;
             }
         }
     }
@@ -295,21 +350,30 @@ __global__ void prep_x_split_kernel(const float* __restrict__ x, __nv_bfloat16* 
     }
 }
 
-// Bias gradient partials: part[s][off + o] = sum_{p in split s} (hi + lo)[p][o]  (fixed order)
-__global__ void colsum_kernel(const __nv_bfloat16* __restrict__ hi, const __nv_bfloat16* __restrict__ lo,
-                              float* __restrict__ part, int64_t part_stride, int64_t off, int R, int C,
-                              int ksplit_rows) {
-    const int o = blockIdx.x * blockDim.x + threadIdx.x;
-    const int s = blockIdx.y;
-    if (o >= C) return;
-    const int p0 = s * ksplit_rows, p1 = min(R, p0 + ksplit_rows);
-    float acc = 0.f;
-    for (int p = p0; p < p1; ++p) {
-        float v = __bfloat162float(hi[(size_t)p * C + o]);
-        if (lo) v += __bfloat162float(lo[(size_t)p * C + o]);
-        acc += v;
+// Weight gradient = sum of the S split-K partials (ascending s); optionally followed by the
+// bias gradient = sum of nbp per-m-tile column sums (ascending m).  Both fixed order.
+__global__ void reduce_wgrad_kernel(const float* __restrict__ part, int64_t part_stride, int S, int64_t nW,
+                                    const float* __restrict__ bpart, int nbp, int C, float* __restrict__ dst) {
+    const int64_t nvw = nW / 4, nvb = nbp > 0 ? C / 4 : 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvw + nvb;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        float4 a;
+        if (v < nvw) {
+            a = reinterpret_cast<const float4*>(part)[v];
+            for (int s = 1; s < S; ++s) {
+                const float4 b = reinterpret_cast<const float4*>(part + (size_t)s * part_stride)[v];
+                a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+            }
+        } else {
+            const int64_t cv = v - nvw;
+            a = reinterpret_cast<const float4*>(bpart)[cv];
+            for (int m = 1; m < nbp; ++m) {
+                const float4 b = reinterpret_cast<const float4*>(bpart + (size_t)m * C)[cv];
+                a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+            }
+        }
+        reinterpret_cast<float4*>(dst)[v] = a;
     }
-    part[(size_t)s * part_stride + off + o] = acc;
 }
 
 __global__ void cast_shadow_split_kernel(const float* __restrict__ w, __nv_bfloat16* __restrict__ hi,
@@ -394,6 +458,7 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     const int npl = g.prec == TEM_FP32 ? 2 : 1;
     UmmaPlan& P = *plan;
     memset(&P, 0, sizeof(P));
+    if (g.R == 0) return true;  // empty shard: nothing to plan (tem_compute takes the B = 0 branch)
     P.npass = npl == 2 ? 3 : 1;
     const int R = g.R, Tp = g.T + 2;
     // tile widths: split (fp32) path uses narrower N tiles for more CTAs at small batch
@@ -455,6 +520,7 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     P.dgrad.mask = b.h1;
     P.dgrad.out_hi = b.dA1;
     P.dgrad.out_lo = b.dA1_lo;
+    P.dgrad.bsum = b.bpart;
     const int64_t wmax = (int64_t)g.C * 3 * (g.Cin > g.C ? g.Cin : g.C) + g.C;
     common(P.wgrad2);
     P.wgrad2.Nout = g.C;
@@ -510,39 +576,30 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     rec.end(SLOT_DGRAD);
     if (e != cudaSuccess) return e;
     ++n;
-    // WGRAD: 4 o-tiles x 6 chunk-tiles (256 columns = 4 chunks of 64) x S splits
+    // WGRAD: 4 o-tiles x 6 chunk-tiles (256 columns = 4 chunks of 64) x S splits.
+    // db2 was summed by the head (from the stored dA2), db1 by the DGRAD epilogue.
     const int wbn = 256;
-    const __nv_bfloat16* dA2_hi = static_cast<const __nv_bfloat16*>(b.dA2);
-    const __nv_bfloat16* dA2_lo = static_cast<const __nv_bfloat16*>(b.dA2_lo);
-    const __nv_bfloat16* dA1_hi = static_cast<const __nv_bfloat16*>(b.dA1);
-    const __nv_bfloat16* dA1_lo = static_cast<const __nv_bfloat16*>(b.dA1_lo);
     rec.begin(SLOT_WGRAD2);
     e = dispatch<WGRAD_>(P.wgrad2, wbn, P.npass, dim3(g.C / umma::BM, (3 * P.wgrad2.cpj + 3) / 4, P.S), s);
-    if (e == cudaSuccess) {
-        umma::colsum_kernel<<<dim3((g.C + 127) / 128, P.S), 128, 0, s>>>(
-            dA2_hi, dA2_lo, b.wpart, P.wgrad2.part_stride, (int64_t)g.C * 3 * g.C, R, g.C, P.ksplit_rows);
-        e = cudaGetLastError();
-    }
     rec.end(SLOT_WGRAD2);
     if (e != cudaSuccess) return e;
-    n += 2;
+    ++n;
     rec.begin(SLOT_RED2);
-    e = launch_reduce_splits(b.wpart, b.grad + g.off_W2, P.wgrad2.part_stride, P.S, s);
+    umma::reduce_wgrad_kernel<<<296, 256, 0, s>>>(b.wpart, P.wgrad2.part_stride, P.S, (int64_t)g.C * 3 * g.C,
+                                                  nullptr, 0, g.C, b.grad + g.off_W2);
+    e = cudaGetLastError();
     rec.end(SLOT_RED2);
     if (e != cudaSuccess) return e;
     ++n;
     rec.begin(SLOT_WGRAD1);
     e = dispatch<WGRAD_>(P.wgrad1, wbn, P.npass, dim3(g.C / umma::BM, (3 * P.wgrad1.cpj + 3) / 4, P.S), s);
-    if (e == cudaSuccess) {
-        umma::colsum_kernel<<<dim3((g.C + 127) / 128, P.S), 128, 0, s>>>(
-            dA1_hi, dA1_lo, b.wpart, P.wgrad1.part_stride, (int64_t)g.C * 3 * g.Cin, R, g.C, P.ksplit_rows);
-        e = cudaGetLastError();
-    }
     rec.end(SLOT_WGRAD1);
     if (e != cudaSuccess) return e;
-    n += 2;
+    ++n;
     rec.begin(SLOT_RED1);
-    e = launch_reduce_splits(b.wpart, b.grad + g.off_W1, P.wgrad1.part_stride, P.S, s);
+    umma::reduce_wgrad_kernel<<<296, 256, 0, s>>>(b.wpart, P.wgrad1.part_stride, P.S, (int64_t)g.C * 3 * g.Cin,
+                                                  b.bpart, mt, g.C, b.grad + g.off_W1);
+    e = cudaGetLastError();
     rec.end(SLOT_RED1);
     if (e != cudaSuccess) return e;
     ++n;
