@@ -1,17 +1,18 @@
 // head.cu -- the TEM head and its deterministic reduction.
 //
-// head_rows_kernel, grid (B videos, HS row-splits), 8 warps, one snippet row per warp
-// iteration:
+// head_rows_kernel: CTA j owns padded rows [j*RPC, (j+1)*RPC) of the halo layout (a chunk
+// spans at most three videos); 8 warps, one snippet row per warp iteration:
 //   z_o  = b3[o] + sum_c W3[o][c] h2[c]                           (conv3, k = 1)
 //   p_o  = sigmoid(z_o); b = [g > 0.5]; alpha+/- = T / max(l+/-, 1) per video and channel
 //   L_o += alpha+ b log p + alpha- (1-b) log(1-p), log p = -softplus(-z), log(1-p) = -softplus(z)
 //   dz_o = lambda_o / (B T) * (alpha- (1-b) p - alpha+ b (1-p))    (row a4)
-//   dA2  = 1[h2 > 0] * (W3^T dz), stored in the operand format of the path (row a5)
-// and per-CTA partials of dW3 = sum dz h2^T, db3 = sum dz, L_o, and db2 = sum dA2 (the
-// bias gradient of conv2 sums the same rounded operand the conv2 weight gradient uses).
-// head_reduce_kernel sums the partials in a fixed order (two levels, the last CTA to
-// finish does the second level) into the gradient and the four loss outputs, and latches
-// NONFINITE.
+//   dA2  = 1[h2 > 0] * (W3^T dz), stored in the operand format of the path (row a5);
+//          halo rows of dA2 are written as zeros
+// and per-CTA partials of dW3 = sum dz h2^T, db3 = sum dz, -(1/T) sum L terms, and
+// db2 = sum dA2 (the conv2 bias gradient sums the same rounded operand the conv2 weight
+// gradient uses).  head_reduce_kernel sums the partials in a fixed order (two levels; the
+// last CTA to finish does the second) into the gradient and the four loss outputs, and
+// latches NONFINITE.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -30,28 +31,30 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
     const float* __restrict__ h2, const float* __restrict__ W3, const float* __restrict__ b3,
     const float* __restrict__ labels, float lam0, float lam1, float lam2, TOp* __restrict__ dA2,
     TOp* __restrict__ dA2_lo, float* __restrict__ z_out, float* __restrict__ part, int B, int Tn, int C,
-    int HS) {
+    int RPC) {
     extern __shared__ __align__(16) float sm[];
     float* sW3 = sm;           // [3][C]
     float* sacc = sm + 3 * C;  // [8][4C]: dW3 (3C) then db2 (C) per warp
-    __shared__ float s_ap[3], s_an[3], s_misc[HEAD_WARPS][6];
-    __shared__ int s_cnt[3];
-    const int v = blockIdx.x, hs = blockIdx.y, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int Tp = Tn + 2;
-    const int t0 = (int)((int64_t)hs * Tn / HS), t1 = (int)((int64_t)(hs + 1) * Tn / HS);
+    __shared__ float s_ap[3][3], s_an[3][3], s_misc[HEAD_WARPS][6];
+    __shared__ int s_cnt[3][3];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int Tp = Tn + 2, R = B * Tp;
+    const int p0 = blockIdx.x * RPC, p1 = min(R, p0 + RPC);
+    const int v0 = p0 / Tp, nv = (p1 - 1) / Tp - v0 + 1;  // <= 3 videos
     const float lam[3] = {lam0, lam1, lam2};
     for (int i = tid; i < 3 * C; i += blockDim.x) sW3[i] = W3[i];
-    if (tid < 3) s_cnt[tid] = 0;
+    if (tid < 9) s_cnt[tid / 3][tid % 3] = 0;
     __syncthreads();
-    for (int i = tid; i < 3 * Tn; i += blockDim.x) {  // l+ per channel (reading R5: strict >)
-        const float g = labels[(size_t)v * 3 * Tn + i];
-        if (g > 0.5f) atomicAdd(&s_cnt[i / Tn], 1);
+    for (int i = tid; i < nv * 3 * Tn; i += blockDim.x) {  // l+ per video and channel (R5: strict >)
+        const int k = i / (3 * Tn), r = i - k * 3 * Tn;
+        if (labels[(size_t)(v0 + k) * 3 * Tn + r] > 0.5f) atomicAdd(&s_cnt[k][r / Tn], 1);
     }
     __syncthreads();
-    if (tid < 3) {
-        const int lp = s_cnt[tid], ln = Tn - lp;
-        s_ap[tid] = (float)Tn / (float)(lp > 1 ? lp : 1);
-        s_an[tid] = (float)Tn / (float)(ln > 1 ? ln : 1);
+    if (tid < 9) {
+        const int k = tid / 3, o = tid % 3;
+        const int lp = s_cnt[k][o], ln = Tn - lp;
+        s_ap[k][o] = (float)Tn / (float)(lp > 1 ? lp : 1);
+        s_an[k][o] = (float)Tn / (float)(ln > 1 ? ln : 1);
     }
     __syncthreads();
     const int NQ = C / 32;  // <= 16
@@ -64,11 +67,21 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
     }
     float lsum[3] = {0.f, 0.f, 0.f}, dbs[3] = {0.f, 0.f, 0.f};
     const float inv_bt = 1.0f / ((float)B * (float)Tn);
-    for (int t = t0 + warp; t < t1; t += HEAD_WARPS) {
-        const size_t p = (size_t)v * Tp + t + 1;
+    for (int p = p0 + warp; p < p1; p += HEAD_WARPS) {
+        const int v = p / Tp, tp = p - v * Tp;
+        if (tp == 0 || tp == Tp - 1) {  // halo row: zero dA2
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                if (q >= NQ) continue;
+                dA2[(size_t)p * C + lane + 32 * q] = from_f<TOp>(0.f);
+                if (dA2_lo) dA2_lo[(size_t)p * C + lane + 32 * q] = from_f<TOp>(0.f);
+            }
+            continue;
+        }
+        const int t = tp - 1, k = v - v0;
         float h[16];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) h[q] = (q < NQ) ? h2[p * C + lane + 32 * q] : 0.f;
+        for (int q = 0; q < 16; ++q) h[q] = (q < NQ) ? h2[(size_t)p * C + lane + 32 * q] : 0.f;
         float z[3];
 #pragma unroll
         for (int o = 0; o < 3; ++o) {
@@ -85,10 +98,11 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
         for (int o = 0; o < 3; ++o) {
             const float g = labels[((size_t)v * 3 + o) * Tn + t];
             const float bt = g > 0.5f ? 1.f : 0.f;
+            const float ap = s_ap[k][o], an = s_an[k][o];
             const float logp = -softplusf(-z[o]), log1mp = -softplusf(z[o]);
-            lsum[o] += s_ap[o] * bt * logp + s_an[o] * (1.f - bt) * log1mp;
+            lsum[o] += ap * bt * logp + an * (1.f - bt) * log1mp;
             const float pr = 1.f / (1.f + expf(-z[o]));
-            dz[o] = lam[o] * inv_bt * (s_an[o] * (1.f - bt) * pr - s_ap[o] * bt * (1.f - pr));
+            dz[o] = lam[o] * inv_bt * (an * (1.f - bt) * pr - ap * bt * (1.f - pr));
             dbs[o] += dz[o];
         }
         if (lane == 0) {
@@ -107,22 +121,15 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
             const float dv = h[q] > 0.f ? d : 0.f;
             const TOp dh = from_f<TOp>(dv);
             float stored = to_f(dh);
-            dA2[p * C + c] = dh;
+            dA2[(size_t)p * C + c] = dh;
             if (dA2_lo) {
                 const TOp dl = from_f<TOp>(dv - stored);
-                dA2_lo[p * C + c] = dl;
+                dA2_lo[(size_t)p * C + c] = dl;
                 stored += to_f(dl);
             }
             bacc[q] += stored;
 #pragma unroll
             for (int o = 0; o < 3; ++o) wacc[o][q] = fmaf(dz[o], h[q], wacc[o][q]);
-        }
-    }
-    if (hs == 0) {  // zero the two halo rows of this video
-        for (int i = tid; i < 2 * C; i += blockDim.x) {
-            const size_t p = (size_t)v * Tp + (i < C ? 0 : Tp - 1);
-            dA2[p * C + (i % C)] = from_f<TOp>(0.f);
-            if (dA2_lo) dA2_lo[p * C + (i % C)] = from_f<TOp>(0.f);
         }
     }
 #pragma unroll
@@ -141,7 +148,7 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
     }
     __syncthreads();
     // partial row layout: [dW3 (3C)][db3 (3)][L (3)][db2 (C)]
-    float* dst = part + ((size_t)v * HS + hs) * (4 * C + 6);
+    float* dst = part + (size_t)blockIdx.x * (4 * C + 6);
     for (int i = tid; i < 4 * C; i += blockDim.x) {
         float s = sacc[i];
         for (int w = 1; w < HEAD_WARPS; ++w) s += sacc[(size_t)w * 4 * C + i];
@@ -158,7 +165,7 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
     }
 }
 
-// Two-level fixed-order reduction of the P = B*HS partial rows (n = 4C+6 entries each).
+// Two-level fixed-order reduction of the P partial rows (n = 4C+6 entries each).
 // Level 1: CTA (x, y) sums rows [y*P/G, (y+1)*P/G) of entries x*256.. into lvl1[y].
 // Level 2: the last CTA to finish sums lvl1[0..G) in order and writes the outputs.
 __global__ void head_reduce_kernel(const float* __restrict__ part, int P, int C, float* __restrict__ lvl1,
@@ -208,41 +215,46 @@ __global__ void head_reduce_kernel(const float* __restrict__ part, int P, int C,
     }
 }
 
+int head_rows_per_cta(const Geom& g) {
+    int rpc = (g.R + 295) / 296;
+    rpc = (rpc + 7) / 8 * 8;
+    if (rpc < 16) rpc = 16;
+    if (rpc > 128) rpc = 128;
+    return rpc;
+}
+
 }  // namespace
 
-int head_splits(const Geom& g) { return g.T >= 32 ? 4 : 1; }
-int head_groups(const Geom& g) {
-    const int P = g.B * head_splits(g);
-    return P >= 256 ? 32 : (P >= 32 ? 8 : 1);
-}
+int head_ctas(const Geom& g) { return g.R > 0 ? (g.R + head_rows_per_cta(g) - 1) / head_rows_per_cta(g) : 0; }
 
 cudaError_t launch_head(const Geom& g, const RankBufs& b, const float* labels, const float lam[3],
                         float* loss_out, Status* status, const EvRec& rec, cudaStream_t s, int* n) {
-    const int HS = head_splits(g);
+    const int P = head_ctas(g);
     const size_t hsm = (size_t)(3 * g.C + HEAD_WARPS * 4 * g.C) * sizeof(float);
-    if (g.B > 0) {
+    if (P > 0) {
         rec.begin(SLOT_HEAD);
-        const dim3 grid(g.B, HS);
+        const int rpc = head_rows_per_cta(g);
         if (g.op_bf16) {
             auto k = head_rows_kernel<__nv_bfloat16>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-            k<<<grid, 256, hsm, s>>>(b.h2, b.params + g.off_W3, b.params + g.off_b3, labels, lam[0], lam[1], lam[2],
-                                     static_cast<__nv_bfloat16*>(b.dA2), static_cast<__nv_bfloat16*>(b.dA2_lo),
-                                     b.z, b.headpart, g.B, g.T, g.C, HS);
+            k<<<P, 256, hsm, s>>>(b.h2, b.params + g.off_W3, b.params + g.off_b3, labels, lam[0], lam[1], lam[2],
+                                  static_cast<__nv_bfloat16*>(b.dA2), static_cast<__nv_bfloat16*>(b.dA2_lo), b.z,
+                                  b.headpart, g.B, g.T, g.C, rpc);
         } else {
             auto k = head_rows_kernel<float>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-            k<<<grid, 256, hsm, s>>>(b.h2, b.params + g.off_W3, b.params + g.off_b3, labels, lam[0], lam[1], lam[2],
-                                     static_cast<float*>(b.dA2), nullptr, b.z, b.headpart, g.B, g.T, g.C, HS);
+            k<<<P, 256, hsm, s>>>(b.h2, b.params + g.off_W3, b.params + g.off_b3, labels, lam[0], lam[1], lam[2],
+                                  static_cast<float*>(b.dA2), nullptr, b.z, b.headpart, g.B, g.T, g.C, rpc);
         }
         rec.end(SLOT_HEAD);
         ++*n;
     }
     rec.begin(SLOT_HEADFIN);
     const int nent = 4 * g.C + 6;
-    head_reduce_kernel<<<dim3((nent + 255) / 256, head_groups(g)), 256, 0, s>>>(
-        b.headpart, g.B * HS, g.C, b.headlvl1, b.counter, b.grad + g.off_W3, b.grad + g.off_b2, loss_out, g.B,
-        lam[0], lam[1], lam[2], status, b.stepctr);
+    const int G = P >= 64 ? 8 : 1;
+    head_reduce_kernel<<<dim3((nent + 255) / 256, G), 256, 0, s>>>(
+        b.headpart, P, g.C, b.headlvl1, b.counter, b.grad + g.off_W3, b.grad + g.off_b2, loss_out, g.B, lam[0],
+        lam[1], lam[2], status, b.stepctr);
     rec.end(SLOT_HEADFIN);
     ++*n;
     return cudaGetLastError();

@@ -51,6 +51,7 @@ struct RankBufs {
     float* headlvl1;      // [32][4C + 6] first-level sums
     unsigned* counter;    // last-CTA ticket of the head reduction (self-resetting)
     float* bpart;         // [m-tiles][C] conv1 bias-gradient partials (tcgen05 DGRAD epilogue)
+    void* ones;           // [R][128] bf16 ones/zeros operand for the bias-gradient column
     float* wpart;         // [S][max(C*3*Cin + C, C*3*C + C)]
     int64_t* stepctr;     // step counter for NONFINITE reporting
     __nv_bfloat16* shadow;     // [Kpad] bf16 weights (hi plane) or nullptr
@@ -75,6 +76,8 @@ struct UmmaParams {
     int64_t part_stride;
     int NW, Cin_w, cpj;  // WGRAD: 3*Cin, Cin, 64-wide chunks per tap
     int ksplit_rows;
+    int ones_chunk;      // WGRAD: chunk slot 3*cpj reads the all-ones map (bias gradient column)
+    CUtensorMap ones;    // [R][128] bf16: columns 0..63 = 1, 64..127 = 0
 };
 struct UmmaPlan {
     UmmaParams conv1, conv2, dgrad, wgrad1, wgrad2;
@@ -82,13 +85,14 @@ struct UmmaPlan {
 };
 int umma_wgrad_splits(const Geom& g);
 bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan);
+cudaError_t launch_fill_ones(void* ones, int64_t rows, cudaStream_t s);
 cudaError_t launch_prep_x_split(const Geom& g, const float* x, void* hi, void* lo, cudaStream_t s);
 cudaError_t launch_cast_shadow_split(const float* params, __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t n,
                                      cudaStream_t s);
 
 // --- SIMT path (tem_simt.cu) ---------------------------------------------------------
 int simt_wgrad_splits(const Geom& g);
-int head_splits(const Geom& g);
+int head_ctas(const Geom& g);
 cudaError_t launch_prep_x(const Geom& g, const void* x, void* xp, cudaStream_t s);
 cudaError_t launch_cast_shadow(const float* params, __nv_bfloat16* shadow, int64_t n, cudaStream_t s);
 cudaError_t launch_relu_decisions(const Geom& g, const RankBufs& b, uint8_t* out, cudaStream_t s);

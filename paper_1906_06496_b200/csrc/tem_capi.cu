@@ -31,7 +31,7 @@ struct HeapLayout {
 
 struct WsLayout {
     size_t xp, h1, h2, dA2, dA1, xp_lo, h1_lo, dA2_lo, dA1_lo, z, grad, headpart, headlvl1, counter, bpart, wpart, shadow,
-        shadow_lo, epochs, stepctr, xstage, labstage, lossstage, per_rank;
+        shadow_lo, ones, epochs, stepctr, xstage, labstage, lossstage, per_rank;
 };
 
 bool cfg_valid(const tem_config* c) {
@@ -134,13 +134,14 @@ WsLayout ws_layout(const tem_config* c) {
     w.dA1_lo = take(lo * g.R * g.C * esz);
     w.z = take((size_t)g.B * g.T * 3 * 4);
     w.grad = take((size_t)g.Kpad * 4);
-    w.headpart = take((size_t)g.B * head_splits(g) * (4 * g.C + 6) * 4);
+    w.headpart = take((size_t)head_ctas(g) * (4 * g.C + 6) * 4);
     w.headlvl1 = take((size_t)32 * (4 * g.C + 6) * 4);
     w.counter = take(64);
     w.bpart = take((size_t)((g.R + 127) / 128) * g.C * 4);
     w.wpart = take((size_t)S * wmax * 4);
     w.shadow = take(g.op_bf16 ? (size_t)g.Kpad * 2 : 0);
     w.shadow_lo = take(lo * (size_t)g.Kpad * 2);
+    w.ones = take(g.path == PATH_UMMA ? (size_t)g.R * 128 * 2 : 0);
     w.epochs = take((size_t)kMaxChannels * 4);
     w.stepctr = take(8);
     w.xstage = take((size_t)g.B * g.T * g.Cin * xsz);
@@ -264,6 +265,7 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
         b.headlvl1 = (float*)(base + wl.headlvl1);
         b.counter = (unsigned*)(base + wl.counter);
         b.bpart = (float*)(base + wl.bpart);
+        b.ones = c->g.path == PATH_UMMA ? base + wl.ones : nullptr;
         b.wpart = (float*)(base + wl.wpart);
         b.stepctr = (int64_t*)(base + wl.stepctr);
         b.xp_lo = c->g.split ? base + wl.xp_lo : nullptr;
@@ -277,6 +279,7 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
         c->epochs[l] = (uint32_t*)(base + wl.epochs);
         cudaError_t e = cudaMemsetAsync(base, 0, wl.per_rank, 0);
         if (e == cudaSuccess && b.shadow) e = launch_cast_shadow_split(b.params, b.shadow, b.shadow_lo, c->g.Kpad, 0);
+        if (e == cudaSuccess && b.ones) e = launch_fill_ones(b.ones, c->g.R, 0);
         if (e == cudaSuccess && c->g.path == PATH_UMMA) {
             c->plan[l] = new (std::nothrow) UmmaPlan();
             if (!c->plan[l] || !umma_plan(c->g, b, c->plan[l])) e = cudaErrorInvalidValue;

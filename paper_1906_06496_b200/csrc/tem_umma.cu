@@ -180,6 +180,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_conv_kernel(const __grid_con
 #pragma unroll
                         for (int q = 0; q < BN / 64; ++q) {
                             int g = ntile * (BN / 64) + q;
+                            if (P.ones_chunk && g == 3 * P.cpj) {
+                                // all-ones B chunk (lo plane: zeros): column 0 of D = sum_p dA[p][o],
+                                // the bias gradient, on the tensor core in the same split precision
+                                tma_load_2d(sb + q * (BK * 128), &P.ones, &full[s], 64 * pl, p0);
+                                continue;
+                            }
                             if (g >= 3 * P.cpj) g = 3 * P.cpj - 1;  // dummy chunk, discarded by the epilogue
                             const int j = g / P.cpj, c0 = (g % P.cpj) * 64;
                             tma_load_2d(sb + q * (BK * 128), &P.b[pl], &full[s], c0, p0 + j - 1);
@@ -289,6 +295,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_conv_kernel(const __grid_con
             } else {  // WGRAD partial: row = o, columns -> (j, c)
                 const int nl = c16 * 16;
                 const int g = ntile * (BN / 64) + nl / 64;
+                if (P.ones_chunk && g == 3 * P.cpj) {
+                    if (nl % 64 == 0)  // column 0 of the ones chunk: bias gradient partial
+                        P.part[(size_t)split * P.part_stride + (size_t)P.Nout * P.NW + row] = v[0];
+                    continue;
+                }
                 if (g >= 3 * P.cpj) continue;
                 const int j = g / P.cpj, c = (g % P.cpj) * 64 + (nl % 64);
                 if (c >= P.Cin_w) continue;
@@ -374,6 +385,13 @@ __global__ void reduce_wgrad_kernel(const float* __restrict__ part, int64_t part
         }
         reinterpret_cast<float4*>(dst)[v] = a;
     }
+}
+
+// [R][128] bf16: columns 0..63 = 1.0, 64..127 = 0 (the bias-gradient "ones" operand)
+__global__ void fill_ones_kernel(__nv_bfloat16* __restrict__ o, int64_t rows) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows * 128;
+         i += (int64_t)gridDim.x * blockDim.x)
+        o[i] = __float2bfloat16_rn((i & 127) < 64 ? 1.f : 0.f);
 }
 
 __global__ void cast_shadow_split_kernel(const float* __restrict__ w, __nv_bfloat16* __restrict__ hi,
@@ -520,7 +538,7 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     P.dgrad.mask = b.h1;
     P.dgrad.out_hi = b.dA1;
     P.dgrad.out_lo = b.dA1_lo;
-    P.dgrad.bsum = b.bpart;
+    P.dgrad.bsum = nullptr;  // db1 comes from the ones column of the conv1 wgrad GEMM
     const int64_t wmax = (int64_t)g.C * 3 * (g.Cin > g.C ? g.Cin : g.C) + g.C;
     common(P.wgrad2);
     P.wgrad2.Nout = g.C;
@@ -536,6 +554,8 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     P.wgrad1.NW = 3 * g.Cin;
     P.wgrad1.part = b.wpart;
     P.wgrad1.part_stride = (int64_t)g.C * 3 * g.Cin + g.C;
+    P.wgrad1.ones_chunk = 1;
+    ok &= map2d(&P.wgrad1.ones, b.ones, 128, R, umma::BK);
     (void)wmax;
     return ok;
 }
@@ -597,8 +617,8 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     if (e != cudaSuccess) return e;
     ++n;
     rec.begin(SLOT_RED1);
-    umma::reduce_wgrad_kernel<<<296, 256, 0, s>>>(b.wpart, P.wgrad1.part_stride, P.S, (int64_t)g.C * 3 * g.Cin,
-                                                  b.bpart, mt, g.C, b.grad + g.off_W1);
+    umma::reduce_wgrad_kernel<<<296, 256, 0, s>>>(b.wpart, P.wgrad1.part_stride, P.S,
+                                                  (int64_t)g.C * 3 * g.Cin + g.C, nullptr, 0, g.C, b.grad + g.off_W1);
     e = cudaGetLastError();
     rec.end(SLOT_RED1);
     if (e != cudaSuccess) return e;
@@ -610,6 +630,12 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
 cudaError_t launch_prep_x_split(const Geom& g, const float* x, void* hi, void* lo, cudaStream_t s) {
     umma::prep_x_split_kernel<<<296, 256, 0, s>>>(x, static_cast<__nv_bfloat16*>(hi), static_cast<__nv_bfloat16*>(lo),
                                                  g.B, g.T, g.Cin);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill_ones(void* ones, int64_t rows, cudaStream_t s) {
+    if (rows <= 0) return cudaSuccess;
+    umma::fill_ones_kernel<<<296, 256, 0, s>>>(static_cast<__nv_bfloat16*>(ones), rows);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,43 @@
+#!/usr/bin/env python
+"""Run a few tem_step calls of a workload (for ncu / compute-sanitizer captures).
+
+    python scripts/prof_step.py [--workload c2|c3|c1] [--steps 3] [--path umma|simt]
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--path", default="umma")
+    ap.add_argument("--ranks", type=int, default=1, help="emulated ranks on this device")
+    args = ap.parse_args()
+    os.environ["TEM_KERNEL_PATH"] = args.path
+    import numpy as np
+    import torch
+    import datagen
+    from paper_1906_06496_b200 import tem
+    B, prec = {"c1": (4, 0), "c2": (16, 0), "c3": (256, 1)}[args.workload]
+    N = args.ranks
+    sc = tem.SessionConfig(world_size=N, rank=0, local_ranks=N, batch_per_rank=B, precision=prec, lr=0.01)
+    s = tem.TemSession(sc, datagen.init_params())
+    xs = np.stack([datagen.features(B, rank=r) for r in range(N)])
+    lab = torch.from_numpy(np.stack([datagen.labels(B, rank=r) for r in range(N)])).cuda()
+    x = torch.from_numpy(datagen.to_bf16_bits(xs).view(np.int16)).cuda() if prec == 1 else torch.from_numpy(xs).cuda()
+    for _ in range(args.steps):
+        s.step(x, lab)
+    code, _ = s.sync()
+    torch.cuda.synchronize()
+    print("path", s.kernel_path(), "status", tem.status_string(code), "loss", s.loss[0].tolist())
+    s.close()
+    return 0 if code == 0 else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
