@@ -67,7 +67,23 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
     }
     float lsum[3] = {0.f, 0.f, 0.f}, dbs[3] = {0.f, 0.f, 0.f};
     const float inv_bt = 1.0f / ((float)B * (float)Tn);
+    // software pipeline: the next row's h2 is in flight while the current row is processed
+    float hn[16];
+    {
+        const int p = p0 + warp;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) hn[q] = (q < NQ && p < p1) ? __ldcs(h2 + (size_t)p * C + lane + 32 * q) : 0.f;
+    }
     for (int p = p0 + warp; p < p1; p += HEAD_WARPS) {
+        float h[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) h[q] = hn[q];
+        {
+            const int pn = p + HEAD_WARPS;
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                hn[q] = (q < NQ && pn < p1) ? __ldcs(h2 + (size_t)pn * C + lane + 32 * q) : 0.f;
+        }
         const int v = p / Tp, tp = p - v * Tp;
         if (tp == 0 || tp == Tp - 1) {  // halo row: zero dA2
 #pragma unroll
@@ -79,9 +95,6 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
             continue;
         }
         const int t = tp - 1, k = v - v0;
-        float h[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) h[q] = (q < NQ) ? h2[(size_t)p * C + lane + 32 * q] : 0.f;
         float z[3];
 #pragma unroll
         for (int o = 0; o < 3; ++o) {
@@ -167,7 +180,8 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
 
 // Two-level fixed-order reduction of the P partial rows (n = 4C+6 entries each).
 // Level 1: CTA (x, y) sums rows [y*P/G, (y+1)*P/G) of entries x*256.. into lvl1[y].
-// Level 2: the last CTA to finish sums lvl1[0..G) in order and writes the outputs.
+// Level 2: per column block x, the last of its G CTAs sums lvl1[0..G) in order and writes
+// those outputs; the block holding the three loss sums also writes loss_out.
 __global__ void head_reduce_kernel(const float* __restrict__ part, int P, int C, float* __restrict__ lvl1,
                                    unsigned* __restrict__ counter, float* __restrict__ gW3,
                                    float* __restrict__ gb2, float* __restrict__ loss_out, int B, float lam0,
@@ -178,30 +192,31 @@ __global__ void head_reduce_kernel(const float* __restrict__ part, int P, int C,
     const int r0 = (int)((int64_t)blockIdx.y * P / G), r1 = (int)((int64_t)(blockIdx.y + 1) * P / G);
     if (e < n) {
         float s = 0.f;
+#pragma unroll 8
         for (int r = r0; r < r1; ++r) s += part[(size_t)r * n + e];
         lvl1[(size_t)blockIdx.y * n + e] = s;
     }
     __threadfence();
     __syncthreads();
     __shared__ unsigned s_last;
-    if (threadIdx.x == 0) {
-        const unsigned total = gridDim.x * gridDim.y;
-        s_last = (atomicAdd(counter, 1u) == total - 1) ? 1u : 0u;
-    }
+    if (threadIdx.x == 0) s_last = (atomicAdd(&counter[blockIdx.x], 1u) == (unsigned)G - 1) ? 1u : 0u;
     __syncthreads();
     if (!s_last) return;
     __threadfence();
     __shared__ float s_L[3];
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int lb = 3 * C + 3;  // first loss entry
+    const bool has_loss = (lb >= (int)(blockIdx.x * blockDim.x)) && (lb < (int)((blockIdx.x + 1) * blockDim.x));
+    if (e < n) {
         float s = 0.f;
-        for (int g = 0; g < G; ++g) s += __ldcg(&lvl1[(size_t)g * n + i]);
-        if (i < 3 * C + 3) gW3[i] = s;                 // dW3 then db3 (contiguous in the flat order)
-        else if (i < 3 * C + 6) s_L[i - 3 * C - 3] = s;  // sum over videos of L_o
-        else gb2[i - 3 * C - 6] = s;                   // db2
+#pragma unroll 8
+        for (int g = 0; g < G; ++g) s += __ldcg(&lvl1[(size_t)g * n + e]);
+        if (e < 3 * C + 3) gW3[e] = s;                 // dW3 then db3 (contiguous in the flat order)
+        else if (e < 3 * C + 6) s_L[e - 3 * C - 3] = s;  // sum over videos of L_o
+        else gb2[e - 3 * C - 6] = s;                   // db2
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        *counter = 0u;
+    if (threadIdx.x == 0) counter[blockIdx.x] = 0u;
+    if (has_loss && threadIdx.x == 0) {
         float L[3];
         for (int o = 0; o < 3; ++o) L[o] = B > 0 ? s_L[o] / (float)B : 0.f;
         const float tot = lam0 * L[0] + lam1 * L[1] + lam2 * L[2];
@@ -251,7 +266,7 @@ cudaError_t launch_head(const Geom& g, const RankBufs& b, const float* labels, c
     }
     rec.begin(SLOT_HEADFIN);
     const int nent = 4 * g.C + 6;
-    const int G = P >= 64 ? 8 : 1;
+    const int G = P >= 128 ? 16 : (P >= 16 ? 4 : 1);
     head_reduce_kernel<<<dim3((nent + 255) / 256, G), 256, 0, s>>>(
         b.headpart, P, g.C, b.headlvl1, b.counter, b.grad + g.off_W3, b.grad + g.off_b2, loss_out, g.B, lam[0],
         lam[1], lam[2], status, b.stepctr);

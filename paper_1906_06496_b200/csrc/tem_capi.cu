@@ -172,7 +172,66 @@ struct tem_ctx {
     // per-kernel timing (tem_timing_*)
     cudaEvent_t* tev;  // [max_steps][NUM_SLOTS*2]
     int t_max, t_idx;
+    // CUDA-graph replay of whole steps (one graph per input pointer set), run on a private
+    // non-blocking stream ordered with the caller's stream by events
+    struct GraphEntry {
+        const void* x;
+        const void* lab;
+        void* loss;
+        cudaGraphExec_t exec;
+        int launches;
+    };
+    static constexpr int kMaxGraphs = 16;
+    GraphEntry graphs[kMaxGraphs];
+    int ngraphs;
+    bool use_graphs;
+    cudaStream_t gstream;
+    cudaEvent_t ev_in, ev_out;
 };
+
+namespace {
+// Replay (capturing on first use) the step for this pointer set.  Returns TEM_OK, or an error
+// from capture; `fn` enqueues the step on the stream it is given and reports its launches.
+template <typename F>
+tem_status graph_step(tem_ctx* c, const void* x, const void* lab, void* loss, cudaStream_t s, F&& fn) {
+    tem_ctx::GraphEntry* e = nullptr;
+    for (int i = 0; i < c->ngraphs; ++i)
+        if (c->graphs[i].x == x && c->graphs[i].lab == lab && c->graphs[i].loss == loss) e = &c->graphs[i];
+    if (!e) {
+        if (c->ngraphs == tem_ctx::kMaxGraphs) {  // evict the oldest
+            cudaGraphExecDestroy(c->graphs[0].exec);
+            for (int i = 1; i < c->ngraphs; ++i) c->graphs[i - 1] = c->graphs[i];
+            --c->ngraphs;
+        }
+        cudaGraph_t graph = nullptr;
+        if (cudaStreamBeginCapture(c->gstream, cudaStreamCaptureModeRelaxed) != cudaSuccess) return TEM_ERR_CUDA;
+        int nl = 0;
+        const tem_status st = fn(c->gstream, &nl);
+        const cudaError_t ce = cudaStreamEndCapture(c->gstream, &graph);
+        if (st != TEM_OK || ce != cudaSuccess) {
+            if (graph) cudaGraphDestroy(graph);
+            cudaGetLastError();
+            return st != TEM_OK ? st : TEM_ERR_CUDA;
+        }
+        cudaGraphExec_t exec = nullptr;
+        const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        if (ie != cudaSuccess) return TEM_ERR_CUDA;
+        e = &c->graphs[c->ngraphs++];
+        e->x = x;
+        e->lab = lab;
+        e->loss = loss;
+        e->exec = exec;
+        e->launches = nl;
+    }
+    if (cudaEventRecord(c->ev_in, s) != cudaSuccess || cudaStreamWaitEvent(c->gstream, c->ev_in, 0) != cudaSuccess ||
+        cudaGraphLaunch(e->exec, c->gstream) != cudaSuccess || cudaEventRecord(c->ev_out, c->gstream) != cudaSuccess ||
+        cudaStreamWaitEvent(s, c->ev_out, 0) != cudaSuccess)
+        return TEM_ERR_CUDA;
+    c->launches_step = e->launches;
+    return TEM_OK;
+}
+}  // namespace
 
 extern "C" {
 
@@ -298,6 +357,18 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
     }
     c->launches_step = 0;
     c->launches_exchange = 0;
+    c->ngraphs = 0;
+    // graphs: one rank per process only (the emulation's cooperative launch is not captured)
+    const char* ng = getenv("TEM_NO_GRAPH");
+    c->use_graphs = c->nlocal == 1 && !(ng && ng[0] == '1');
+    c->gstream = nullptr;
+    if (c->use_graphs &&
+        (cudaStreamCreateWithFlags(&c->gstream, cudaStreamNonBlocking) != cudaSuccess ||
+         cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming) != cudaSuccess ||
+         cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming) != cudaSuccess)) {
+        cudaGetLastError();
+        c->use_graphs = false;
+    }
     c->alive = true;
     *out = c;
     return TEM_OK;
@@ -415,6 +486,16 @@ tem_status tem_step(tem_ctx* c, const void* x, const float* labels, float* loss_
     if (st != TEM_OK) return st;
     if ((!x || !labels) && c->g.B > 0) return TEM_ERR_INVALID_ARG;
     if (!loss_out) return TEM_ERR_INVALID_ARG;
+    if (c->use_graphs && !c->tev) {
+        return graph_step(c, x, labels, loss_out, (cudaStream_t)stream, [&](cudaStream_t gs, int* n) {
+            int a = 0, b = 0;
+            tem_status r = compute_impl(c, x, labels, loss_out, gs, &a);
+            if (r == TEM_OK) r = exchange_impl(c, gs, &b);
+            *n = a + b;
+            c->launches_exchange = b;
+            return r;
+        });
+    }
     int nl = 0;
     st = compute_impl(c, x, labels, loss_out, (cudaStream_t)stream, &nl);
     if (st != TEM_OK) return st;
@@ -540,6 +621,12 @@ tem_status tem_shutdown(tem_ctx* c) {
     if (st == TEM_OK && code != 0) st = (tem_status)code;
     cudaFreeHost(c->st_host);
     for (int l = 0; l < c->nlocal; ++l) delete c->plan[l];
+    for (int i = 0; i < c->ngraphs; ++i) cudaGraphExecDestroy(c->graphs[i].exec);
+    if (c->gstream) {
+        cudaStreamDestroy(c->gstream);
+        cudaEventDestroy(c->ev_in);
+        cudaEventDestroy(c->ev_out);
+    }
     if (c->tev) {
         for (size_t i = 0; i < (size_t)c->t_max * NUM_SLOTS * 2; ++i) cudaEventDestroy(c->tev[i]);
         delete[] c->tev;
