@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
     int RPC) {
     extern __shared__ __align__(16) float sm[];
     float* sW3 = sm;           // [3][C]
-    float* sacc = sm + 3 * C;  // [8][4C]: dW3 (3C) then db2 (C) per warp
+    float* sdz = sm + 3 * C;   // [RPC][3] dz of this CTA's rows (0 on halo rows)
     __shared__ float s_ap[3][3], s_an[3][3], s_misc[HEAD_WARPS][6];
     __shared__ int s_cnt[3][3];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -57,44 +57,21 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
         s_an[k][o] = (float)Tn / (float)(ln > 1 ? ln : 1);
     }
     __syncthreads();
+    // ---- phase 1: one row per warp: z, loss terms, dz -> smem ----
     const int NQ = C / 32;  // <= 16
-    float wacc[3][16], bacc[16];
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-        bacc[q] = 0.f;
-#pragma unroll
-        for (int o = 0; o < 3; ++o) wacc[o][q] = 0.f;
-    }
     float lsum[3] = {0.f, 0.f, 0.f}, dbs[3] = {0.f, 0.f, 0.f};
     const float inv_bt = 1.0f / ((float)B * (float)Tn);
-    // software pipeline: the next row's h2 is in flight while the current row is processed
-    float hn[16];
-    {
-        const int p = p0 + warp;
-#pragma unroll
-        for (int q = 0; q < 16; ++q) hn[q] = (q < NQ && p < p1) ? __ldcs(h2 + (size_t)p * C + lane + 32 * q) : 0.f;
-    }
     for (int p = p0 + warp; p < p1; p += HEAD_WARPS) {
-        float h[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) h[q] = hn[q];
-        {
-            const int pn = p + HEAD_WARPS;
-#pragma unroll
-            for (int q = 0; q < 16; ++q)
-                hn[q] = (q < NQ && pn < p1) ? __ldcs(h2 + (size_t)pn * C + lane + 32 * q) : 0.f;
-        }
         const int v = p / Tp, tp = p - v * Tp;
-        if (tp == 0 || tp == Tp - 1) {  // halo row: zero dA2
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                if (q >= NQ) continue;
-                dA2[(size_t)p * C + lane + 32 * q] = from_f<TOp>(0.f);
-                if (dA2_lo) dA2_lo[(size_t)p * C + lane + 32 * q] = from_f<TOp>(0.f);
-            }
+        float* dzr = sdz + (p - p0) * 3;
+        if (tp == 0 || tp == Tp - 1) {
+            if (lane < 3) dzr[lane] = 0.f;
             continue;
         }
         const int t = tp - 1, k = v - v0;
+        float h[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) h[q] = (q < NQ) ? h2[(size_t)p * C + lane + 32 * q] : 0.f;
         float z[3];
 #pragma unroll
         for (int o = 0; o < 3; ++o) {
@@ -123,34 +100,10 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
             zo[0] = z[0];
             zo[1] = z[1];
             zo[2] = z[2];
+            dzr[0] = dz[0];
+            dzr[1] = dz[1];
+            dzr[2] = dz[2];
         }
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            if (q >= NQ) continue;
-            const int c = lane + 32 * q;
-            float d = sW3[c] * dz[0];
-            d = fmaf(sW3[C + c], dz[1], d);
-            d = fmaf(sW3[2 * C + c], dz[2], d);
-            const float dv = h[q] > 0.f ? d : 0.f;
-            const TOp dh = from_f<TOp>(dv);
-            float stored = to_f(dh);
-            dA2[(size_t)p * C + c] = dh;
-            if (dA2_lo) {
-                const TOp dl = from_f<TOp>(dv - stored);
-                dA2_lo[(size_t)p * C + c] = dl;
-                stored += to_f(dl);
-            }
-            bacc[q] += stored;
-#pragma unroll
-            for (int o = 0; o < 3; ++o) wacc[o][q] = fmaf(dz[o], h[q], wacc[o][q]);
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < 16; ++q) {
-        if (q >= NQ) continue;
-#pragma unroll
-        for (int o = 0; o < 3; ++o) sacc[(size_t)warp * 4 * C + o * C + lane + 32 * q] = wacc[o][q];
-        sacc[(size_t)warp * 4 * C + 3 * C + lane + 32 * q] = bacc[q];
     }
     if (lane == 0) {
 #pragma unroll
@@ -160,12 +113,39 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
         }
     }
     __syncthreads();
-    // partial row layout: [dW3 (3C)][db3 (3)][L (3)][db2 (C)]
+    // ---- phase 2: column-parallel over the CTA's rows (h2 rows are L2-resident now) ----
+    // dA2 = 1[h2>0] W3^T dz (halo rows: dz = 0 -> 0); dW3 += dz h2; db2 += stored dA2
     float* dst = part + (size_t)blockIdx.x * (4 * C + 6);
-    for (int i = tid; i < 4 * C; i += blockDim.x) {
-        float s = sacc[i];
-        for (int w = 1; w < HEAD_WARPS; ++w) s += sacc[(size_t)w * 4 * C + i];
-        dst[i < 3 * C ? i : i + 6] = s;
+    for (int c = tid; c < C; c += blockDim.x) {
+        const float w0 = sW3[c], w1 = sW3[C + c], w2 = sW3[2 * C + c];
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f, bsum = 0.f;
+#pragma unroll 4
+        for (int p = p0; p < p1; ++p) {
+            const float* dzr = sdz + (p - p0) * 3;
+            const float d0 = dzr[0], d1 = dzr[1], d2 = dzr[2];
+            const float hv = h2[(size_t)p * C + c];
+            float d = w0 * d0;
+            d = fmaf(w1, d1, d);
+            d = fmaf(w2, d2, d);
+            const float dv = hv > 0.f ? d : 0.f;
+            const TOp dh = from_f<TOp>(dv);
+            float stored = to_f(dh);
+            dA2[(size_t)p * C + c] = dh;
+            if (dA2_lo) {
+                const TOp dl = from_f<TOp>(dv - stored);
+                dA2_lo[(size_t)p * C + c] = dl;
+                stored += to_f(dl);
+            }
+            bsum += stored;
+            a0 = fmaf(d0, hv, a0);
+            a1 = fmaf(d1, hv, a1);
+            a2 = fmaf(d2, hv, a2);
+        }
+        // partial row layout: [dW3 (3C)][db3 (3)][L (3)][db2 (C)]
+        dst[c] = a0;
+        dst[C + c] = a1;
+        dst[2 * C + c] = a2;
+        dst[3 * C + 6 + c] = bsum;
     }
     if (tid < 3) {
         float l = s_misc[0][tid], d = s_misc[0][3 + tid];
@@ -245,10 +225,10 @@ int head_ctas(const Geom& g) { return g.R > 0 ? (g.R + head_rows_per_cta(g) - 1)
 cudaError_t launch_head(const Geom& g, const RankBufs& b, const float* labels, const float lam[3],
                         float* loss_out, Status* status, const EvRec& rec, cudaStream_t s, int* n) {
     const int P = head_ctas(g);
-    const size_t hsm = (size_t)(3 * g.C + HEAD_WARPS * 4 * g.C) * sizeof(float);
+    const int rpc = head_rows_per_cta(g);
+    const size_t hsm = (size_t)(3 * g.C + 3 * rpc) * sizeof(float);
     if (P > 0) {
         rec.begin(SLOT_HEAD);
-        const int rpc = head_rows_per_cta(g);
         if (g.op_bf16) {
             auto k = head_rows_kernel<__nv_bfloat16>;
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);

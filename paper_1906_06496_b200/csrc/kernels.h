@@ -52,7 +52,8 @@ struct RankBufs {
     unsigned* counter;    // last-CTA ticket of the head reduction (self-resetting)
     float* bpart;         // [m-tiles][C] conv1 bias-gradient partials (tcgen05 DGRAD epilogue)
     void* ones;           // [R][128] bf16 ones/zeros operand for the bias-gradient column
-    float* wpart;         // [S][max(C*3*Cin + C, C*3*C + C)]
+    float* wpart;         // [S][max(C*3*Cin + C, C*3*C + C)] split-K partials (conv1 wgrad; SIMT: both)
+    float* wpart2;        // [S][C*3*C + C] split-K partials of the tcgen05 conv2 wgrad
     int64_t* stepctr;     // step counter for NONFINITE reporting
     __nv_bfloat16* shadow;     // [Kpad] bf16 weights (hi plane) or nullptr
     __nv_bfloat16* shadow_lo;  // [Kpad] residual plane (UMMA fp32) or nullptr
@@ -82,7 +83,10 @@ struct UmmaParams {
 struct UmmaPlan {
     UmmaParams conv1, conv2, dgrad, wgrad1, wgrad2;
     int npass, bn_fwd, S, ksplit_rows;
+    cudaStream_t aux;         // second stream: conv2 wgrad runs beside conv2 dgrad / conv1 wgrad
+    cudaEvent_t fork, join;
 };
+void umma_plan_destroy(UmmaPlan* plan);
 int umma_wgrad_splits(const Geom& g);
 bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan);
 cudaError_t launch_fill_ones(void* ones, int64_t rows, cudaStream_t s);

@@ -30,7 +30,7 @@ struct HeapLayout {
 };
 
 struct WsLayout {
-    size_t xp, h1, h2, dA2, dA1, xp_lo, h1_lo, dA2_lo, dA1_lo, z, grad, headpart, headlvl1, counter, bpart, wpart, shadow,
+    size_t xp, h1, h2, dA2, dA1, xp_lo, h1_lo, dA2_lo, dA1_lo, z, grad, headpart, headlvl1, counter, bpart, wpart, wpart2, shadow,
         shadow_lo, ones, epochs, stepctr, xstage, labstage, lossstage, per_rank;
 };
 
@@ -139,6 +139,7 @@ WsLayout ws_layout(const tem_config* c) {
     w.counter = take(64);
     w.bpart = take((size_t)((g.R + 127) / 128) * g.C * 4);
     w.wpart = take((size_t)S * wmax * 4);
+    w.wpart2 = take(g.path == PATH_UMMA ? (size_t)umma_wgrad_splits(g) * ((size_t)g.C * 3 * g.C + g.C) * 4 : 0);
     w.shadow = take(g.op_bf16 ? (size_t)g.Kpad * 2 : 0);
     w.shadow_lo = take(lo * (size_t)g.Kpad * 2);
     w.ones = take(g.path == PATH_UMMA ? (size_t)g.R * 128 * 2 : 0);
@@ -326,6 +327,7 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
         b.bpart = (float*)(base + wl.bpart);
         b.ones = c->g.path == PATH_UMMA ? base + wl.ones : nullptr;
         b.wpart = (float*)(base + wl.wpart);
+        b.wpart2 = (float*)(base + wl.wpart2);
         b.stepctr = (int64_t*)(base + wl.stepctr);
         b.xp_lo = c->g.split ? base + wl.xp_lo : nullptr;
         b.h1_lo = c->g.split ? base + wl.h1_lo : nullptr;
@@ -344,7 +346,7 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
             if (!c->plan[l] || !umma_plan(c->g, b, c->plan[l])) e = cudaErrorInvalidValue;
         }
         if (e != cudaSuccess) {
-            for (int q = 0; q <= l; ++q) delete c->plan[q];
+            for (int q = 0; q <= l; ++q) umma_plan_destroy(c->plan[q]);
             cudaFreeHost(c->st_host);
             delete c;
             return TEM_ERR_CUDA;
@@ -620,7 +622,7 @@ tem_status tem_shutdown(tem_ctx* c) {
     const int32_t code = *(volatile int32_t*)&c->st_host->code;
     if (st == TEM_OK && code != 0) st = (tem_status)code;
     cudaFreeHost(c->st_host);
-    for (int l = 0; l < c->nlocal; ++l) delete c->plan[l];
+    for (int l = 0; l < c->nlocal; ++l) umma_plan_destroy(c->plan[l]);
     for (int i = 0; i < c->ngraphs; ++i) cudaGraphExecDestroy(c->graphs[i].exec);
     if (c->gstream) {
         cudaStreamDestroy(c->gstream);

@@ -477,6 +477,10 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     UmmaPlan& P = *plan;
     memset(&P, 0, sizeof(P));
     if (g.R == 0) return true;  // empty shard: nothing to plan (tem_compute takes the B = 0 branch)
+    if (cudaStreamCreateWithFlags(&P.aux, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&P.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&P.join, cudaEventDisableTiming) != cudaSuccess)
+        return false;
     P.npass = npl == 2 ? 3 : 1;
     const int R = g.R, Tp = g.T + 2;
     // tile widths: split (fp32) path uses narrower N tiles for more CTAs at small batch
@@ -545,7 +549,7 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     P.wgrad2.Cin_w = g.C;
     P.wgrad2.cpj = (g.C + 63) / 64;
     P.wgrad2.NW = 3 * g.C;
-    P.wgrad2.part = b.wpart;
+    P.wgrad2.part = b.wpart2;
     P.wgrad2.part_stride = (int64_t)g.C * 3 * g.C + g.C;
     common(P.wgrad1);
     P.wgrad1.Nout = g.C;
@@ -558,6 +562,14 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     ok &= map2d(&P.wgrad1.ones, b.ones, 128, R, umma::BK);
     (void)wmax;
     return ok;
+}
+
+void umma_plan_destroy(UmmaPlan* plan) {
+    if (!plan) return;
+    if (plan->aux) cudaStreamDestroy(plan->aux);
+    if (plan->fork) cudaEventDestroy(plan->fork);
+    if (plan->join) cudaEventDestroy(plan->join);
+    delete plan;
 }
 
 template <int MODE>
@@ -591,24 +603,28 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     ++n;
     e = launch_head(g, b, labels, lam, loss_out, status, rec, s, &n);
     if (e != cudaSuccess) return e;
+    // Fork: conv2 wgrad (+ its reduction) on the aux stream runs alongside conv2 dgrad ->
+    // conv1 wgrad on s; both only read dA2 / h1 / xp (captured as parallel graph branches).
+    const int wbn = 256;
+    const EvRec rec2{rec.ev, P.aux};
+    if (cudaEventRecord(P.fork, s) != cudaSuccess || cudaStreamWaitEvent(P.aux, P.fork, 0) != cudaSuccess)
+        return cudaErrorUnknown;
+    rec2.begin(SLOT_WGRAD2);
+    e = dispatch<WGRAD_>(P.wgrad2, wbn, P.npass, dim3(g.C / umma::BM, (3 * P.wgrad2.cpj + 3) / 4, P.S), P.aux);
+    rec2.end(SLOT_WGRAD2);
+    if (e != cudaSuccess) return e;
+    ++n;
+    rec2.begin(SLOT_RED2);
+    umma::reduce_wgrad_kernel<<<296, 256, 0, P.aux>>>(b.wpart2, P.wgrad2.part_stride, P.S, (int64_t)g.C * 3 * g.C,
+                                                      nullptr, 0, g.C, b.grad + g.off_W2);
+    e = cudaGetLastError();
+    rec2.end(SLOT_RED2);
+    if (e != cudaSuccess) return e;
+    ++n;
+    if (cudaEventRecord(P.join, P.aux) != cudaSuccess) return cudaErrorUnknown;
     rec.begin(SLOT_DGRAD);
     e = dispatch<DGRAD_>(P.dgrad, P.bn_fwd, P.npass, dim3(mt, g.C / P.bn_fwd, 1), s);
     rec.end(SLOT_DGRAD);
-    if (e != cudaSuccess) return e;
-    ++n;
-    // WGRAD: 4 o-tiles x 6 chunk-tiles (256 columns = 4 chunks of 64) x S splits.
-    // db2 was summed by the head (from the stored dA2), db1 by the DGRAD epilogue.
-    const int wbn = 256;
-    rec.begin(SLOT_WGRAD2);
-    e = dispatch<WGRAD_>(P.wgrad2, wbn, P.npass, dim3(g.C / umma::BM, (3 * P.wgrad2.cpj + 3) / 4, P.S), s);
-    rec.end(SLOT_WGRAD2);
-    if (e != cudaSuccess) return e;
-    ++n;
-    rec.begin(SLOT_RED2);
-    umma::reduce_wgrad_kernel<<<296, 256, 0, s>>>(b.wpart, P.wgrad2.part_stride, P.S, (int64_t)g.C * 3 * g.C,
-                                                  nullptr, 0, g.C, b.grad + g.off_W2);
-    e = cudaGetLastError();
-    rec.end(SLOT_RED2);
     if (e != cudaSuccess) return e;
     ++n;
     rec.begin(SLOT_WGRAD1);
@@ -623,6 +639,7 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     rec.end(SLOT_RED1);
     if (e != cudaSuccess) return e;
     ++n;
+    if (cudaStreamWaitEvent(s, P.join, 0) != cudaSuccess) return cudaErrorUnknown;  // join
     *nl += n;
     return cudaSuccess;
 }
