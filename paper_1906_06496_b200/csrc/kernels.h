@@ -77,6 +77,7 @@ struct UmmaParams {
     int64_t part_stride;
     int NW, Cin_w, cpj;  // WGRAD: 3*Cin, Cin, 64-wide chunks per tap
     int ksplit_rows;
+    int mtiles, ntiles, nsplit;  // tile grid (persistent kernels walk it cluster tile by cluster tile)
     int ones_chunk;      // WGRAD: chunk slot 3*cpj reads the all-ones map (bias gradient column)
     CUtensorMap ones;    // [R][128] bf16: columns 0..63 = 1, 64..127 = 0
 };

@@ -18,6 +18,14 @@
 //
 // Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer
 // (one elected lane), warps 2..5 = epilogue (TMEM -> registers -> global).
+//
+// Persistent: each cluster of CM x CN CTAs walks a static list of cluster tiles (CM m-tiles
+// x CN n-tiles [x split]); the two TMEM accumulator buffers let the epilogue of tile i run
+// while tile i+1 is in the MMA pipe.  Inside a cluster, the CN CTAs that share an m-tile
+// each load 1/CN of the A tile and TMA-multicast it to the others; the CM CTAs that share an
+// n-tile do the same for B.  A stage slot is refilled only after every CTA that reads data
+// this CTA wrote has released it (its MMA completion is multicast-committed to the empty
+// barriers of its CM + CN - 1 producers).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -40,9 +48,8 @@ struct Cfg {
     static constexpr uint32_t A_BYTES = BM * BK * 2;
     static constexpr uint32_t B_BYTES = BN * BK * 2;
     static constexpr uint32_t STAGE_BYTES = NPL * (A_BYTES + B_BYTES);
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
-                                     4 * BN * 4 /*epilogue column sums*/;
-    static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
 };
 
 TEM_DEV bool halo_row(int p, int Tp) {
@@ -77,59 +84,37 @@ TEM_DEV void store16_planes(__nv_bfloat16* hi, __nv_bfloat16* lo, const float (&
     }
 }
 
-// Column sums of a 32-row x 16-column register tile (one row per lane): a reduce-scatter
-// over the warp in a fixed order.  Returns, in lanes L and L^1, the 32-row sum of
-// column ((L>>4)&1)*8 + ((L>>3)&1)*4 + ((L>>2)&1)*2 + ((L>>1)&1).
-TEM_DEV float warp_colsum16(const float (&v)[16], int lane, int* col) {
-    const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4, b1 = lane & 2;
-    float a[8], b[4], c[2];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const float keep = b4 ? v[i + 8] : v[i], send = b4 ? v[i] : v[i + 8];
-        a[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const float keep = b3 ? a[i + 4] : a[i], send = b3 ? a[i] : a[i + 4];
-        b[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-    }
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const float keep = b2 ? b[i + 2] : b[i], send = b2 ? b[i] : b[i + 2];
-        c[i] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-    }
-    float d = (b1 ? c[1] : c[0]) + __shfl_xor_sync(0xffffffffu, b1 ? c[0] : c[1], 2);
-    d += __shfl_xor_sync(0xffffffffu, d, 1);
-    *col = (b4 ? 8 : 0) + (b3 ? 4 : 0) + (b2 ? 2 : 0) + (b1 ? 1 : 0);
-    return d;
-}
 
-template <int MODE, int BN, int NPASS, int STAGES>
+template <int MODE, int BN, int NPASS, int STAGES, int CM, int CN>
 __global__ void __launch_bounds__(NTHREADS, 1) umma_conv_kernel(const __grid_constant__ UmmaParams P) {
     using C_ = Cfg<BN, NPASS, STAGES>;
     constexpr int NPL = C_::NPL;
+    constexpr int CS = CM * CN;
+    constexpr bool A_MN = (MODE == WGRAD_);
+    constexpr bool B_MN = (MODE != FWD_);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C_::STAGE_BYTES);
     uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
-    float* csum = reinterpret_cast<float*>(smem + STAGES * C_::STAGE_BYTES + 256);  // [4][BN]
+    uint64_t* tfull = empty + STAGES;   // [2]
+    uint64_t* tempty = tfull + 2;       // [2]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.x * BM;
-    const int ntile = blockIdx.y;
-    const int split = blockIdx.z;
+    // cluster coordinates: x = m direction (CM), y = n direction (CN); rank = cx + cy*CM
+    const int cx = CS > 1 ? (int)(blockIdx.x % CM) : 0;
+    const int cy = CS > 1 ? (int)blockIdx.y : 0;
+    const int cluster_id = blockIdx.x / CM, nclusters = gridDim.x / CM;
+    uint16_t rowpeers = 0, colpeers = 0;  // CTAs sharing my m-tile (A) / my n-tile (B)
+#pragma unroll
+    for (int y = 0; y < CN; ++y) rowpeers |= (uint16_t)(1u << (cx + y * CM));
+#pragma unroll
+    for (int x = 0; x < CM; ++x) colpeers |= (uint16_t)(1u << (x + cy * CM));
+    const uint16_t peers = rowpeers | colpeers;
 
-    // k-block range
-    int nkb, p_begin = 0;
-    if (MODE == WGRAD_) {
-        p_begin = split * P.ksplit_rows;
-        const int p_end = min(P.R, p_begin + P.ksplit_rows);
-        nkb = (p_end - p_begin + BK - 1) / BK;
-    } else {
-        nkb = 3 * P.cpb;
-    }
+    const int mtiles_c = (P.mtiles + CM - 1) / CM;  // cluster tiles along m
+    const int ntiles_c = P.ntiles / CN;
+    const int total_ct = mtiles_c * ntiles_c * P.nsplit;
 
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < 2; ++i) {
@@ -138,57 +123,102 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_conv_kernel(const __grid_con
         }
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], CS > 1 ? CM + CN - 1 : 1);
         }
-        mbar_init(tfull, 1);
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<C_::TMEM_COLS>(tslot);
     tc_fence_before();
     __syncthreads();
+    if (CS > 1) cluster_sync();  // barrier inits visible cluster-wide before any multicast
     tc_fence_after();
     const uint32_t tbase = *tslot;
+
+    auto tile_coords = [&](int ct, int& m_tile, int& n_tile, int& split) {
+        const int ng = ct % ntiles_c;
+        const int rest = ct / ntiles_c;
+        const int mg = rest % mtiles_c;
+        split = rest / mtiles_c;
+        m_tile = mg * CM + cx;
+        n_tile = ng * CN + cy;
+    };
+    auto kblocks = [&](int split, int& p_begin) -> int {
+        if (MODE == WGRAD_) {
+            p_begin = split * P.ksplit_rows;
+            const int p_end = min(P.R, p_begin + P.ksplit_rows);
+            return (p_end - p_begin + BK - 1) / BK;
+        }
+        p_begin = 0;
+        return 3 * P.cpb;
+    };
 
     if (warp == 0) {
         if (lane == 0) {
             // ===================== TMA producer =====================
-            for (int kb = 0; kb < nkb; ++kb) {
-                const int s = kb % STAGES;
-                const uint32_t ph = (kb / STAGES) & 1;
-                mbar_wait(&empty[s], ph ^ 1);
-                uint8_t* st = smem + s * C_::STAGE_BYTES;
-                mbar_arrive_expect_tx(&full[s], C_::STAGE_BYTES);
+            constexpr int AR = A_MN ? BK / CN : BM / CN;  // rows per A slice
+            constexpr int BR = B_MN ? BK / CM : BN / CM;  // rows per B slice
+            int it = 0;
+            for (int ct = cluster_id; ct < total_ct; ct += nclusters) {
+                int m_tile, n_tile, split, p_begin;
+                tile_coords(ct, m_tile, n_tile, split);
+                const int nkb = kblocks(split, p_begin);
+                const int m0 = m_tile * BM;
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    mbar_wait(&empty[s], ph ^ 1);
+                    uint8_t* st = smem + s * C_::STAGE_BYTES;
+                    mbar_arrive_expect_tx(&full[s], C_::STAGE_BYTES);
 #pragma unroll
-                for (int pl = 0; pl < NPL; ++pl) {
-                    uint8_t* sa = st + pl * C_::A_BYTES;
-                    uint8_t* sb = st + NPL * C_::A_BYTES + pl * C_::B_BYTES;
-                    if (MODE == FWD_) {
-                        const int j = kb / P.cpb, c0 = (kb % P.cpb) * BK;
-                        tma_load_2d(sa, &P.a[pl], &full[s], c0, m0 + j - 1);
-                        tma_load_2d(sb, &P.b[pl], &full[s], j * P.Kc + c0, ntile * BN);
-                    } else if (MODE == DGRAD_) {
-                        const int j = kb / P.cpb, o0 = (kb % P.cpb) * BK;
-                        tma_load_2d(sa, &P.a[pl], &full[s], o0, m0 + 1 - j);
+                    for (int pl = 0; pl < NPL; ++pl) {
+                        uint8_t* sa = st + pl * C_::A_BYTES;
+                        uint8_t* sb = st + NPL * C_::A_BYTES + pl * C_::B_BYTES;
+                        auto ldA = [&](uint8_t* dst, int c0, int c1) {
+                            if (CS > 1) tma_load_2d_mc(dst, &P.a[pl], &full[s], c0, c1, rowpeers);
+                            else tma_load_2d(dst, &P.a[pl], &full[s], c0, c1);
+                        };
+                        auto ldB = [&](uint8_t* dst, const CUtensorMap* map, int c0, int c1) {
+                            if (CS > 1) tma_load_2d_mc(dst, map, &full[s], c0, c1, colpeers);
+                            else tma_load_2d(dst, map, &full[s], c0, c1);
+                        };
+                        if (MODE == FWD_) {
+                            const int j = kb / P.cpb, c0 = (kb % P.cpb) * BK;
+                            ldA(sa + cy * AR * 128, c0, m0 + j - 1 + cy * AR);
+                            ldB(sb + cx * BR * 128, &P.b[pl], j * P.Kc + c0, n_tile * BN + cx * BR);
+                        } else if (MODE == DGRAD_) {
+                            const int j = kb / P.cpb, o0 = (kb % P.cpb) * BK;
+                            ldA(sa + cy * AR * 128, o0, m0 + 1 - j + cy * AR);
 #pragma unroll
-                        for (int q = 0; q < BN / 64; ++q)
-                            tma_load_3d(sb + q * (BK * 128), &P.b[pl], &full[s], ntile * BN + 64 * q, j, o0);
-                    } else {  // WGRAD
-                        const int p0 = p_begin + kb * BK;
-#pragma unroll
-                        for (int q = 0; q < BM / 64; ++q)
-                            tma_load_2d(sa + q * (BK * 128), &P.a[pl], &full[s], m0 + 64 * q, p0);
-#pragma unroll
-                        for (int q = 0; q < BN / 64; ++q) {
-                            int g = ntile * (BN / 64) + q;
-                            if (P.ones_chunk && g == 3 * P.cpj) {
-                                // all-ones B chunk (lo plane: zeros): column 0 of D = sum_p dA[p][o],
-                                // the bias gradient, on the tensor core in the same split precision
-                                tma_load_2d(sb + q * (BK * 128), &P.ones, &full[s], 64 * pl, p0);
-                                continue;
+                            for (int q = 0; q < BN / 64; ++q) {
+                                uint8_t* dst = sb + q * (BK * 128) + cx * BR * 128;
+                                if (CS > 1)
+                                    tma_load_3d_mc(dst, &P.b[pl], &full[s], n_tile * BN + 64 * q, j, o0 + cx * BR,
+                                                   colpeers);
+                                else
+                                    tma_load_3d(dst, &P.b[pl], &full[s], n_tile * BN + 64 * q, j, o0 + cx * BR);
                             }
-                            if (g >= 3 * P.cpj) g = 3 * P.cpj - 1;  // dummy chunk, discarded by the epilogue
-                            const int j = g / P.cpj, c0 = (g % P.cpj) * 64;
-                            tma_load_2d(sb + q * (BK * 128), &P.b[pl], &full[s], c0, p0 + j - 1);
+                        } else {  // WGRAD
+                            const int p0 = p_begin + kb * BK;
+#pragma unroll
+                            for (int q = 0; q < BM / 64; ++q)
+                                ldA(sa + q * (BK * 128) + cy * AR * 128, m0 + 64 * q, p0 + cy * AR);
+#pragma unroll
+                            for (int q = 0; q < BN / 64; ++q) {
+                                uint8_t* dst = sb + q * (BK * 128) + cx * BR * 128;
+                                int g = n_tile * (BN / 64) + q;
+                                if (P.ones_chunk && g == 3 * P.cpj) {
+                                    // all-ones chunk (lo plane: zeros): D column = sum_p dA[p][o]
+                                    ldB(dst, &P.ones, 64 * pl, p0 + cx * BR);
+                                    continue;
+                                }
+                                if (g >= 3 * P.cpj) g = 3 * P.cpj - 1;  // dummy chunk, discarded
+                                const int j = g / P.cpj, c0 = (g % P.cpj) * 64;
+                                ldB(dst, &P.b[pl], c0, p0 + j - 1 + cx * BR);
+                            }
                         }
                     }
                 }
@@ -197,136 +227,130 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_conv_kernel(const __grid_con
     } else if (warp == 1) {
         if (lane == 0) {
             // ===================== MMA issuer =====================
-            constexpr bool A_MN = (MODE == WGRAD_);
-            constexpr bool B_MN = (MODE != FWD_);
             constexpr uint32_t idesc = make_idesc_bf16(BM, BN, A_MN, B_MN);
-            for (int kb = 0; kb < nkb; ++kb) {
-                const int s = kb % STAGES;
-                const uint32_t ph = (kb / STAGES) & 1;
-                mbar_wait(&full[s], ph);
+            int it = 0, t = 0;
+            for (int ct = cluster_id; ct < total_ct; ct += nclusters, ++t) {
+                int m_tile, n_tile, split, p_begin;
+                tile_coords(ct, m_tile, n_tile, split);
+                const int nkb = kblocks(split, p_begin);
+                const int acc = t & 1;
+                mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);  // epilogue drained this buffer
                 tc_fence_after();
-                const uint32_t st = smem_u32(smem + s * C_::STAGE_BYTES);
+                const uint32_t dt = tbase + (uint32_t)(acc * BN);
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t st = smem_u32(smem + s * C_::STAGE_BYTES);
 #pragma unroll
-                for (int k = 0; k < BK / UK; ++k) {
+                    for (int k = 0; k < BK / UK; ++k) {
 #pragma unroll
-                    for (int pass = 0; pass < NPASS; ++pass) {
-                        const int pa = (pass == 2) ? 1 : 0;  // hi*hi, hi*lo, lo*hi
-                        const int pb = (pass == 1) ? 1 : 0;
-                        const uint32_t a_addr = st + pa * C_::A_BYTES;
-                        const uint32_t b_addr = st + NPL * C_::A_BYTES + pb * C_::B_BYTES;
-                        uint64_t ad, bd;
-                        if (A_MN) ad = make_desc(a_addr + k * (UK * 128), BK * 128, 1024);
-                        else ad = make_desc(a_addr + k * (UK * 2), 16, 1024);
-                        if (B_MN) bd = make_desc(b_addr + k * (UK * 128), BK * 128, 1024);
-                        else bd = make_desc(b_addr + k * (UK * 2), 16, 1024);
-                        mma_bf16(tbase, ad, bd, idesc, (kb | k | pass) != 0 ? 1u : 0u);
+                        for (int pass = 0; pass < NPASS; ++pass) {
+                            const int pa = (pass == 2) ? 1 : 0;  // hi*hi, hi*lo, lo*hi
+                            const int pb = (pass == 1) ? 1 : 0;
+                            const uint32_t a_addr = st + pa * C_::A_BYTES;
+                            const uint32_t b_addr = st + NPL * C_::A_BYTES + pb * C_::B_BYTES;
+                            const uint64_t ad = A_MN ? make_desc(a_addr + k * (UK * 128), BK * 128, 1024)
+                                                     : make_desc(a_addr + k * (UK * 2), 16, 1024);
+                            const uint64_t bd = B_MN ? make_desc(b_addr + k * (UK * 128), BK * 128, 1024)
+                                                     : make_desc(b_addr + k * (UK * 2), 16, 1024);
+                            mma_bf16(dt, ad, bd, idesc, (kb | k | pass) != 0 ? 1u : 0u);
+                        }
                     }
+                    if (CS > 1) mma_commit_mc(&empty[s], peers);  // release the slot cluster-wide
+                    else mma_commit(&empty[s]);
                 }
-                mma_commit(&empty[s]);  // frees the smem stage once these MMAs are done
+                mma_commit(&tfull[acc]);  // accumulator complete
             }
-            mma_commit(tfull);  // accumulator complete
         }
         __syncwarp();
     } else {
         // ===================== epilogue (warps 2..5) =====================
         const int q = warp & 3;  // TMEM lane quarter accessible to this warp
-        const int row = m0 + 32 * q + lane;
-        mbar_wait(tfull, 0);
-        tc_fence_after();
+        int t = 0;
+        for (int ct = cluster_id; ct < total_ct; ct += nclusters, ++t) {
+            int m_tile, n_tile, split, p_begin;
+            tile_coords(ct, m_tile, n_tile, split);
+            const int acc = t & 1;
+            const int row = m_tile * BM + 32 * q + lane;
+            mbar_wait(&tfull[acc], (t >> 1) & 1);
+            tc_fence_after();
+            const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN);
 #pragma unroll 1
-        for (int c16 = 0; c16 < BN / 16; ++c16) {
-            uint32_t r[16];
-            tmem_ld16(tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(c16 * 16), r);
-            tmem_ld_wait();
-            float v[16];
+            for (int c16 = 0; c16 < BN / 16; ++c16) {
+                uint32_t r[16];
+                tmem_ld16(tq + (uint32_t)(c16 * 16), r);
+                tmem_ld_wait();
+                float v[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-            if (MODE == FWD_ || MODE == DGRAD_) {
-                const int n = ntile * BN + c16 * 16;  // Nout is a multiple of BN
-                const bool valid = row < P.R;
-                const bool halo = !valid || halo_row(row, P.Tp);
-                if (MODE == FWD_) {
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        const float t = v[i] + P.bias[n + i];
-                        v[i] = (!halo && t > 0.f) ? t : 0.f;
-                    }
-                } else {
-                    uint32_t mw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                    if (!halo) {
-                        const uint4* mk = reinterpret_cast<const uint4*>(
-                            static_cast<const __nv_bfloat16*>(P.mask) + (size_t)row * P.Nout + n);
-                        const uint4 m0v = mk[0], m1v = mk[1];
-                        mw[0] = m0v.x; mw[1] = m0v.y; mw[2] = m0v.z; mw[3] = m0v.w;
-                        mw[4] = m1v.x; mw[5] = m1v.y; mw[6] = m1v.z; mw[7] = m1v.w;
-                    }
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        const bool p0 = __uint_as_float(mw[i] << 16) > 0.f;
-                        const bool p1 = __uint_as_float(mw[i] & 0xFFFF0000u) > 0.f;
-                        v[2 * i] = p0 ? v[2 * i] : 0.f;
-                        v[2 * i + 1] = p1 ? v[2 * i + 1] : 0.f;
-                    }
-                    if (P.bsum) {
-                        // bias gradient of conv1 (row a8): column sums of the STORED operand
-                        // (bf16(v) [+ bf16(v - bf16(v))]), reduced over this CTA's 128 rows
-                        float sv[16];
+                for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+                if (MODE == FWD_ || MODE == DGRAD_) {
+                    if (m_tile >= P.mtiles || row >= P.R) continue;
+                    const int n = n_tile * BN + c16 * 16;  // Nout is a multiple of BN
+                    const bool halo = halo_row(row, P.Tp);
+                    if (MODE == FWD_) {
 #pragma unroll
                         for (int i = 0; i < 16; ++i) {
-                            const float h = __bfloat162float(__float2bfloat16_rn(v[i]));
-                            sv[i] = P.out_lo ? h + __bfloat162float(__float2bfloat16_rn(v[i] - h)) : h;
+                            const float tv = v[i] + P.bias[n + i];
+                            v[i] = (!halo && tv > 0.f) ? tv : 0.f;
                         }
-                        int col;
-                        const float cs = warp_colsum16(sv, lane, &col);
-                        if ((lane & 1) == 0) csum[q * BN + c16 * 16 + col] = cs;
+                    } else {
+                        uint32_t mw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                        if (!halo) {
+                            const uint4* mk = reinterpret_cast<const uint4*>(
+                                static_cast<const __nv_bfloat16*>(P.mask) + (size_t)row * P.Nout + n);
+                            const uint4 m0v = mk[0], m1v = mk[1];
+                            mw[0] = m0v.x; mw[1] = m0v.y; mw[2] = m0v.z; mw[3] = m0v.w;
+                            mw[4] = m1v.x; mw[5] = m1v.y; mw[6] = m1v.z; mw[7] = m1v.w;
+                        }
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            v[2 * i] = __uint_as_float(mw[i] << 16) > 0.f ? v[2 * i] : 0.f;
+                            v[2 * i + 1] = __uint_as_float(mw[i] & 0xFFFF0000u) > 0.f ? v[2 * i + 1] : 0.f;
+                        }
+                    }
+                    if (P.out_f32) {
+                        float4* d = reinterpret_cast<float4*>(static_cast<float*>(P.out_hi) + (size_t)row * P.Nout + n);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                    } else {
+                        __nv_bfloat16* hi = static_cast<__nv_bfloat16*>(P.out_hi) + (size_t)row * P.Nout + n;
+                        __nv_bfloat16* lo = P.out_lo ? static_cast<__nv_bfloat16*>(P.out_lo) + (size_t)row * P.Nout + n
+                                                     : nullptr;
+                        store16_planes(hi, lo, v);
+                    }
+                } else {  // WGRAD partial: row = o, columns -> (j, c)
+                    const int nl = c16 * 16;
+                    const int g = n_tile * (BN / 64) + nl / 64;
+                    float* part = P.part + (size_t)split * P.part_stride;
+                    if (P.ones_chunk && g == 3 * P.cpj) {
+                        if (nl % 64 == 0) part[(size_t)P.Nout * P.NW + row] = v[0];  // bias gradient partial
+                        continue;
+                    }
+                    if (g >= 3 * P.cpj) continue;
+                    const int j = g / P.cpj, c = (g % P.cpj) * 64 + (nl % 64);
+                    if (c >= P.Cin_w) continue;
+                    float* dst = part + (size_t)row * P.NW + (size_t)j * P.Cin_w + c;
+                    if (c + 16 <= P.Cin_w) {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            if (c + i < P.Cin_w) dst[i] = v[i];
                     }
                 }
-                if (!valid) continue;
-                if (P.out_f32) {
-                    float4* d = reinterpret_cast<float4*>(static_cast<float*>(P.out_hi) + (size_t)row * P.Nout + n);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-                } else {
-                    __nv_bfloat16* hi = static_cast<__nv_bfloat16*>(P.out_hi) + (size_t)row * P.Nout + n;
-                    __nv_bfloat16* lo = P.out_lo ? static_cast<__nv_bfloat16*>(P.out_lo) + (size_t)row * P.Nout + n
-                                                 : nullptr;
-                    store16_planes(hi, lo, v);
-                }
-            } else {  // WGRAD partial: row = o, columns -> (j, c)
-                const int nl = c16 * 16;
-                const int g = ntile * (BN / 64) + nl / 64;
-                if (P.ones_chunk && g == 3 * P.cpj) {
-                    if (nl % 64 == 0)  // column 0 of the ones chunk: bias gradient partial
-                        P.part[(size_t)split * P.part_stride + (size_t)P.Nout * P.NW + row] = v[0];
-                    continue;
-                }
-                if (g >= 3 * P.cpj) continue;
-                const int j = g / P.cpj, c = (g % P.cpj) * 64 + (nl % 64);
-                if (c >= P.Cin_w) continue;
-                float* dst = P.part + (size_t)split * P.part_stride + (size_t)row * P.NW + (size_t)j * P.Cin_w + c;
-                if (c + 16 <= P.Cin_w) {
-#pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 16; ++i)
-                        if (c + i < P.Cin_w) dst[i] = v[i];
-                }
             }
-        }
-        if (MODE == DGRAD_ && P.bsum) {
-            // combine the 4 row-quarters in a fixed order -> bsum[m-tile][n]
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            const int et = threadIdx.x - 64;  // 0..127
-            for (int cidx = et; cidx < BN; cidx += 128) {
-                const float s = ((csum[cidx] + csum[BN + cidx]) + csum[2 * BN + cidx]) + csum[3 * BN + cidx];
-                P.bsum[(size_t)blockIdx.x * P.Nout + ntile * BN + cidx] = s;
-            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_local(&tempty[acc]);  // buffer free for tile t + 2
         }
     }
     tc_fence_before();
     __syncthreads();
+    if (CS > 1) cluster_sync();  // no CTA leaves while peers may still signal its barriers
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<C_::TMEM_COLS>(tbase);
@@ -434,37 +458,75 @@ bool map2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uin
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-// W2 [o][j][c] as 3D (c, j, o), box {64, 1, BK}: an MN-major (c-contiguous) tile of BK o-rows.
-bool map_w_mn(CUtensorMap* m, const void* base, uint64_t C) {
+// W2 [o][j][c] as 3D (c, j, o), box {64, 1, box_rows}: an MN-major (c-contiguous) tile of o-rows.
+bool map_w_mn(CUtensorMap* m, const void* base, uint64_t C, uint32_t box_rows) {
     auto fn = encode_fn();
     if (!fn || !base) return false;
     cuuint64_t dims[3] = {C, 3, C};
     cuuint64_t strides[2] = {C * 2, 3 * C * 2};
-    cuuint32_t box[3] = {64, 1, (cuuint32_t)umma::BK};
+    cuuint32_t box[3] = {64, 1, box_rows};
     cuuint32_t es[3] = {1, 1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int MODE, int BN, int NPASS, int STAGES>
-cudaError_t launch_one(const UmmaParams& p, dim3 grid, cudaStream_t s) {
+// Launch a persistent cluster grid: as many clusters as fit (<= cluster tiles).
+template <int MODE, int BN, int NPASS, int STAGES, int CM, int CN>
+cudaError_t launch_one(const UmmaParams& p, cudaStream_t s) {
     using C_ = umma::Cfg<BN, NPASS, STAGES>;
-    auto k = umma::umma_conv_kernel<MODE, BN, NPASS, STAGES>;
-    static bool attr = false;
-    if (!attr) {
+    auto k = umma::umma_conv_kernel<MODE, BN, NPASS, STAGES, CM, CN>;
+    static int max_clusters = -1;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CM;
+    attr[0].val.clusterDim.y = CN;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(umma::NTHREADS);
+    cfg.dynamicSmemBytes = C_::SMEM;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (max_clusters < 0) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM);
         if (e != cudaSuccess) return e;
-        attr = true;
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        cfg.gridDim = dim3(CM * (sms / (CM * CN)), CN, 1);
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            n = sms / (CM * CN);
+        }
+        max_clusters = n;
     }
-    k<<<grid, umma::NTHREADS, C_::SMEM, s>>>(p);
-    return cudaGetLastError();
+    const int total = ((p.mtiles + CM - 1) / CM) * (p.ntiles / CN) * p.nsplit;
+    const int ncl = total < max_clusters ? total : max_clusters;
+    if (ncl <= 0) return cudaSuccess;
+    cfg.gridDim = dim3(CM * ncl, CN, 1);
+    return cudaLaunchKernelEx(&cfg, k, p);
 }
 
 }  // namespace
 
+// Tile / cluster configurations (BN, STAGES, CM, CN) per GEMM and precision.
+//   1-pass bf16: FWD/DGRAD 128x256 tiles, B multicast over 2 m-tiles; WGRAD 128x256,
+//                B multicast over the 4 o-tiles.
+//   3-pass fp32: FWD/DGRAD 128x64 tiles, cluster 2 (m) x 4 (n): A multicast over 4 n-tiles,
+//                B over 2 m-tiles; WGRAD 128x128, B multicast over the 4 o-tiles.
+struct GemmCfg {
+    int bn, stages, cm, cn;
+};
+static GemmCfg cfg_for(int mode, int npass) {
+    if (npass == 1) return mode == WGRAD_ ? GemmCfg{256, 4, 4, 1} : GemmCfg{256, 4, 2, 1};
+    return mode == WGRAD_ ? GemmCfg{128, 3, 4, 1} : GemmCfg{64, 4, 2, 4};
+}
+
 int umma_wgrad_splits(const Geom& g) {
-    const int tiles = (g.C / umma::BM) * 6;
+    const GemmCfg c = cfg_for(WGRAD_, g.prec == TEM_FP32 ? 3 : 1);
+    const int chunks = 3 * (((g.Cin > g.C ? g.Cin : g.C) + 63) / 64) + 1;
+    const int tiles = (g.C / umma::BM) * ((chunks + c.bn / 64 - 1) / (c.bn / 64));
     int S = (148 + tiles - 1) / tiles;
     const int nkb = (g.R + umma::BK - 1) / umma::BK;
     if (S > nkb) S = nkb;
@@ -483,48 +545,50 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
         return false;
     P.npass = npl == 2 ? 3 : 1;
     const int R = g.R, Tp = g.T + 2;
-    // tile widths: split (fp32) path uses narrower N tiles for more CTAs at small batch
-    P.bn_fwd = (npl == 2 || (R + 127) / 128 * (g.C / 256) < 148) ? 128 : 256;
-    if (npl == 2 && (R + 127) / 128 * (g.C / 128) < 148) P.bn_fwd = 64;
+    const int mtiles = (R + umma::BM - 1) / umma::BM;
+    const GemmCfg cf = cfg_for(FWD_, P.npass), cw = cfg_for(WGRAD_, P.npass);
+    P.bn_fwd = cf.bn;
     const void* xp[2] = {b.xp, b.xp_lo};
     const void* h1[2] = {b.h1, b.h1_lo};
     const void* dA2[2] = {b.dA2, b.dA2_lo};
     const void* dA1[2] = {b.dA1, b.dA1_lo};
     const __nv_bfloat16* W[2] = {b.shadow, b.shadow_lo};
+    // slice rows of the multicast boxes
+    const uint32_t arK = umma::BM / cf.cn, brK = cf.bn / cf.cm;        // FWD/DGRAD K-major A / B
+    const uint32_t brD = umma::BK / cf.cm;                              // DGRAD MN-major B
+    const uint32_t arW = umma::BK / cw.cn, brW = umma::BK / cw.cm;       // WGRAD MN-major A / B
     bool ok = true;
     for (int pl = 0; pl < npl; ++pl) {
         const __nv_bfloat16* W1 = W[pl] + g.off_W1;
         const __nv_bfloat16* W2 = W[pl] + g.off_W2;
-        // conv1 FWD: A = xp [R][Cin], B = W1 [C][3*Cin]
-        ok &= map2d(&P.conv1.a[pl], xp[pl], g.Cin, R, umma::BM);
-        ok &= map2d(&P.conv1.b[pl], W1, 3 * (uint64_t)g.Cin, g.C, P.bn_fwd);
-        // conv2 FWD: A = h1 [R][C], B = W2 [C][3*C]
-        ok &= map2d(&P.conv2.a[pl], h1[pl], g.C, R, umma::BM);
-        ok &= map2d(&P.conv2.b[pl], W2, 3 * (uint64_t)g.C, g.C, P.bn_fwd);
-        // DGRAD: A = dA2 [R][C] (K-major), B = W2 MN-major (3D)
-        ok &= map2d(&P.dgrad.a[pl], dA2[pl], g.C, R, umma::BM);
-        ok &= map_w_mn(&P.dgrad.b[pl], W2, g.C);
-        // WGRAD2: A = dA2 MN-major box {64, BK}, B = h1 MN-major box {64, BK}
-        ok &= map2d(&P.wgrad2.a[pl], dA2[pl], g.C, R, umma::BK);
-        ok &= map2d(&P.wgrad2.b[pl], h1[pl], g.C, R, umma::BK);
-        // WGRAD1: A = dA1, B = xp
-        ok &= map2d(&P.wgrad1.a[pl], dA1[pl], g.C, R, umma::BK);
-        ok &= map2d(&P.wgrad1.b[pl], xp[pl], g.Cin, R, umma::BK);
+        ok &= map2d(&P.conv1.a[pl], xp[pl], g.Cin, R, arK);
+        ok &= map2d(&P.conv1.b[pl], W1, 3 * (uint64_t)g.Cin, g.C, brK);
+        ok &= map2d(&P.conv2.a[pl], h1[pl], g.C, R, arK);
+        ok &= map2d(&P.conv2.b[pl], W2, 3 * (uint64_t)g.C, g.C, brK);
+        ok &= map2d(&P.dgrad.a[pl], dA2[pl], g.C, R, arK);
+        ok &= map_w_mn(&P.dgrad.b[pl], W2, g.C, brD);
+        ok &= map2d(&P.wgrad2.a[pl], dA2[pl], g.C, R, arW);
+        ok &= map2d(&P.wgrad2.b[pl], h1[pl], g.C, R, brW);
+        ok &= map2d(&P.wgrad1.a[pl], dA1[pl], g.C, R, arW);
+        ok &= map2d(&P.wgrad1.b[pl], xp[pl], g.Cin, R, brW);
     }
-    const int S = umma_wgrad_splits(g);
+    P.S = umma_wgrad_splits(g);
     const int nkb = (R + umma::BK - 1) / umma::BK;
-    const int kb_per = (nkb + S - 1) / S;
+    const int kb_per = (nkb + P.S - 1) / P.S;
     P.ksplit_rows = kb_per * umma::BK;
     P.S = (R + P.ksplit_rows - 1) / P.ksplit_rows;
     auto common = [&](UmmaParams& q) {
         q.R = R;
         q.Tp = Tp;
         q.ksplit_rows = P.ksplit_rows;
+        q.nsplit = 1;
     };
     common(P.conv1);
     P.conv1.Kc = g.Cin;
     P.conv1.cpb = (g.Cin + umma::BK - 1) / umma::BK;
     P.conv1.Nout = g.C;
+    P.conv1.mtiles = mtiles;
+    P.conv1.ntiles = g.C / cf.bn;
     P.conv1.bias = b.params + g.off_b1;
     P.conv1.out_hi = b.h1;
     P.conv1.out_lo = b.h1_lo;
@@ -532,6 +596,8 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     P.conv2.Kc = g.C;
     P.conv2.cpb = g.C / umma::BK;
     P.conv2.Nout = g.C;
+    P.conv2.mtiles = mtiles;
+    P.conv2.ntiles = g.C / cf.bn;
     P.conv2.bias = b.params + g.off_b2;
     P.conv2.out_hi = b.h2;
     P.conv2.out_f32 = 1;
@@ -539,28 +605,37 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     P.dgrad.Kc = g.C;
     P.dgrad.cpb = g.C / umma::BK;
     P.dgrad.Nout = g.C;
+    P.dgrad.mtiles = mtiles;
+    P.dgrad.ntiles = g.C / cf.bn;
     P.dgrad.mask = b.h1;
     P.dgrad.out_hi = b.dA1;
     P.dgrad.out_lo = b.dA1_lo;
-    P.dgrad.bsum = nullptr;  // db1 comes from the ones column of the conv1 wgrad GEMM
-    const int64_t wmax = (int64_t)g.C * 3 * (g.Cin > g.C ? g.Cin : g.C) + g.C;
+    const int wc = cw.bn / 64;  // chunks per WGRAD n-tile
     common(P.wgrad2);
     P.wgrad2.Nout = g.C;
     P.wgrad2.Cin_w = g.C;
     P.wgrad2.cpj = (g.C + 63) / 64;
     P.wgrad2.NW = 3 * g.C;
+    P.wgrad2.mtiles = g.C / umma::BM;
+    P.wgrad2.ntiles = (3 * P.wgrad2.cpj + wc - 1) / wc;
+    P.wgrad2.nsplit = P.S;
     P.wgrad2.part = b.wpart2;
     P.wgrad2.part_stride = (int64_t)g.C * 3 * g.C + g.C;
     common(P.wgrad1);
+    P.wgrad1.nsplit = P.S;
     P.wgrad1.Nout = g.C;
     P.wgrad1.Cin_w = g.Cin;
     P.wgrad1.cpj = (g.Cin + 63) / 64;
     P.wgrad1.NW = 3 * g.Cin;
+    P.wgrad1.mtiles = g.C / umma::BM;
+    P.wgrad1.ntiles = (3 * P.wgrad1.cpj + 1 + wc - 1) / wc;  // + the all-ones chunk
     P.wgrad1.part = b.wpart;
     P.wgrad1.part_stride = (int64_t)g.C * 3 * g.Cin + g.C;
     P.wgrad1.ones_chunk = 1;
-    ok &= map2d(&P.wgrad1.ones, b.ones, 128, R, umma::BK);
-    (void)wmax;
+    ok &= map2d(&P.wgrad1.ones, b.ones, 128, R, brW);
+    // cluster shapes must tile the tile grids
+    ok &= (P.conv1.ntiles % cf.cn == 0) && (P.wgrad1.mtiles % cw.cm == 0);
+    ok &= (P.wgrad1.ntiles % cw.cn == 0) && (P.wgrad2.ntiles % cw.cn == 0);
     return ok;
 }
 
@@ -573,31 +648,28 @@ void umma_plan_destroy(UmmaPlan* plan) {
 }
 
 template <int MODE>
-static cudaError_t dispatch(const UmmaParams& p, int bn, int npass, dim3 grid, cudaStream_t s) {
-    if (npass == 3) {
-        if (bn == 64) return launch_one<MODE, 64, 3, 4>(p, grid, s);
-        if (bn == 128) return launch_one<MODE, 128, 3, 3>(p, grid, s);
-        return launch_one<MODE, 256, 3, 2>(p, grid, s);
+static cudaError_t dispatch(const UmmaParams& p, int npass, cudaStream_t s) {
+    if constexpr (MODE == WGRAD_) {
+        if (npass == 3) return launch_one<MODE, 128, 3, 3, 4, 1>(p, s);
+        return launch_one<MODE, 256, 1, 4, 4, 1>(p, s);
+    } else {
+        if (npass == 3) return launch_one<MODE, 64, 3, 4, 2, 4>(p, s);
+        return launch_one<MODE, 256, 1, 4, 2, 1>(p, s);
     }
-    if (bn == 64) return launch_one<MODE, 64, 1, 6>(p, grid, s);
-    if (bn == 128) return launch_one<MODE, 128, 1, 6>(p, grid, s);
-    return launch_one<MODE, 256, 1, 4>(p, grid, s);
 }
 
 cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, const float* labels,
                          const float lam[3], float* loss_out, Status* status, int* nl, const EvRec& rec,
                          cudaStream_t s) {
-    const int R = g.R;
-    const int mt = (R + umma::BM - 1) / umma::BM;
     int n = 0;
     cudaError_t e;
     rec.begin(SLOT_CONV1);
-    e = dispatch<FWD_>(P.conv1, P.bn_fwd, P.npass, dim3(mt, g.C / P.bn_fwd, 1), s);
+    e = dispatch<FWD_>(P.conv1, P.npass, s);
     rec.end(SLOT_CONV1);
     if (e != cudaSuccess) return e;
     ++n;
     rec.begin(SLOT_CONV2);
-    e = dispatch<FWD_>(P.conv2, P.bn_fwd, P.npass, dim3(mt, g.C / P.bn_fwd, 1), s);
+    e = dispatch<FWD_>(P.conv2, P.npass, s);
     rec.end(SLOT_CONV2);
     if (e != cudaSuccess) return e;
     ++n;
@@ -605,12 +677,11 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     if (e != cudaSuccess) return e;
     // Fork: conv2 wgrad (+ its reduction) on the aux stream runs alongside conv2 dgrad ->
     // conv1 wgrad on s; both only read dA2 / h1 / xp (captured as parallel graph branches).
-    const int wbn = 256;
     const EvRec rec2{rec.ev, P.aux};
     if (cudaEventRecord(P.fork, s) != cudaSuccess || cudaStreamWaitEvent(P.aux, P.fork, 0) != cudaSuccess)
         return cudaErrorUnknown;
     rec2.begin(SLOT_WGRAD2);
-    e = dispatch<WGRAD_>(P.wgrad2, wbn, P.npass, dim3(g.C / umma::BM, (3 * P.wgrad2.cpj + 3) / 4, P.S), P.aux);
+    e = dispatch<WGRAD_>(P.wgrad2, P.npass, P.aux);
     rec2.end(SLOT_WGRAD2);
     if (e != cudaSuccess) return e;
     ++n;
@@ -623,12 +694,12 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     ++n;
     if (cudaEventRecord(P.join, P.aux) != cudaSuccess) return cudaErrorUnknown;
     rec.begin(SLOT_DGRAD);
-    e = dispatch<DGRAD_>(P.dgrad, P.bn_fwd, P.npass, dim3(mt, g.C / P.bn_fwd, 1), s);
+    e = dispatch<DGRAD_>(P.dgrad, P.npass, s);
     rec.end(SLOT_DGRAD);
     if (e != cudaSuccess) return e;
     ++n;
     rec.begin(SLOT_WGRAD1);
-    e = dispatch<WGRAD_>(P.wgrad1, wbn, P.npass, dim3(g.C / umma::BM, (3 * P.wgrad1.cpj + 3) / 4, P.S), s);
+    e = dispatch<WGRAD_>(P.wgrad1, P.npass, s);
     rec.end(SLOT_WGRAD1);
     if (e != cudaSuccess) return e;
     ++n;
