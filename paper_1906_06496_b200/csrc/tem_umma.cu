@@ -30,6 +30,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "kernels.h"
 #include "umma.cuh"
@@ -357,6 +359,271 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_conv_kernel(const __grid_con
     }
 }
 
+// ------------------------------------------------------------------ 2-CTA (pair) kernel
+// A cluster of 2 CTAs computes a 256 x BN tile with tcgen05.mma.cta_group::2 issued by the
+// leader (rank 0): each CTA stages its own 128 rows of A and half of the BN columns of B,
+// so per-SM operand ingress per k-block is (128 + BN/2) rows instead of (128 + BN).  Both
+// CTAs' TMA bytes are counted on the leader's full barrier; the leader's MMA commits free
+// the stage in both CTAs and signal both epilogues; both epilogues release the accumulator
+// buffer on the leader's barrier.
+template <int BN, int NPASS, int STAGES>
+struct CfgPair {
+    static constexpr int NPL = NPASS == 3 ? 2 : 1;
+    static constexpr uint32_t A_BYTES = BM * BK * 2;            // this CTA's 128 rows
+    static constexpr uint32_t B_BYTES = (BN / 2) * BK * 2;      // this CTA's half of B
+    static constexpr uint32_t STAGE_BYTES = NPL * (A_BYTES + B_BYTES);
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr int TMEM_COLS = 2 * BN;
+};
+
+template <int MODE, int BN, int NPASS, int STAGES>
+__global__ void __launch_bounds__(NTHREADS, 1) umma_pair_kernel(const __grid_constant__ UmmaParams P) {
+    using C_ = CfgPair<BN, NPASS, STAGES>;
+    constexpr int NPL = C_::NPL;
+    constexpr bool A_MN = (MODE == WGRAD_);
+    constexpr bool B_MN = (MODE != FWD_);
+    constexpr int BH = BN / 2;  // B columns held by this CTA
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C_::STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;  // [2]
+    uint64_t* tempty = tfull + 2;      // [2] (used in the leader)
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair_id = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const int mtiles_p = (P.mtiles + 1) / 2;  // pair tiles along m (256 rows)
+    const int total = mtiles_p * P.ntiles * P.nsplit;
+
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < 2; ++i) {
+            tma_prefetch(&P.a[i]);
+            tma_prefetch(&P.b[i]);
+        }
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 2);   // leader: own expect_tx arrive + the peer's arrive
+            mbar_init(&empty[s], 1);  // one multicast commit from the leader's MMA
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc_pair<C_::TMEM_COLS>(tslot);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tbase = *tslot;
+
+    auto tile_coords = [&](int ct, int& mp, int& n_tile, int& split) {
+        n_tile = ct % P.ntiles;
+        const int rest = ct / P.ntiles;
+        mp = rest % mtiles_p;
+        split = rest / mtiles_p;
+    };
+    auto kblocks = [&](int split, int& p_begin) -> int {
+        if (MODE == WGRAD_) {
+            p_begin = split * P.ksplit_rows;
+            const int p_end = min(P.R, p_begin + P.ksplit_rows);
+            return (p_end - p_begin + BK - 1) / BK;
+        }
+        p_begin = 0;
+        return 3 * P.cpb;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ===================== TMA producer (both CTAs) =====================
+            const uint32_t full_leader0 = mapa_shared(&full[0], 0);
+            int it = 0;
+            for (int ct = pair_id; ct < total; ct += npairs) {
+                int mp, n_tile, split, p_begin;
+                tile_coords(ct, mp, n_tile, split);
+                const int nkb = kblocks(split, p_begin);
+                const int m0 = mp * 2 * BM + (int)rank * BM;  // this CTA's 128 rows
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    mbar_wait(&empty[s], ph ^ 1);
+                    uint8_t* st = smem + s * C_::STAGE_BYTES;
+                    if (leader) mbar_arrive_expect_tx(&full[s], 2 * C_::STAGE_BYTES);
+                    else mbar_arrive_remote(full_leader0 + s * 8);
+#pragma unroll
+                    for (int pl = 0; pl < NPL; ++pl) {
+                        uint8_t* sa = st + pl * C_::A_BYTES;
+                        uint8_t* sb = st + NPL * C_::A_BYTES + pl * C_::B_BYTES;
+                        if (MODE == FWD_) {
+                            const int j = kb / P.cpb, c0 = (kb % P.cpb) * BK;
+                            tma_load_2d_pair(sa, &P.a[pl], &full[s], c0, m0 + j - 1);
+                            tma_load_2d_pair(sb, &P.b[pl], &full[s], j * P.Kc + c0, n_tile * BN + (int)rank * BH);
+                        } else if (MODE == DGRAD_) {
+                            const int j = kb / P.cpb, o0 = (kb % P.cpb) * BK;
+                            tma_load_2d_pair(sa, &P.a[pl], &full[s], o0, m0 + 1 - j);
+#pragma unroll
+                            for (int q = 0; q < BH / 64; ++q)
+                                tma_load_3d_pair(sb + q * (BK * 128), &P.b[pl], &full[s],
+                                                 n_tile * BN + (int)rank * BH + 64 * q, j, o0);
+                        } else {  // WGRAD: m = output channel o (this CTA: 128 of the 256)
+                            const int p0 = p_begin + kb * BK;
+#pragma unroll
+                            for (int q = 0; q < BM / 64; ++q)
+                                tma_load_2d_pair(sa + q * (BK * 128), &P.a[pl], &full[s], m0 + 64 * q, p0);
+#pragma unroll
+                            for (int q = 0; q < BH / 64; ++q) {
+                                uint8_t* dst = sb + q * (BK * 128);
+                                int g = n_tile * (BN / 64) + (int)rank * (BH / 64) + q;
+                                if (P.ones_chunk && g == 3 * P.cpj) {
+                                    tma_load_2d_pair(dst, &P.ones, &full[s], 64 * pl, p0);
+                                    continue;
+                                }
+                                if (g >= 3 * P.cpj) g = 3 * P.cpj - 1;
+                                const int j = g / P.cpj, c0 = (g % P.cpj) * 64;
+                                tma_load_2d_pair(dst, &P.b[pl], &full[s], c0, p0 + j - 1);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && leader) {
+            // ===================== MMA issuer (leader only) =====================
+            constexpr uint32_t idesc = make_idesc_bf16(2 * BM, BN, A_MN, B_MN);
+            int it = 0, t = 0;
+            for (int ct = pair_id; ct < total; ct += npairs, ++t) {
+                int mp, n_tile, split, p_begin;
+                tile_coords(ct, mp, n_tile, split);
+                const int nkb = kblocks(split, p_begin);
+                const int acc = t & 1;
+                mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t dt = tbase + (uint32_t)(acc * BN);
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    const uint32_t ph = (it / STAGES) & 1;
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t st = smem_u32(smem + s * C_::STAGE_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / UK; ++k) {
+#pragma unroll
+                        for (int pass = 0; pass < NPASS; ++pass) {
+                            const int pa = (pass == 2) ? 1 : 0;
+                            const int pb = (pass == 1) ? 1 : 0;
+                            const uint32_t a_addr = st + pa * C_::A_BYTES;
+                            const uint32_t b_addr = st + NPL * C_::A_BYTES + pb * C_::B_BYTES;
+                            const uint64_t ad = A_MN ? make_desc(a_addr + k * (UK * 128), BK * 128, 1024)
+                                                     : make_desc(a_addr + k * (UK * 2), 16, 1024);
+                            const uint64_t bd = B_MN ? make_desc(b_addr + k * (UK * 128), BK * 128, 1024)
+                                                     : make_desc(b_addr + k * (UK * 2), 16, 1024);
+                            mma_bf16_pair(dt, ad, bd, idesc, (kb | k | pass) != 0 ? 1u : 0u);
+                        }
+                    }
+                    mma_commit_pair(&empty[s]);
+                }
+                mma_commit_pair(&tfull[acc]);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ===================== epilogue (warps 2..5, both CTAs) =====================
+        const int q = warp & 3;
+        const uint32_t tempty_leader = mapa_shared(&tempty[0], 0);
+        int t = 0;
+        for (int ct = pair_id; ct < total; ct += npairs, ++t) {
+            int mp, n_tile, split, p_begin;
+            tile_coords(ct, mp, n_tile, split);
+            const int acc = t & 1;
+            const int m_tile = mp * 2 + (int)rank;  // 128-row tile index of this CTA
+            const int row = m_tile * BM + 32 * q + lane;
+            mbar_wait(&tfull[acc], (t >> 1) & 1);
+            tc_fence_after();
+            const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN);
+#pragma unroll 1
+            for (int c16 = 0; c16 < BN / 16; ++c16) {
+                uint32_t r[16];
+                tmem_ld16(tq + (uint32_t)(c16 * 16), r);
+                tmem_ld_wait();
+                float v[16];
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+                if (MODE == FWD_ || MODE == DGRAD_) {
+                    if (m_tile >= P.mtiles || row >= P.R) continue;
+                    const int n = n_tile * BN + c16 * 16;
+                    const bool halo = halo_row(row, P.Tp);
+                    if (MODE == FWD_) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            const float tv = v[i] + P.bias[n + i];
+                            v[i] = (!halo && tv > 0.f) ? tv : 0.f;
+                        }
+                    } else {
+                        uint32_t mw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                        if (!halo) {
+                            const uint4* mk = reinterpret_cast<const uint4*>(
+                                static_cast<const __nv_bfloat16*>(P.mask) + (size_t)row * P.Nout + n);
+                            const uint4 m0v = mk[0], m1v = mk[1];
+                            mw[0] = m0v.x; mw[1] = m0v.y; mw[2] = m0v.z; mw[3] = m0v.w;
+                            mw[4] = m1v.x; mw[5] = m1v.y; mw[6] = m1v.z; mw[7] = m1v.w;
+                        }
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            v[2 * i] = __uint_as_float(mw[i] << 16) > 0.f ? v[2 * i] : 0.f;
+                            v[2 * i + 1] = __uint_as_float(mw[i] & 0xFFFF0000u) > 0.f ? v[2 * i + 1] : 0.f;
+                        }
+                    }
+                    if (P.out_f32) {
+                        float4* d = reinterpret_cast<float4*>(static_cast<float*>(P.out_hi) + (size_t)row * P.Nout + n);
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                    } else {
+                        __nv_bfloat16* hi = static_cast<__nv_bfloat16*>(P.out_hi) + (size_t)row * P.Nout + n;
+                        __nv_bfloat16* lo = P.out_lo ? static_cast<__nv_bfloat16*>(P.out_lo) + (size_t)row * P.Nout + n
+                                                     : nullptr;
+                        store16_planes(hi, lo, v);
+                    }
+                } else {  // WGRAD partial: row = o, columns -> (j, c)
+                    const int nl = c16 * 16;
+                    const int g = n_tile * (BN / 64) + nl / 64;
+                    float* part = P.part + (size_t)split * P.part_stride;
+                    if (P.ones_chunk && g == 3 * P.cpj) {
+                        if (nl % 64 == 0) part[(size_t)P.Nout * P.NW + row] = v[0];
+                        continue;
+                    }
+                    if (g >= 3 * P.cpj) continue;
+                    const int j = g / P.cpj, c = (g % P.cpj) * 64 + (nl % 64);
+                    if (c >= P.Cin_w) continue;
+                    float* dst = part + (size_t)row * P.NW + (size_t)j * P.Cin_w + c;
+                    if (c + 16 <= P.Cin_w) {
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            if (c + i < P.Cin_w) dst[i] = v[i];
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(tempty_leader + acc * 8);  // free the buffer (leader's barrier)
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_pair<C_::TMEM_COLS>(tbase);
+    }
+}
+
 // ------------------------------------------------------------------ companions
 // x [B][T][Cin] fp32 -> halo-padded hi/lo bf16 planes [B][T+2][Cin].
 __global__ void prep_x_split_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ hi,
@@ -508,6 +775,42 @@ cudaError_t launch_one(const UmmaParams& p, cudaStream_t s) {
     return cudaLaunchKernelEx(&cfg, k, p);
 }
 
+template <int MODE, int BN, int NPASS, int STAGES>
+cudaError_t launch_pair(const UmmaParams& p, cudaStream_t s) {
+    using C_ = umma::CfgPair<BN, NPASS, STAGES>;
+    auto k = umma::umma_pair_kernel<MODE, BN, NPASS, STAGES>;
+    static int max_clusters = -1;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(umma::NTHREADS);
+    cfg.dynamicSmemBytes = C_::SMEM;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (max_clusters < 0) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM);
+        if (e != cudaSuccess) return e;
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+        cfg.gridDim = dim3(2 * (sms / 2), 1, 1);
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            n = sms / 2;
+        }
+        max_clusters = n;
+    }
+    const int total = ((p.mtiles + 1) / 2) * p.ntiles * p.nsplit;
+    const int npairs = total < max_clusters ? total : max_clusters;
+    if (npairs <= 0) return cudaSuccess;
+    cfg.gridDim = dim3(2 * npairs, 1, 1);
+    return cudaLaunchKernelEx(&cfg, k, p);
+}
+
 }  // namespace
 
 // Tile / cluster configurations (BN, STAGES, CM, CN) per GEMM and precision.
@@ -517,17 +820,33 @@ cudaError_t launch_one(const UmmaParams& p, cudaStream_t s) {
 //                B over 2 m-tiles; WGRAD 128x128, B multicast over the 4 o-tiles.
 struct GemmCfg {
     int bn, stages, cm, cn;
+    int pair;  // 1: 2-CTA kernel (256-row pair tiles, cta_group::2)
 };
+// TEM_GEMM_VARIANT (experiments): 2 = 2-CTA pairs (default), 1 = 1-CTA without clusters,
+// 0 = 1-CTA with multicast clusters.
+static int gemm_variant() {
+    const char* e = getenv("TEM_GEMM_VARIANT");
+    return e ? atoi(e) : 2;
+}
 static GemmCfg cfg_for(int mode, int npass) {
-    if (npass == 1) return mode == WGRAD_ ? GemmCfg{256, 4, 4, 1} : GemmCfg{256, 4, 2, 1};
-    return mode == WGRAD_ ? GemmCfg{128, 3, 4, 1} : GemmCfg{64, 4, 2, 4};
+    const int v = gemm_variant();
+    if (v == 2) {
+        if (npass == 1) return GemmCfg{256, 6, 1, 1, 1};
+        return mode == WGRAD_ ? GemmCfg{256, 3, 1, 1, 1} : GemmCfg{128, 4, 1, 1, 1};
+    }
+    if (v == 1) {
+        if (npass == 1) return GemmCfg{256, 4, 1, 1, 0};
+        return mode == WGRAD_ ? GemmCfg{128, 3, 1, 1, 0} : GemmCfg{64, 4, 1, 1, 0};
+    }
+    if (npass == 1) return mode == WGRAD_ ? GemmCfg{256, 4, 4, 1, 0} : GemmCfg{256, 4, 2, 1, 0};
+    return mode == WGRAD_ ? GemmCfg{128, 3, 4, 1, 0} : GemmCfg{64, 4, 2, 4, 0};
 }
 
 int umma_wgrad_splits(const Geom& g) {
     const GemmCfg c = cfg_for(WGRAD_, g.prec == TEM_FP32 ? 3 : 1);
     const int chunks = 3 * (((g.Cin > g.C ? g.Cin : g.C) + 63) / 64) + 1;
     const int tiles = (g.C / umma::BM) * ((chunks + c.bn / 64 - 1) / (c.bn / 64));
-    int S = (148 + tiles - 1) / tiles;
+    int S = c.pair ? (74 * 2) / tiles : (148 + tiles - 1) / tiles;  // pairs: one wave of 74 pairs
     const int nkb = (g.R + umma::BK - 1) / umma::BK;
     if (S > nkb) S = nkb;
     if (S < 1) S = 1;
@@ -553,8 +872,8 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     const void* dA2[2] = {b.dA2, b.dA2_lo};
     const void* dA1[2] = {b.dA1, b.dA1_lo};
     const __nv_bfloat16* W[2] = {b.shadow, b.shadow_lo};
-    // slice rows of the multicast boxes
-    const uint32_t arK = umma::BM / cf.cn, brK = cf.bn / cf.cm;        // FWD/DGRAD K-major A / B
+    // box rows: multicast slices (1-CTA clusters) or the pair half of B (2-CTA)
+    const uint32_t arK = umma::BM / cf.cn, brK = cf.pair ? cf.bn / 2 : cf.bn / cf.cm;  // FWD/DGRAD K-major A / B
     const uint32_t brD = umma::BK / cf.cm;                              // DGRAD MN-major B
     const uint32_t arW = umma::BK / cw.cn, brW = umma::BK / cw.cm;       // WGRAD MN-major A / B
     bool ok = true;
@@ -649,12 +968,22 @@ void umma_plan_destroy(UmmaPlan* plan) {
 
 template <int MODE>
 static cudaError_t dispatch(const UmmaParams& p, int npass, cudaStream_t s) {
+    const GemmCfg c = cfg_for(MODE, npass);
+    if (c.pair) {
+        if constexpr (MODE == WGRAD_) {
+            if (npass == 3) return launch_pair<MODE, 256, 3, 3>(p, s);
+            return launch_pair<MODE, 256, 1, 6>(p, s);
+        } else {
+            if (npass == 3) return launch_pair<MODE, 128, 3, 4>(p, s);
+            return launch_pair<MODE, 256, 1, 6>(p, s);
+        }
+    }
     if constexpr (MODE == WGRAD_) {
-        if (npass == 3) return launch_one<MODE, 128, 3, 3, 4, 1>(p, s);
-        return launch_one<MODE, 256, 1, 4, 4, 1>(p, s);
+        if (npass == 3) return c.cm == 1 ? launch_one<MODE, 128, 3, 3, 1, 1>(p, s) : launch_one<MODE, 128, 3, 3, 4, 1>(p, s);
+        return c.cm == 1 ? launch_one<MODE, 256, 1, 4, 1, 1>(p, s) : launch_one<MODE, 256, 1, 4, 4, 1>(p, s);
     } else {
-        if (npass == 3) return launch_one<MODE, 64, 3, 4, 2, 4>(p, s);
-        return launch_one<MODE, 256, 1, 4, 2, 1>(p, s);
+        if (npass == 3) return c.cm == 1 ? launch_one<MODE, 64, 3, 4, 1, 1>(p, s) : launch_one<MODE, 64, 3, 4, 2, 4>(p, s);
+        return c.cm == 1 ? launch_one<MODE, 256, 1, 4, 1, 1>(p, s) : launch_one<MODE, 256, 1, 4, 2, 1>(p, s);
     }
 }
 
