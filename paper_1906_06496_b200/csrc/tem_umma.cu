@@ -822,11 +822,11 @@ struct GemmCfg {
     int bn, stages, cm, cn;
     int pair;  // 1: 2-CTA kernel (256-row pair tiles, cta_group::2)
 };
-// TEM_GEMM_VARIANT (experiments): 2 = 2-CTA pairs (default), 1 = 1-CTA without clusters,
+// TEM_GEMM_VARIANT (experiments): 1 = 1-CTA without clusters (default), 2 = 2-CTA pairs,
 // 0 = 1-CTA with multicast clusters.
 static int gemm_variant() {
     const char* e = getenv("TEM_GEMM_VARIANT");
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 1;
 }
 static GemmCfg cfg_for(int mode, int npass) {
     const int v = gemm_variant();
