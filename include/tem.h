@@ -86,7 +86,15 @@ typedef struct {
     /* --- ring tuning (0 = automatic)                                                       */
     int32_t ring_channels;  /* G: CTAs per rank in the ring kernel                           */
     int32_t ring_chunks;    /* C: pipelined sub-chunks per channel per block                 */
+    /* --- gradient exchange of tem_step / tem_exchange                                      */
+    int32_t exchange;       /* TEM_EXCHANGE_RING (the paper's ring; default) or
+                               TEM_EXCHANGE_PS (the parameter-server comparator, P:115-124:
+                               ranks push gradients to rank 0, which sums them in ascending
+                               rank order, applies mean + SGD to its weights and pushes w'
+                               back to every rank)                                           */
 } tem_config;
+
+enum { TEM_EXCHANGE_RING = 0, TEM_EXCHANGE_PS = 1 };
 
 /* --- sizes -----------------------------------------------------------------------------
  * K      = c_hidden*3*c_in + c_hidden + c_hidden*3*c_hidden + c_hidden + 3*c_hidden + 3

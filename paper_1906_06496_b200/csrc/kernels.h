@@ -150,7 +150,8 @@ cudaError_t launch_sgd_single(const float* g, float* w, __nv_bfloat16* shadow, _
                               int64_t n, int op, float lr, cudaStream_t s);
 struct PsParams {
     RingLocal loc[TEM_MAX_RANKS];
-    int N, rank_base, nlocal, G, op;
+    int N, rank_base, nlocal, G, op, mode;  // mode 0 = allreduce, 1 = SGD (server updates)
+    float lr;
     int64_t K;
     int64_t off_dst, off_slots, off_flags;
     Status* status;

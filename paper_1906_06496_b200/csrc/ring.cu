@@ -314,7 +314,14 @@ __global__ void __launch_bounds__(RING_THREADS) ps_kernel(const __grid_constant_
             if (P.op == TEM_MEAN) {
                 a.x = a.x * inv_n; a.y = a.y * inv_n; a.z = a.z * inv_n; a.w = a.w * inv_n;
             }
-            for (int r = 0; r < N; ++r)  // downlink broadcast
+            if (P.mode == 1) {  // the server holds and upgrades the weights: w' = w - lr*gbar
+                const float4 w = *reinterpret_cast<const float4*>(L.dst_self + e);
+                a.x = __fmaf_rn(-P.lr, a.x, w.x);
+                a.y = __fmaf_rn(-P.lr, a.y, w.y);
+                a.z = __fmaf_rn(-P.lr, a.z, w.z);
+                a.w = __fmaf_rn(-P.lr, a.w, w.w);
+            }
+            for (int r = 0; r < N; ++r)  // downlink broadcast (gbar, or w' in SGD mode)
                 st4_masked(reinterpret_cast<float*>(L.heaps[r] + P.off_dst), e, K, a);
         }
         __syncthreads();
@@ -328,6 +335,9 @@ __global__ void __launch_bounds__(RING_THREADS) ps_kernel(const __grid_constant_
         const uint64_t* f = reinterpret_cast<const uint64_t*>(L.heaps[n] + P.off_flags) + (int64_t)(TEM_MAX_RANKS + n) * kMaxChannels + g;
         if (!wait_flag(f, epoch, K, P.status, P.spin_ns, &s_abort)) return;
     }
+    if (L.shadow)  // refresh this rank's operand copies of the new weights (its channel slice)
+        for (int64_t v = v0 + tid; v < v1; v += RING_THREADS)
+            store_shadow4(L.shadow, L.shadow_lo, 4 * v, ld_cg4(L.dst_self + 4 * v));
     if (tid == 0) L.epochs[g] = epoch;
 }
 

@@ -50,6 +50,7 @@ bool cfg_valid(const tem_config* c) {
     if (c->max_allreduce_elems < 0) return false;
     if (c->ring_channels < 0 || c->ring_channels > kMaxChannels) return false;
     if (c->ring_chunks < 0 || c->ring_chunks > kMaxChunks) return false;
+    if (c->exchange != TEM_EXCHANGE_RING && c->exchange != TEM_EXCHANGE_PS) return false;
     return true;
 }
 
@@ -458,7 +459,27 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
     p.off_flags = (int64_t)c->hl.off_flags;
     p.status = c->st_dev;
     p.spin_ns = kSpinNs;
-    if (launch_ring(p, s) != cudaSuccess) return TEM_ERR_CUDA;
+    if (c->cfg.exchange == TEM_EXCHANGE_PS) {  // comparator: push / server update / pull
+        PsParams q;
+        memset(&q, 0, sizeof(q));
+        for (int l = 0; l < c->nlocal; ++l) q.loc[l] = p.loc[l];
+        q.N = c->N;
+        q.rank_base = c->rank;
+        q.nlocal = c->nlocal;
+        q.G = c->G;
+        q.op = TEM_MEAN;
+        q.mode = 1;
+        q.lr = c->cfg.lr;
+        q.K = g.Kpad;
+        q.off_dst = 0;
+        q.off_slots = (int64_t)c->hl.off_ps;
+        q.off_flags = (int64_t)c->hl.off_psflags;
+        q.status = c->st_dev;
+        q.spin_ns = kSpinNs;
+        if (launch_ps(q, s) != cudaSuccess) return TEM_ERR_CUDA;
+    } else if (launch_ring(p, s) != cudaSuccess) {
+        return TEM_ERR_CUDA;
+    }
     rec.end(SLOT_EXCHANGE);
     ++*nl;
     return st;

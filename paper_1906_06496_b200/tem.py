@@ -21,6 +21,7 @@ TEM_OK, TEM_ERR_INVALID_ARG, TEM_ERR_PROTOCOL, TEM_ERR_TRANSPORT, TEM_ERR_CUDA, 
     TEM_ERR_NONFINITE, TEM_ERR_STATE = range(7)
 TEM_SUM, TEM_MEAN = 0, 1
 TEM_FP32, TEM_BF16 = 0, 1
+TEM_EXCHANGE_RING, TEM_EXCHANGE_PS = 0, 1
 MAX_RANKS = 8
 
 _P = ctypes.c_void_p
@@ -38,6 +39,7 @@ class tem_config(ctypes.Structure):
         ("max_allreduce_elems", ctypes.c_int64),
         ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
         ("ring_channels", ctypes.c_int32), ("ring_chunks", ctypes.c_int32),
+        ("exchange", ctypes.c_int32),
     ]
 
 
@@ -208,6 +210,7 @@ class SessionConfig:
     max_allreduce_elems: int = 0
     ring_channels: int = 0
     ring_chunks: int = 0
+    exchange: int = TEM_EXCHANGE_RING
 
 
 class TemSession:
@@ -233,6 +236,7 @@ class TemSession:
             cfg.loss_weight[i] = float(sc.loss_weight[i])
         cfg.max_allreduce_elems = sc.max_allreduce_elems
         cfg.ring_channels, cfg.ring_chunks = sc.ring_channels, sc.ring_chunks
+        cfg.exchange = sc.exchange
         self.K = tem_num_params(cfg)
         if self.K == 0:
             raise TemError(TEM_ERR_INVALID_ARG, "config")
@@ -250,10 +254,18 @@ class TemSession:
         else:
             import torch.distributed as dist
             import torch.distributed._symmetric_memory as symm_mem
+            from . import dist as tdist
             grp = group if group is not None else dist.group.WORLD
+            tdist.check_symmetric(sc, grp)  # equal K / shapes on every rank before any peer wait
+            gname = grp.group_name
+            if hasattr(symm_mem, "enable_symm_mem_for_group"):
+                try:  # required on some torch versions, a no-op / deprecated on newer ones
+                    symm_mem.enable_symm_mem_for_group(gname)
+                except Exception:
+                    pass
             t = symm_mem.empty(self.sym_bytes, dtype=torch.uint8, device=self.dev)
             t.zero_()
-            hdl = symm_mem.rendezvous(t, grp)
+            hdl = symm_mem.rendezvous(t, gname)
             self._symm = (t, hdl)
             ptrs = list(hdl.buffer_ptrs)
             if any(p % 4096 for p in ptrs):
