@@ -197,6 +197,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--lr", type=float, default=0.01)
+    ap.add_argument("--exchange", default="ring", choices=["ring", "ps"],
+                    help="gradient exchange: the paper's ring (default) or the PS comparator")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -227,7 +229,7 @@ def main():
 
     B, prec = wl["B"], wl["prec"]
     sc = tem.SessionConfig(world_size=world, rank=rank, local_ranks=1, batch_per_rank=B, precision=prec,
-                           lr=args.lr)
+                           lr=args.lr, exchange=tem.TEM_EXCHANGE_PS if args.exchange == "ps" else tem.TEM_EXCHANGE_RING)
     t_init0 = time.perf_counter()
     sess = tem.TemSession(sc, datagen.init_params(), device=local)
     t_init = time.perf_counter() - t_init0
@@ -366,7 +368,9 @@ def main():
         "vs_baseline": None, "dtype": wl["dtype"], "data": "synthetic (seeded ActivityNet-shaped features/labels, random-init weights)",
         "config": {"workload": wl["desc"], "batch_per_gpu": B, "global_batch": B * world, "seq_len": T,
                    "channels": "400->512->512->3", "parallelism": f"dp{world}",
-                   "exchange": "fused ring allreduce + mean + SGD (KR1)" if world > 1 else "N=1: owner SGD only",
+                   "exchange": ("N=1: owner SGD only" if world == 1 else
+                                ("parameter server on rank 0 (KP1)" if args.exchange == "ps"
+                                 else "fused ring allreduce + mean + SGD (KR1)")),
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",
                    "kernel_path": sess.kernel_path()},
         "gpu_launches": launches * args.steps,
@@ -375,6 +379,15 @@ def main():
         "e2e": e2e,
         "clocks": clk,
         "t3_init_s": t_init,
+        # P:163 training-time decomposition, per step, from the instrumented pass:
+        # t1 = forward + backward (all kernels but the exchange), t2 = gradient exchange.
+        "paper_metrics": {
+            "t1_fwd_bwd_ms": sum(v for k, v in slot_ms.items() if k != "exchange") / max(nrec, 1),
+            "t2_exchange_ms": slot_ms.get("exchange", 0.0) / max(nrec, 1),
+            "t3_setup_s": t_init,
+            "epoch_videos": 9997,
+            "epoch_time_s": 9997 / value,
+        },
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(wl, args.cpu_videos)

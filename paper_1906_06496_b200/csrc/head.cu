@@ -222,28 +222,33 @@ int head_rows_per_cta(const Geom& g) {
 
 int head_ctas(const Geom& g) { return g.R > 0 ? (g.R + head_rows_per_cta(g) - 1) / head_rows_per_cta(g) : 0; }
 
-cudaError_t launch_head(const Geom& g, const RankBufs& b, const float* labels, const float lam[3],
-                        float* loss_out, Status* status, const EvRec& rec, cudaStream_t s, int* n) {
+cudaError_t launch_head_rows(const Geom& g, const RankBufs& b, const float* labels, const float lam[3],
+                             const EvRec& rec, cudaStream_t s, int* n) {
     const int P = head_ctas(g);
     const int rpc = head_rows_per_cta(g);
     const size_t hsm = (size_t)(3 * g.C + 3 * rpc) * sizeof(float);
-    if (P > 0) {
-        rec.begin(SLOT_HEAD);
-        if (g.op_bf16) {
-            auto k = head_rows_kernel<__nv_bfloat16>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-            k<<<P, 256, hsm, s>>>(b.h2, b.params + g.off_W3, b.params + g.off_b3, labels, lam[0], lam[1], lam[2],
-                                  static_cast<__nv_bfloat16*>(b.dA2), static_cast<__nv_bfloat16*>(b.dA2_lo), b.z,
-                                  b.headpart, g.B, g.T, g.C, rpc);
-        } else {
-            auto k = head_rows_kernel<float>;
-            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-            k<<<P, 256, hsm, s>>>(b.h2, b.params + g.off_W3, b.params + g.off_b3, labels, lam[0], lam[1], lam[2],
-                                  static_cast<float*>(b.dA2), nullptr, b.z, b.headpart, g.B, g.T, g.C, rpc);
-        }
-        rec.end(SLOT_HEAD);
-        ++*n;
+    if (P == 0) return cudaSuccess;
+    rec.begin(SLOT_HEAD);
+    if (g.op_bf16) {
+        auto k = head_rows_kernel<__nv_bfloat16>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+        k<<<P, 256, hsm, s>>>(b.h2, b.params + g.off_W3, b.params + g.off_b3, labels, lam[0], lam[1], lam[2],
+                              static_cast<__nv_bfloat16*>(b.dA2), static_cast<__nv_bfloat16*>(b.dA2_lo), b.z,
+                              b.headpart, g.B, g.T, g.C, rpc);
+    } else {
+        auto k = head_rows_kernel<float>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+        k<<<P, 256, hsm, s>>>(b.h2, b.params + g.off_W3, b.params + g.off_b3, labels, lam[0], lam[1], lam[2],
+                              static_cast<float*>(b.dA2), nullptr, b.z, b.headpart, g.B, g.T, g.C, rpc);
     }
+    rec.end(SLOT_HEAD);
+    ++*n;
+    return cudaGetLastError();
+}
+
+cudaError_t launch_head_reduce(const Geom& g, const RankBufs& b, const float lam[3], float* loss_out,
+                               Status* status, const EvRec& rec, cudaStream_t s, int* n) {
+    const int P = head_ctas(g);
     rec.begin(SLOT_HEADFIN);
     const int nent = 4 * g.C + 6;
     const int G = P >= 128 ? 16 : (P >= 16 ? 4 : 1);
@@ -253,6 +258,13 @@ cudaError_t launch_head(const Geom& g, const RankBufs& b, const float* labels, c
     rec.end(SLOT_HEADFIN);
     ++*n;
     return cudaGetLastError();
+}
+
+cudaError_t launch_head(const Geom& g, const RankBufs& b, const float* labels, const float lam[3],
+                        float* loss_out, Status* status, const EvRec& rec, cudaStream_t s, int* n) {
+    cudaError_t e = launch_head_rows(g, b, labels, lam, rec, s, n);
+    if (e != cudaSuccess) return e;
+    return launch_head_reduce(g, b, lam, loss_out, status, rec, s, n);
 }
 
 }  // namespace tem

@@ -123,6 +123,10 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
 // writes dA2 as b.dA2 (+ b.dA2_lo when present) in the operand type of the path.
 cudaError_t launch_head(const Geom& g, const RankBufs& b, const float* labels, const float lam[3],
                         float* loss_out, Status* status, const EvRec& rec, cudaStream_t s, int* n);
+cudaError_t launch_head_rows(const Geom& g, const RankBufs& b, const float* labels, const float lam[3],
+                             const EvRec& rec, cudaStream_t s, int* n);
+cudaError_t launch_head_reduce(const Geom& g, const RankBufs& b, const float lam[3], float* loss_out,
+                               Status* status, const EvRec& rec, cudaStream_t s, int* n);
 cudaError_t launch_reduce_splits(const float* part, float* dst, int64_t n, int S, cudaStream_t s);
 
 // --- ring / exchange (ring.cu) --------------------------------------------------------

@@ -1002,13 +1002,16 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     rec.end(SLOT_CONV2);
     if (e != cudaSuccess) return e;
     ++n;
-    e = launch_head(g, b, labels, lam, loss_out, status, rec, s, &n);
+    e = launch_head_rows(g, b, labels, lam, rec, s, &n);
     if (e != cudaSuccess) return e;
-    // Fork: conv2 wgrad (+ its reduction) on the aux stream runs alongside conv2 dgrad ->
-    // conv1 wgrad on s; both only read dA2 / h1 / xp (captured as parallel graph branches).
+    // Fork: the head reduction and conv2 wgrad (+ its reduction) run on the aux stream
+    // alongside conv2 dgrad -> conv1 wgrad on s; all only read dA2 / h1 / xp / head
+    // partials (captured as parallel graph branches).
     const EvRec rec2{rec.ev, P.aux};
     if (cudaEventRecord(P.fork, s) != cudaSuccess || cudaStreamWaitEvent(P.aux, P.fork, 0) != cudaSuccess)
         return cudaErrorUnknown;
+    e = launch_head_reduce(g, b, lam, loss_out, status, rec2, P.aux, &n);
+    if (e != cudaSuccess) return e;
     rec2.begin(SLOT_WGRAD2);
     e = dispatch<WGRAD_>(P.wgrad2, P.npass, P.aux);
     rec2.end(SLOT_WGRAD2);
