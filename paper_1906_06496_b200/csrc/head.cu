@@ -61,7 +61,19 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
     const int NQ = C / 32;  // <= 16
     float lsum[3] = {0.f, 0.f, 0.f}, dbs[3] = {0.f, 0.f, 0.f};
     const float inv_bt = 1.0f / ((float)B * (float)Tn);
+    float hn[16];  // software pipeline: the next row of this warp is in flight
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+        hn[q] = (q < NQ && p0 + warp < p1) ? h2[(size_t)(p0 + warp) * C + lane + 32 * q] : 0.f;
     for (int p = p0 + warp; p < p1; p += HEAD_WARPS) {
+        float h[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) h[q] = hn[q];
+        {
+            const int pn = p + HEAD_WARPS;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) hn[q] = (q < NQ && pn < p1) ? h2[(size_t)pn * C + lane + 32 * q] : 0.f;
+        }
         const int v = p / Tp, tp = p - v * Tp;
         float* dzr = sdz + (p - p0) * 3;
         if (tp == 0 || tp == Tp - 1) {
@@ -69,9 +81,6 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
             continue;
         }
         const int t = tp - 1, k = v - v0;
-        float h[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) h[q] = (q < NQ) ? h2[(size_t)p * C + lane + 32 * q] : 0.f;
         float z[3];
 #pragma unroll
         for (int o = 0; o < 3; ++o) {
@@ -119,27 +128,34 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
     for (int c = tid; c < C; c += blockDim.x) {
         const float w0 = sW3[c], w1 = sW3[C + c], w2 = sW3[2 * C + c];
         float a0 = 0.f, a1 = 0.f, a2 = 0.f, bsum = 0.f;
-#pragma unroll 4
-        for (int p = p0; p < p1; ++p) {
-            const float* dzr = sdz + (p - p0) * 3;
-            const float d0 = dzr[0], d1 = dzr[1], d2 = dzr[2];
-            const float hv = h2[(size_t)p * C + c];
-            float d = w0 * d0;
-            d = fmaf(w1, d1, d);
-            d = fmaf(w2, d2, d);
-            const float dv = hv > 0.f ? d : 0.f;
-            const TOp dh = from_f<TOp>(dv);
-            float stored = to_f(dh);
-            dA2[(size_t)p * C + c] = dh;
-            if (dA2_lo) {
-                const TOp dl = from_f<TOp>(dv - stored);
-                dA2_lo[(size_t)p * C + c] = dl;
-                stored += to_f(dl);
+        constexpr int U = 8;  // rows per batch: U independent h2 loads in flight per thread
+        for (int pb = p0; pb < p1; pb += U) {
+            float hv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) hv[u] = (pb + u < p1) ? h2[(size_t)(pb + u) * C + c] : 0.f;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int p = pb + u;
+                if (p >= p1) break;
+                const float* dzr = sdz + (p - p0) * 3;
+                const float d0 = dzr[0], d1 = dzr[1], d2 = dzr[2];
+                float d = w0 * d0;
+                d = fmaf(w1, d1, d);
+                d = fmaf(w2, d2, d);
+                const float dv = hv[u] > 0.f ? d : 0.f;
+                const TOp dh = from_f<TOp>(dv);
+                float stored = to_f(dh);
+                dA2[(size_t)p * C + c] = dh;
+                if (dA2_lo) {
+                    const TOp dl = from_f<TOp>(dv - stored);
+                    dA2_lo[(size_t)p * C + c] = dl;
+                    stored += to_f(dl);
+                }
+                bsum += stored;
+                a0 = fmaf(d0, hv[u], a0);
+                a1 = fmaf(d1, hv[u], a1);
+                a2 = fmaf(d2, hv[u], a2);
             }
-            bsum += stored;
-            a0 = fmaf(d0, hv, a0);
-            a1 = fmaf(d1, hv, a1);
-            a2 = fmaf(d2, hv, a2);
         }
         // partial row layout: [dW3 (3C)][db3 (3)][L (3)][db2 (C)]
         dst[c] = a0;
@@ -211,7 +227,7 @@ __global__ void head_reduce_kernel(const float* __restrict__ part, int P, int C,
 }
 
 int head_rows_per_cta(const Geom& g) {
-    int rpc = (g.R + 295) / 296;
+    int rpc = (g.R + 591) / 592;  // ~4 CTAs per SM
     rpc = (rpc + 7) / 8 * 8;
     if (rpc < 16) rpc = 16;
     if (rpc > 128) rpc = 128;

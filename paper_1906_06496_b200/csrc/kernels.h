@@ -64,6 +64,7 @@ enum UmmaMode { FWD_ = 0, DGRAD_ = 1, WGRAD_ = 2 };
 struct UmmaParams {
     CUtensorMap a[2];  // A operand, hi / lo planes
     CUtensorMap b[2];  // B operand, hi / lo planes
+    CUtensorMap out[2];  // epilogue TMA-store maps (output hi / lo plane, fp32 output, or split-K partials)
     int R, Tp;         // padded rows, T + 2
     int Kc, cpb;       // FWD/DGRAD: channels per tap along K, k-blocks per tap
     int Nout;          // output columns (row stride of outputs / mask)

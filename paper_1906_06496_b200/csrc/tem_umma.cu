@@ -50,7 +50,7 @@ struct Cfg {
     static constexpr uint32_t A_BYTES = BM * BK * 2;
     static constexpr uint32_t B_BYTES = BN * BK * 2;
     static constexpr uint32_t STAGE_BYTES = NPL * (A_BYTES + B_BYTES);
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ + 4 * 2 * 2048;
     static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
 };
 
@@ -86,6 +86,104 @@ TEM_DEV void store16_planes(__nv_bfloat16* hi, __nv_bfloat16* lo, const float (&
     }
 }
 
+
+// ------------------------------------------------------------------ epilogue (shared)
+// Each epilogue warp owns 32 accumulator rows (its TMEM lane quarter).  Per 16-column chunk:
+// tcgen05.ld -> registers -> bias/ReLU/halo (FWD) or ReLU-mask/halo (DGRAD) or raw (WGRAD)
+// -> a 32x16 staging tile in shared memory -> one TMA bulk-tensor store (asynchronous,
+// coalesced by the TMA unit, rows >= R clipped).  Two staging buffers per warp alternate.
+constexpr uint32_t EPI_BUF = 2048;                 // 32 x 16 fp32, or hi + lo 32 x 16 bf16
+constexpr uint32_t EPI_BYTES = 4 * 2 * EPI_BUF;    // 4 warps x 2 buffers
+
+template <int MODE, int BN>
+TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_tile, int split, int q,
+                           int lane, uint8_t* stg, int& buf) {
+    const int row0 = m_tile * BM + 32 * q;
+    const int row = row0 + lane;
+    if ((MODE == FWD_ || MODE == DGRAD_) && (m_tile >= P.mtiles || row0 >= P.R)) return;
+#pragma unroll 1
+    for (int c16 = 0; c16 < BN / 16; ++c16) {
+        int gc = 0;  // global column of the store box (FWD/DGRAD: n; WGRAD: j*Cin + c)
+        if (MODE == WGRAD_) {
+            const int nl = c16 * 16;
+            const int g = n_tile * (BN / 64) + nl / 64;
+            if (P.ones_chunk && g == 3 * P.cpj) {
+                if (nl % 64 == 0) {  // column 0 of the all-ones chunk: bias-gradient partial
+                    uint32_t r[16];
+                    tmem_ld16(tq + (uint32_t)(c16 * 16), r);
+                    tmem_ld_wait();
+                    P.part[(size_t)split * P.part_stride + (size_t)P.Nout * P.NW + row] = __uint_as_float(r[0]);
+                }
+                continue;
+            }
+            if (g >= 3 * P.cpj) continue;
+            const int j = g / P.cpj, c = (g % P.cpj) * 64 + (nl % 64);
+            if (c >= P.Cin_w) continue;
+            gc = j * P.Cin_w + c;
+        } else {
+            gc = n_tile * BN + c16 * 16;
+        }
+        uint32_t r[16];
+        tmem_ld16(tq + (uint32_t)(c16 * 16), r);
+        tmem_ld_wait();
+        float v[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+        if (MODE == FWD_) {
+            const bool halo = row >= P.R || halo_row(row, P.Tp);
+            const float4* bp = reinterpret_cast<const float4*>(P.bias + gc);
+#pragma unroll
+            for (int i4 = 0; i4 < 4; ++i4) {
+                const float4 bb = __ldg(bp + i4);
+                const float bv[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float tv = v[4 * i4 + k] + bv[k];
+                    v[4 * i4 + k] = (!halo && tv > 0.f) ? tv : 0.f;
+                }
+            }
+        } else if (MODE == DGRAD_) {
+            const bool halo = row >= P.R || halo_row(row, P.Tp);
+            uint32_t mw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            if (!halo) {
+                const uint4* mk = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(P.mask) +
+                                                                 (size_t)row * P.Nout + gc);
+                const uint4 m0v = mk[0], m1v = mk[1];
+                mw[0] = m0v.x; mw[1] = m0v.y; mw[2] = m0v.z; mw[3] = m0v.w;
+                mw[4] = m1v.x; mw[5] = m1v.y; mw[6] = m1v.z; mw[7] = m1v.w;
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                v[2 * i] = __uint_as_float(mw[i] << 16) > 0.f ? v[2 * i] : 0.f;
+                v[2 * i + 1] = __uint_as_float(mw[i] & 0xFFFF0000u) > 0.f ? v[2 * i + 1] : 0.f;
+            }
+        }
+        uint8_t* sb = stg + buf * EPI_BUF;
+        if (lane == 0) bulk_wait_read<1>();  // this buffer's previous store has read its data
+        __syncwarp();
+        const bool f32 = (MODE == WGRAD_) || P.out_f32;
+        if (f32) {
+            float4* d = reinterpret_cast<float4*>(sb + lane * 64);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        } else {
+            store16_planes(reinterpret_cast<__nv_bfloat16*>(sb + lane * 32),
+                           P.out_lo ? reinterpret_cast<__nv_bfloat16*>(sb + 1024 + lane * 32) : nullptr, v);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+            if (MODE == WGRAD_) {
+                tma_store_3d(&P.out[0], sb, gc, row0, split);
+            } else {
+                tma_store_2d(&P.out[0], sb, gc, row0);
+                if (!f32 && P.out_lo) tma_store_2d(&P.out[1], sb + 1024, gc, row0);
+            }
+            bulk_commit();
+        }
+        buf ^= 1;
+    }
+}
 
 template <int MODE, int BN, int NPASS, int STAGES, int CM, int CN>
 __global__ void __launch_bounds__(NTHREADS, 1) umma_conv_kernel(const __grid_constant__ UmmaParams P) {
@@ -270,85 +368,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_conv_kernel(const __grid_con
     } else {
         // ===================== epilogue (warps 2..5) =====================
         const int q = warp & 3;  // TMEM lane quarter accessible to this warp
-        int t = 0;
+        uint8_t* stg = smem + STAGES * C_::STAGE_BYTES + 1024 + (warp - 2) * 2 * EPI_BUF;
+        int buf = 0, t = 0;
         for (int ct = cluster_id; ct < total_ct; ct += nclusters, ++t) {
             int m_tile, n_tile, split, p_begin;
             tile_coords(ct, m_tile, n_tile, split);
             const int acc = t & 1;
-            const int row = m_tile * BM + 32 * q + lane;
             mbar_wait(&tfull[acc], (t >> 1) & 1);
             tc_fence_after();
             const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN);
-#pragma unroll 1
-            for (int c16 = 0; c16 < BN / 16; ++c16) {
-                uint32_t r[16];
-                tmem_ld16(tq + (uint32_t)(c16 * 16), r);
-                tmem_ld_wait();
-                float v[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-                if (MODE == FWD_ || MODE == DGRAD_) {
-                    if (m_tile >= P.mtiles || row >= P.R) continue;
-                    const int n = n_tile * BN + c16 * 16;  // Nout is a multiple of BN
-                    const bool halo = halo_row(row, P.Tp);
-                    if (MODE == FWD_) {
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const float tv = v[i] + P.bias[n + i];
-                            v[i] = (!halo && tv > 0.f) ? tv : 0.f;
-                        }
-                    } else {
-                        uint32_t mw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                        if (!halo) {
-                            const uint4* mk = reinterpret_cast<const uint4*>(
-                                static_cast<const __nv_bfloat16*>(P.mask) + (size_t)row * P.Nout + n);
-                            const uint4 m0v = mk[0], m1v = mk[1];
-                            mw[0] = m0v.x; mw[1] = m0v.y; mw[2] = m0v.z; mw[3] = m0v.w;
-                            mw[4] = m1v.x; mw[5] = m1v.y; mw[6] = m1v.z; mw[7] = m1v.w;
-                        }
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            v[2 * i] = __uint_as_float(mw[i] << 16) > 0.f ? v[2 * i] : 0.f;
-                            v[2 * i + 1] = __uint_as_float(mw[i] & 0xFFFF0000u) > 0.f ? v[2 * i + 1] : 0.f;
-                        }
-                    }
-                    if (P.out_f32) {
-                        float4* d = reinterpret_cast<float4*>(static_cast<float*>(P.out_hi) + (size_t)row * P.Nout + n);
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-                    } else {
-                        __nv_bfloat16* hi = static_cast<__nv_bfloat16*>(P.out_hi) + (size_t)row * P.Nout + n;
-                        __nv_bfloat16* lo = P.out_lo ? static_cast<__nv_bfloat16*>(P.out_lo) + (size_t)row * P.Nout + n
-                                                     : nullptr;
-                        store16_planes(hi, lo, v);
-                    }
-                } else {  // WGRAD partial: row = o, columns -> (j, c)
-                    const int nl = c16 * 16;
-                    const int g = n_tile * (BN / 64) + nl / 64;
-                    float* part = P.part + (size_t)split * P.part_stride;
-                    if (P.ones_chunk && g == 3 * P.cpj) {
-                        if (nl % 64 == 0) part[(size_t)P.Nout * P.NW + row] = v[0];  // bias gradient partial
-                        continue;
-                    }
-                    if (g >= 3 * P.cpj) continue;
-                    const int j = g / P.cpj, c = (g % P.cpj) * 64 + (nl % 64);
-                    if (c >= P.Cin_w) continue;
-                    float* dst = part + (size_t)row * P.NW + (size_t)j * P.Cin_w + c;
-                    if (c + 16 <= P.Cin_w) {
-#pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            if (c + i < P.Cin_w) dst[i] = v[i];
-                    }
-                }
-            }
+            epilogue_tile<MODE, BN>(P, tq, m_tile, n_tile, split, q, lane, stg, buf);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_local(&tempty[acc]);  // buffer free for tile t + 2
         }
+        if (lane == 0) bulk_wait_all();
     }
     tc_fence_before();
     __syncthreads();
@@ -372,7 +406,7 @@ struct CfgPair {
     static constexpr uint32_t A_BYTES = BM * BK * 2;            // this CTA's 128 rows
     static constexpr uint32_t B_BYTES = (BN / 2) * BK * 2;      // this CTA's half of B
     static constexpr uint32_t STAGE_BYTES = NPL * (A_BYTES + B_BYTES);
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 1024 + 4 * 2 * 2048;
     static constexpr int TMEM_COLS = 2 * BN;
 };
 
@@ -534,86 +568,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_pair_kernel(const __grid_con
         // ===================== epilogue (warps 2..5, both CTAs) =====================
         const int q = warp & 3;
         const uint32_t tempty_leader = mapa_shared(&tempty[0], 0);
-        int t = 0;
+        uint8_t* stg = smem + STAGES * C_::STAGE_BYTES + 1024 + (warp - 2) * 2 * EPI_BUF;
+        int buf = 0, t = 0;
         for (int ct = pair_id; ct < total; ct += npairs, ++t) {
             int mp, n_tile, split, p_begin;
             tile_coords(ct, mp, n_tile, split);
             const int acc = t & 1;
             const int m_tile = mp * 2 + (int)rank;  // 128-row tile index of this CTA
-            const int row = m_tile * BM + 32 * q + lane;
             mbar_wait(&tfull[acc], (t >> 1) & 1);
             tc_fence_after();
             const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN);
-#pragma unroll 1
-            for (int c16 = 0; c16 < BN / 16; ++c16) {
-                uint32_t r[16];
-                tmem_ld16(tq + (uint32_t)(c16 * 16), r);
-                tmem_ld_wait();
-                float v[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-                if (MODE == FWD_ || MODE == DGRAD_) {
-                    if (m_tile >= P.mtiles || row >= P.R) continue;
-                    const int n = n_tile * BN + c16 * 16;
-                    const bool halo = halo_row(row, P.Tp);
-                    if (MODE == FWD_) {
-#pragma unroll
-                        for (int i = 0; i < 16; ++i) {
-                            const float tv = v[i] + P.bias[n + i];
-                            v[i] = (!halo && tv > 0.f) ? tv : 0.f;
-                        }
-                    } else {
-                        uint32_t mw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                        if (!halo) {
-                            const uint4* mk = reinterpret_cast<const uint4*>(
-                                static_cast<const __nv_bfloat16*>(P.mask) + (size_t)row * P.Nout + n);
-                            const uint4 m0v = mk[0], m1v = mk[1];
-                            mw[0] = m0v.x; mw[1] = m0v.y; mw[2] = m0v.z; mw[3] = m0v.w;
-                            mw[4] = m1v.x; mw[5] = m1v.y; mw[6] = m1v.z; mw[7] = m1v.w;
-                        }
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) {
-                            v[2 * i] = __uint_as_float(mw[i] << 16) > 0.f ? v[2 * i] : 0.f;
-                            v[2 * i + 1] = __uint_as_float(mw[i] & 0xFFFF0000u) > 0.f ? v[2 * i + 1] : 0.f;
-                        }
-                    }
-                    if (P.out_f32) {
-                        float4* d = reinterpret_cast<float4*>(static_cast<float*>(P.out_hi) + (size_t)row * P.Nout + n);
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-                    } else {
-                        __nv_bfloat16* hi = static_cast<__nv_bfloat16*>(P.out_hi) + (size_t)row * P.Nout + n;
-                        __nv_bfloat16* lo = P.out_lo ? static_cast<__nv_bfloat16*>(P.out_lo) + (size_t)row * P.Nout + n
-                                                     : nullptr;
-                        store16_planes(hi, lo, v);
-                    }
-                } else {  // WGRAD partial: row = o, columns -> (j, c)
-                    const int nl = c16 * 16;
-                    const int g = n_tile * (BN / 64) + nl / 64;
-                    float* part = P.part + (size_t)split * P.part_stride;
-                    if (P.ones_chunk && g == 3 * P.cpj) {
-                        if (nl % 64 == 0) part[(size_t)P.Nout * P.NW + row] = v[0];
-                        continue;
-                    }
-                    if (g >= 3 * P.cpj) continue;
-                    const int j = g / P.cpj, c = (g % P.cpj) * 64 + (nl % 64);
-                    if (c >= P.Cin_w) continue;
-                    float* dst = part + (size_t)row * P.NW + (size_t)j * P.Cin_w + c;
-                    if (c + 16 <= P.Cin_w) {
-#pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            reinterpret_cast<float4*>(dst)[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-                    } else {
-#pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            if (c + i < P.Cin_w) dst[i] = v[i];
-                    }
-                }
-            }
+            epilogue_tile<MODE, BN>(P, tq, m_tile, n_tile, split, q, lane, stg, buf);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(tempty_leader + acc * 8);  // free the buffer (leader's barrier)
         }
+        if (lane == 0) bulk_wait_all();
     }
     tc_fence_before();
     __syncthreads();
@@ -736,6 +706,32 @@ bool map_w_mn(CUtensorMap* m, const void* base, uint64_t C, uint32_t box_rows) {
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Output (store) maps: row-major [outer][inner] of bf16 or fp32, box {16, 32}, no swizzle.
+bool map_store2d(CUtensorMap* m, const void* base, bool f32, uint64_t inner, uint64_t outer) {
+    auto fn = encode_fn();
+    if (!fn || !base) return false;
+    const uint64_t es = f32 ? 4 : 2;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {inner * es};
+    cuuint32_t box[2] = {16, 32};
+    cuuint32_t el[2] = {1, 1};
+    return fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+              dims, strides, box, el, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+// Split-K partials [S][rows][NW] fp32 with split stride `split_elems`, box {16, 32, 1}.
+bool map_store_part(CUtensorMap* m, float* base, uint64_t NW, uint64_t rows, uint64_t S, uint64_t split_elems) {
+    auto fn = encode_fn();
+    if (!fn || !base) return false;
+    cuuint64_t dims[3] = {NW, rows, S};
+    cuuint64_t strides[2] = {NW * 4, split_elems * 4};
+    cuuint32_t box[3] = {16, 32, 1};
+    cuuint32_t el[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, base, dims, strides, box, el, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
 }
 
 // Launch a persistent cluster grid: as many clusters as fit (<= cluster tiles).
@@ -952,6 +948,14 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     P.wgrad1.part_stride = (int64_t)g.C * 3 * g.Cin + g.C;
     P.wgrad1.ones_chunk = 1;
     ok &= map2d(&P.wgrad1.ones, b.ones, 128, R, brW);
+    // epilogue store maps
+    ok &= map_store2d(&P.conv1.out[0], b.h1, false, g.C, R);
+    if (b.h1_lo) ok &= map_store2d(&P.conv1.out[1], b.h1_lo, false, g.C, R);
+    ok &= map_store2d(&P.conv2.out[0], b.h2, true, g.C, R);
+    ok &= map_store2d(&P.dgrad.out[0], b.dA1, false, g.C, R);
+    if (b.dA1_lo) ok &= map_store2d(&P.dgrad.out[1], b.dA1_lo, false, g.C, R);
+    ok &= map_store_part(&P.wgrad2.out[0], b.wpart2, 3 * (uint64_t)g.C, g.C, P.S, P.wgrad2.part_stride);
+    ok &= map_store_part(&P.wgrad1.out[0], b.wpart, 3 * (uint64_t)g.Cin, g.C, P.S, P.wgrad1.part_stride);
     // cluster shapes must tile the tile grids
     ok &= (P.conv1.ntiles % cf.cn == 0) && (P.wgrad1.mtiles % cw.cm == 0);
     ok &= (P.wgrad1.ntiles % cw.cn == 0) && (P.wgrad2.ntiles % cw.cn == 0);
