@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
     const float* __restrict__ h2, const float* __restrict__ W3, const float* __restrict__ b3,
     const float* __restrict__ labels, float lam0, float lam1, float lam2, TOp* __restrict__ dA2,
     TOp* __restrict__ dA2_lo, float* __restrict__ z_out, float* __restrict__ part, int B, int Tn, int C,
-    int RPC) {
+    int RPC, const float* __restrict__ zpart, int nzp) {
     extern __shared__ __align__(16) float sm[];
     float* sW3 = sm;           // [3][C]
     float* sdz = sm + 3 * C;   // [RPC][3] dz of this CTA's rows (0 on halo rows)
@@ -64,12 +64,12 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
     float hn[16];  // software pipeline: the next row of this warp is in flight
 #pragma unroll
     for (int q = 0; q < 16; ++q)
-        hn[q] = (q < NQ && p0 + warp < p1) ? h2[(size_t)(p0 + warp) * C + lane + 32 * q] : 0.f;
+        hn[q] = (nzp == 0 && q < NQ && p0 + warp < p1) ? h2[(size_t)(p0 + warp) * C + lane + 32 * q] : 0.f;
     for (int p = p0 + warp; p < p1; p += HEAD_WARPS) {
         float h[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) h[q] = hn[q];
-        {
+        if (nzp == 0) {
             const int pn = p + HEAD_WARPS;
 #pragma unroll
             for (int q = 0; q < 16; ++q) hn[q] = (q < NQ && pn < p1) ? h2[(size_t)pn * C + lane + 32 * q] : 0.f;
@@ -82,15 +82,24 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
         }
         const int t = tp - 1, k = v - v0;
         float z[3];
+        if (nzp > 0) {  // logits from the conv2 epilogue's partial sums (fixed order over tiles)
 #pragma unroll
-        for (int o = 0; o < 3; ++o) {
-            float s = 0.f;
+            for (int o = 0; o < 3; ++o) {
+                float s = zpart[(size_t)p * 3 + o];
+                for (int kk = 1; kk < nzp; ++kk) s += zpart[((size_t)kk * R + p) * 3 + o];
+                z[o] = s + b3[o];
+            }
+        } else {
 #pragma unroll
-            for (int q = 0; q < 16; ++q)
-                if (q < NQ) s = fmaf(sW3[o * C + lane + 32 * q], h[q], s);
+            for (int o = 0; o < 3; ++o) {
+                float s = 0.f;
 #pragma unroll
-            for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-            z[o] = s + b3[o];
+                for (int q = 0; q < 16; ++q)
+                    if (q < NQ) s = fmaf(sW3[o * C + lane + 32 * q], h[q], s);
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+                z[o] = s + b3[o];
+            }
         }
         float dz[3];
 #pragma unroll
@@ -250,12 +259,12 @@ cudaError_t launch_head_rows(const Geom& g, const RankBufs& b, const float* labe
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
         k<<<P, 256, hsm, s>>>(b.h2, b.params + g.off_W3, b.params + g.off_b3, labels, lam[0], lam[1], lam[2],
                               static_cast<__nv_bfloat16*>(b.dA2), static_cast<__nv_bfloat16*>(b.dA2_lo), b.z,
-                              b.headpart, g.B, g.T, g.C, rpc);
+                              b.headpart, g.B, g.T, g.C, rpc, b.zpart, b.nzpart);
     } else {
         auto k = head_rows_kernel<float>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
         k<<<P, 256, hsm, s>>>(b.h2, b.params + g.off_W3, b.params + g.off_b3, labels, lam[0], lam[1], lam[2],
-                              static_cast<float*>(b.dA2), nullptr, b.z, b.headpart, g.B, g.T, g.C, rpc);
+                              static_cast<float*>(b.dA2), nullptr, b.z, b.headpart, g.B, g.T, g.C, rpc, nullptr, 0);
     }
     rec.end(SLOT_HEAD);
     ++*n;

@@ -52,6 +52,8 @@ struct RankBufs {
     unsigned* counter;    // last-CTA ticket of the head reduction (self-resetting)
     float* bpart;         // [m-tiles][C] conv1 bias-gradient partials (tcgen05 DGRAD epilogue)
     void* ones;           // [R][128] bf16 ones/zeros operand for the bias-gradient column
+    float* zpart;         // [C/BN][R][3] partial logits from the conv2 epilogue (tcgen05), or nullptr
+    int nzpart;           // number of partial-logit planes (C / conv2 tile width); 0 = head computes z
     float* wpart;         // [S][max(C*3*Cin + C, C*3*C + C)] split-K partials (conv1 wgrad; SIMT: both)
     float* wpart2;        // [S][C*3*C + C] split-K partials of the tcgen05 conv2 wgrad
     int64_t* stepctr;     // step counter for NONFINITE reporting
@@ -74,6 +76,8 @@ struct UmmaParams {
     void* out_lo;      // residual plane or nullptr
     int out_f32;
     float* bsum;       // DGRAD: per-m-tile column sums of the stored dA1 [m-tiles][Nout] or nullptr
+    const float* w3;   // FWD conv2: W3 [3][Nout] (fp32) for the fused partial logits
+    float* zpart;      // FWD conv2: [Nout/BN][R][3] partial logits, or nullptr
     float* part;       // WGRAD split partials
     int64_t part_stride;
     int NW, Cin_w, cpj;  // WGRAD: 3*Cin, Cin, 64-wide chunks per tap

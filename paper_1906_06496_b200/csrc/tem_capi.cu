@@ -31,7 +31,7 @@ struct HeapLayout {
 
 struct WsLayout {
     size_t xp, h1, h2, dA2, dA1, xp_lo, h1_lo, dA2_lo, dA1_lo, z, grad, headpart, headlvl1, counter, bpart, wpart, wpart2, shadow,
-        shadow_lo, ones, epochs, stepctr, xstage, labstage, lossstage, per_rank;
+        shadow_lo, ones, zpart, epochs, stepctr, xstage, labstage, lossstage, per_rank;
 };
 
 bool cfg_valid(const tem_config* c) {
@@ -144,6 +144,7 @@ WsLayout ws_layout(const tem_config* c) {
     w.shadow = take(g.op_bf16 ? (size_t)g.Kpad * 2 : 0);
     w.shadow_lo = take(lo * (size_t)g.Kpad * 2);
     w.ones = take(g.path == PATH_UMMA ? (size_t)g.R * 128 * 2 : 0);
+    w.zpart = take(g.path == PATH_UMMA ? (size_t)(g.C / 64) * g.R * 3 * 4 : 0);
     w.epochs = take((size_t)kMaxChannels * 4);
     w.stepctr = take(8);
     w.xstage = take((size_t)g.B * g.T * g.Cin * xsz);
@@ -327,6 +328,8 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
         b.counter = (unsigned*)(base + wl.counter);
         b.bpart = (float*)(base + wl.bpart);
         b.ones = c->g.path == PATH_UMMA ? base + wl.ones : nullptr;
+        b.zpart = c->g.path == PATH_UMMA ? (float*)(base + wl.zpart) : nullptr;
+        b.nzpart = 0;  // set by the tcgen05 plan
         b.wpart = (float*)(base + wl.wpart);
         b.wpart2 = (float*)(base + wl.wpart2);
         b.stepctr = (int64_t*)(base + wl.stepctr);
@@ -345,6 +348,7 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
         if (e == cudaSuccess && c->g.path == PATH_UMMA) {
             c->plan[l] = new (std::nothrow) UmmaPlan();
             if (!c->plan[l] || !umma_plan(c->g, b, c->plan[l])) e = cudaErrorInvalidValue;
+            else b.nzpart = c->plan[l]->conv2.ntiles;
         }
         if (e != cudaSuccess) {
             for (int q = 0; q <= l; ++q) umma_plan_destroy(c->plan[q]);

@@ -101,6 +101,7 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
     const int row0 = m_tile * BM + 32 * q;
     const int row = row0 + lane;
     if ((MODE == FWD_ || MODE == DGRAD_) && (m_tile >= P.mtiles || row0 >= P.R)) return;
+    float zp0 = 0.f, zp1 = 0.f, zp2 = 0.f;  // FWD conv2: partial logits W3 . h2 over this tile's columns
 #pragma unroll 1
     for (int c16 = 0; c16 < BN / 16; ++c16) {
         int gc = 0;  // global column of the store box (FWD/DGRAD: n; WGRAD: j*Cin + c)
@@ -140,6 +141,17 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
                 for (int k = 0; k < 4; ++k) {
                     const float tv = v[4 * i4 + k] + bv[k];
                     v[4 * i4 + k] = (!halo && tv > 0.f) ? tv : 0.f;
+                }
+            }
+            if (P.zpart) {  // head row a3, fused: z_o += sum_c W3[o][c] h2[c] (fixed order)
+                const float4* w = reinterpret_cast<const float4*>(P.w3 + gc);
+#pragma unroll
+                for (int i4 = 0; i4 < 4; ++i4) {
+                    const float4 a = __ldg(w + i4), b = __ldg(w + P.Nout / 4 + i4), c = __ldg(w + P.Nout / 2 + i4);
+                    const float* hv = v + 4 * i4;
+                    zp0 = fmaf(a.x, hv[0], zp0); zp0 = fmaf(a.y, hv[1], zp0); zp0 = fmaf(a.z, hv[2], zp0); zp0 = fmaf(a.w, hv[3], zp0);
+                    zp1 = fmaf(b.x, hv[0], zp1); zp1 = fmaf(b.y, hv[1], zp1); zp1 = fmaf(b.z, hv[2], zp1); zp1 = fmaf(b.w, hv[3], zp1);
+                    zp2 = fmaf(c.x, hv[0], zp2); zp2 = fmaf(c.y, hv[1], zp2); zp2 = fmaf(c.z, hv[2], zp2); zp2 = fmaf(c.w, hv[3], zp2);
                 }
             }
         } else if (MODE == DGRAD_) {
@@ -182,6 +194,12 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
             bulk_commit();
         }
         buf ^= 1;
+    }
+    if (MODE == FWD_ && P.zpart && row < P.R) {
+        float* zp = P.zpart + ((size_t)n_tile * P.R + row) * 3;
+        zp[0] = zp0;
+        zp[1] = zp1;
+        zp[2] = zp2;
     }
 }
 
@@ -916,6 +934,8 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     P.conv2.bias = b.params + g.off_b2;
     P.conv2.out_hi = b.h2;
     P.conv2.out_f32 = 1;
+    P.conv2.w3 = b.params + g.off_W3;
+    P.conv2.zpart = b.zpart;  // [C/BN][R][3] partial logits for the head
     common(P.dgrad);
     P.dgrad.Kc = g.C;
     P.dgrad.cpb = g.C / umma::BK;
