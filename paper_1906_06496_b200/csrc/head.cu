@@ -132,45 +132,98 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
     }
     __syncthreads();
     // ---- phase 2: column-parallel over the CTA's rows (h2 rows are L2-resident now) ----
-    // dA2 = 1[h2>0] W3^T dz (halo rows: dz = 0 -> 0); dW3 += dz h2; db2 += stored dA2
+    // dA2 = 1[h2>0] W3^T dz (halo rows: dz = 0 -> 0); dW3 += dz h2; db2 += stored dA2.
+    // Thread = 4 consecutive columns (float4 loads) x one of RP row phases; the RP phase
+    // partials are combined in a fixed order through shared memory.
     float* dst = part + (size_t)blockIdx.x * (4 * C + 6);
-    for (int c = tid; c < C; c += blockDim.x) {
-        const float w0 = sW3[c], w1 = sW3[C + c], w2 = sW3[2 * C + c];
-        float a0 = 0.f, a1 = 0.f, a2 = 0.f, bsum = 0.f;
-        constexpr int U = 8;  // rows per batch: U independent h2 loads in flight per thread
-        for (int pb = p0; pb < p1; pb += U) {
-            float hv[U];
+    const int CG = C / 4;                 // column groups (<= 128)
+    const int RP = blockDim.x / CG;       // row phases (>= 2)
+    const int cg = tid % CG, rp = tid / CG;
+    const int c0 = 4 * cg;
+    float acc[3][4], bs[4];
 #pragma unroll
-            for (int u = 0; u < U; ++u) hv[u] = (pb + u < p1) ? h2[(size_t)(pb + u) * C + c] : 0.f;
+    for (int i = 0; i < 4; ++i) {
+        bs[i] = 0.f;
+        acc[0][i] = acc[1][i] = acc[2][i] = 0.f;
+    }
+    if (rp < RP) {
+        float w[3][4];
+#pragma unroll
+        for (int o = 0; o < 3; ++o)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) w[o][i] = sW3[o * C + c0 + i];
+        constexpr int U = 4;
+        for (int pb = p0 + rp; pb < p1; pb += U * RP) {
+            float4 hv[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int p = pb + u;
+                const int p = pb + u * RP;
+                hv[u] = p < p1 ? *reinterpret_cast<const float4*>(h2 + (size_t)p * C + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int p = pb + u * RP;
                 if (p >= p1) break;
                 const float* dzr = sdz + (p - p0) * 3;
                 const float d0 = dzr[0], d1 = dzr[1], d2 = dzr[2];
-                float d = w0 * d0;
-                d = fmaf(w1, d1, d);
-                d = fmaf(w2, d2, d);
-                const float dv = hv[u] > 0.f ? d : 0.f;
-                const TOp dh = from_f<TOp>(dv);
-                float stored = to_f(dh);
-                dA2[(size_t)p * C + c] = dh;
-                if (dA2_lo) {
-                    const TOp dl = from_f<TOp>(dv - stored);
-                    dA2_lo[(size_t)p * C + c] = dl;
-                    stored += to_f(dl);
+                const float h[4] = {hv[u].x, hv[u].y, hv[u].z, hv[u].w};
+                float st[4];
+                TOp dh[4], dl[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    float d = w[0][i] * d0;
+                    d = fmaf(w[1][i], d1, d);
+                    d = fmaf(w[2][i], d2, d);
+                    const float dv = h[i] > 0.f ? d : 0.f;
+                    dh[i] = from_f<TOp>(dv);
+                    st[i] = to_f(dh[i]);
+                    if (dA2_lo) {
+                        dl[i] = from_f<TOp>(dv - st[i]);
+                        st[i] += to_f(dl[i]);
+                    }
+                    bs[i] += st[i];
+                    acc[0][i] = fmaf(d0, h[i], acc[0][i]);
+                    acc[1][i] = fmaf(d1, h[i], acc[1][i]);
+                    acc[2][i] = fmaf(d2, h[i], acc[2][i]);
                 }
-                bsum += stored;
-                a0 = fmaf(d0, hv[u], a0);
-                a1 = fmaf(d1, hv[u], a1);
-                a2 = fmaf(d2, hv[u], a2);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    dA2[(size_t)p * C + c0 + i] = dh[i];
+                    if (dA2_lo) dA2_lo[(size_t)p * C + c0 + i] = dl[i];
+                }
             }
         }
+    }
+    // combine the row phases in order: smem reuse of sW3 region is unsafe (still read), use sdz tail
+    __syncthreads();
+    float* red = sdz;  // [RP][CG][16] floats: phase 1 data (dz) is dead after the sync below
+    __syncthreads();
+    if (rp < RP) {
+        float* r = red + ((size_t)rp * CG + cg) * 16;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            r[i] = acc[0][i];
+            r[4 + i] = acc[1][i];
+            r[8 + i] = acc[2][i];
+            r[12 + i] = bs[i];
+        }
+    }
+    __syncthreads();
+    if (rp == 0) {
+        float sum[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) sum[k] = red[(size_t)cg * 16 + k];
+        for (int ph = 1; ph < RP; ++ph)
+#pragma unroll
+            for (int k = 0; k < 16; ++k) sum[k] += red[((size_t)ph * CG + cg) * 16 + k];
         // partial row layout: [dW3 (3C)][db3 (3)][L (3)][db2 (C)]
-        dst[c] = a0;
-        dst[C + c] = a1;
-        dst[2 * C + c] = a2;
-        dst[3 * C + 6 + c] = bsum;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            dst[c0 + i] = sum[i];
+            dst[C + c0 + i] = sum[4 + i];
+            dst[2 * C + c0 + i] = sum[8 + i];
+            dst[3 * C + 6 + c0 + i] = sum[12 + i];
+        }
     }
     if (tid < 3) {
         float l = s_misc[0][tid], d = s_misc[0][3 + tid];
@@ -251,7 +304,8 @@ cudaError_t launch_head_rows(const Geom& g, const RankBufs& b, const float* labe
                              const EvRec& rec, cudaStream_t s, int* n) {
     const int P = head_ctas(g);
     const int rpc = head_rows_per_cta(g);
-    const size_t hsm = (size_t)(3 * g.C + 3 * rpc) * sizeof(float);
+    const size_t red = (size_t)256 * 16;  // phase-2 row-phase reduction [RP][C/4][16]
+    const size_t hsm = (size_t)(3 * g.C + (3 * rpc > (int)red ? 3 * rpc : red)) * sizeof(float);
     if (P == 0) return cudaSuccess;
     rec.begin(SLOT_HEAD);
     if (g.op_bf16) {

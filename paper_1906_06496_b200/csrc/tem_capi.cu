@@ -348,7 +348,7 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
         if (e == cudaSuccess && c->g.path == PATH_UMMA) {
             c->plan[l] = new (std::nothrow) UmmaPlan();
             if (!c->plan[l] || !umma_plan(c->g, b, c->plan[l])) e = cudaErrorInvalidValue;
-            else b.nzpart = c->plan[l]->conv2.ntiles;
+            else b.nzpart = c->plan[l]->conv2.zpart ? c->plan[l]->conv2.ntiles : 0;
         }
         if (e != cudaSuccess) {
             for (int q = 0; q <= l; ++q) umma_plan_destroy(c->plan[q]);
