@@ -57,51 +57,13 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
         s_an[k][o] = (float)Tn / (float)(ln > 1 ? ln : 1);
     }
     __syncthreads();
-    // ---- phase 1: one row per warp: z, loss terms, dz -> smem ----
+    // ---- phase 1: z, loss terms, dz -> smem ----
     const int NQ = C / 32;  // <= 16
     float lsum[3] = {0.f, 0.f, 0.f}, dbs[3] = {0.f, 0.f, 0.f};
     const float inv_bt = 1.0f / ((float)B * (float)Tn);
-    float hn[16];  // software pipeline: the next row of this warp is in flight
-#pragma unroll
-    for (int q = 0; q < 16; ++q)
-        hn[q] = (nzp == 0 && q < NQ && p0 + warp < p1) ? h2[(size_t)(p0 + warp) * C + lane + 32 * q] : 0.f;
-    for (int p = p0 + warp; p < p1; p += HEAD_WARPS) {
-        float h[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) h[q] = hn[q];
-        if (nzp == 0) {
-            const int pn = p + HEAD_WARPS;
-#pragma unroll
-            for (int q = 0; q < 16; ++q) hn[q] = (q < NQ && pn < p1) ? h2[(size_t)pn * C + lane + 32 * q] : 0.f;
-        }
-        const int v = p / Tp, tp = p - v * Tp;
+    auto row_loss = [&](int p, const float (&z)[3]) {  // rows a3/a4 for one snippet row
+        const int v = p / Tp, t = p - v * Tp - 1, k = v - v0;
         float* dzr = sdz + (p - p0) * 3;
-        if (tp == 0 || tp == Tp - 1) {
-            if (lane < 3) dzr[lane] = 0.f;
-            continue;
-        }
-        const int t = tp - 1, k = v - v0;
-        float z[3];
-        if (nzp > 0) {  // logits from the conv2 epilogue's partial sums (fixed order over tiles)
-#pragma unroll
-            for (int o = 0; o < 3; ++o) {
-                float s = zpart[(size_t)p * 3 + o];
-                for (int kk = 1; kk < nzp; ++kk) s += zpart[((size_t)kk * R + p) * 3 + o];
-                z[o] = s + b3[o];
-            }
-        } else {
-#pragma unroll
-            for (int o = 0; o < 3; ++o) {
-                float s = 0.f;
-#pragma unroll
-                for (int q = 0; q < 16; ++q)
-                    if (q < NQ) s = fmaf(sW3[o * C + lane + 32 * q], h[q], s);
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-                z[o] = s + b3[o];
-            }
-        }
-        float dz[3];
 #pragma unroll
         for (int o = 0; o < 3; ++o) {
             const float g = labels[((size_t)v * 3 + o) * Tn + t];
@@ -110,17 +72,60 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
             const float logp = -softplusf(-z[o]), log1mp = -softplusf(z[o]);
             lsum[o] += ap * bt * logp + an * (1.f - bt) * log1mp;
             const float pr = 1.f / (1.f + expf(-z[o]));
-            dz[o] = lam[o] * inv_bt * (an * (1.f - bt) * pr - ap * bt * (1.f - pr));
-            dbs[o] += dz[o];
+            const float dz = lam[o] * inv_bt * (an * (1.f - bt) * pr - ap * bt * (1.f - pr));
+            dbs[o] += dz;
+            dzr[o] = dz;
+            z_out[((size_t)v * Tn + t) * 3 + o] = z[o];
         }
-        if (lane == 0) {
-            float* zo = z_out + ((size_t)v * Tn + t) * 3;
-            zo[0] = z[0];
-            zo[1] = z[1];
-            zo[2] = z[2];
-            dzr[0] = dz[0];
-            dzr[1] = dz[1];
-            dzr[2] = dz[2];
+    };
+    if (nzp > 0) {
+        // logits precomputed by the conv2 epilogue: one row per THREAD (no redundant lanes)
+        for (int p = p0 + tid; p < p1; p += blockDim.x) {
+            const int tp = p % Tp;
+            if (tp == 0 || tp == Tp - 1) {
+                sdz[(p - p0) * 3] = sdz[(p - p0) * 3 + 1] = sdz[(p - p0) * 3 + 2] = 0.f;
+                continue;
+            }
+            float z[3];
+#pragma unroll
+            for (int o = 0; o < 3; ++o) {
+                float sz = zpart[(size_t)p * 3 + o];
+                for (int kk = 1; kk < nzp; ++kk) sz += zpart[((size_t)kk * R + p) * 3 + o];
+                z[o] = sz + b3[o];
+            }
+            row_loss(p, z);
+        }
+        // warp-level fixed-order reduction of the per-thread loss / db3 sums
+#pragma unroll
+        for (int o = 0; o < 3; ++o)
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                lsum[o] += __shfl_xor_sync(0xffffffffu, lsum[o], off);
+                dbs[o] += __shfl_xor_sync(0xffffffffu, dbs[o], off);
+            }
+    } else {
+        // one row per warp: z = W3 . h2 by a warp reduction, then the row's loss (lanes redundant)
+        for (int p = p0 + warp; p < p1; p += HEAD_WARPS) {
+            const int tp = p % Tp;
+            if (tp == 0 || tp == Tp - 1) {
+                if (lane < 3) sdz[(p - p0) * 3 + lane] = 0.f;
+                continue;
+            }
+            float h[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) h[q] = (q < NQ) ? h2[(size_t)p * C + lane + 32 * q] : 0.f;
+            float z[3];
+#pragma unroll
+            for (int o = 0; o < 3; ++o) {
+                float sz = 0.f;
+#pragma unroll
+                for (int q = 0; q < 16; ++q)
+                    if (q < NQ) sz = fmaf(sW3[o * C + lane + 32 * q], h[q], sz);
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) sz += __shfl_xor_sync(0xffffffffu, sz, off);
+                z[o] = sz + b3[o];
+            }
+            if (lane == 0) row_loss(p, z);
         }
     }
     if (lane == 0) {

@@ -50,7 +50,8 @@ struct Cfg {
     static constexpr uint32_t A_BYTES = BM * BK * 2;
     static constexpr uint32_t B_BYTES = BN * BK * 2;
     static constexpr uint32_t STAGE_BYTES = NPL * (A_BYTES + B_BYTES);
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ + 4 * 2 * 2048;
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ + 4 * 2 * 2048 +
+                                     3 * 512 * 4 /*W3*/;
     static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
 };
 
@@ -95,9 +96,19 @@ TEM_DEV void store16_planes(__nv_bfloat16* hi, __nv_bfloat16* lo, const float (&
 constexpr uint32_t EPI_BUF = 2048;                 // 32 x 16 fp32, or hi + lo 32 x 16 bf16
 constexpr uint32_t EPI_BYTES = 4 * 2 * EPI_BUF;    // 4 warps x 2 buffers
 
+constexpr uint32_t W3_BYTES = 3 * 512 * 4;       // W3 copy for the fused conv2 logits (C <= 512)
+
+// Epilogue warps copy W3 into shared memory (conv2 FWD with fused logits only).
+TEM_DEV void load_w3_smem(const UmmaParams& P, float* sw3, int et) {
+    if (P.zpart) {
+        for (int i = et; i < 3 * P.Nout; i += 128) sw3[i] = P.w3[i];
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+}
+
 template <int MODE, int BN>
 TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_tile, int split, int q,
-                           int lane, uint8_t* stg, int& buf) {
+                           int lane, uint8_t* stg, int& buf, const float* sw3) {
     const int row0 = m_tile * BM + 32 * q;
     const int row = row0 + lane;
     if ((MODE == FWD_ || MODE == DGRAD_) && (m_tile >= P.mtiles || row0 >= P.R)) return;
@@ -144,10 +155,10 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
                 }
             }
             if (P.zpart) {  // head row a3, fused: z_o += sum_c W3[o][c] h2[c] (fixed order)
-                const float4* w = reinterpret_cast<const float4*>(P.w3 + gc);
+                const float4* w = reinterpret_cast<const float4*>(sw3 + gc);
 #pragma unroll
                 for (int i4 = 0; i4 < 4; ++i4) {
-                    const float4 a = __ldg(w + i4), b = __ldg(w + P.Nout / 4 + i4), c = __ldg(w + P.Nout / 2 + i4);
+                    const float4 a = w[i4], b = w[P.Nout / 4 + i4], c = w[P.Nout / 2 + i4];
                     const float* hv = v + 4 * i4;
                     zp0 = fmaf(a.x, hv[0], zp0); zp0 = fmaf(a.y, hv[1], zp0); zp0 = fmaf(a.z, hv[2], zp0); zp0 = fmaf(a.w, hv[3], zp0);
                     zp1 = fmaf(b.x, hv[0], zp1); zp1 = fmaf(b.y, hv[1], zp1); zp1 = fmaf(b.z, hv[2], zp1); zp1 = fmaf(b.w, hv[3], zp1);
@@ -387,6 +398,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_conv_kernel(const __grid_con
         // ===================== epilogue (warps 2..5) =====================
         const int q = warp & 3;  // TMEM lane quarter accessible to this warp
         uint8_t* stg = smem + STAGES * C_::STAGE_BYTES + 1024 + (warp - 2) * 2 * EPI_BUF;
+        float* sw3 = reinterpret_cast<float*>(smem + STAGES * C_::STAGE_BYTES + 1024 + EPI_BYTES);
+        if (MODE == FWD_) load_w3_smem(P, sw3, threadIdx.x - 64);
         int buf = 0, t = 0;
         for (int ct = cluster_id; ct < total_ct; ct += nclusters, ++t) {
             int m_tile, n_tile, split, p_begin;
@@ -395,7 +408,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_conv_kernel(const __grid_con
             mbar_wait(&tfull[acc], (t >> 1) & 1);
             tc_fence_after();
             const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN);
-            epilogue_tile<MODE, BN>(P, tq, m_tile, n_tile, split, q, lane, stg, buf);
+            epilogue_tile<MODE, BN>(P, tq, m_tile, n_tile, split, q, lane, stg, buf, sw3);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_local(&tempty[acc]);  // buffer free for tile t + 2
@@ -424,7 +437,7 @@ struct CfgPair {
     static constexpr uint32_t A_BYTES = BM * BK * 2;            // this CTA's 128 rows
     static constexpr uint32_t B_BYTES = (BN / 2) * BK * 2;      // this CTA's half of B
     static constexpr uint32_t STAGE_BYTES = NPL * (A_BYTES + B_BYTES);
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 1024 + 4 * 2 * 2048;
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 1024 + 4 * 2 * 2048 + 3 * 512 * 4;
     static constexpr int TMEM_COLS = 2 * BN;
 };
 
@@ -587,6 +600,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_pair_kernel(const __grid_con
         const int q = warp & 3;
         const uint32_t tempty_leader = mapa_shared(&tempty[0], 0);
         uint8_t* stg = smem + STAGES * C_::STAGE_BYTES + 1024 + (warp - 2) * 2 * EPI_BUF;
+        float* sw3 = reinterpret_cast<float*>(smem + STAGES * C_::STAGE_BYTES + 1024 + EPI_BYTES);
+        if (MODE == FWD_) load_w3_smem(P, sw3, threadIdx.x - 64);
         int buf = 0, t = 0;
         for (int ct = pair_id; ct < total; ct += npairs, ++t) {
             int mp, n_tile, split, p_begin;
@@ -596,7 +611,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_pair_kernel(const __grid_con
             mbar_wait(&tfull[acc], (t >> 1) & 1);
             tc_fence_after();
             const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN);
-            epilogue_tile<MODE, BN>(P, tq, m_tile, n_tile, split, q, lane, stg, buf);
+            epilogue_tile<MODE, BN>(P, tq, m_tile, n_tile, split, q, lane, stg, buf, sw3);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_remote(tempty_leader + acc * 8);  // free the buffer (leader's barrier)
