@@ -50,8 +50,8 @@ struct Cfg {
     static constexpr uint32_t A_BYTES = BM * BK * 2;
     static constexpr uint32_t B_BYTES = BN * BK * 2;
     static constexpr uint32_t STAGE_BYTES = NPL * (A_BYTES + B_BYTES);
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ + 4 * 2 * 2048 +
-                                     3 * 512 * 4 /*W3*/;
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ +
+                                     4 * 2 * 2048 /*staging*/ + 3 * 512 * 4 /*W3*/ + 512 * 4 /*bias*/;
     static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
 };
 
@@ -97,14 +97,25 @@ constexpr uint32_t EPI_BUF = 2048;                 // 32 x 16 fp32, or hi + lo 3
 constexpr uint32_t EPI_BYTES = 4 * 2 * EPI_BUF;    // 4 warps x 2 buffers
 
 constexpr uint32_t W3_BYTES = 3 * 512 * 4;       // W3 copy for the fused conv2 logits (C <= 512)
+constexpr uint32_t BIAS_BYTES = 512 * 4;         // FWD bias copy (Nout <= 512)
+constexpr uint32_t EPI_SMEM = EPI_BYTES + W3_BYTES + BIAS_BYTES;
 
-// Epilogue warps copy W3 into shared memory (conv2 FWD with fused logits only).
-TEM_DEV void load_w3_smem(const UmmaParams& P, float* sw3, int et) {
+// Epilogue warps copy W3 (conv2 FWD with fused logits) and the bias (FWD) to shared memory.
+TEM_DEV void load_epi_smem(const UmmaParams& P, float* sw3, int et) {
     if (P.zpart) {
         for (int i = et; i < 3 * P.Nout; i += 128) sw3[i] = P.w3[i];
     }
+    if (P.bias) {
+        for (int i = et; i < P.Nout; i += 128) sw3[3 * 512 + i] = P.bias[i];
+    }
     asm volatile("bar.sync 1, 128;" ::: "memory");
 }
+
+// Per-chunk register set: 16 accumulator columns (+ the DGRAD ReLU-mask words of the chunk).
+struct EpiRegs {
+    uint32_t r[16];
+    uint32_t mw[8];
+};
 
 template <int MODE, int BN>
 TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_tile, int split, int q,
@@ -112,41 +123,51 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
     const int row0 = m_tile * BM + 32 * q;
     const int row = row0 + lane;
     if ((MODE == FWD_ || MODE == DGRAD_) && (m_tile >= P.mtiles || row0 >= P.R)) return;
+    const bool halo = (MODE != WGRAD_) && (row >= P.R || halo_row(row, P.Tp));
+    const float* sbias = sw3 + 3 * 512;
     float zp0 = 0.f, zp1 = 0.f, zp2 = 0.f;  // FWD conv2: partial logits W3 . h2 over this tile's columns
-#pragma unroll 1
-    for (int c16 = 0; c16 < BN / 16; ++c16) {
+
+    // Issue the TMEM load (and the DGRAD mask load) of chunk c16; consumed after tmem_ld_wait.
+    auto issue = [&](int c16, EpiRegs& e) {
+        tmem_ld16(tq + (uint32_t)(c16 * 16), e.r);
+        if (MODE == DGRAD_) {
+            if (!halo) {
+                const uint4* mk = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(P.mask) +
+                                                                 (size_t)row * P.Nout + n_tile * BN + c16 * 16);
+                const uint4 m0v = __ldg(mk), m1v = __ldg(mk + 1);
+                e.mw[0] = m0v.x; e.mw[1] = m0v.y; e.mw[2] = m0v.z; e.mw[3] = m0v.w;
+                e.mw[4] = m1v.x; e.mw[5] = m1v.y; e.mw[6] = m1v.z; e.mw[7] = m1v.w;
+            } else {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) e.mw[i] = 0u;
+            }
+        }
+    };
+    auto process = [&](int c16, EpiRegs& e) {
         int gc = 0;  // global column of the store box (FWD/DGRAD: n; WGRAD: j*Cin + c)
         if (MODE == WGRAD_) {
             const int nl = c16 * 16;
             const int g = n_tile * (BN / 64) + nl / 64;
             if (P.ones_chunk && g == 3 * P.cpj) {
-                if (nl % 64 == 0) {  // column 0 of the all-ones chunk: bias-gradient partial
-                    uint32_t r[16];
-                    tmem_ld16(tq + (uint32_t)(c16 * 16), r);
-                    tmem_ld_wait();
-                    P.part[(size_t)split * P.part_stride + (size_t)P.Nout * P.NW + row] = __uint_as_float(r[0]);
-                }
-                continue;
+                if (nl % 64 == 0)  // column 0 of the all-ones chunk: bias-gradient partial
+                    P.part[(size_t)split * P.part_stride + (size_t)P.Nout * P.NW + row] = __uint_as_float(e.r[0]);
+                return;
             }
-            if (g >= 3 * P.cpj) continue;
+            if (g >= 3 * P.cpj) return;
             const int j = g / P.cpj, c = (g % P.cpj) * 64 + (nl % 64);
-            if (c >= P.Cin_w) continue;
+            if (c >= P.Cin_w) return;
             gc = j * P.Cin_w + c;
         } else {
             gc = n_tile * BN + c16 * 16;
         }
-        uint32_t r[16];
-        tmem_ld16(tq + (uint32_t)(c16 * 16), r);
-        tmem_ld_wait();
         float v[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(e.r[i]);
         if (MODE == FWD_) {
-            const bool halo = row >= P.R || halo_row(row, P.Tp);
-            const float4* bp = reinterpret_cast<const float4*>(P.bias + gc);
+            const float4* bp = reinterpret_cast<const float4*>(sbias + gc);
 #pragma unroll
             for (int i4 = 0; i4 < 4; ++i4) {
-                const float4 bb = __ldg(bp + i4);
+                const float4 bb = bp[i4];
                 const float bv[4] = {bb.x, bb.y, bb.z, bb.w};
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -166,19 +187,10 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
                 }
             }
         } else if (MODE == DGRAD_) {
-            const bool halo = row >= P.R || halo_row(row, P.Tp);
-            uint32_t mw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            if (!halo) {
-                const uint4* mk = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(P.mask) +
-                                                                 (size_t)row * P.Nout + gc);
-                const uint4 m0v = mk[0], m1v = mk[1];
-                mw[0] = m0v.x; mw[1] = m0v.y; mw[2] = m0v.z; mw[3] = m0v.w;
-                mw[4] = m1v.x; mw[5] = m1v.y; mw[6] = m1v.z; mw[7] = m1v.w;
-            }
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-                v[2 * i] = __uint_as_float(mw[i] << 16) > 0.f ? v[2 * i] : 0.f;
-                v[2 * i + 1] = __uint_as_float(mw[i] & 0xFFFF0000u) > 0.f ? v[2 * i + 1] : 0.f;
+                v[2 * i] = __uint_as_float(e.mw[i] << 16) > 0.f ? v[2 * i] : 0.f;
+                v[2 * i + 1] = __uint_as_float(e.mw[i] & 0xFFFF0000u) > 0.f ? v[2 * i + 1] : 0.f;
             }
         }
         uint8_t* sb = stg + buf * EPI_BUF;
@@ -205,6 +217,21 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
             bulk_commit();
         }
         buf ^= 1;
+    };
+
+    // Two register sets: the TMEM load of chunk c+1 is in flight while chunk c is processed.
+    constexpr int NC = BN / 16;
+    static_assert(NC % 2 == 0, "BN must be a multiple of 32");
+    EpiRegs ea, eb;
+    issue(0, ea);
+#pragma unroll 1
+    for (int c16 = 0; c16 < NC; c16 += 2) {
+        tmem_ld_wait_regs(ea.r);
+        issue(c16 + 1, eb);
+        process(c16, ea);
+        tmem_ld_wait_regs(eb.r);
+        if (c16 + 2 < NC) issue(c16 + 2, ea);
+        process(c16 + 1, eb);
     }
     if (MODE == FWD_ && P.zpart && row < P.R) {
         float* zp = P.zpart + ((size_t)n_tile * P.R + row) * 3;
@@ -399,7 +426,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_conv_kernel(const __grid_con
         const int q = warp & 3;  // TMEM lane quarter accessible to this warp
         uint8_t* stg = smem + STAGES * C_::STAGE_BYTES + 1024 + (warp - 2) * 2 * EPI_BUF;
         float* sw3 = reinterpret_cast<float*>(smem + STAGES * C_::STAGE_BYTES + 1024 + EPI_BYTES);
-        if (MODE == FWD_) load_w3_smem(P, sw3, threadIdx.x - 64);
+        if (MODE == FWD_) load_epi_smem(P, sw3, threadIdx.x - 64);
         int buf = 0, t = 0;
         for (int ct = cluster_id; ct < total_ct; ct += nclusters, ++t) {
             int m_tile, n_tile, split, p_begin;
@@ -437,7 +464,7 @@ struct CfgPair {
     static constexpr uint32_t A_BYTES = BM * BK * 2;            // this CTA's 128 rows
     static constexpr uint32_t B_BYTES = (BN / 2) * BK * 2;      // this CTA's half of B
     static constexpr uint32_t STAGE_BYTES = NPL * (A_BYTES + B_BYTES);
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 1024 + 4 * 2 * 2048 + 3 * 512 * 4;
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 1024 + 4 * 2 * 2048 + 3 * 512 * 4 + 512 * 4;
     static constexpr int TMEM_COLS = 2 * BN;
 };
 
@@ -469,7 +496,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_pair_kernel(const __grid_con
             tma_prefetch(&P.b[i]);
         }
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 2);   // leader: own expect_tx arrive + the peer's arrive
+            mbar_init(&full[s], 1);   // the leader's expect_tx arrive covers both CTAs' bytes
             mbar_init(&empty[s], 1);  // one multicast commit from the leader's MMA
         }
         for (int a = 0; a < 2; ++a) {
@@ -504,7 +531,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_pair_kernel(const __grid_con
     if (warp == 0) {
         if (lane == 0) {
             // ===================== TMA producer (both CTAs) =====================
-            const uint32_t full_leader0 = mapa_shared(&full[0], 0);
             int it = 0;
             for (int ct = pair_id; ct < total; ct += npairs) {
                 int mp, n_tile, split, p_begin;
@@ -516,8 +542,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_pair_kernel(const __grid_con
                     const uint32_t ph = (it / STAGES) & 1;
                     mbar_wait(&empty[s], ph ^ 1);
                     uint8_t* st = smem + s * C_::STAGE_BYTES;
+                    // Only the leader arms the barrier (both halves' bytes); the peer's loads
+                    // complete_tx on it directly.  The peer issues after empty[s] flipped, so the
+                    // barrier is already in this phase; a transiently negative tx-count is legal.
                     if (leader) mbar_arrive_expect_tx(&full[s], 2 * C_::STAGE_BYTES);
-                    else mbar_arrive_remote(full_leader0 + s * 8);
 #pragma unroll
                     for (int pl = 0; pl < NPL; ++pl) {
                         uint8_t* sa = st + pl * C_::A_BYTES;
@@ -601,7 +629,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_pair_kernel(const __grid_con
         const uint32_t tempty_leader = mapa_shared(&tempty[0], 0);
         uint8_t* stg = smem + STAGES * C_::STAGE_BYTES + 1024 + (warp - 2) * 2 * EPI_BUF;
         float* sw3 = reinterpret_cast<float*>(smem + STAGES * C_::STAGE_BYTES + 1024 + EPI_BYTES);
-        if (MODE == FWD_) load_w3_smem(P, sw3, threadIdx.x - 64);
+        if (MODE == FWD_) load_epi_smem(P, sw3, threadIdx.x - 64);
         int buf = 0, t = 0;
         for (int ct = pair_id; ct < total; ct += npairs, ++t) {
             int mp, n_tile, split, p_begin;
@@ -851,14 +879,16 @@ struct GemmCfg {
     int bn, stages, cm, cn;
     int pair;  // 1: 2-CTA kernel (256-row pair tiles, cta_group::2)
 };
-// TEM_GEMM_VARIANT (experiments): 1 = 1-CTA without clusters (default), 2 = 2-CTA pairs,
-// 0 = 1-CTA with multicast clusters.
+// TEM_GEMM_VARIANT (experiments): unset = auto (2-CTA pairs for the 1-pass bf16 GEMMs, 1-CTA
+// for the 3-pass fp32 ones -- the measured winners on B200), 1 = 1-CTA without clusters,
+// 2 = 2-CTA pairs everywhere, 0 = 1-CTA with multicast clusters.
 static int gemm_variant() {
     const char* e = getenv("TEM_GEMM_VARIANT");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : -1;
 }
 static GemmCfg cfg_for(int mode, int npass) {
-    const int v = gemm_variant();
+    int v = gemm_variant();
+    if (v < 0) v = npass == 1 ? 2 : 1;
     if (v == 2) {
         if (npass == 1) return GemmCfg{256, 6, 1, 1, 1};
         return mode == WGRAD_ ? GemmCfg{256, 3, 1, 1, 1} : GemmCfg{128, 4, 1, 1, 1};
@@ -873,9 +903,12 @@ static GemmCfg cfg_for(int mode, int npass) {
 
 int umma_wgrad_splits(const Geom& g) {
     const GemmCfg c = cfg_for(WGRAD_, g.prec == TEM_FP32 ? 3 : 1);
-    const int chunks = 3 * (((g.Cin > g.C ? g.Cin : g.C) + 63) / 64) + 1;
-    const int tiles = (g.C / umma::BM) * ((chunks + c.bn / 64 - 1) / (c.bn / 64));
-    int S = c.pair ? (74 * 2) / tiles : (148 + tiles - 1) / tiles;  // pairs: one wave of 74 pairs
+    // n-tiles of the larger of the two weight gradients: conv1 (3 taps x Cin chunks + the
+    // all-ones bias chunk) and conv2 (3 taps x C chunks)
+    const int wc = c.bn / 64;
+    const int n1 = (3 * ((g.Cin + 63) / 64) + 1 + wc - 1) / wc, n2 = (3 * ((g.C + 63) / 64) + wc - 1) / wc;
+    const int tiles = (g.C / umma::BM) * (n1 > n2 ? n1 : n2);  // 128-row CTA tiles per split
+    int S = 148 / tiles;  // one wave of CTAs (pairs: 74 pairs = 148 CTAs)
     const int nkb = (g.R + umma::BK - 1) / umma::BK;
     if (S > nkb) S = nkb;
     if (S < 1) S = 1;

@@ -130,7 +130,10 @@ UMMA_DEV uint32_t mapa_shared(const void* p, uint32_t rank) {
     return r;
 }
 UMMA_DEV void mbar_arrive_remote(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+    // Default (.release.cta) semantics: the TMEM reads it publishes are ordered by the
+    // tcgen05.fence::before_thread_sync the caller issues; .cluster scope would cost a
+    // GPU-wide MEMBAR per arrive.
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 template <int NCOLS>
 UMMA_DEV void tmem_alloc_pair(uint32_t* slot_smem) {  // one warp in EACH CTA of the pair
@@ -214,6 +217,16 @@ UMMA_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
         : "memory");
 }
 UMMA_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// Wait that also ties the destination registers of the pending loads to this point, so the
+// compiler cannot read them before the wait (the load writes them asynchronously).
+UMMA_DEV void tmem_ld_wait_regs(uint32_t (&r)[16]) {
+    asm volatile("tcgen05.wait::ld.sync.aligned;"
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15])
+                 :
+                 : "memory");
+}
 
 // ------------------------------------------------------------------ descriptors
 // Shared-memory matrix descriptor, SWIZZLE_128B, version 1 (sm_100).
