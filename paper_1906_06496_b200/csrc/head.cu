@@ -23,39 +23,78 @@ namespace tem {
 namespace {
 
 constexpr int HEAD_WARPS = 8;
+constexpr int NZP_MAX = 8;  // fused-logit partials per row (C / BN of the conv2 epilogue)
 
 TEM_DEV float softplusf(float u) { return u > 0.f ? u + log1pf(expf(-u)) : log1pf(expf(u)); }
 
+TEM_DEV void store4(float* dst, const float (&v)[4]) {
+    *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+}
+TEM_DEV void store4(__nv_bfloat16* dst, const __nv_bfloat16 (&v)[4]) {
+    __nv_bfloat162 a, b;
+    a.x = v[0]; a.y = v[1]; b.x = v[2]; b.y = v[3];
+    *reinterpret_cast<uint2*>(dst) = make_uint2(*reinterpret_cast<uint32_t*>(&a), *reinterpret_cast<uint32_t*>(&b));
+}
+
+// Latency structure: every global load the CTA needs that does not depend on another (W3
+// columns, the first batch of h2 rows, the labels, the fused logits) is issued before the
+// first barrier, so a CTA costs about one memory round trip plus its arithmetic.  <= 85
+// registers: 3 CTAs (768 threads) per SM, and head_rows_per_cta sizes the grid to one wave.
 template <typename TOp>
-__global__ void __launch_bounds__(256) head_rows_kernel(
+__global__ void __launch_bounds__(256, 3) head_rows_kernel(
     const float* __restrict__ h2, const float* __restrict__ W3, const float* __restrict__ b3,
     const float* __restrict__ labels, float lam0, float lam1, float lam2, TOp* __restrict__ dA2,
     TOp* __restrict__ dA2_lo, float* __restrict__ z_out, float* __restrict__ part, int B, int Tn, int C,
     int RPC, const float* __restrict__ zpart, int nzp) {
     extern __shared__ __align__(16) float sm[];
-    float* sW3 = sm;           // [3][C]
+    float* sW3 = sm;           // [3][C] (only the nzp == 0 path reads it)
     float* sdz = sm + 3 * C;   // [RPC][3] dz of this CTA's rows (0 on halo rows)
     __shared__ float s_ap[3][3], s_an[3][3], s_misc[HEAD_WARPS][6];
-    __shared__ int s_cnt[3][3];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int Tp = Tn + 2, R = B * Tp;
     const int p0 = blockIdx.x * RPC, p1 = min(R, p0 + RPC);
     const int v0 = p0 / Tp, nv = (p1 - 1) / Tp - v0 + 1;  // <= 3 videos
     const float lam[3] = {lam0, lam1, lam2};
-    for (int i = tid; i < 3 * C; i += blockDim.x) sW3[i] = W3[i];
-    if (tid < 9) s_cnt[tid / 3][tid % 3] = 0;
-    __syncthreads();
-    for (int i = tid; i < nv * 3 * Tn; i += blockDim.x) {  // l+ per video and channel (R5: strict >)
-        const int k = i / (3 * Tn), r = i - k * 3 * Tn;
-        if (labels[(size_t)(v0 + k) * 3 * Tn + r] > 0.5f) atomicAdd(&s_cnt[k][r / Tn], 1);
+
+    // ---- phase-2 operands first: thread = 4 consecutive columns x one of RP row phases ----
+    const int CG = C / 4;            // column groups (<= 128)
+    const int RP = blockDim.x / CG;  // row phases (>= 2)
+    const int cg = tid % CG, rp = tid / CG;
+    const int c0 = 4 * cg;
+    const bool act2 = rp < RP;
+    constexpr int U = 4;
+    float w[3][4];
+    float4 hv[U];
+    if (act2) {
+#pragma unroll
+        for (int o = 0; o < 3; ++o) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(W3 + (size_t)o * C + c0));
+            w[o][0] = t.x; w[o][1] = t.y; w[o][2] = t.z; w[o][3] = t.w;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int p = p0 + rp + u * RP;
+            hv[u] = p < p1 ? *reinterpret_cast<const float4*>(h2 + (size_t)p * C + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
     }
-    __syncthreads();
-    if (tid < 9) {
-        const int k = tid / 3, o = tid % 3;
-        const int lp = s_cnt[k][o], ln = Tn - lp;
-        s_ap[k][o] = (float)Tn / (float)(lp > 1 ? lp : 1);
-        s_an[k][o] = (float)Tn / (float)(ln > 1 ? ln : 1);
+    // ---- label statistics: one warp per (video, channel); l+ counts strict > 0.5 (R5) ----
+    for (int pr = warp; pr < nv * 3; pr += HEAD_WARPS) {
+        const int k = pr / 3, o = pr - 3 * k;
+        const float* lab = labels + ((size_t)(v0 + k) * 3 + o) * Tn;
+        int lp = 0;
+#pragma unroll 4
+        for (int t0 = 0; t0 < Tn; t0 += 32) {
+            const bool pos = (t0 + lane < Tn) && lab[t0 + lane] > 0.5f;
+            lp += __popc(__ballot_sync(0xffffffffu, pos));
+        }
+        if (lane == 0) {
+            const int ln = Tn - lp;
+            s_ap[k][o] = (float)Tn / (float)(lp > 1 ? lp : 1);
+            s_an[k][o] = (float)Tn / (float)(ln > 1 ? ln : 1);
+        }
     }
+    if (nzp == 0)
+        for (int i = tid; i < 3 * C; i += blockDim.x) sW3[i] = W3[i];
     __syncthreads();
     // ---- phase 1: z, loss terms, dz -> smem ----
     const int NQ = C / 32;  // <= 16
@@ -79,18 +118,26 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
         }
     };
     if (nzp > 0) {
-        // logits precomputed by the conv2 epilogue: one row per THREAD (no redundant lanes)
+        // logits precomputed by the conv2 epilogue: one row per THREAD, partials summed in
+        // ascending n-tile order (all loads issued together)
         for (int p = p0 + tid; p < p1; p += blockDim.x) {
             const int tp = p % Tp;
             if (tp == 0 || tp == Tp - 1) {
                 sdz[(p - p0) * 3] = sdz[(p - p0) * 3 + 1] = sdz[(p - p0) * 3 + 2] = 0.f;
                 continue;
             }
+            float zz[NZP_MAX][3];
+#pragma unroll
+            for (int kk = 0; kk < NZP_MAX; ++kk)
+#pragma unroll
+                for (int o = 0; o < 3; ++o) zz[kk][o] = kk < nzp ? zpart[((size_t)kk * R + p) * 3 + o] : 0.f;
             float z[3];
 #pragma unroll
             for (int o = 0; o < 3; ++o) {
-                float sz = zpart[(size_t)p * 3 + o];
-                for (int kk = 1; kk < nzp; ++kk) sz += zpart[((size_t)kk * R + p) * 3 + o];
+                float sz = zz[0][o];
+#pragma unroll
+                for (int kk = 1; kk < NZP_MAX; ++kk)
+                    if (kk < nzp) sz += zz[kk][o];
                 z[o] = sz + b3[o];
             }
             row_loss(p, z);
@@ -111,19 +158,17 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
                 if (lane < 3) sdz[(p - p0) * 3 + lane] = 0.f;
                 continue;
             }
-            float h[16];
+            float z[3] = {0.f, 0.f, 0.f};
+            for (int q = 0; q < NQ; ++q) {
+                const float h = h2[(size_t)p * C + lane + 32 * q];
 #pragma unroll
-            for (int q = 0; q < 16; ++q) h[q] = (q < NQ) ? h2[(size_t)p * C + lane + 32 * q] : 0.f;
-            float z[3];
+                for (int o = 0; o < 3; ++o) z[o] = fmaf(sW3[o * C + lane + 32 * q], h, z[o]);
+            }
 #pragma unroll
             for (int o = 0; o < 3; ++o) {
-                float sz = 0.f;
 #pragma unroll
-                for (int q = 0; q < 16; ++q)
-                    if (q < NQ) sz = fmaf(sW3[o * C + lane + 32 * q], h[q], sz);
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) sz += __shfl_xor_sync(0xffffffffu, sz, off);
-                z[o] = sz + b3[o];
+                for (int off = 16; off > 0; off >>= 1) z[o] += __shfl_xor_sync(0xffffffffu, z[o], off);
+                z[o] += b3[o];
             }
             if (lane == 0) row_loss(p, z);
         }
@@ -136,34 +181,23 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
         }
     }
     __syncthreads();
-    // ---- phase 2: column-parallel over the CTA's rows (h2 rows are L2-resident now) ----
-    // dA2 = 1[h2>0] W3^T dz (halo rows: dz = 0 -> 0); dW3 += dz h2; db2 += stored dA2.
-    // Thread = 4 consecutive columns (float4 loads) x one of RP row phases; the RP phase
-    // partials are combined in a fixed order through shared memory.
-    float* dst = part + (size_t)blockIdx.x * (4 * C + 6);
-    const int CG = C / 4;                 // column groups (<= 128)
-    const int RP = blockDim.x / CG;       // row phases (>= 2)
-    const int cg = tid % CG, rp = tid / CG;
-    const int c0 = 4 * cg;
+    // ---- phase 2: dA2 = 1[h2>0] W3^T dz (halo rows: dz = 0 -> 0); dW3 += dz h2; db2 += stored dA2 ----
+    float* dst = part + (size_t)blockIdx.x * (4 * C + 8);  // row stride padded to 16 bytes
     float acc[3][4], bs[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         bs[i] = 0.f;
         acc[0][i] = acc[1][i] = acc[2][i] = 0.f;
     }
-    if (rp < RP) {
-        float w[3][4];
-#pragma unroll
-        for (int o = 0; o < 3; ++o)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) w[o][i] = sW3[o * C + c0 + i];
-        constexpr int U = 4;
+    if (act2) {
         for (int pb = p0 + rp; pb < p1; pb += U * RP) {
-            float4 hv[U];
+            if (pb != p0 + rp) {
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int p = pb + u * RP;
-                hv[u] = p < p1 ? *reinterpret_cast<const float4*>(h2 + (size_t)p * C + c0) : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int u = 0; u < U; ++u) {
+                    const int p = pb + u * RP;
+                    hv[u] = p < p1 ? *reinterpret_cast<const float4*>(h2 + (size_t)p * C + c0)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -172,7 +206,6 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
                 const float* dzr = sdz + (p - p0) * 3;
                 const float d0 = dzr[0], d1 = dzr[1], d2 = dzr[2];
                 const float h[4] = {hv[u].x, hv[u].y, hv[u].z, hv[u].w};
-                float st[4];
                 TOp dh[4], dl[4];
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
@@ -181,29 +214,25 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
                     d = fmaf(w[2][i], d2, d);
                     const float dv = h[i] > 0.f ? d : 0.f;
                     dh[i] = from_f<TOp>(dv);
-                    st[i] = to_f(dh[i]);
+                    float st = to_f(dh[i]);
                     if (dA2_lo) {
-                        dl[i] = from_f<TOp>(dv - st[i]);
-                        st[i] += to_f(dl[i]);
+                        dl[i] = from_f<TOp>(dv - st);
+                        st += to_f(dl[i]);
                     }
-                    bs[i] += st[i];
+                    bs[i] += st;
                     acc[0][i] = fmaf(d0, h[i], acc[0][i]);
                     acc[1][i] = fmaf(d1, h[i], acc[1][i]);
                     acc[2][i] = fmaf(d2, h[i], acc[2][i]);
                 }
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    dA2[(size_t)p * C + c0 + i] = dh[i];
-                    if (dA2_lo) dA2_lo[(size_t)p * C + c0 + i] = dl[i];
-                }
+                store4(dA2 + (size_t)p * C + c0, dh);
+                if (dA2_lo) store4(dA2_lo + (size_t)p * C + c0, dl);
             }
         }
     }
-    // combine the row phases in order: smem reuse of sW3 region is unsafe (still read), use sdz tail
+    // combine the row phases in a fixed order through shared memory (sdz is dead after the sync)
+    float* red = sdz;  // [RP][CG][16]
     __syncthreads();
-    float* red = sdz;  // [RP][CG][16] floats: phase 1 data (dz) is dead after the sync below
-    __syncthreads();
-    if (rp < RP) {
+    if (act2) {
         float* r = red + ((size_t)rp * CG + cg) * 16;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -222,26 +251,24 @@ __global__ void __launch_bounds__(256) head_rows_kernel(
 #pragma unroll
             for (int k = 0; k < 16; ++k) sum[k] += red[((size_t)ph * CG + cg) * 16 + k];
         // partial row layout: [dW3 (3C)][db3 (3)][L (3)][db2 (C)]
+        store4(dst + c0, {sum[0], sum[1], sum[2], sum[3]});
+        store4(dst + C + c0, {sum[4], sum[5], sum[6], sum[7]});
+        store4(dst + 2 * C + c0, {sum[8], sum[9], sum[10], sum[11]});
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            dst[c0 + i] = sum[i];
-            dst[C + c0 + i] = sum[4 + i];
-            dst[2 * C + c0 + i] = sum[8 + i];
-            dst[3 * C + 6 + c0 + i] = sum[12 + i];
-        }
+        for (int i = 0; i < 4; ++i) dst[3 * C + 6 + c0 + i] = sum[12 + i];  // offset 3C+6: 8-byte aligned only
     }
     if (tid < 3) {
         float l = s_misc[0][tid], d = s_misc[0][3 + tid];
-        for (int w = 1; w < HEAD_WARPS; ++w) {
-            l += s_misc[w][tid];
-            d += s_misc[w][3 + tid];
+        for (int w2 = 1; w2 < HEAD_WARPS; ++w2) {
+            l += s_misc[w2][tid];
+            d += s_misc[w2][3 + tid];
         }
         dst[3 * C + tid] = d;
         dst[3 * C + 3 + tid] = -l / (float)Tn;
     }
 }
 
-// Two-level fixed-order reduction of the P partial rows (n = 4C+6 entries each).
+// Two-level fixed-order reduction of the P partial rows (n = 4C+6 entries each, stride 4C+8).
 // Level 1: CTA (x, y) sums rows [y*P/G, (y+1)*P/G) of entries x*256.. into lvl1[y].
 // Level 2: per column block x, the last of its G CTAs sums lvl1[0..G) in order and writes
 // those outputs; the block holding the three loss sums also writes loss_out.
@@ -249,14 +276,14 @@ __global__ void head_reduce_kernel(const float* __restrict__ part, int P, int C,
                                    unsigned* __restrict__ counter, float* __restrict__ gW3,
                                    float* __restrict__ gb2, float* __restrict__ loss_out, int B, float lam0,
                                    float lam1, float lam2, Status* status, int64_t* stepctr) {
-    const int n = 4 * C + 6;
+    const int n = 4 * C + 6, stride = 4 * C + 8;  // entries / padded row stride
     const int G = gridDim.y;
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     const int r0 = (int)((int64_t)blockIdx.y * P / G), r1 = (int)((int64_t)(blockIdx.y + 1) * P / G);
     if (e < n) {
         float s = 0.f;
 #pragma unroll 8
-        for (int r = r0; r < r1; ++r) s += part[(size_t)r * n + e];
+        for (int r = r0; r < r1; ++r) s += part[(size_t)r * stride + e];
         lvl1[(size_t)blockIdx.y * n + e] = s;
     }
     __threadfence();
@@ -294,9 +321,9 @@ __global__ void head_reduce_kernel(const float* __restrict__ part, int P, int C,
 }
 
 int head_rows_per_cta(const Geom& g) {
-    int rpc = (g.R + 591) / 592;  // ~4 CTAs per SM
+    int rpc = (g.R + 443) / 444;  // one wave at 3 CTAs per SM
     rpc = (rpc + 7) / 8 * 8;
-    if (rpc < 16) rpc = 16;
+    if (rpc < 8) rpc = 8;
     if (rpc > 128) rpc = 128;
     return rpc;
 }

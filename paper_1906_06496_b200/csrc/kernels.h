@@ -47,7 +47,7 @@ struct RankBufs {
     void* dA1_lo;
     float* z;             // [B][T][3]
     float* grad;          // [Kpad] local gradient (flat order W1 b1 W2 b2 W3 b3 pad)
-    float* headpart;      // [B*HS][4C + 6] head partials (dW3, db3, L, db2)
+    float* headpart;      // [ctas][4C + 8] head partials (dW3, db3, L, db2; 2 pad)
     float* headlvl1;      // [32][4C + 6] first-level sums
     unsigned* counter;    // last-CTA ticket of the head reduction (self-resetting)
     float* bpart;         // [m-tiles][C] conv1 bias-gradient partials (tcgen05 DGRAD epilogue)

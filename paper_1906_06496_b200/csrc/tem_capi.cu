@@ -135,7 +135,7 @@ WsLayout ws_layout(const tem_config* c) {
     w.dA1_lo = take(lo * g.R * g.C * esz);
     w.z = take((size_t)g.B * g.T * 3 * 4);
     w.grad = take((size_t)g.Kpad * 4);
-    w.headpart = take((size_t)head_ctas(g) * (4 * g.C + 6) * 4);
+    w.headpart = take((size_t)head_ctas(g) * (4 * g.C + 8) * 4);
     w.headlvl1 = take((size_t)32 * (4 * g.C + 6) * 4);
     w.counter = take(64);
     w.bpart = take((size_t)((g.R + 127) / 128) * g.C * 4);

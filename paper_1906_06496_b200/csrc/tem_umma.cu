@@ -983,7 +983,8 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     P.conv2.out_hi = b.h2;
     P.conv2.out_f32 = 1;
     P.conv2.w3 = b.params + g.off_W3;
-    P.conv2.zpart = getenv("TEM_NO_ZPART") ? nullptr : b.zpart;  // [C/BN][R][3] partial logits for the head
+    // [C/BN][R][3] partial logits for the head (which sums at most 8 per row)
+    P.conv2.zpart = (getenv("TEM_NO_ZPART") || g.C / cf.bn > 8) ? nullptr : b.zpart;
     common(P.dgrad);
     P.dgrad.Kc = g.C;
     P.dgrad.cpb = g.C / umma::BK;
