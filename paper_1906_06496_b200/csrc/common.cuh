@@ -52,6 +52,14 @@ TEM_DEV uint64_t globaltimer() {
 // L2-coherent 128-bit load (bypasses L1: data written by a peer GPU lands in our L2).
 TEM_DEV float4 ld_cg4(const float* p) { return __ldcg(reinterpret_cast<const float4*>(p)); }
 
+// Programmatic dependent launch (PDL): a kernel launched with the programmatic-serialization
+// attribute may start while its stream predecessor is still running; it must call pdl_wait()
+// before touching global memory that the predecessor writes or reads.  pdl_trigger() lets
+// the NEXT kernel launch now (its CTAs still block in their own pdl_wait).  Both are no-ops
+// for a kernel launched without the attribute.
+TEM_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+TEM_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // Device-side error latch (host-mapped pinned word): first error wins.
 struct Status {
     int32_t code;      // tem_status

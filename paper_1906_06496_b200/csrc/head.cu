@@ -47,6 +47,8 @@ __global__ void __launch_bounds__(256, 3) head_rows_kernel(
     TOp* __restrict__ dA2_lo, float* __restrict__ z_out, float* __restrict__ part, int B, int Tn, int C,
     int RPC, const float* __restrict__ zpart, int nzp) {
     extern __shared__ __align__(16) float sm[];
+    pdl_trigger();
+    pdl_wait();
     float* sW3 = sm;           // [3][C] (only the nzp == 0 path reads it)
     float* sdz = sm + 3 * C;   // [RPC][3] dz of this CTA's rows (0 on halo rows)
     __shared__ float s_ap[3][3], s_an[3][3], s_misc[HEAD_WARPS][6];
@@ -276,6 +278,8 @@ __global__ void head_reduce_kernel(const float* __restrict__ part, int P, int C,
                                    unsigned* __restrict__ counter, float* __restrict__ gW3,
                                    float* __restrict__ gb2, float* __restrict__ loss_out, int B, float lam0,
                                    float lam1, float lam2, Status* status, int64_t* stepctr) {
+    pdl_trigger();
+    pdl_wait();
     const int n = 4 * C + 6, stride = 4 * C + 8;  // entries / padded row stride
     const int G = gridDim.y;
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -340,21 +344,24 @@ cudaError_t launch_head_rows(const Geom& g, const RankBufs& b, const float* labe
     const size_t hsm = (size_t)(3 * g.C + (3 * rpc > (int)red ? 3 * rpc : red)) * sizeof(float);
     if (P == 0) return cudaSuccess;
     rec.begin(SLOT_HEAD);
+    cudaError_t e;
     if (g.op_bf16) {
         auto k = head_rows_kernel<__nv_bfloat16>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-        k<<<P, 256, hsm, s>>>(b.h2, b.params + g.off_W3, b.params + g.off_b3, labels, lam[0], lam[1], lam[2],
-                              static_cast<__nv_bfloat16*>(b.dA2), static_cast<__nv_bfloat16*>(b.dA2_lo), b.z,
-                              b.headpart, g.B, g.T, g.C, rpc, b.zpart, b.nzpart);
+        e = launch_pdl(k, dim3(P), dim3(256), hsm, s, (const float*)b.h2, (const float*)(b.params + g.off_W3),
+                       (const float*)(b.params + g.off_b3), labels, lam[0], lam[1], lam[2],
+                       static_cast<__nv_bfloat16*>(b.dA2), static_cast<__nv_bfloat16*>(b.dA2_lo), b.z, b.headpart, g.B,
+                       g.T, g.C, rpc, (const float*)b.zpart, b.nzpart);
     } else {
         auto k = head_rows_kernel<float>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-        k<<<P, 256, hsm, s>>>(b.h2, b.params + g.off_W3, b.params + g.off_b3, labels, lam[0], lam[1], lam[2],
-                              static_cast<float*>(b.dA2), nullptr, b.z, b.headpart, g.B, g.T, g.C, rpc, nullptr, 0);
+        e = launch_pdl(k, dim3(P), dim3(256), hsm, s, (const float*)b.h2, (const float*)(b.params + g.off_W3),
+                       (const float*)(b.params + g.off_b3), labels, lam[0], lam[1], lam[2], static_cast<float*>(b.dA2),
+                       (float*)nullptr, b.z, b.headpart, g.B, g.T, g.C, rpc, (const float*)nullptr, 0);
     }
     rec.end(SLOT_HEAD);
     ++*n;
-    return cudaGetLastError();
+    return e;
 }
 
 cudaError_t launch_head_reduce(const Geom& g, const RankBufs& b, const float lam[3], float* loss_out,
@@ -363,12 +370,12 @@ cudaError_t launch_head_reduce(const Geom& g, const RankBufs& b, const float lam
     rec.begin(SLOT_HEADFIN);
     const int nent = 4 * g.C + 6;
     const int G = P >= 128 ? 16 : (P >= 16 ? 4 : 1);
-    head_reduce_kernel<<<dim3((nent + 255) / 256, G), 256, 0, s>>>(
-        b.headpart, P, g.C, b.headlvl1, b.counter, b.grad + g.off_W3, b.grad + g.off_b2, loss_out, g.B, lam[0],
-        lam[1], lam[2], status, b.stepctr);
+    cudaError_t e = launch_pdl(head_reduce_kernel, dim3((nent + 255) / 256, G), dim3(256), 0, s,
+                               (const float*)b.headpart, P, g.C, b.headlvl1, b.counter, b.grad + g.off_W3,
+                               b.grad + g.off_b2, loss_out, g.B, lam[0], lam[1], lam[2], status, b.stepctr);
     rec.end(SLOT_HEADFIN);
     ++*n;
-    return cudaGetLastError();
+    return e;
 }
 
 cudaError_t launch_head(const Geom& g, const RankBufs& b, const float* labels, const float lam[3],

@@ -10,6 +10,24 @@
 
 namespace tem {
 
+// Kernel launch with programmatic dependent launch allowed (unless TEM_NO_PDL is set): the
+// kernel's prologue overlaps the tail of its stream predecessor (see pdl_wait/pdl_trigger).
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute a[1];
+    a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    a[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = a;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
+}
+
 // Geometry of one rank's TEM step.  Activations use the halo-padded row layout
 // [B][T+2][C]: row p = v*(T+2) + t + 1 holds snippet t of video v; rows v*(T+2)
 // and v*(T+2)+T+1 are zero, so every k=3 tap is a plain row shift (reading R1's

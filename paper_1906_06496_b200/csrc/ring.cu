@@ -247,6 +247,8 @@ __global__ void __launch_bounds__(RING_THREADS) ring_kernel(const __grid_constan
 __global__ void sgd_single_kernel(const float* __restrict__ g, float* __restrict__ w,
                                   __nv_bfloat16* __restrict__ shadow, __nv_bfloat16* __restrict__ shadow_lo,
                                   int64_t n, int op, float lr) {
+    pdl_trigger();
+    pdl_wait();
     const int64_t nv = n / 4;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv;
          v += (int64_t)gridDim.x * blockDim.x) {
@@ -357,8 +359,7 @@ cudaError_t launch_ring(const RingParams& p, cudaStream_t s) {
 
 cudaError_t launch_sgd_single(const float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo,
                               int64_t n, int op, float lr, cudaStream_t s) {
-    sgd_single_kernel<<<296, 512, 0, s>>>(g, w, shadow, shadow_lo, n, op, lr);
-    return cudaGetLastError();
+    return launch_pdl(sgd_single_kernel, dim3(296), dim3(512), 0, s, g, w, shadow, shadow_lo, n, op, lr);
 }
 
 cudaError_t launch_ps(const PsParams& p, cudaStream_t s) {

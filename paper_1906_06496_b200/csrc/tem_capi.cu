@@ -17,6 +17,11 @@
 
 using namespace tem;
 
+bool tem::pdl_enabled() {
+    static const int on = getenv("TEM_NO_PDL") ? 0 : 1;
+    return on != 0;
+}
+
 namespace {
 
 constexpr size_t kAlign = 256;

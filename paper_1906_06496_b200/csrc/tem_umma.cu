@@ -44,17 +44,6 @@ constexpr int BK = 64;   // bf16 elements per k-block = one 128-byte swizzle row
 constexpr int UK = 16;   // K per tcgen05.mma (kind::f16)
 constexpr int NTHREADS = 192;
 
-template <int BN, int NPASS, int STAGES>
-struct Cfg {
-    static constexpr int NPL = NPASS == 3 ? 2 : 1;
-    static constexpr uint32_t A_BYTES = BM * BK * 2;
-    static constexpr uint32_t B_BYTES = BN * BK * 2;
-    static constexpr uint32_t STAGE_BYTES = NPL * (A_BYTES + B_BYTES);
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 1024 /*barriers*/ +
-                                     4 * 2 * 2048 /*staging*/ + 3 * 512 * 4 /*W3*/ + 512 * 4 /*bias*/;
-    static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulator buffers
-};
-
 TEM_DEV bool halo_row(int p, int Tp) {
     const int t = p % Tp;
     return t == 0 || t == Tp - 1;
@@ -241,342 +230,193 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
     }
 }
 
-template <int MODE, int BN, int NPASS, int STAGES, int CM, int CN>
-__global__ void __launch_bounds__(NTHREADS, 1) umma_conv_kernel(const __grid_constant__ UmmaParams P) {
-    using C_ = Cfg<BN, NPASS, STAGES>;
-    constexpr int NPL = C_::NPL;
-    constexpr int CS = CM * CN;
-    constexpr bool A_MN = (MODE == WGRAD_);
-    constexpr bool B_MN = (MODE != FWD_);
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C_::STAGE_BYTES);
-    uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;   // [2]
-    uint64_t* tempty = tfull + 2;       // [2]
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+// ------------------------------------------------------------------ common kernel pieces
+// PAIR = false: one CTA computes a 128 x BN tile (tcgen05.mma.cta_group::1).
+// PAIR = true : a cluster of 2 CTAs computes a 256 x BN tile with tcgen05.mma.cta_group::2
+// issued by the leader (rank 0): each CTA stages its own 128 rows of A and half of the BN
+// columns of B, so per-SM operand ingress per k-block is (128 + BN/2) rows instead of
+// (128 + BN).  The leader arms every full barrier with both CTAs' bytes (the peer's TMA
+// loads complete_tx on the leader's barrier directly); the leader's MMA commits free the
+// stage in both CTAs and signal both epilogues; both epilogues release the accumulator
+// buffer on the leader's barrier.
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // cluster coordinates: x = m direction (CM), y = n direction (CN); rank = cx + cy*CM
-    const int cx = CS > 1 ? (int)(blockIdx.x % CM) : 0;
-    const int cy = CS > 1 ? (int)blockIdx.y : 0;
-    const int cluster_id = blockIdx.x / CM, nclusters = gridDim.x / CM;
-    uint16_t rowpeers = 0, colpeers = 0;  // CTAs sharing my m-tile (A) / my n-tile (B)
-#pragma unroll
-    for (int y = 0; y < CN; ++y) rowpeers |= (uint16_t)(1u << (cx + y * CM));
-#pragma unroll
-    for (int x = 0; x < CM; ++x) colpeers |= (uint16_t)(1u << (x + cy * CM));
-    const uint16_t peers = rowpeers | colpeers;
+template <bool PAIR>
+TEM_DEV void ld2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1) {
+    if (PAIR) tma_load_2d_pair(dst, m, bar, c0, c1);
+    else tma_load_2d(dst, m, bar, c0, c1);
+}
+template <bool PAIR>
+TEM_DEV void ld3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
+    if (PAIR) tma_load_3d_pair(dst, m, bar, c0, c1, c2);
+    else tma_load_3d(dst, m, bar, c0, c1, c2);
+}
+template <bool PAIR>
+TEM_DEV void issue_mma(uint32_t dt, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t accum) {
+    if (PAIR) mma_bf16_pair(dt, ad, bd, idesc, accum);
+    else mma_bf16(dt, ad, bd, idesc, accum);
+}
+template <bool PAIR>
+TEM_DEV void commit_to(uint64_t* bar) {  // PAIR: the same barrier offset in both CTAs
+    if (PAIR) mma_commit_pair(bar);
+    else mma_commit(bar);
+}
 
-    const int mtiles_c = (P.mtiles + CM - 1) / CM;  // cluster tiles along m
-    const int ntiles_c = P.ntiles / CN;
-    const int total_ct = mtiles_c * ntiles_c * P.nsplit;
-
+// Kernel prologue shared by both kernels: barrier init (warp 0), TMEM allocation (warp 1).
+template <int TMEM_COLS, bool PAIR>
+TEM_DEV uint32_t gemm_prologue(const UmmaParams& P, uint64_t* bars, int nstage_bars, uint64_t* tfull,
+                               uint64_t* tempty, uint32_t* tslot, int warp, int lane) {
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < 2; ++i) {
             tma_prefetch(&P.a[i]);
             tma_prefetch(&P.b[i]);
         }
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], CS > 1 ? CM + CN - 1 : 1);
-        }
+        for (int i = 0; i < nstage_bars; ++i) mbar_init(&bars[i], 1);
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);
+            mbar_init(&tempty[a], PAIR ? 8 : 4);  // 4 epilogue warps (x 2 CTAs)
         }
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc<C_::TMEM_COLS>(tslot);
-    tc_fence_before();
-    __syncthreads();
-    if (CS > 1) cluster_sync();  // barrier inits visible cluster-wide before any multicast
-    tc_fence_after();
-    const uint32_t tbase = *tslot;
-
-    auto tile_coords = [&](int ct, int& m_tile, int& n_tile, int& split) {
-        const int ng = ct % ntiles_c;
-        const int rest = ct / ntiles_c;
-        const int mg = rest % mtiles_c;
-        split = rest / mtiles_c;
-        m_tile = mg * CM + cx;
-        n_tile = ng * CN + cy;
-    };
-    auto kblocks = [&](int split, int& p_begin) -> int {
-        if (MODE == WGRAD_) {
-            p_begin = split * P.ksplit_rows;
-            const int p_end = min(P.R, p_begin + P.ksplit_rows);
-            return (p_end - p_begin + BK - 1) / BK;
-        }
-        p_begin = 0;
-        return 3 * P.cpb;
-    };
-
-    if (warp == 0) {
-        if (lane == 0) {
-            // ===================== TMA producer =====================
-            constexpr int AR = A_MN ? BK / CN : BM / CN;  // rows per A slice
-            constexpr int BR = B_MN ? BK / CM : BN / CM;  // rows per B slice
-            int it = 0;
-            for (int ct = cluster_id; ct < total_ct; ct += nclusters) {
-                int m_tile, n_tile, split, p_begin;
-                tile_coords(ct, m_tile, n_tile, split);
-                const int nkb = kblocks(split, p_begin);
-                const int m0 = m_tile * BM;
-                for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const int s = it % STAGES;
-                    const uint32_t ph = (it / STAGES) & 1;
-                    mbar_wait(&empty[s], ph ^ 1);
-                    uint8_t* st = smem + s * C_::STAGE_BYTES;
-                    mbar_arrive_expect_tx(&full[s], C_::STAGE_BYTES);
-#pragma unroll
-                    for (int pl = 0; pl < NPL; ++pl) {
-                        uint8_t* sa = st + pl * C_::A_BYTES;
-                        uint8_t* sb = st + NPL * C_::A_BYTES + pl * C_::B_BYTES;
-                        auto ldA = [&](uint8_t* dst, int c0, int c1) {
-                            if (CS > 1) tma_load_2d_mc(dst, &P.a[pl], &full[s], c0, c1, rowpeers);
-                            else tma_load_2d(dst, &P.a[pl], &full[s], c0, c1);
-                        };
-                        auto ldB = [&](uint8_t* dst, const CUtensorMap* map, int c0, int c1) {
-                            if (CS > 1) tma_load_2d_mc(dst, map, &full[s], c0, c1, colpeers);
-                            else tma_load_2d(dst, map, &full[s], c0, c1);
-                        };
-                        if (MODE == FWD_) {
-                            const int j = kb / P.cpb, c0 = (kb % P.cpb) * BK;
-                            ldA(sa + cy * AR * 128, c0, m0 + j - 1 + cy * AR);
-                            ldB(sb + cx * BR * 128, &P.b[pl], j * P.Kc + c0, n_tile * BN + cx * BR);
-                        } else if (MODE == DGRAD_) {
-                            const int j = kb / P.cpb, o0 = (kb % P.cpb) * BK;
-                            ldA(sa + cy * AR * 128, o0, m0 + 1 - j + cy * AR);
-#pragma unroll
-                            for (int q = 0; q < BN / 64; ++q) {
-                                uint8_t* dst = sb + q * (BK * 128) + cx * BR * 128;
-                                if (CS > 1)
-                                    tma_load_3d_mc(dst, &P.b[pl], &full[s], n_tile * BN + 64 * q, j, o0 + cx * BR,
-                                                   colpeers);
-                                else
-                                    tma_load_3d(dst, &P.b[pl], &full[s], n_tile * BN + 64 * q, j, o0 + cx * BR);
-                            }
-                        } else {  // WGRAD
-                            const int p0 = p_begin + kb * BK;
-#pragma unroll
-                            for (int q = 0; q < BM / 64; ++q)
-                                ldA(sa + q * (BK * 128) + cy * AR * 128, m0 + 64 * q, p0 + cy * AR);
-#pragma unroll
-                            for (int q = 0; q < BN / 64; ++q) {
-                                uint8_t* dst = sb + q * (BK * 128) + cx * BR * 128;
-                                int g = n_tile * (BN / 64) + q;
-                                if (P.ones_chunk && g == 3 * P.cpj) {
-                                    // all-ones chunk (lo plane: zeros): D column = sum_p dA[p][o]
-                                    ldB(dst, &P.ones, 64 * pl, p0 + cx * BR);
-                                    continue;
-                                }
-                                if (g >= 3 * P.cpj) g = 3 * P.cpj - 1;  // dummy chunk, discarded
-                                const int j = g / P.cpj, c0 = (g % P.cpj) * 64;
-                                ldB(dst, &P.b[pl], c0, p0 + j - 1 + cx * BR);
-                            }
-                        }
-                    }
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            // ===================== MMA issuer =====================
-            constexpr uint32_t idesc = make_idesc_bf16(BM, BN, A_MN, B_MN);
-            int it = 0, t = 0;
-            for (int ct = cluster_id; ct < total_ct; ct += nclusters, ++t) {
-                int m_tile, n_tile, split, p_begin;
-                tile_coords(ct, m_tile, n_tile, split);
-                const int nkb = kblocks(split, p_begin);
-                const int acc = t & 1;
-                mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);  // epilogue drained this buffer
-                tc_fence_after();
-                const uint32_t dt = tbase + (uint32_t)(acc * BN);
-                for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const int s = it % STAGES;
-                    const uint32_t ph = (it / STAGES) & 1;
-                    mbar_wait(&full[s], ph);
-                    tc_fence_after();
-                    const uint32_t st = smem_u32(smem + s * C_::STAGE_BYTES);
-#pragma unroll
-                    for (int k = 0; k < BK / UK; ++k) {
-#pragma unroll
-                        for (int pass = 0; pass < NPASS; ++pass) {
-                            const int pa = (pass == 2) ? 1 : 0;  // hi*hi, hi*lo, lo*hi
-                            const int pb = (pass == 1) ? 1 : 0;
-                            const uint32_t a_addr = st + pa * C_::A_BYTES;
-                            const uint32_t b_addr = st + NPL * C_::A_BYTES + pb * C_::B_BYTES;
-                            const uint64_t ad = A_MN ? make_desc(a_addr + k * (UK * 128), BK * 128, 1024)
-                                                     : make_desc(a_addr + k * (UK * 2), 16, 1024);
-                            const uint64_t bd = B_MN ? make_desc(b_addr + k * (UK * 128), BK * 128, 1024)
-                                                     : make_desc(b_addr + k * (UK * 2), 16, 1024);
-                            mma_bf16(dt, ad, bd, idesc, (kb | k | pass) != 0 ? 1u : 0u);
-                        }
-                    }
-                    if (CS > 1) mma_commit_mc(&empty[s], peers);  // release the slot cluster-wide
-                    else mma_commit(&empty[s]);
-                }
-                mma_commit(&tfull[acc]);  // accumulator complete
-            }
-        }
-        __syncwarp();
-    } else {
-        // ===================== epilogue (warps 2..5) =====================
-        const int q = warp & 3;  // TMEM lane quarter accessible to this warp
-        uint8_t* stg = smem + STAGES * C_::STAGE_BYTES + 1024 + (warp - 2) * 2 * EPI_BUF;
-        float* sw3 = reinterpret_cast<float*>(smem + STAGES * C_::STAGE_BYTES + 1024 + EPI_BYTES);
-        if (MODE == FWD_) load_epi_smem(P, sw3, threadIdx.x - 64);
-        int buf = 0, t = 0;
-        for (int ct = cluster_id; ct < total_ct; ct += nclusters, ++t) {
-            int m_tile, n_tile, split, p_begin;
-            tile_coords(ct, m_tile, n_tile, split);
-            const int acc = t & 1;
-            mbar_wait(&tfull[acc], (t >> 1) & 1);
-            tc_fence_after();
-            const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN);
-            epilogue_tile<MODE, BN>(P, tq, m_tile, n_tile, split, q, lane, stg, buf, sw3);
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_local(&tempty[acc]);  // buffer free for tile t + 2
-        }
-        if (lane == 0) bulk_wait_all();
+    if (warp == 1) {
+        if (PAIR) tmem_alloc_pair<TMEM_COLS>(tslot);
+        else tmem_alloc<TMEM_COLS>(tslot);
     }
     tc_fence_before();
     __syncthreads();
-    if (CS > 1) cluster_sync();  // no CTA leaves while peers may still signal its barriers
+    if (PAIR) cluster_sync();  // barrier inits visible to the peer before any remote signal
+    tc_fence_after();
+    pdl_trigger();  // everything above overlapped the predecessor kernel's tail
+    pdl_wait();
+    return *tslot;
+}
+
+template <int TMEM_COLS, bool PAIR>
+TEM_DEV void gemm_epilogue_done(uint32_t tbase, int warp) {
+    tc_fence_before();
+    __syncthreads();
+    if (PAIR) cluster_sync();  // no CTA leaves while its peer may still signal its barriers
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<C_::TMEM_COLS>(tbase);
+        if (PAIR) tmem_dealloc_pair<TMEM_COLS>(tbase);
+        else tmem_dealloc<TMEM_COLS>(tbase);
     }
 }
 
-// ------------------------------------------------------------------ 2-CTA (pair) kernel
-// A cluster of 2 CTAs computes a 256 x BN tile with tcgen05.mma.cta_group::2 issued by the
-// leader (rank 0): each CTA stages its own 128 rows of A and half of the BN columns of B,
-// so per-SM operand ingress per k-block is (128 + BN/2) rows instead of (128 + BN).  Both
-// CTAs' TMA bytes are counted on the leader's full barrier; the leader's MMA commits free
-// the stage in both CTAs and signal both epilogues; both epilogues release the accumulator
-// buffer on the leader's barrier.
-template <int BN, int NPASS, int STAGES>
-struct CfgPair {
+// Epilogue warp loop (warps 2..5): drain accumulator buffer t&1 of every tile this unit owns.
+template <int MODE, int BN, bool PAIR, typename Coords>
+TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, uint64_t* tfull, uint64_t* tempty,
+                           int unit, int nunits, int total, Coords coords, int warp, int lane) {
+    const int q = warp & 3;  // TMEM lane quarter accessible to this warp
+    uint8_t* stg = epi + (warp - 2) * 2 * EPI_BUF;
+    float* sw3 = reinterpret_cast<float*>(epi + EPI_BYTES);
+    if (MODE == FWD_) load_epi_smem(P, sw3, threadIdx.x - 64);
+    const uint32_t tempty_leader = PAIR ? mapa_shared(&tempty[0], 0) : 0u;
+    int buf = 0, t = 0;
+    for (int ct = unit; ct < total; ct += nunits, ++t) {
+        int m_tile, n_tile, split;
+        coords(ct, m_tile, n_tile, split);
+        const int acc = t & 1;
+        mbar_wait(&tfull[acc], (t >> 1) & 1);
+        tc_fence_after();
+        const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN);
+        epilogue_tile<MODE, BN>(P, tq, m_tile, n_tile, split, q, lane, stg, buf, sw3);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {  // buffer free for tile t + 2
+            if (PAIR) mbar_arrive_remote(tempty_leader + acc * 8);
+            else mbar_arrive_local(&tempty[acc]);
+        }
+    }
+    if (lane == 0) bulk_wait_all();
+}
+
+// ------------------------------------------------------------------ FWD / DGRAD (halo reuse)
+// The k = 3 taps of a c-block read rows shifted by one of the same activation window, so the
+// A operand is staged ONCE per c-block as a 130-row window (rows m0-1 .. m0+128) and each
+// tap's MMA addresses it at a row offset (FWD: j, DGRAD: 2-j; one 128-byte swizzle row per
+// step -- the swizzle phase follows the absolute shared-memory address).  A and B live in
+// separate rings: SA window stages (released after the third tap) and SB per-tap B stages.
+// Versus per-tap A reloads this cuts A traffic 3 -> 130/128 tiles.
+template <int BN, int NPASS, int SA, int SB, bool PAIR>
+struct CfgHalo {
     static constexpr int NPL = NPASS == 3 ? 2 : 1;
-    static constexpr uint32_t A_BYTES = BM * BK * 2;            // this CTA's 128 rows
-    static constexpr uint32_t B_BYTES = (BN / 2) * BK * 2;      // this CTA's half of B
-    static constexpr uint32_t STAGE_BYTES = NPL * (A_BYTES + B_BYTES);
-    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 1024 + 4 * 2 * 2048 + 3 * 512 * 4 + 512 * 4;
-    static constexpr int TMEM_COLS = 2 * BN;
+    static constexpr int A_ROWS = BM + 2;
+    static constexpr uint32_t A_PLANE = 17 * 1024;              // 130 rows, padded to 1 KB
+    static constexpr uint32_t A_STAGE = NPL * A_PLANE;
+    static constexpr uint32_t A_TX = NPL * A_ROWS * 128;        // bytes the window loads deliver
+    static constexpr int BR = PAIR ? BN / 2 : BN;               // B rows (FWD) / columns (DGRAD) here
+    static constexpr uint32_t B_PLANE = BR * BK * 2;
+    static constexpr uint32_t B_STAGE = NPL * B_PLANE;
+    static constexpr uint32_t RINGS = SA * A_STAGE + SB * B_STAGE;
+    static constexpr uint32_t SMEM = RINGS + 1024 /*align*/ + 1024 /*barriers*/ + EPI_SMEM;
+    static constexpr int TMEM_COLS = 2 * BN;  // two accumulator buffers
 };
 
-template <int MODE, int BN, int NPASS, int STAGES>
-__global__ void __launch_bounds__(NTHREADS, 1) umma_pair_kernel(const __grid_constant__ UmmaParams P) {
-    using C_ = CfgPair<BN, NPASS, STAGES>;
+template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR>
+__global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_constant__ UmmaParams P) {
+    static_assert(MODE == FWD_ || MODE == DGRAD_, "halo kernel: FWD / DGRAD");
+    using C_ = CfgHalo<BN, NPASS, SA, SB, PAIR>;
     constexpr int NPL = C_::NPL;
-    constexpr bool A_MN = (MODE == WGRAD_);
-    constexpr bool B_MN = (MODE != FWD_);
-    constexpr int BH = BN / 2;  // B columns held by this CTA
+    constexpr bool B_MN = (MODE == DGRAD_);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C_::STAGE_BYTES);
-    uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;  // [2]
-    uint64_t* tempty = tfull + 2;      // [2] (used in the leader)
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + SA * C_::A_STAGE;
+    uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + C_::RINGS);
+    uint64_t* emptyA = fullA + SA;
+    uint64_t* fullB = emptyA + SA;
+    uint64_t* emptyB = fullB + SB;
+    uint64_t* tfull = emptyB + SB;  // [2]
+    uint64_t* tempty = tfull + 2;   // [2]
     uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint8_t* epi = smem + C_::RINGS + 1024;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_ctarank();
+    const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
     const bool leader = rank == 0;
-    const int pair_id = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-    const int mtiles_p = (P.mtiles + 1) / 2;  // pair tiles along m (256 rows)
-    const int total = mtiles_p * P.ntiles * P.nsplit;
+    const int unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int nunits = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+    const int mt_u = PAIR ? (P.mtiles + 1) / 2 : P.mtiles;
+    const int total = mt_u * P.ntiles;
+    const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, fullA, 2 * (SA + SB), tfull, tempty, tslot, warp, lane);
 
-    if (warp == 0 && lane == 0) {
-        for (int i = 0; i < 2; ++i) {
-            tma_prefetch(&P.a[i]);
-            tma_prefetch(&P.b[i]);
-        }
-        for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);   // the leader's expect_tx arrive covers both CTAs' bytes
-            mbar_init(&empty[s], 1);  // one multicast commit from the leader's MMA
-        }
-        for (int a = 0; a < 2; ++a) {
-            mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
-        }
-        fence_barrier_init();
-    }
-    if (warp == 1) tmem_alloc_pair<C_::TMEM_COLS>(tslot);
-    tc_fence_before();
-    __syncthreads();
-    cluster_sync();
-    tc_fence_after();
-    const uint32_t tbase = *tslot;
-
-    auto tile_coords = [&](int ct, int& mp, int& n_tile, int& split) {
+    auto coords = [&](int ct, int& m_tile, int& n_tile, int& split) {
         n_tile = ct % P.ntiles;
-        const int rest = ct / P.ntiles;
-        mp = rest % mtiles_p;
-        split = rest / mtiles_p;
-    };
-    auto kblocks = [&](int split, int& p_begin) -> int {
-        if (MODE == WGRAD_) {
-            p_begin = split * P.ksplit_rows;
-            const int p_end = min(P.R, p_begin + P.ksplit_rows);
-            return (p_end - p_begin + BK - 1) / BK;
-        }
-        p_begin = 0;
-        return 3 * P.cpb;
+        const int mu = ct / P.ntiles;
+        m_tile = PAIR ? mu * 2 + (int)rank : mu;
+        split = 0;
     };
 
     if (warp == 0) {
         if (lane == 0) {
-            // ===================== TMA producer (both CTAs) =====================
-            int it = 0;
-            for (int ct = pair_id; ct < total; ct += npairs) {
-                int mp, n_tile, split, p_begin;
-                tile_coords(ct, mp, n_tile, split);
-                const int nkb = kblocks(split, p_begin);
-                const int m0 = mp * 2 * BM + (int)rank * BM;  // this CTA's 128 rows
-                for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const int s = it % STAGES;
-                    const uint32_t ph = (it / STAGES) & 1;
-                    mbar_wait(&empty[s], ph ^ 1);
-                    uint8_t* st = smem + s * C_::STAGE_BYTES;
-                    // Only the leader arms the barrier (both halves' bytes); the peer's loads
-                    // complete_tx on it directly.  The peer issues after empty[s] flipped, so the
-                    // barrier is already in this phase; a transiently negative tx-count is legal.
-                    if (leader) mbar_arrive_expect_tx(&full[s], 2 * C_::STAGE_BYTES);
+            // ===================== TMA producer (both CTAs of a pair) =====================
+            int ia = 0, ib = 0;
+            for (int ct = unit; ct < total; ct += nunits) {
+                int m_tile, n_tile, split;
+                coords(ct, m_tile, n_tile, split);
+                const int m0 = m_tile * BM;
+                const int n0 = n_tile * BN + (int)rank * C_::BR;
+                for (int cb = 0; cb < P.cpb; ++cb) {
+                    const int sa = ia % SA;
+                    mbar_wait(&emptyA[sa], ((ia / SA) & 1) ^ 1);
+                    if (leader) mbar_arrive_expect_tx(&fullA[sa], (PAIR ? 2 : 1) * C_::A_TX);
 #pragma unroll
-                    for (int pl = 0; pl < NPL; ++pl) {
-                        uint8_t* sa = st + pl * C_::A_BYTES;
-                        uint8_t* sb = st + NPL * C_::A_BYTES + pl * C_::B_BYTES;
-                        if (MODE == FWD_) {
-                            const int j = kb / P.cpb, c0 = (kb % P.cpb) * BK;
-                            tma_load_2d_pair(sa, &P.a[pl], &full[s], c0, m0 + j - 1);
-                            tma_load_2d_pair(sb, &P.b[pl], &full[s], j * P.Kc + c0, n_tile * BN + (int)rank * BH);
-                        } else if (MODE == DGRAD_) {
-                            const int j = kb / P.cpb, o0 = (kb % P.cpb) * BK;
-                            tma_load_2d_pair(sa, &P.a[pl], &full[s], o0, m0 + 1 - j);
+                    for (int pl = 0; pl < NPL; ++pl)
+                        ld2d<PAIR>(sA + sa * C_::A_STAGE + pl * C_::A_PLANE, &P.a[pl], &fullA[sa], cb * BK, m0 - 1);
+                    ++ia;
+                    for (int j = 0; j < 3; ++j, ++ib) {
+                        const int sb = ib % SB;
+                        mbar_wait(&emptyB[sb], ((ib / SB) & 1) ^ 1);
+                        if (leader) mbar_arrive_expect_tx(&fullB[sb], (PAIR ? 2 : 1) * C_::B_STAGE);
 #pragma unroll
-                            for (int q = 0; q < BH / 64; ++q)
-                                tma_load_3d_pair(sb + q * (BK * 128), &P.b[pl], &full[s],
-                                                 n_tile * BN + (int)rank * BH + 64 * q, j, o0);
-                        } else {  // WGRAD: m = output channel o (this CTA: 128 of the 256)
-                            const int p0 = p_begin + kb * BK;
+                        for (int pl = 0; pl < NPL; ++pl) {
+                            uint8_t* dst = sB + sb * C_::B_STAGE + pl * C_::B_PLANE;
+                            if (MODE == FWD_) {
+                                ld2d<PAIR>(dst, &P.b[pl], &fullB[sb], j * P.Kc + cb * BK, n0);
+                            } else {
 #pragma unroll
-                            for (int q = 0; q < BM / 64; ++q)
-                                tma_load_2d_pair(sa + q * (BK * 128), &P.a[pl], &full[s], m0 + 64 * q, p0);
-#pragma unroll
-                            for (int q = 0; q < BH / 64; ++q) {
-                                uint8_t* dst = sb + q * (BK * 128);
-                                int g = n_tile * (BN / 64) + (int)rank * (BH / 64) + q;
-                                if (P.ones_chunk && g == 3 * P.cpj) {
-                                    tma_load_2d_pair(dst, &P.ones, &full[s], 64 * pl, p0);
-                                    continue;
-                                }
-                                if (g >= 3 * P.cpj) g = 3 * P.cpj - 1;
-                                const int j = g / P.cpj, c0 = (g % P.cpj) * 64;
-                                tma_load_2d_pair(dst, &P.b[pl], &full[s], c0, p0 + j - 1);
+                                for (int q = 0; q < C_::BR / 64; ++q)
+                                    ld3d<PAIR>(dst + q * (BK * 128), &P.b[pl], &fullB[sb], n0 + 64 * q, j, cb * BK);
                             }
                         }
                     }
@@ -585,12 +425,149 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_pair_kernel(const __grid_con
         }
     } else if (warp == 1) {
         if (lane == 0 && leader) {
-            // ===================== MMA issuer (leader only) =====================
-            constexpr uint32_t idesc = make_idesc_bf16(2 * BM, BN, A_MN, B_MN);
+            // ===================== MMA issuer =====================
+            constexpr uint32_t idesc = make_idesc_bf16(PAIR ? 2 * BM : BM, BN, false, B_MN);
+            int ia = 0, ib = 0, t = 0;
+            for (int ct = unit; ct < total; ct += nunits, ++t) {
+                const int acc = t & 1;
+                mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);  // epilogue drained this buffer
+                tc_fence_after();
+                const uint32_t dt = tbase + (uint32_t)(acc * BN);
+                for (int cb = 0; cb < P.cpb; ++cb) {
+                    const int sa = ia % SA;
+                    mbar_wait(&fullA[sa], (ia / SA) & 1);
+                    tc_fence_after();
+                    const uint32_t a_st = smem_u32(sA + sa * C_::A_STAGE);
+                    for (int j = 0; j < 3; ++j, ++ib) {
+                        const int sb = ib % SB;
+                        mbar_wait(&fullB[sb], (ib / SB) & 1);
+                        tc_fence_after();
+                        const uint32_t b_st = smem_u32(sB + sb * C_::B_STAGE);
+                        const uint32_t roff = (uint32_t)((MODE == FWD_ ? j : 2 - j) * 128);
+#pragma unroll
+                        for (int k = 0; k < BK / UK; ++k) {
+#pragma unroll
+                            for (int pass = 0; pass < NPASS; ++pass) {
+                                const int pa = (pass == 2) ? 1 : 0;  // hi*hi, hi*lo, lo*hi
+                                const int pb = (pass == 1) ? 1 : 0;
+                                const uint64_t ad = make_desc(a_st + pa * C_::A_PLANE + roff + k * (UK * 2), 16, 1024);
+                                const uint32_t b_addr = b_st + pb * C_::B_PLANE;
+                                const uint64_t bd = B_MN ? make_desc(b_addr + k * (UK * 128), BK * 128, 1024)
+                                                         : make_desc(b_addr + k * (UK * 2), 16, 1024);
+                                issue_mma<PAIR>(dt, ad, bd, idesc, (cb | j | k | pass) != 0 ? 1u : 0u);
+                            }
+                        }
+                        commit_to<PAIR>(&emptyB[sb]);
+                    }
+                    commit_to<PAIR>(&emptyA[sa]);  // window consumed by all three taps
+                    ++ia;
+                }
+                commit_to<PAIR>(&tfull[acc]);  // accumulator complete
+            }
+        }
+        __syncwarp();
+    } else {
+        epilogue_loop<MODE, BN, PAIR>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane);
+    }
+    gemm_epilogue_done<C_::TMEM_COLS, PAIR>(tbase, warp);
+}
+
+// ------------------------------------------------------------------ WGRAD (split-K)
+// m = output channel o (128 per CTA), n = (tap, input-channel chunk) columns [+ the all-ones
+// bias chunk], K = snippet rows of split s.  Both operands MN-major.
+template <int BN, int NPASS, int STAGES, bool PAIR>
+struct CfgW {
+    static constexpr int NPL = NPASS == 3 ? 2 : 1;
+    static constexpr int BR = PAIR ? BN / 2 : BN;
+    static constexpr uint32_t A_BYTES = BM * BK * 2;
+    static constexpr uint32_t B_BYTES = BR * BK * 2;
+    static constexpr uint32_t STAGE_BYTES = NPL * (A_BYTES + B_BYTES);
+    static constexpr uint32_t SMEM = STAGES * STAGE_BYTES + 1024 + 1024 + EPI_SMEM;
+    static constexpr int TMEM_COLS = 2 * BN;
+};
+
+template <int BN, int NPASS, int STAGES, bool PAIR>
+__global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_constant__ UmmaParams P) {
+    using C_ = CfgW<BN, NPASS, STAGES, PAIR>;
+    constexpr int NPL = C_::NPL;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C_::STAGE_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;  // [2]
+    uint64_t* tempty = tfull + 2;      // [2]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint8_t* epi = smem + STAGES * C_::STAGE_BYTES + 1024;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+    const bool leader = rank == 0;
+    const int unit = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int nunits = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+    const int mt_u = PAIR ? (P.mtiles + 1) / 2 : P.mtiles;
+    const int total = mt_u * P.ntiles * P.nsplit;
+    const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, full, 2 * STAGES, tfull, tempty, tslot, warp, lane);
+
+    auto coords = [&](int ct, int& m_tile, int& n_tile, int& split) {
+        n_tile = ct % P.ntiles;
+        const int rest = ct / P.ntiles;
+        const int mu = rest % mt_u;
+        split = rest / mt_u;
+        m_tile = PAIR ? mu * 2 + (int)rank : mu;
+    };
+    auto kblocks = [&](int split, int& p_begin) -> int {
+        p_begin = split * P.ksplit_rows;
+        const int p_end = min(P.R, p_begin + P.ksplit_rows);
+        return (p_end - p_begin + BK - 1) / BK;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ===================== TMA producer =====================
+            int it = 0;
+            for (int ct = unit; ct < total; ct += nunits) {
+                int m_tile, n_tile, split, p_begin;
+                coords(ct, m_tile, n_tile, split);
+                const int nkb = kblocks(split, p_begin);
+                const int m0 = m_tile * BM;
+                for (int kb = 0; kb < nkb; ++kb, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+                    uint8_t* st = smem + s * C_::STAGE_BYTES;
+                    if (leader) mbar_arrive_expect_tx(&full[s], (PAIR ? 2 : 1) * C_::STAGE_BYTES);
+                    const int p0 = p_begin + kb * BK;
+#pragma unroll
+                    for (int pl = 0; pl < NPL; ++pl) {
+                        uint8_t* sa = st + pl * C_::A_BYTES;
+                        uint8_t* sb = st + NPL * C_::A_BYTES + pl * C_::B_BYTES;
+#pragma unroll
+                        for (int q = 0; q < BM / 64; ++q)
+                            ld2d<PAIR>(sa + q * (BK * 128), &P.a[pl], &full[s], m0 + 64 * q, p0);
+#pragma unroll
+                        for (int q = 0; q < C_::BR / 64; ++q) {
+                            uint8_t* dst = sb + q * (BK * 128);
+                            int g = n_tile * (BN / 64) + (int)rank * (C_::BR / 64) + q;
+                            if (P.ones_chunk && g == 3 * P.cpj) {
+                                // all-ones chunk (lo plane: zeros): D column = sum_p dA[p][o]
+                                ld2d<PAIR>(dst, &P.ones, &full[s], 64 * pl, p0);
+                                continue;
+                            }
+                            if (g >= 3 * P.cpj) g = 3 * P.cpj - 1;  // dummy chunk, discarded
+                            const int j = g / P.cpj, c0 = (g % P.cpj) * 64;
+                            ld2d<PAIR>(dst, &P.b[pl], &full[s], c0, p0 + j - 1);
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && leader) {
+            // ===================== MMA issuer =====================
+            constexpr uint32_t idesc = make_idesc_bf16(PAIR ? 2 * BM : BM, BN, true, true);
             int it = 0, t = 0;
-            for (int ct = pair_id; ct < total; ct += npairs, ++t) {
-                int mp, n_tile, split, p_begin;
-                tile_coords(ct, mp, n_tile, split);
+            for (int ct = unit; ct < total; ct += nunits, ++t) {
+                int m_tile, n_tile, split, p_begin;
+                coords(ct, m_tile, n_tile, split);
                 const int nkb = kblocks(split, p_begin);
                 const int acc = t & 1;
                 mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
@@ -598,8 +575,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_pair_kernel(const __grid_con
                 const uint32_t dt = tbase + (uint32_t)(acc * BN);
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
                     const int s = it % STAGES;
-                    const uint32_t ph = (it / STAGES) & 1;
-                    mbar_wait(&full[s], ph);
+                    mbar_wait(&full[s], (it / STAGES) & 1);
                     tc_fence_after();
                     const uint32_t st = smem_u32(smem + s * C_::STAGE_BYTES);
 #pragma unroll
@@ -608,57 +584,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_pair_kernel(const __grid_con
                         for (int pass = 0; pass < NPASS; ++pass) {
                             const int pa = (pass == 2) ? 1 : 0;
                             const int pb = (pass == 1) ? 1 : 0;
-                            const uint32_t a_addr = st + pa * C_::A_BYTES;
-                            const uint32_t b_addr = st + NPL * C_::A_BYTES + pb * C_::B_BYTES;
-                            const uint64_t ad = A_MN ? make_desc(a_addr + k * (UK * 128), BK * 128, 1024)
-                                                     : make_desc(a_addr + k * (UK * 2), 16, 1024);
-                            const uint64_t bd = B_MN ? make_desc(b_addr + k * (UK * 128), BK * 128, 1024)
-                                                     : make_desc(b_addr + k * (UK * 2), 16, 1024);
-                            mma_bf16_pair(dt, ad, bd, idesc, (kb | k | pass) != 0 ? 1u : 0u);
+                            const uint64_t ad = make_desc(st + pa * C_::A_BYTES + k * (UK * 128), BK * 128, 1024);
+                            const uint64_t bd = make_desc(st + NPL * C_::A_BYTES + pb * C_::B_BYTES + k * (UK * 128),
+                                                          BK * 128, 1024);
+                            issue_mma<PAIR>(dt, ad, bd, idesc, (kb | k | pass) != 0 ? 1u : 0u);
                         }
                     }
-                    mma_commit_pair(&empty[s]);
+                    commit_to<PAIR>(&empty[s]);
                 }
-                mma_commit_pair(&tfull[acc]);
+                commit_to<PAIR>(&tfull[acc]);
             }
         }
         __syncwarp();
     } else {
-        // ===================== epilogue (warps 2..5, both CTAs) =====================
-        const int q = warp & 3;
-        const uint32_t tempty_leader = mapa_shared(&tempty[0], 0);
-        uint8_t* stg = smem + STAGES * C_::STAGE_BYTES + 1024 + (warp - 2) * 2 * EPI_BUF;
-        float* sw3 = reinterpret_cast<float*>(smem + STAGES * C_::STAGE_BYTES + 1024 + EPI_BYTES);
-        if (MODE == FWD_) load_epi_smem(P, sw3, threadIdx.x - 64);
-        int buf = 0, t = 0;
-        for (int ct = pair_id; ct < total; ct += npairs, ++t) {
-            int mp, n_tile, split, p_begin;
-            tile_coords(ct, mp, n_tile, split);
-            const int acc = t & 1;
-            const int m_tile = mp * 2 + (int)rank;  // 128-row tile index of this CTA
-            mbar_wait(&tfull[acc], (t >> 1) & 1);
-            tc_fence_after();
-            const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN);
-            epilogue_tile<MODE, BN>(P, tq, m_tile, n_tile, split, q, lane, stg, buf, sw3);
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_remote(tempty_leader + acc * 8);  // free the buffer (leader's barrier)
-        }
-        if (lane == 0) bulk_wait_all();
+        epilogue_loop<WGRAD_, BN, PAIR>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane);
     }
-    tc_fence_before();
-    __syncthreads();
-    cluster_sync();
-    if (warp == 1) {
-        tc_fence_after();
-        tmem_dealloc_pair<C_::TMEM_COLS>(tbase);
-    }
+    gemm_epilogue_done<C_::TMEM_COLS, PAIR>(tbase, warp);
 }
 
 // ------------------------------------------------------------------ companions
 // x [B][T][Cin] fp32 -> halo-padded hi/lo bf16 planes [B][T+2][Cin].
 __global__ void prep_x_split_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ hi,
                                     __nv_bfloat16* __restrict__ lo, int B, int Tn, int Cin) {
+    pdl_trigger();
+    pdl_wait();
     const int per_row = Cin / 4;
     const int64_t total = (int64_t)B * (Tn + 2) * per_row;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -687,6 +636,8 @@ __global__ void prep_x_split_kernel(const float* __restrict__ x, __nv_bfloat16* 
 // bias gradient = sum of nbp per-m-tile column sums (ascending m).  Both fixed order.
 __global__ void reduce_wgrad_kernel(const float* __restrict__ part, int64_t part_stride, int S, int64_t nW,
                                     const float* __restrict__ bpart, int nbp, int C, float* __restrict__ dst) {
+    pdl_trigger();
+    pdl_wait();
     const int64_t nvw = nW / 4, nvb = nbp > 0 ? C / 4 : 0;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvw + nvb;
          v += (int64_t)gridDim.x * blockDim.x) {
@@ -795,110 +746,103 @@ bool map_store_part(CUtensorMap* m, float* base, uint64_t NW, uint64_t rows, uin
            CUDA_SUCCESS;
 }
 
-// Launch a persistent cluster grid: as many clusters as fit (<= cluster tiles).
-template <int MODE, int BN, int NPASS, int STAGES, int CM, int CN>
-cudaError_t launch_one(const UmmaParams& p, cudaStream_t s) {
-    using C_ = umma::Cfg<BN, NPASS, STAGES>;
-    auto k = umma::umma_conv_kernel<MODE, BN, NPASS, STAGES, CM, CN>;
-    static int max_clusters = -1;
+// Persistent launch: as many units (CTAs, or 2-CTA clusters) as fit, <= the tile count.
+template <typename K>
+cudaError_t launch_persistent(K k, uint32_t smem, bool pair, int total, int* max_units, const UmmaParams& p,
+                              cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CM;
-    attr[0].val.clusterDim.y = CN;
-    attr[0].val.clusterDim.z = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl_enabled()) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    if (pair) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = 2;
+        attr[na].val.clusterDim.y = 1;
+        attr[na++].val.clusterDim.z = 1;
+    }
     cfg.blockDim = dim3(umma::NTHREADS);
-    cfg.dynamicSmemBytes = C_::SMEM;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (max_clusters < 0) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM);
+    cfg.numAttrs = na;
+    if (*max_units < 0) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         int sms = 148;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-        cfg.gridDim = dim3(CM * (sms / (CM * CN)), CN, 1);
         int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess || n <= 0) {
-            cudaGetLastError();
-            n = sms / (CM * CN);
+        if (pair) {
+            cfg.gridDim = dim3(2 * (sms / 2), 1, 1);
+            if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess || n <= 0) {
+                cudaGetLastError();
+                n = sms / 2;
+            }
+        } else {
+            int per_sm = 0;
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, umma::NTHREADS, smem) != cudaSuccess ||
+                per_sm <= 0) {
+                cudaGetLastError();
+                per_sm = 1;
+            }
+            n = per_sm * sms;
         }
-        max_clusters = n;
+        *max_units = n;
     }
-    const int total = ((p.mtiles + CM - 1) / CM) * (p.ntiles / CN) * p.nsplit;
-    const int ncl = total < max_clusters ? total : max_clusters;
-    if (ncl <= 0) return cudaSuccess;
-    cfg.gridDim = dim3(CM * ncl, CN, 1);
+    const int units = total < *max_units ? total : *max_units;
+    if (units <= 0) return cudaSuccess;
+    cfg.gridDim = dim3((pair ? 2 : 1) * units, 1, 1);
     return cudaLaunchKernelEx(&cfg, k, p);
 }
 
-template <int MODE, int BN, int NPASS, int STAGES>
-cudaError_t launch_pair(const UmmaParams& p, cudaStream_t s) {
-    using C_ = umma::CfgPair<BN, NPASS, STAGES>;
-    auto k = umma::umma_pair_kernel<MODE, BN, NPASS, STAGES>;
-    static int max_clusters = -1;
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.blockDim = dim3(umma::NTHREADS);
-    cfg.dynamicSmemBytes = C_::SMEM;
-    cfg.stream = s;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (max_clusters < 0) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM);
-        if (e != cudaSuccess) return e;
-        int sms = 148;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-        cfg.gridDim = dim3(2 * (sms / 2), 1, 1);
-        int n = 0;
-        if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess || n <= 0) {
-            cudaGetLastError();
-            n = sms / 2;
-        }
-        max_clusters = n;
-    }
-    const int total = ((p.mtiles + 1) / 2) * p.ntiles * p.nsplit;
-    const int npairs = total < max_clusters ? total : max_clusters;
-    if (npairs <= 0) return cudaSuccess;
-    cfg.gridDim = dim3(2 * npairs, 1, 1);
-    return cudaLaunchKernelEx(&cfg, k, p);
+template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR>
+cudaError_t launch_halo(const UmmaParams& p, cudaStream_t s) {
+    static int max_units = -1;
+    const int total = (PAIR ? (p.mtiles + 1) / 2 : p.mtiles) * p.ntiles;
+    return launch_persistent(umma::umma_halo_kernel<MODE, BN, NPASS, SA, SB, PAIR>,
+                             umma::CfgHalo<BN, NPASS, SA, SB, PAIR>::SMEM, PAIR, total, &max_units, p, s);
+}
+
+template <int BN, int NPASS, int STAGES, bool PAIR>
+cudaError_t launch_wgrad(const UmmaParams& p, cudaStream_t s) {
+    static int max_units = -1;
+    const int total = (PAIR ? (p.mtiles + 1) / 2 : p.mtiles) * p.ntiles * p.nsplit;
+    return launch_persistent(umma::umma_wgrad_kernel<BN, NPASS, STAGES, PAIR>,
+                             umma::CfgW<BN, NPASS, STAGES, PAIR>::SMEM, PAIR, total, &max_units, p, s);
 }
 
 }  // namespace
 
-// Tile / cluster configurations (BN, STAGES, CM, CN) per GEMM and precision.
-//   1-pass bf16: FWD/DGRAD 128x256 tiles, B multicast over 2 m-tiles; WGRAD 128x256,
-//                B multicast over the 4 o-tiles.
-//   3-pass fp32: FWD/DGRAD 128x64 tiles, cluster 2 (m) x 4 (n): A multicast over 4 n-tiles,
-//                B over 2 m-tiles; WGRAD 128x128, B multicast over the 4 o-tiles.
+// Tile configurations per GEMM and precision (measured on B200):
+//   1-pass bf16: 2-CTA pairs, 256 x 256 tiles (FWD/DGRAD: 4 window + 8 tap stages; WGRAD 6).
+//   3-pass fp32: 1 CTA, FWD/DGRAD 128 x 64 tiles (3 window + 6 tap stages), WGRAD 128 x 128
+//                (3 stages) -- the small B = 16 problem needs the SM count more than the
+//                per-SM ingress saving of pairs.
+// TEM_GEMM_VARIANT (experiments): unset = auto (as above), 1 = 1-CTA everywhere, 2 = pairs
+// everywhere.
 struct GemmCfg {
-    int bn, stages, cm, cn;
+    int bn;
     int pair;  // 1: 2-CTA kernel (256-row pair tiles, cta_group::2)
 };
-// TEM_GEMM_VARIANT (experiments): unset = auto (2-CTA pairs for the 1-pass bf16 GEMMs, 1-CTA
-// for the 3-pass fp32 ones -- the measured winners on B200), 1 = 1-CTA without clusters,
-// 2 = 2-CTA pairs everywhere, 0 = 1-CTA with multicast clusters.
 static int gemm_variant() {
     const char* e = getenv("TEM_GEMM_VARIANT");
     return e ? atoi(e) : -1;
 }
 static GemmCfg cfg_for(int mode, int npass) {
     int v = gemm_variant();
-    if (v < 0) v = npass == 1 ? 2 : 1;
+    if (v == 3) {  // experiment: fp32 FWD as 2-CTA pairs of 256 x 64 (DGRAD's MN-major B needs >= 64 per CTA)
+        if (npass == 3 && mode == FWD_) return GemmCfg{64, 1};
+        v = npass == 1 ? 2 : 1;
+    }
+    if (v != 1 && v != 2) v = npass == 1 ? 2 : 1;
     if (v == 2) {
-        if (npass == 1) return GemmCfg{256, 6, 1, 1, 1};
-        return mode == WGRAD_ ? GemmCfg{256, 3, 1, 1, 1} : GemmCfg{128, 4, 1, 1, 1};
+        if (npass == 1) return GemmCfg{256, 1};
+        return mode == WGRAD_ ? GemmCfg{256, 1} : GemmCfg{128, 1};
     }
-    if (v == 1) {
-        if (npass == 1) return GemmCfg{256, 4, 1, 1, 0};
-        return mode == WGRAD_ ? GemmCfg{128, 3, 1, 1, 0} : GemmCfg{64, 4, 1, 1, 0};
-    }
-    if (npass == 1) return mode == WGRAD_ ? GemmCfg{256, 4, 4, 1, 0} : GemmCfg{256, 4, 2, 1, 0};
-    return mode == WGRAD_ ? GemmCfg{128, 3, 4, 1, 0} : GemmCfg{64, 4, 2, 4, 0};
+    if (npass == 1) return GemmCfg{256, 0};
+    return mode == WGRAD_ ? GemmCfg{128, 0} : GemmCfg{64, 0};
 }
 
 int umma_wgrad_splits(const Geom& g) {
@@ -934,10 +878,11 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     const void* dA2[2] = {b.dA2, b.dA2_lo};
     const void* dA1[2] = {b.dA1, b.dA1_lo};
     const __nv_bfloat16* W[2] = {b.shadow, b.shadow_lo};
-    // box rows: multicast slices (1-CTA clusters) or the pair half of B (2-CTA)
-    const uint32_t arK = umma::BM / cf.cn, brK = cf.pair ? cf.bn / 2 : cf.bn / cf.cm;  // FWD/DGRAD K-major A / B
-    const uint32_t brD = umma::BK / cf.cm;                              // DGRAD MN-major B
-    const uint32_t arW = umma::BK / cw.cn, brW = umma::BK / cw.cm;       // WGRAD MN-major A / B
+    // box rows: FWD/DGRAD A = the 130-row halo window; B = this CTA's rows (a pair holds half)
+    const uint32_t arK = umma::BM + 2, brK = cf.pair ? cf.bn / 2 : cf.bn;
+    if (cfg_for(DGRAD_, P.npass).bn != cf.bn) return false;  // FWD and DGRAD share the n-tiling
+    const uint32_t brD = umma::BK;                    // DGRAD MN-major B: 64 o-rows per box
+    const uint32_t arW = umma::BK, brW = umma::BK;     // WGRAD MN-major A / B
     bool ok = true;
     for (int pl = 0; pl < npl; ++pl) {
         const __nv_bfloat16* W1 = W[pl] + g.off_W1;
@@ -1025,9 +970,6 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     if (b.dA1_lo) ok &= map_store2d(&P.dgrad.out[1], b.dA1_lo, false, g.C, R);
     ok &= map_store_part(&P.wgrad2.out[0], b.wpart2, 3 * (uint64_t)g.C, g.C, P.S, P.wgrad2.part_stride);
     ok &= map_store_part(&P.wgrad1.out[0], b.wpart, 3 * (uint64_t)g.Cin, g.C, P.S, P.wgrad1.part_stride);
-    // cluster shapes must tile the tile grids
-    ok &= (P.conv1.ntiles % cf.cn == 0) && (P.wgrad1.mtiles % cw.cm == 0);
-    ok &= (P.wgrad1.ntiles % cw.cn == 0) && (P.wgrad2.ntiles % cw.cn == 0);
     return ok;
 }
 
@@ -1042,21 +984,14 @@ void umma_plan_destroy(UmmaPlan* plan) {
 template <int MODE>
 static cudaError_t dispatch(const UmmaParams& p, int npass, cudaStream_t s) {
     const GemmCfg c = cfg_for(MODE, npass);
-    if (c.pair) {
-        if constexpr (MODE == WGRAD_) {
-            if (npass == 3) return launch_pair<MODE, 256, 3, 3>(p, s);
-            return launch_pair<MODE, 256, 1, 6>(p, s);
-        } else {
-            if (npass == 3) return launch_pair<MODE, 128, 3, 4>(p, s);
-            return launch_pair<MODE, 256, 1, 6>(p, s);
-        }
-    }
     if constexpr (MODE == WGRAD_) {
-        if (npass == 3) return c.cm == 1 ? launch_one<MODE, 128, 3, 3, 1, 1>(p, s) : launch_one<MODE, 128, 3, 3, 4, 1>(p, s);
-        return c.cm == 1 ? launch_one<MODE, 256, 1, 4, 1, 1>(p, s) : launch_one<MODE, 256, 1, 4, 4, 1>(p, s);
+        if (c.pair) return npass == 3 ? launch_wgrad<256, 3, 3, true>(p, s) : launch_wgrad<256, 1, 6, true>(p, s);
+        return npass == 3 ? launch_wgrad<128, 3, 3, false>(p, s) : launch_wgrad<256, 1, 4, false>(p, s);
     } else {
-        if (npass == 3) return c.cm == 1 ? launch_one<MODE, 64, 3, 4, 1, 1>(p, s) : launch_one<MODE, 64, 3, 4, 2, 4>(p, s);
-        return c.cm == 1 ? launch_one<MODE, 256, 1, 4, 1, 1>(p, s) : launch_one<MODE, 256, 1, 4, 2, 1>(p, s);
+        if (c.pair && c.bn == 64) return launch_halo<MODE, 64, 3, 3, 6, true>(p, s);
+        if (c.pair)
+            return npass == 3 ? launch_halo<MODE, 128, 3, 3, 6, true>(p, s) : launch_halo<MODE, 256, 1, 4, 8, true>(p, s);
+        return npass == 3 ? launch_halo<MODE, 64, 3, 3, 6, false>(p, s) : launch_halo<MODE, 256, 1, 3, 4, false>(p, s);
     }
 }
 
@@ -1091,9 +1026,9 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     if (e != cudaSuccess) return e;
     ++n;
     rec2.begin(SLOT_RED2);
-    umma::reduce_wgrad_kernel<<<296, 256, 0, P.aux>>>(b.wpart2, P.wgrad2.part_stride, P.S, (int64_t)g.C * 3 * g.C,
-                                                      nullptr, 0, g.C, b.grad + g.off_W2);
-    e = cudaGetLastError();
+    e = launch_pdl(umma::reduce_wgrad_kernel, dim3(296), dim3(256), 0, P.aux, (const float*)b.wpart2,
+                   P.wgrad2.part_stride, P.S, (int64_t)g.C * 3 * g.C, (const float*)nullptr, 0, g.C,
+                   b.grad + g.off_W2);
     rec2.end(SLOT_RED2);
     if (e != cudaSuccess) return e;
     ++n;
@@ -1109,9 +1044,8 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     if (e != cudaSuccess) return e;
     ++n;
     rec.begin(SLOT_RED1);
-    umma::reduce_wgrad_kernel<<<296, 256, 0, s>>>(b.wpart, P.wgrad1.part_stride, P.S,
-                                                  (int64_t)g.C * 3 * g.Cin + g.C, nullptr, 0, g.C, b.grad + g.off_W1);
-    e = cudaGetLastError();
+    e = launch_pdl(umma::reduce_wgrad_kernel, dim3(296), dim3(256), 0, s, (const float*)b.wpart, P.wgrad1.part_stride,
+                   P.S, (int64_t)g.C * 3 * g.Cin + g.C, (const float*)nullptr, 0, g.C, b.grad + g.off_W1);
     rec.end(SLOT_RED1);
     if (e != cudaSuccess) return e;
     ++n;
@@ -1121,9 +1055,8 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
 }
 
 cudaError_t launch_prep_x_split(const Geom& g, const float* x, void* hi, void* lo, cudaStream_t s) {
-    umma::prep_x_split_kernel<<<296, 256, 0, s>>>(x, static_cast<__nv_bfloat16*>(hi), static_cast<__nv_bfloat16*>(lo),
-                                                 g.B, g.T, g.Cin);
-    return cudaGetLastError();
+    return launch_pdl(umma::prep_x_split_kernel, dim3(296), dim3(256), 0, s, x, static_cast<__nv_bfloat16*>(hi),
+                      static_cast<__nv_bfloat16*>(lo), g.B, g.T, g.Cin);
 }
 
 cudaError_t launch_fill_ones(void* ones, int64_t rows, cudaStream_t s) {
