@@ -172,7 +172,8 @@ float* tem_logits(tem_ctx* ctx, int32_t local_rank);     /* [B][T][3] fp32 z, la
 /* Device address and size of an internal workspace tensor of local rank `local_rank`, for
  * tests: "xp", "h1", "h2", "dA2", "dA1" (halo-padded [B][T+2][C] rows in the path's operand
  * type; h2 fp32), their residual planes "xp_lo", "h1_lo", "dA2_lo", "dA1_lo", and the weight
- * operand copies "shadow", "shadow_lo" ([K_pad] bf16).  NULL / 0 if absent. */
+ * operand copies "shadow", "shadow_lo" ([K_pad] bf16).  Diagnostics: "tstamp_on" / "tstamp"
+ * enable / disable the split-K GEMM phase timestamps ([1024][16] u64 ns).  NULL / 0 if absent. */
 void* tem_debug_buffer(tem_ctx* ctx, int32_t local_rank, const char* name, int64_t* nbytes);
 /* ReLU decisions of the last tem_compute of local rank `local_rank`: writes
  * out[layer][b][t][c] = 1[a_layer > 0] (uint8, layer 0 = conv1, 1 = conv2) into the

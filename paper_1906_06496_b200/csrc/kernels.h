@@ -102,6 +102,7 @@ struct UmmaParams {
     int ksplit_rows;
     int mtiles, ntiles, nsplit;  // tile grid (persistent kernels walk it cluster tile by cluster tile)
     int ones_chunk;      // WGRAD: chunk slot 3*cpj reads the all-ones map (bias gradient column)
+    int kclust;          // FWD/DGRAD: > 0 -> split-K cluster kernel with this many CTAs per tile
     CUtensorMap ones;    // [R][128] bf16: columns 0..63 = 1, 64..127 = 0
 };
 struct UmmaPlan {
@@ -111,6 +112,7 @@ struct UmmaPlan {
     cudaEvent_t fork, join;
 };
 void umma_plan_destroy(UmmaPlan* plan);
+void* umma_tstamp_buffer(int64_t* nbytes, int on);  // split-K phase timestamps (diagnostics)
 int umma_wgrad_splits(const Geom& g);
 bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan);
 cudaError_t launch_fill_ones(void* ones, int64_t rows, cudaStream_t s);

@@ -8,10 +8,14 @@
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
+
+#include <algorithm>
 #include <string.h>
 
 #include <new>
 #include <stdlib.h>
+
+#include <algorithm>
 
 #include "kernels.h"
 
@@ -353,7 +357,7 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
         if (e == cudaSuccess && c->g.path == PATH_UMMA) {
             c->plan[l] = new (std::nothrow) UmmaPlan();
             if (!c->plan[l] || !umma_plan(c->g, b, c->plan[l])) e = cudaErrorInvalidValue;
-            else b.nzpart = c->plan[l]->conv2.zpart ? c->plan[l]->conv2.ntiles : 0;
+            else b.nzpart = c->plan[l]->conv2.zpart ? c->plan[l]->conv2.ntiles * std::max(c->plan[l]->conv2.kclust, 1) : 0;
         }
         if (e != cudaSuccess) {
             for (int q = 0; q <= l; ++q) umma_plan_destroy(c->plan[q]);
@@ -681,6 +685,8 @@ float* tem_logits(tem_ctx* c, int32_t l) {
 void* tem_debug_buffer(tem_ctx* c, int32_t l, const char* name, int64_t* nbytes) {
     if (nbytes) *nbytes = 0;
     if (!c || !c->alive || l < 0 || l >= c->nlocal || !name) return nullptr;
+    if (strcmp(name, "tstamp_on") == 0 || strcmp(name, "tstamp") == 0)
+        return umma_tstamp_buffer(nbytes, strcmp(name, "tstamp_on") == 0 ? 1 : 0);
     const Geom& g = c->g;
     const RankBufs& b = c->rb[l];
     const int64_t esz = g.op_bf16 ? 2 : 4;

@@ -30,6 +30,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
+#include <algorithm>
 #include <stdlib.h>
 #include <string.h>
 
@@ -103,10 +104,14 @@ TEM_DEV void load_epi_smem(const UmmaParams& P, float* sw3, int et) {
 // Per-chunk register set: 16 accumulator columns (+ the DGRAD ReLU-mask words of the chunk).
 struct EpiRegs {
     uint32_t r[16];
+    uint32_t r2[16], r3[16];  // ACC = 3: the hi*lo and lo*hi accumulator slices
     uint32_t mw[8];
 };
 
-template <int MODE, int BN>
+// ACC = 1: one accumulator of BN columns.  ACC = 3 (3-pass split, dual-accumulator MMAs): the
+// accumulator holds [hi*hi | hi*lo] (2 BN columns, one N = 2 BN MMA against the contiguous
+// B hi / lo planes) and lo*hi (BN columns); the epilogue sums (hi*hi + hi*lo) + lo*hi.
+template <int MODE, int BN, int ACC = 1>
 TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_tile, int split, int q,
                            int lane, uint8_t* stg, int& buf, const float* sw3) {
     const int row0 = m_tile * BM + 32 * q;
@@ -119,6 +124,10 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
     // Issue the TMEM load (and the DGRAD mask load) of chunk c16; consumed after tmem_ld_wait.
     auto issue = [&](int c16, EpiRegs& e) {
         tmem_ld16(tq + (uint32_t)(c16 * 16), e.r);
+        if (ACC == 3) {
+            tmem_ld16(tq + (uint32_t)(BN + c16 * 16), e.r2);
+            tmem_ld16(tq + (uint32_t)(2 * BN + c16 * 16), e.r3);
+        }
         if (MODE == DGRAD_) {
             if (!halo) {
                 const uint4* mk = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(P.mask) +
@@ -151,7 +160,10 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
         }
         float v[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(e.r[i]);
+        for (int i = 0; i < 16; ++i) {
+            v[i] = __uint_as_float(e.r[i]);
+            if (ACC == 3) v[i] = (v[i] + __uint_as_float(e.r2[i])) + __uint_as_float(e.r3[i]);
+        }
         if (MODE == FWD_) {
             const float4* bp = reinterpret_cast<const float4*>(sbias + gc);
 #pragma unroll
@@ -216,9 +228,17 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
 #pragma unroll 1
     for (int c16 = 0; c16 < NC; c16 += 2) {
         tmem_ld_wait_regs(ea.r);
+        if (ACC == 3) {
+            tmem_regs_fence(ea.r2);
+            tmem_regs_fence(ea.r3);
+        }
         issue(c16 + 1, eb);
         process(c16, ea);
         tmem_ld_wait_regs(eb.r);
+        if (ACC == 3) {
+            tmem_regs_fence(eb.r2);
+            tmem_regs_fence(eb.r3);
+        }
         if (c16 + 2 < NC) issue(c16 + 2, ea);
         process(c16 + 1, eb);
     }
@@ -303,7 +323,7 @@ TEM_DEV void gemm_epilogue_done(uint32_t tbase, int warp) {
 }
 
 // Epilogue warp loop (warps 2..5): drain accumulator buffer t&1 of every tile this unit owns.
-template <int MODE, int BN, bool PAIR, typename Coords>
+template <int MODE, int BN, bool PAIR, int ACC, typename Coords>
 TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, uint64_t* tfull, uint64_t* tempty,
                            int unit, int nunits, int total, Coords coords, int warp, int lane) {
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
@@ -318,8 +338,8 @@ TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, ui
         const int acc = t & 1;
         mbar_wait(&tfull[acc], (t >> 1) & 1);
         tc_fence_after();
-        const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BN);
-        epilogue_tile<MODE, BN>(P, tq, m_tile, n_tile, split, q, lane, stg, buf, sw3);
+        const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * ACC * BN);
+        epilogue_tile<MODE, BN, ACC>(P, tq, m_tile, n_tile, split, q, lane, stg, buf, sw3);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {  // buffer free for tile t + 2
@@ -328,6 +348,14 @@ TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, ui
         }
     }
     if (lane == 0) bulk_wait_all();
+}
+
+// Phase timestamps of the GEMM kernels (diagnostics: tem_debug_buffer "tstamp",
+// [grid][16] globaltimer ns; written only while g_tstamp_on is set).
+__device__ unsigned long long g_tstamp[1024 * 16];
+__device__ int g_tstamp_on;
+TEM_DEV void tstamp(int k) {
+    if (g_tstamp_on) g_tstamp[blockIdx.x * 16 + k] = globaltimer();
 }
 
 // ------------------------------------------------------------------ FWD / DGRAD (halo reuse)
@@ -349,7 +377,9 @@ struct CfgHalo {
     static constexpr uint32_t B_STAGE = NPL * B_PLANE;
     static constexpr uint32_t RINGS = SA * A_STAGE + SB * B_STAGE;
     static constexpr uint32_t SMEM = RINGS + 1024 /*align*/ + 1024 /*barriers*/ + EPI_SMEM;
-    static constexpr int TMEM_COLS = 2 * BN;  // two accumulator buffers
+    // 3-pass 1-CTA: dual-accumulator MMAs (see epilogue_tile), 3 BN columns per buffer
+    static constexpr int ACC = (NPASS == 3 && !PAIR && 6 * BN <= 512) ? 3 : 1;
+    static constexpr int TMEM_COLS = ACC == 3 ? 512 : 2 * BN;  // two accumulator buffers
 };
 
 template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR>
@@ -378,7 +408,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
     const int nunits = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
     const int mt_u = PAIR ? (P.mtiles + 1) / 2 : P.mtiles;
     const int total = mt_u * P.ntiles;
+    if (threadIdx.x == 0) tstamp(0);
     const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, fullA, 2 * (SA + SB), tfull, tempty, tslot, warp, lane);
+    if (threadIdx.x == 0) tstamp(1);
 
     auto coords = [&](int ct, int& m_tile, int& n_tile, int& split) {
         n_tile = ct % P.ntiles;
@@ -432,10 +464,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                 const int acc = t & 1;
                 mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);  // epilogue drained this buffer
                 tc_fence_after();
-                const uint32_t dt = tbase + (uint32_t)(acc * BN);
+                const uint32_t dt = tbase + (uint32_t)(acc * C_::ACC * BN);
                 for (int cb = 0; cb < P.cpb; ++cb) {
                     const int sa = ia % SA;
                     mbar_wait(&fullA[sa], (ia / SA) & 1);
+                    if (ia == 0) tstamp(2);
                     tc_fence_after();
                     const uint32_t a_st = smem_u32(sA + sa * C_::A_STAGE);
                     for (int j = 0; j < 3; ++j, ++ib) {
@@ -446,15 +479,26 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                         const uint32_t roff = (uint32_t)((MODE == FWD_ ? j : 2 - j) * 128);
 #pragma unroll
                         for (int k = 0; k < BK / UK; ++k) {
+                            const uint64_t bd0 = B_MN ? make_desc(b_st + k * (UK * 128), BK * 128, 1024)
+                                                      : make_desc(b_st + k * (UK * 2), 16, 1024);
+                            if (C_::ACC == 3) {
+                                // A_hi x [B_hi | B_lo] (N = 2 BN, planes contiguous), A_lo x B_hi (N = BN)
+                                constexpr uint32_t idesc2 = make_idesc_bf16(BM, 2 * BN, false, B_MN);
+                                const uint32_t acc_on = (cb | j | k) != 0 ? 1u : 0u;
+                                issue_mma<PAIR>(dt, make_desc(a_st + roff + k * (UK * 2), 16, 1024), bd0, idesc2, acc_on);
+                                issue_mma<PAIR>(dt + 2 * BN, make_desc(a_st + C_::A_PLANE + roff + k * (UK * 2), 16, 1024),
+                                                bd0, idesc, acc_on);
+                            } else {
 #pragma unroll
-                            for (int pass = 0; pass < NPASS; ++pass) {
-                                const int pa = (pass == 2) ? 1 : 0;  // hi*hi, hi*lo, lo*hi
-                                const int pb = (pass == 1) ? 1 : 0;
-                                const uint64_t ad = make_desc(a_st + pa * C_::A_PLANE + roff + k * (UK * 2), 16, 1024);
-                                const uint32_t b_addr = b_st + pb * C_::B_PLANE;
-                                const uint64_t bd = B_MN ? make_desc(b_addr + k * (UK * 128), BK * 128, 1024)
-                                                         : make_desc(b_addr + k * (UK * 2), 16, 1024);
-                                issue_mma<PAIR>(dt, ad, bd, idesc, (cb | j | k | pass) != 0 ? 1u : 0u);
+                                for (int pass = 0; pass < NPASS; ++pass) {
+                                    const int pa = (pass == 2) ? 1 : 0;  // hi*hi, hi*lo, lo*hi
+                                    const int pb = (pass == 1) ? 1 : 0;
+                                    const uint64_t ad = make_desc(a_st + pa * C_::A_PLANE + roff + k * (UK * 2), 16, 1024);
+                                    const uint32_t b_addr = b_st + pb * C_::B_PLANE;
+                                    const uint64_t bd = B_MN ? make_desc(b_addr + k * (UK * 128), BK * 128, 1024)
+                                                             : make_desc(b_addr + k * (UK * 2), 16, 1024);
+                                    issue_mma<PAIR>(dt, ad, bd, idesc, (cb | j | k | pass) != 0 ? 1u : 0u);
+                                }
                             }
                         }
                         commit_to<PAIR>(&emptyB[sb]);
@@ -463,13 +507,330 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                     ++ia;
                 }
                 commit_to<PAIR>(&tfull[acc]);  // accumulator complete
+                tstamp(t == 0 ? 3 : 4);
             }
         }
         __syncwarp();
     } else {
-        epilogue_loop<MODE, BN, PAIR>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane);
+        epilogue_loop<MODE, BN, PAIR, C_::ACC>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane);
+        if (threadIdx.x == 64) tstamp(6);
     }
     gemm_epilogue_done<C_::TMEM_COLS, PAIR>(tbase, warp);
+}
+
+// ------------------------------------------------------------------ FWD / DGRAD, split-K cluster
+// Small-M problems (the fp32 B = 16 step: 13 row tiles) cannot fill 148 SMs with efficient
+// tiles: 128 x 64 tiles use N = 64 MMAs, which B200 runs at 50 clk instead of the 32-clk floor
+// (scripts/probes/mma_probe.cu), and re-stream the A window for every 64 columns.  Here a
+// cluster of S CTAs computes one 128 x 256 tile (N = 256 MMAs, at the floor): CTA r of the
+// cluster accumulates c-blocks [r*cpb/S, (r+1)*cpb/S) of K (halo window reuse as above)
+// into its own TMEM.  Column slice k of the partial tile belongs to CTA k: every CTA packs
+// its S-1 foreign slices into shared memory (the drained operand rings; 16-byte chunks
+// XOR-swizzled by row, bank-conflict free) and ships each with ONE bulk copy
+// (cp.async.bulk shared::cta -> shared::cluster) that completes on the owner's mbarrier.
+// The owner sums its own slice (from TMEM) and the S-1 received ones in rank order
+// 0..S-1 (deterministic), applies the epilogue (bias/ReLU/halo, or ReLU-mask/halo, hi/lo
+// split, fused logits) and stores it.  A final cluster barrier keeps every source buffer
+// alive until all copies have landed.
+template <int NPASS, int SA, int SB>
+struct CfgSplit {
+    static constexpr int BN = 256;
+    static constexpr int NPL = NPASS == 3 ? 2 : 1;
+    static constexpr uint32_t A_PLANE = 17 * 1024;
+    static constexpr uint32_t A_STAGE = NPL * A_PLANE;
+    static constexpr uint32_t A_TX = NPL * (BM + 2) * 128;
+    static constexpr uint32_t B_PLANE = BN * BK * 2;
+    static constexpr uint32_t B_STAGE = NPL * B_PLANE;
+    static constexpr uint32_t RINGS = SA * A_STAGE + SB * B_STAGE;
+    // outgoing [S-1] + received [S-1] slices of [BM][BN/S] fp32 each: 2 (S-1)/S of a tile, S <= 4
+    static constexpr uint32_t XCH_BYTES = 2 * BM * BN * 4 * 3 / 4;
+    static_assert(XCH_BYTES <= RINGS, "the slice buffers reuse the operand rings");
+    static constexpr uint32_t SMEM = RINGS + 1024 /*align*/ + 1024 /*barriers*/ + 4 * 64 * 4 /*bias, W3 slice*/;
+    static constexpr int TMEM_COLS = BN;
+};
+
+template <int MODE, int NPASS, int SA, int SB>
+__global__ void __launch_bounds__(NTHREADS, 1) umma_splitk_kernel(const __grid_constant__ UmmaParams P) {
+    static_assert(MODE == FWD_ || MODE == DGRAD_, "split-K cluster kernel: FWD / DGRAD");
+    using C_ = CfgSplit<NPASS, SA, SB>;
+    constexpr int BN = C_::BN, NPL = C_::NPL;
+    constexpr bool B_MN = (MODE == DGRAD_);
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + SA * C_::A_STAGE;
+    uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + C_::RINGS);
+    uint64_t* emptyA = fullA + SA;
+    uint64_t* fullB = emptyA + SA;
+    uint64_t* emptyB = fullB + SB;
+    uint64_t* tfull = emptyB + SB;
+    uint64_t* recv = tfull + 1;  // received-slices barrier
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(recv + 1);
+    float* sepi = reinterpret_cast<float*>(smem + C_::RINGS + 1024);  // [4][W]: bias, W3 rows of this slice
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int S = (int)cluster_nctarank(), r = (int)cluster_ctarank();
+    const int tile = (int)blockIdx.x / S;
+    const int n_tile = tile % P.ntiles, m_tile = tile / P.ntiles;
+    const int cb0 = r * P.cpb / S, cb1 = (r + 1) * P.cpb / S;  // host: S <= cpb, so cb1 > cb0
+    if (threadIdx.x == 0) tstamp(0);
+
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < 2; ++i) {
+            tma_prefetch(&P.a[i]);
+            tma_prefetch(&P.b[i]);
+        }
+        for (int i = 0; i < 2 * (SA + SB) + 2; ++i) mbar_init(&fullA[i], 1);
+        fence_barrier_init();
+        // the S-1 foreign partial slices of this CTA's columns (complete_tx may precede this)
+        mbar_arrive_expect_tx(recv, (uint32_t)((S - 1) * BM * (BN / S) * 4));
+    }
+    if (warp == 1) tmem_alloc<C_::TMEM_COLS>(tslot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    pdl_trigger();
+    pdl_wait();
+    if (threadIdx.x == 0) tstamp(1);
+    const uint32_t tbase = *tslot;
+    const int m0 = m_tile * BM;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ===================== TMA producer =====================
+            int ib = 0;
+            for (int cb = cb0, ia = 0; cb < cb1; ++cb, ++ia) {
+                const int sa = ia % SA;
+                mbar_wait(&emptyA[sa], ((ia / SA) & 1) ^ 1);
+                mbar_arrive_expect_tx(&fullA[sa], C_::A_TX);
+                if (cb == cb0) tstamp(2);
+#pragma unroll
+                for (int pl = 0; pl < NPL; ++pl)
+                    tma_load_2d(sA + sa * C_::A_STAGE + pl * C_::A_PLANE, &P.a[pl], &fullA[sa], cb * BK, m0 - 1);
+                for (int j = 0; j < 3; ++j, ++ib) {
+                    const int sb = ib % SB;
+                    mbar_wait(&emptyB[sb], ((ib / SB) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&fullB[sb], C_::B_STAGE);
+#pragma unroll
+                    for (int pl = 0; pl < NPL; ++pl) {
+                        uint8_t* dst = sB + sb * C_::B_STAGE + pl * C_::B_PLANE;
+                        if (MODE == FWD_) {
+                            tma_load_2d(dst, &P.b[pl], &fullB[sb], j * P.Kc + cb * BK, n_tile * BN);
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < BN / 64; ++q)
+                                tma_load_3d(dst + q * (BK * 128), &P.b[pl], &fullB[sb], n_tile * BN + 64 * q, j, cb * BK);
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ===================== MMA issuer =====================
+            constexpr uint32_t idesc = make_idesc_bf16(BM, BN, false, B_MN);
+            int ib = 0;
+            for (int cb = cb0, ia = 0; cb < cb1; ++cb, ++ia) {
+                const int sa = ia % SA;
+                mbar_wait(&fullA[sa], (ia / SA) & 1);
+                if (cb == cb0) tstamp(3);
+                tc_fence_after();
+                const uint32_t a_st = smem_u32(sA + sa * C_::A_STAGE);
+                for (int j = 0; j < 3; ++j, ++ib) {
+                    const int sb = ib % SB;
+                    mbar_wait(&fullB[sb], (ib / SB) & 1);
+                    if (cb == cb0 && j == 0) tstamp(4);
+                    tc_fence_after();
+                    const uint32_t b_st = smem_u32(sB + sb * C_::B_STAGE);
+                    const uint32_t roff = (uint32_t)((MODE == FWD_ ? j : 2 - j) * 128);
+#pragma unroll
+                    for (int k = 0; k < BK / UK; ++k) {
+#pragma unroll
+                        for (int pass = 0; pass < NPASS; ++pass) {
+                            const int pa = (pass == 2) ? 1 : 0;
+                            const int pb = (pass == 1) ? 1 : 0;
+                            const uint64_t ad = make_desc(a_st + pa * C_::A_PLANE + roff + k * (UK * 2), 16, 1024);
+                            const uint32_t b_addr = b_st + pb * C_::B_PLANE;
+                            const uint64_t bd = B_MN ? make_desc(b_addr + k * (UK * 128), BK * 128, 1024)
+                                                     : make_desc(b_addr + k * (UK * 2), 16, 1024);
+                            mma_bf16(tbase, ad, bd, idesc, (cb != cb0 || j | k | pass) ? 1u : 0u);
+                        }
+                    }
+                    mma_commit(&emptyB[sb]);
+                }
+                mma_commit(&emptyA[sa]);
+            }
+            mma_commit(tfull);  // partial accumulator complete (all operand reads done)
+            tstamp(5);
+        }
+        __syncwarp();
+    }
+    // Every CTA must have drained its operand rings (all its MMAs complete) before any CTA of
+    // the cluster writes slices into them: the epilogue warps wait for tfull, then the cluster syncs.
+    // Epilogue warps are idle during the mainloop: fetch what the slice epilogue needs that does
+    // not depend on this kernel (bias / W3 slice to smem; the DGRAD ReLU mask of this row).
+    const int Wsl = BN / S;
+    const int erow = 32 * (warp & 3) + lane;
+    uint4 mkr[8];  // DGRAD: mask of this row's slice (W <= 64 columns of bf16), 4 x 2 x 16 B
+    if (warp >= 2) {
+        if (MODE == FWD_) {
+            for (int i = threadIdx.x - 64; i < Wsl; i += 128) {
+                const int gc = n_tile * BN + r * Wsl + i;
+                sepi[i] = P.bias[gc];
+                if (P.zpart) {
+                    sepi[64 + i] = P.w3[gc];
+                    sepi[128 + i] = P.w3[P.Nout + gc];
+                    sepi[192 + i] = P.w3[2 * P.Nout + gc];
+                }
+            }
+        } else {
+            const int p = m0 + erow;
+            const bool on = p < P.R && !halo_row(p, P.Tp);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                mkr[i] = make_uint4(0u, 0u, 0u, 0u);
+                if (on && i < Wsl / 8)
+                    mkr[i] = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(P.mask) +
+                                                                  (size_t)p * P.Nout + n_tile * BN + r * Wsl) + i);
+            }
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        mbar_wait(tfull, 0);
+        tc_fence_after();
+        if (threadIdx.x == 64) tstamp(6);
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    if (threadIdx.x == 64) tstamp(7);
+    if (warp >= 2) {
+        // ===================== ship foreign slices, reduce own slice, epilogue =====================
+        const int q = warp & 3;
+        const int W = BN / S;                     // columns per slice
+        const int NCH = W / 4;                    // 16-byte chunks per slice row
+        const int row = 32 * q + lane;            // TMEM lane = tile row
+        const uint32_t SLICE = BM * W * 4;        // bytes
+        uint8_t* outb = smem;                     // [S-1][BM][W] foreign slices of this CTA
+        uint8_t* rcvb = smem + (S - 1) * SLICE;   // [S-1][BM][W] received slices (slot = source rank order)
+        const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16);
+        auto chunk_off = [&](int c4) { return (uint32_t)(row * W * 4 + ((c4 ^ (row & 7)) * 16)); };
+        // (1) pack: TMEM columns of owner k -> outb[slot k] (slot = k, minus one past r)
+        for (int k = 0; k < S; ++k) {
+            if (k == r) continue;
+            uint8_t* dstb = outb + (k < r ? k : k - 1) * SLICE;
+            for (int c16 = 0; c16 < W / 16; ++c16) {
+                uint32_t v[16];
+                tmem_ld16(tq + (uint32_t)(k * W + c16 * 16), v);
+                tmem_ld_wait_regs(v);
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+                    *reinterpret_cast<uint4*>(dstb + chunk_off(c16 * 4 + i)) =
+                        make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+            }
+        }
+        fence_proxy_async_smem();  // generic-proxy writes -> visible to the bulk copies
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == 64) {
+            tstamp(8);
+            // (2) one bulk copy per owner: my slice for owner k lands in its slot for rank r
+            for (int k = 0; k < S; ++k) {
+                if (k == r) continue;
+                const uint32_t slot = (uint32_t)(r < k ? r : r - 1);
+                bulk_copy_to_peer(mapa_shared(rcvb + slot * SLICE, (uint32_t)k), outb + (k < r ? k : k - 1) * SLICE,
+                                  SLICE, mapa_shared(recv, (uint32_t)k));
+            }
+        }
+        // (3) own slice: sum in rank order (own partial from TMEM), epilogue, store
+        const bool live = m0 + row < P.R;
+        const int p = m0 + row;
+        const bool halo = !live || halo_row(p, P.Tp);
+        const bool zp_on = (MODE == FWD_) && P.zpart != nullptr;
+        mbar_wait(recv, 0);
+        if (threadIdx.x == 64) tstamp(9);
+        float z0 = 0.f, z1 = 0.f, z2 = 0.f;
+        for (int c16 = 0; c16 < W / 16; ++c16) {
+            const int gc = n_tile * BN + r * W + c16 * 16;  // output column of v[0]
+            uint32_t own[16];
+            tmem_ld16(tq + (uint32_t)(r * W + c16 * 16), own);
+            tmem_ld_wait_regs(own);
+            float v[16];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+                bool first = true;
+                for (int k = 0; k < S; ++k) {  // rank order
+                    float4 b;
+                    if (k == r) {
+                        b = make_float4(__uint_as_float(own[4 * i]), __uint_as_float(own[4 * i + 1]),
+                                        __uint_as_float(own[4 * i + 2]), __uint_as_float(own[4 * i + 3]));
+                    } else {
+                        b = *reinterpret_cast<const float4*>(rcvb + (k < r ? k : k - 1) * SLICE + chunk_off(c16 * 4 + i));
+                    }
+                    if (first) {
+                        a = b;
+                        first = false;
+                    } else {
+                        a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+                    }
+                }
+                v[4 * i] = a.x; v[4 * i + 1] = a.y; v[4 * i + 2] = a.z; v[4 * i + 3] = a.w;
+            }
+            if (MODE == FWD_) {
+                const float* sb = sepi + c16 * 16;  // smem broadcast reads
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const float t = v[i] + sb[i];
+                    v[i] = (!halo && t > 0.f) ? t : 0.f;
+                }
+                if (zp_on) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        z0 = fmaf(sb[64 + i], v[i], z0);
+                        z1 = fmaf(sb[128 + i], v[i], z1);
+                        z2 = fmaf(sb[192 + i], v[i], z2);
+                    }
+                }
+            } else {
+                uint4 mk0 = mkr[0], mk1 = mkr[1];  // chunk c16 of the prefetched row mask
+#pragma unroll
+                for (int i = 1; i < 4; ++i)
+                    if (c16 == i) {
+                        mk0 = mkr[2 * i];
+                        mk1 = mkr[2 * i + 1];
+                    }
+                const uint32_t mw[8] = {mk0.x, mk0.y, mk0.z, mk0.w, mk1.x, mk1.y, mk1.z, mk1.w};
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    v[2 * i] = __uint_as_float(mw[i] << 16) > 0.f ? v[2 * i] : 0.f;
+                    v[2 * i + 1] = __uint_as_float(mw[i] & 0xFFFF0000u) > 0.f ? v[2 * i + 1] : 0.f;
+                }
+            }
+            if (live) {
+                if (P.out_f32) {
+                    float4* d = reinterpret_cast<float4*>(static_cast<float*>(P.out_hi) + (size_t)p * P.Nout + gc);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+                } else {
+                    store16_planes(static_cast<__nv_bfloat16*>(P.out_hi) + (size_t)p * P.Nout + gc,
+                                   P.out_lo ? static_cast<__nv_bfloat16*>(P.out_lo) + (size_t)p * P.Nout + gc : nullptr,
+                                   v);
+                }
+            }
+        }
+        if (zp_on && live) {
+            float* zp = P.zpart + ((size_t)(n_tile * S + r) * P.R + p) * 3;
+            zp[0] = z0;
+            zp[1] = z1;
+            zp[2] = z2;
+        }
+    }
+    tc_fence_before();
+    cluster_sync();  // every bulk copy has landed (owners waited on them): sources may be released
+    if (threadIdx.x == 64) tstamp(10);
+    if (warp == 1) {  // every TMEM read finished before the second cluster barrier
+        tc_fence_after();
+        tmem_dealloc<C_::TMEM_COLS>(tbase);
+    }
 }
 
 // ------------------------------------------------------------------ WGRAD (split-K)
@@ -597,7 +958,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
         }
         __syncwarp();
     } else {
-        epilogue_loop<WGRAD_, BN, PAIR>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane);
+        epilogue_loop<WGRAD_, BN, PAIR, 1>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane);
     }
     gemm_epilogue_done<C_::TMEM_COLS, PAIR>(tbase, warp);
 }
@@ -805,6 +1166,40 @@ cudaError_t launch_halo(const UmmaParams& p, cudaStream_t s) {
                              umma::CfgHalo<BN, NPASS, SA, SB, PAIR>::SMEM, PAIR, total, &max_units, p, s);
 }
 
+template <int MODE, int NPASS, int SA, int SB>
+cudaError_t launch_splitk(const UmmaParams& p, cudaStream_t s) {
+    using C_ = umma::CfgSplit<NPASS, SA, SB>;
+    auto k = umma::umma_splitk_kernel<MODE, NPASS, SA, SB>;
+    static bool init = false;
+    if (!init) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM);
+        if (e != cudaSuccess) return e;
+        if (p.kclust > 8)
+            cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        init = true;
+    }
+    const int tiles = p.mtiles * p.ntiles;
+    if (tiles <= 0) return cudaSuccess;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl_enabled()) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = p.kclust;
+    attr[na].val.clusterDim.y = 1;
+    attr[na++].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(tiles * p.kclust, 1, 1);
+    cfg.blockDim = dim3(umma::NTHREADS);
+    cfg.dynamicSmemBytes = C_::SMEM;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, k, p);
+}
+
 template <int BN, int NPASS, int STAGES, bool PAIR>
 cudaError_t launch_wgrad(const UmmaParams& p, cudaStream_t s) {
     static int max_units = -1;
@@ -939,6 +1334,25 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     P.dgrad.mask = b.h1;
     P.dgrad.out_hi = b.dA1;
     P.dgrad.out_lo = b.dA1_lo;
+    // Experimental (TEM_SPLITK=1): small-M fp32 FWD / DGRAD as split-K clusters of 128 x 256
+    // tiles (umma_splitk_kernel).  Correct, but on B200 the slice exchange costs what the
+    // N = 256 mainloop saves at B = 16, so the halo kernel is the default.
+    if (P.npass == 3 && g.C % 256 == 0 && getenv("TEM_SPLITK")) {  // opt-in: see DESIGN.md 6
+        const int cpb_min = std::min(P.conv1.cpb, std::min(P.conv2.cpb, P.dgrad.cpb));
+        const int tiles = mtiles * (g.C / 256);
+        const int S = 4;  // slice exchange buffers / prefetched mask sized for S = 4 (64-column slices)
+        if (S <= cpb_min && tiles * S <= 148) {
+            for (UmmaParams* q : {&P.conv1, &P.conv2, &P.dgrad}) {
+                q->kclust = S;
+                q->ntiles = g.C / 256;
+            }
+            for (int pl = 0; pl < npl; ++pl) {
+                ok &= map2d(&P.conv1.b[pl], W[pl] + g.off_W1, 3 * (uint64_t)g.Cin, g.C, 256);
+                ok &= map2d(&P.conv2.b[pl], W[pl] + g.off_W2, 3 * (uint64_t)g.C, g.C, 256);
+            }
+            if ((g.C / 256) * S > 8) P.conv2.zpart = nullptr;  // the head sums at most 8 partial logits
+        }
+    }
     const int wc = cw.bn / 64;  // chunks per WGRAD n-tile
     common(P.wgrad2);
     P.wgrad2.Nout = g.C;
@@ -988,6 +1402,7 @@ static cudaError_t dispatch(const UmmaParams& p, int npass, cudaStream_t s) {
         if (c.pair) return npass == 3 ? launch_wgrad<256, 3, 3, true>(p, s) : launch_wgrad<256, 1, 6, true>(p, s);
         return npass == 3 ? launch_wgrad<128, 3, 3, false>(p, s) : launch_wgrad<256, 1, 4, false>(p, s);
     } else {
+        if (p.kclust > 0 && npass == 3) return launch_splitk<MODE, 3, 2, 2>(p, s);  // plan: fp32 only
         if (c.pair && c.bn == 64) return launch_halo<MODE, 64, 3, 3, 6, true>(p, s);
         if (c.pair)
             return npass == 3 ? launch_halo<MODE, 128, 3, 3, 6, true>(p, s) : launch_halo<MODE, 256, 1, 4, 8, true>(p, s);
@@ -1052,6 +1467,14 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     if (cudaStreamWaitEvent(s, P.join, 0) != cudaSuccess) return cudaErrorUnknown;  // join
     *nl += n;
     return cudaSuccess;
+}
+
+void* umma_tstamp_buffer(int64_t* nbytes, int on) {
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, umma::g_tstamp) != cudaSuccess) return nullptr;
+    cudaMemcpyToSymbol(umma::g_tstamp_on, &on, sizeof(int));
+    if (nbytes) *nbytes = sizeof(unsigned long long) * 1024 * 16;
+    return p;
 }
 
 cudaError_t launch_prep_x_split(const Geom& g, const float* x, void* hi, void* lo, cudaStream_t s) {

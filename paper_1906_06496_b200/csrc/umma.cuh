@@ -97,6 +97,35 @@ UMMA_DEV uint32_t cluster_ctarank() {
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
     return r;
 }
+UMMA_DEV uint32_t cluster_nctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+    return r;
+}
+// 16-byte load from a shared::cluster address (another CTA's shared memory, via mapa).
+UMMA_DEV float4 ld_dsmem_v4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+// 16-byte store to a shared::cluster address (another CTA's shared memory, via mapa).
+UMMA_DEV void st_dsmem_v4(uint32_t addr, float a, float b, float c, float d) {
+    asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
+// Bulk copy of `bytes` (multiple of 16) from this CTA's shared memory into another CTA's
+// shared memory (shared::cluster address from mapa), completing transaction bytes on the
+// destination CTA's mbarrier (also a shared::cluster address).
+UMMA_DEV void bulk_copy_to_peer(uint32_t dst_cluster, const void* src, uint32_t bytes, uint32_t mbar_cluster) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            dst_cluster),
+        "r"(smem_u32(src)), "r"(bytes), "r"(mbar_cluster)
+        : "memory");
+}
 UMMA_DEV void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -226,6 +255,15 @@ UMMA_DEV void tmem_ld_wait_regs(uint32_t (&r)[16]) {
                    "+r"(r[15])
                  :
                  : "memory");
+}
+
+// Ties 16 more registers to the preceding wait (an empty asm ordered after it that
+// "redefines" them), for callers with several loads in flight.
+UMMA_DEV void tmem_regs_fence(uint32_t (&r)[16]) {
+    asm volatile(""
+                 : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                   "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
+                   "+r"(r[15]));
 }
 
 // ------------------------------------------------------------------ descriptors

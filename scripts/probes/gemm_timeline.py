@@ -1,0 +1,63 @@
+#!/usr/bin/env python
+"""Phase timeline of a FWD/DGRAD GEMM launch (diagnostics; needs a GPU).
+
+    TEM_NO_GRAPH=1 [TEM_SPLITK=1] python scripts/probes/split_timeline.py [--workload c2] [--kernel halo|split]
+
+Runs steps, enables the kernel's globaltimer stamps for the last one, and prints the per-phase
+times (us after the earliest CTA entry; median / max over CTAs) of the step's last FWD/DGRAD
+launch (conv2 dgrad).
+"""
+import argparse
+import ctypes
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+
+PHASES = {"split": ["entry", "pdl_wait", "prod_firstA", "mma_fullA", "mma_fullB", "mma_done", "epi_tfull",
+                    "cluster1", "packed", "received", "done"],
+          "halo": ["entry", "pdl_wait", "mma_fullA0", "tile0_mma_done", "last_mma_done", "-", "epi_done"]}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="c2")
+    ap.add_argument("--kernel", default="halo", choices=["halo", "split"])
+    args = ap.parse_args()
+    import numpy as np
+    import torch
+    import datagen
+    from paper_1906_06496_b200 import tem
+    B = {"c1": 4, "c2": 16}[args.workload]
+    sc = tem.SessionConfig(world_size=1, rank=0, local_ranks=1, batch_per_rank=B, precision=0, lr=0.01)
+    s = tem.TemSession(sc, datagen.init_params())
+    x = torch.from_numpy(datagen.features(B)).cuda()
+    lab = torch.from_numpy(datagen.labels(B)).cuda()
+    for _ in range(3):
+        s.step(x, lab)
+    torch.cuda.synchronize()
+    lib = tem.lib()
+    nb = ctypes.c_int64(0)
+    lib.tem_debug_buffer(tem._P(s.ctx), 0, b"tstamp_on", ctypes.byref(nb))
+    s.step(x, lab)
+    torch.cuda.synchronize()
+    ptr = lib.tem_debug_buffer(tem._P(s.ctx), 0, b"tstamp", ctypes.byref(nb))
+    class _Arr:  # wrap the raw device pointer (a __device__ symbol, outside the workspace)
+        __cuda_array_interface__ = {"shape": (nb.value // 8,), "typestr": "<i8", "data": (ptr, False), "version": 3}
+    raw = torch.as_tensor(_Arr(), device="cuda").cpu().numpy().reshape(1024, 16)
+    used = raw[:, 0] > 0
+    raw = raw[used]
+    t0 = raw[:, 0].min()
+    print(f"{used.sum()} CTAs stamped")
+    for k, name in enumerate(PHASES[args.kernel]):
+        col = raw[:, k]
+        col = col[col > 0]
+        if len(col):
+            d = (col - t0) / 1e3
+            print(f"{name:>12}: median {np.median(d):7.2f} us  max {d.max():7.2f} us  (n={len(col)})")
+    s.close()
+
+
+if __name__ == "__main__":
+    main()
