@@ -111,9 +111,20 @@ struct EpiRegs {
 // ACC = 1: one accumulator of BN columns.  ACC = 3 (3-pass split, dual-accumulator MMAs): the
 // accumulator holds [hi*hi | hi*lo] (2 BN columns, one N = 2 BN MMA against the contiguous
 // B hi / lo planes) and lo*hi (BN columns); the epilogue sums (hi*hi + hi*lo) + lo*hi.
+// DGRAD: first 16 mask columns of this lane's row, loaded by the caller BEFORE it waits for
+// the accumulator (the remaining chunks are prefetched one chunk ahead inside).
+TEM_DEV void dgrad_mask_chunk0(const UmmaParams& P, int row, int col0, uint4 (&pm)[2]) {
+    pm[0] = pm[1] = make_uint4(0u, 0u, 0u, 0u);
+    if (row < P.R && !halo_row(row, P.Tp)) {
+        const uint4* mk = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(P.mask) + (size_t)row * P.Nout + col0);
+        pm[0] = __ldg(mk);
+        pm[1] = __ldg(mk + 1);
+    }
+}
+
 template <int MODE, int BN, int ACC = 1>
 TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_tile, int split, int q,
-                           int lane, uint8_t* stg, int& buf, const float* sw3) {
+                           int lane, uint8_t* stg, int& buf, const float* sw3, const uint4 (&pm)[2]) {
     const int row0 = m_tile * BM + 32 * q;
     const int row = row0 + lane;
     if ((MODE == FWD_ || MODE == DGRAD_) && (m_tile >= P.mtiles || row0 >= P.R)) return;
@@ -128,7 +139,10 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
             tmem_ld16(tq + (uint32_t)(BN + c16 * 16), e.r2);
             tmem_ld16(tq + (uint32_t)(2 * BN + c16 * 16), e.r3);
         }
-        if (MODE == DGRAD_) {
+        if (MODE == DGRAD_ && c16 == 0) {
+            e.mw[0] = pm[0].x; e.mw[1] = pm[0].y; e.mw[2] = pm[0].z; e.mw[3] = pm[0].w;
+            e.mw[4] = pm[1].x; e.mw[5] = pm[1].y; e.mw[6] = pm[1].z; e.mw[7] = pm[1].w;
+        } else if (MODE == DGRAD_) {
             if (!halo) {
                 const uint4* mk = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(P.mask) +
                                                                  (size_t)row * P.Nout + n_tile * BN + c16 * 16);
@@ -336,10 +350,12 @@ TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, ui
         int m_tile, n_tile, split;
         coords(ct, m_tile, n_tile, split);
         const int acc = t & 1;
+        uint4 pm[2];
+        if (MODE == DGRAD_) dgrad_mask_chunk0(P, m_tile * BM + 32 * q + lane, n_tile * BN, pm);
         mbar_wait(&tfull[acc], (t >> 1) & 1);
         tc_fence_after();
         const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * ACC * BN);
-        epilogue_tile<MODE, BN, ACC>(P, tq, m_tile, n_tile, split, q, lane, stg, buf, sw3);
+        epilogue_tile<MODE, BN, ACC>(P, tq, m_tile, n_tile, split, q, lane, stg, buf, sw3, pm);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {  // buffer free for tile t + 2
@@ -347,7 +363,7 @@ TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, ui
             else mbar_arrive_local(&tempty[acc]);
         }
     }
-    if (lane == 0) bulk_wait_all();
+    if (lane == 0) bulk_wait_read<0>();  // staging smem must outlive the stores' reads
 }
 
 // Phase timestamps of the GEMM kernels (diagnostics: tem_debug_buffer "tstamp",
