@@ -346,10 +346,12 @@ def main():
         else:
             key = "bf16_tflops_sustained"
             bf16 = peaks.get(key, peaks.get("bf16_tflops"))
-            peak = bf16 if prec == 1 else bf16 / 2.0
+            # fp32 path: three bf16 products per fp32 MAC (hi*hi + hi*lo + lo*hi, R16)
+            peak = bf16 if prec == 1 else bf16 / 3.0
             roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak, "traffic": None,
-                    "peak_source": f"{key} ({peak_src})" + ("" if prec == 1 else " x 1/2 (tf32:bf16 nominal ratio)")}
+                    "peak_source": f"{key} ({peak_src})" + ("" if prec == 1 else
+                                                            " / 3 (3 bf16 tensor-core products per fp32 MAC, DESIGN.md R16)")}
         tr = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tr):
             try:
