@@ -49,6 +49,20 @@ TEM_DEV uint64_t globaltimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+// Kernel-span trace (diagnostics, scripts/probes/step_trace.py): while g_trace is set (one
+// copy per translation unit, set by trace_set_<unit>), each traced kernel records the minimum
+// start and maximum end globaltimer over its CTAs in g_trace[2 slot], g_trace[2 slot + 1].
+static __device__ unsigned long long* g_trace;
+TEM_DEV void trace_begin(int slot) {
+    if (g_trace != nullptr && threadIdx.x == 0) atomicMin(&g_trace[2 * slot], (unsigned long long)globaltimer());
+}
+TEM_DEV void trace_end(int slot) {  // all threads of the CTA, at its end
+    if (g_trace != nullptr) {
+        __syncthreads();
+        if (threadIdx.x == 0) atomicMax(&g_trace[2 * slot + 1], (unsigned long long)globaltimer());
+    }
+}
+
 // L2-coherent 128-bit load (bypasses L1: data written by a peer GPU lands in our L2).
 TEM_DEV float4 ld_cg4(const float* p) { return __ldcg(reinterpret_cast<const float4*>(p)); }
 

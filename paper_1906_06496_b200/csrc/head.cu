@@ -47,8 +47,10 @@ __global__ void __launch_bounds__(256, 3) head_rows_kernel(
     TOp* __restrict__ dA2_lo, float* __restrict__ z_out, float* __restrict__ part, int B, int Tn, int C,
     int RPC, const float* __restrict__ zpart, int nzp) {
     extern __shared__ __align__(16) float sm[];
+    trace_begin(SLOT_HEAD);
     pdl_trigger();
     pdl_wait();
+    if (g_trace != nullptr && threadIdx.x == 0) g_trace[2 * NUM_SLOTS + blockIdx.x * 8 + 0] = globaltimer();
     float* sW3 = sm;           // [3][C] (only the nzp == 0 path reads it)
     float* sdz = sm + 3 * C;   // [RPC][3] dz of this CTA's rows (0 on halo rows)
     __shared__ float s_ap[3][3], s_an[3][3], s_misc[HEAD_WARPS][6];
@@ -98,6 +100,7 @@ __global__ void __launch_bounds__(256, 3) head_rows_kernel(
     if (nzp == 0)
         for (int i = tid; i < 3 * C; i += blockDim.x) sW3[i] = W3[i];
     __syncthreads();
+    if (g_trace != nullptr && threadIdx.x == 0) g_trace[2 * NUM_SLOTS + blockIdx.x * 8 + 1] = globaltimer();
     // ---- phase 1: z, loss terms, dz -> smem ----
     const int NQ = C / 32;  // <= 16
     float lsum[3] = {0.f, 0.f, 0.f}, dbs[3] = {0.f, 0.f, 0.f};
@@ -183,6 +186,7 @@ __global__ void __launch_bounds__(256, 3) head_rows_kernel(
         }
     }
     __syncthreads();
+    if (g_trace != nullptr && threadIdx.x == 0) g_trace[2 * NUM_SLOTS + blockIdx.x * 8 + 2] = globaltimer();
     // ---- phase 2: dA2 = 1[h2>0] W3^T dz (halo rows: dz = 0 -> 0); dW3 += dz h2; db2 += stored dA2 ----
     float* dst = part + (size_t)blockIdx.x * (4 * C + 8);  // row stride padded to 16 bytes
     float acc[3][4], bs[4];
@@ -234,6 +238,7 @@ __global__ void __launch_bounds__(256, 3) head_rows_kernel(
     // combine the row phases in a fixed order through shared memory (sdz is dead after the sync)
     float* red = sdz;  // [RP][CG][16]
     __syncthreads();
+    if (g_trace != nullptr && threadIdx.x == 0) g_trace[2 * NUM_SLOTS + blockIdx.x * 8 + 3] = globaltimer();
     if (act2) {
         float* r = red + ((size_t)rp * CG + cg) * 16;
 #pragma unroll
@@ -245,6 +250,7 @@ __global__ void __launch_bounds__(256, 3) head_rows_kernel(
         }
     }
     __syncthreads();
+    if (g_trace != nullptr && threadIdx.x == 0) g_trace[2 * NUM_SLOTS + blockIdx.x * 8 + 4] = globaltimer();
     if (rp == 0) {
         float sum[16];
 #pragma unroll
@@ -268,6 +274,8 @@ __global__ void __launch_bounds__(256, 3) head_rows_kernel(
         dst[3 * C + tid] = d;
         dst[3 * C + 3 + tid] = -l / (float)Tn;
     }
+    if (g_trace != nullptr && threadIdx.x == 0) g_trace[2 * NUM_SLOTS + blockIdx.x * 8 + 5] = globaltimer();
+    trace_end(SLOT_HEAD);
 }
 
 // Two-level fixed-order reduction of the P partial rows (n = 4C+6 entries each, stride 4C+8).
@@ -278,6 +286,7 @@ __global__ void head_reduce_kernel(const float* __restrict__ part, int P, int C,
                                    unsigned* __restrict__ counter, float* __restrict__ gW3,
                                    float* __restrict__ gb2, float* __restrict__ loss_out, int B, float lam0,
                                    float lam1, float lam2, Status* status, int64_t* stepctr) {
+    trace_begin(SLOT_HEADFIN);
     pdl_trigger();
     pdl_wait();
     const int n = 4 * C + 6, stride = 4 * C + 8;  // entries / padded row stride
@@ -322,7 +331,14 @@ __global__ void head_reduce_kernel(const float* __restrict__ part, int P, int C,
         *stepctr = step + 1;
         if (!isfinite(tot)) latch(status, TEM_ERR_NONFINITE, step);
     }
+    trace_end(SLOT_HEADFIN);
 }
+
+}  // namespace
+
+void trace_set_head(unsigned long long* p) { cudaMemcpyToSymbol(g_trace, &p, sizeof(p)); }
+
+namespace {
 
 int head_rows_per_cta(const Geom& g) {
     int rpc = (g.R + 443) / 444;  // one wave at 3 CTAs per SM
@@ -348,14 +364,14 @@ cudaError_t launch_head_rows(const Geom& g, const RankBufs& b, const float* labe
     if (g.op_bf16) {
         auto k = head_rows_kernel<__nv_bfloat16>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-        e = launch_pdl(k, dim3(P), dim3(256), hsm, s, (const float*)b.h2, (const float*)(b.params + g.off_W3),
+        e = launch_pdl(k, dim3(P), dim3(256), hsm, s, false, (const float*)b.h2, (const float*)(b.params + g.off_W3),
                        (const float*)(b.params + g.off_b3), labels, lam[0], lam[1], lam[2],
                        static_cast<__nv_bfloat16*>(b.dA2), static_cast<__nv_bfloat16*>(b.dA2_lo), b.z, b.headpart, g.B,
                        g.T, g.C, rpc, (const float*)b.zpart, b.nzpart);
     } else {
         auto k = head_rows_kernel<float>;
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-        e = launch_pdl(k, dim3(P), dim3(256), hsm, s, (const float*)b.h2, (const float*)(b.params + g.off_W3),
+        e = launch_pdl(k, dim3(P), dim3(256), hsm, s, false, (const float*)b.h2, (const float*)(b.params + g.off_W3),
                        (const float*)(b.params + g.off_b3), labels, lam[0], lam[1], lam[2], static_cast<float*>(b.dA2),
                        (float*)nullptr, b.z, b.headpart, g.B, g.T, g.C, rpc, (const float*)nullptr, 0);
     }
@@ -370,7 +386,7 @@ cudaError_t launch_head_reduce(const Geom& g, const RankBufs& b, const float lam
     rec.begin(SLOT_HEADFIN);
     const int nent = 4 * g.C + 6;
     const int G = P >= 128 ? 16 : (P >= 16 ? 4 : 1);
-    cudaError_t e = launch_pdl(head_reduce_kernel, dim3((nent + 255) / 256, G), dim3(256), 0, s,
+    cudaError_t e = launch_pdl(head_reduce_kernel, dim3((nent + 255) / 256, G), dim3(256), 0, s, true,
                                (const float*)b.headpart, P, g.C, b.headlvl1, b.counter, b.grad + g.off_W3,
                                b.grad + g.off_b2, loss_out, g.B, lam[0], lam[1], lam[2], status, b.stepctr);
     rec.end(SLOT_HEADFIN);

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <cuda.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -13,18 +14,30 @@ namespace tem {
 // Kernel launch with programmatic dependent launch allowed (unless TEM_NO_PDL is set): the
 // kernel's prologue overlaps the tail of its stream predecessor (see pdl_wait/pdl_trigger).
 bool pdl_enabled();
+// Launch priority of the step's two graph branches: the critical path (prep -> convs -> head ->
+// dgrad -> conv1 wgrad -> exchange) high, the side branch (head reduction, conv2 wgrad) low,
+// so the block scheduler hands the side branch only the SMs the critical path leaves idle.
+// TEM_NO_PRIO disables.  Returns the number of attributes written (0 or 1).
+int launch_priority_attr(cudaLaunchAttribute* a, bool side_branch);
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool side,
+                       Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute a[1];
-    a[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    a[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute a[2];
+    int na = 0;
+    // side-branch kernels follow a cross-stream event: no early launch (their CTAs would sit on
+    // SMs the critical path needs)
+    if (pdl_enabled() && !(side && getenv("TEM_SIDE_PDL") == nullptr)) {
+        a[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        a[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    na += launch_priority_attr(&a[na], side);
     cfg.attrs = a;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...);
 }
 
@@ -103,6 +116,8 @@ struct UmmaParams {
     int mtiles, ntiles, nsplit;  // tile grid (persistent kernels walk it cluster tile by cluster tile)
     int ones_chunk;      // WGRAD: chunk slot 3*cpj reads the all-ones map (bias gradient column)
     int kclust;          // FWD/DGRAD: > 0 -> split-K cluster kernel with this many CTAs per tile
+    int slot;            // trace / timing slot (Slot)
+    int side;            // 1: launched on the side branch (low priority)
     CUtensorMap ones;    // [R][128] bf16: columns 0..63 = 1, 64..127 = 0
 };
 struct UmmaPlan {
@@ -132,6 +147,10 @@ cudaError_t launch_relu_decisions(const Geom& g, const RankBufs& b, uint8_t* out
 enum Slot { SLOT_PREP = 0, SLOT_CONV1, SLOT_CONV2, SLOT_HEAD, SLOT_HEADFIN, SLOT_DGRAD, SLOT_WGRAD2,
             SLOT_RED2, SLOT_WGRAD1, SLOT_RED1, SLOT_EXCHANGE, NUM_SLOTS };
 const char* slot_name(int slot);
+// kernel-span trace buffers (diagnostics): one setter per translation unit with traced kernels
+void trace_set_umma(unsigned long long* p);
+void trace_set_head(unsigned long long* p);
+void trace_set_ring(unsigned long long* p);
 struct EvRec {
     cudaEvent_t* ev;  // [NUM_SLOTS*2] or nullptr
     cudaStream_t s;
@@ -141,9 +160,11 @@ struct EvRec {
 cudaError_t simt_compute(const Geom& g, const RankBufs& b, const float* labels,
                          const float lam[3], float* loss_out, Status* status, int* nlaunch,
                          const EvRec& rec, cudaStream_t s);
+// defer_reduce: skip the two split-K reductions; the N = 1 exchange sums the partials itself
+// (launch_sgd_fused) -- used by tem_step only, so tem_compute still leaves the full gradient.
 cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, const float* labels,
                          const float lam[3], float* loss_out, Status* status, int* nlaunch,
-                         const EvRec& rec, cudaStream_t s);
+                         const EvRec& rec, cudaStream_t s, bool defer_reduce = false);
 // head (conv3 + sigmoid + loss + dz + dA2) and its deterministic finalisation (rows a3-a5);
 // writes dA2 as b.dA2 (+ b.dA2_lo when present) in the operand type of the path.
 cudaError_t launch_head(const Geom& g, const RankBufs& b, const float* labels, const float lam[3],
@@ -175,6 +196,12 @@ struct RingParams {
     uint64_t spin_ns;
 };
 cudaError_t launch_ring(const RingParams& p, cudaStream_t s);
+// N = 1 owner update with the deferred split-K reductions fused in: grad[e] = sum_s part1[s][e]
+// (W1, b1), sum_s part2[s][e - off2] (W2), or grad[e] (the head-written entries); the same
+// ascending-s order as reduce_wgrad_kernel, so the result is bit-identical to the unfused path.
+cudaError_t launch_sgd_fused(float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo, int64_t n,
+                             float lr, const float* p1, int64_t stride1, int64_t n1, const float* p2,
+                             int64_t stride2, int64_t off2, int64_t n2, int S, cudaStream_t s);
 cudaError_t launch_sgd_single(const float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo,
                               int64_t n, int op, float lr, cudaStream_t s);
 struct PsParams {

@@ -247,6 +247,7 @@ __global__ void __launch_bounds__(RING_THREADS) ring_kernel(const __grid_constan
 __global__ void sgd_single_kernel(const float* __restrict__ g, float* __restrict__ w,
                                   __nv_bfloat16* __restrict__ shadow, __nv_bfloat16* __restrict__ shadow_lo,
                                   int64_t n, int op, float lr) {
+    trace_begin(SLOT_EXCHANGE);
     pdl_trigger();
     pdl_wait();
     const int64_t nv = n / 4;
@@ -264,6 +265,50 @@ __global__ void sgd_single_kernel(const float* __restrict__ g, float* __restrict
         reinterpret_cast<float4*>(w)[v] = x;
         if (shadow) store_shadow4(shadow, shadow_lo, 4 * v, x);
     }
+    trace_end(SLOT_EXCHANGE);
+}
+
+__global__ void sgd_fused_kernel(float* __restrict__ g, float* __restrict__ w, __nv_bfloat16* __restrict__ shadow,
+                                 __nv_bfloat16* __restrict__ shadow_lo, int64_t n, float lr,
+                                 const float* __restrict__ p1, int64_t stride1, int64_t n1,
+                                 const float* __restrict__ p2, int64_t stride2, int64_t off2, int64_t n2, int S) {
+    trace_begin(SLOT_EXCHANGE);
+    pdl_trigger();
+    pdl_wait();
+    const int64_t nv = n / 4;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = 4 * v;
+        const float* src = nullptr;
+        int64_t stride = 0;
+        if (e < n1) {
+            src = p1 + e;
+            stride = stride1;
+        } else if (e >= off2 && e < off2 + n2) {
+            src = p2 + (e - off2);
+            stride = stride2;
+        }
+        float4 a;
+        if (src) {  // split-K partials, ascending s (as reduce_wgrad_kernel)
+            a = __ldcs(reinterpret_cast<const float4*>(src));
+            for (int s = 1; s < S; ++s) {
+                const float4 b = __ldcs(reinterpret_cast<const float4*>(src + (size_t)s * stride));
+                a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+            }
+            reinterpret_cast<float4*>(g)[v] = a;  // the local gradient stays observable
+        } else {
+            a = reinterpret_cast<const float4*>(g)[v];
+        }
+        // TEM_MEAN at N = 1: a * fl(1/1) is exact
+        float4 x = reinterpret_cast<float4*>(w)[v];
+        x.x = __fmaf_rn(-lr, a.x, x.x);
+        x.y = __fmaf_rn(-lr, a.y, x.y);
+        x.z = __fmaf_rn(-lr, a.z, x.z);
+        x.w = __fmaf_rn(-lr, a.w, x.w);
+        reinterpret_cast<float4*>(w)[v] = x;
+        if (shadow) store_shadow4(shadow, shadow_lo, e, x);
+    }
+    trace_end(SLOT_EXCHANGE);
 }
 
 // KP1 parameter-server comparator: every rank pushes its buffer into
@@ -359,7 +404,16 @@ cudaError_t launch_ring(const RingParams& p, cudaStream_t s) {
 
 cudaError_t launch_sgd_single(const float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo,
                               int64_t n, int op, float lr, cudaStream_t s) {
-    return launch_pdl(sgd_single_kernel, dim3(296), dim3(512), 0, s, g, w, shadow, shadow_lo, n, op, lr);
+    return launch_pdl(sgd_single_kernel, dim3(296), dim3(512), 0, s, false, g, w, shadow, shadow_lo, n, op, lr);
+}
+
+void trace_set_ring(unsigned long long* p) { cudaMemcpyToSymbol(g_trace, &p, sizeof(p)); }
+
+cudaError_t launch_sgd_fused(float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo, int64_t n,
+                             float lr, const float* p1, int64_t stride1, int64_t n1, const float* p2,
+                             int64_t stride2, int64_t off2, int64_t n2, int S, cudaStream_t s) {
+    return launch_pdl(sgd_fused_kernel, dim3(296), dim3(512), 0, s, false, g, w, shadow, shadow_lo, n, lr, p1, stride1, n1, p2,
+                      stride2, off2, n2, S);
 }
 
 cudaError_t launch_ps(const PsParams& p, cudaStream_t s) {

@@ -26,6 +26,21 @@ bool tem::pdl_enabled() {
     return on != 0;
 }
 
+int tem::launch_priority_attr(cudaLaunchAttribute* a, bool side) {
+    static int lo = 1, hi = 1, on = -1;  // numerically lower = higher priority
+    if (on < 0) {
+        on = getenv("TEM_NO_PRIO") ? 0 : 1;
+        if (on && cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) {
+            cudaGetLastError();
+            on = 0;
+        }
+    }
+    if (!on || lo == hi) return 0;
+    a->id = cudaLaunchAttributePriority;
+    a->val.priority = side ? lo : hi;
+    return 1;
+}
+
 namespace {
 
 constexpr size_t kAlign = 256;
@@ -181,6 +196,7 @@ struct tem_ctx {
     Status* st_dev;
     int launches_step, launches_exchange;
     bool alive;
+    bool reduce_deferred;  // last compute left the split-K partials for the fused N = 1 exchange
     // per-kernel timing (tem_timing_*)
     cudaEvent_t* tev;  // [max_steps][NUM_SLOTS*2]
     int t_max, t_idx;
@@ -403,7 +419,7 @@ static cudaEvent_t* timing_slot_events(tem_ctx* c) {
 }
 
 static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, float* loss_out,
-                               cudaStream_t s, int* nl) {
+                               cudaStream_t s, int* nl, bool fuse_reduce = false) {
     const EvRec rec{timing_slot_events(c), s};
     const Geom& g = c->g;
     const size_t esz = g.prec == TEM_BF16 ? 2 : 4;  // caller's x element size
@@ -417,8 +433,10 @@ static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, f
         rec.end(SLOT_PREP);
         if (e != cudaSuccess) return TEM_ERR_CUDA;
         ++*nl;
+        const bool defer = fuse_reduce && c->N == 1 && g.path == PATH_UMMA && g.B > 0;
+        c->reduce_deferred = defer;
         if (g.path == PATH_UMMA && g.B > 0)
-            e = umma_compute(g, c->rb[l], *c->plan[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s);
+            e = umma_compute(g, c->rb[l], *c->plan[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s, defer);
         else
             e = simt_compute(g, c->rb[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s);
         if (e != cudaSuccess) return TEM_ERR_CUDA;
@@ -443,6 +461,18 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
     const EvRec rec{timing_slot_events(c), s};
     rec.begin(SLOT_EXCHANGE);
     tem_status st = TEM_OK;
+    if (c->N == 1 && c->reduce_deferred) {  // tem_step: split-K reductions fused into the update
+        const RankBufs& b = c->rb[0];
+        const UmmaPlan& P = *c->plan[0];
+        c->reduce_deferred = false;
+        if (launch_sgd_fused(b.grad, (float*)b.params, b.shadow, b.shadow_lo, g.Kpad, c->cfg.lr, b.wpart,
+                             P.wgrad1.part_stride, g.off_W2, b.wpart2, P.wgrad2.part_stride, g.off_W2,
+                             (int64_t)3 * g.C * g.C, P.S, s) != cudaSuccess)
+            return TEM_ERR_CUDA;
+        ++*nl;
+        rec.end(SLOT_EXCHANGE);
+        return st;
+    }
     if (c->N == 1) {
         for (int l = 0; l < c->nlocal; ++l) {
             if (launch_sgd_single(c->rb[l].grad, (float*)c->rb[l].params, c->rb[l].shadow, c->rb[l].shadow_lo, g.Kpad,
@@ -525,7 +555,7 @@ tem_status tem_step(tem_ctx* c, const void* x, const float* labels, float* loss_
     if (c->use_graphs && !c->tev) {
         return graph_step(c, x, labels, loss_out, (cudaStream_t)stream, [&](cudaStream_t gs, int* n) {
             int a = 0, b = 0;
-            tem_status r = compute_impl(c, x, labels, loss_out, gs, &a);
+            tem_status r = compute_impl(c, x, labels, loss_out, gs, &a, true);
             if (r == TEM_OK) r = exchange_impl(c, gs, &b);
             *n = a + b;
             c->launches_exchange = b;
@@ -533,7 +563,7 @@ tem_status tem_step(tem_ctx* c, const void* x, const float* labels, float* loss_
         });
     }
     int nl = 0;
-    st = compute_impl(c, x, labels, loss_out, (cudaStream_t)stream, &nl);
+    st = compute_impl(c, x, labels, loss_out, (cudaStream_t)stream, &nl, true);
     if (st != TEM_OK) return st;
     int ne = 0;
     st = exchange_impl(c, (cudaStream_t)stream, &ne);
@@ -685,6 +715,20 @@ float* tem_logits(tem_ctx* c, int32_t l) {
 void* tem_debug_buffer(tem_ctx* c, int32_t l, const char* name, int64_t* nbytes) {
     if (nbytes) *nbytes = 0;
     if (!c || !c->alive || l < 0 || l >= c->nlocal || !name) return nullptr;
+    if (strcmp(name, "trace_on") == 0 || strcmp(name, "trace_off") == 0 || strcmp(name, "trace") == 0) {
+        // [NUM_SLOTS][2] kernel spans + [4096][8] head phase stamps (ns), diagnostics
+        static unsigned long long* buf = nullptr;
+        const size_t words = 2 * NUM_SLOTS + 4096 * 8;
+        if (!buf && cudaMalloc(&buf, sizeof(unsigned long long) * words) != cudaSuccess) return nullptr;
+        if (strcmp(name, "trace") != 0) {
+            unsigned long long* p = strcmp(name, "trace_on") == 0 ? buf : nullptr;
+            trace_set_umma(p);
+            trace_set_head(p);
+            trace_set_ring(p);
+        }
+        if (nbytes) *nbytes = (int64_t)(sizeof(unsigned long long) * words);
+        return buf;
+    }
     if (strcmp(name, "tstamp_on") == 0 || strcmp(name, "tstamp") == 0)
         return umma_tstamp_buffer(nbytes, strcmp(name, "tstamp_on") == 0 ? 1 : 0);
     const Geom& g = c->g;

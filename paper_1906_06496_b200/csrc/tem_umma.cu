@@ -425,6 +425,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
     const int mt_u = PAIR ? (P.mtiles + 1) / 2 : P.mtiles;
     const int total = mt_u * P.ntiles;
     if (threadIdx.x == 0) tstamp(0);
+    trace_begin(P.slot);
     const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, fullA, 2 * (SA + SB), tfull, tempty, tslot, warp, lane);
     if (threadIdx.x == 0) tstamp(1);
 
@@ -532,6 +533,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
         if (threadIdx.x == 64) tstamp(6);
     }
     gemm_epilogue_done<C_::TMEM_COLS, PAIR>(tbase, warp);
+    trace_end(P.slot);
 }
 
 // ------------------------------------------------------------------ FWD / DGRAD, split-K cluster
@@ -883,6 +885,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
     const int nunits = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
     const int mt_u = PAIR ? (P.mtiles + 1) / 2 : P.mtiles;
     const int total = mt_u * P.ntiles * P.nsplit;
+    trace_begin(P.slot);
     const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, full, 2 * STAGES, tfull, tempty, tslot, warp, lane);
 
     auto coords = [&](int ct, int& m_tile, int& n_tile, int& split) {
@@ -977,12 +980,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
         epilogue_loop<WGRAD_, BN, PAIR, 1>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane);
     }
     gemm_epilogue_done<C_::TMEM_COLS, PAIR>(tbase, warp);
+    trace_end(P.slot);
 }
 
 // ------------------------------------------------------------------ companions
 // x [B][T][Cin] fp32 -> halo-padded hi/lo bf16 planes [B][T+2][Cin].
 __global__ void prep_x_split_kernel(const float* __restrict__ x, __nv_bfloat16* __restrict__ hi,
                                     __nv_bfloat16* __restrict__ lo, int B, int Tn, int Cin) {
+    trace_begin(SLOT_PREP);
     pdl_trigger();
     pdl_wait();
     const int per_row = Cin / 4;
@@ -1007,12 +1012,14 @@ __global__ void prep_x_split_kernel(const float* __restrict__ x, __nv_bfloat16* 
         reinterpret_cast<uint2*>(hi + (size_t)p * Cin)[cv] = hv;
         reinterpret_cast<uint2*>(lo + (size_t)p * Cin)[cv] = lv;
     }
+    trace_end(SLOT_PREP);
 }
 
 // Weight gradient = sum of the S split-K partials (ascending s); optionally followed by the
 // bias gradient = sum of nbp per-m-tile column sums (ascending m).  Both fixed order.
 __global__ void reduce_wgrad_kernel(const float* __restrict__ part, int64_t part_stride, int S, int64_t nW,
-                                    const float* __restrict__ bpart, int nbp, int C, float* __restrict__ dst) {
+                                    const float* __restrict__ bpart, int nbp, int C, float* __restrict__ dst, int slot) {
+    trace_begin(slot);
     pdl_trigger();
     pdl_wait();
     const int64_t nvw = nW / 4, nvb = nbp > 0 ? C / 4 : 0;
@@ -1035,6 +1042,7 @@ __global__ void reduce_wgrad_kernel(const float* __restrict__ part, int64_t part
         }
         reinterpret_cast<float4*>(dst)[v] = a;
     }
+    trace_end(slot);
 }
 
 // [R][128] bf16: columns 0..63 = 1.0, 64..127 = 0 (the bias-gradient "ones" operand)
@@ -1128,12 +1136,13 @@ template <typename K>
 cudaError_t launch_persistent(K k, uint32_t smem, bool pair, int total, int* max_units, const UmmaParams& p,
                               cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[3];
     int na = 0;
-    if (pdl_enabled()) {
+    if (pdl_enabled() && !(p.side && getenv("TEM_SIDE_PDL") == nullptr)) {
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[na++].val.programmaticStreamSerializationAllowed = 1;
     }
+    na += launch_priority_attr(&attr[na], p.side != 0);
     if (pair) {
         attr[na].id = cudaLaunchAttributeClusterDimension;
         attr[na].val.clusterDim.x = 2;
@@ -1321,6 +1330,7 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
         q.nsplit = 1;
     };
     common(P.conv1);
+    P.conv1.slot = SLOT_CONV1;
     P.conv1.Kc = g.Cin;
     P.conv1.cpb = (g.Cin + umma::BK - 1) / umma::BK;
     P.conv1.Nout = g.C;
@@ -1330,6 +1340,7 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     P.conv1.out_hi = b.h1;
     P.conv1.out_lo = b.h1_lo;
     common(P.conv2);
+    P.conv2.slot = SLOT_CONV2;
     P.conv2.Kc = g.C;
     P.conv2.cpb = g.C / umma::BK;
     P.conv2.Nout = g.C;
@@ -1342,6 +1353,7 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     // [C/BN][R][3] partial logits for the head (which sums at most 8 per row)
     P.conv2.zpart = (getenv("TEM_NO_ZPART") || g.C / cf.bn > 8) ? nullptr : b.zpart;
     common(P.dgrad);
+    P.dgrad.slot = SLOT_DGRAD;
     P.dgrad.Kc = g.C;
     P.dgrad.cpb = g.C / umma::BK;
     P.dgrad.Nout = g.C;
@@ -1371,6 +1383,8 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     }
     const int wc = cw.bn / 64;  // chunks per WGRAD n-tile
     common(P.wgrad2);
+    P.wgrad2.slot = SLOT_WGRAD2;
+    P.wgrad2.side = 1;
     P.wgrad2.Nout = g.C;
     P.wgrad2.Cin_w = g.C;
     P.wgrad2.cpj = (g.C + 63) / 64;
@@ -1381,6 +1395,7 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     P.wgrad2.part = b.wpart2;
     P.wgrad2.part_stride = (int64_t)g.C * 3 * g.C + g.C;
     common(P.wgrad1);
+    P.wgrad1.slot = SLOT_WGRAD1;
     P.wgrad1.nsplit = P.S;
     P.wgrad1.Nout = g.C;
     P.wgrad1.Cin_w = g.Cin;
@@ -1428,7 +1443,7 @@ static cudaError_t dispatch(const UmmaParams& p, int npass, cudaStream_t s) {
 
 cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, const float* labels,
                          const float lam[3], float* loss_out, Status* status, int* nl, const EvRec& rec,
-                         cudaStream_t s) {
+                         cudaStream_t s, bool defer_reduce) {
     int n = 0;
     cudaError_t e;
     rec.begin(SLOT_CONV1);
@@ -1446,24 +1461,29 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     // Fork: the head reduction and conv2 wgrad (+ its reduction) run on the aux stream
     // alongside conv2 dgrad -> conv1 wgrad on s; all only read dA2 / h1 / xp / head
     // partials (captured as parallel graph branches).
-    const EvRec rec2{rec.ev, P.aux};
-    if (cudaEventRecord(P.fork, s) != cudaSuccess || cudaStreamWaitEvent(P.aux, P.fork, 0) != cudaSuccess)
+    static const bool no_fork = getenv("TEM_NO_FORK") != nullptr;  // experiment: side branch serialised
+    cudaStream_t aux = no_fork ? s : P.aux;
+    const EvRec rec2{rec.ev, aux};
+    if (!no_fork &&
+        (cudaEventRecord(P.fork, s) != cudaSuccess || cudaStreamWaitEvent(P.aux, P.fork, 0) != cudaSuccess))
         return cudaErrorUnknown;
-    e = launch_head_reduce(g, b, lam, loss_out, status, rec2, P.aux, &n);
+    e = launch_head_reduce(g, b, lam, loss_out, status, rec2, aux, &n);
     if (e != cudaSuccess) return e;
     rec2.begin(SLOT_WGRAD2);
-    e = dispatch<WGRAD_>(P.wgrad2, P.npass, P.aux);
+    e = dispatch<WGRAD_>(P.wgrad2, P.npass, aux);
     rec2.end(SLOT_WGRAD2);
     if (e != cudaSuccess) return e;
     ++n;
+    if (!defer_reduce) {
     rec2.begin(SLOT_RED2);
-    e = launch_pdl(umma::reduce_wgrad_kernel, dim3(296), dim3(256), 0, P.aux, (const float*)b.wpart2,
+    e = launch_pdl(umma::reduce_wgrad_kernel, dim3(296), dim3(256), 0, aux, true, (const float*)b.wpart2,
                    P.wgrad2.part_stride, P.S, (int64_t)g.C * 3 * g.C, (const float*)nullptr, 0, g.C,
-                   b.grad + g.off_W2);
+                   b.grad + g.off_W2, (int)SLOT_RED2);
     rec2.end(SLOT_RED2);
     if (e != cudaSuccess) return e;
     ++n;
-    if (cudaEventRecord(P.join, P.aux) != cudaSuccess) return cudaErrorUnknown;
+    }
+    if (!no_fork && cudaEventRecord(P.join, P.aux) != cudaSuccess) return cudaErrorUnknown;
     rec.begin(SLOT_DGRAD);
     e = dispatch<DGRAD_>(P.dgrad, P.npass, s);
     rec.end(SLOT_DGRAD);
@@ -1474,16 +1494,21 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     rec.end(SLOT_WGRAD1);
     if (e != cudaSuccess) return e;
     ++n;
+    if (!defer_reduce) {
     rec.begin(SLOT_RED1);
-    e = launch_pdl(umma::reduce_wgrad_kernel, dim3(296), dim3(256), 0, s, (const float*)b.wpart, P.wgrad1.part_stride,
-                   P.S, (int64_t)g.C * 3 * g.Cin + g.C, (const float*)nullptr, 0, g.C, b.grad + g.off_W1);
+    e = launch_pdl(umma::reduce_wgrad_kernel, dim3(296), dim3(256), 0, s, false, (const float*)b.wpart, P.wgrad1.part_stride,
+                   P.S, (int64_t)g.C * 3 * g.Cin + g.C, (const float*)nullptr, 0, g.C, b.grad + g.off_W1,
+                   (int)SLOT_RED1);
     rec.end(SLOT_RED1);
     if (e != cudaSuccess) return e;
     ++n;
-    if (cudaStreamWaitEvent(s, P.join, 0) != cudaSuccess) return cudaErrorUnknown;  // join
+    }
+    if (!no_fork && cudaStreamWaitEvent(s, P.join, 0) != cudaSuccess) return cudaErrorUnknown;  // join
     *nl += n;
     return cudaSuccess;
 }
+
+void trace_set_umma(unsigned long long* p) { cudaMemcpyToSymbol(g_trace, &p, sizeof(p)); }
 
 void* umma_tstamp_buffer(int64_t* nbytes, int on) {
     void* p = nullptr;
@@ -1494,7 +1519,7 @@ void* umma_tstamp_buffer(int64_t* nbytes, int on) {
 }
 
 cudaError_t launch_prep_x_split(const Geom& g, const float* x, void* hi, void* lo, cudaStream_t s) {
-    return launch_pdl(umma::prep_x_split_kernel, dim3(296), dim3(256), 0, s, x, static_cast<__nv_bfloat16*>(hi),
+    return launch_pdl(umma::prep_x_split_kernel, dim3(296), dim3(256), 0, s, false, x, static_cast<__nv_bfloat16*>(hi),
                       static_cast<__nv_bfloat16*>(lo), g.B, g.T, g.Cin);
 }
 
