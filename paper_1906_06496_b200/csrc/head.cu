@@ -382,7 +382,12 @@ cudaError_t launch_head_rows(const Geom& g, const RankBufs& b, const float* labe
 
 cudaError_t launch_head_reduce(const Geom& g, const RankBufs& b, const float lam[3], float* loss_out,
                                Status* status, const EvRec& rec, cudaStream_t s, int* n) {
-    const int P = head_ctas(g);
+    return launch_head_reduce_rows(g, b, head_ctas(g), lam, loss_out, status, rec, s, n);
+}
+
+// Sum `P` partial rows ([P][4C + 8]: head_rows CTAs, or the fused-head row tiles).
+cudaError_t launch_head_reduce_rows(const Geom& g, const RankBufs& b, int P, const float lam[3], float* loss_out,
+                                    Status* status, const EvRec& rec, cudaStream_t s, int* n) {
     rec.begin(SLOT_HEADFIN);
     const int nent = 4 * g.C + 6;
     const int G = P >= 128 ? 16 : (P >= 16 ? 4 : 1);

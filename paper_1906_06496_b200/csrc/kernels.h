@@ -118,6 +118,15 @@ struct UmmaParams {
     int kclust;          // FWD/DGRAD: > 0 -> split-K cluster kernel with this many CTAs per tile
     int slot;            // trace / timing slot (Slot)
     int side;            // 1: launched on the side branch (low priority)
+    // conv2 FWD with the fused head (fp32 single-wave path, clusters of ntiles CTAs):
+    int fused_head;
+    CUtensorMap out2[2];   // dA2 hi / lo store maps
+    const float* labels;   // [B][3][T] (per call)
+    float lam[3];          // per call
+    const float* b3;
+    float* z_out;          // [B][T][3]
+    float* headpart;       // [mtiles][4C + 8] partial rows (head_reduce input)
+    int Bv, Tn;
     CUtensorMap ones;    // [R][128] bf16: columns 0..63 = 1, 64..127 = 0
 };
 struct UmmaPlan {
@@ -171,6 +180,8 @@ cudaError_t launch_head(const Geom& g, const RankBufs& b, const float* labels, c
                         float* loss_out, Status* status, const EvRec& rec, cudaStream_t s, int* n);
 cudaError_t launch_head_rows(const Geom& g, const RankBufs& b, const float* labels, const float lam[3],
                              const EvRec& rec, cudaStream_t s, int* n);
+cudaError_t launch_head_reduce_rows(const Geom& g, const RankBufs& b, int nrows, const float lam[3],
+                                   float* loss_out, Status* status, const EvRec& rec, cudaStream_t s, int* n);
 cudaError_t launch_head_reduce(const Geom& g, const RankBufs& b, const float lam[3], float* loss_out,
                                Status* status, const EvRec& rec, cudaStream_t s, int* n);
 cudaError_t launch_reduce_splits(const float* part, float* dst, int64_t n, int S, cudaStream_t s);

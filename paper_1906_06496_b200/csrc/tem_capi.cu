@@ -242,9 +242,11 @@ tem_status graph_step(tem_ctx* c, const void* x, const void* lab, void* loss, cu
             return st != TEM_OK ? st : TEM_ERR_CUDA;
         }
         cudaGraphExec_t exec = nullptr;
-        const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+        // per-node launch priorities (critical path vs side branch) only apply with this flag
+        const cudaError_t ie = cudaGraphInstantiateWithFlags(&exec, graph, cudaGraphInstantiateFlagUseNodePriority);
         cudaGraphDestroy(graph);
         if (ie != cudaSuccess) return TEM_ERR_CUDA;
+        cudaGraphUpload(exec, s);
         e = &c->graphs[c->ngraphs++];
         e->x = x;
         e->lab = lab;
@@ -252,10 +254,9 @@ tem_status graph_step(tem_ctx* c, const void* x, const void* lab, void* loss, cu
         e->exec = exec;
         e->launches = nl;
     }
-    if (cudaEventRecord(c->ev_in, s) != cudaSuccess || cudaStreamWaitEvent(c->gstream, c->ev_in, 0) != cudaSuccess ||
-        cudaGraphLaunch(e->exec, c->gstream) != cudaSuccess || cudaEventRecord(c->ev_out, c->gstream) != cudaSuccess ||
-        cudaStreamWaitEvent(s, c->ev_out, 0) != cudaSuccess)
-        return TEM_ERR_CUDA;
+    // Captured on the private stream, replayed directly on the caller's stream (stream order
+    // gives the dependencies; no cross-stream event handoff per step).
+    if (cudaGraphLaunch(e->exec, s) != cudaSuccess) return TEM_ERR_CUDA;
     c->launches_step = e->launches;
     return TEM_OK;
 }

@@ -92,7 +92,7 @@ constexpr uint32_t EPI_SMEM = EPI_BYTES + W3_BYTES + BIAS_BYTES;
 
 // Epilogue warps copy W3 (conv2 FWD with fused logits) and the bias (FWD) to shared memory.
 TEM_DEV void load_epi_smem(const UmmaParams& P, float* sw3, int et) {
-    if (P.zpart) {
+    if (P.zpart || P.fused_head) {
         for (int i = et; i < 3 * P.Nout; i += 128) sw3[i] = P.w3[i];
     }
     if (P.bias) {
@@ -124,7 +124,8 @@ TEM_DEV void dgrad_mask_chunk0(const UmmaParams& P, int row, int col0, uint4 (&p
 
 template <int MODE, int BN, int ACC = 1>
 TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_tile, int split, int q,
-                           int lane, uint8_t* stg, int& buf, const float* sw3, const uint4 (&pm)[2]) {
+                           int lane, uint8_t* stg, int& buf, const float* sw3, const uint4 (&pm)[2],
+                           float* zloc = nullptr) {
     const int row0 = m_tile * BM + 32 * q;
     const int row = row0 + lane;
     if ((MODE == FWD_ || MODE == DGRAD_) && (m_tile >= P.mtiles || row0 >= P.R)) return;
@@ -190,7 +191,7 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
                     v[4 * i4 + k] = (!halo && tv > 0.f) ? tv : 0.f;
                 }
             }
-            if (P.zpart) {  // head row a3, fused: z_o += sum_c W3[o][c] h2[c] (fixed order)
+            if (P.zpart || zloc) {  // head row a3, fused: z_o += sum_c W3[o][c] h2[c] (fixed order)
                 const float4* w = reinterpret_cast<const float4*>(sw3 + gc);
 #pragma unroll
                 for (int i4 = 0; i4 < 4; ++i4) {
@@ -256,7 +257,11 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
         if (c16 + 2 < NC) issue(c16 + 2, ea);
         process(c16 + 1, eb);
     }
-    if (MODE == FWD_ && P.zpart && row < P.R) {
+    if (MODE == FWD_ && zloc) {  // fused head: this tile's partial logits stay in shared memory
+        zloc[(32 * q + lane) * 3 + 0] = zp0;
+        zloc[(32 * q + lane) * 3 + 1] = zp1;
+        zloc[(32 * q + lane) * 3 + 2] = zp2;
+    } else if (MODE == FWD_ && P.zpart && row < P.R) {
         float* zp = P.zpart + ((size_t)n_tile * P.R + row) * 3;
         zp[0] = zp0;
         zp[1] = zp1;
@@ -339,7 +344,8 @@ TEM_DEV void gemm_epilogue_done(uint32_t tbase, int warp) {
 // Epilogue warp loop (warps 2..5): drain accumulator buffer t&1 of every tile this unit owns.
 template <int MODE, int BN, bool PAIR, int ACC, typename Coords>
 TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, uint64_t* tfull, uint64_t* tempty,
-                           int unit, int nunits, int total, Coords coords, int warp, int lane) {
+                           int unit, int nunits, int total, Coords coords, int warp, int lane,
+                           float* zloc = nullptr) {
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
     uint8_t* stg = epi + (warp - 2) * 2 * EPI_BUF;
     float* sw3 = reinterpret_cast<float*>(epi + EPI_BYTES);
@@ -355,7 +361,7 @@ TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, ui
         mbar_wait(&tfull[acc], (t >> 1) & 1);
         tc_fence_after();
         const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * ACC * BN);
-        epilogue_tile<MODE, BN, ACC>(P, tq, m_tile, n_tile, split, q, lane, stg, buf, sw3, pm);
+        epilogue_tile<MODE, BN, ACC>(P, tq, m_tile, n_tile, split, q, lane, stg, buf, sw3, pm, zloc);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {  // buffer free for tile t + 2
@@ -398,9 +404,184 @@ struct CfgHalo {
     static constexpr int TMEM_COLS = ACC == 3 ? 512 : 2 * BN;  // two accumulator buffers
 };
 
-template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR>
+TEM_DEV float softplus_f(float u) { return u > 0.f ? u + log1pf(expf(-u)) : log1pf(expf(u)); }
+
+// ------------------------------------------------------------------ fused head (conv2 FWD)
+// SURVEY 8(a) rows a3-a5 inside conv2's FWD kernel (fp32 single-wave case, HEAD = true): the
+// CTAs of one row tile (one per column tile) form a cluster.  While the mainloop runs, the
+// epilogue warps count the labels of the row tile's videos (alpha+/-, R5/R6) and load their
+// rows' labels.  The epilogue keeps the tile's partial logits W3.h2 in shared memory; after a
+// cluster barrier every CTA sums the partials of its 128 rows over distributed shared memory
+// in column-tile order (the order the unfused head uses), computes z, the loss terms and dz
+// with head_rows_kernel's arithmetic, recomputes h2 from its TMEM accumulator, writes dA2 =
+// 1[h2>0] W3^T dz for its columns in the DGRAD/WGRAD operand format, and reduces dW3 / db2 for
+// its columns over the rows in row order; CTA 0 adds db3, the loss sums and the logits.  One
+// partial row per row tile goes to head_reduce.  A second cluster barrier keeps every CTA's
+// partial logits alive until its peers have read them.
+constexpr uint32_t HEAD_ZLOC_OFF = 140 * 1024;          // in the drained operand rings
+constexpr uint32_t HEAD_LRED_OFF = HEAD_ZLOC_OFF + BM * 3 * 4;
+
+// Epilogue warps, before the accumulator wait: alpha+/- of the (<= 3) videos the row tile
+// touches (one warp per (video, channel), strict > 0.5 -- R5) and this thread's row labels.
+TEM_DEV void head_labels(const UmmaParams& P, float* hap, int m_tile, int warp, int lane, float (&glab)[3]) {
+    const int Tp = P.Tp, Tn = P.Tn, m0 = m_tile * BM;
+    const int last = min(m0 + BM, P.R) - 1;
+    const int v0 = m0 / Tp, nv = last / Tp - v0 + 1;
+    for (int pr = warp - 2; pr < nv * 3; pr += 4) {
+        const int k = pr / 3, o = pr - 3 * k;
+        const float* lab = P.labels + ((size_t)(v0 + k) * 3 + o) * Tn;
+        int lp = 0;
+        for (int t0 = 0; t0 < Tn; t0 += 32) {
+            const bool pos = (t0 + lane < Tn) && lab[t0 + lane] > 0.5f;
+            lp += __popc(__ballot_sync(0xffffffffu, pos));
+        }
+        if (lane == 0) {
+            const int ln = Tn - lp;
+            hap[k * 3 + o] = (float)Tn / (float)(lp > 1 ? lp : 1);
+            hap[9 + k * 3 + o] = (float)Tn / (float)(ln > 1 ? ln : 1);
+        }
+    }
+    const int p = m0 + 32 * (warp & 3) + lane;
+    if (p < P.R && !halo_row(p, Tp)) {
+        const int v = p / Tp, t = p - v * Tp - 1;
+#pragma unroll
+        for (int o = 0; o < 3; ++o) glab[o] = P.labels[((size_t)v * 3 + o) * Tn + t];
+    }
+}
+
+template <int BN, int ACC>
+TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const float* hap, uint32_t tbase,
+                       int m_tile, int n_tile, int warp, int lane, const float (&glab)[3]) {
+    constexpr int RLD = 4 * BN + 4;  // column-partial row: {dz0 h2, dz1 h2, dz2 h2, stored dA2} per column
+    float* red = reinterpret_cast<float*>(smem);
+    float* zloc = reinterpret_cast<float*>(smem + HEAD_ZLOC_OFF);
+    float* lred = reinterpret_cast<float*>(smem + HEAD_LRED_OFF);  // [BM][6] (rank 0)
+    const int S = P.ntiles, r = n_tile;
+    const int C = P.Nout, m0 = m_tile * BM, n0 = n_tile * BN;
+    if (threadIdx.x == 64) tstamp(8);
+    tc_fence_before();
+    cluster_sync();  // every column tile's partial logits are in its shared memory
+    tc_fence_after();
+    if (threadIdx.x == 64) tstamp(9);
+    if (warp >= 2) {
+        const int q = warp & 3, row = 32 * q + lane, p = m0 + row;
+        const int Tp = P.Tp, Tn = P.Tn;
+        const bool live = p < P.R, halo = !live || halo_row(p, Tp);
+        // z: partial logits of all column tiles, column-tile order, then + b3
+        float pz[8][3];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+#pragma unroll
+            for (int o = 0; o < 3; ++o)
+                pz[k][o] = k < S ? ld_dsmem_f32(mapa_shared(zloc + row * 3 + o, (uint32_t)k)) : 0.f;
+        float z[3], dz[3] = {0.f, 0.f, 0.f}, lt[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+        for (int o = 0; o < 3; ++o) {
+            float sz = pz[0][o];
+#pragma unroll
+            for (int k = 1; k < 8; ++k)
+                if (k < S) sz += pz[k][o];
+            z[o] = sz + P.b3[o];
+        }
+        if (!halo) {  // rows a3/a4 exactly as head_rows_kernel's row_loss
+            const int v = p / Tp, t = p - v * Tp - 1, k = v - m0 / Tp;
+            const float inv_bt = 1.0f / ((float)P.Bv * (float)Tn);
+#pragma unroll
+            for (int o = 0; o < 3; ++o) {
+                const float bt = glab[o] > 0.5f ? 1.f : 0.f;
+                const float ap = hap[k * 3 + o], an = hap[9 + k * 3 + o];
+                const float logp = -softplus_f(-z[o]), log1mp = -softplus_f(z[o]);
+                lt[o] = ap * bt * logp + an * (1.f - bt) * log1mp;
+                const float pr = 1.f / (1.f + expf(-z[o]));
+                dz[o] = P.lam[o] * inv_bt * (an * (1.f - bt) * pr - ap * bt * (1.f - pr));
+                if (r == 0) P.z_out[((size_t)v * Tn + t) * 3 + o] = z[o];
+            }
+        }
+        if (r == 0) {
+#pragma unroll
+            for (int o = 0; o < 3; ++o) {
+                lred[row * 6 + o] = lt[o];
+                lred[row * 6 + 3 + o] = dz[o];
+            }
+        }
+        if (threadIdx.x == 64) tstamp(10);
+        // dA2 for this CTA's columns (h2 recomputed from the accumulator exactly as the epilogue)
+        const float* sw3 = reinterpret_cast<const float*>(epi + EPI_BYTES);
+        const float* sbias = sw3 + 3 * 512;
+        uint8_t* stg = epi + (warp - 2) * 2 * EPI_BUF;
+        const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16);
+        float* rrow = red + (size_t)row * RLD;
+        int buf = 0;
+        for (int c16 = 0; c16 < BN / 16; ++c16) {
+            const int gc = n0 + c16 * 16;
+            uint32_t ra[16], rb[16], rc[16];
+            tmem_ld16(tq + (uint32_t)(c16 * 16), ra);
+            if (ACC == 3) {
+                tmem_ld16(tq + (uint32_t)(BN + c16 * 16), rb);
+                tmem_ld16(tq + (uint32_t)(2 * BN + c16 * 16), rc);
+            }
+            tmem_ld_wait_regs(ra);
+            if (ACC == 3) {
+                tmem_regs_fence(rb);
+                tmem_regs_fence(rc);
+            }
+            float dv[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                float v = __uint_as_float(ra[i]);
+                if (ACC == 3) v = (v + __uint_as_float(rb[i])) + __uint_as_float(rc[i]);
+                const float tv = v + sbias[gc + i];
+                const float h = (!halo && tv > 0.f) ? tv : 0.f;
+                const float w0 = sw3[gc + i], w1 = sw3[C + gc + i], w2 = sw3[2 * C + gc + i];
+                float d = w0 * dz[0];
+                d = fmaf(w1, dz[1], d);
+                d = fmaf(w2, dz[2], d);
+                dv[i] = h > 0.f ? d : 0.f;
+                const __nv_bfloat16 hi = __float2bfloat16_rn(dv[i]);
+                const float stv = __bfloat162float(hi) + __bfloat162float(__float2bfloat16_rn(dv[i] - __bfloat162float(hi)));
+                *reinterpret_cast<float4*>(rrow + (c16 * 16 + i) * 4) = make_float4(dz[0] * h, dz[1] * h, dz[2] * h, stv);
+            }
+            uint8_t* sb = stg + buf * EPI_BUF;
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+            store16_planes(reinterpret_cast<__nv_bfloat16*>(sb + lane * 32),
+                           reinterpret_cast<__nv_bfloat16*>(sb + 1024 + lane * 32), dv);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_2d(&P.out2[0], sb, gc, m0 + 32 * q);
+                tma_store_2d(&P.out2[1], sb + 1024, gc, m0 + 32 * q);
+                bulk_commit();
+            }
+            buf ^= 1;
+        }
+        if (lane == 0) bulk_wait_read<0>();
+        if (threadIdx.x == 64) tstamp(11);
+    }
+    __syncthreads();  // column partials of all rows in shared memory
+    float* dst = P.headpart + (size_t)m_tile * (4 * C + 8);  // [dW3 (3C)][db3 (3)][L (3)][db2 (C)]
+    for (int j = threadIdx.x; j < 4 * BN; j += NTHREADS) {
+        float acc = 0.f;
+        for (int row = 0; row < BM; ++row) acc += red[(size_t)row * RLD + j];  // row order
+        const int c = j >> 2, kind = j & 3;
+        dst[kind < 3 ? kind * C + n0 + c : 3 * C + 6 + n0 + c] = acc;
+    }
+    if (r == 0 && threadIdx.x < 6) {
+        float acc = 0.f;
+        for (int row = 0; row < BM; ++row) acc += lred[row * 6 + threadIdx.x];
+        if (threadIdx.x < 3) dst[3 * C + 3 + threadIdx.x] = -acc / (float)P.Tn;  // loss sum
+        else dst[3 * C + threadIdx.x - 3] = acc;                                  // db3
+    }
+    if (threadIdx.x == 64) tstamp(12);
+    tc_fence_before();
+    cluster_sync();  // peers have read this CTA's partial logits
+    if (threadIdx.x == 64) tstamp(13);
+}
+
+template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR, bool HEAD = false>
 __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_constant__ UmmaParams P) {
     static_assert(MODE == FWD_ || MODE == DGRAD_, "halo kernel: FWD / DGRAD");
+    static_assert(!HEAD || (MODE == FWD_ && !PAIR), "fused head: 1-CTA conv2 FWD");
     using C_ = CfgHalo<BN, NPASS, SA, SB, PAIR>;
     constexpr int NPL = C_::NPL;
     constexpr bool B_MN = (MODE == DGRAD_);
@@ -416,6 +597,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
     uint64_t* tempty = tfull + 2;   // [2]
     uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
     uint8_t* epi = smem + C_::RINGS + 1024;
+    float* hap = reinterpret_cast<float*>(smem + C_::RINGS + 512);  // HEAD: alpha+ [3][3], alpha- [3][3]
+    static_assert(!HEAD || HEAD_LRED_OFF + BM * 6 * 4 <= C_::RINGS, "head scratch fits the rings");
+    static_assert(!HEAD || BM * (4 * BN + 4) * 4 <= HEAD_ZLOC_OFF, "head column buffer below the logits");
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
@@ -426,6 +610,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
     const int total = mt_u * P.ntiles;
     if (threadIdx.x == 0) tstamp(0);
     trace_begin(P.slot);
+    float glab[3] = {0.f, 0.f, 0.f};  // HEAD: this epilogue thread's row labels
     const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, fullA, 2 * (SA + SB), tfull, tempty, tslot, warp, lane);
     if (threadIdx.x == 0) tstamp(1);
 
@@ -529,9 +714,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
         }
         __syncwarp();
     } else {
-        epilogue_loop<MODE, BN, PAIR, C_::ACC>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane);
+        if (HEAD) head_labels(P, hap, unit / P.ntiles, warp, lane, glab);
+        epilogue_loop<MODE, BN, PAIR, C_::ACC>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane,
+                                               HEAD ? reinterpret_cast<float*>(smem + HEAD_ZLOC_OFF) : nullptr);
         if (threadIdx.x == 64) tstamp(6);
     }
+    if constexpr (HEAD) head_tail<BN, C_::ACC>(P, smem, epi, hap, tbase, unit / P.ntiles, unit % P.ntiles, warp, lane, glab);
     gemm_epilogue_done<C_::TMEM_COLS, PAIR>(tbase, warp);
     trace_end(P.slot);
 }
@@ -1183,6 +1371,65 @@ cudaError_t launch_persistent(K k, uint32_t smem, bool pair, int total, int* max
     return cudaLaunchKernelEx(&cfg, k, p);
 }
 
+// conv2 FWD with the fused head: clusters of ntiles CTAs (one row tile each), one wave.
+template <int BN, int NPASS, int SA, int SB>
+cudaError_t launch_halo_head(const UmmaParams& p, cudaStream_t s) {
+    using C_ = umma::CfgHalo<BN, NPASS, SA, SB, false>;
+    auto k = umma::umma_halo_kernel<FWD_, BN, NPASS, SA, SB, false, true>;
+    static bool init = false;
+    if (!init) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM);
+        if (e != cudaSuccess) return e;
+        init = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[3];
+    int na = 0;
+    if (pdl_enabled()) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    na += launch_priority_attr(&attr[na], false);
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = p.ntiles;
+    attr[na].val.clusterDim.y = 1;
+    attr[na++].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(p.mtiles * p.ntiles, 1, 1);
+    cfg.blockDim = dim3(umma::NTHREADS);
+    cfg.dynamicSmemBytes = C_::SMEM;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, k, p);
+}
+
+// How many row tiles of fused-head clusters fit at once (0 if the kernel cannot launch).
+int umma_head_max_clusters(int ntiles) {
+    using C_ = umma::CfgHalo<64, 3, 3, 6, false>;
+    auto k = umma::umma_halo_kernel<FWD_, 64, 3, 3, 6, false, true>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ntiles;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(ntiles * 16, 1, 1);
+    cfg.blockDim = dim3(umma::NTHREADS);
+    cfg.dynamicSmemBytes = C_::SMEM;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
 template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR>
 cudaError_t launch_halo(const UmmaParams& p, cudaStream_t s) {
     static int max_units = -1;
@@ -1352,6 +1599,21 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     P.conv2.w3 = b.params + g.off_W3;
     // [C/BN][R][3] partial logits for the head (which sums at most 8 per row)
     P.conv2.zpart = (getenv("TEM_NO_ZPART") || g.C / cf.bn > 8) ? nullptr : b.zpart;
+    // fp32 single-wave path: the head fused into conv2 FWD (clusters of the C/64 column tiles
+    // of a row tile).  TEM_NO_FUSED_HEAD=1 keeps the separate head kernel.
+    if (P.npass == 3 && !cf.pair && cf.bn == 64 && P.conv2.kclust == 0 && P.conv2.ntiles <= 8 &&
+        mtiles * P.conv2.ntiles <= 148 && Tp >= 64 && g.C <= 512 && !getenv("TEM_NO_FUSED_HEAD") &&
+        umma_head_max_clusters(P.conv2.ntiles) >= mtiles) {
+        P.conv2.fused_head = 1;
+        P.conv2.zpart = nullptr;
+        P.conv2.b3 = b.params + g.off_b3;
+        P.conv2.z_out = b.z;
+        P.conv2.headpart = b.headpart;
+        P.conv2.Bv = g.B;
+        P.conv2.Tn = g.T;
+        ok &= map_store2d(&P.conv2.out2[0], b.dA2, false, g.C, R);
+        ok &= map_store2d(&P.conv2.out2[1], b.dA2_lo, false, g.C, R);
+    }
     common(P.dgrad);
     P.dgrad.slot = SLOT_DGRAD;
     P.dgrad.Kc = g.C;
@@ -1365,7 +1627,7 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     // Experimental (TEM_SPLITK=1): small-M fp32 FWD / DGRAD as split-K clusters of 128 x 256
     // tiles (umma_splitk_kernel).  Correct, but on B200 the slice exchange costs what the
     // N = 256 mainloop saves at B = 16, so the halo kernel is the default.
-    if (P.npass == 3 && g.C % 256 == 0 && getenv("TEM_SPLITK")) {  // opt-in: see DESIGN.md 6
+    if (P.npass == 3 && g.C % 256 == 0 && getenv("TEM_SPLITK") && !P.conv2.fused_head) {  // opt-in: DESIGN.md 6
         const int cpb_min = std::min(P.conv1.cpb, std::min(P.conv2.cpb, P.dgrad.cpb));
         const int tiles = mtiles * (g.C / 256);
         const int S = 4;  // slice exchange buffers / prefetched mask sized for S = 4 (64-column slices)
@@ -1426,6 +1688,8 @@ void umma_plan_destroy(UmmaPlan* plan) {
     delete plan;
 }
 
+static int mtiles_of(const UmmaPlan& P) { return P.conv2.mtiles; }
+
 template <int MODE>
 static cudaError_t dispatch(const UmmaParams& p, int npass, cudaStream_t s) {
     const GemmCfg c = cfg_for(MODE, npass);
@@ -1434,6 +1698,8 @@ static cudaError_t dispatch(const UmmaParams& p, int npass, cudaStream_t s) {
         return npass == 3 ? launch_wgrad<128, 3, 3, false>(p, s) : launch_wgrad<256, 1, 4, false>(p, s);
     } else {
         if (p.kclust > 0 && npass == 3) return launch_splitk<MODE, 3, 2, 2>(p, s);  // plan: fp32 only
+        if constexpr (MODE == FWD_)
+            if (p.fused_head) return launch_halo_head<64, 3, 3, 6>(p, s);  // plan: fp32, BN = 64
         if (c.pair && c.bn == 64) return launch_halo<MODE, 64, 3, 3, 6, true>(p, s);
         if (c.pair)
             return npass == 3 ? launch_halo<MODE, 128, 3, 3, 6, true>(p, s) : launch_halo<MODE, 256, 1, 4, 8, true>(p, s);
@@ -1452,12 +1718,23 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     if (e != cudaSuccess) return e;
     ++n;
     rec.begin(SLOT_CONV2);
-    e = dispatch<FWD_>(P.conv2, P.npass, s);
+    if (P.conv2.fused_head) {
+        UmmaParams c2 = P.conv2;  // per-call: labels and loss weights
+        c2.labels = labels;
+        c2.lam[0] = lam[0];
+        c2.lam[1] = lam[1];
+        c2.lam[2] = lam[2];
+        e = dispatch<FWD_>(c2, P.npass, s);
+    } else {
+        e = dispatch<FWD_>(P.conv2, P.npass, s);
+    }
     rec.end(SLOT_CONV2);
     if (e != cudaSuccess) return e;
     ++n;
-    e = launch_head_rows(g, b, labels, lam, rec, s, &n);
-    if (e != cudaSuccess) return e;
+    if (!P.conv2.fused_head) {
+        e = launch_head_rows(g, b, labels, lam, rec, s, &n);
+        if (e != cudaSuccess) return e;
+    }
     // Fork: the head reduction and conv2 wgrad (+ its reduction) run on the aux stream
     // alongside conv2 dgrad -> conv1 wgrad on s; all only read dA2 / h1 / xp / head
     // partials (captured as parallel graph branches).
@@ -1467,7 +1744,8 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     if (!no_fork &&
         (cudaEventRecord(P.fork, s) != cudaSuccess || cudaStreamWaitEvent(P.aux, P.fork, 0) != cudaSuccess))
         return cudaErrorUnknown;
-    e = launch_head_reduce(g, b, lam, loss_out, status, rec2, aux, &n);
+    e = P.conv2.fused_head ? launch_head_reduce_rows(g, b, mtiles_of(P), lam, loss_out, status, rec2, aux, &n)
+                           : launch_head_reduce(g, b, lam, loss_out, status, rec2, aux, &n);
     if (e != cudaSuccess) return e;
     rec2.begin(SLOT_WGRAD2);
     e = dispatch<WGRAD_>(P.wgrad2, P.npass, aux);

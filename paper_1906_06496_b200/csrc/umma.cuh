@@ -102,6 +102,11 @@ UMMA_DEV uint32_t cluster_nctarank() {
     asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
     return r;
 }
+UMMA_DEV float ld_dsmem_f32(uint32_t addr) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+    return v;
+}
 // 16-byte load from a shared::cluster address (another CTA's shared memory, via mapa).
 UMMA_DEV float4 ld_dsmem_v4(uint32_t addr) {
     float4 v;

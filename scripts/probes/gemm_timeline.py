@@ -17,13 +17,15 @@ sys.path.insert(0, ROOT)
 
 PHASES = {"split": ["entry", "pdl_wait", "prod_firstA", "mma_fullA", "mma_fullB", "mma_done", "epi_tfull",
                     "cluster1", "packed", "received", "done"],
-          "halo": ["entry", "pdl_wait", "mma_fullA0", "tile0_mma_done", "last_mma_done", "-", "epi_done"]}
+          "halo": ["entry", "pdl_wait", "mma_fullA0", "tile0_mma_done", "last_mma_done", "-", "epi_done"],
+          # conv2 FWD with the fused head (stamps 8..13; conv2 dgrad overwrites 0..6)
+          "head": ["-"] * 8 + ["head_start", "cluster1", "dz_done", "dA2_done", "colsum_done", "cluster2"]}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c2")
-    ap.add_argument("--kernel", default="halo", choices=["halo", "split"])
+    ap.add_argument("--kernel", default="halo", choices=["halo", "split", "head"])
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -48,12 +50,12 @@ def main():
     raw = torch.as_tensor(_Arr(), device="cuda").cpu().numpy().reshape(1024, 16)
     used = raw[:, 0] > 0
     raw = raw[used]
-    t0 = raw[:, 0].min()
+    t0 = raw[:, 0].min() if args.kernel != "head" else raw[:, 8][raw[:, 8] > 0].min()
     print(f"{used.sum()} CTAs stamped")
     for k, name in enumerate(PHASES[args.kernel]):
         col = raw[:, k]
         col = col[col > 0]
-        if len(col):
+        if len(col) and name != "-":
             d = (col - t0) / 1e3
             print(f"{name:>12}: median {np.median(d):7.2f} us  max {d.max():7.2f} us  (n={len(col)})")
     s.close()
