@@ -49,6 +49,22 @@ TEM_DEV uint64_t globaltimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
+// One snippet row of the head (readings R5-R7) for output channel o:
+// the loss term alpha+ b log p + alpha- (1-b) log(1-p) and dz = lam/(B T) (alpha- (1-b) p -
+// alpha+ b (1-p)).  With e = exp(-|z|): p and 1-p are 1/(1+e) and e/(1+e) (which one depends on
+// the sign of z; no cancellation), log p = -softplus(-z), log(1-p) = -softplus(z) and
+// softplus(+-z) = max(+-z, 0) + log1p(e) -- one exp and one log1p per row and channel.
+TEM_DEV void head_row_terms(float z, float bt, float ap, float an, float lam_over_bt, float& lt, float& dz) {
+    const float e = expf(-fabsf(z));
+    const float r = __frcp_rn(1.f + e);
+    const float er = e * r;
+    const float p = z >= 0.f ? r : er, q = z >= 0.f ? er : r;  // p, 1 - p
+    const float l1 = log1pf(e);
+    const float logp = -(fmaxf(-z, 0.f) + l1), log1mp = -(fmaxf(z, 0.f) + l1);
+    lt = ap * bt * logp + an * (1.f - bt) * log1mp;
+    dz = lam_over_bt * (an * (1.f - bt) * p - ap * bt * q);
+}
+
 // Kernel-span trace (diagnostics, scripts/probes/step_trace.py): while g_trace is set (one
 // copy per translation unit, set by trace_set_<unit>), each traced kernel records the minimum
 // start and maximum end globaltimer over its CTAs in g_trace[2 slot], g_trace[2 slot + 1].

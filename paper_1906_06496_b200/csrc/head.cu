@@ -25,7 +25,6 @@ namespace {
 constexpr int HEAD_WARPS = 8;
 constexpr int NZP_MAX = 8;  // fused-logit partials per row (C / BN of the conv2 epilogue)
 
-TEM_DEV float softplusf(float u) { return u > 0.f ? u + log1pf(expf(-u)) : log1pf(expf(u)); }
 
 TEM_DEV void store4(float* dst, const float (&v)[4]) {
     *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
@@ -113,10 +112,9 @@ __global__ void __launch_bounds__(256, 3) head_rows_kernel(
             const float g = labels[((size_t)v * 3 + o) * Tn + t];
             const float bt = g > 0.5f ? 1.f : 0.f;
             const float ap = s_ap[k][o], an = s_an[k][o];
-            const float logp = -softplusf(-z[o]), log1mp = -softplusf(z[o]);
-            lsum[o] += ap * bt * logp + an * (1.f - bt) * log1mp;
-            const float pr = 1.f / (1.f + expf(-z[o]));
-            const float dz = lam[o] * inv_bt * (an * (1.f - bt) * pr - ap * bt * (1.f - pr));
+            float lt, dz;
+            head_row_terms(z[o], bt, ap, an, lam[o] * inv_bt, lt, dz);
+            lsum[o] += lt;
             dbs[o] += dz;
             dzr[o] = dz;
             z_out[((size_t)v * Tn + t) * 3 + o] = z[o];

@@ -257,10 +257,11 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
         if (c16 + 2 < NC) issue(c16 + 2, ea);
         process(c16 + 1, eb);
     }
-    if (MODE == FWD_ && zloc) {  // fused head: this tile's partial logits stay in shared memory
-        zloc[(32 * q + lane) * 3 + 0] = zp0;
-        zloc[(32 * q + lane) * 3 + 1] = zp1;
-        zloc[(32 * q + lane) * 3 + 2] = zp2;
+    if (MODE == FWD_ && zloc) {
+        // fused head: push this tile's partial logits into slot n_tile of every CTA of the
+        // cluster (zloc = the receive buffer [ntiles][BM][4]; distributed-shared-memory stores)
+        float* mine = zloc + ((size_t)n_tile * BM + 32 * q + lane) * 4;
+        for (int k = 0; k < P.ntiles; ++k) st_dsmem_v4(mapa_shared(mine, (uint32_t)k), zp0, zp1, zp2, 0.f);
     } else if (MODE == FWD_ && P.zpart && row < P.R) {
         float* zp = P.zpart + ((size_t)n_tile * P.R + row) * 3;
         zp[0] = zp0;
@@ -270,6 +271,9 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
 }
 
 // ------------------------------------------------------------------ common kernel pieces
+// 1 KB-aligned dynamic shared memory base, by pointer arithmetic on the __shared__ array so the
+// compiler keeps the shared address space (LDS/STS, not generic LD/ST) for derived pointers.
+TEM_DEV uint8_t* align_smem_1k(uint8_t* raw) { return raw + ((1024u - (smem_u32(raw) & 1023u)) & 1023u); }
 // PAIR = false: one CTA computes a 128 x BN tile (tcgen05.mma.cta_group::1).
 // PAIR = true : a cluster of 2 CTAs computes a 256 x BN tile with tcgen05.mma.cta_group::2
 // issued by the leader (rank 0): each CTA stages its own 128 rows of A and half of the BN
@@ -404,7 +408,6 @@ struct CfgHalo {
     static constexpr int TMEM_COLS = ACC == 3 ? 512 : 2 * BN;  // two accumulator buffers
 };
 
-TEM_DEV float softplus_f(float u) { return u > 0.f ? u + log1pf(expf(-u)) : log1pf(expf(u)); }
 
 // ------------------------------------------------------------------ fused head (conv2 FWD)
 // SURVEY 8(a) rows a3-a5 inside conv2's FWD kernel (fp32 single-wave case, HEAD = true): the
@@ -418,8 +421,8 @@ TEM_DEV float softplus_f(float u) { return u > 0.f ? u + log1pf(expf(-u)) : log1
 // its columns over the rows in row order; CTA 0 adds db3, the loss sums and the logits.  One
 // partial row per row tile goes to head_reduce.  A second cluster barrier keeps every CTA's
 // partial logits alive until its peers have read them.
-constexpr uint32_t HEAD_ZLOC_OFF = 140 * 1024;          // in the drained operand rings
-constexpr uint32_t HEAD_LRED_OFF = HEAD_ZLOC_OFF + BM * 3 * 4;
+constexpr uint32_t HEAD_LRED_OFF = 136 * 1024;  // [BM][6], in the drained operand rings
+constexpr uint32_t HEAD_ZRECV_BYTES = 8 * BM * 4 * 4;  // [ntiles <= 8][BM][4] partial logits received
 
 // Epilogue warps, before the accumulator wait: alpha+/- of the (<= 3) videos the row tile
 // touches (one warp per (video, channel), strict > 0.5 -- R5) and this thread's row labels.
@@ -450,17 +453,16 @@ TEM_DEV void head_labels(const UmmaParams& P, float* hap, int m_tile, int warp, 
 }
 
 template <int BN, int ACC>
-TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const float* hap, uint32_t tbase,
-                       int m_tile, int n_tile, int warp, int lane, const float (&glab)[3]) {
+TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const float* zrecv, const float* hap,
+                       uint32_t tbase, int m_tile, int n_tile, int warp, int lane, const float (&glab)[3]) {
     constexpr int RLD = 4 * BN + 4;  // column-partial row: {dz0 h2, dz1 h2, dz2 h2, stored dA2} per column
     float* red = reinterpret_cast<float*>(smem);
-    float* zloc = reinterpret_cast<float*>(smem + HEAD_ZLOC_OFF);
     float* lred = reinterpret_cast<float*>(smem + HEAD_LRED_OFF);  // [BM][6] (rank 0)
     const int S = P.ntiles, r = n_tile;
     const int C = P.Nout, m0 = m_tile * BM, n0 = n_tile * BN;
     if (threadIdx.x == 64) tstamp(8);
     tc_fence_before();
-    cluster_sync();  // every column tile's partial logits are in its shared memory
+    cluster_sync();  // every column tile has pushed its partial logits into every CTA's zrecv
     tc_fence_after();
     if (threadIdx.x == 64) tstamp(9);
     if (warp >= 2) {
@@ -470,10 +472,13 @@ TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const f
         // z: partial logits of all column tiles, column-tile order, then + b3
         float pz[8][3];
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-#pragma unroll
-            for (int o = 0; o < 3; ++o)
-                pz[k][o] = k < S ? ld_dsmem_f32(mapa_shared(zloc + row * 3 + o, (uint32_t)k)) : 0.f;
+        for (int k = 0; k < 8; ++k) {
+            float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (k < S) t = *reinterpret_cast<const float4*>(zrecv + ((size_t)k * BM + row) * 4);
+            pz[k][0] = t.x;
+            pz[k][1] = t.y;
+            pz[k][2] = t.z;
+        }
         float z[3], dz[3] = {0.f, 0.f, 0.f}, lt[3] = {0.f, 0.f, 0.f};
 #pragma unroll
         for (int o = 0; o < 3; ++o) {
@@ -490,10 +495,7 @@ TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const f
             for (int o = 0; o < 3; ++o) {
                 const float bt = glab[o] > 0.5f ? 1.f : 0.f;
                 const float ap = hap[k * 3 + o], an = hap[9 + k * 3 + o];
-                const float logp = -softplus_f(-z[o]), log1mp = -softplus_f(z[o]);
-                lt[o] = ap * bt * logp + an * (1.f - bt) * log1mp;
-                const float pr = 1.f / (1.f + expf(-z[o]));
-                dz[o] = P.lam[o] * inv_bt * (an * (1.f - bt) * pr - ap * bt * (1.f - pr));
+                head_row_terms(z[o], bt, ap, an, P.lam[o] * inv_bt, lt[o], dz[o]);
                 if (r == 0) P.z_out[((size_t)v * Tn + t) * 3 + o] = z[o];
             }
         }
@@ -525,27 +527,58 @@ TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const f
                 tmem_regs_fence(rb);
                 tmem_regs_fence(rc);
             }
-            float dv[16];
+            if (c16 == 0 && threadIdx.x == 64) tstamp(13);
+            float dv[16], hv[16];
+            const float4* w0p = reinterpret_cast<const float4*>(sw3 + gc);
+            const float4* w1p = reinterpret_cast<const float4*>(sw3 + C + gc);
+            const float4* w2p = reinterpret_cast<const float4*>(sw3 + 2 * C + gc);
+            const float4* bip = reinterpret_cast<const float4*>(sbias + gc);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                float v = __uint_as_float(ra[i]);
-                if (ACC == 3) v = (v + __uint_as_float(rb[i])) + __uint_as_float(rc[i]);
-                const float tv = v + sbias[gc + i];
-                const float h = (!halo && tv > 0.f) ? tv : 0.f;
-                const float w0 = sw3[gc + i], w1 = sw3[C + gc + i], w2 = sw3[2 * C + gc + i];
-                float d = w0 * dz[0];
-                d = fmaf(w1, dz[1], d);
-                d = fmaf(w2, dz[2], d);
-                dv[i] = h > 0.f ? d : 0.f;
-                const __nv_bfloat16 hi = __float2bfloat16_rn(dv[i]);
-                const float stv = __bfloat162float(hi) + __bfloat162float(__float2bfloat16_rn(dv[i] - __bfloat162float(hi)));
-                *reinterpret_cast<float4*>(rrow + (c16 * 16 + i) * 4) = make_float4(dz[0] * h, dz[1] * h, dz[2] * h, stv);
+            for (int i4 = 0; i4 < 4; ++i4) {
+                const float4 a0 = w0p[i4], a1 = w1p[i4], a2 = w2p[i4], bb = bip[i4];
+                const float w0[4] = {a0.x, a0.y, a0.z, a0.w}, w1[4] = {a1.x, a1.y, a1.z, a1.w};
+                const float w2[4] = {a2.x, a2.y, a2.z, a2.w}, bv[4] = {bb.x, bb.y, bb.z, bb.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int i = 4 * i4 + k;
+                    float v = __uint_as_float(ra[i]);
+                    if (ACC == 3) v = (v + __uint_as_float(rb[i])) + __uint_as_float(rc[i]);
+                    const float tv = v + bv[k];
+                    const float h = (!halo && tv > 0.f) ? tv : 0.f;  // = the h2 the epilogue stored
+                    float d = w0[k] * dz[0];
+                    d = fmaf(w1[k], dz[1], d);
+                    d = fmaf(w2[k], dz[2], d);
+                    dv[i] = h > 0.f ? d : 0.f;
+                    hv[i] = h;
+                }
+            }
+            if (c16 == 0 && threadIdx.x == 64) tstamp(14);
+            // hi / lo operand planes of dA2 (R16) and the stored value hi + lo for db2
+            uint32_t hp[8], lp[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const __nv_bfloat16 h0 = __float2bfloat16_rn(dv[2 * i]), h1 = __float2bfloat16_rn(dv[2 * i + 1]);
+                const float f0 = __bfloat162float(h0), f1 = __bfloat162float(h1);
+                const __nv_bfloat16 l0 = __float2bfloat16_rn(dv[2 * i] - f0), l1 = __float2bfloat16_rn(dv[2 * i + 1] - f1);
+                __nv_bfloat162 hh, ll;
+                hh.x = h0; hh.y = h1; ll.x = l0; ll.y = l1;
+                hp[i] = *reinterpret_cast<uint32_t*>(&hh);
+                lp[i] = *reinterpret_cast<uint32_t*>(&ll);
+                *reinterpret_cast<float4*>(rrow + (c16 * 16 + 2 * i) * 4) =
+                    make_float4(dz[0] * hv[2 * i], dz[1] * hv[2 * i], dz[2] * hv[2 * i], f0 + __bfloat162float(l0));
+                *reinterpret_cast<float4*>(rrow + (c16 * 16 + 2 * i + 1) * 4) =
+                    make_float4(dz[0] * hv[2 * i + 1], dz[1] * hv[2 * i + 1], dz[2] * hv[2 * i + 1],
+                                f1 + __bfloat162float(l1));
             }
             uint8_t* sb = stg + buf * EPI_BUF;
             if (lane == 0) bulk_wait_read<1>();
             __syncwarp();
-            store16_planes(reinterpret_cast<__nv_bfloat16*>(sb + lane * 32),
-                           reinterpret_cast<__nv_bfloat16*>(sb + 1024 + lane * 32), dv);
+            uint4* dh = reinterpret_cast<uint4*>(sb + lane * 32);
+            uint4* dl = reinterpret_cast<uint4*>(sb + 1024 + lane * 32);
+            dh[0] = make_uint4(hp[0], hp[1], hp[2], hp[3]);
+            dh[1] = make_uint4(hp[4], hp[5], hp[6], hp[7]);
+            dl[0] = make_uint4(lp[0], lp[1], lp[2], lp[3]);
+            dl[1] = make_uint4(lp[4], lp[5], lp[6], lp[7]);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) {
@@ -554,6 +587,7 @@ TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const f
                 bulk_commit();
             }
             buf ^= 1;
+            if (c16 == 0 && threadIdx.x == 64) tstamp(15);
         }
         if (lane == 0) bulk_wait_read<0>();
         if (threadIdx.x == 64) tstamp(11);
@@ -573,9 +607,7 @@ TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const f
         else dst[3 * C + threadIdx.x - 3] = acc;                                  // db3
     }
     if (threadIdx.x == 64) tstamp(12);
-    tc_fence_before();
-    cluster_sync();  // peers have read this CTA's partial logits
-    if (threadIdx.x == 64) tstamp(13);
+    // no second cluster barrier: every remote access (the pushes) happened before the first
 }
 
 template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR, bool HEAD = false>
@@ -586,7 +618,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
     constexpr int NPL = C_::NPL;
     constexpr bool B_MN = (MODE == DGRAD_);
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = align_smem_1k(smem_raw);
     uint8_t* sA = smem;
     uint8_t* sB = smem + SA * C_::A_STAGE;
     uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + C_::RINGS);
@@ -599,7 +631,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
     uint8_t* epi = smem + C_::RINGS + 1024;
     float* hap = reinterpret_cast<float*>(smem + C_::RINGS + 512);  // HEAD: alpha+ [3][3], alpha- [3][3]
     static_assert(!HEAD || HEAD_LRED_OFF + BM * 6 * 4 <= C_::RINGS, "head scratch fits the rings");
-    static_assert(!HEAD || BM * (4 * BN + 4) * 4 <= HEAD_ZLOC_OFF, "head column buffer below the logits");
+    static_assert(!HEAD || BM * (4 * BN + 4) * 4 <= HEAD_LRED_OFF, "head column buffer below the loss terms");
+    float* zrecv = reinterpret_cast<float*>(smem + C_::RINGS + 1024 + EPI_SMEM);  // HEAD only (SMEM_HEAD)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
@@ -716,10 +749,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
     } else {
         if (HEAD) head_labels(P, hap, unit / P.ntiles, warp, lane, glab);
         epilogue_loop<MODE, BN, PAIR, C_::ACC>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane,
-                                               HEAD ? reinterpret_cast<float*>(smem + HEAD_ZLOC_OFF) : nullptr);
+                                               HEAD ? zrecv : nullptr);
         if (threadIdx.x == 64) tstamp(6);
     }
-    if constexpr (HEAD) head_tail<BN, C_::ACC>(P, smem, epi, hap, tbase, unit / P.ntiles, unit % P.ntiles, warp, lane, glab);
+    if constexpr (HEAD)
+        head_tail<BN, C_::ACC>(P, smem, epi, zrecv, hap, tbase, unit / P.ntiles, unit % P.ntiles, warp, lane, glab);
     gemm_epilogue_done<C_::TMEM_COLS, PAIR>(tbase, warp);
     trace_end(P.slot);
 }
@@ -762,7 +796,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_splitk_kernel(const __grid_c
     constexpr int BN = C_::BN, NPL = C_::NPL;
     constexpr bool B_MN = (MODE == DGRAD_);
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = align_smem_1k(smem_raw);
     uint8_t* sA = smem;
     uint8_t* sB = smem + SA * C_::A_STAGE;
     uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + C_::RINGS);
@@ -1058,7 +1092,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
     using C_ = CfgW<BN, NPASS, STAGES, PAIR>;
     constexpr int NPL = C_::NPL;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* smem = align_smem_1k(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C_::STAGE_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;  // [2]
@@ -1375,10 +1409,12 @@ cudaError_t launch_persistent(K k, uint32_t smem, bool pair, int total, int* max
 template <int BN, int NPASS, int SA, int SB>
 cudaError_t launch_halo_head(const UmmaParams& p, cudaStream_t s) {
     using C_ = umma::CfgHalo<BN, NPASS, SA, SB, false>;
+    constexpr uint32_t SMEM = C_::SMEM + umma::HEAD_ZRECV_BYTES;
+    static_assert(SMEM <= 232448, "fused-head smem");
     auto k = umma::umma_halo_kernel<FWD_, BN, NPASS, SA, SB, false, true>;
     static bool init = false;
     if (!init) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM);
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
         if (e != cudaSuccess) return e;
         init = true;
     }
@@ -1396,7 +1432,7 @@ cudaError_t launch_halo_head(const UmmaParams& p, cudaStream_t s) {
     attr[na++].val.clusterDim.z = 1;
     cfg.gridDim = dim3(p.mtiles * p.ntiles, 1, 1);
     cfg.blockDim = dim3(umma::NTHREADS);
-    cfg.dynamicSmemBytes = C_::SMEM;
+    cfg.dynamicSmemBytes = SMEM;
     cfg.stream = s;
     cfg.attrs = attr;
     cfg.numAttrs = na;
@@ -1405,9 +1441,10 @@ cudaError_t launch_halo_head(const UmmaParams& p, cudaStream_t s) {
 
 // How many row tiles of fused-head clusters fit at once (0 if the kernel cannot launch).
 int umma_head_max_clusters(int ntiles) {
-    using C_ = umma::CfgHalo<64, 3, 3, 6, false>;
-    auto k = umma::umma_halo_kernel<FWD_, 64, 3, 3, 6, false, true>;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM) != cudaSuccess) {
+    using C_ = umma::CfgHalo<64, 3, 2, 6, false>;
+    constexpr uint32_t SMEM = C_::SMEM + umma::HEAD_ZRECV_BYTES;
+    auto k = umma::umma_halo_kernel<FWD_, 64, 3, 2, 6, false, true>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM) != cudaSuccess) {
         cudaGetLastError();
         return 0;
     }
@@ -1419,7 +1456,7 @@ int umma_head_max_clusters(int ntiles) {
     attr[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(ntiles * 16, 1, 1);
     cfg.blockDim = dim3(umma::NTHREADS);
-    cfg.dynamicSmemBytes = C_::SMEM;
+    cfg.dynamicSmemBytes = SMEM;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int n = 0;
@@ -1699,7 +1736,7 @@ static cudaError_t dispatch(const UmmaParams& p, int npass, cudaStream_t s) {
     } else {
         if (p.kclust > 0 && npass == 3) return launch_splitk<MODE, 3, 2, 2>(p, s);  // plan: fp32 only
         if constexpr (MODE == FWD_)
-            if (p.fused_head) return launch_halo_head<64, 3, 3, 6>(p, s);  // plan: fp32, BN = 64
+            if (p.fused_head) return launch_halo_head<64, 3, 2, 6>(p, s);  // plan: fp32, BN = 64
         if (c.pair && c.bn == 64) return launch_halo<MODE, 64, 3, 3, 6, true>(p, s);
         if (c.pair)
             return npass == 3 ? launch_halo<MODE, 128, 3, 3, 6, true>(p, s) : launch_halo<MODE, 256, 1, 4, 8, true>(p, s);

@@ -19,7 +19,8 @@ PHASES = {"split": ["entry", "pdl_wait", "prod_firstA", "mma_fullA", "mma_fullB"
                     "cluster1", "packed", "received", "done"],
           "halo": ["entry", "pdl_wait", "mma_fullA0", "tile0_mma_done", "last_mma_done", "-", "epi_done"],
           # conv2 FWD with the fused head (stamps 8..13; conv2 dgrad overwrites 0..6)
-          "head": ["-"] * 8 + ["head_start", "cluster1", "dz_done", "dA2_done", "colsum_done", "cluster2"]}
+          "head": ["-"] * 8 + ["head_start", "cluster1", "dz_done", "dA2_done", "colsum_done",
+                               "c0_tmem", "c0_math", "c0_stored"]}
 
 
 def main():
