@@ -36,8 +36,9 @@ int tem::launch_priority_attr(cudaLaunchAttribute* a, bool side) {
         }
     }
     if (!on || lo == hi) return 0;
+    static const bool side_high = getenv("TEM_PRIO_MAIN") == nullptr;
     a->id = cudaLaunchAttributePriority;
-    a->val.priority = side ? lo : hi;
+    a->val.priority = (side == side_high) ? hi : lo;
     return 1;
 }
 
@@ -732,6 +733,8 @@ void* tem_debug_buffer(tem_ctx* c, int32_t l, const char* name, int64_t* nbytes)
     }
     if (strcmp(name, "tstamp_on") == 0 || strcmp(name, "tstamp") == 0)
         return umma_tstamp_buffer(nbytes, strcmp(name, "tstamp_on") == 0 ? 1 : 0);
+    if (strncmp(name, "tstamp_slot:", 12) == 0)  // stamps of one launch: "tstamp_slot:<Slot>"
+        return umma_tstamp_buffer(nbytes, 100 + atoi(name + 12));
     const Geom& g = c->g;
     const RankBufs& b = c->rb[l];
     const int64_t esz = g.op_bf16 ? 2 : 4;

@@ -381,7 +381,11 @@ TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, ui
 __device__ unsigned long long g_tstamp[1024 * 16];
 __device__ int g_tstamp_on;
 TEM_DEV void tstamp(int k) {
-    if (g_tstamp_on) g_tstamp[blockIdx.x * 16 + k] = globaltimer();
+    if (g_tstamp_on == 1) g_tstamp[blockIdx.x * 16 + k] = globaltimer();
+}
+// only while g_tstamp_on == 100 + slot (one launch of the step)
+TEM_DEV void tstamp_s(int slot, int k) {
+    if (g_tstamp_on == 100 + slot) g_tstamp[blockIdx.x * 16 + k] = globaltimer();
 }
 
 // ------------------------------------------------------------------ FWD / DGRAD (halo reuse)
@@ -426,7 +430,10 @@ constexpr uint32_t HEAD_ZRECV_BYTES = 8 * BM * 4 * 4;  // [ntiles <= 8][BM][4] p
 
 // Epilogue warps, before the accumulator wait: alpha+/- of the (<= 3) videos the row tile
 // touches (one warp per (video, channel), strict > 0.5 -- R5) and this thread's row labels.
-TEM_DEV void head_labels(const UmmaParams& P, float* hap, int m_tile, int warp, int lane, float (&glab)[3]) {
+TEM_DEV void head_labels(const UmmaParams& P, float* hap, int m_tile, int warp, int lane, float (&glab)[3],
+                         float (&b3)[3]) {
+#pragma unroll
+    for (int o = 0; o < 3; ++o) b3[o] = P.b3[o];
     const int Tp = P.Tp, Tn = P.Tn, m0 = m_tile * BM;
     const int last = min(m0 + BM, P.R) - 1;
     const int v0 = m0 / Tp, nv = last / Tp - v0 + 1;
@@ -454,7 +461,8 @@ TEM_DEV void head_labels(const UmmaParams& P, float* hap, int m_tile, int warp, 
 
 template <int BN, int ACC>
 TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const float* zrecv, const float* hap,
-                       uint32_t tbase, int m_tile, int n_tile, int warp, int lane, const float (&glab)[3]) {
+                       uint32_t tbase, int m_tile, int n_tile, int warp, int lane, const float (&glab)[3],
+                       const float (&b3)[3]) {
     constexpr int RLD = 4 * BN + 4;  // column-partial row: {dz0 h2, dz1 h2, dz2 h2, stored dA2} per column
     float* red = reinterpret_cast<float*>(smem);
     float* lred = reinterpret_cast<float*>(smem + HEAD_LRED_OFF);  // [BM][6] (rank 0)
@@ -486,7 +494,7 @@ TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const f
 #pragma unroll
             for (int k = 1; k < 8; ++k)
                 if (k < S) sz += pz[k][o];
-            z[o] = sz + P.b3[o];
+            z[o] = sz + b3[o];
         }
         if (!halo) {  // rows a3/a4 exactly as head_rows_kernel's row_loss
             const int v = p / Tp, t = p - v * Tp - 1, k = v - m0 / Tp;
@@ -643,7 +651,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
     const int total = mt_u * P.ntiles;
     if (threadIdx.x == 0) tstamp(0);
     trace_begin(P.slot);
-    float glab[3] = {0.f, 0.f, 0.f};  // HEAD: this epilogue thread's row labels
+    float glab[3] = {0.f, 0.f, 0.f}, gb3[3] = {0.f, 0.f, 0.f};  // HEAD: row labels, b3 (prefetched)
     const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, fullA, 2 * (SA + SB), tfull, tempty, tslot, warp, lane);
     if (threadIdx.x == 0) tstamp(1);
 
@@ -747,13 +755,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
         }
         __syncwarp();
     } else {
-        if (HEAD) head_labels(P, hap, unit / P.ntiles, warp, lane, glab);
+        if (HEAD) head_labels(P, hap, unit / P.ntiles, warp, lane, glab, gb3);
         epilogue_loop<MODE, BN, PAIR, C_::ACC>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane,
                                                HEAD ? zrecv : nullptr);
         if (threadIdx.x == 64) tstamp(6);
     }
     if constexpr (HEAD)
-        head_tail<BN, C_::ACC>(P, smem, epi, zrecv, hap, tbase, unit / P.ntiles, unit % P.ntiles, warp, lane, glab);
+        head_tail<BN, C_::ACC>(P, smem, epi, zrecv, hap, tbase, unit / P.ntiles, unit % P.ntiles, warp, lane, glab,
+                               gb3);
     gemm_epilogue_done<C_::TMEM_COLS, PAIR>(tbase, warp);
     trace_end(P.slot);
 }
@@ -1108,7 +1117,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
     const int mt_u = PAIR ? (P.mtiles + 1) / 2 : P.mtiles;
     const int total = mt_u * P.ntiles * P.nsplit;
     trace_begin(P.slot);
+    if (threadIdx.x == 0) tstamp_s(P.slot, 0);
     const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, full, 2 * STAGES, tfull, tempty, tslot, warp, lane);
+    if (threadIdx.x == 0) tstamp_s(P.slot, 1);
 
     auto coords = [&](int ct, int& m_tile, int& n_tile, int& split) {
         n_tile = ct % P.ntiles;
@@ -1178,6 +1189,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
                     const int s = it % STAGES;
                     mbar_wait(&full[s], (it / STAGES) & 1);
+                    if (it == 0) tstamp_s(P.slot, 2);
                     tc_fence_after();
                     const uint32_t st = smem_u32(smem + s * C_::STAGE_BYTES);
 #pragma unroll
@@ -1195,11 +1207,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
                     commit_to<PAIR>(&empty[s]);
                 }
                 commit_to<PAIR>(&tfull[acc]);
+                tstamp_s(P.slot, 3);
             }
         }
         __syncwarp();
     } else {
         epilogue_loop<WGRAD_, BN, PAIR, 1>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane);
+        if (threadIdx.x == 64) tstamp_s(P.slot, 6);
     }
     gemm_epilogue_done<C_::TMEM_COLS, PAIR>(tbase, warp);
     trace_end(P.slot);
@@ -1825,7 +1839,7 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
 
 void trace_set_umma(unsigned long long* p) { cudaMemcpyToSymbol(g_trace, &p, sizeof(p)); }
 
-void* umma_tstamp_buffer(int64_t* nbytes, int on) {
+void* umma_tstamp_buffer(int64_t* nbytes, int on) {  // on: 0 off, 1 all, 100 + slot one launch
     void* p = nullptr;
     if (cudaGetSymbolAddress(&p, umma::g_tstamp) != cudaSuccess) return nullptr;
     cudaMemcpyToSymbol(umma::g_tstamp_on, &on, sizeof(int));

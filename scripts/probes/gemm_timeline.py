@@ -20,13 +20,16 @@ PHASES = {"split": ["entry", "pdl_wait", "prod_firstA", "mma_fullA", "mma_fullB"
           "halo": ["entry", "pdl_wait", "mma_fullA0", "tile0_mma_done", "last_mma_done", "-", "epi_done"],
           # conv2 FWD with the fused head (stamps 8..13; conv2 dgrad overwrites 0..6)
           "head": ["-"] * 8 + ["head_start", "cluster1", "dz_done", "dA2_done", "colsum_done",
-                               "c0_tmem", "c0_math", "c0_stored"]}
+                               "c0_tmem", "c0_math", "c0_stored"],
+          "wgrad1": ["entry", "prologue", "mma_full0", "mma_done", "-", "-", "epi_done"],
+          "wgrad2": ["entry", "prologue", "mma_full0", "mma_done", "-", "-", "epi_done"]}
+SLOTS = {"wgrad2": 6, "wgrad1": 8}  # Slot enum (kernels.h)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c2")
-    ap.add_argument("--kernel", default="halo", choices=["halo", "split", "head"])
+    ap.add_argument("--kernel", default="halo", choices=["halo", "split", "head", "wgrad1", "wgrad2"])
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -42,7 +45,8 @@ def main():
     torch.cuda.synchronize()
     lib = tem.lib()
     nb = ctypes.c_int64(0)
-    lib.tem_debug_buffer(tem._P(s.ctx), 0, b"tstamp_on", ctypes.byref(nb))
+    on = b"tstamp_on" if args.kernel not in SLOTS else f"tstamp_slot:{SLOTS[args.kernel]}".encode()
+    lib.tem_debug_buffer(tem._P(s.ctx), 0, on, ctypes.byref(nb))
     s.step(x, lab)
     torch.cuda.synchronize()
     ptr = lib.tem_debug_buffer(tem._P(s.ctx), 0, b"tstamp", ctypes.byref(nb))
