@@ -1,0 +1,95 @@
+"""GPU parity of the alternative kernel paths the default configuration does not take.
+
+The plan picks kernels by shape: the fp32 single-wave path fuses the head into
+conv2 FWD, larger fp32 batches use the persistent halo kernel with several tiles per CTA,
+bf16 uses 2-CTA pairs. These tests force the other paths through the plan's switches
+(read when a session is created) and hold each to the same oracle contract.
+"""
+import numpy as np
+import pytest
+import torch
+
+from test_gpu_parity import (TOL, check_tensors, make_inputs, oracle_with_gpu_decisions, session,  # noqa: F401
+                             tem, to_dev_x)
+
+pytestmark = pytest.mark.gpu
+
+
+def _compute(tem, B, prec, batch_idx=0, lam=(2.0, 1.0, 1.0)):
+    s, p = session(tem, 1, B, prec, lr=0.01, lam=lam)
+    x, lab = make_inputs(1, B, prec, batch_idx=batch_idx)
+    loss = s.compute(to_dev_x(x, prec), torch.from_numpy(lab).cuda())
+    assert s.sync()[0] == 0
+    out = {"grad": s.local_grad(0).cpu().numpy()[:s.K].copy(), "z": s.logits(0).cpu().numpy().copy(),
+           "loss": loss[0].cpu().numpy().copy(), "path": s.kernel_path()}
+    return s, p, x, lab, out
+
+
+def _check(orc, s, p, x, lab, out, prec, lam=(2.0, 1.0, 1.0)):
+    ref = oracle_with_gpu_decisions(orc, s, 0, x[0], p, lab[0], lam, prec)
+    check_tensors(orc, out["grad"], out["z"], out["loss"], ref, TOL[prec])
+
+
+def test_unfused_head_fp32(tem, orc, monkeypatch):
+    """fp32 B = 4 with the separate head kernel (TEM_NO_FUSED_HEAD) vs the oracle."""
+    monkeypatch.setenv("TEM_NO_FUSED_HEAD", "1")
+    s, p, x, lab, out = _compute(tem, 4, 0)
+    _check(orc, s, p, x, lab, out, 0)
+    s.close()
+
+
+def test_fused_and_unfused_head_agree(tem, monkeypatch):
+    """Same inputs through the fused head (default at B = 16 fp32) and the head kernel: every
+    output agrees to fp32 rounding-order differences (1e-5 of the tensor's max)."""
+    s1, _, _, _, fused = _compute(tem, 16, 0, batch_idx=3)
+    s1.close()
+    monkeypatch.setenv("TEM_NO_FUSED_HEAD", "1")
+    s2, _, _, _, plain = _compute(tem, 16, 0, batch_idx=3)
+    s2.close()
+    for k in ("grad", "z", "loss"):
+        a, b = fused[k].astype(np.float64), plain[k].astype(np.float64)
+        assert np.abs(a - b).max() <= 1e-5 * max(np.abs(b).max(), 1e-30), k
+
+
+def test_fp32_multi_tile_per_cta(tem, orc):
+    """fp32 B = 24: 20 row tiles x 8 column tiles > 148 CTAs, so the persistent halo kernel runs
+    several tiles per CTA (double-buffered dual accumulators) and the head is not fused."""
+    s, p, x, lab, out = _compute(tem, 24, 0, batch_idx=1)
+    _check(orc, s, p, x, lab, out, 0)
+    s.close()
+
+
+def test_splitk_cluster_kernel(tem, orc, monkeypatch):
+    """The experimental split-K cluster FWD/DGRAD kernel (TEM_SPLITK=1) at B = 16 fp32."""
+    monkeypatch.setenv("TEM_SPLITK", "1")
+    s, p, x, lab, out = _compute(tem, 16, 0, batch_idx=2)
+    _check(orc, s, p, x, lab, out, 0)
+    s.close()
+
+
+@pytest.mark.parametrize("variant,prec", [("1", 1), ("2", 0)])
+def test_gemm_variants(tem, orc, monkeypatch, variant, prec):
+    """TEM_GEMM_VARIANT=1 (1-CTA bf16 GEMMs) and =2 (2-CTA pairs for the fp32 GEMMs), B = 4."""
+    monkeypatch.setenv("TEM_GEMM_VARIANT", variant)
+    s, p, x, lab, out = _compute(tem, 4, prec, batch_idx=4)
+    _check(orc, s, p, x, lab, out, prec)
+    s.close()
+
+
+def test_graph_and_eager_steps_identical(tem, monkeypatch):
+    """tem_step replayed from a CUDA graph and launched eagerly (TEM_NO_GRAPH) run the same
+    kernels: parameters after three steps are bitwise identical."""
+    def run():
+        s, _ = session(tem, 1, 8, 0, lr=0.05)
+        x, lab = make_inputs(1, 8, 0, batch_idx=6)
+        xd, ld = to_dev_x(x, 0), torch.from_numpy(lab).cuda()
+        for _ in range(3):
+            s.step(xd, ld)
+        assert s.sync()[0] == 0
+        w = s.params(0).cpu().numpy().copy()
+        s.close()
+        return w
+    w_graph = run()
+    monkeypatch.setenv("TEM_NO_GRAPH", "1")
+    w_eager = run()
+    assert np.array_equal(w_graph, w_eager)
