@@ -361,7 +361,9 @@ def main():
                 pass
         roof["share_of_step"] = conv[dom] / max(sum(slot_ms.values()), 1e-9)
         roof["timing"] = (f"kernel duration from an instrumented pass of {nrec} steps (CUDA events around "
-                          f"every kernel, no graph); value from {args.steps} graph-replayed steps")
+                          f"every kernel on its stream, no graph, side branch serialised so each slot is one "
+                          f"kernel alone; ~3-4 us event overhead per slot); value from {args.steps} "
+                          f"graph-replayed steps")
         roof["slot_ms_per_step"] = {k: v / max(nrec, 1) for k, v in slot_ms.items()}
 
     out = {

@@ -132,6 +132,7 @@ struct UmmaParams {
 struct UmmaPlan {
     UmmaParams conv1, conv2, dgrad, wgrad1, wgrad2;
     int npass, bn_fwd, S, ksplit_rows;
+    int S1, S2;  // split-K factors of conv1 / conv2 wgrad (<= S, the workspace's)
     cudaStream_t aux;         // second stream: conv2 wgrad runs beside conv2 dgrad / conv1 wgrad
     cudaEvent_t fork, join;
 };
@@ -211,8 +212,8 @@ cudaError_t launch_ring(const RingParams& p, cudaStream_t s);
 // (W1, b1), sum_s part2[s][e - off2] (W2), or grad[e] (the head-written entries); the same
 // ascending-s order as reduce_wgrad_kernel, so the result is bit-identical to the unfused path.
 cudaError_t launch_sgd_fused(float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo, int64_t n,
-                             float lr, const float* p1, int64_t stride1, int64_t n1, const float* p2,
-                             int64_t stride2, int64_t off2, int64_t n2, int S, cudaStream_t s);
+                             float lr, const float* p1, int64_t stride1, int64_t n1, int S1, const float* p2,
+                             int64_t stride2, int64_t off2, int64_t n2, int S2, cudaStream_t s);
 cudaError_t launch_sgd_single(const float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo,
                               int64_t n, int op, float lr, cudaStream_t s);
 struct PsParams {

@@ -270,8 +270,8 @@ __global__ void sgd_single_kernel(const float* __restrict__ g, float* __restrict
 
 __global__ void sgd_fused_kernel(float* __restrict__ g, float* __restrict__ w, __nv_bfloat16* __restrict__ shadow,
                                  __nv_bfloat16* __restrict__ shadow_lo, int64_t n, float lr,
-                                 const float* __restrict__ p1, int64_t stride1, int64_t n1,
-                                 const float* __restrict__ p2, int64_t stride2, int64_t off2, int64_t n2, int S) {
+                                 const float* __restrict__ p1, int64_t stride1, int64_t n1, int S1,
+                                 const float* __restrict__ p2, int64_t stride2, int64_t off2, int64_t n2, int S2) {
     trace_begin(SLOT_EXCHANGE);
     pdl_trigger();
     pdl_wait();
@@ -281,12 +281,15 @@ __global__ void sgd_fused_kernel(float* __restrict__ g, float* __restrict__ w, _
         const int64_t e = 4 * v;
         const float* src = nullptr;
         int64_t stride = 0;
+        int S = 1;
         if (e < n1) {
             src = p1 + e;
             stride = stride1;
+            S = S1;
         } else if (e >= off2 && e < off2 + n2) {
             src = p2 + (e - off2);
             stride = stride2;
+            S = S2;
         }
         float4 a;
         if (src) {  // split-K partials, ascending s (as reduce_wgrad_kernel)
@@ -410,10 +413,10 @@ cudaError_t launch_sgd_single(const float* g, float* w, __nv_bfloat16* shadow, _
 void trace_set_ring(unsigned long long* p) { cudaMemcpyToSymbol(g_trace, &p, sizeof(p)); }
 
 cudaError_t launch_sgd_fused(float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo, int64_t n,
-                             float lr, const float* p1, int64_t stride1, int64_t n1, const float* p2,
-                             int64_t stride2, int64_t off2, int64_t n2, int S, cudaStream_t s) {
-    return launch_pdl(sgd_fused_kernel, dim3(296), dim3(512), 0, s, false, g, w, shadow, shadow_lo, n, lr, p1, stride1, n1, p2,
-                      stride2, off2, n2, S);
+                             float lr, const float* p1, int64_t stride1, int64_t n1, int S1, const float* p2,
+                             int64_t stride2, int64_t off2, int64_t n2, int S2, cudaStream_t s) {
+    return launch_pdl(sgd_fused_kernel, dim3(296), dim3(512), 0, s, false, g, w, shadow, shadow_lo, n, lr, p1, stride1,
+                      n1, S1, p2, stride2, off2, n2, S2);
 }
 
 cudaError_t launch_ps(const PsParams& p, cudaStream_t s) {

@@ -468,8 +468,8 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
         const UmmaPlan& P = *c->plan[0];
         c->reduce_deferred = false;
         if (launch_sgd_fused(b.grad, (float*)b.params, b.shadow, b.shadow_lo, g.Kpad, c->cfg.lr, b.wpart,
-                             P.wgrad1.part_stride, g.off_W2, b.wpart2, P.wgrad2.part_stride, g.off_W2,
-                             (int64_t)3 * g.C * g.C, P.S, s) != cudaSuccess)
+                             P.wgrad1.part_stride, g.off_W2, P.S1, b.wpart2, P.wgrad2.part_stride, g.off_W2,
+                             (int64_t)3 * g.C * g.C, P.S2, s) != cudaSuccess)
             return TEM_ERR_CUDA;
         ++*nl;
         rec.end(SLOT_EXCHANGE);

@@ -1621,6 +1621,17 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     const int kb_per = (nkb + P.S - 1) / P.S;
     P.ksplit_rows = kb_per * umma::BK;
     P.S = (R + P.ksplit_rows - 1) / P.ksplit_rows;
+    // per-WGRAD split factors (<= P.S, which sizes the partial buffers); TEM_S1 / TEM_S2 override
+    auto split_rows = [&](const char* env, int& S, int& rows) {
+        S = P.S;
+        if (const char* e = getenv(env)) S = std::max(1, std::min(P.S, atoi(e)));
+        const int per = (nkb + S - 1) / S;
+        rows = per * umma::BK;
+        S = (R + rows - 1) / rows;
+    };
+    int rows1 = 0, rows2 = 0;
+    split_rows("TEM_S1", P.S1, rows1);
+    split_rows("TEM_S2", P.S2, rows2);
     auto common = [&](UmmaParams& q) {
         q.R = R;
         q.Tp = Tp;
@@ -1704,12 +1715,14 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     P.wgrad2.NW = 3 * g.C;
     P.wgrad2.mtiles = g.C / umma::BM;
     P.wgrad2.ntiles = (3 * P.wgrad2.cpj + wc - 1) / wc;
-    P.wgrad2.nsplit = P.S;
+    P.wgrad2.nsplit = P.S2;
+    P.wgrad2.ksplit_rows = rows2;
     P.wgrad2.part = b.wpart2;
     P.wgrad2.part_stride = (int64_t)g.C * 3 * g.C + g.C;
     common(P.wgrad1);
     P.wgrad1.slot = SLOT_WGRAD1;
-    P.wgrad1.nsplit = P.S;
+    P.wgrad1.nsplit = P.S1;
+    P.wgrad1.ksplit_rows = rows1;
     P.wgrad1.Nout = g.C;
     P.wgrad1.Cin_w = g.Cin;
     P.wgrad1.cpj = (g.Cin + 63) / 64;
@@ -1726,8 +1739,8 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     ok &= map_store2d(&P.conv2.out[0], b.h2, true, g.C, R);
     ok &= map_store2d(&P.dgrad.out[0], b.dA1, false, g.C, R);
     if (b.dA1_lo) ok &= map_store2d(&P.dgrad.out[1], b.dA1_lo, false, g.C, R);
-    ok &= map_store_part(&P.wgrad2.out[0], b.wpart2, 3 * (uint64_t)g.C, g.C, P.S, P.wgrad2.part_stride);
-    ok &= map_store_part(&P.wgrad1.out[0], b.wpart, 3 * (uint64_t)g.Cin, g.C, P.S, P.wgrad1.part_stride);
+    ok &= map_store_part(&P.wgrad2.out[0], b.wpart2, 3 * (uint64_t)g.C, g.C, P.S2, P.wgrad2.part_stride);
+    ok &= map_store_part(&P.wgrad1.out[0], b.wpart, 3 * (uint64_t)g.Cin, g.C, P.S1, P.wgrad1.part_stride);
     return ok;
 }
 
@@ -1789,7 +1802,10 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     // Fork: the head reduction and conv2 wgrad (+ its reduction) run on the aux stream
     // alongside conv2 dgrad -> conv1 wgrad on s; all only read dA2 / h1 / xp / head
     // partials (captured as parallel graph branches).
-    static const bool no_fork = getenv("TEM_NO_FORK") != nullptr;  // experiment: side branch serialised
+    // The side branch is serialised onto s for the instrumented (timing) pass -- each slot is
+    // then one kernel's own duration on its stream -- and with TEM_NO_FORK (experiments).
+    static const bool no_fork_env = getenv("TEM_NO_FORK") != nullptr;
+    const bool no_fork = no_fork_env || rec.ev != nullptr;
     cudaStream_t aux = no_fork ? s : P.aux;
     const EvRec rec2{rec.ev, aux};
     if (!no_fork &&
@@ -1806,7 +1822,7 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     if (!defer_reduce) {
     rec2.begin(SLOT_RED2);
     e = launch_pdl(umma::reduce_wgrad_kernel, dim3(296), dim3(256), 0, aux, true, (const float*)b.wpart2,
-                   P.wgrad2.part_stride, P.S, (int64_t)g.C * 3 * g.C, (const float*)nullptr, 0, g.C,
+                   P.wgrad2.part_stride, P.S2, (int64_t)g.C * 3 * g.C, (const float*)nullptr, 0, g.C,
                    b.grad + g.off_W2, (int)SLOT_RED2);
     rec2.end(SLOT_RED2);
     if (e != cudaSuccess) return e;
@@ -1826,7 +1842,7 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     if (!defer_reduce) {
     rec.begin(SLOT_RED1);
     e = launch_pdl(umma::reduce_wgrad_kernel, dim3(296), dim3(256), 0, s, false, (const float*)b.wpart, P.wgrad1.part_stride,
-                   P.S, (int64_t)g.C * 3 * g.Cin + g.C, (const float*)nullptr, 0, g.C, b.grad + g.off_W1,
+                   P.S1, (int64_t)g.C * 3 * g.Cin + g.C, (const float*)nullptr, 0, g.C, b.grad + g.off_W1,
                    (int)SLOT_RED1);
     rec.end(SLOT_RED1);
     if (e != cudaSuccess) return e;
