@@ -174,7 +174,8 @@ cudaError_t simt_compute(const Geom& g, const RankBufs& b, const float* labels,
 // (launch_sgd_fused) -- used by tem_step only, so tem_compute still leaves the full gradient.
 cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, const float* labels,
                          const float lam[3], float* loss_out, Status* status, int* nlaunch,
-                         const EvRec& rec, cudaStream_t s, bool defer_reduce = false);
+                         const EvRec& rec, cudaStream_t s, bool defer_reduce = false,
+                         float* loss_host = nullptr);
 // head (conv3 + sigmoid + loss + dz + dA2) and its deterministic finalisation (rows a3-a5);
 // writes dA2 as b.dA2 (+ b.dA2_lo when present) in the operand type of the path.
 cudaError_t launch_head(const Geom& g, const RankBufs& b, const float* labels, const float lam[3],

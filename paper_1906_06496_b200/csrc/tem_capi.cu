@@ -203,10 +203,13 @@ struct tem_ctx {
     int t_max, t_idx;
     // CUDA-graph replay of whole steps (one graph per input pointer set), run on a private
     // non-blocking stream ordered with the caller's stream by events
+    float* loss_host_pending;  // tem_step_host: host loss buffer the compute reads back into
+    bool loss_host_done;
     struct GraphEntry {
         const void* x;
         const void* lab;
         void* loss;
+        void* loss_host;
         cudaGraphExec_t exec;
         int launches;
     };
@@ -225,7 +228,9 @@ template <typename F>
 tem_status graph_step(tem_ctx* c, const void* x, const void* lab, void* loss, cudaStream_t s, F&& fn) {
     tem_ctx::GraphEntry* e = nullptr;
     for (int i = 0; i < c->ngraphs; ++i)
-        if (c->graphs[i].x == x && c->graphs[i].lab == lab && c->graphs[i].loss == loss) e = &c->graphs[i];
+        if (c->graphs[i].x == x && c->graphs[i].lab == lab && c->graphs[i].loss == loss &&
+            c->graphs[i].loss_host == c->loss_host_pending)
+            e = &c->graphs[i];
     if (!e) {
         if (c->ngraphs == tem_ctx::kMaxGraphs) {  // evict the oldest
             cudaGraphExecDestroy(c->graphs[0].exec);
@@ -252,12 +257,14 @@ tem_status graph_step(tem_ctx* c, const void* x, const void* lab, void* loss, cu
         e->x = x;
         e->lab = lab;
         e->loss = loss;
+        e->loss_host = c->loss_host_pending;
         e->exec = exec;
         e->launches = nl;
     }
     // Captured on the private stream, replayed directly on the caller's stream (stream order
     // gives the dependencies; no cross-stream event handoff per step).
     if (cudaGraphLaunch(e->exec, s) != cudaSuccess) return TEM_ERR_CUDA;
+    if (e->loss_host && c->g.path == PATH_UMMA && c->g.B > 0) c->loss_host_done = true;
     c->launches_step = e->launches;
     return TEM_OK;
 }
@@ -437,8 +444,11 @@ static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, f
         ++*nl;
         const bool defer = fuse_reduce && c->N == 1 && g.path == PATH_UMMA && g.B > 0;
         c->reduce_deferred = defer;
-        if (g.path == PATH_UMMA && g.B > 0)
-            e = umma_compute(g, c->rb[l], *c->plan[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s, defer);
+        float* lh = (c->nlocal == 1) ? c->loss_host_pending : nullptr;
+        if (g.path == PATH_UMMA && g.B > 0) {
+            e = umma_compute(g, c->rb[l], *c->plan[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s, defer, lh);
+            if (lh) c->loss_host_done = true;
+        }
         else
             e = simt_compute(g, c->rb[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s);
         if (e != cudaSuccess) return TEM_ERR_CUDA;
@@ -589,12 +599,18 @@ tem_status tem_step_host(tem_ctx* c, const void* x_host, const float* labels_hos
     float* ld = (float*)(base + c->wl.labstage);
     float* lossd = (float*)(base + c->wl.lossstage);
     const size_t xb = (size_t)g.B * g.T * g.Cin * esz, lb = (size_t)g.B * 3 * g.T * 4;
+    // one copy each on `s` (measured: splitting x over parallel copy streams is slower)
     if (xb && cudaMemcpyAsync(xd, x_host, xb, cudaMemcpyHostToDevice, s) != cudaSuccess) return TEM_ERR_CUDA;
     if (lb && cudaMemcpyAsync(ld, labels_host, lb, cudaMemcpyHostToDevice, s) != cudaSuccess)
         return TEM_ERR_CUDA;
+    c->loss_host_pending = loss_host;  // the tcgen05 path reads the loss back inside the step
+    c->loss_host_done = false;
     st = tem_step(c, xd, ld, lossd, stream);
+    const bool done = c->loss_host_done;
+    c->loss_host_pending = nullptr;
+    c->loss_host_done = false;
     if (st != TEM_OK) return st;
-    if (cudaMemcpyAsync(loss_host, lossd, 16, cudaMemcpyDeviceToHost, s) != cudaSuccess) return TEM_ERR_CUDA;
+    if (!done && cudaMemcpyAsync(loss_host, lossd, 16, cudaMemcpyDeviceToHost, s) != cudaSuccess) return TEM_ERR_CUDA;
     return TEM_OK;
 }
 

@@ -1773,7 +1773,7 @@ static cudaError_t dispatch(const UmmaParams& p, int npass, cudaStream_t s) {
 
 cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, const float* labels,
                          const float lam[3], float* loss_out, Status* status, int* nl, const EvRec& rec,
-                         cudaStream_t s, bool defer_reduce) {
+                         cudaStream_t s, bool defer_reduce, float* loss_host) {
     int n = 0;
     cudaError_t e;
     rec.begin(SLOT_CONV1);
@@ -1814,6 +1814,10 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     e = P.conv2.fused_head ? launch_head_reduce_rows(g, b, mtiles_of(P), lam, loss_out, status, rec2, aux, &n)
                            : launch_head_reduce(g, b, lam, loss_out, status, rec2, aux, &n);
     if (e != cudaSuccess) return e;
+    // tem_step_host: the loss read-back overlaps the rest of the step (the join orders it
+    // before the exchange, so it is complete when the step is)
+    if (loss_host && cudaMemcpyAsync(loss_host, loss_out, 4 * sizeof(float), cudaMemcpyDeviceToHost, aux) != cudaSuccess)
+        return cudaErrorUnknown;
     rec2.begin(SLOT_WGRAD2);
     e = dispatch<WGRAD_>(P.wgrad2, P.npass, aux);
     rec2.end(SLOT_WGRAD2);

@@ -93,3 +93,29 @@ def test_graph_and_eager_steps_identical(tem, monkeypatch):
     monkeypatch.setenv("TEM_NO_GRAPH", "1")
     w_eager = run()
     assert np.array_equal(w_graph, w_eager)
+
+
+def test_step_host_matches_device_step(tem):
+    """tem_step_host (pinned host x / labels / loss, copies inside the step; the loss is read
+    back on the side stream) == tem_step on device buffers: same loss, bitwise equal params."""
+    B = 8
+    x, lab = make_inputs(1, B, 0, batch_idx=7)
+    s1, _ = session(tem, 1, B, 0, lr=0.05)
+    xd, ld = to_dev_x(x, 0), torch.from_numpy(lab).cuda()
+    losses_dev = []
+    for _ in range(3):
+        losses_dev.append(s1.step(xd, ld).cpu().numpy().copy())
+    assert s1.sync()[0] == 0
+    w1 = s1.params(0).cpu().numpy().copy()
+    s1.close()
+    s2, _ = session(tem, 1, B, 0, lr=0.05)
+    xh = torch.from_numpy(x[0].copy()).pin_memory()
+    lh = torch.from_numpy(lab[0].copy()).pin_memory()
+    loss_h = torch.zeros(4, dtype=torch.float32).pin_memory()
+    for i in range(3):
+        s2.step_host(xh, lh, loss_h)
+        torch.cuda.synchronize()
+        assert np.array_equal(loss_h.numpy(), losses_dev[i].reshape(-1)[:4]), i
+    assert s2.sync()[0] == 0
+    assert np.array_equal(s2.params(0).cpu().numpy(), w1)
+    s2.close()
