@@ -70,6 +70,11 @@ def lib():
             L.orc_tem_fwd_bwd_ex.restype = i32
             L.orc_tem_fwd_bwd_ex.argtypes = [i32, i32, i32, i32, i32, i32, P, P, P, P, P, P, P,
                                              P, i64, ctypes.c_double, P, i64, P, P]
+            L.orc_pem_num_params.restype = i64
+            L.orc_pem_num_params.argtypes = [i32, i32]
+            L.orc_pem_fwd_bwd.restype = i32
+            L.orc_pem_fwd_bwd.argtypes = [i32, i32, i32, P, P, P, P, P, P, P, i64, ctypes.c_double, P, i64,
+                                          P, P]
             _lib = L
     return _lib
 
@@ -196,6 +201,55 @@ def tem_fwd_bwd(x, params, labels, lam=(1.0, 1.0, 1.0), prec: int = 0, C: int = 
     n = int(nk[0])
     return {"loss": loss, "z": z, "grad": grad, "kinks": kinks[:min(n, kinks_cap)].copy(), "nkinks": n,
             "decisions": dec}
+
+
+# --------------------------------------------------------------------------- PEM
+def pem_num_params(F: int = 32, H: int = 512) -> int:
+    return int(lib().orc_pem_num_params(F, H))
+
+
+def pem_fwd_bwd(f, params, g, flips=(), kink_tau: float = 0.0, kinks_cap: int = 4096):
+    """BSN PEM forward + MSE-to-IoU loss + backward (configs[4], readings R19-R21), fp64.
+
+    f [M][F] BSP features, params flat [W1 (H x F), b1 (H), w2 (H), b2], g [M] IoU targets.
+    flips / kink_tau: ReLU decision overrides and ambiguity band, indices m*H + j (R7b).
+    Returns dict(loss f64, y [M], grad [K_pem], kinks, nkinks, decisions [M*H] u8)."""
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    M, F = f.shape
+    Kp = None
+    p = np.asarray(params, dtype=np.float64).ravel()
+    # H from the parameter count: K = H*F + 2H + 1
+    H = (p.size - 1) // (F + 2)
+    Kp = pem_num_params(F, H)
+    assert p.size == Kp, (p.size, Kp)
+    p = np.ascontiguousarray(p)
+    g = np.ascontiguousarray(g, dtype=np.float64).ravel()
+    assert g.size == M
+    loss = np.zeros(1)
+    y = np.zeros(M)
+    grad = np.zeros(Kp)
+    fl = np.ascontiguousarray(np.sort(np.asarray(flips, dtype=np.int64)))
+    kinks = np.zeros(max(kinks_cap, 1), dtype=np.int64)
+    nk = np.zeros(1, dtype=np.int64)
+    dec = np.zeros(max(M * H, 1), dtype=np.uint8)
+    rc = lib().orc_pem_fwd_bwd(M, F, H, _ptr(f), _ptr(p), _ptr(g), _ptr(loss), _ptr(y), _ptr(grad),
+                               _ptr(fl) if fl.size else None, int(fl.size), float(kink_tau), _ptr(kinks),
+                               int(kinks_cap), _ptr(nk), _ptr(dec))
+    if rc:
+        raise ValueError("invalid PEM arguments")
+    n = int(nk[0])
+    return {"loss": float(loss[0]), "y": y, "grad": grad, "kinks": kinks[:min(n, kinks_cap)].copy(), "nkinks": n,
+            "decisions": dec[:M * H]}
+
+
+def pem_param_slices(F: int = 32, H: int = 512):
+    """Flat PEM parameter order [W1p, b1p, w2p, b2p] (reading R21)."""
+    sizes = [("W1p", H * F), ("b1p", H), ("w2p", H), ("b2p", 1)]
+    out, off = {}, 0
+    for name, n in sizes:
+        out[name] = slice(off, off + n)
+        off += n
+    return out
 
 
 def param_slices(Cin: int = 400, C: int = 512, Co: int = 3):

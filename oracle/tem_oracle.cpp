@@ -27,6 +27,8 @@
 //   TEM loss       : closed form 2 ln 2 per channel at z == 0
 //   TEM backward   : central finite differences + torch.autograd float64
 //   DP equivalence : N ranks x B (mean) == 1 rank x N*B
+//   PEM            : torch.autograd float64 (library routine); closed form at W1 = 0;
+//                    central finite differences (tests/test_oracle_pem.py)
 // ============================================================================
 #include <algorithm>
 #include <cmath>
@@ -448,4 +450,75 @@ int orc_tem_fwd_bwd(int prec, int B, int T, int Cin, int C, int Co,
                               grad_out, nullptr, 0, 0.0, nullptr, 0, nullptr, nullptr);
 }
 
+// ============================================================================ PEM
+// BSN's proposal evaluation module, trained jointly with TEM in BASELINE configs[4] (SURVEY
+// 8(f) NEXT #1; the paper shows BSN's stages only in Fig. 1b, P:63 -- the module itself is
+// BSN's, readings R19-R21 in DESIGN.md).  Per proposal m with BSP feature f_m (F = 32) and
+// IoU target g_m:
+//   a_m = W1 f_m + b1 (H = 512),  h_m = ReLU(a_m),  z_m = w2 . h_m + b2,  y_m = sigmoid(z_m)
+//   L   = (1/M) sum_m (y_m - g_m)^2                                   (R20: plain MSE)
+// Backward (chain rule):  dz_m = (2/M)(y_m - g_m) y_m (1 - y_m);  dw2 = sum_m dz_m h_m;
+//   db2 = sum_m dz_m;  dh_m = 1[a_m > 0] dz_m w2;  dW1 = sum_m dh_m f_m^T;  db1 = sum_m dh_m.
+// Parameters (and gradient) flat [W1 (H x F, row [j][k]), b1 (H), w2 (H), b2 (1)] (R21).
+// flips / kinks / decisions: as orc_tem_fwd_bwd_ex (reading R7b), index m*H + j.
+int64_t orc_pem_num_params(int F, int H) { return (int64_t)H * F + 2 * (int64_t)H + 1; }
+
+int orc_pem_fwd_bwd(int M, int F, int H, const double* f, const double* params, const double* g,
+                    double* loss_out, double* y_out, double* grad_out, const int64_t* flips, int64_t nflips,
+                    double kink_tau, int64_t* kinks_out, int64_t kinks_cap, int64_t* nkinks,
+                    uint8_t* decisions_out) {
+    if (M < 0 || F < 1 || H < 1 || !params || !loss_out || !grad_out) return 1;
+    const double* W1 = params;
+    const double* b1 = W1 + (int64_t)H * F;
+    const double* w2 = b1 + H;
+    const double b2 = w2[H];
+    const int64_t K = orc_pem_num_params(F, H);
+    for (int64_t i = 0; i < K; ++i) grad_out[i] = 0.0;
+    double* gW1 = grad_out;
+    double* gb1 = gW1 + (int64_t)H * F;
+    double* gw2 = gb1 + H;
+    double* gb2 = gw2 + H;
+    std::vector<double> h(H);
+    std::vector<uint8_t> pos(H);
+    int64_t nk = 0;
+    double L = 0.0;
+    for (int m = 0; m < M; ++m) {
+        const double* fm = f + (int64_t)m * F;
+        for (int j = 0; j < H; ++j) {
+            double a = b1[j], mag = std::fabs(b1[j]);
+            for (int k = 0; k < F; ++k) {
+                a += W1[(int64_t)j * F + k] * fm[k];
+                mag += std::fabs(W1[(int64_t)j * F + k] * fm[k]);
+            }
+            const int64_t idx = (int64_t)m * H + j;
+            bool p = a > 0.0;
+            if (flips && nflips > 0 && std::binary_search(flips, flips + nflips, idx)) p = !p;
+            if (kink_tau > 0.0 && std::fabs(a) <= kink_tau * mag) {
+                if (kinks_out && nk < kinks_cap) kinks_out[nk] = idx;
+                ++nk;
+            }
+            if (decisions_out) decisions_out[idx] = p ? 1 : 0;
+            pos[j] = p ? 1 : 0;
+            h[j] = p ? a : 0.0;
+        }
+        double z = b2;
+        for (int j = 0; j < H; ++j) z += w2[j] * h[j];
+        const double y = 1.0 / (1.0 + std::exp(-z));
+        if (y_out) y_out[m] = y;
+        L += (y - g[m]) * (y - g[m]);
+        const double dz = (2.0 / M) * (y - g[m]) * y * (1.0 - y);
+        *gb2 += dz;
+        for (int j = 0; j < H; ++j) {
+            gw2[j] += dz * h[j];
+            const double dh = pos[j] ? dz * w2[j] : 0.0;
+            gb1[j] += dh;
+            for (int k = 0; k < F; ++k) gW1[(int64_t)j * F + k] += dh * fm[k];
+        }
+    }
+    loss_out[0] = M > 0 ? L / M : 0.0;
+    if (nkinks) *nkinks = nk;
+    return 0;
+}
+
 }  // extern "C"
+
