@@ -18,6 +18,10 @@ Recipe:
   * parameters: torch-default-style U(-1/sqrt(fan_in), +1/sqrt(fan_in)) for each
     weight and bias, fan_in = Cin*3, C*3, C for conv1/2/3, flat order
     [W1, b1, W2, b2, W3, b3], zero-padded to any requested length.
+  * PEM (BASELINE configs[4], reading R19): P = 128 proposals per video; BSP features
+    [B][P][32] ~ U(0, 1) (BSN's BSP feature samples probability sequences, values in
+    [0, 1]); IoU targets [B][P] = U(0, 1)^2 (skewed to low overlap, as dense proposal sets
+    are); PEM parameters [W1p (512 x 32), b1p, w2p, b2p] ~ U(+-1/sqrt(fan_in)), fan_in 32, 512.
 """
 from __future__ import annotations
 
@@ -25,6 +29,7 @@ import numpy as np
 
 SEED_BASE = 1906064960
 T_DEFAULT, CIN_DEFAULT, C_DEFAULT, CO_DEFAULT = 100, 400, 512, 3
+PEM_P, PEM_F, PEM_H = 128, 32, 512
 
 
 def batch_seed(rank: int, batch_idx: int) -> int:
@@ -80,6 +85,30 @@ def init_params(Cin: int = CIN_DEFAULT, C: int = C_DEFAULT, Co: int = CO_DEFAULT
         assert pad_to >= flat.size
         flat = np.concatenate([flat, np.zeros(pad_to - flat.size, np.float32)])
     return flat
+
+
+def bsp_features(B: int, P: int = PEM_P, F: int = PEM_F, *, rank: int = 0, batch_idx: int = 0) -> np.ndarray:
+    rng = np.random.default_rng(batch_seed(rank, batch_idx) + 11_000_000)
+    return rng.random((B, P, F), dtype=np.float32)
+
+
+def iou_targets(B: int, P: int = PEM_P, *, rank: int = 0, batch_idx: int = 0) -> np.ndarray:
+    rng = np.random.default_rng(batch_seed(rank, batch_idx) + 13_000_000)
+    u = rng.random((B, P), dtype=np.float32)
+    return (u * u).astype(np.float32)
+
+
+def pem_num_params(F: int = PEM_F, H: int = PEM_H) -> int:
+    return H * F + 2 * H + 1
+
+
+def init_pem_params(F: int = PEM_F, H: int = PEM_H, *, seed: int = SEED_BASE) -> np.ndarray:
+    rng = np.random.default_rng(seed + 199)
+    b1 = 1.0 / np.sqrt(F)
+    b2 = 1.0 / np.sqrt(H)
+    parts = [rng.uniform(-b1, b1, size=H * F), rng.uniform(-b1, b1, size=H),
+             rng.uniform(-b2, b2, size=H), rng.uniform(-b2, b2, size=1)]
+    return np.concatenate(parts).astype(np.float32)
 
 
 def gradients(N: int, K: int, *, seed: int = SEED_BASE, scale: float = 1e-3) -> np.ndarray:

@@ -92,6 +92,14 @@ typedef struct {
                                ranks push gradients to rank 0, which sums them in ascending
                                rank order, applies mean + SGD to its weights and pushes w'
                                back to every rank)                                           */
+    /* --- PEM: joint TEM + PEM training (BASELINE configs[4]).  BSN's
+     *     proposal evaluation module: per proposal a BSP feature f (F) -> ReLU(W1 f + b1) (H)
+     *     -> sigmoid(w2 . h + b2), MSE to the proposal's IoU (readings R19-R20).  Its
+     *     F*H + 2H + 1 parameters follow TEM's in the flat vector (R21), so tem_num_params
+     *     grows by 17,409 and one exchange carries both gradients.                           */
+    int32_t pem_proposals;  /* P proposals per video per step; 0 = TEM only                  */
+    int32_t pem_features;   /* F: 32 (required when pem_proposals > 0)                       */
+    int32_t pem_hidden;     /* H: 512 (required when pem_proposals > 0)                      */
 } tem_config;
 
 enum { TEM_EXCHANGE_RING = 0, TEM_EXCHANGE_PS = 1 };
@@ -137,6 +145,19 @@ tem_status tem_compute(tem_ctx* ctx, const void* x, const float* labels, float* 
 /* t2 of P:163 only: ring allreduce (Mean) of the local gradients fused with the owner's
  * SGD update w = fma(-lr, gbar, w) and the gather of the updated weights. */
 tem_status tem_exchange(tem_ctx* ctx, void* stream);
+/* Joint TEM + PEM step / compute (cfg->pem_proposals > 0; tem_step / tem_compute return
+ * TEM_ERR_INVALID_ARG on such a config).  x, labels as tem_step; bsp: device [B][P][F] fp32 BSP
+ * features; iou: device [B][P] fp32 IoU targets (R19).  loss_out: device, 5 * local_ranks
+ * floats: the tem_step losses (4 per local rank), then one PEM MSE per local rank.  The TEM
+ * and PEM gradients go through one exchange of the concatenated vector. */
+tem_status tem_step_pem(tem_ctx* ctx, const void* x, const float* labels, const float* bsp, const float* iou,
+                        float* loss_out, void* stream);
+tem_status tem_compute_pem(tem_ctx* ctx, const void* x, const float* labels, const float* bsp,
+                           const float* iou, float* loss_out, void* stream);
+/* PEM ReLU decisions of the last tem_*_pem call of local rank `local_rank`: out[m][j] =
+ * 1[a_mj > 0] (uint8, M = B*P rows, H columns) into the caller's device buffer (R7b). */
+tem_status tem_pem_relu_decisions(tem_ctx* ctx, int32_t local_rank, uint8_t* out, void* stream);
+
 /* tem_step with HOST buffers (pinned recommended): copies x and labels host->device into
  * the workspace, runs the step, copies loss (local_ranks*4 floats) device->host, all on
  * `stream`.  The end-to-end path a user calls. */

@@ -54,7 +54,14 @@ struct Geom {
     int split;      // hi/lo residual planes present (UMMA + TEM_FP32)
     int64_t K, Kpad;
     int64_t off_W1, off_b1, off_W2, off_b2, off_W3, off_b3;
+    // PEM (joint TEM + PEM step, BASELINE configs[4]): pem_P proposals per video, 0 = off;
+    // its parameters follow TEM's in the flat vector at off_pem (reading R21)
+    int pem_P, pem_F, pem_H;
+    int64_t off_pem;
 };
+inline int64_t pem_num_params_of(const Geom& g) {
+    return g.pem_P > 0 ? (int64_t)g.pem_H * g.pem_F + 2 * (int64_t)g.pem_H + 1 : 0;
+}
 
 // Kernel paths.  UMMA (default): tcgen05/TMA bf16 tensor-core GEMMs, one plane of bf16
 // operands (TEM_BF16) or hi/lo planes (TEM_FP32, 3-pass split).  SIMT: CUDA-core
@@ -65,6 +72,8 @@ enum Path { PATH_SIMT = 0, PATH_UMMA = 1 };
 // Operand tensors ("hi" = the plane used by SIMT and by the 1-plane UMMA path; "_lo" =
 // residual plane x - bf16(x), present only on the UMMA fp32 path).
 struct RankBufs {
+    float* pempart;       // PEM per-CTA partial rows [pem_ctas][K_pem + 1]
+    uint8_t* pemdec;      // PEM ReLU decisions [B*P][H] of the last step (recorded on request)
     const float* params;  // fp32 master weights [Kpad] (symmetric heap)
     const void* wop;      // SIMT operand copy of the weights: params (fp32) or bf16 shadow
     void* xp;             // [R][Cin] operand type
@@ -137,6 +146,7 @@ struct UmmaPlan {
     cudaEvent_t fork, join;
 };
 void umma_plan_destroy(UmmaPlan* plan);
+bool umma_side_branch_enabled();  // false under TEM_NO_FORK (side branch serialised)
 void* umma_tstamp_buffer(int64_t* nbytes, int on);  // split-K phase timestamps (diagnostics)
 int umma_wgrad_splits(const Geom& g);
 bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan);
@@ -182,6 +192,12 @@ cudaError_t launch_head(const Geom& g, const RankBufs& b, const float* labels, c
                         float* loss_out, Status* status, const EvRec& rec, cudaStream_t s, int* n);
 cudaError_t launch_head_rows(const Geom& g, const RankBufs& b, const float* labels, const float lam[3],
                              const EvRec& rec, cudaStream_t s, int* n);
+// PEM forward + loss + backward (pem.cu): the gradient at grad (K_pem floats, the PEM block of
+// the flat gradient) and the loss at *loss_out; dec_out (nullable): ReLU decisions [M][H].
+int pem_ctas(const Geom& g);
+cudaError_t launch_pem(const Geom& g, const float* f, const float* iou, const float* params, float* part,
+                       float* grad, float* loss_out, Status* status, const int64_t* stepctr, uint8_t* dec_out,
+                       cudaStream_t s, bool side, int* n);
 cudaError_t launch_head_reduce_rows(const Geom& g, const RankBufs& b, int nrows, const float lam[3],
                                    float* loss_out, Status* status, const EvRec& rec, cudaStream_t s, int* n);
 cudaError_t launch_head_reduce(const Geom& g, const RankBufs& b, const float lam[3], float* loss_out,

@@ -56,7 +56,7 @@ struct HeapLayout {
 
 struct WsLayout {
     size_t xp, h1, h2, dA2, dA1, xp_lo, h1_lo, dA2_lo, dA1_lo, z, grad, headpart, headlvl1, counter, bpart, wpart, wpart2, shadow,
-        shadow_lo, ones, zpart, epochs, stepctr, xstage, labstage, lossstage, per_rank;
+        shadow_lo, ones, zpart, epochs, stepctr, xstage, labstage, lossstage, pempart, pemdec, per_rank;
 };
 
 bool cfg_valid(const tem_config* c) {
@@ -76,12 +76,20 @@ bool cfg_valid(const tem_config* c) {
     if (c->ring_channels < 0 || c->ring_channels > kMaxChannels) return false;
     if (c->ring_chunks < 0 || c->ring_chunks > kMaxChunks) return false;
     if (c->exchange != TEM_EXCHANGE_RING && c->exchange != TEM_EXCHANGE_PS) return false;
+    if (c->pem_proposals < 0) return false;
+    if (c->pem_proposals > 0 && (c->pem_features != 32 || c->pem_hidden != 512)) return false;  // kernel shape
     return true;
 }
 
-int64_t num_params(const tem_config* c) {
+int64_t tem_params_only(const tem_config* c) {
     const int64_t C = c->c_hidden, Ci = c->c_in, Co = c->c_out;
     return C * 3 * Ci + C + C * 3 * C + C + Co * C + Co;
+}
+int64_t num_params(const tem_config* c) {  // [TEM | PEM] (reading R21)
+    const int64_t pem = c->pem_proposals > 0
+                            ? (int64_t)c->pem_hidden * c->pem_features + 2 * (int64_t)c->pem_hidden + 1
+                            : 0;
+    return tem_params_only(c) + pem;
 }
 
 int env_path() {
@@ -110,6 +118,10 @@ Geom make_geom(const tem_config* c) {
     g.off_b2 = g.off_W2 + (int64_t)g.C * 3 * g.C;
     g.off_W3 = g.off_b2 + g.C;
     g.off_b3 = g.off_W3 + (int64_t)g.Co * g.C;
+    g.pem_P = c->pem_proposals;
+    g.pem_F = c->pem_proposals > 0 ? c->pem_features : 0;
+    g.pem_H = c->pem_proposals > 0 ? c->pem_hidden : 0;
+    g.off_pem = tem_params_only(c);
     return g;
 }
 
@@ -166,6 +178,8 @@ WsLayout ws_layout(const tem_config* c) {
     w.bpart = take((size_t)((g.R + 127) / 128) * g.C * 4);
     w.wpart = take((size_t)S * wmax * 4);
     w.wpart2 = take(g.path == PATH_UMMA ? (size_t)umma_wgrad_splits(g) * ((size_t)g.C * 3 * g.C + g.C) * 4 : 0);
+    w.pempart = take((size_t)pem_ctas(g) * (pem_num_params_of(g) + 1) * 4);
+    w.pemdec = take(g.pem_P > 0 ? (size_t)g.B * g.pem_P * g.pem_H : 0);  // last ReLU decisions (tests)
     w.shadow = take(g.op_bf16 ? (size_t)g.Kpad * 2 : 0);
     w.shadow_lo = take(lo * (size_t)g.Kpad * 2);
     w.ones = take(g.path == PATH_UMMA ? (size_t)g.R * 128 * 2 : 0);
@@ -205,9 +219,14 @@ struct tem_ctx {
     // non-blocking stream ordered with the caller's stream by events
     float* loss_host_pending;  // tem_step_host: host loss buffer the compute reads back into
     bool loss_host_done;
+    const float* pem_bsp;      // tem_*_pem: this call's PEM inputs (nullptr: TEM-only call)
+    const float* pem_iou;
+    bool pem_record_dec;       // record the PEM ReLU decisions (tem_pem_relu_decisions)
     struct GraphEntry {
         const void* x;
         const void* lab;
+        const void* bsp;
+        const void* iou;
         void* loss;
         void* loss_host;
         cudaGraphExec_t exec;
@@ -229,7 +248,8 @@ tem_status graph_step(tem_ctx* c, const void* x, const void* lab, void* loss, cu
     tem_ctx::GraphEntry* e = nullptr;
     for (int i = 0; i < c->ngraphs; ++i)
         if (c->graphs[i].x == x && c->graphs[i].lab == lab && c->graphs[i].loss == loss &&
-            c->graphs[i].loss_host == c->loss_host_pending)
+            c->graphs[i].loss_host == c->loss_host_pending && c->graphs[i].bsp == c->pem_bsp &&
+            c->graphs[i].iou == c->pem_iou)
             e = &c->graphs[i];
     if (!e) {
         if (c->ngraphs == tem_ctx::kMaxGraphs) {  // evict the oldest
@@ -258,6 +278,8 @@ tem_status graph_step(tem_ctx* c, const void* x, const void* lab, void* loss, cu
         e->lab = lab;
         e->loss = loss;
         e->loss_host = c->loss_host_pending;
+        e->bsp = c->pem_bsp;
+        e->iou = c->pem_iou;
         e->exec = exec;
         e->launches = nl;
     }
@@ -366,6 +388,8 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
         b.nzpart = 0;  // set by the tcgen05 plan
         b.wpart = (float*)(base + wl.wpart);
         b.wpart2 = (float*)(base + wl.wpart2);
+        b.pempart = (float*)(base + wl.pempart);
+        b.pemdec = (uint8_t*)(base + wl.pemdec);
         b.stepctr = (int64_t*)(base + wl.stepctr);
         b.xp_lo = c->g.split ? base + wl.xp_lo : nullptr;
         b.h1_lo = c->g.split ? base + wl.h1_lo : nullptr;
@@ -445,6 +469,21 @@ static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, f
         const bool defer = fuse_reduce && c->N == 1 && g.path == PATH_UMMA && g.B > 0;
         c->reduce_deferred = defer;
         float* lh = (c->nlocal == 1) ? c->loss_host_pending : nullptr;
+        if (g.pem_P > 0) {
+            // PEM (configs[4]) is independent of TEM: on the tcgen05 path it runs on the side
+            // stream from the start of the step, beside the TEM forward GEMMs
+            const int M = g.B * g.pem_P;
+            const bool side = g.path == PATH_UMMA && g.B > 0 && !rec.ev && umma_side_branch_enabled();
+            cudaStream_t ps = side ? c->plan[l]->aux : s;
+            if (side && (cudaEventRecord(c->plan[l]->fork, s) != cudaSuccess ||
+                         cudaStreamWaitEvent(ps, c->plan[l]->fork, 0) != cudaSuccess))
+                return TEM_ERR_CUDA;
+            e = launch_pem(g, c->pem_bsp + (size_t)l * M * g.pem_F, c->pem_iou + (size_t)l * M,
+                           c->rb[l].params + g.off_pem, c->rb[l].pempart, c->rb[l].grad + g.off_pem,
+                           loss_out + 4 * c->nlocal + l, c->st_dev, c->rb[l].stepctr,
+                           c->pem_record_dec ? c->rb[l].pemdec : nullptr, ps, side, nl);
+            if (e != cudaSuccess) return TEM_ERR_CUDA;
+        }
         if (g.path == PATH_UMMA && g.B > 0) {
             e = umma_compute(g, c->rb[l], *c->plan[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s, defer, lh);
             if (lh) c->loss_host_done = true;
@@ -543,6 +582,7 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
 tem_status tem_compute(tem_ctx* c, const void* x, const float* labels, float* loss_out, void* stream) {
     tem_status st = check_ctx(c);
     if (st != TEM_OK) return st;
+    if (c->g.pem_P > 0 && !c->pem_bsp) return TEM_ERR_INVALID_ARG;  // PEM config: tem_compute_pem
     if ((!x || !labels) && c->g.B > 0) return TEM_ERR_INVALID_ARG;
     if (!loss_out) return TEM_ERR_INVALID_ARG;
     int nl = 0;
@@ -562,6 +602,7 @@ tem_status tem_exchange(tem_ctx* c, void* stream) {
 tem_status tem_step(tem_ctx* c, const void* x, const float* labels, float* loss_out, void* stream) {
     tem_status st = check_ctx(c);
     if (st != TEM_OK) return st;
+    if (c->g.pem_P > 0 && !c->pem_bsp) return TEM_ERR_INVALID_ARG;  // PEM config: tem_step_pem
     if ((!x || !labels) && c->g.B > 0) return TEM_ERR_INVALID_ARG;
     if (!loss_out) return TEM_ERR_INVALID_ARG;
     if (c->use_graphs && !c->tev) {
@@ -585,12 +626,61 @@ tem_status tem_step(tem_ctx* c, const void* x, const float* labels, float* loss_
     return st;
 }
 
+// Joint TEM + PEM (configs[4]): the PEM inputs ride along in the ctx for this call only.
+static bool pem_args_ok(tem_ctx* c, const float* bsp, const float* iou) {
+    return c->g.pem_P > 0 && ((bsp && iou) || c->g.B == 0);
+}
+
+tem_status tem_step_pem(tem_ctx* c, const void* x, const float* labels, const float* bsp, const float* iou,
+                        float* loss_out, void* stream) {
+    tem_status st = check_ctx(c);
+    if (st != TEM_OK) return st;
+    if (!pem_args_ok(c, bsp, iou)) return TEM_ERR_INVALID_ARG;
+    static const float kDummy = 0.f;
+    c->pem_bsp = bsp ? bsp : &kDummy;  // non-null marks a PEM call (B = 0: no PEM inputs read)
+    c->pem_iou = iou;
+    st = tem_step(c, x, labels, loss_out, stream);
+    c->pem_bsp = c->pem_iou = nullptr;
+    return st;
+}
+
+tem_status tem_compute_pem(tem_ctx* c, const void* x, const float* labels, const float* bsp, const float* iou,
+                           float* loss_out, void* stream) {
+    tem_status st = check_ctx(c);
+    if (st != TEM_OK) return st;
+    if (!pem_args_ok(c, bsp, iou)) return TEM_ERR_INVALID_ARG;
+    static const float kDummy = 0.f;
+    c->pem_bsp = bsp ? bsp : &kDummy;
+    c->pem_iou = iou;
+    st = tem_compute(c, x, labels, loss_out, stream);
+    c->pem_bsp = c->pem_iou = nullptr;
+    return st;
+}
+
+tem_status tem_pem_relu_decisions(tem_ctx* c, int32_t l, uint8_t* out, void* stream) {
+    if (!c || !c->alive) return TEM_ERR_STATE;
+    if (c->g.pem_P <= 0 || l < 0 || l >= c->nlocal) return TEM_ERR_INVALID_ARG;
+    if (!out) {  // start recording for the following steps (recording changes no result)
+        c->pem_record_dec = true;
+        for (int i = 0; i < c->ngraphs; ++i) cudaGraphExecDestroy(c->graphs[i].exec);
+        c->ngraphs = 0;
+        return TEM_OK;
+    }
+    if (!c->pem_record_dec) return TEM_ERR_STATE;
+    const size_t n = (size_t)c->g.B * c->g.pem_P * c->g.pem_H;
+    return n == 0 || cudaMemcpyAsync(out, c->rb[l].pemdec, n, cudaMemcpyDeviceToDevice, (cudaStream_t)stream) ==
+                         cudaSuccess
+               ? TEM_OK
+               : TEM_ERR_CUDA;
+}
+
 tem_status tem_step_host(tem_ctx* c, const void* x_host, const float* labels_host, float* loss_host,
                          void* stream) {
     tem_status st = check_ctx(c);
     if (st != TEM_OK) return st;
     if (!loss_host || ((!x_host || !labels_host) && c->g.B > 0)) return TEM_ERR_INVALID_ARG;
     if (c->nlocal != 1) return TEM_ERR_INVALID_ARG;  // host path: one rank per process
+    if (c->g.pem_P > 0) return TEM_ERR_INVALID_ARG;  // host path: TEM-only configs
     cudaStream_t s = (cudaStream_t)stream;
     const Geom& g = c->g;
     const size_t esz = g.prec == TEM_BF16 ? 2 : 4;

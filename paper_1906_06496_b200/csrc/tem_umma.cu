@@ -1857,6 +1857,8 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     return cudaSuccess;
 }
 
+bool umma_side_branch_enabled() { return getenv("TEM_NO_FORK") == nullptr; }
+
 void trace_set_umma(unsigned long long* p) { cudaMemcpyToSymbol(g_trace, &p, sizeof(p)); }
 
 void* umma_tstamp_buffer(int64_t* nbytes, int on) {  // on: 0 off, 1 all, 100 + slot one launch

@@ -40,6 +40,7 @@ class tem_config(ctypes.Structure):
         ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
         ("ring_channels", ctypes.c_int32), ("ring_chunks", ctypes.c_int32),
         ("exchange", ctypes.c_int32),
+        ("pem_proposals", ctypes.c_int32), ("pem_features", ctypes.c_int32), ("pem_hidden", ctypes.c_int32),
     ]
 
 
@@ -71,6 +72,11 @@ def lib():
         for f in (L.tem_step, L.tem_compute):
             f.restype = ctypes.c_int
             f.argtypes = [_P, _P, _P, _P, _P]
+        for f in (L.tem_step_pem, L.tem_compute_pem):
+            f.restype = ctypes.c_int
+            f.argtypes = [_P, _P, _P, _P, _P, _P, _P]
+        L.tem_pem_relu_decisions.restype = ctypes.c_int
+        L.tem_pem_relu_decisions.argtypes = [_P, ctypes.c_int32, _P, _P]
         L.tem_step_host.restype = ctypes.c_int
         L.tem_step_host.argtypes = [_P, _P, _P, _P, _P]
         L.tem_exchange.restype = ctypes.c_int
@@ -113,7 +119,8 @@ EXPORTS = ["tem_num_params", "tem_kpad", "tem_workspace_bytes", "tem_sym_bytes",
            "tem_step_host", "ring_allreduce", "ps_allreduce", "tem_sync", "tem_shutdown",
            "tem_local_grad", "tem_logits", "tem_launches_per_step", "tem_launches_per_exchange",
            "tem_status_string", "tem_kernel_path", "tem_timing_slots", "tem_timing_slot_name",
-           "tem_timing_begin", "tem_timing_end", "tem_relu_decisions", "tem_debug_buffer"]
+           "tem_timing_begin", "tem_timing_end", "tem_relu_decisions", "tem_debug_buffer",
+           "tem_step_pem", "tem_compute_pem", "tem_pem_relu_decisions"]
 
 
 def status_string(code: int) -> str:
@@ -211,6 +218,9 @@ class SessionConfig:
     ring_channels: int = 0
     ring_chunks: int = 0
     exchange: int = TEM_EXCHANGE_RING
+    pem_proposals: int = 0  # > 0: joint TEM + PEM (configs[4]); params = [TEM | PEM]
+    pem_features: int = 32
+    pem_hidden: int = 512
 
 
 class TemSession:
@@ -237,6 +247,7 @@ class TemSession:
         cfg.max_allreduce_elems = sc.max_allreduce_elems
         cfg.ring_channels, cfg.ring_chunks = sc.ring_channels, sc.ring_chunks
         cfg.exchange = sc.exchange
+        cfg.pem_proposals, cfg.pem_features, cfg.pem_hidden = sc.pem_proposals, sc.pem_features, sc.pem_hidden
         self.K = tem_num_params(cfg)
         if self.K == 0:
             raise TemError(TEM_ERR_INVALID_ARG, "config")
@@ -288,6 +299,8 @@ class TemSession:
         torch.cuda.synchronize(self.dev)
         self.ctx = tem_init(cfg, ptrs[sc.rank])
         self.loss = torch.zeros(sc.local_ranks, 4, dtype=torch.float32, device=self.dev)
+        # joint TEM + PEM: [local_ranks * 4 TEM losses | local_ranks PEM losses]
+        self.loss_pem = torch.zeros(5 * sc.local_ranks, dtype=torch.float32, device=self.dev)
 
     # -- views into caller-owned memory
     def _heap(self, l: int) -> torch.Tensor:
@@ -341,6 +354,30 @@ class TemSession:
     def compute(self, x: torch.Tensor, labels: torch.Tensor, stream=None) -> torch.Tensor:
         tem_compute(self.ctx, x.data_ptr(), labels.data_ptr(), self.loss.data_ptr(), stream)
         return self.loss
+
+    def step_pem(self, x: torch.Tensor, labels: torch.Tensor, bsp: torch.Tensor, iou: torch.Tensor, stream=None):
+        """Joint TEM + PEM step (configs[4]); returns (tem_loss [local_ranks][4], pem_loss [local_ranks])."""
+        _check(lib().tem_step_pem(_P(self.ctx), _P(x.data_ptr()), _P(labels.data_ptr()), _P(bsp.data_ptr()),
+                                  _P(iou.data_ptr()), _P(self.loss_pem.data_ptr()), _stream_ptr(stream)), "tem_step_pem")
+        n = self.sc.local_ranks
+        return self.loss_pem[:4 * n].view(n, 4), self.loss_pem[4 * n:]
+
+    def compute_pem(self, x: torch.Tensor, labels: torch.Tensor, bsp: torch.Tensor, iou: torch.Tensor, stream=None):
+        _check(lib().tem_compute_pem(_P(self.ctx), _P(x.data_ptr()), _P(labels.data_ptr()), _P(bsp.data_ptr()),
+                                     _P(iou.data_ptr()), _P(self.loss_pem.data_ptr()), _stream_ptr(stream)),
+               "tem_compute_pem")
+        n = self.sc.local_ranks
+        return self.loss_pem[:4 * n].view(n, 4), self.loss_pem[4 * n:]
+
+    def pem_record_decisions(self):
+        _check(lib().tem_pem_relu_decisions(_P(self.ctx), 0, None, None), "tem_pem_relu_decisions")
+
+    def pem_relu_decisions(self, l: int = 0) -> torch.Tensor:
+        M = self.sc.batch_per_rank * self.sc.pem_proposals
+        out = torch.zeros(M * self.sc.pem_hidden, dtype=torch.uint8, device=self.dev)
+        _check(lib().tem_pem_relu_decisions(_P(self.ctx), l, _P(out.data_ptr()), _stream_ptr(None)),
+               "tem_pem_relu_decisions")
+        return out
 
     def exchange(self, stream=None):
         tem_exchange(self.ctx, stream)
