@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """bench.py -- data-parallel BSN-TEM training throughput on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c1] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3|c1|c5] [--impl ours|reference]
 
 One "step" = one pass of the whole hot path over one batch per
 rank: conv1/conv2 forward, head + weighted logistic loss, backward, and the fused ring
@@ -35,6 +35,9 @@ WORKLOADS = {
                     "features", B=16, prec=0, dtype="f32"),
     "c3": dict(desc="configs[2]: BSN TEM bf16-operand/fp32-accumulate training, batch 256/GPU", B=256,
                prec=1, dtype="bf16 operands, f32 accumulate"),
+    "c5": dict(desc="configs[4]: BSN TEM + PEM (proposal evaluation MLP 32->512->1 over 32-d BSP features) "
+                    "joint data-parallel training, fp32, batch 16 videos/GPU x 128 proposals", B=16, prec=0,
+               dtype="f32", pem=128),
 }
 T, CIN, C = 100, 400, 512
 # Algorithmic FLOPs per sample of each kernel (dense count incl. zero-pad taps).
@@ -143,17 +146,23 @@ def cpu_baseline(workload: dict, videos: int):
     p = datagen.init_params()
     t0 = time.perf_counter()
     oracle.tem_fwd_bwd(x, p, lab, prec=workload["prec"])
+    P = workload.get("pem", 0)
+    if P:
+        oracle.pem_fwd_bwd(datagen.bsp_features(videos).reshape(videos * P, datagen.PEM_F),
+                           datagen.init_pem_params(), datagen.iou_targets(videos).ravel())
     g = np.zeros((2, oracle.kpad(1403395, 2)), np.float32)
     oracle.ring_sgd(g, np.zeros(g.shape[1], np.float32), 0.01)
     dt = time.perf_counter() - t0
     return {"value": videos / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{videos} videos ({'fp64' if workload['prec'] == 0 else 'bf16-emulated fp64'} "
-                      f"fwd+loss+bwd, T=100, 400->512->512->3) + fp32 ring/SGD replay of K=1403395 at N=2; "
-                      f"{dt:.1f} s single-threaded"}
+                      f"fwd+loss+bwd, T=100, 400->512->512->3"
+                      + (f", + PEM over {workload['pem']} proposals each" if workload.get("pem") else "")
+                      + f") + fp32 ring/SGD replay of K=1403395 at N=2; {dt:.1f} s single-threaded"}
 
 
 def run_reference(args, workload):
-    """--impl reference: the CPU oracle on this arm's config/metric/unit (rank 0 only)."""
+    """--impl reference: the CPU oracle on this arm's config/metric/unit (rank 0 only); for the
+    joint workload each video also runs the PEM oracle over its proposals."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
@@ -165,11 +174,21 @@ def run_reference(args, workload):
     per_step = 1  # one video of the workload per step: a bounded sample
     x = datagen.features(per_step, rank=0, batch_idx=0)
     lab = datagen.labels(per_step, rank=0, batch_idx=0)
-    for _ in range(args.warmup):
+    P = workload.get("pem", 0)
+    if P:
+        pp = datagen.init_pem_params()
+        fb = datagen.bsp_features(per_step).reshape(per_step * P, datagen.PEM_F)
+        gb = datagen.iou_targets(per_step).ravel()
+
+    def one():
         oracle.tem_fwd_bwd(x, p, lab, prec=workload["prec"])
+        if P:
+            oracle.pem_fwd_bwd(fb, pp, gb)
+    for _ in range(args.warmup):
+        one()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.tem_fwd_bwd(x, p, lab, prec=workload["prec"])
+        one()
     dt = time.perf_counter() - t0
     v = per_step * args.steps / dt
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
@@ -228,14 +247,17 @@ def main():
             dist.barrier()
 
     B, prec = wl["B"], wl["prec"]
+    P = wl.get("pem", 0)
     sc = tem.SessionConfig(world_size=world, rank=rank, local_ranks=1, batch_per_rank=B, precision=prec,
-                           lr=args.lr, exchange=tem.TEM_EXCHANGE_PS if args.exchange == "ps" else tem.TEM_EXCHANGE_RING)
+                           lr=args.lr, exchange=tem.TEM_EXCHANGE_PS if args.exchange == "ps" else tem.TEM_EXCHANGE_RING,
+                           pem_proposals=P)
     t_init0 = time.perf_counter()
-    sess = tem.TemSession(sc, datagen.init_params(), device=local)
+    params0 = datagen.init_params() if not P else np.concatenate([datagen.init_params(), datagen.init_pem_params()])
+    sess = tem.TemSession(sc, params0, device=local)
     t_init = time.perf_counter() - t_init0
 
     # resident input pool (HBM); rank r's shard of global batch k uses seeds (r, k)
-    xs, labs = [], []
+    xs, labs, fs, gs = [], [], [], []
     for k in range(args.pool):
         x = datagen.features(B, rank=rank, batch_idx=k)
         lab = datagen.labels(B, rank=rank, batch_idx=k)
@@ -244,13 +266,23 @@ def main():
         else:
             xs.append(torch.from_numpy(x).to(dev))
         labs.append(torch.from_numpy(lab).to(dev))
+        if P:
+            fs.append(torch.from_numpy(datagen.bsp_features(B, P, rank=rank, batch_idx=k)).to(dev))
+            gs.append(torch.from_numpy(datagen.iou_targets(B, P, rank=rank, batch_idx=k)).to(dev))
+
+    def do_step(i):
+        j = i % args.pool
+        if P:
+            sess.step_pem(xs[j], labs[j], fs[j], gs[j])
+        else:
+            sess.step(xs[j], labs[j])
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
     clocks = ClockSampler(local)
     clocks.start()
     for i in range(args.warmup):
-        sess.step(xs[i % args.pool], labs[i % args.pool])
+        do_step(i)
     code, _ = sess.sync()
     if code != 0:
         raise tem.TemError(code, "warmup")
@@ -263,7 +295,7 @@ def main():
     for i in range(args.steps):
         flush.zero_()
         ev[i][0].record(stream)
-        sess.step(xs[i % args.pool], labs[i % args.pool])  # CUDA-graph replay of the whole step
+        do_step(i)  # CUDA-graph replay of the whole step
         ev[i][1].record(stream)
     torch.cuda.synchronize()
     clocks.mark_stop()
@@ -273,6 +305,8 @@ def main():
     if code != 0:
         raise tem.TemError(code, "timed steps")
     step_ms = [a.elapsed_time(b) for a, b in ev]
+    step_stats = {"min_us": min(step_ms) * 1e3, "median_us": statistics.median(step_ms) * 1e3,
+                  "max_us": max(step_ms) * 1e3}
     tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tot, op=dist.ReduceOp.MAX)
@@ -288,7 +322,7 @@ def main():
     sess.timing_begin(n_inst)
     for i in range(n_inst):
         flush.zero_()
-        sess.step(xs[i % args.pool], labs[i % args.pool])
+        do_step(i)
     torch.cuda.synchronize()
     slot_ms, nrec = sess.timing_end()
     code, _ = sess.sync()
@@ -305,8 +339,24 @@ def main():
             xh = [torch.from_numpy(datagen.features(B, rank=rank, batch_idx=k)).pin_memory() for k in range(2)]
         lh = [torch.from_numpy(datagen.labels(B, rank=rank, batch_idx=k)).pin_memory() for k in range(2)]
         loss_h = torch.zeros(4, dtype=torch.float32).pin_memory()
+        if P:  # joint workload: host copies + tem_step_pem + loss read-back inside each step
+            fh = [torch.from_numpy(datagen.bsp_features(B, P, rank=rank, batch_idx=k)).pin_memory() for k in range(2)]
+            gh = [torch.from_numpy(datagen.iou_targets(B, P, rank=rank, batch_idx=k)).pin_memory() for k in range(2)]
+            xd_, ld_, fd_, gd_ = (torch.empty_like(t, device=dev) for t in (xh[0], lh[0], fh[0], gh[0]))
+            loss_h = torch.zeros(5, dtype=torch.float32).pin_memory()
+
+            def host_step(i):
+                xd_.copy_(xh[i % 2], non_blocking=True)
+                ld_.copy_(lh[i % 2], non_blocking=True)
+                fd_.copy_(fh[i % 2], non_blocking=True)
+                gd_.copy_(gh[i % 2], non_blocking=True)
+                sess.step_pem(xd_, ld_, fd_, gd_)
+                loss_h.copy_(sess.loss_pem, non_blocking=True)
+        else:
+            def host_step(i):
+                sess.step_host(xh[i % 2], lh[i % 2], loss_h)
         for i in range(2):
-            sess.step_host(xh[i], lh[i], loss_h)
+            host_step(i)
         torch.cuda.synchronize()
         ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         barrier()
@@ -314,7 +364,7 @@ def main():
         for i in range(args.steps):
             flush.zero_()
             ev2[i][0].record(stream)
-            sess.step_host(xh[i % 2], lh[i % 2], loss_h)
+            host_step(i)
             ev2[i][1].record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -324,9 +374,12 @@ def main():
         t2 = torch.tensor([sum(a.elapsed_time(b) for a, b in ev2)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t2, op=dist.ReduceOp.MAX)
+        h2d = int(xh[0].numel() * xh[0].element_size() + lh[0].numel() * 4)
+        if P:
+            h2d += int(fh[0].numel() * 4 + gh[0].numel() * 4)
         e2e = {"value": world * B * args.steps / (float(t2.item()) / 1e3), "unit": UNIT,
-               "h2d_bytes_per_step": int(xh[0].numel() * xh[0].element_size() + lh[0].numel() * 4),
-               "d2h_bytes_per_step": 16, "api": "tem_step_host"}
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(loss_h.numel() * 4),
+               "api": "tem_step_pem (host copies on the stream)" if P else "tem_step_host"}
 
     # ---------------- roofline of the dominant kernel ----------------
     peaks, peak_src = load_peaks()
@@ -376,7 +429,10 @@ def main():
                                 ("parameter server on rank 0 (KP1)" if args.exchange == "ps"
                                  else "fused ring allreduce + mean + SGD (KR1)")),
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",
-                   "kernel_path": sess.kernel_path()},
+                   "kernel_path": sess.kernel_path(),
+                   **({"pem": f"{P} proposals/video, 32-d BSP features, MLP 32->512->1, gradient [TEM | PEM] "
+                              f"= {sess.K} elements in one exchange"} if P else {})},
+        "step_us": step_stats,
         "gpu_launches": launches * args.steps,
         "launches_per_step": launches,
         "roofline": roof,

@@ -14,9 +14,9 @@ namespace tem {
 // Kernel launch with programmatic dependent launch allowed (unless TEM_NO_PDL is set): the
 // kernel's prologue overlaps the tail of its stream predecessor (see pdl_wait/pdl_trigger).
 bool pdl_enabled();
-// Launch priority of the step's two graph branches: the critical path (prep -> convs -> head ->
-// dgrad -> conv1 wgrad -> exchange) high, the side branch (head reduction, conv2 wgrad) low,
-// so the block scheduler hands the side branch only the SMs the critical path leaves idle.
+// Launch priority of the step's graph branches: the critical path (prep -> convs -> head ->
+// dgrad -> conv1 wgrad -> exchange) high, the side branches (head reduction, conv2 wgrad, PEM)
+// low, so the block scheduler hands them the SMs the critical path leaves idle.
 // TEM_NO_PRIO disables.  Returns the number of attributes written (0 or 1).
 int launch_priority_attr(cudaLaunchAttribute* a, bool side_branch);
 template <typename... KArgs, typename... Args>
@@ -144,6 +144,9 @@ struct UmmaPlan {
     int S1, S2;  // split-K factors of conv1 / conv2 wgrad (<= S, the workspace's)
     cudaStream_t aux;         // second stream: conv2 wgrad runs beside conv2 dgrad / conv1 wgrad
     cudaEvent_t fork, join;
+    cudaStream_t pem;         // third stream: the PEM (configs[4]) beside the whole TEM step
+    cudaEvent_t pem_fork, pem_join;
+    bool pem_pending;         // a PEM launch on `pem` awaits its join before the exchange
 };
 void umma_plan_destroy(UmmaPlan* plan);
 bool umma_side_branch_enabled();  // false under TEM_NO_FORK (side branch serialised)
@@ -165,12 +168,13 @@ cudaError_t launch_relu_decisions(const Geom& g, const RankBufs& b, uint8_t* out
 // Kernel slots of one step (for tem_timing_*): every launch is bracketed by
 // ev[2*slot] / ev[2*slot+1] when ev != nullptr.
 enum Slot { SLOT_PREP = 0, SLOT_CONV1, SLOT_CONV2, SLOT_HEAD, SLOT_HEADFIN, SLOT_DGRAD, SLOT_WGRAD2,
-            SLOT_RED2, SLOT_WGRAD1, SLOT_RED1, SLOT_EXCHANGE, NUM_SLOTS };
+            SLOT_RED2, SLOT_WGRAD1, SLOT_RED1, SLOT_EXCHANGE, SLOT_PEM, SLOT_PEMRED, NUM_SLOTS };
 const char* slot_name(int slot);
 // kernel-span trace buffers (diagnostics): one setter per translation unit with traced kernels
 void trace_set_umma(unsigned long long* p);
 void trace_set_head(unsigned long long* p);
 void trace_set_ring(unsigned long long* p);
+void trace_set_pem(unsigned long long* p);
 struct EvRec {
     cudaEvent_t* ev;  // [NUM_SLOTS*2] or nullptr
     cudaStream_t s;
@@ -195,9 +199,10 @@ cudaError_t launch_head_rows(const Geom& g, const RankBufs& b, const float* labe
 // PEM forward + loss + backward (pem.cu): the gradient at grad (K_pem floats, the PEM block of
 // the flat gradient) and the loss at *loss_out; dec_out (nullable): ReLU decisions [M][H].
 int pem_ctas(const Geom& g);
+// pem_kernel runs on `s`; pem_reduce on `s_red` (forked from `s` through `fork` when they differ).
 cudaError_t launch_pem(const Geom& g, const float* f, const float* iou, const float* params, float* part,
                        float* grad, float* loss_out, Status* status, const int64_t* stepctr, uint8_t* dec_out,
-                       cudaStream_t s, bool side, int* n);
+                       cudaStream_t s, cudaStream_t s_red, cudaEvent_t fork, int* n);
 cudaError_t launch_head_reduce_rows(const Geom& g, const RankBufs& b, int nrows, const float lam[3],
                                    float* loss_out, Status* status, const EvRec& rec, cudaStream_t s, int* n);
 cudaError_t launch_head_reduce(const Geom& g, const RankBufs& b, const float lam[3], float* loss_out,

@@ -28,6 +28,7 @@ constexpr int PEM_F = 32, PEM_H = 512, PEM_THREADS = 256, PEM_RB = 8;  // rows p
 __global__ void __launch_bounds__(PEM_THREADS, 1) pem_kernel(const float* __restrict__ f, const float* __restrict__ g,
                                                           const float* __restrict__ prm, int M, int rows_per_cta,
                                                           float* __restrict__ part, uint8_t* __restrict__ dec_out) {
+    trace_begin(SLOT_PEM);
     pdl_trigger();
     pdl_wait();
     constexpr int KP = PEM_H * PEM_F + 2 * PEM_H + 1;
@@ -41,15 +42,26 @@ __global__ void __launch_bounds__(PEM_THREADS, 1) pem_kernel(const float* __rest
     const float b2 = w2[PEM_H];
     float w[2][PEM_F], acc[2][PEM_F];
     float bb[2], ww[2], gb[2] = {0.f, 0.f}, gw[2] = {0.f, 0.f};
+    {
+        // W1 rows via shared memory: fully coalesced loads (consecutive threads, consecutive
+        // floats), then each thread reads its two rows from a 33-float padded layout (conflict
+        // free).  Direct row loads were 32 cache lines per warp instruction.
+        extern __shared__ float w1s[];  // [H][F + 1]
+        for (int i = tid; i < PEM_H * PEM_F; i += PEM_THREADS) {
+            const int j = i / PEM_F, k = i - j * PEM_F;
+            w1s[j * (PEM_F + 1) + k] = __ldg(W1 + i);
+        }
+        __syncthreads();
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-        const int j = tid + u * PEM_THREADS;
+        for (int u = 0; u < 2; ++u) {
+            const int j = tid + u * PEM_THREADS;
 #pragma unroll
-        for (int k = 0; k < PEM_F; ++k) w[u][k] = __ldg(W1 + (size_t)j * PEM_F + k);  // PEM block: any alignment
+            for (int k = 0; k < PEM_F; ++k) w[u][k] = w1s[j * (PEM_F + 1) + k];
 #pragma unroll
-        for (int k = 0; k < PEM_F; ++k) acc[u][k] = 0.f;
-        bb[u] = b1[j];
-        ww[u] = w2[j];
+            for (int k = 0; k < PEM_F; ++k) acc[u][k] = 0.f;
+            bb[u] = b1[j];
+            ww[u] = w2[j];
+        }
     }
     float gb2 = 0.f, lsum = 0.f;  // thread 0
     const int m0 = blockIdx.x * rows_per_cta, m1 = min(M, m0 + rows_per_cta);
@@ -125,40 +137,50 @@ __global__ void __launch_bounds__(PEM_THREADS, 1) pem_kernel(const float* __rest
         dst[KP - 1] = gb2;
         dst[KP] = lsum;
     }
+    trace_end(SLOT_PEM);
 }
 
 // grad[e] = sum over CTA partials in CTA order; loss = sum_j L_j / M; NONFINITE latch.
 __global__ void pem_reduce_kernel(const float* __restrict__ part, int G, int M, float* __restrict__ grad,
                                   float* __restrict__ loss_out, Status* status, const int64_t* stepctr) {
+    trace_begin(SLOT_PEMRED);
     pdl_trigger();
     pdl_wait();
     constexpr int KP = PEM_H * PEM_F + 2 * PEM_H + 1;
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e > KP) return;
-    float s = 0.f;
-    for (int j = 0; j < G; ++j) s += part[(size_t)j * (KP + 1) + e];
-    if (e < KP) {
-        grad[e] = s;
-    } else {
-        const float L = M > 0 ? s / (float)M : 0.f;
-        *loss_out = L;
-        if (!isfinite(L)) latch(status, TEM_ERR_NONFINITE, stepctr ? *stepctr : 0);
+    if (e <= KP) {
+        float s = 0.f;
+        for (int j = 0; j < G; ++j) s += part[(size_t)j * (KP + 1) + e];
+        if (e < KP) {
+            grad[e] = s;
+        } else {
+            const float L = M > 0 ? s / (float)M : 0.f;
+            *loss_out = L;
+            if (!isfinite(L)) latch(status, TEM_ERR_NONFINITE, stepctr ? *stepctr : 0);
+        }
     }
+    trace_end(SLOT_PEMRED);
 }
 
 }  // namespace
 
+void trace_set_pem(unsigned long long* p) { cudaMemcpyToSymbol(g_trace, &p, sizeof(p)); }
+
 int pem_ctas(const Geom& g) {
     const int M = g.B * g.pem_P;
     if (M <= 0) return 0;
-    int G = (M + 31) / 32;  // ~32 proposals per CTA
+    // All SMs, on the critical path right after prep_x.  Measured alternatives
+    // (scripts/probes/step_trace.py --workload c5): on a graph branch of its own (16 CTAs
+    // beside the TEM step) steps were ~20 us slower and occasionally stalled for milliseconds;
+    // more CTAs there took SMs conv2's 8-CTA clusters need.
+    int G = (M + 13) / 14;
     if (G > 148) G = 148;
     return G;
 }
 
 cudaError_t launch_pem(const Geom& g, const float* f, const float* iou, const float* params, float* part,
                        float* grad, float* loss_out, Status* status, const int64_t* stepctr, uint8_t* dec_out,
-                       cudaStream_t s, bool side, int* n) {
+                       cudaStream_t s, cudaStream_t s_red, cudaEvent_t fork, int* n) {
     const int M = g.B * g.pem_P;
     const int G = pem_ctas(g);
     if (G == 0) {
@@ -167,11 +189,24 @@ cudaError_t launch_pem(const Geom& g, const float* f, const float* iou, const fl
         return e;
     }
     const int rows = (M + G - 1) / G;
-    cudaError_t e = launch_pdl(pem_kernel, dim3(G), dim3(PEM_THREADS), 0, s, side, f, iou, params, M, rows, part, dec_out);
+    // pem_kernel on the caller's (critical-path) stream with programmatic dependent launch;
+    // pem_reduce follows a cross-stream event and launches without it
+    constexpr size_t W1S = sizeof(float) * PEM_H * (PEM_F + 1);  // 67.6 KB staging
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t ea = cudaFuncSetAttribute(pem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)W1S);
+        if (ea != cudaSuccess) return ea;
+        attr = true;
+    }
+    cudaError_t e = launch_pdl(pem_kernel, dim3(G), dim3(PEM_THREADS), W1S, s, false, f, iou, params, M, rows, part,
+                               dec_out);
     if (e != cudaSuccess) return e;
     ++*n;
+    if (s_red != s && fork &&
+        (cudaEventRecord(fork, s) != cudaSuccess || cudaStreamWaitEvent(s_red, fork, 0) != cudaSuccess))
+        return cudaErrorUnknown;
     const int KP = (int)pem_num_params_of(g);
-    e = launch_pdl(pem_reduce_kernel, dim3((KP + 1 + 255) / 256), dim3(256), 0, s, side, (const float*)part, G, M, grad,
+    e = launch_pdl(pem_reduce_kernel, dim3((KP + 1 + 255) / 256), dim3(256), 0, s_red, true, (const float*)part, G, M, grad,
                    loss_out, status, stepctr);
     if (e == cudaSuccess) ++*n;
     return e;

@@ -36,7 +36,10 @@ int tem::launch_priority_attr(cudaLaunchAttribute* a, bool side) {
         }
     }
     if (!on || lo == hi) return 0;
-    static const bool side_high = getenv("TEM_PRIO_MAIN") == nullptr;
+    // critical path high, side branches (head reduction, conv2 wgrad, PEM) low.  Measured: with
+    // the PEM branch at high or equal priority, single c5 steps stalled for 2-22 ms; neutral
+    // for c2.  TEM_PRIO_SIDE=1 inverts (experiments).
+    static const bool side_high = getenv("TEM_PRIO_SIDE") != nullptr;
     a->id = cudaLaunchAttributePriority;
     a->val.priority = (side == side_high) ? hi : lo;
     return 1;
@@ -473,15 +476,16 @@ static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, f
             // PEM (configs[4]) is independent of TEM: on the tcgen05 path it runs on the side
             // stream from the start of the step, beside the TEM forward GEMMs
             const int M = g.B * g.pem_P;
-            const bool side = g.path == PATH_UMMA && g.B > 0 && !rec.ev && umma_side_branch_enabled();
-            cudaStream_t ps = side ? c->plan[l]->aux : s;
-            if (side && (cudaEventRecord(c->plan[l]->fork, s) != cudaSuccess ||
-                         cudaStreamWaitEvent(ps, c->plan[l]->fork, 0) != cudaSuccess))
-                return TEM_ERR_CUDA;
+            // PEM (configs[4]): both kernels on the critical path right after prep_x (all SMs)
+            const bool side = getenv("TEM_PEM_SIDE") != nullptr && g.path == PATH_UMMA && g.B > 0 && !rec.ev &&
+                              umma_side_branch_enabled();
+            cudaStream_t ps = side ? c->plan[l]->pem : s;
+            if (side) c->plan[l]->pem_pending = true;  // umma_compute joins it before returning
             e = launch_pem(g, c->pem_bsp + (size_t)l * M * g.pem_F, c->pem_iou + (size_t)l * M,
                            c->rb[l].params + g.off_pem, c->rb[l].pempart, c->rb[l].grad + g.off_pem,
                            loss_out + 4 * c->nlocal + l, c->st_dev, c->rb[l].stepctr,
-                           c->pem_record_dec ? c->rb[l].pemdec : nullptr, ps, side, nl);
+                           c->pem_record_dec ? c->rb[l].pemdec : nullptr, s, ps,
+                           side ? c->plan[l]->pem_fork : nullptr, nl);
             if (e != cudaSuccess) return TEM_ERR_CUDA;
         }
         if (g.path == PATH_UMMA && g.B > 0) {
@@ -833,6 +837,7 @@ void* tem_debug_buffer(tem_ctx* c, int32_t l, const char* name, int64_t* nbytes)
             trace_set_umma(p);
             trace_set_head(p);
             trace_set_ring(p);
+            trace_set_pem(p);
         }
         if (nbytes) *nbytes = (int64_t)(sizeof(unsigned long long) * words);
         return buf;

@@ -1584,7 +1584,10 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     if (g.R == 0) return true;  // empty shard: nothing to plan (tem_compute takes the B = 0 branch)
     if (cudaStreamCreateWithFlags(&P.aux, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&P.fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&P.join, cudaEventDisableTiming) != cudaSuccess)
+        cudaEventCreateWithFlags(&P.join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&P.pem, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&P.pem_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&P.pem_join, cudaEventDisableTiming) != cudaSuccess)
         return false;
     P.npass = npl == 2 ? 3 : 1;
     const int R = g.R, Tp = g.T + 2;
@@ -1749,6 +1752,9 @@ void umma_plan_destroy(UmmaPlan* plan) {
     if (plan->aux) cudaStreamDestroy(plan->aux);
     if (plan->fork) cudaEventDestroy(plan->fork);
     if (plan->join) cudaEventDestroy(plan->join);
+    if (plan->pem) cudaStreamDestroy(plan->pem);
+    if (plan->pem_fork) cudaEventDestroy(plan->pem_fork);
+    if (plan->pem_join) cudaEventDestroy(plan->pem_join);
     delete plan;
 }
 
@@ -1853,6 +1859,11 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     ++n;
     }
     if (!no_fork && cudaStreamWaitEvent(s, P.join, 0) != cudaSuccess) return cudaErrorUnknown;  // join
+    if (P.pem_pending) {  // the PEM branch (configs[4]) joins before the exchange too
+        const_cast<UmmaPlan&>(P).pem_pending = false;
+        if (cudaEventRecord(P.pem_join, P.pem) != cudaSuccess || cudaStreamWaitEvent(s, P.pem_join, 0) != cudaSuccess)
+            return cudaErrorUnknown;
+    }
     *nl += n;
     return cudaSuccess;
 }

@@ -25,14 +25,23 @@ def main():
     import torch
     import datagen
     from paper_1906_06496_b200 import tem
-    B, prec = {"c1": (4, 0), "c2": (16, 0), "c3": (256, 1)}[args.workload]
-    sc = tem.SessionConfig(world_size=1, rank=0, local_ranks=1, batch_per_rank=B, precision=prec, lr=0.01)
-    s = tem.TemSession(sc, datagen.init_params())
+    B, prec = {"c1": (4, 0), "c2": (16, 0), "c3": (256, 1), "c5": (16, 0)}[args.workload]
+    P = datagen.PEM_P if args.workload == "c5" else 0
+    sc = tem.SessionConfig(world_size=1, rank=0, local_ranks=1, batch_per_rank=B, precision=prec, lr=0.01,
+                           pem_proposals=P)
+    p0 = datagen.init_params() if not P else np.concatenate([datagen.init_params(), datagen.init_pem_params()])
+    s = tem.TemSession(sc, p0)
     xs = datagen.features(B)
     x = torch.from_numpy(datagen.to_bf16_bits(xs).view(np.int16)).cuda() if prec == 1 else torch.from_numpy(xs).cuda()
     lab = torch.from_numpy(datagen.labels(B)).cuda()
+    if P:
+        fd = torch.from_numpy(datagen.bsp_features(B)).cuda()
+        gd = torch.from_numpy(datagen.iou_targets(B)).cuda()
+        step = lambda: s.step_pem(x, lab, fd, gd)  # noqa: E731
+    else:
+        step = lambda: s.step(x, lab)  # noqa: E731
     for _ in range(5):
-        s.step(x, lab)
+        step()
     torch.cuda.synchronize()
     lib = tem.lib()
     nb = ctypes.c_int64(0)
@@ -49,7 +58,7 @@ def main():
         init[0:2 * nslots:2] = -1  # 0xFFFF... as u64: min() identity
         buf.copy_(init.view(torch.uint64) if hasattr(torch, "uint64") else init)
         torch.cuda.synchronize()
-        s.step(x, lab)
+        step()
         torch.cuda.synchronize()
         allv = buf.cpu().view(torch.int64).numpy().astype(np.float64)
         runs.append(allv[:2 * nslots].reshape(nslots, 2))
