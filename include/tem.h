@@ -91,7 +91,11 @@ typedef struct {
                                TEM_EXCHANGE_PS (the parameter-server comparator, P:115-124:
                                ranks push gradients to rank 0, which sums them in ascending
                                rank order, applies mean + SGD to its weights and pushes w'
-                               back to every rank)                                           */
+                               back to every rank) or TEM_EXCHANGE_TWOSHOT (NVSwitch two-shot,
+                               SURVEY 8(f) NEXT #3(i): each block's owner reads the block from
+                               every rank and sums in the ring's chain order -- bit-identical
+                               to the ring -- then writes w' into every rank: 2 phases instead
+                               of 2(N-1) rounds)                                              */
     /* --- PEM: joint TEM + PEM training (BASELINE configs[4]).  BSN's
      *     proposal evaluation module: per proposal a BSP feature f (F) -> ReLU(W1 f + b1) (H)
      *     -> sigmoid(w2 . h + b2), MSE to the proposal's IoU (readings R19-R20).  Its
@@ -102,7 +106,7 @@ typedef struct {
     int32_t pem_hidden;     /* H: 512 (required when pem_proposals > 0)                      */
 } tem_config;
 
-enum { TEM_EXCHANGE_RING = 0, TEM_EXCHANGE_PS = 1 };
+enum { TEM_EXCHANGE_RING = 0, TEM_EXCHANGE_PS = 1, TEM_EXCHANGE_TWOSHOT = 2 };
 
 /* --- sizes -----------------------------------------------------------------------------
  * K      = c_hidden*3*c_in + c_hidden + c_hidden*3*c_hidden + c_hidden + 3*c_hidden + 3
@@ -179,6 +183,12 @@ tem_status ring_allreduce(tem_ctx* ctx, float* buf, int64_t K, int32_t op, void*
  * rank 0's heap; rank 0 sums in ascending rank order, applies op, and pushes the
  * result back to every rank.  Same buffer rules as ring_allreduce. */
 tem_status ps_allreduce(tem_ctx* ctx, float* buf, int64_t K, int32_t op, void* stream);
+
+/* Two-shot allreduce over NVSwitch: the owner of block b reads block b
+ * from every rank's heap and sums along the ring's chain g_b + g_{b+1} + ... + g_{b+N-1}, applies
+ * op once and stores the result into every rank's buffer.  Same buffer rules, partition (R9)
+ * and result bits as ring_allreduce, with two communication phases instead of 2(N-1). */
+tem_status twoshot_allreduce(tem_ctx* ctx, float* buf, int64_t K, int32_t op, void* stream);
 
 /* Blocks until all work of ctx on `stream` is done; returns the latched device status.
  * For NONFINITE, *bad_step (if non-NULL) receives the 0-based step index. */

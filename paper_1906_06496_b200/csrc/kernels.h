@@ -226,10 +226,13 @@ struct RingParams {
     int64_t K, Kpad;
     float lr;
     int64_t off_dst, off_stage, off_flags;
+    int64_t off_src;  // two-shot: heap offset of the source when it already lives in the heap
+                      // (off_stage < 0), i.e. ring_allreduce's user region
     Status* status;
     uint64_t spin_ns;
 };
 cudaError_t launch_ring(const RingParams& p, cudaStream_t s);
+cudaError_t launch_twoshot(const RingParams& p, cudaStream_t s);  // NVSwitch two-shot (NEXT #3(i))
 // N = 1 owner update with the deferred split-K reductions fused in: grad[e] = sum_s part1[s][e]
 // (W1, b1), sum_s part2[s][e - off2] (W2), or grad[e] (the head-written entries); the same
 // ascending-s order as reduce_wgrad_kernel, so the result is bit-identical to the unfused path.

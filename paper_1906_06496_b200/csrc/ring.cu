@@ -243,6 +243,98 @@ __global__ void __launch_bounds__(RING_THREADS) ring_kernel(const __grid_constan
     if (tid == 0) L.epochs[g] = epoch;
 }
 
+// Two-shot allreduce over NVSwitch: the same result bits as the
+// ring, in two communication phases instead of 2(N-1) dependent rounds.
+//   phase 0: every rank stages its gradient in its own heap (skipped when the source already
+//            is its heap's user region) and raises, per channel, a ready flag in every peer.
+//   phase 1: rank n owns block b = (n+1) mod N (the ring's owner).  Channel g waits for
+//            the ready flags of all N sources, reads its piece of block b from every rank's
+//            heap and sums along the ring's chain g_b + g_{b+1} + ... + g_{b+N-1} (SURVEY 8(c)
+//            c.1) -- so every element is bit-identical to the ring and to the oracle -- applies
+//            mean (and SGD), writes the result into EVERY rank's destination (direct NVLink
+//            stores) and raises a done flag in every peer.
+//   then:    each rank waits for the done flags of the N-1 other owners and refreshes its bf16
+//            operand copies of those blocks.
+// Flags: [epoch | K tag] as the ring; ready[src][channel], done[owner][channel] at off_flags.
+__global__ void __launch_bounds__(RING_THREADS) twoshot_kernel(const __grid_constant__ RingParams P) {
+    __shared__ uint32_t s_epoch;
+    __shared__ int s_abort;
+    const int l = blockIdx.y, g = blockIdx.x, tid = threadIdx.x;
+    const int N = P.N, n = P.rank_base + l, G = P.G;
+    const RingLocal& L = P.loc[l];
+    const int64_t K = P.K, Bk = P.Kpad / N, nvec = Bk / 4;
+    const float inv_n = 1.0f / (float)N;
+    auto heap = [&](int r) { return L.heaps[r]; };
+    auto stage = [&](int r) -> float* {  // rank r's readable copy of its gradient
+        return P.off_stage >= 0 ? reinterpret_cast<float*>(heap(r) + P.off_stage) : reinterpret_cast<float*>(heap(r) + P.off_src);
+    };
+    auto flag = [&](int r, int phase, int who) -> uint64_t* {
+        return reinterpret_cast<uint64_t*>(heap(r) + P.off_flags) + ((int64_t)phase * TEM_MAX_RANKS + who) * kMaxChannels + g;
+    };
+    if (tid == 0) {
+        s_epoch = L.epochs[g] + 1;
+        s_abort = 0;
+    }
+    __syncthreads();
+    const uint32_t epoch = s_epoch;
+    // channel g's piece of every block: vectors [v0, v1) of each block
+    const int64_t v0 = (int64_t)g * nvec / G, v1 = (int64_t)(g + 1) * nvec / G;
+    // ---------------- phase 0: stage (own heap) + ready flags ----------------
+    if (P.off_stage >= 0) {
+        float* st = stage(n);
+        for (int b = 0; b < N; ++b)
+            for (int64_t v = v0 + tid; v < v1; v += RING_THREADS) {
+                const int64_t e = (int64_t)b * Bk + 4 * v;
+                if (e >= K) continue;
+                st4_masked(st, e, K, ld4_masked(L.src, e, K));
+            }
+    }
+    __syncthreads();
+    if (tid < N) st_release_sys(flag(tid, 0, n), flag_value(epoch, K));  // ready: my piece g is readable
+    // ---------------- phase 1: owner reduce (chain order) + mean/SGD + broadcast ----------------
+    const int b = modn(n + 1, N);
+    for (int r = 0; r < N; ++r)
+        if (!wait_flag(flag(n, 0, r), epoch, K, P.status, P.spin_ns, &s_abort)) return;
+    for (int64_t v = v0 + tid; v < v1; v += RING_THREADS) {
+        const int64_t e = (int64_t)b * Bk + 4 * v;
+        if (e >= K) continue;
+        float4 a = ldcg4_masked(stage(b), e, K);  // chain start: rank b
+        for (int q = 1; q < N; ++q) {
+            const float4 t = ldcg4_masked(stage(modn(b + q, N)), e, K);
+            a.x = a.x + t.x; a.y = a.y + t.y; a.z = a.z + t.z; a.w = a.w + t.w;
+        }
+        if (P.op == TEM_MEAN) {
+            a.x = a.x * inv_n; a.y = a.y * inv_n; a.z = a.z * inv_n; a.w = a.w * inv_n;
+        }
+        float4 out = a;
+        if (P.mode == 1) {
+            const float4 w = *reinterpret_cast<const float4*>(L.dst_self + e);
+            out.x = __fmaf_rn(-P.lr, a.x, w.x);
+            out.y = __fmaf_rn(-P.lr, a.y, w.y);
+            out.z = __fmaf_rn(-P.lr, a.z, w.z);
+            out.w = __fmaf_rn(-P.lr, a.w, w.w);
+            if (L.shadow) store_shadow4(L.shadow, L.shadow_lo, e, out);
+        }
+        for (int r = 0; r < N; ++r) st4_masked(reinterpret_cast<float*>(heap(r) + P.off_dst), e, K, out);
+    }
+    __syncthreads();
+    if (tid < N) st_release_sys(flag(tid, 1, n), flag_value(epoch, K));  // done: block b piece g written
+    // ---------------- receive: the other owners' blocks, refresh operand copies ----------------
+    for (int q = 1; q < N; ++q) {
+        const int owner = modn(n + q, N), blk = modn(owner + 1, N);
+        if (!wait_flag(flag(n, 1, owner), epoch, K, P.status, P.spin_ns, &s_abort)) return;
+        if (L.shadow) {
+            for (int64_t v = v0 + tid; v < v1; v += RING_THREADS) {
+                const int64_t e = (int64_t)blk * Bk + 4 * v;
+                store_shadow4(L.shadow, L.shadow_lo, e, ld_cg4(L.dst_self + e));
+            }
+        }
+    }
+    // no rank may restage (next collective) before every owner has read this one: the done
+    // flags above cover it -- an owner raises done only after reading all N stages
+    if (tid == 0) L.epochs[g] = epoch;
+}
+
 // N = 1: the ring is the identity; the owner update alone.
 __global__ void sgd_single_kernel(const float* __restrict__ g, float* __restrict__ w,
                                   __nv_bfloat16* __restrict__ shadow, __nv_bfloat16* __restrict__ shadow_lo,
@@ -417,6 +509,16 @@ cudaError_t launch_sgd_fused(float* g, float* w, __nv_bfloat16* shadow, __nv_bfl
                              int64_t stride2, int64_t off2, int64_t n2, int S2, cudaStream_t s) {
     return launch_pdl(sgd_fused_kernel, dim3(296), dim3(512), 0, s, false, g, w, shadow, shadow_lo, n, lr, p1, stride1,
                       n1, S1, p2, stride2, off2, n2, S2);
+}
+
+cudaError_t launch_twoshot(const RingParams& p, cudaStream_t s) {
+    dim3 grid(p.G, p.nlocal), block(RING_THREADS);
+    if (p.nlocal > 1) {
+        void* args[] = {const_cast<RingParams*>(&p)};
+        return cudaLaunchCooperativeKernel((const void*)twoshot_kernel, grid, block, args, 0, s);
+    }
+    twoshot_kernel<<<grid, block, 0, s>>>(p);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_ps(const PsParams& p, cudaStream_t s) {

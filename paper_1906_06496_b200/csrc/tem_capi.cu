@@ -54,7 +54,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 int64_t roundup(int64_t x, int64_t q) { return (x + q - 1) / q * q; }
 
 struct HeapLayout {
-    size_t off_user, user_bytes, off_stage, off_ps, off_flags, off_psflags, total;
+    size_t off_user, user_bytes, off_stage, off_ps, off_flags, off_psflags, off_tsflags, total;
 };
 
 struct WsLayout {
@@ -78,7 +78,8 @@ bool cfg_valid(const tem_config* c) {
     if (c->max_allreduce_elems < 0) return false;
     if (c->ring_channels < 0 || c->ring_channels > kMaxChannels) return false;
     if (c->ring_chunks < 0 || c->ring_chunks > kMaxChunks) return false;
-    if (c->exchange != TEM_EXCHANGE_RING && c->exchange != TEM_EXCHANGE_PS) return false;
+    if (c->exchange != TEM_EXCHANGE_RING && c->exchange != TEM_EXCHANGE_PS && c->exchange != TEM_EXCHANGE_TWOSHOT)
+        return false;
     if (c->pem_proposals < 0) return false;
     if (c->pem_proposals > 0 && (c->pem_features != 32 || c->pem_hidden != 512)) return false;  // kernel shape
     return true;
@@ -146,7 +147,8 @@ HeapLayout heap_layout(const tem_config* c) {
     h.off_flags = align_up(h.off_ps + (size_t)N * kps * 4, 4096);
     const size_t ring_flags = (size_t)kMaxChannels * kMaxChunks * 2 * (TEM_MAX_RANKS - 1) * 8;
     h.off_psflags = h.off_flags + ring_flags;
-    h.total = align_up(h.off_psflags + (size_t)2 * TEM_MAX_RANKS * kMaxChannels * 8, 4096);
+    h.off_tsflags = h.off_psflags + (size_t)2 * TEM_MAX_RANKS * kMaxChannels * 8;
+    h.total = align_up(h.off_tsflags + (size_t)2 * TEM_MAX_RANKS * kMaxChannels * 8, 4096);
     return h;
 }
 
@@ -575,6 +577,9 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
         q.status = c->st_dev;
         q.spin_ns = kSpinNs;
         if (launch_ps(q, s) != cudaSuccess) return TEM_ERR_CUDA;
+    } else if (c->cfg.exchange == TEM_EXCHANGE_TWOSHOT) {  // NVSwitch two-shot (NEXT #3(i))
+        p.off_flags = (int64_t)c->hl.off_tsflags;
+        if (launch_twoshot(p, s) != cudaSuccess) return TEM_ERR_CUDA;
     } else if (launch_ring(p, s) != cudaSuccess) {
         return TEM_ERR_CUDA;
     }
@@ -751,6 +756,36 @@ tem_status ring_allreduce(tem_ctx* c, float* buf, int64_t K, int32_t op, void* s
     p.status = c->st_dev;
     p.spin_ns = kSpinNs;
     if (launch_ring(p, (cudaStream_t)stream) != cudaSuccess) return TEM_ERR_CUDA;
+    return TEM_OK;
+}
+
+tem_status twoshot_allreduce(tem_ctx* c, float* buf, int64_t K, int32_t op, void* stream) {
+    tem_status st = check_ctx(c);
+    if (st != TEM_OK) return st;
+    if (op != TEM_SUM && op != TEM_MEAN) return TEM_ERR_INVALID_ARG;
+    if (K < 1 || K > max_ar(&c->cfg)) return TEM_ERR_INVALID_ARG;
+    if ((char*)buf != (char*)c->peers[c->rank] + c->hl.off_user) return TEM_ERR_INVALID_ARG;
+    RingParams p;
+    memset(&p, 0, sizeof(p));
+    for (int l = 0; l < c->nlocal; ++l) {
+        float* ub = (float*)((char*)c->peers[c->rank + l] + c->hl.off_user);
+        p.loc[l] = ring_local(c, l, ub, ub, nullptr, nullptr);
+    }
+    p.N = c->N;
+    p.rank_base = c->rank;
+    p.nlocal = c->nlocal;
+    p.Kpad = roundup(K, 4 * (int64_t)c->N);
+    p.G = ar_channels(c, p.Kpad);
+    p.op = op;
+    p.mode = 0;
+    p.K = K;
+    p.off_dst = (int64_t)c->hl.off_user;
+    p.off_stage = -1;  // in place: the user region is the readable source
+    p.off_src = (int64_t)c->hl.off_user;
+    p.off_flags = (int64_t)c->hl.off_tsflags;
+    p.status = c->st_dev;
+    p.spin_ns = kSpinNs;
+    if (launch_twoshot(p, (cudaStream_t)stream) != cudaSuccess) return TEM_ERR_CUDA;
     return TEM_OK;
 }
 

@@ -21,7 +21,7 @@ TEM_OK, TEM_ERR_INVALID_ARG, TEM_ERR_PROTOCOL, TEM_ERR_TRANSPORT, TEM_ERR_CUDA, 
     TEM_ERR_NONFINITE, TEM_ERR_STATE = range(7)
 TEM_SUM, TEM_MEAN = 0, 1
 TEM_FP32, TEM_BF16 = 0, 1
-TEM_EXCHANGE_RING, TEM_EXCHANGE_PS = 0, 1
+TEM_EXCHANGE_RING, TEM_EXCHANGE_PS, TEM_EXCHANGE_TWOSHOT = 0, 1, 2
 MAX_RANKS = 8
 
 _P = ctypes.c_void_p
@@ -81,7 +81,7 @@ def lib():
         L.tem_step_host.argtypes = [_P, _P, _P, _P, _P]
         L.tem_exchange.restype = ctypes.c_int
         L.tem_exchange.argtypes = [_P, _P]
-        for f in (L.ring_allreduce, L.ps_allreduce):
+        for f in (L.ring_allreduce, L.ps_allreduce, L.twoshot_allreduce):
             f.restype = ctypes.c_int
             f.argtypes = [_P, _P, ctypes.c_int64, ctypes.c_int32, _P]
         L.tem_sync.restype = ctypes.c_int
@@ -120,7 +120,7 @@ EXPORTS = ["tem_num_params", "tem_kpad", "tem_workspace_bytes", "tem_sym_bytes",
            "tem_local_grad", "tem_logits", "tem_launches_per_step", "tem_launches_per_exchange",
            "tem_status_string", "tem_kernel_path", "tem_timing_slots", "tem_timing_slot_name",
            "tem_timing_begin", "tem_timing_end", "tem_relu_decisions", "tem_debug_buffer",
-           "tem_step_pem", "tem_compute_pem", "tem_pem_relu_decisions"]
+           "tem_step_pem", "tem_compute_pem", "tem_pem_relu_decisions", "twoshot_allreduce"]
 
 
 def status_string(code: int) -> str:
@@ -188,6 +188,10 @@ def ring_allreduce(ctx: int, buf_ptr: int, K: int, op: int = TEM_SUM, stream=Non
 
 def ps_allreduce(ctx: int, buf_ptr: int, K: int, op: int = TEM_SUM, stream=None):
     _check(lib().ps_allreduce(_P(ctx), _P(buf_ptr), int(K), int(op), _stream_ptr(stream)), "ps_allreduce")
+
+
+def twoshot_allreduce(ctx: int, buf_ptr: int, K: int, op: int = TEM_SUM, stream=None):
+    _check(lib().twoshot_allreduce(_P(ctx), _P(buf_ptr), int(K), int(op), _stream_ptr(stream)), "twoshot_allreduce")
 
 
 def tem_sync(ctx: int, stream=None):
@@ -387,6 +391,9 @@ class TemSession:
 
     def ps_allreduce(self, K: int, op: int = TEM_SUM, stream=None):
         ps_allreduce(self.ctx, self.user(0).data_ptr(), K, op, stream)
+
+    def twoshot_allreduce(self, K: int, op: int = TEM_SUM, stream=None):
+        twoshot_allreduce(self.ctx, self.user(0).data_ptr(), K, op, stream)
 
     def sync(self, stream=None):
         return tem_sync(self.ctx, stream)
