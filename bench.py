@@ -216,8 +216,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--lr", type=float, default=0.01)
-    ap.add_argument("--exchange", default="ring", choices=["ring", "ps"],
-                    help="gradient exchange: the paper's ring (default) or the PS comparator")
+    ap.add_argument("--exchange", default="ring", choices=["ring", "ps", "twoshot"],
+                    help="gradient exchange: the paper's ring (default), the PS comparator, or the "
+                         "NVSwitch two-shot (ring-identical bits, 2 phases)")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -249,7 +250,8 @@ def main():
     B, prec = wl["B"], wl["prec"]
     P = wl.get("pem", 0)
     sc = tem.SessionConfig(world_size=world, rank=rank, local_ranks=1, batch_per_rank=B, precision=prec,
-                           lr=args.lr, exchange=tem.TEM_EXCHANGE_PS if args.exchange == "ps" else tem.TEM_EXCHANGE_RING,
+                           lr=args.lr, exchange={"ps": tem.TEM_EXCHANGE_PS, "twoshot": tem.TEM_EXCHANGE_TWOSHOT}.get(
+                               args.exchange, tem.TEM_EXCHANGE_RING),
                            pem_proposals=P)
     t_init0 = time.perf_counter()
     params0 = datagen.init_params() if not P else np.concatenate([datagen.init_params(), datagen.init_pem_params()])
@@ -426,8 +428,9 @@ def main():
         "config": {"workload": wl["desc"], "batch_per_gpu": B, "global_batch": B * world, "seq_len": T,
                    "channels": "400->512->512->3", "parallelism": f"dp{world}",
                    "exchange": ("N=1: owner SGD only" if world == 1 else
-                                ("parameter server on rank 0 (KP1)" if args.exchange == "ps"
-                                 else "fused ring allreduce + mean + SGD (KR1)")),
+                                {"ps": "parameter server on rank 0 (KP1)",
+                                 "twoshot": "NVSwitch two-shot allreduce + mean + SGD (ring-identical bits)"}.get(
+                                     args.exchange, "fused ring allreduce + mean + SGD (KR1)")),
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",
                    "kernel_path": sess.kernel_path(),
                    **({"pem": f"{P} proposals/video, 32-d BSP features, MLP 32->512->1, gradient [TEM | PEM] "

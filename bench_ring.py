@@ -5,7 +5,8 @@
 
 For each message size S (64 KiB .. 256 MiB, plus the TEM gradient 5,613,580 B) it times, with
 CUDA events on each rank and the max over ranks:
-  * ours : ring_allreduce (KR1, P:126-158) of S/4 fp32 elements, Sum;
+  * ours : ring_allreduce (KR1) of S/4 fp32 elements, Sum; and the NVSwitch
+           two-shot (same result bits, 2 phases instead of 2(N-1) rounds);
   * ps   : the parameter-server comparator (P:115-124) at the TEM gradient size;
   * nccl : torch.distributed.all_reduce (NCCL), with whatever algorithm NCCL picks; run the
            script again with NCCL_ALGO=Ring for NCCL's ring.
@@ -85,6 +86,10 @@ def main():
         code, _ = sess.sync()
         assert code == 0, tem.status_string(code)
         out.append(("ours-ring", S, t))
+        t = timeit(lambda: sess.twoshot_allreduce(K, tem.TEM_SUM))
+        code, _ = sess.sync()
+        assert code == 0, tem.status_string(code)
+        out.append(("ours-twoshot", S, t))
         if S == TEM_BYTES:
             t = timeit(lambda: sess.ps_allreduce(K, tem.TEM_SUM))
             out.append(("ours-ps", S, t))
