@@ -70,6 +70,8 @@ def lib():
             L.orc_tem_fwd_bwd_ex.restype = i32
             L.orc_tem_fwd_bwd_ex.argtypes = [i32, i32, i32, i32, i32, i32, P, P, P, P, P, P, P,
                                              P, i64, ctypes.c_double, P, i64, P, P]
+            L.orc_ring_adam_f32.restype = i32
+            L.orc_ring_adam_f32.argtypes = [P, P, P, P, P, i32, i64, f32, f32, f32, f32]
             L.orc_pem_num_params.restype = i64
             L.orc_pem_num_params.argtypes = [i32, i32]
             L.orc_pem_fwd_bwd.restype = i32
@@ -201,6 +203,23 @@ def tem_fwd_bwd(x, params, labels, lam=(1.0, 1.0, 1.0), prec: int = 0, C: int = 
     n = int(nk[0])
     return {"loss": loss, "z": z, "grad": grad, "kinks": kinks[:min(n, kinks_cap)].copy(), "nkinks": n,
             "decisions": dec}
+
+
+def ring_adam(grads, params, m, v, scal, lr, beta1=0.9, beta2=0.999, eps=1e-8):
+    """Ring mean + Adam owner update (reading R22).  grads [N][K_pad] f32; params, m, v [K_pad]
+    f32 (one replica; every rank ends with the same params); scal [2] = (beta1^t, beta2^t) of the
+    previous step, updated in place.  Returns (params', m', v', scal')."""
+    g = np.ascontiguousarray(grads, dtype=np.float32)
+    N, Kp = g.shape
+    w = np.array(params, dtype=np.float32, copy=True)
+    mm = np.array(m, dtype=np.float32, copy=True)
+    vv = np.array(v, dtype=np.float32, copy=True)
+    sc = np.array(scal, dtype=np.float32, copy=True)
+    rc = lib().orc_ring_adam_f32(_ptr(g), _ptr(w), _ptr(mm), _ptr(vv), _ptr(sc), N, Kp, float(lr), float(beta1),
+                                 float(beta2), float(eps))
+    if rc:
+        raise ValueError("invalid ring_adam arguments")
+    return w, mm, vv, sc
 
 
 # --------------------------------------------------------------------------- PEM

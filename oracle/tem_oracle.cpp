@@ -188,6 +188,46 @@ int orc_ring_chain_f32(const float* grads, int N, int64_t K_pad, int op, float* 
     return 0;
 }
 
+// Ring allreduce fused with an Adam owner update (reading R22): the mean
+// gradient gbar of every element comes from the ring's chain (orc_ring_chain_f32), then, in
+// fp32 with every operation rounded once, in this order (t = this step, b1t = beta1^t and
+// b2t = beta2^t kept as running fp32 products, updated BEFORE use: b1t *= beta1, b2t *= beta2):
+//   m    = beta1 * m + (1 - beta1) * gbar          (products, then the sum)
+//   v    = beta2 * v + (1 - beta2) * (gbar * gbar)
+//   mhat = m / (1 - b1t),   vhat = v / (1 - b2t)
+//   w    = w - lr * (mhat / (sqrt(vhat) + eps))
+// (1 - beta1), (1 - beta2) are fp32 constants.  The optimizer state is sharded by ownership
+// on the GPU (the owner of a block holds its m, v); here it is one array.
+// scal: [b1t, b2t] in/out.  All replicas receive the same w.
+int orc_ring_adam_f32(const float* grads, float* params, float* m, float* v, float* scal, int N, int64_t K_pad,
+                      float lr, float beta1, float beta2, float eps) {
+    std::vector<float> gbar((size_t)K_pad);
+    const int rc = orc_ring_chain_f32(grads, N, K_pad, 1, gbar.data());
+    if (rc) return rc;
+    const float b1t = scal[0] * beta1, b2t = scal[1] * beta2;
+    scal[0] = b1t;
+    scal[1] = b2t;
+    const float c1 = 1.0f - beta1, c2 = 1.0f - beta2;
+    const float d1 = 1.0f - b1t, d2 = 1.0f - b2t;
+    for (int64_t e = 0; e < K_pad; ++e) {
+        const float g = gbar[(size_t)e];
+        const float a1 = beta1 * m[e];
+        const float a2 = c1 * g;
+        m[e] = a1 + a2;
+        const float gg = g * g;
+        const float q1 = beta2 * v[e];
+        const float q2 = c2 * gg;
+        v[e] = q1 + q2;
+        const float mhat = m[e] / d1;
+        const float vhat = v[e] / d2;
+        const float den = std::sqrt(vhat) + eps;
+        const float step = mhat / den;
+        const float upd = lr * step;
+        params[e] = params[e] - upd;
+    }
+    return 0;
+}
+
 // Parameter-server comparator ("accumulates all N buffers in
 // ascending-rank order").  out = ((g_0 + g_1) + g_2) + ... ; mean once.
 int orc_ps_allreduce_f32(const float* grads, int N, int64_t K, int op, float* out) {

@@ -210,3 +210,58 @@ def test_ps_ascending_order(orc):
     g[0] = w["big"]
     g[1] = -w["big"]
     assert np.all(orc.ps_allreduce(g) == 1.0)
+
+
+# ------------------------------------------------------------------ Adam owner update (R22)
+def _adam_ref64(gbar, w, m, v, b1t, b2t, lr, b1, b2, eps):
+    """Textbook Adam (Kingma & Ba, Alg. 1) in float64, for the tolerance pin."""
+    m = b1 * m + (1 - b1) * gbar
+    v = b2 * v + (1 - b2) * gbar * gbar
+    mhat = m / (1 - b1t)
+    vhat = v / (1 - b2t)
+    return w - lr * mhat / (np.sqrt(vhat) + eps), m, v
+
+
+def test_ring_adam_matches_textbook_adam(orc):
+    """Three steps of the oracle's fused ring mean + Adam vs textbook float64 Adam on the
+    float64 mean gradient: agreement within a few fp32 ulps of the update size."""
+    rng = np.random.default_rng(5)
+    N, K = 4, 4096
+    w = rng.standard_normal(K).astype(np.float32)
+    m = np.zeros(K, np.float32)
+    v = np.zeros(K, np.float32)
+    sc = np.ones(2, np.float32)
+    w64, m64, v64 = w.astype(np.float64), m.astype(np.float64), v.astype(np.float64)
+    lr, b1, b2, eps = 1e-3, 0.9, 0.999, 1e-8
+    for t in range(1, 4):
+        g = rng.standard_normal((N, K)).astype(np.float32)
+        w, m, v, sc = orc.ring_adam(g, w, m, v, sc, lr, b1, b2, eps)
+        gbar = g.astype(np.float64).mean(axis=0)
+        w64, m64, v64 = _adam_ref64(gbar, w64, m64, v64, b1 ** t, b2 ** t, lr, b1, b2, eps)
+        assert np.allclose(sc, [np.float32(b1) ** t, np.float32(b2) ** t], rtol=1e-6)
+        assert np.abs(w - w64).max() <= 1e-6 * max(1.0, np.abs(w64).max())
+        assert np.allclose(m, m64, rtol=1e-5, atol=1e-7)
+
+
+def test_ring_adam_first_step_is_sign_step(orc):
+    """Closed form at t = 1 from zero state: mhat = g, vhat = g^2, so w' = w - lr*g/(|g|+eps)
+    (= w - lr*sign(g) for |g| >> eps) -- Adam's first step."""
+    N, K = 2, 1000
+    g = np.random.default_rng(2).standard_normal((N, K)).astype(np.float32)
+    w = np.zeros(K, np.float32)
+    lr = 0.01
+    w1, _, _, _ = orc.ring_adam(g, w, np.zeros(K, np.float32), np.zeros(K, np.float32), np.ones(2, np.float32), lr)
+    gbar = g.astype(np.float64).mean(axis=0)
+    assert np.allclose(w1, -lr * gbar / (np.abs(gbar) + 1e-8), rtol=1e-5, atol=1e-9)
+
+
+def test_ring_adam_uses_ring_order_sum(orc):
+    """The gradient fed to Adam is the ring chain sum (order witness inputs, N = 3): with
+    lr = 0, beta1 = 0 the new m is exactly (1 - 0) * gbar = the ring's mean."""
+    N, K = 3, 6
+    big = np.float32(2.0 ** 25)
+    g = np.stack([np.full(K, big), np.full(K, -big), np.ones(K)]).astype(np.float32)
+    _, m, _, _ = orc.ring_adam(g, np.zeros(K, np.float32), np.zeros(K, np.float32), np.zeros(K, np.float32),
+                               np.ones(2, np.float32), 0.0, beta1=0.0)
+    expect, _ = orc.ring_allreduce(g, 1)
+    assert np.array_equal(m, expect[0])
