@@ -104,9 +104,17 @@ typedef struct {
     int32_t pem_proposals;  /* P proposals per video per step; 0 = TEM only                  */
     int32_t pem_features;   /* F: 32 (required when pem_proposals > 0)                       */
     int32_t pem_hidden;     /* H: 512 (required when pem_proposals > 0)                      */
+    /* --- optimizer of the owner update                                */
+    int32_t optimizer;      /* TEM_OPT_SGD (default: w = fma(-lr, gbar, w), R12) or TEM_OPT_ADAM
+                               (reading R22: m, v sharded by block ownership -- the owner of a
+                               block keeps its moments; bias correction by running fp32 products
+                               beta^t; every op single-rounded, so replicas stay bitwise equal
+                               and the result equals the oracle's orc_ring_adam_f32)            */
+    float beta1, beta2, eps; /* Adam: 0 <= beta < 1, eps > 0 (ignored for SGD)                */
 } tem_config;
 
 enum { TEM_EXCHANGE_RING = 0, TEM_EXCHANGE_PS = 1, TEM_EXCHANGE_TWOSHOT = 2 };
+enum { TEM_OPT_SGD = 0, TEM_OPT_ADAM = 1 };
 
 /* --- sizes -----------------------------------------------------------------------------
  * K      = c_hidden*3*c_in + c_hidden + c_hidden*3*c_hidden + c_hidden + 3*c_hidden + 3

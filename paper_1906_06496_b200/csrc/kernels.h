@@ -210,7 +210,18 @@ cudaError_t launch_head_reduce(const Geom& g, const RankBufs& b, const float lam
 cudaError_t launch_reduce_splits(const float* part, float* dst, int64_t n, int S, cudaStream_t s);
 
 // --- ring / exchange (ring.cu) --------------------------------------------------------
+// Owner update (tem_step exchanges): SGD, or Adam with per-rank moments (reading R22).
+struct OptCfg {
+    int kind;  // TEM_OPT_SGD / TEM_OPT_ADAM
+    float lr, beta1, beta2, c1, c2, eps;  // c1 = fl(1 - beta1), c2 = fl(1 - beta2)
+};
+struct OptState {
+    float* m;           // [K_pad] first moments (each rank touches only the blocks it owns)
+    float* v;           // [K_pad] second moments
+    const float* scal;  // [beta1^t, beta2^t] of this step (opt_scalars_kernel, before the exchange)
+};
 struct RingLocal {
+    OptState opt;
     const float* src;       // contribution of this rank (local grads, or the user buffer)
     float* dst_self;        // result on this rank (params, or the user buffer)
     __nv_bfloat16* shadow;  // bf16 copy of dst to refresh (operand weights) or nullptr
@@ -222,9 +233,9 @@ constexpr int kMaxChannels = 128;
 constexpr int kMaxChunks = 16;
 struct RingParams {
     RingLocal loc[TEM_MAX_RANKS];
-    int N, rank_base, nlocal, G, C, op, mode;  // mode 0 = allreduce, 1 = SGD
+    int N, rank_base, nlocal, G, C, op, mode;  // mode 0 = allreduce, 1 = optimizer step
     int64_t K, Kpad;
-    float lr;
+    OptCfg oc;
     int64_t off_dst, off_stage, off_flags;
     int64_t off_src;  // two-shot: heap offset of the source when it already lives in the heap
                       // (off_stage < 0), i.e. ring_allreduce's user region
@@ -237,14 +248,17 @@ cudaError_t launch_twoshot(const RingParams& p, cudaStream_t s);  // NVSwitch tw
 // (W1, b1), sum_s part2[s][e - off2] (W2), or grad[e] (the head-written entries); the same
 // ascending-s order as reduce_wgrad_kernel, so the result is bit-identical to the unfused path.
 cudaError_t launch_sgd_fused(float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo, int64_t n,
-                             float lr, const float* p1, int64_t stride1, int64_t n1, int S1, const float* p2,
-                             int64_t stride2, int64_t off2, int64_t n2, int S2, cudaStream_t s);
+                             const OptCfg& oc, const OptState& os, const float* p1, int64_t stride1, int64_t n1,
+                             int S1, const float* p2, int64_t stride2, int64_t off2, int64_t n2, int S2,
+                             cudaStream_t s);
 cudaError_t launch_sgd_single(const float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo,
-                              int64_t n, int op, float lr, cudaStream_t s);
+                              int64_t n, int op, const OptCfg& oc, const OptState& os, cudaStream_t s);
+// Adam: scal[0] *= beta1, scal[1] *= beta2 (fp32, once per step, before the exchange kernel).
+cudaError_t launch_opt_scalars(float* scal, float beta1, float beta2, cudaStream_t s);
 struct PsParams {
     RingLocal loc[TEM_MAX_RANKS];
-    int N, rank_base, nlocal, G, op, mode;  // mode 0 = allreduce, 1 = SGD (server updates)
-    float lr;
+    int N, rank_base, nlocal, G, op, mode;  // mode 0 = allreduce, 1 = optimizer step (server)
+    OptCfg oc;
     int64_t K;
     int64_t off_dst, off_slots, off_flags;
     Status* status;

@@ -101,6 +101,43 @@ TEM_DEV void store_shadow4(__nv_bfloat16* sh, __nv_bfloat16* sl, int64_t e, floa
     }
 }
 
+// The owner's optimizer step on 4 elements at e (tem_step exchanges, K = K_pad).
+//   SGD  (R12): w' = fma(-lr, g, w), one rounding.
+//   Adam (R22): m' = b1*m + c1*g; v' = b2*v + c2*(g*g); w' = w - lr*((m'/(1-b1^t)) /
+//               (sqrt(v'/(1-b2^t)) + eps)), every operation single-rounded (no contraction), in
+//               the oracle's order (orc_ring_adam_f32); the moments live in the owner's OptState.
+TEM_DEV float adam1(const OptCfg& o, float d1, float d2, float g, float& m, float& v, float w) {
+    m = __fadd_rn(__fmul_rn(o.beta1, m), __fmul_rn(o.c1, g));
+    v = __fadd_rn(__fmul_rn(o.beta2, v), __fmul_rn(o.c2, __fmul_rn(g, g)));
+    const float mhat = __fdiv_rn(m, d1), vhat = __fdiv_rn(v, d2);
+    const float step = __fdiv_rn(mhat, __fadd_rn(__fsqrt_rn(vhat), o.eps));
+    return __fsub_rn(w, __fmul_rn(o.lr, step));
+}
+TEM_DEV float4 owner_update(const OptCfg& o, const OptState& st, int64_t e, float4 g, float4 w) {
+    if (o.kind == TEM_OPT_ADAM) {
+        const float d1 = __fsub_rn(1.0f, st.scal[0]), d2 = __fsub_rn(1.0f, st.scal[1]);
+        float4 m = *reinterpret_cast<const float4*>(st.m + e), v = *reinterpret_cast<const float4*>(st.v + e);
+        float4 r;
+        r.x = adam1(o, d1, d2, g.x, m.x, v.x, w.x);
+        r.y = adam1(o, d1, d2, g.y, m.y, v.y, w.y);
+        r.z = adam1(o, d1, d2, g.z, m.z, v.z, w.z);
+        r.w = adam1(o, d1, d2, g.w, m.w, v.w, w.w);
+        *reinterpret_cast<float4*>(st.m + e) = m;
+        *reinterpret_cast<float4*>(st.v + e) = v;
+        return r;
+    }
+    return make_float4(__fmaf_rn(-o.lr, g.x, w.x), __fmaf_rn(-o.lr, g.y, w.y), __fmaf_rn(-o.lr, g.z, w.z),
+                       __fmaf_rn(-o.lr, g.w, w.w));
+}
+
+// Adam's running products beta^t (reading R22), one thread, before the step's update kernel.
+__global__ void opt_scalars_kernel(float* scal, float beta1, float beta2) {
+    pdl_trigger();
+    pdl_wait();
+    scal[0] = __fmul_rn(scal[0], beta1);
+    scal[1] = __fmul_rn(scal[1], beta2);
+}
+
 // Masked vector helpers for ring_allreduce with K < K_pad (elements >= K untouched).
 TEM_DEV float4 ld4_masked(const float* p, int64_t e, int64_t K) {
     if (e + 4 <= K) return *reinterpret_cast<const float4*>(p + e);
@@ -197,11 +234,7 @@ __global__ void __launch_bounds__(RING_THREADS) ring_kernel(const __grid_constan
                 }
                 float4 out = a;
                 if (P.mode == 1) {
-                    const float4 w = *reinterpret_cast<const float4*>(dst_self + e);
-                    out.x = __fmaf_rn(-P.lr, a.x, w.x);
-                    out.y = __fmaf_rn(-P.lr, a.y, w.y);
-                    out.z = __fmaf_rn(-P.lr, a.z, w.z);
-                    out.w = __fmaf_rn(-P.lr, a.w, w.w);
+                    out = owner_update(P.oc, L.opt, e, a, *reinterpret_cast<const float4*>(dst_self + e));
                     if (L.shadow) store_shadow4(L.shadow, L.shadow_lo, e, out);
                 }
                 st4_masked(dst_self, e, K, out);
@@ -308,11 +341,7 @@ __global__ void __launch_bounds__(RING_THREADS) twoshot_kernel(const __grid_cons
         }
         float4 out = a;
         if (P.mode == 1) {
-            const float4 w = *reinterpret_cast<const float4*>(L.dst_self + e);
-            out.x = __fmaf_rn(-P.lr, a.x, w.x);
-            out.y = __fmaf_rn(-P.lr, a.y, w.y);
-            out.z = __fmaf_rn(-P.lr, a.z, w.z);
-            out.w = __fmaf_rn(-P.lr, a.w, w.w);
+            out = owner_update(P.oc, L.opt, e, a, *reinterpret_cast<const float4*>(L.dst_self + e));
             if (L.shadow) store_shadow4(L.shadow, L.shadow_lo, e, out);
         }
         for (int r = 0; r < N; ++r) st4_masked(reinterpret_cast<float*>(heap(r) + P.off_dst), e, K, out);
@@ -338,7 +367,7 @@ __global__ void __launch_bounds__(RING_THREADS) twoshot_kernel(const __grid_cons
 // N = 1: the ring is the identity; the owner update alone.
 __global__ void sgd_single_kernel(const float* __restrict__ g, float* __restrict__ w,
                                   __nv_bfloat16* __restrict__ shadow, __nv_bfloat16* __restrict__ shadow_lo,
-                                  int64_t n, int op, float lr) {
+                                  int64_t n, int op, OptCfg oc, OptState os) {
     trace_begin(SLOT_EXCHANGE);
     pdl_trigger();
     pdl_wait();
@@ -349,11 +378,7 @@ __global__ void sgd_single_kernel(const float* __restrict__ g, float* __restrict
         if (op == TEM_MEAN) {  // fl(1/1) = 1: a * 1 is exact
             a.x = a.x * 1.0f; a.y = a.y * 1.0f; a.z = a.z * 1.0f; a.w = a.w * 1.0f;
         }
-        float4 x = reinterpret_cast<float4*>(w)[v];
-        x.x = __fmaf_rn(-lr, a.x, x.x);
-        x.y = __fmaf_rn(-lr, a.y, x.y);
-        x.z = __fmaf_rn(-lr, a.z, x.z);
-        x.w = __fmaf_rn(-lr, a.w, x.w);
+        const float4 x = owner_update(oc, os, 4 * v, a, reinterpret_cast<float4*>(w)[v]);
         reinterpret_cast<float4*>(w)[v] = x;
         if (shadow) store_shadow4(shadow, shadow_lo, 4 * v, x);
     }
@@ -361,7 +386,7 @@ __global__ void sgd_single_kernel(const float* __restrict__ g, float* __restrict
 }
 
 __global__ void sgd_fused_kernel(float* __restrict__ g, float* __restrict__ w, __nv_bfloat16* __restrict__ shadow,
-                                 __nv_bfloat16* __restrict__ shadow_lo, int64_t n, float lr,
+                                 __nv_bfloat16* __restrict__ shadow_lo, int64_t n, OptCfg oc, OptState os,
                                  const float* __restrict__ p1, int64_t stride1, int64_t n1, int S1,
                                  const float* __restrict__ p2, int64_t stride2, int64_t off2, int64_t n2, int S2) {
     trace_begin(SLOT_EXCHANGE);
@@ -395,11 +420,7 @@ __global__ void sgd_fused_kernel(float* __restrict__ g, float* __restrict__ w, _
             a = reinterpret_cast<const float4*>(g)[v];
         }
         // TEM_MEAN at N = 1: a * fl(1/1) is exact
-        float4 x = reinterpret_cast<float4*>(w)[v];
-        x.x = __fmaf_rn(-lr, a.x, x.x);
-        x.y = __fmaf_rn(-lr, a.y, x.y);
-        x.z = __fmaf_rn(-lr, a.z, x.z);
-        x.w = __fmaf_rn(-lr, a.w, x.w);
+        const float4 x = owner_update(oc, os, e, a, reinterpret_cast<float4*>(w)[v]);
         reinterpret_cast<float4*>(w)[v] = x;
         if (shadow) store_shadow4(shadow, shadow_lo, e, x);
     }
@@ -456,13 +477,8 @@ __global__ void __launch_bounds__(RING_THREADS) ps_kernel(const __grid_constant_
             if (P.op == TEM_MEAN) {
                 a.x = a.x * inv_n; a.y = a.y * inv_n; a.z = a.z * inv_n; a.w = a.w * inv_n;
             }
-            if (P.mode == 1) {  // the server holds and upgrades the weights: w' = w - lr*gbar
-                const float4 w = *reinterpret_cast<const float4*>(L.dst_self + e);
-                a.x = __fmaf_rn(-P.lr, a.x, w.x);
-                a.y = __fmaf_rn(-P.lr, a.y, w.y);
-                a.z = __fmaf_rn(-P.lr, a.z, w.z);
-                a.w = __fmaf_rn(-P.lr, a.w, w.w);
-            }
+            if (P.mode == 1)  // the server holds and upgrades the weights
+                a = owner_update(P.oc, L.opt, e, a, *reinterpret_cast<const float4*>(L.dst_self + e));
             for (int r = 0; r < N; ++r)  // downlink broadcast (gbar, or w' in SGD mode)
                 st4_masked(reinterpret_cast<float*>(L.heaps[r] + P.off_dst), e, K, a);
         }
@@ -498,17 +514,22 @@ cudaError_t launch_ring(const RingParams& p, cudaStream_t s) {
 }
 
 cudaError_t launch_sgd_single(const float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo,
-                              int64_t n, int op, float lr, cudaStream_t s) {
-    return launch_pdl(sgd_single_kernel, dim3(296), dim3(512), 0, s, false, g, w, shadow, shadow_lo, n, op, lr);
+                              int64_t n, int op, const OptCfg& oc, const OptState& os, cudaStream_t s) {
+    return launch_pdl(sgd_single_kernel, dim3(296), dim3(512), 0, s, false, g, w, shadow, shadow_lo, n, op, oc, os);
+}
+
+cudaError_t launch_opt_scalars(float* scal, float beta1, float beta2, cudaStream_t s) {
+    return launch_pdl(opt_scalars_kernel, dim3(1), dim3(1), 0, s, false, scal, beta1, beta2);
 }
 
 void trace_set_ring(unsigned long long* p) { cudaMemcpyToSymbol(g_trace, &p, sizeof(p)); }
 
 cudaError_t launch_sgd_fused(float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo, int64_t n,
-                             float lr, const float* p1, int64_t stride1, int64_t n1, int S1, const float* p2,
-                             int64_t stride2, int64_t off2, int64_t n2, int S2, cudaStream_t s) {
-    return launch_pdl(sgd_fused_kernel, dim3(296), dim3(512), 0, s, false, g, w, shadow, shadow_lo, n, lr, p1, stride1,
-                      n1, S1, p2, stride2, off2, n2, S2);
+                             const OptCfg& oc, const OptState& os, const float* p1, int64_t stride1, int64_t n1,
+                             int S1, const float* p2, int64_t stride2, int64_t off2, int64_t n2, int S2,
+                             cudaStream_t s) {
+    return launch_pdl(sgd_fused_kernel, dim3(296), dim3(512), 0, s, false, g, w, shadow, shadow_lo, n, oc, os, p1,
+                      stride1, n1, S1, p2, stride2, off2, n2, S2);
 }
 
 cudaError_t launch_twoshot(const RingParams& p, cudaStream_t s) {

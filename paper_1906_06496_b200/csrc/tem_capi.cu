@@ -59,7 +59,7 @@ struct HeapLayout {
 
 struct WsLayout {
     size_t xp, h1, h2, dA2, dA1, xp_lo, h1_lo, dA2_lo, dA1_lo, z, grad, headpart, headlvl1, counter, bpart, wpart, wpart2, shadow,
-        shadow_lo, ones, zpart, epochs, stepctr, xstage, labstage, lossstage, pempart, pemdec, per_rank;
+        shadow_lo, ones, zpart, epochs, stepctr, xstage, labstage, lossstage, pempart, pemdec, opt_m, opt_v, opt_scal, per_rank;
 };
 
 bool cfg_valid(const tem_config* c) {
@@ -82,6 +82,11 @@ bool cfg_valid(const tem_config* c) {
         return false;
     if (c->pem_proposals < 0) return false;
     if (c->pem_proposals > 0 && (c->pem_features != 32 || c->pem_hidden != 512)) return false;  // kernel shape
+    if (c->optimizer != TEM_OPT_SGD && c->optimizer != TEM_OPT_ADAM) return false;
+    if (c->optimizer == TEM_OPT_ADAM &&
+        !(c->beta1 >= 0.0f && c->beta1 < 1.0f && c->beta2 >= 0.0f && c->beta2 < 1.0f && c->eps > 0.0f &&
+          isfinite(c->eps)))
+        return false;
     return true;
 }
 
@@ -194,6 +199,10 @@ WsLayout ws_layout(const tem_config* c) {
     w.xstage = take((size_t)g.B * g.T * g.Cin * xsz);
     w.labstage = take((size_t)g.B * 3 * g.T * 4);
     w.lossstage = take(4 * 4);
+    const size_t adam = c->optimizer == TEM_OPT_ADAM ? 1 : 0;  // reading R22
+    w.opt_m = take(adam * (size_t)g.Kpad * 4);
+    w.opt_v = take(adam * (size_t)g.Kpad * 4);
+    w.opt_scal = take(adam * 8);
     w.per_rank = o;
     return w;
 }
@@ -406,6 +415,10 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
         c->plan[l] = nullptr;
         c->epochs[l] = (uint32_t*)(base + wl.epochs);
         cudaError_t e = cudaMemsetAsync(base, 0, wl.per_rank, 0);
+        if (e == cudaSuccess && cfg->optimizer == TEM_OPT_ADAM) {  // beta^0 = 1 (reading R22)
+            static const float one2[2] = {1.0f, 1.0f};
+            e = cudaMemcpy(base + wl.opt_scal, one2, sizeof(one2), cudaMemcpyHostToDevice);
+        }
         if (e == cudaSuccess && b.shadow) e = launch_cast_shadow_split(b.params, b.shadow, b.shadow_lo, c->g.Kpad, 0);
         if (e == cudaSuccess && b.ones) e = launch_fill_ones(b.ones, c->g.R, 0);
         if (e == cudaSuccess && c->g.path == PATH_UMMA) {
@@ -501,9 +514,44 @@ static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, f
     return TEM_OK;
 }
 
+static OptCfg opt_cfg(const tem_ctx* c) {
+    OptCfg o;
+    o.kind = c->cfg.optimizer;
+    o.lr = c->cfg.lr;
+    o.beta1 = c->cfg.beta1;
+    o.beta2 = c->cfg.beta2;
+    o.c1 = 1.0f - c->cfg.beta1;  // fp32 subtraction (the oracle's c1)
+    o.c2 = 1.0f - c->cfg.beta2;
+    o.eps = c->cfg.eps;
+    return o;
+}
+
+static OptState opt_state(const tem_ctx* c, int l) {
+    OptState o{nullptr, nullptr, nullptr};
+    if (c->cfg.optimizer == TEM_OPT_ADAM) {
+        o.m = (float*)(c->ws_base[l] + c->wl.opt_m);
+        o.v = (float*)(c->ws_base[l] + c->wl.opt_v);
+        o.scal = (const float*)(c->ws_base[l] + c->wl.opt_scal);
+    }
+    return o;
+}
+
+// Adam: advance every local rank's beta^t before the update reads it
+static tem_status opt_scalars(tem_ctx* c, cudaStream_t s, int* nl) {
+    if (c->cfg.optimizer != TEM_OPT_ADAM) return TEM_OK;
+    for (int l = 0; l < c->nlocal; ++l) {
+        if (launch_opt_scalars((float*)(c->ws_base[l] + c->wl.opt_scal), c->cfg.beta1, c->cfg.beta2, s) !=
+            cudaSuccess)
+            return TEM_ERR_CUDA;
+        ++*nl;
+    }
+    return TEM_OK;
+}
+
 static RingLocal ring_local(tem_ctx* c, int l, const float* src, float* dst, __nv_bfloat16* shadow,
                             __nv_bfloat16* shadow_lo) {
     RingLocal L;
+    L.opt = opt_state(c, l);
     L.src = src;
     L.dst_self = dst;
     L.shadow = shadow;
@@ -517,12 +565,14 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
     const Geom& g = c->g;
     const EvRec rec{timing_slot_events(c), s};
     rec.begin(SLOT_EXCHANGE);
-    tem_status st = TEM_OK;
+    tem_status st = opt_scalars(c, s, nl);
+    if (st != TEM_OK) return st;
+    const OptCfg oc = opt_cfg(c);
     if (c->N == 1 && c->reduce_deferred) {  // tem_step: split-K reductions fused into the update
         const RankBufs& b = c->rb[0];
         const UmmaPlan& P = *c->plan[0];
         c->reduce_deferred = false;
-        if (launch_sgd_fused(b.grad, (float*)b.params, b.shadow, b.shadow_lo, g.Kpad, c->cfg.lr, b.wpart,
+        if (launch_sgd_fused(b.grad, (float*)b.params, b.shadow, b.shadow_lo, g.Kpad, oc, opt_state(c, 0), b.wpart,
                              P.wgrad1.part_stride, g.off_W2, P.S1, b.wpart2, P.wgrad2.part_stride, g.off_W2,
                              (int64_t)3 * g.C * g.C, P.S2, s) != cudaSuccess)
             return TEM_ERR_CUDA;
@@ -533,7 +583,7 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
     if (c->N == 1) {
         for (int l = 0; l < c->nlocal; ++l) {
             if (launch_sgd_single(c->rb[l].grad, (float*)c->rb[l].params, c->rb[l].shadow, c->rb[l].shadow_lo, g.Kpad,
-                                  TEM_MEAN, c->cfg.lr, s) != cudaSuccess)
+                                  TEM_MEAN, oc, opt_state(c, l), s) != cudaSuccess)
                 return TEM_ERR_CUDA;
             ++*nl;
         }
@@ -553,7 +603,7 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
     p.mode = 1;
     p.K = g.Kpad;
     p.Kpad = g.Kpad;
-    p.lr = c->cfg.lr;
+    p.oc = oc;
     p.off_dst = 0;
     p.off_stage = (int64_t)c->hl.off_stage;
     p.off_flags = (int64_t)c->hl.off_flags;
@@ -569,7 +619,7 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
         q.G = c->G;
         q.op = TEM_MEAN;
         q.mode = 1;
-        q.lr = c->cfg.lr;
+        q.oc = oc;
         q.K = g.Kpad;
         q.off_dst = 0;
         q.off_slots = (int64_t)c->hl.off_ps;
@@ -749,7 +799,6 @@ tem_status ring_allreduce(tem_ctx* c, float* buf, int64_t K, int32_t op, void* s
     p.op = op;
     p.mode = 0;
     p.K = K;
-    p.lr = 0.f;
     p.off_dst = (int64_t)c->hl.off_user;
     p.off_stage = (int64_t)c->hl.off_stage;
     p.off_flags = (int64_t)c->hl.off_flags;

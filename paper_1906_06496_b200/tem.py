@@ -22,6 +22,7 @@ TEM_OK, TEM_ERR_INVALID_ARG, TEM_ERR_PROTOCOL, TEM_ERR_TRANSPORT, TEM_ERR_CUDA, 
 TEM_SUM, TEM_MEAN = 0, 1
 TEM_FP32, TEM_BF16 = 0, 1
 TEM_EXCHANGE_RING, TEM_EXCHANGE_PS, TEM_EXCHANGE_TWOSHOT = 0, 1, 2
+TEM_OPT_SGD, TEM_OPT_ADAM = 0, 1
 MAX_RANKS = 8
 
 _P = ctypes.c_void_p
@@ -41,6 +42,7 @@ class tem_config(ctypes.Structure):
         ("ring_channels", ctypes.c_int32), ("ring_chunks", ctypes.c_int32),
         ("exchange", ctypes.c_int32),
         ("pem_proposals", ctypes.c_int32), ("pem_features", ctypes.c_int32), ("pem_hidden", ctypes.c_int32),
+        ("optimizer", ctypes.c_int32), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float), ("eps", ctypes.c_float),
     ]
 
 
@@ -225,6 +227,10 @@ class SessionConfig:
     pem_proposals: int = 0  # > 0: joint TEM + PEM (configs[4]); params = [TEM | PEM]
     pem_features: int = 32
     pem_hidden: int = 512
+    optimizer: int = TEM_OPT_SGD  # TEM_OPT_ADAM: owner-side Adam (reading R22)
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
 
 
 class TemSession:
@@ -252,6 +258,7 @@ class TemSession:
         cfg.ring_channels, cfg.ring_chunks = sc.ring_channels, sc.ring_chunks
         cfg.exchange = sc.exchange
         cfg.pem_proposals, cfg.pem_features, cfg.pem_hidden = sc.pem_proposals, sc.pem_features, sc.pem_hidden
+        cfg.optimizer, cfg.beta1, cfg.beta2, cfg.eps = sc.optimizer, sc.beta1, sc.beta2, sc.eps
         self.K = tem_num_params(cfg)
         if self.K == 0:
             raise TemError(TEM_ERR_INVALID_ARG, "config")

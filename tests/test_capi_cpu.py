@@ -67,6 +67,27 @@ def test_invalid_configs_rejected(field, value):
     assert not ctx.value
 
 
+@pytest.mark.parametrize("fields", [dict(optimizer=2), dict(optimizer=1, beta1=1.0, beta2=0.999, eps=1e-8),
+                                    dict(optimizer=1, beta1=0.9, beta2=-0.1, eps=1e-8),
+                                    dict(optimizer=1, beta1=0.9, beta2=0.999, eps=0.0)])
+def test_invalid_optimizer_rejected(fields):
+    from paper_1906_06496_b200 import tem
+    c = base_cfg(tem)
+    for k, v in fields.items():
+        setattr(c, k, v)
+    assert tem.tem_num_params(c) == 0
+
+
+def test_adam_workspace_holds_moments():
+    """Adam adds m and v ([K_pad] fp32 each) and beta^t to every rank's workspace (reading R22)."""
+    from paper_1906_06496_b200 import tem
+    c = base_cfg(tem, 2)
+    sgd = tem.tem_workspace_bytes(c)
+    c.optimizer, c.beta1, c.beta2, c.eps = tem.TEM_OPT_ADAM, 0.9, 0.999, 1e-8
+    assert tem.tem_num_params(c) == 1403395
+    assert tem.tem_workspace_bytes(c) - sgd >= 2 * 4 * tem.tem_kpad(c, 1403395)
+
+
 def test_null_context_calls():
     from paper_1906_06496_b200 import tem
     L = tem.lib()
