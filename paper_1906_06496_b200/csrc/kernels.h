@@ -144,6 +144,7 @@ struct UmmaPlan {
     int S1, S2;  // split-K factors of conv1 / conv2 wgrad (<= S, the workspace's)
     cudaStream_t aux;         // second stream: conv2 wgrad runs beside conv2 dgrad / conv1 wgrad
     cudaEvent_t fork, join;
+    cudaEvent_t dgrad_done;   // N = 1 split update: the W2.. range starts once conv2 dgrad has read W2
     cudaStream_t pem;         // third stream: the PEM (configs[4]) beside the whole TEM step
     cudaEvent_t pem_fork, pem_join;
     bool pem_pending;         // a PEM launch on `pem` awaits its join before the exchange
@@ -168,7 +169,8 @@ cudaError_t launch_relu_decisions(const Geom& g, const RankBufs& b, uint8_t* out
 // Kernel slots of one step (for tem_timing_*): every launch is bracketed by
 // ev[2*slot] / ev[2*slot+1] when ev != nullptr.
 enum Slot { SLOT_PREP = 0, SLOT_CONV1, SLOT_CONV2, SLOT_HEAD, SLOT_HEADFIN, SLOT_DGRAD, SLOT_WGRAD2,
-            SLOT_RED2, SLOT_WGRAD1, SLOT_RED1, SLOT_EXCHANGE, SLOT_PEM, SLOT_PEMRED, NUM_SLOTS };
+            SLOT_RED2, SLOT_WGRAD1, SLOT_RED1, SLOT_EXCHANGE, SLOT_PEM, SLOT_PEMRED, SLOT_EXCH2,
+            NUM_SLOTS };
 const char* slot_name(int slot);
 // kernel-span trace buffers (diagnostics): one setter per translation unit with traced kernels
 void trace_set_umma(unsigned long long* p);
@@ -186,10 +188,13 @@ cudaError_t simt_compute(const Geom& g, const RankBufs& b, const float* labels,
                          const EvRec& rec, cudaStream_t s);
 // defer_reduce: skip the two split-K reductions; the N = 1 exchange sums the partials itself
 // (launch_sgd_fused) -- used by tem_step only, so tem_compute still leaves the full gradient.
+// split: (defer_reduce only) also apply the owner update to [off_W2, K_pad) on the side branch
+// once conv2 dgrad is done, beside conv1 wgrad; the exchange then updates [0, off_W2) only.
+struct SplitUpdate;
 cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, const float* labels,
                          const float lam[3], float* loss_out, Status* status, int* nlaunch,
                          const EvRec& rec, cudaStream_t s, bool defer_reduce = false,
-                         float* loss_host = nullptr);
+                         float* loss_host = nullptr, const SplitUpdate* split = nullptr);
 // head (conv3 + sigmoid + loss + dz + dA2) and its deterministic finalisation (rows a3-a5);
 // writes dA2 as b.dA2 (+ b.dA2_lo when present) in the operand type of the path.
 cudaError_t launch_head(const Geom& g, const RankBufs& b, const float* labels, const float lam[3],
@@ -202,7 +207,7 @@ int pem_ctas(const Geom& g);
 // pem_kernel runs on `s`; pem_reduce on `s_red` (forked from `s` through `fork` when they differ).
 cudaError_t launch_pem(const Geom& g, const float* f, const float* iou, const float* params, float* part,
                        float* grad, float* loss_out, Status* status, const int64_t* stepctr, uint8_t* dec_out,
-                       cudaStream_t s, cudaStream_t s_red, cudaEvent_t fork, int* n);
+                       cudaStream_t s, cudaStream_t s_red, cudaEvent_t fork, int* n, const EvRec& rec);
 cudaError_t launch_head_reduce_rows(const Geom& g, const RankBufs& b, int nrows, const float lam[3],
                                    float* loss_out, Status* status, const EvRec& rec, cudaStream_t s, int* n);
 cudaError_t launch_head_reduce(const Geom& g, const RankBufs& b, const float lam[3], float* loss_out,
@@ -219,6 +224,10 @@ struct OptState {
     float* m;           // [K_pad] first moments (each rank touches only the blocks it owns)
     float* v;           // [K_pad] second moments
     const float* scal;  // [beta1^t, beta2^t] of this step (opt_scalars_kernel, before the exchange)
+};
+struct SplitUpdate {
+    OptCfg oc;
+    OptState os;
 };
 struct RingLocal {
     OptState opt;
@@ -247,10 +256,12 @@ cudaError_t launch_twoshot(const RingParams& p, cudaStream_t s);  // NVSwitch tw
 // N = 1 owner update with the deferred split-K reductions fused in: grad[e] = sum_s part1[s][e]
 // (W1, b1), sum_s part2[s][e - off2] (W2), or grad[e] (the head-written entries); the same
 // ascending-s order as reduce_wgrad_kernel, so the result is bit-identical to the unfused path.
-cudaError_t launch_sgd_fused(float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo, int64_t n,
-                             const OptCfg& oc, const OptState& os, const float* p1, int64_t stride1, int64_t n1,
+// Owner update of elements [e0, e1) at N = 1 with the split-K partial sums fused (p1 covers
+// [0, n1), p2 covers [off2, off2 + n2)); e0, e1 multiples of 4.
+cudaError_t launch_sgd_fused(float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo, int64_t e0,
+                             int64_t e1, const OptCfg& oc, const OptState& os, const float* p1, int64_t stride1, int64_t n1,
                              int S1, const float* p2, int64_t stride2, int64_t off2, int64_t n2, int S2,
-                             cudaStream_t s);
+                             cudaStream_t s, bool side = false, int ctas = 0);
 cudaError_t launch_sgd_single(const float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo,
                               int64_t n, int op, const OptCfg& oc, const OptState& os, cudaStream_t s);
 // Adam: scal[0] *= beta1, scal[1] *= beta2 (fp32, once per step, before the exchange kernel).

@@ -180,7 +180,7 @@ int pem_ctas(const Geom& g) {
 
 cudaError_t launch_pem(const Geom& g, const float* f, const float* iou, const float* params, float* part,
                        float* grad, float* loss_out, Status* status, const int64_t* stepctr, uint8_t* dec_out,
-                       cudaStream_t s, cudaStream_t s_red, cudaEvent_t fork, int* n) {
+                       cudaStream_t s, cudaStream_t s_red, cudaEvent_t fork, int* n, const EvRec& rec) {
     const int M = g.B * g.pem_P;
     const int G = pem_ctas(g);
     if (G == 0) {
@@ -198,16 +198,20 @@ cudaError_t launch_pem(const Geom& g, const float* f, const float* iou, const fl
         if (ea != cudaSuccess) return ea;
         attr = true;
     }
+    rec.begin(SLOT_PEM);
     cudaError_t e = launch_pdl(pem_kernel, dim3(G), dim3(PEM_THREADS), W1S, s, false, f, iou, params, M, rows, part,
                                dec_out);
+    rec.end(SLOT_PEM);
     if (e != cudaSuccess) return e;
     ++*n;
     if (s_red != s && fork &&
         (cudaEventRecord(fork, s) != cudaSuccess || cudaStreamWaitEvent(s_red, fork, 0) != cudaSuccess))
         return cudaErrorUnknown;
     const int KP = (int)pem_num_params_of(g);
+    rec.begin(SLOT_PEMRED);
     e = launch_pdl(pem_reduce_kernel, dim3((KP + 1 + 255) / 256), dim3(256), 0, s_red, true, (const float*)part, G, M, grad,
                    loss_out, status, stepctr);
+    rec.end(SLOT_PEMRED);
     if (e == cudaSuccess) ++*n;
     return e;
 }

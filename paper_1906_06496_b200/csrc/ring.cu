@@ -28,6 +28,7 @@
 // cooperative launch, "peer" heaps on the same device).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+#include <algorithm>
 
 #include "kernels.h"
 
@@ -105,7 +106,8 @@ TEM_DEV void store_shadow4(__nv_bfloat16* sh, __nv_bfloat16* sl, int64_t e, floa
 //   SGD  (R12): w' = fma(-lr, g, w), one rounding.
 //   Adam (R22): m' = b1*m + c1*g; v' = b2*v + c2*(g*g); w' = w - lr*((m'/(1-b1^t)) /
 //               (sqrt(v'/(1-b2^t)) + eps)), every operation single-rounded (no contraction), in
-//               the oracle's order (orc_ring_adam_f32); the moments live in the owner's OptState.
+//               the oracle's order (orc_ring_adam_f32); the moments live in the owner's OptState;
+//               scal holds beta^(t-1) during the step.
 TEM_DEV float adam1(const OptCfg& o, float d1, float d2, float g, float& m, float& v, float w) {
     m = __fadd_rn(__fmul_rn(o.beta1, m), __fmul_rn(o.c1, g));
     v = __fadd_rn(__fmul_rn(o.beta2, v), __fmul_rn(o.c2, __fmul_rn(g, g)));
@@ -113,9 +115,14 @@ TEM_DEV float adam1(const OptCfg& o, float d1, float d2, float g, float& m, floa
     const float step = __fdiv_rn(mhat, __fadd_rn(__fsqrt_rn(vhat), o.eps));
     return __fsub_rn(w, __fmul_rn(o.lr, step));
 }
+// KIND = -1: chosen at run time from o.kind; TEM_OPT_SGD / TEM_OPT_ADAM: fixed at compile time
+template <int KIND = -1>
 TEM_DEV float4 owner_update(const OptCfg& o, const OptState& st, int64_t e, float4 g, float4 w) {
-    if (o.kind == TEM_OPT_ADAM) {
-        const float d1 = __fsub_rn(1.0f, st.scal[0]), d2 = __fsub_rn(1.0f, st.scal[1]);
+    if (KIND == TEM_OPT_ADAM || (KIND < 0 && o.kind == TEM_OPT_ADAM)) {
+        // this step's beta^t = fl(beta^(t-1) * beta): every thread forms the same product; the
+        // stored pair advances after the step's last update (opt_scalars_kernel)
+        const float d1 = __fsub_rn(1.0f, __fmul_rn(st.scal[0], o.beta1));
+        const float d2 = __fsub_rn(1.0f, __fmul_rn(st.scal[1], o.beta2));
         float4 m = *reinterpret_cast<const float4*>(st.m + e), v = *reinterpret_cast<const float4*>(st.v + e);
         float4 r;
         r.x = adam1(o, d1, d2, g.x, m.x, v.x, w.x);
@@ -130,7 +137,7 @@ TEM_DEV float4 owner_update(const OptCfg& o, const OptState& st, int64_t e, floa
                        __fmaf_rn(-o.lr, g.w, w.w));
 }
 
-// Adam's running products beta^t (reading R22), one thread, before the step's update kernel.
+// Adam's running products beta^t (reading R22), one thread, after the step's update kernels.
 __global__ void opt_scalars_kernel(float* scal, float beta1, float beta2) {
     pdl_trigger();
     pdl_wait();
@@ -385,15 +392,18 @@ __global__ void sgd_single_kernel(const float* __restrict__ g, float* __restrict
     trace_end(SLOT_EXCHANGE);
 }
 
-__global__ void sgd_fused_kernel(float* __restrict__ g, float* __restrict__ w, __nv_bfloat16* __restrict__ shadow,
-                                 __nv_bfloat16* __restrict__ shadow_lo, int64_t n, OptCfg oc, OptState os,
+template <int KIND>
+__global__ void __launch_bounds__(512) sgd_fused_kernel(float* __restrict__ g, float* __restrict__ w, __nv_bfloat16* __restrict__ shadow,
+                                 __nv_bfloat16* __restrict__ shadow_lo, int64_t e0, int64_t e1, OptCfg oc,
+                                 OptState os,
                                  const float* __restrict__ p1, int64_t stride1, int64_t n1, int S1,
                                  const float* __restrict__ p2, int64_t stride2, int64_t off2, int64_t n2, int S2) {
-    trace_begin(SLOT_EXCHANGE);
+    const int slot = e0 > 0 ? SLOT_EXCH2 : SLOT_EXCHANGE;  // the split update's W2.. range
+    trace_begin(slot);
     pdl_trigger();
     pdl_wait();
-    const int64_t nv = n / 4;
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv;
+    const int64_t nv = e1 / 4;
+    for (int64_t v = e0 / 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nv;
          v += (int64_t)gridDim.x * blockDim.x) {
         const int64_t e = 4 * v;
         const float* src = nullptr;
@@ -408,23 +418,36 @@ __global__ void sgd_fused_kernel(float* __restrict__ g, float* __restrict__ w, _
             stride = stride2;
             S = S2;
         }
+        // every load of the element group is issued before the first use (one memory latency
+        // per iteration): the weights, then up to 4 partials unrolled
+        const float4 wv = reinterpret_cast<const float4*>(w)[v];
         float4 a;
-        if (src) {  // split-K partials, ascending s (as reduce_wgrad_kernel)
-            a = __ldcs(reinterpret_cast<const float4*>(src));
-            for (int s = 1; s < S; ++s) {
-                const float4 b = __ldcs(reinterpret_cast<const float4*>(src + (size_t)s * stride));
-                a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+        if (src) {  // split-K partials, summed in ascending s (as reduce_wgrad_kernel)
+            constexpr int SU = 4;
+            float4 p[SU];
+#pragma unroll
+            for (int s = 0; s < SU; ++s)
+                if (s < S) p[s] = __ldcs(reinterpret_cast<const float4*>(src + (size_t)s * stride));
+            a = p[0];
+#pragma unroll
+            for (int s = 1; s < SU; ++s)
+                if (s < S) {
+                    a.x += p[s].x; a.y += p[s].y; a.z += p[s].z; a.w += p[s].w;
+                }
+            for (int s = SU; s < S; ++s) {
+                const float4 q = __ldcs(reinterpret_cast<const float4*>(src + (size_t)s * stride));
+                a.x += q.x; a.y += q.y; a.z += q.z; a.w += q.w;
             }
             reinterpret_cast<float4*>(g)[v] = a;  // the local gradient stays observable
         } else {
             a = reinterpret_cast<const float4*>(g)[v];
         }
         // TEM_MEAN at N = 1: a * fl(1/1) is exact
-        const float4 x = owner_update(oc, os, e, a, reinterpret_cast<float4*>(w)[v]);
+        const float4 x = owner_update<KIND>(oc, os, e, a, wv);
         reinterpret_cast<float4*>(w)[v] = x;
         if (shadow) store_shadow4(shadow, shadow_lo, e, x);
     }
-    trace_end(SLOT_EXCHANGE);
+    trace_end(slot);
 }
 
 // KP1 parameter-server comparator: every rank pushes its buffer into
@@ -524,11 +547,14 @@ cudaError_t launch_opt_scalars(float* scal, float beta1, float beta2, cudaStream
 
 void trace_set_ring(unsigned long long* p) { cudaMemcpyToSymbol(g_trace, &p, sizeof(p)); }
 
-cudaError_t launch_sgd_fused(float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo, int64_t n,
-                             const OptCfg& oc, const OptState& os, const float* p1, int64_t stride1, int64_t n1,
-                             int S1, const float* p2, int64_t stride2, int64_t off2, int64_t n2, int S2,
-                             cudaStream_t s) {
-    return launch_pdl(sgd_fused_kernel, dim3(296), dim3(512), 0, s, false, g, w, shadow, shadow_lo, n, oc, os, p1,
+cudaError_t launch_sgd_fused(float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo, int64_t e0,
+                             int64_t e1, const OptCfg& oc, const OptState& os, const float* p1, int64_t stride1,
+                             int64_t n1, int S1, const float* p2, int64_t stride2, int64_t off2, int64_t n2, int S2,
+                             cudaStream_t s, bool side, int ctas) {
+    // 2 x 512 threads per SM, grid-stride (one element group per thread and 256-thread CTAs
+    // measured 0.7 us slower at c2)
+    auto k = oc.kind == TEM_OPT_ADAM ? sgd_fused_kernel<TEM_OPT_ADAM> : sgd_fused_kernel<TEM_OPT_SGD>;
+    return launch_pdl(k, dim3(ctas > 0 ? ctas : 296), dim3(512), 0, s, side, g, w, shadow, shadow_lo, e0, e1, oc, os, p1,
                       stride1, n1, S1, p2, stride2, off2, n2, S2);
 }
 

@@ -226,6 +226,7 @@ struct tem_ctx {
     int launches_step, launches_exchange;
     bool alive;
     bool reduce_deferred;  // last compute left the split-K partials for the fused N = 1 exchange
+    bool split_done;       // ... and already updated [off_W2, K_pad) (SplitUpdate)
     // per-kernel timing (tem_timing_*)
     cudaEvent_t* tev;  // [max_steps][NUM_SLOTS*2]
     int t_max, t_idx;
@@ -469,51 +470,6 @@ static cudaEvent_t* timing_slot_events(tem_ctx* c) {
     return c->tev + (size_t)c->t_idx * NUM_SLOTS * 2;
 }
 
-static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, float* loss_out,
-                               cudaStream_t s, int* nl, bool fuse_reduce = false) {
-    const EvRec rec{timing_slot_events(c), s};
-    const Geom& g = c->g;
-    const size_t esz = g.prec == TEM_BF16 ? 2 : 4;  // caller's x element size
-    const float lam[3] = {c->cfg.loss_weight[0], c->cfg.loss_weight[1], c->cfg.loss_weight[2]};
-    for (int l = 0; l < c->nlocal; ++l) {
-        const char* xl = (const char*)x + (size_t)l * g.B * g.T * g.Cin * esz;
-        const float* labl = labels + (size_t)l * g.B * 3 * g.T;
-        rec.begin(SLOT_PREP);
-        cudaError_t e = g.split ? launch_prep_x_split(g, (const float*)xl, c->rb[l].xp, c->rb[l].xp_lo, s)
-                                : launch_prep_x(g, xl, c->rb[l].xp, s);
-        rec.end(SLOT_PREP);
-        if (e != cudaSuccess) return TEM_ERR_CUDA;
-        ++*nl;
-        const bool defer = fuse_reduce && c->N == 1 && g.path == PATH_UMMA && g.B > 0;
-        c->reduce_deferred = defer;
-        float* lh = (c->nlocal == 1) ? c->loss_host_pending : nullptr;
-        if (g.pem_P > 0) {
-            // PEM (configs[4]) is independent of TEM: on the tcgen05 path it runs on the side
-            // stream from the start of the step, beside the TEM forward GEMMs
-            const int M = g.B * g.pem_P;
-            // PEM (configs[4]): both kernels on the critical path right after prep_x (all SMs)
-            const bool side = getenv("TEM_PEM_SIDE") != nullptr && g.path == PATH_UMMA && g.B > 0 && !rec.ev &&
-                              umma_side_branch_enabled();
-            cudaStream_t ps = side ? c->plan[l]->pem : s;
-            if (side) c->plan[l]->pem_pending = true;  // umma_compute joins it before returning
-            e = launch_pem(g, c->pem_bsp + (size_t)l * M * g.pem_F, c->pem_iou + (size_t)l * M,
-                           c->rb[l].params + g.off_pem, c->rb[l].pempart, c->rb[l].grad + g.off_pem,
-                           loss_out + 4 * c->nlocal + l, c->st_dev, c->rb[l].stepctr,
-                           c->pem_record_dec ? c->rb[l].pemdec : nullptr, s, ps,
-                           side ? c->plan[l]->pem_fork : nullptr, nl);
-            if (e != cudaSuccess) return TEM_ERR_CUDA;
-        }
-        if (g.path == PATH_UMMA && g.B > 0) {
-            e = umma_compute(g, c->rb[l], *c->plan[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s, defer, lh);
-            if (lh) c->loss_host_done = true;
-        }
-        else
-            e = simt_compute(g, c->rb[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s);
-        if (e != cudaSuccess) return TEM_ERR_CUDA;
-    }
-    return TEM_OK;
-}
-
 static OptCfg opt_cfg(const tem_ctx* c) {
     OptCfg o;
     o.kind = c->cfg.optimizer;
@@ -534,6 +490,58 @@ static OptState opt_state(const tem_ctx* c, int l) {
         o.scal = (const float*)(c->ws_base[l] + c->wl.opt_scal);
     }
     return o;
+}
+
+static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, float* loss_out,
+                               cudaStream_t s, int* nl, bool fuse_reduce = false) {
+    const EvRec rec{timing_slot_events(c), s};
+    const Geom& g = c->g;
+    const size_t esz = g.prec == TEM_BF16 ? 2 : 4;  // caller's x element size
+    const float lam[3] = {c->cfg.loss_weight[0], c->cfg.loss_weight[1], c->cfg.loss_weight[2]};
+    for (int l = 0; l < c->nlocal; ++l) {
+        const char* xl = (const char*)x + (size_t)l * g.B * g.T * g.Cin * esz;
+        const float* labl = labels + (size_t)l * g.B * 3 * g.T;
+        rec.begin(SLOT_PREP);
+        cudaError_t e = g.split ? launch_prep_x_split(g, (const float*)xl, c->rb[l].xp, c->rb[l].xp_lo, s)
+                                : launch_prep_x(g, xl, c->rb[l].xp, s);
+        rec.end(SLOT_PREP);
+        if (e != cudaSuccess) return TEM_ERR_CUDA;
+        ++*nl;
+        const bool defer = fuse_reduce && c->N == 1 && g.path == PATH_UMMA && g.B > 0;
+        c->reduce_deferred = defer;
+        // TEM_SPLIT_UPDATE=1 (experiment, off: measured 2-14 % slower at c2):
+        // tem_step at N = 1 updates [off_W2, K_pad) inside the compute on the side branch, beside
+        // conv1 wgrad, and the exchange only [0, off_W2)
+        const bool split_on = getenv("TEM_SPLIT_UPDATE") != nullptr;
+        const SplitUpdate su{opt_cfg(c), opt_state(c, l)};
+        c->split_done = defer && split_on;
+        float* lh = (c->nlocal == 1) ? c->loss_host_pending : nullptr;
+        if (g.pem_P > 0) {
+            // PEM (configs[4]) is independent of TEM: on the tcgen05 path it runs on the side
+            // stream from the start of the step, beside the TEM forward GEMMs
+            const int M = g.B * g.pem_P;
+            // PEM (configs[4]): both kernels on the critical path right after prep_x (all SMs)
+            const bool side = getenv("TEM_PEM_SIDE") != nullptr && g.path == PATH_UMMA && g.B > 0 && !rec.ev &&
+                              umma_side_branch_enabled();
+            cudaStream_t ps = side ? c->plan[l]->pem : s;
+            if (side) c->plan[l]->pem_pending = true;  // umma_compute joins it before returning
+            e = launch_pem(g, c->pem_bsp + (size_t)l * M * g.pem_F, c->pem_iou + (size_t)l * M,
+                           c->rb[l].params + g.off_pem, c->rb[l].pempart, c->rb[l].grad + g.off_pem,
+                           loss_out + 4 * c->nlocal + l, c->st_dev, c->rb[l].stepctr,
+                           c->pem_record_dec ? c->rb[l].pemdec : nullptr, s, ps,
+                           side ? c->plan[l]->pem_fork : nullptr, nl, rec);
+            if (e != cudaSuccess) return TEM_ERR_CUDA;
+        }
+        if (g.path == PATH_UMMA && g.B > 0) {
+            e = umma_compute(g, c->rb[l], *c->plan[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s, defer, lh,
+                             c->split_done ? &su : nullptr);
+            if (lh) c->loss_host_done = true;
+        }
+        else
+            e = simt_compute(g, c->rb[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s);
+        if (e != cudaSuccess) return TEM_ERR_CUDA;
+    }
+    return TEM_OK;
 }
 
 // Adam: advance every local rank's beta^t before the update reads it
@@ -565,20 +573,21 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
     const Geom& g = c->g;
     const EvRec rec{timing_slot_events(c), s};
     rec.begin(SLOT_EXCHANGE);
-    tem_status st = opt_scalars(c, s, nl);
-    if (st != TEM_OK) return st;
+    tem_status st = TEM_OK;
     const OptCfg oc = opt_cfg(c);
     if (c->N == 1 && c->reduce_deferred) {  // tem_step: split-K reductions fused into the update
         const RankBufs& b = c->rb[0];
         const UmmaPlan& P = *c->plan[0];
         c->reduce_deferred = false;
-        if (launch_sgd_fused(b.grad, (float*)b.params, b.shadow, b.shadow_lo, g.Kpad, oc, opt_state(c, 0), b.wpart,
+        const int64_t e1 = c->split_done ? g.off_W2 : g.Kpad;  // [off_W2, K_pad) done in the compute
+        c->split_done = false;
+        if (launch_sgd_fused(b.grad, (float*)b.params, b.shadow, b.shadow_lo, 0, e1, oc, opt_state(c, 0), b.wpart,
                              P.wgrad1.part_stride, g.off_W2, P.S1, b.wpart2, P.wgrad2.part_stride, g.off_W2,
                              (int64_t)3 * g.C * g.C, P.S2, s) != cudaSuccess)
             return TEM_ERR_CUDA;
         ++*nl;
         rec.end(SLOT_EXCHANGE);
-        return st;
+        return opt_scalars(c, s, nl);
     }
     if (c->N == 1) {
         for (int l = 0; l < c->nlocal; ++l) {
@@ -588,7 +597,7 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
             ++*nl;
         }
         rec.end(SLOT_EXCHANGE);
-        return st;
+        return opt_scalars(c, s, nl);
     }
     RingParams p;
     memset(&p, 0, sizeof(p));
@@ -635,7 +644,7 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
     }
     rec.end(SLOT_EXCHANGE);
     ++*nl;
-    return st;
+    return opt_scalars(c, s, nl);
 }
 
 tem_status tem_compute(tem_ctx* c, const void* x, const float* labels, float* loss_out, void* stream) {

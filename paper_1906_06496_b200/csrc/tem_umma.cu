@@ -1585,6 +1585,7 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     if (cudaStreamCreateWithFlags(&P.aux, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&P.fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&P.join, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&P.dgrad_done, cudaEventDisableTiming) != cudaSuccess ||
         cudaStreamCreateWithFlags(&P.pem, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&P.pem_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&P.pem_join, cudaEventDisableTiming) != cudaSuccess)
@@ -1752,6 +1753,7 @@ void umma_plan_destroy(UmmaPlan* plan) {
     if (plan->aux) cudaStreamDestroy(plan->aux);
     if (plan->fork) cudaEventDestroy(plan->fork);
     if (plan->join) cudaEventDestroy(plan->join);
+    if (plan->dgrad_done) cudaEventDestroy(plan->dgrad_done);
     if (plan->pem) cudaStreamDestroy(plan->pem);
     if (plan->pem_fork) cudaEventDestroy(plan->pem_fork);
     if (plan->pem_join) cudaEventDestroy(plan->pem_join);
@@ -1777,9 +1779,19 @@ static cudaError_t dispatch(const UmmaParams& p, int npass, cudaStream_t s) {
     }
 }
 
+// CTAs of the side-branch update (split update): at most one 512-thread CTA per SM so that
+// conv1 wgrad's CTAs (one per SM, ~200 KB smem) still fit beside it
+static int split_ctas() {
+    static const int v = [] {
+        const char* e = getenv("TEM_SPLIT_CTAS");
+        return e ? atoi(e) : 32;
+    }();
+    return v;
+}
+
 cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, const float* labels,
                          const float lam[3], float* loss_out, Status* status, int* nl, const EvRec& rec,
-                         cudaStream_t s, bool defer_reduce, float* loss_host) {
+                         cudaStream_t s, bool defer_reduce, float* loss_host, const SplitUpdate* split) {
     int n = 0;
     cudaError_t e;
     rec.begin(SLOT_CONV1);
@@ -1838,12 +1850,30 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     if (e != cudaSuccess) return e;
     ++n;
     }
-    if (!no_fork && cudaEventRecord(P.join, P.aux) != cudaSuccess) return cudaErrorUnknown;
+    if (!split && !no_fork && cudaEventRecord(P.join, P.aux) != cudaSuccess) return cudaErrorUnknown;
     rec.begin(SLOT_DGRAD);
     e = dispatch<DGRAD_>(P.dgrad, P.npass, s);
     rec.end(SLOT_DGRAD);
     if (e != cudaSuccess) return e;
     ++n;
+    if (split && defer_reduce) {
+        // N = 1 tem_step: the owner update of [off_W2, K_pad) (W2 with its split-K partials, b2,
+        // W3, b3, PEM) needs only conv2 wgrad / the head and runs once conv2 dgrad -- the last
+        // reader of W2 -- is done, on the side branch beside conv1 wgrad
+        if (!no_fork &&
+            (cudaEventRecord(P.dgrad_done, s) != cudaSuccess || cudaStreamWaitEvent(P.aux, P.dgrad_done, 0) != cudaSuccess))
+            return cudaErrorUnknown;
+        rec2.begin(SLOT_EXCH2);
+        e = launch_sgd_fused(b.grad, const_cast<float*>(b.params), b.shadow, b.shadow_lo, g.off_W2, g.Kpad, split->oc,
+                             split->os, nullptr, 0, 0, 1, b.wpart2, P.wgrad2.part_stride, g.off_W2,
+                             (int64_t)3 * g.C * g.C, P.S2, aux, !no_fork, split_ctas());
+        rec2.end(SLOT_EXCH2);
+        if (e != cudaSuccess) return e;
+        ++n;
+        if (!no_fork && cudaEventRecord(P.join, P.aux) != cudaSuccess) return cudaErrorUnknown;
+    } else if (split && !no_fork && cudaEventRecord(P.join, P.aux) != cudaSuccess) {
+        return cudaErrorUnknown;
+    }
     rec.begin(SLOT_WGRAD1);
     e = dispatch<WGRAD_>(P.wgrad1, P.npass, s);
     rec.end(SLOT_WGRAD1);

@@ -85,5 +85,30 @@ def full(path, out):
     print("\n".join(lines))
 
 
+def details(path, out, kernel_regex):
+    """The --page details sections (SOL, memory workload, occupancy, warp state, rules) of the LAST
+    launch whose name matches kernel_regex (the steady-state step's launch)."""
+    import re
+    raw = subprocess.run([NCU, "-i", path, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr = rows[0]
+    ii, si, mi, ui, vi = (hdr.index(k) for k in ("ID", "Section Name", "Metric Name", "Metric Unit", "Metric Value"))
+    ki = hdr.index("Kernel Name")
+    rows = [hdr] + [r for r in rows[1:] if len(r) > vi and re.search(kernel_regex, r[ki])]
+    last = max(int(r[ii]) for r in rows[1:])
+    sel = [r for r in rows[1:] if len(r) > vi and int(r[ii]) == last]
+    lines = [f"# ncu --set full details ({os.path.basename(path)}), launch ID {last}: {sel[0][hdr.index('Kernel Name')]}",
+             f"# grid {sel[0][hdr.index('Grid Size')]} block {sel[0][hdr.index('Block Size')]}, --clock-control none", ""]
+    sec = None
+    for r in sel:
+        if r[si] != sec:
+            sec = r[si]
+            lines.append(f"## {sec}")
+        if r[mi]:
+            lines.append(f"  {r[mi]:<48} {r[vi]:>16} {r[ui]}")
+    open(out, "w").write("\n".join(lines) + "\n")
+    print("\n".join(lines[:40]))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2], sys.argv[3])
+    {"launches": launches, "full": full, "details": details}[sys.argv[1]](*sys.argv[2:])

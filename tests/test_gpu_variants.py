@@ -95,6 +95,26 @@ def test_graph_and_eager_steps_identical(tem, monkeypatch):
     assert np.array_equal(w_graph, w_eager)
 
 
+@pytest.mark.parametrize("optimizer", [0, 1])
+def test_split_update_identical(tem, monkeypatch, optimizer):
+    """TEM_SPLIT_UPDATE=1 (the W2.. range of the N = 1 update on the side branch beside conv1
+    wgrad, the rest after it) runs the same per-element arithmetic: parameters after three
+    steps are bitwise identical to the single update kernel's, for SGD and Adam."""
+    def run():
+        s, _ = session(tem, 1, 8, 0, lr=0.05 if optimizer == 0 else 1e-3, optimizer=optimizer)
+        x, lab = make_inputs(1, 8, 0, batch_idx=8)
+        xd, ld = to_dev_x(x, 0), torch.from_numpy(lab).cuda()
+        for _ in range(3):
+            s.step(xd, ld)
+        assert s.sync()[0] == 0
+        w = s.params(0).cpu().numpy().copy()
+        s.close()
+        return w
+    w_plain = run()
+    monkeypatch.setenv("TEM_SPLIT_UPDATE", "1")
+    assert np.array_equal(run(), w_plain)
+
+
 def test_step_host_matches_device_step(tem):
     """tem_step_host (pinned host x / labels / loss, copies inside the step; the loss is read
     back on the side stream) == tem_step on device buffers: same loss, bitwise equal params."""
