@@ -170,11 +170,19 @@ tem_status tem_compute_pem(tem_ctx* ctx, const void* x, const float* labels, con
  * 1[a_mj > 0] (uint8, M = B*P rows, H columns) into the caller's device buffer (R7b). */
 tem_status tem_pem_relu_decisions(tem_ctx* ctx, int32_t local_rank, uint8_t* out, void* stream);
 
-/* tem_step with HOST buffers (pinned recommended): copies x and labels host->device into
- * the workspace, runs the step, copies loss (local_ranks*4 floats) device->host, all on
- * `stream`.  The end-to-end path a user calls. */
+/* tem_step with HOST buffers (pinned recommended; local_ranks == 1; TEM-only configs): the
+ * end-to-end path a user calls.  Copies x and labels host->device into one of two staging sets
+ * in the workspace on a private copy stream, runs the step on `stream` once the copy is done,
+ * and copies the loss (4 floats) device->host.  Everything is complete when `stream`'s work of
+ * this call is; the host buffers may be reused from then on.  Consecutive calls overlap the
+ * copy of a step with the compute of the previous one (the staging set of call k is reused by
+ * call k+2, after the step of call k is done). */
 tem_status tem_step_host(tem_ctx* ctx, const void* x_host, const float* labels_host,
                          float* loss_host, void* stream);
+/* Same for a PEM config (pem_proposals > 0): also copies the BSP features [B][P][F] and IoU
+ * targets [B][P]; loss_host receives 5 floats: the 4 TEM values of tem_step, then L_PEM. */
+tem_status tem_step_pem_host(tem_ctx* ctx, const void* x_host, const float* labels_host,
+                             const float* bsp_host, const float* iou_host, float* loss_host, void* stream);
 
 /* ring_allreduce: in-place allreduce of K fp32 elements.
  *   buf   device; must be the user region of this rank's heap, i.e.

@@ -59,7 +59,7 @@ struct HeapLayout {
 
 struct WsLayout {
     size_t xp, h1, h2, dA2, dA1, xp_lo, h1_lo, dA2_lo, dA1_lo, z, grad, headpart, headlvl1, counter, bpart, wpart, wpart2, shadow,
-        shadow_lo, ones, zpart, epochs, stepctr, xstage, labstage, lossstage, pempart, pemdec, opt_m, opt_v, opt_scal, per_rank;
+        shadow_lo, ones, zpart, epochs, stepctr, xstage, labstage, lossstage, bspstage, ioustage, pempart, pemdec, opt_m, opt_v, opt_scal, per_rank;
 };
 
 bool cfg_valid(const tem_config* c) {
@@ -196,9 +196,13 @@ WsLayout ws_layout(const tem_config* c) {
     w.zpart = take(g.path == PATH_UMMA ? (size_t)(g.C / 64) * g.R * 3 * 4 : 0);
     w.epochs = take((size_t)kMaxChannels * 4);
     w.stepctr = take(8);
-    w.xstage = take((size_t)g.B * g.T * g.Cin * xsz);
-    w.labstage = take((size_t)g.B * 3 * g.T * 4);
-    w.lossstage = take(4 * 4);
+    // host-input staging (tem_step_host / tem_step_pem_host), double-buffered: the copy of step
+    // k+1 lands in the other set while step k computes
+    w.xstage = take(2 * (size_t)g.B * g.T * g.Cin * xsz);
+    w.labstage = take(2 * (size_t)g.B * 3 * g.T * 4);
+    w.lossstage = take(8 * 4);
+    w.bspstage = take(2 * (size_t)g.B * g.pem_P * g.pem_F * 4);
+    w.ioustage = take(2 * (size_t)g.B * g.pem_P * 4);
     const size_t adam = c->optimizer == TEM_OPT_ADAM ? 1 : 0;  // reading R22
     w.opt_m = take(adam * (size_t)g.Kpad * 4);
     w.opt_v = take(adam * (size_t)g.Kpad * 4);
@@ -253,6 +257,10 @@ struct tem_ctx {
     bool use_graphs;
     cudaStream_t gstream;
     cudaEvent_t ev_in, ev_out;
+    // host-input pipeline (tem_step_host): copy stream, per staging set "copied" / "consumed"
+    cudaStream_t cstream;
+    cudaEvent_t ev_copied[2], ev_consumed[2];
+    int hslot;
 };
 
 namespace {
@@ -742,25 +750,60 @@ tem_status tem_pem_relu_decisions(tem_ctx* c, int32_t l, uint8_t* out, void* str
                : TEM_ERR_CUDA;
 }
 
+// Host-input pipeline shared by tem_step_host / tem_step_pem_host: this call's inputs are
+// copied on a private copy stream into staging set `hslot`, which the step on `s` waits for;
+// the set is reused two calls later, once the step that consumed it is done.  A caller that
+// issues steps back to back therefore overlaps the copy of step k+1 with the compute of step k.
+static tem_status host_stage(tem_ctx* c, cudaStream_t s, const void* x_host, const float* labels_host,
+                             const float* bsp_host, const float* iou_host, int* slot, void** xd, float** ld,
+                             float** bd, float** id) {
+    const Geom& g = c->g;
+    if (!c->cstream) {
+        if (cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking) != cudaSuccess) return TEM_ERR_CUDA;
+        for (int i = 0; i < 2; ++i)
+            if (cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&c->ev_consumed[i], cudaEventDisableTiming) != cudaSuccess)
+                return TEM_ERR_CUDA;
+    }
+    const int i = c->hslot;
+    c->hslot ^= 1;
+    *slot = i;
+    const size_t esz = g.prec == TEM_BF16 ? 2 : 4;
+    const size_t xb = (size_t)g.B * g.T * g.Cin * esz, lb = (size_t)g.B * 3 * g.T * 4;
+    const size_t bb = (size_t)g.B * g.pem_P * g.pem_F * 4, ib = (size_t)g.B * g.pem_P * 4;
+    char* base = c->ws_base[0];
+    *xd = base + c->wl.xstage + i * xb;
+    *ld = (float*)(base + c->wl.labstage + i * lb);
+    *bd = (float*)(base + c->wl.bspstage + i * bb);
+    *id = (float*)(base + c->wl.ioustage + i * ib);
+    cudaStream_t cs = c->cstream;
+    // one copy per tensor (measured: splitting x over parallel copy streams is slower)
+    if (cudaStreamWaitEvent(cs, c->ev_consumed[i], 0) != cudaSuccess) return TEM_ERR_CUDA;
+    if (xb && cudaMemcpyAsync(*xd, x_host, xb, cudaMemcpyHostToDevice, cs) != cudaSuccess) return TEM_ERR_CUDA;
+    if (lb && cudaMemcpyAsync(*ld, labels_host, lb, cudaMemcpyHostToDevice, cs) != cudaSuccess) return TEM_ERR_CUDA;
+    if (bsp_host && bb && cudaMemcpyAsync(*bd, bsp_host, bb, cudaMemcpyHostToDevice, cs) != cudaSuccess)
+        return TEM_ERR_CUDA;
+    if (iou_host && ib && cudaMemcpyAsync(*id, iou_host, ib, cudaMemcpyHostToDevice, cs) != cudaSuccess)
+        return TEM_ERR_CUDA;
+    if (cudaEventRecord(c->ev_copied[i], cs) != cudaSuccess || cudaStreamWaitEvent(s, c->ev_copied[i], 0) != cudaSuccess)
+        return TEM_ERR_CUDA;
+    return TEM_OK;
+}
+
 tem_status tem_step_host(tem_ctx* c, const void* x_host, const float* labels_host, float* loss_host,
                          void* stream) {
     tem_status st = check_ctx(c);
     if (st != TEM_OK) return st;
     if (!loss_host || ((!x_host || !labels_host) && c->g.B > 0)) return TEM_ERR_INVALID_ARG;
     if (c->nlocal != 1) return TEM_ERR_INVALID_ARG;  // host path: one rank per process
-    if (c->g.pem_P > 0) return TEM_ERR_INVALID_ARG;  // host path: TEM-only configs
+    if (c->g.pem_P > 0) return TEM_ERR_INVALID_ARG;  // PEM configs: tem_step_pem_host
     cudaStream_t s = (cudaStream_t)stream;
-    const Geom& g = c->g;
-    const size_t esz = g.prec == TEM_BF16 ? 2 : 4;
-    char* base = c->ws_base[0];
-    void* xd = base + c->wl.xstage;
-    float* ld = (float*)(base + c->wl.labstage);
-    float* lossd = (float*)(base + c->wl.lossstage);
-    const size_t xb = (size_t)g.B * g.T * g.Cin * esz, lb = (size_t)g.B * 3 * g.T * 4;
-    // one copy each on `s` (measured: splitting x over parallel copy streams is slower)
-    if (xb && cudaMemcpyAsync(xd, x_host, xb, cudaMemcpyHostToDevice, s) != cudaSuccess) return TEM_ERR_CUDA;
-    if (lb && cudaMemcpyAsync(ld, labels_host, lb, cudaMemcpyHostToDevice, s) != cudaSuccess)
-        return TEM_ERR_CUDA;
+    int slot;
+    void* xd;
+    float *ld, *bd, *id;
+    st = host_stage(c, s, x_host, labels_host, nullptr, nullptr, &slot, &xd, &ld, &bd, &id);
+    if (st != TEM_OK) return st;
+    float* lossd = (float*)(c->ws_base[0] + c->wl.lossstage);
     c->loss_host_pending = loss_host;  // the tcgen05 path reads the loss back inside the step
     c->loss_host_done = false;
     st = tem_step(c, xd, ld, lossd, stream);
@@ -769,6 +812,29 @@ tem_status tem_step_host(tem_ctx* c, const void* x_host, const float* labels_hos
     c->loss_host_done = false;
     if (st != TEM_OK) return st;
     if (!done && cudaMemcpyAsync(loss_host, lossd, 16, cudaMemcpyDeviceToHost, s) != cudaSuccess) return TEM_ERR_CUDA;
+    if (cudaEventRecord(c->ev_consumed[slot], s) != cudaSuccess) return TEM_ERR_CUDA;
+    return TEM_OK;
+}
+
+tem_status tem_step_pem_host(tem_ctx* c, const void* x_host, const float* labels_host, const float* bsp_host,
+                             const float* iou_host, float* loss_host, void* stream) {
+    tem_status st = check_ctx(c);
+    if (st != TEM_OK) return st;
+    if (!loss_host || ((!x_host || !labels_host || !bsp_host || !iou_host) && c->g.B > 0)) return TEM_ERR_INVALID_ARG;
+    if (c->nlocal != 1 || c->g.pem_P <= 0) return TEM_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    int slot;
+    void* xd;
+    float *ld, *bd, *id;
+    st = host_stage(c, s, x_host, labels_host, bsp_host, iou_host, &slot, &xd, &ld, &bd, &id);
+    if (st != TEM_OK) return st;
+    float* lossd = (float*)(c->ws_base[0] + c->wl.lossstage);
+    st = tem_step_pem(c, xd, ld, bd, id, lossd, stream);
+    if (st != TEM_OK) return st;
+    // [4 TEM | 1 PEM] floats, after the step
+    if (cudaMemcpyAsync(loss_host, lossd, 5 * sizeof(float), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaEventRecord(c->ev_consumed[slot], s) != cudaSuccess)
+        return TEM_ERR_CUDA;
     return TEM_OK;
 }
 
@@ -893,6 +959,13 @@ tem_status tem_shutdown(tem_ctx* c) {
     cudaFreeHost(c->st_host);
     for (int l = 0; l < c->nlocal; ++l) umma_plan_destroy(c->plan[l]);
     for (int i = 0; i < c->ngraphs; ++i) cudaGraphExecDestroy(c->graphs[i].exec);
+    if (c->cstream) {
+        cudaStreamDestroy(c->cstream);
+        for (int i = 0; i < 2; ++i) {
+            cudaEventDestroy(c->ev_copied[i]);
+            cudaEventDestroy(c->ev_consumed[i]);
+        }
+    }
     if (c->gstream) {
         cudaStreamDestroy(c->gstream);
         cudaEventDestroy(c->ev_in);

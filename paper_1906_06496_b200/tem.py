@@ -81,6 +81,8 @@ def lib():
         L.tem_pem_relu_decisions.argtypes = [_P, ctypes.c_int32, _P, _P]
         L.tem_step_host.restype = ctypes.c_int
         L.tem_step_host.argtypes = [_P, _P, _P, _P, _P]
+        L.tem_step_pem_host.restype = ctypes.c_int
+        L.tem_step_pem_host.argtypes = [_P, _P, _P, _P, _P, _P, _P]
         L.tem_exchange.restype = ctypes.c_int
         L.tem_exchange.argtypes = [_P, _P]
         for f in (L.ring_allreduce, L.ps_allreduce, L.twoshot_allreduce):
@@ -122,7 +124,7 @@ EXPORTS = ["tem_num_params", "tem_kpad", "tem_workspace_bytes", "tem_sym_bytes",
            "tem_local_grad", "tem_logits", "tem_launches_per_step", "tem_launches_per_exchange",
            "tem_status_string", "tem_kernel_path", "tem_timing_slots", "tem_timing_slot_name",
            "tem_timing_begin", "tem_timing_end", "tem_relu_decisions", "tem_debug_buffer",
-           "tem_step_pem", "tem_compute_pem", "tem_pem_relu_decisions", "twoshot_allreduce"]
+           "tem_step_pem", "tem_compute_pem", "tem_pem_relu_decisions", "twoshot_allreduce", "tem_step_pem_host"]
 
 
 def status_string(code: int) -> str:
@@ -424,6 +426,13 @@ class TemSession:
 
     def step_host(self, x_host: torch.Tensor, labels_host: torch.Tensor, loss_host: torch.Tensor, stream=None):
         tem_step_host(self.ctx, x_host.data_ptr(), labels_host.data_ptr(), loss_host.data_ptr(), stream)
+
+    def step_pem_host(self, x_host: torch.Tensor, labels_host: torch.Tensor, bsp_host: torch.Tensor,
+                      iou_host: torch.Tensor, loss_host: torch.Tensor, stream=None):
+        """Joint step from host buffers (pinned); loss_host: 5 floats [4 TEM | PEM]."""
+        _check(lib().tem_step_pem_host(_P(self.ctx), _P(x_host.data_ptr()), _P(labels_host.data_ptr()),
+                                       _P(bsp_host.data_ptr()), _P(iou_host.data_ptr()), _P(loss_host.data_ptr()),
+                                       _stream_ptr(stream)), "tem_step_pem_host")
 
     def kernel_path(self) -> str:
         return lib().tem_kernel_path(_P(self.ctx)).decode()

@@ -139,3 +139,66 @@ def test_step_host_matches_device_step(tem):
     assert s2.sync()[0] == 0
     assert np.array_equal(s2.params(0).cpu().numpy(), w1)
     s2.close()
+
+
+def test_step_host_pipelined_inputs(tem):
+    """Back-to-back tem_step_host calls with a different batch each (copy of step k+1 on the
+    copy stream beside step k, two staging sets): every step sees its own inputs -- losses
+    and final params bitwise equal to device-buffer steps on the same batches."""
+    B, n = 4, 5
+    batches = [make_inputs(1, B, 0, batch_idx=20 + i) for i in range(n)]
+    s1, _ = session(tem, 1, B, 0, lr=0.05)
+    losses = []
+    for x, lab in batches:
+        losses.append(s1.step(to_dev_x(x, 0), torch.from_numpy(lab).cuda()).cpu().numpy().reshape(-1)[:4].copy())
+    assert s1.sync()[0] == 0
+    w1 = s1.params(0).cpu().numpy().copy()
+    s1.close()
+    s2, _ = session(tem, 1, B, 0, lr=0.05)
+    xh = [torch.from_numpy(x[0].copy()).pin_memory() for x, _ in batches]
+    lh = [torch.from_numpy(lab[0].copy()).pin_memory() for _, lab in batches]
+    outs = [torch.zeros(4, dtype=torch.float32).pin_memory() for _ in range(n)]
+    for i in range(n):  # no host synchronisation between calls
+        s2.step_host(xh[i], lh[i], outs[i])
+    torch.cuda.synchronize()
+    assert s2.sync()[0] == 0
+    for i in range(n):
+        assert np.array_equal(outs[i].numpy(), losses[i]), i
+    assert np.array_equal(s2.params(0).cpu().numpy(), w1)
+    s2.close()
+
+
+def test_step_pem_host_matches_device_step(tem):
+    """tem_step_pem_host (host x, labels, BSP features, IoU; 5 loss floats) == tem_step_pem on
+    device buffers, over several pipelined calls."""
+    import datagen
+    from test_gpu_pem import pem_inputs, pem_session
+    B, n = 2, 3
+    s1, _ = pem_session(tem, 1, B)
+    ref = []
+    for i in range(n):
+        x, lab = make_inputs(1, B, 0, batch_idx=30 + i)
+        f, g = pem_inputs(1, B, batch_idx=30 + i)
+        tl, pl = s1.step_pem(to_dev_x(x, 0), torch.from_numpy(lab).cuda(), torch.from_numpy(f).cuda(),
+                             torch.from_numpy(g).cuda())
+        ref.append(np.concatenate([tl.cpu().numpy().reshape(-1), pl.cpu().numpy().reshape(-1)]))
+    assert s1.sync()[0] == 0
+    w1 = s1.params(0).cpu().numpy().copy()
+    s1.close()
+    s2, _ = pem_session(tem, 1, B)
+    outs = []
+    keep = []
+    for i in range(n):
+        x, lab = make_inputs(1, B, 0, batch_idx=30 + i)
+        f, g = pem_inputs(1, B, batch_idx=30 + i)
+        hs = [torch.from_numpy(np.ascontiguousarray(a[0])).pin_memory() for a in (x, lab, f, g)]
+        keep.append(hs)
+        outs.append(torch.zeros(5, dtype=torch.float32).pin_memory())
+        s2.step_pem_host(*hs, outs[-1])
+    torch.cuda.synchronize()
+    assert s2.sync()[0] == 0
+    for i in range(n):
+        assert np.array_equal(outs[i].numpy(), ref[i]), i
+    assert np.array_equal(s2.params(0).cpu().numpy(), w1)
+    assert datagen.PEM_P > 0
+    s2.close()
