@@ -72,6 +72,8 @@ def lib():
                                              P, i64, ctypes.c_double, P, i64, P, P]
             L.orc_ring_adam_f32.restype = i32
             L.orc_ring_adam_f32.argtypes = [P, P, P, P, P, i32, i64, f32, f32, f32, f32]
+            L.orc_ring_momentum_f32.restype = i32
+            L.orc_ring_momentum_f32.argtypes = [P, P, P, i32, i64, f32, f32]
             L.orc_pem_num_params.restype = i64
             L.orc_pem_num_params.argtypes = [i32, i32]
             L.orc_pem_fwd_bwd.restype = i32
@@ -220,6 +222,18 @@ def ring_adam(grads, params, m, v, scal, lr, beta1=0.9, beta2=0.999, eps=1e-8):
     if rc:
         raise ValueError("invalid ring_adam arguments")
     return w, mm, vv, sc
+
+
+def ring_momentum(grads, params, u, lr, mu):
+    """Ring mean + heavy-ball momentum owner update (reading R23): u = fma(mu, u, gbar),
+    w = fma(-lr, u, w).  grads [N][K_pad] f32; params, u [K_pad] f32.  Returns (params', u')."""
+    g = np.ascontiguousarray(grads, dtype=np.float32)
+    N, Kp = g.shape
+    w = np.array(params, dtype=np.float32, copy=True)
+    uu = np.array(u, dtype=np.float32, copy=True)
+    if lib().orc_ring_momentum_f32(_ptr(g), _ptr(w), _ptr(uu), N, Kp, float(lr), float(mu)):
+        raise ValueError("invalid ring_momentum arguments")
+    return w, uu
 
 
 # --------------------------------------------------------------------------- PEM

@@ -228,6 +228,23 @@ int orc_ring_adam_f32(const float* grads, float* params, float* m, float* v, flo
     return 0;
 }
 
+// Ring mean + SGD with heavy-ball momentum (reading R23), fp32 with
+// explicit fused multiply-adds as the SGD step of R12:
+//   gbar = ring chain mean (as orc_ring_chain_f32, op = mean)
+//   u    = fma(mu, u, gbar)          (momentum buffer, zero before the first step)
+//   w    = fma(-lr, u, w)
+// mu = 0 reduces to orc_ring_sgd_f32 bit for bit.  All replicas receive the same w.
+int orc_ring_momentum_f32(const float* grads, float* params, float* u, int N, int64_t K_pad, float lr, float mu) {
+    std::vector<float> gbar((size_t)K_pad);
+    const int rc = orc_ring_chain_f32(grads, N, K_pad, 1, gbar.data());
+    if (rc) return rc;
+    for (int64_t e = 0; e < K_pad; ++e) {
+        u[e] = std::fma(mu, u[e], gbar[(size_t)e]);
+        params[e] = std::fma(-lr, u[e], params[e]);
+    }
+    return 0;
+}
+
 // Parameter-server comparator ("accumulates all N buffers in
 // ascending-rank order").  out = ((g_0 + g_1) + g_2) + ... ; mean once.
 int orc_ps_allreduce_f32(const float* grads, int N, int64_t K, int op, float* out) {

@@ -265,3 +265,47 @@ def test_ring_adam_uses_ring_order_sum(orc):
                                np.ones(2, np.float32), 0.0, beta1=0.0)
     expect, _ = orc.ring_allreduce(g, 1)
     assert np.array_equal(m, expect[0])
+
+
+def test_ring_momentum_zero_mu_is_sgd(orc):
+    """mu = 0: u = gbar exactly, and the update is the plain SGD step of R12 bit for bit."""
+    rng = np.random.default_rng(11)
+    N, K = 4, 4096
+    g = rng.standard_normal((N, K)).astype(np.float32)
+    w = rng.standard_normal(K).astype(np.float32)
+    w1, u1 = orc.ring_momentum(g, w, np.zeros(K, np.float32), 0.05, 0.0)
+    assert np.array_equal(w1, orc.ring_sgd(g, w, 0.05)[0])
+    assert np.array_equal(u1, orc.ring_allreduce(g, 1)[0][0])
+
+
+def test_ring_momentum_constant_gradient_closed_form(orc):
+    """Constant gradient g (identical on every rank, so the mean is exact): after t steps
+    u_t = g (1 - mu^t) / (1 - mu) and w_t = w_0 - lr g sum_{s=1..t} (1 - mu^s) / (1 - mu)."""
+    N, K, lr, mu = 2, 64, 0.01, 0.9
+    gv = np.linspace(-2, 2, K).astype(np.float32)
+    g = np.stack([gv] * N)
+    w = np.zeros(K, np.float32)
+    u = np.zeros(K, np.float32)
+    acc = 0.0
+    for t in range(1, 11):
+        w, u = orc.ring_momentum(g, w, u, lr, mu)
+        acc += (1 - mu ** t) / (1 - mu)
+        assert np.allclose(u, gv * (1 - mu ** t) / (1 - mu), rtol=1e-5, atol=1e-6), t
+        assert np.allclose(w, -lr * gv * acc, rtol=1e-5, atol=1e-6), t
+
+
+def test_ring_momentum_matches_float64_heavy_ball(orc):
+    """Random gradients, 5 steps: within fp32 rounding of float64 heavy-ball on the float64 mean."""
+    rng = np.random.default_rng(12)
+    N, K, lr, mu = 3, 999, 0.02, 0.9
+    Kp = orc.kpad(K, N)
+    w = rng.standard_normal(Kp).astype(np.float32)
+    u = np.zeros(Kp, np.float32)
+    w64, u64 = w.astype(np.float64), u.astype(np.float64)
+    for _ in range(5):
+        g = rng.standard_normal((N, Kp)).astype(np.float32)
+        w, u = orc.ring_momentum(g, w, u, lr, mu)
+        u64 = mu * u64 + g.astype(np.float64).mean(axis=0)
+        w64 = w64 - lr * u64
+        assert np.abs(u - u64).max() <= 1e-5 * max(1.0, np.abs(u64).max())
+        assert np.abs(w - w64).max() <= 1e-5 * max(1.0, np.abs(w64).max())
