@@ -219,8 +219,9 @@ def main():
     ap.add_argument("--exchange", default="ring", choices=["ring", "ps", "twoshot"],
                     help="gradient exchange: the paper's ring (default), the PS comparator, or the "
                          "NVSwitch two-shot (ring-identical bits, 2 phases)")
-    ap.add_argument("--optimizer", default="sgd", choices=["sgd", "adam"],
-                    help="owner update: the paper's SGD (default) or Adam (reading R22)")
+    ap.add_argument("--optimizer", default="sgd", choices=["sgd", "adam", "momentum"],
+                    help="owner update: the paper's SGD (default), Adam (reading R22) or heavy-ball "
+                         "momentum 0.9 (reading R23)")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
@@ -255,7 +256,8 @@ def main():
                            lr=args.lr, exchange={"ps": tem.TEM_EXCHANGE_PS, "twoshot": tem.TEM_EXCHANGE_TWOSHOT}.get(
                                args.exchange, tem.TEM_EXCHANGE_RING),
                            pem_proposals=P,
-                           optimizer=tem.TEM_OPT_ADAM if args.optimizer == "adam" else tem.TEM_OPT_SGD)
+                           optimizer={"adam": tem.TEM_OPT_ADAM, "momentum": tem.TEM_OPT_MOMENTUM}.get(
+                               args.optimizer, tem.TEM_OPT_SGD))
     t_init0 = time.perf_counter()
     params0 = datagen.init_params() if not P else np.concatenate([datagen.init_params(), datagen.init_pem_params()])
     sess = tem.TemSession(sc, params0, device=local)

@@ -110,11 +110,14 @@ typedef struct {
                                block keeps its moments; bias correction by running fp32 products
                                beta^t; every op single-rounded, so replicas stay bitwise equal
                                and the result equals the oracle's orc_ring_adam_f32)            */
-    float beta1, beta2, eps; /* Adam: 0 <= beta < 1, eps > 0 (ignored for SGD)                */
+    float beta1, beta2, eps; /* Adam: 0 <= beta < 1, eps > 0 (ignored otherwise)               */
+    float momentum;         /* TEM_OPT_MOMENTUM (reading R23): heavy ball u = fma(mu, u, gbar),
+                               w = fma(-lr, u, w); 0 <= mu < 1; u sharded by block ownership
+                               like Adam's moments                                            */
 } tem_config;
 
 enum { TEM_EXCHANGE_RING = 0, TEM_EXCHANGE_PS = 1, TEM_EXCHANGE_TWOSHOT = 2 };
-enum { TEM_OPT_SGD = 0, TEM_OPT_ADAM = 1 };
+enum { TEM_OPT_SGD = 0, TEM_OPT_ADAM = 1, TEM_OPT_MOMENTUM = 2 };
 
 /* --- sizes -----------------------------------------------------------------------------
  * K      = c_hidden*3*c_in + c_hidden + c_hidden*3*c_hidden + c_hidden + 3*c_hidden + 3

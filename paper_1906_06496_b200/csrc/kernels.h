@@ -219,9 +219,10 @@ cudaError_t launch_reduce_splits(const float* part, float* dst, int64_t n, int S
 struct OptCfg {
     int kind;  // TEM_OPT_SGD / TEM_OPT_ADAM
     float lr, beta1, beta2, c1, c2, eps;  // c1 = fl(1 - beta1), c2 = fl(1 - beta2)
+    float mu;                             // momentum (TEM_OPT_MOMENTUM)
 };
 struct OptState {
-    float* m;           // [K_pad] first moments (each rank touches only the blocks it owns)
+    float* m;           // [K_pad] first moments / momentum buffer (each rank touches only the blocks it owns)
     float* v;           // [K_pad] second moments
     const float* scal;  // [beta1^t, beta2^t] of this step (opt_scalars_kernel, before the exchange)
 };

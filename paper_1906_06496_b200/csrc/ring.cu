@@ -118,7 +118,15 @@ TEM_DEV float adam1(const OptCfg& o, float d1, float d2, float g, float& m, floa
 // KIND = -1: chosen at run time from o.kind; TEM_OPT_SGD / TEM_OPT_ADAM: fixed at compile time
 template <int KIND = -1>
 TEM_DEV float4 owner_update(const OptCfg& o, const OptState& st, int64_t e, float4 g, float4 w) {
-    if (KIND == TEM_OPT_ADAM || (KIND < 0 && o.kind == TEM_OPT_ADAM)) {
+    if (KIND == TEM_OPT_MOMENTUM || (KIND < 0 && o.kind == TEM_OPT_MOMENTUM)) {  // reading R23
+        float4 u = *reinterpret_cast<const float4*>(st.m + e);
+        u.x = __fmaf_rn(o.mu, u.x, g.x);
+        u.y = __fmaf_rn(o.mu, u.y, g.y);
+        u.z = __fmaf_rn(o.mu, u.z, g.z);
+        u.w = __fmaf_rn(o.mu, u.w, g.w);
+        *reinterpret_cast<float4*>(st.m + e) = u;
+        g = u;  // w = fma(-lr, u, w) below
+    } else if (KIND == TEM_OPT_ADAM || (KIND < 0 && o.kind == TEM_OPT_ADAM)) {
         // this step's beta^t = fl(beta^(t-1) * beta): every thread forms the same product; the
         // stored pair advances after the step's last update (opt_scalars_kernel)
         const float d1 = __fsub_rn(1.0f, __fmul_rn(st.scal[0], o.beta1));
@@ -553,7 +561,9 @@ cudaError_t launch_sgd_fused(float* g, float* w, __nv_bfloat16* shadow, __nv_bfl
                              cudaStream_t s, bool side, int ctas) {
     // 2 x 512 threads per SM, grid-stride (one element group per thread and 256-thread CTAs
     // measured 0.7 us slower at c2)
-    auto k = oc.kind == TEM_OPT_ADAM ? sgd_fused_kernel<TEM_OPT_ADAM> : sgd_fused_kernel<TEM_OPT_SGD>;
+    auto k = oc.kind == TEM_OPT_ADAM       ? sgd_fused_kernel<TEM_OPT_ADAM>
+             : oc.kind == TEM_OPT_MOMENTUM ? sgd_fused_kernel<TEM_OPT_MOMENTUM>
+                                           : sgd_fused_kernel<TEM_OPT_SGD>;
     return launch_pdl(k, dim3(ctas > 0 ? ctas : 296), dim3(512), 0, s, side, g, w, shadow, shadow_lo, e0, e1, oc, os, p1,
                       stride1, n1, S1, p2, stride2, off2, n2, S2);
 }

@@ -82,7 +82,8 @@ bool cfg_valid(const tem_config* c) {
         return false;
     if (c->pem_proposals < 0) return false;
     if (c->pem_proposals > 0 && (c->pem_features != 32 || c->pem_hidden != 512)) return false;  // kernel shape
-    if (c->optimizer != TEM_OPT_SGD && c->optimizer != TEM_OPT_ADAM) return false;
+    if (c->optimizer != TEM_OPT_SGD && c->optimizer != TEM_OPT_ADAM && c->optimizer != TEM_OPT_MOMENTUM) return false;
+    if (c->optimizer == TEM_OPT_MOMENTUM && !(c->momentum >= 0.0f && c->momentum < 1.0f)) return false;
     if (c->optimizer == TEM_OPT_ADAM &&
         !(c->beta1 >= 0.0f && c->beta1 < 1.0f && c->beta2 >= 0.0f && c->beta2 < 1.0f && c->eps > 0.0f &&
           isfinite(c->eps)))
@@ -204,7 +205,8 @@ WsLayout ws_layout(const tem_config* c) {
     w.bspstage = take(2 * (size_t)g.B * g.pem_P * g.pem_F * 4);
     w.ioustage = take(2 * (size_t)g.B * g.pem_P * 4);
     const size_t adam = c->optimizer == TEM_OPT_ADAM ? 1 : 0;  // reading R22
-    w.opt_m = take(adam * (size_t)g.Kpad * 4);
+    const size_t state1 = c->optimizer != TEM_OPT_SGD ? 1 : 0;  // Adam's m / momentum's u (R23)
+    w.opt_m = take(state1 * (size_t)g.Kpad * 4);
     w.opt_v = take(adam * (size_t)g.Kpad * 4);
     w.opt_scal = take(adam * 8);
     w.per_rank = o;
@@ -487,11 +489,13 @@ static OptCfg opt_cfg(const tem_ctx* c) {
     o.c1 = 1.0f - c->cfg.beta1;  // fp32 subtraction (the oracle's c1)
     o.c2 = 1.0f - c->cfg.beta2;
     o.eps = c->cfg.eps;
+    o.mu = c->cfg.momentum;
     return o;
 }
 
 static OptState opt_state(const tem_ctx* c, int l) {
     OptState o{nullptr, nullptr, nullptr};
+    if (c->cfg.optimizer == TEM_OPT_MOMENTUM) o.m = (float*)(c->ws_base[l] + c->wl.opt_m);
     if (c->cfg.optimizer == TEM_OPT_ADAM) {
         o.m = (float*)(c->ws_base[l] + c->wl.opt_m);
         o.v = (float*)(c->ws_base[l] + c->wl.opt_v);

@@ -22,7 +22,7 @@ TEM_OK, TEM_ERR_INVALID_ARG, TEM_ERR_PROTOCOL, TEM_ERR_TRANSPORT, TEM_ERR_CUDA, 
 TEM_SUM, TEM_MEAN = 0, 1
 TEM_FP32, TEM_BF16 = 0, 1
 TEM_EXCHANGE_RING, TEM_EXCHANGE_PS, TEM_EXCHANGE_TWOSHOT = 0, 1, 2
-TEM_OPT_SGD, TEM_OPT_ADAM = 0, 1
+TEM_OPT_SGD, TEM_OPT_ADAM, TEM_OPT_MOMENTUM = 0, 1, 2
 MAX_RANKS = 8
 
 _P = ctypes.c_void_p
@@ -43,6 +43,7 @@ class tem_config(ctypes.Structure):
         ("exchange", ctypes.c_int32),
         ("pem_proposals", ctypes.c_int32), ("pem_features", ctypes.c_int32), ("pem_hidden", ctypes.c_int32),
         ("optimizer", ctypes.c_int32), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float), ("eps", ctypes.c_float),
+        ("momentum", ctypes.c_float),
     ]
 
 
@@ -233,6 +234,7 @@ class SessionConfig:
     beta1: float = 0.9
     beta2: float = 0.999
     eps: float = 1e-8
+    momentum: float = 0.9  # TEM_OPT_MOMENTUM (reading R23)
 
 
 class TemSession:
@@ -261,6 +263,7 @@ class TemSession:
         cfg.exchange = sc.exchange
         cfg.pem_proposals, cfg.pem_features, cfg.pem_hidden = sc.pem_proposals, sc.pem_features, sc.pem_hidden
         cfg.optimizer, cfg.beta1, cfg.beta2, cfg.eps = sc.optimizer, sc.beta1, sc.beta2, sc.eps
+        cfg.momentum = sc.momentum
         self.K = tem_num_params(cfg)
         if self.K == 0:
             raise TemError(TEM_ERR_INVALID_ARG, "config")

@@ -67,9 +67,10 @@ def test_invalid_configs_rejected(field, value):
     assert not ctx.value
 
 
-@pytest.mark.parametrize("fields", [dict(optimizer=2), dict(optimizer=1, beta1=1.0, beta2=0.999, eps=1e-8),
+@pytest.mark.parametrize("fields", [dict(optimizer=3), dict(optimizer=1, beta1=1.0, beta2=0.999, eps=1e-8),
                                     dict(optimizer=1, beta1=0.9, beta2=-0.1, eps=1e-8),
-                                    dict(optimizer=1, beta1=0.9, beta2=0.999, eps=0.0)])
+                                    dict(optimizer=1, beta1=0.9, beta2=0.999, eps=0.0),
+                                    dict(optimizer=2, momentum=1.0), dict(optimizer=2, momentum=-0.5)])
 def test_invalid_optimizer_rejected(fields):
     from paper_1906_06496_b200 import tem
     c = base_cfg(tem)

@@ -83,3 +83,28 @@ def test_adam_graph_and_eager_identical(tem, monkeypatch):
     w_graph = run()
     monkeypatch.setenv("TEM_NO_GRAPH", "1")
     assert np.array_equal(w_graph, run())
+
+
+MU = 0.9
+
+
+@pytest.mark.parametrize("N,B,prec,exchange", [(1, 4, 0, 0), (1, 2, 1, 0), (2, 2, 0, 0), (3, 1, 0, 0),
+                                               (4, 1, 0, 2), (3, 1, 0, 1)])
+def test_momentum_steps_bitexact(tem, orc, N, B, prec, exchange):
+    """Heavy-ball momentum (reading R23) in every exchange: params after each of 3 steps equal
+    orc.ring_momentum's replay on the GPU's own local gradients, bitwise, on every rank."""
+    lr = 0.02
+    s, _ = session(tem, N, B, prec, lr=lr, exchange=exchange, optimizer=tem.TEM_OPT_MOMENTUM, momentum=MU)
+    w = s.params(0).cpu().numpy().copy()
+    u = np.zeros(s.Kpad, np.float32)
+    for it in range(3):
+        x, lab = make_inputs(N, B, prec, batch_idx=10 + it)
+        s.step(to_dev_x(x, prec), torch.from_numpy(lab).cuda())
+        assert s.sync()[0] == 0
+        grads = np.stack([s.local_grad(r).cpu().numpy() for r in range(N)])
+        if exchange == tem.TEM_EXCHANGE_PS:
+            grads = orc.ps_allreduce(grads, orc.MEAN)[None, :]
+        w, u = orc.ring_momentum(grads, w, u, lr, MU)
+        for r in range(N):
+            assert np.array_equal(s.params(r).cpu().numpy(), w), (it, r)
+    s.close()
