@@ -22,6 +22,8 @@ Recipe:
     [B][P][32] ~ U(0, 1) (BSN's BSP feature samples probability sequences, values in
     [0, 1]); IoU targets [B][P] = U(0, 1)^2 (skewed to low overlap, as dense proposal sets
     are); PEM parameters [W1p (512 x 32), b1p, w2p, b2p] ~ U(+-1/sqrt(fan_in)), fan_in 32, 512.
+  * PGM (reading R24): the labels' instances in snippet units (instances()), and TEM-shaped
+    probability sequences 0.05 + 0.8 * labels + U(0, 0.1) (tem_probabilities()).
 """
 from __future__ import annotations
 
@@ -48,17 +50,51 @@ def _overlap_over_snippet(t0, t1, a, b):
     return inter / (t1 - t0)
 
 
-def labels(B: int, T: int = T_DEFAULT, *, rank: int = 0, batch_idx: int = 0) -> np.ndarray:
+def _instance_draws(B: int, rank: int, batch_idx: int):
+    """Per video the list of (start, end, length) action instances in [0, 1] (labels' recipe)."""
     rng = np.random.default_rng(batch_seed(rank, batch_idx) + 7_000_000)
-    out = np.zeros((B, 3, T), dtype=np.float32)
-    t0 = np.arange(T, dtype=np.float64) / T
-    t1 = (np.arange(T, dtype=np.float64) + 1.0) / T
-    for v in range(B):
+    out = []
+    for _ in range(B):
         n_inst = int(rng.integers(1, 4))
+        segs = []
         for _ in range(n_inst):
             ln = rng.uniform(0.05, 0.5)
             s = rng.uniform(0.0, 1.0 - ln)
-            e = s + ln
+            segs.append((s, s + ln, ln))
+        out.append(segs)
+    return out
+
+
+GT_MAX = 3  # instances per video (labels' recipe draws 1-3)
+
+
+def instances(B: int, T: int = T_DEFAULT, *, rank: int = 0, batch_idx: int = 0):
+    """The ground-truth instances behind labels(B, T, rank, batch_idx), in snippet units
+    (time * T): seg [B][GT_MAX][2] float32 (unused rows 0), count [B] int32."""
+    seg = np.zeros((B, GT_MAX, 2), np.float32)
+    cnt = np.zeros(B, np.int32)
+    for v, segs in enumerate(_instance_draws(B, rank, batch_idx)):
+        cnt[v] = len(segs)
+        for i, (s, e, _) in enumerate(segs):
+            seg[v, i] = (s * T, e * T)
+    return seg, cnt
+
+
+def tem_probabilities(B: int, T: int = T_DEFAULT, *, rank: int = 0, batch_idx: int = 0) -> np.ndarray:
+    """TEM-output-shaped probability sequences [B][3][T] (actionness, start, end) for the PGM
+    tests / bench: the labels of the same batch, scaled into [0.05, 0.85], plus U(0, 0.1)
+    noise (a partly trained TEM: peaks near the true boundaries, spurious local maxima)."""
+    lab = labels(B, T, rank=rank, batch_idx=batch_idx)
+    rng = np.random.default_rng(batch_seed(rank, batch_idx) + 17_000_000)
+    return (0.05 + 0.8 * lab + 0.1 * rng.random(lab.shape)).astype(np.float32)
+
+
+def labels(B: int, T: int = T_DEFAULT, *, rank: int = 0, batch_idx: int = 0) -> np.ndarray:
+    out = np.zeros((B, 3, T), dtype=np.float32)
+    t0 = np.arange(T, dtype=np.float64) / T
+    t1 = (np.arange(T, dtype=np.float64) + 1.0) / T
+    for v, segs in enumerate(_instance_draws(B, rank, batch_idx)):
+        for s, e, ln in segs:
             w = max(0.1 * ln, 1.0 / T)
             out[v, 0] = np.maximum(out[v, 0], _overlap_over_snippet(t0, t1, s, e))
             out[v, 1] = np.maximum(out[v, 1], _overlap_over_snippet(t0, t1, s - w / 2, s + w / 2))

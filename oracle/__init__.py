@@ -293,3 +293,7 @@ def param_slices(Cin: int = 400, C: int = 512, Co: int = 3):
         out[name] = slice(off, off + n)
         off += n
     return out
+
+
+# --------------------------------------------------------------------------- PGM
+from .proposals import pgm, pgm_video, candidates as pgm_candidates, bsp_feature, F_BSP  # noqa: E402,F401
