@@ -209,6 +209,26 @@ tem_status ps_allreduce(tem_ctx* ctx, float* buf, int64_t K, int32_t op, void* s
  * and result bits as ring_allreduce, with two communication phases instead of 2(N-1). */
 tem_status twoshot_allreduce(tem_ctx* ctx, float* buf, int64_t K, int32_t op, void* stream);
 
+/* PGM, BSN's proposal generation (reading R24; the paper names the
+ * stage at P:85): for each of B videos, candidate boundaries of TEM's start / end probability
+ * sequences, the P best (start, end) proposals and their 32-d Boundary-Sensitive Proposal
+ * features -- the input of PEM -- with IoU targets.  Context-free; all pointers device, on
+ * `stream`, written completely (unused proposal rows: ts = te = -1, zero features / IoU).
+ *   prob      [B][3][T] fp32: 0 actionness, 1 start, 2 end probabilities (R4); 1 <= T <= 128
+ *   gt, n_gt  [B][G][2] fp32 ground-truth instances (start, end) in snippet units and [B]
+ *             int32 counts (n_gt[v] > G is clamped to G); G >= 0
+ *   P         proposals per video, 1 <= P <= 65536
+ *   features  [B][P][32] fp32: 8 samples of the start region, 16 of the proposal, 8 of the end
+ *             region of the actionness sequence (linear interpolation, zero outside [0, T-1])
+ *   iou       [B][P] fp32: max IoU of [ts + 1/2, te + 1/2] with the instances
+ *   ts, te    [B][P] int32 proposal boundaries, ranked by (score desc, ts asc, te asc), score
+ *             = fl32(p_start[ts] * p_end[te]); count [B] int32 = proposals found (<= P)
+ * Candidates, scores and ranking are fp32 decisions, bit-identical to the oracle.
+ * Errors: INVALID_ARG (shapes / null pointers), CUDA (launch). */
+tem_status tem_pgm(int32_t B, int32_t T, int32_t G, int32_t P, const float* prob, const float* gt,
+                   const int32_t* n_gt, float* features, float* iou, int32_t* ts, int32_t* te, int32_t* count,
+                   void* stream);
+
 /* Blocks until all work of ctx on `stream` is done; returns the latched device status.
  * For NONFINITE, *bad_step (if non-NULL) receives the 0-based step index. */
 tem_status tem_sync(tem_ctx* ctx, void* stream, int64_t* bad_step);

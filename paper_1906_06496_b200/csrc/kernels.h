@@ -239,6 +239,9 @@ struct RingLocal {
     uint32_t* epochs;       // [kMaxChannels] per-channel collective counters (workspace)
     char* heaps[TEM_MAX_RANKS];  // every rank's heap base as mapped in this process
 };
+// PGM (pgm.cu, reading R24): proposals, BSP features, IoU targets of B videos (T <= 128)
+cudaError_t launch_pgm(int B, int T, int G, int P, const float* prob, const float* gt, const int32_t* n_gt,
+                       float* feat, float* iou, int32_t* ts, int32_t* te, int32_t* count, cudaStream_t s);
 constexpr int kMaxChannels = 128;
 constexpr int kMaxChunks = 16;
 struct RingParams {

@@ -82,6 +82,8 @@ def lib():
         L.tem_pem_relu_decisions.argtypes = [_P, ctypes.c_int32, _P, _P]
         L.tem_step_host.restype = ctypes.c_int
         L.tem_step_host.argtypes = [_P, _P, _P, _P, _P]
+        L.tem_pgm.restype = ctypes.c_int
+        L.tem_pgm.argtypes = [ctypes.c_int32] * 4 + [_P] * 9
         L.tem_step_pem_host.restype = ctypes.c_int
         L.tem_step_pem_host.argtypes = [_P, _P, _P, _P, _P, _P, _P]
         L.tem_exchange.restype = ctypes.c_int
@@ -125,7 +127,7 @@ EXPORTS = ["tem_num_params", "tem_kpad", "tem_workspace_bytes", "tem_sym_bytes",
            "tem_local_grad", "tem_logits", "tem_launches_per_step", "tem_launches_per_exchange",
            "tem_status_string", "tem_kernel_path", "tem_timing_slots", "tem_timing_slot_name",
            "tem_timing_begin", "tem_timing_end", "tem_relu_decisions", "tem_debug_buffer",
-           "tem_step_pem", "tem_compute_pem", "tem_pem_relu_decisions", "twoshot_allreduce", "tem_step_pem_host"]
+           "tem_step_pem", "tem_compute_pem", "tem_pem_relu_decisions", "twoshot_allreduce", "tem_step_pem_host", "tem_pgm"]
 
 
 def status_string(code: int) -> str:
@@ -207,6 +209,25 @@ def tem_sync(ctx: int, stream=None):
 
 def tem_shutdown(ctx: int):
     _check(lib().tem_shutdown(_P(ctx)), "tem_shutdown")
+
+
+
+def pgm(prob: torch.Tensor, gt: torch.Tensor, n_gt: torch.Tensor, P: int, stream=None) -> dict:
+    """BSN proposal generation on the GPU (tem_pgm, reading R24).  prob [B][3][T] fp32, gt
+    [B][G][2] fp32, n_gt [B] int32, all on one CUDA device.  Returns device tensors count [B],
+    ts / te [B][P] int32, features [B][P][32], iou [B][P]."""
+    B, _, T = prob.shape
+    G = gt.shape[1]
+    dev = prob.device
+    out = {"count": torch.empty(B, dtype=torch.int32, device=dev),
+           "ts": torch.empty(B, P, dtype=torch.int32, device=dev),
+           "te": torch.empty(B, P, dtype=torch.int32, device=dev),
+           "features": torch.empty(B, P, 32, dtype=torch.float32, device=dev),
+           "iou": torch.empty(B, P, dtype=torch.float32, device=dev)}
+    _check(lib().tem_pgm(B, T, G, P, _P(prob.data_ptr()), _P(gt.data_ptr()), _P(n_gt.data_ptr()),
+                         _P(out["features"].data_ptr()), _P(out["iou"].data_ptr()), _P(out["ts"].data_ptr()),
+                         _P(out["te"].data_ptr()), _P(out["count"].data_ptr()), _stream_ptr(stream)), "tem_pgm")
+    return out
 
 
 # ----------------------------------------------------------------------------- session helper

@@ -89,6 +89,17 @@ def test_adam_workspace_holds_moments():
     assert tem.tem_workspace_bytes(c) - sgd >= 2 * 4 * tem.tem_kpad(c, 1403395)
 
 
+def test_pgm_rejects_bad_shapes():
+    """tem_pgm validates before touching the GPU (T <= 128, P >= 1; B = 0 is a no-op)."""
+    from paper_1906_06496_b200 import tem
+    L = tem.lib()
+    nul = [None] * 9
+    assert L.tem_pgm(1, 129, 0, 4, *nul) == tem.TEM_ERR_INVALID_ARG
+    assert L.tem_pgm(1, 10, 0, 0, *nul) == tem.TEM_ERR_INVALID_ARG
+    assert L.tem_pgm(1, 10, 0, 4, *nul) == tem.TEM_ERR_INVALID_ARG
+    assert L.tem_pgm(0, 10, 0, 4, *nul) == tem.TEM_OK
+
+
 def test_null_context_calls():
     from paper_1906_06496_b200 import tem
     L = tem.lib()
