@@ -38,6 +38,10 @@ WORKLOADS = {
     "c5": dict(desc="configs[4]: BSN TEM + PEM (proposal evaluation MLP 32->512->1 over 32-d BSP features) "
                     "joint data-parallel training, fp32, batch 16 videos/GPU x 128 proposals", B=16, prec=0,
                dtype="f32", pem=128),
+    "c6": dict(desc="configs[4] with PGM: BSN TEM + PGM + PEM joint data-parallel training, fp32, batch 16 "
+                    "videos/GPU; PEM trained on the 128 best proposals PGM generates from the step's own TEM "
+                    "output (BSP features, IoU targets vs the ground-truth instances)", B=16, prec=0,
+               dtype="f32", pem=128, pgm=3),
 }
 T, CIN, C = 100, 400, 512
 # Algorithmic FLOPs per sample of each kernel (dense count incl. zero-pad taps).
@@ -145,9 +149,15 @@ def cpu_baseline(workload: dict, videos: int):
     lab = datagen.labels(videos, rank=0, batch_idx=0)
     p = datagen.init_params()
     t0 = time.perf_counter()
-    oracle.tem_fwd_bwd(x, p, lab, prec=workload["prec"])
+    ref = oracle.tem_fwd_bwd(x, p, lab, prec=workload["prec"])
     P = workload.get("pem", 0)
-    if P:
+    if P and workload.get("pgm"):
+        gt, n = datagen.instances(videos)
+        prob = (1.0 / (1.0 + np.exp(-np.asarray(ref["z"], np.float64).reshape(videos, T, 3)))).transpose(0, 2, 1)
+        pg = oracle.pgm(prob.astype(np.float32), gt, n, P)
+        oracle.pem_fwd_bwd(pg["features"].reshape(videos * P, datagen.PEM_F), datagen.init_pem_params(),
+                           pg["iou"].ravel())
+    elif P:
         oracle.pem_fwd_bwd(datagen.bsp_features(videos).reshape(videos * P, datagen.PEM_F),
                            datagen.init_pem_params(), datagen.iou_targets(videos).ravel())
     g = np.zeros((2, oracle.kpad(1403395, 2)), np.float32)
@@ -157,6 +167,7 @@ def cpu_baseline(workload: dict, videos: int):
             "sample": f"{videos} videos ({'fp64' if workload['prec'] == 0 else 'bf16-emulated fp64'} "
                       f"fwd+loss+bwd, T=100, 400->512->512->3"
                       + (f", + PEM over {workload['pem']} proposals each" if workload.get("pem") else "")
+                      + (", + PGM" if workload.get("pgm") else "")
                       + f") + fp32 ring/SGD replay of K=1403395 at N=2; {dt:.1f} s single-threaded"}
 
 
@@ -180,9 +191,17 @@ def run_reference(args, workload):
         fb = datagen.bsp_features(per_step).reshape(per_step * P, datagen.PEM_F)
         gb = datagen.iou_targets(per_step).ravel()
 
+    if P and workload.get("pgm"):
+        gt, n = datagen.instances(per_step)
+
     def one():
-        oracle.tem_fwd_bwd(x, p, lab, prec=workload["prec"])
-        if P:
+        ref = oracle.tem_fwd_bwd(x, p, lab, prec=workload["prec"])
+        if P and workload.get("pgm"):
+            z = np.asarray(ref["z"], np.float64).reshape(per_step, T, 3)
+            prob = (1.0 / (1.0 + np.exp(-z))).transpose(0, 2, 1).astype(np.float32)
+            pg = oracle.pgm(prob, gt, n, P)
+            oracle.pem_fwd_bwd(pg["features"].reshape(per_step * P, datagen.PEM_F), pp, pg["iou"].ravel())
+        elif P:
             oracle.pem_fwd_bwd(fb, pp, gb)
     for _ in range(args.warmup):
         one()
@@ -255,7 +274,7 @@ def main():
     sc = tem.SessionConfig(world_size=world, rank=rank, local_ranks=1, batch_per_rank=B, precision=prec,
                            lr=args.lr, exchange={"ps": tem.TEM_EXCHANGE_PS, "twoshot": tem.TEM_EXCHANGE_TWOSHOT}.get(
                                args.exchange, tem.TEM_EXCHANGE_RING),
-                           pem_proposals=P,
+                           pem_proposals=P, pgm_gt_max=wl.get("pgm", 0),
                            optimizer={"adam": tem.TEM_OPT_ADAM, "momentum": tem.TEM_OPT_MOMENTUM}.get(
                                args.optimizer, tem.TEM_OPT_SGD))
     t_init0 = time.perf_counter()
@@ -273,13 +292,19 @@ def main():
         else:
             xs.append(torch.from_numpy(x).to(dev))
         labs.append(torch.from_numpy(lab).to(dev))
-        if P:
+        if P and wl.get("pgm"):  # ground-truth instances and counts (PGM-fed PEM)
+            seg, cnt = datagen.instances(B, rank=rank, batch_idx=k)
+            fs.append(torch.from_numpy(seg).to(dev))
+            gs.append(torch.from_numpy(cnt).to(dev))
+        elif P:
             fs.append(torch.from_numpy(datagen.bsp_features(B, P, rank=rank, batch_idx=k)).to(dev))
             gs.append(torch.from_numpy(datagen.iou_targets(B, P, rank=rank, batch_idx=k)).to(dev))
 
     def do_step(i):
         j = i % args.pool
-        if P:
+        if P and wl.get("pgm"):
+            sess.step_pgm(xs[j], labs[j], fs[j], gs[j])
+        elif P:
             sess.step_pem(xs[j], labs[j], fs[j], gs[j])
         else:
             sess.step(xs[j], labs[j])
@@ -347,8 +372,12 @@ def main():
         lh = [torch.from_numpy(datagen.labels(B, rank=rank, batch_idx=k)).pin_memory() for k in range(2)]
         loss_h = torch.zeros(4, dtype=torch.float32).pin_memory()
         if P:  # joint workload: tem_step_pem_host (copies, step, loss read-back)
-            fh = [torch.from_numpy(datagen.bsp_features(B, P, rank=rank, batch_idx=k)).pin_memory() for k in range(2)]
-            gh = [torch.from_numpy(datagen.iou_targets(B, P, rank=rank, batch_idx=k)).pin_memory() for k in range(2)]
+            if wl.get("pgm"):  # PGM-fed: the extra host inputs are the instances and their counts
+                fh = [torch.from_numpy(datagen.instances(B, rank=rank, batch_idx=k)[0]).pin_memory() for k in range(2)]
+                gh = [torch.from_numpy(datagen.instances(B, rank=rank, batch_idx=k)[1]).pin_memory() for k in range(2)]
+            else:
+                fh = [torch.from_numpy(datagen.bsp_features(B, P, rank=rank, batch_idx=k)).pin_memory() for k in range(2)]
+                gh = [torch.from_numpy(datagen.iou_targets(B, P, rank=rank, batch_idx=k)).pin_memory() for k in range(2)]
             loss_h = torch.zeros(5, dtype=torch.float32).pin_memory()
 
             def host_step(i):
@@ -385,7 +414,7 @@ def main():
             dist.all_reduce(t2, op=dist.ReduceOp.MAX)
         h2d = int(xh[0].numel() * xh[0].element_size() + lh[0].numel() * 4)
         if P:
-            h2d += int(fh[0].numel() * 4 + gh[0].numel() * 4)
+            h2d += int(fh[0].numel() * fh[0].element_size() + gh[0].numel() * gh[0].element_size())
         e2e = {"value": world * B * args.steps / (float(t2.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(loss_h.numel() * 4),
                "api": "tem_step_pem_host" if P else "tem_step_host",
@@ -445,7 +474,10 @@ def main():
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",
                    "kernel_path": sess.kernel_path(),
                    **({"pem": f"{P} proposals/video, 32-d BSP features, MLP 32->512->1, gradient [TEM | PEM] "
-                              f"= {sess.K} elements in one exchange"} if P else {})},
+                              f"= {sess.K} elements in one exchange"} if P else {}),
+                   **({"pgm": "PEM inputs generated on the GPU each step by PGM (tem_pgm kernel) from the "
+                              "step's own TEM probabilities: top-128 proposals, BSP features, IoU targets "
+                              f"vs <= {wl['pgm']} instances/video (reading R24)"} if wl.get("pgm") else {})},
         "step_us": step_stats,
         "gpu_launches": launches * args.steps,
         "launches_per_step": launches,

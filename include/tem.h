@@ -114,6 +114,11 @@ typedef struct {
     float momentum;         /* TEM_OPT_MOMENTUM (reading R23): heavy ball u = fma(mu, u, gbar),
                                w = fma(-lr, u, w); 0 <= mu < 1; u sharded by block ownership
                                like Adam's moments                                            */
+    int32_t pgm_gt_max;     /* > 0 (requires pem_proposals > 0, seq_len <= 128): PGM-fed PEM --
+                               tem_step_pgm runs PGM (tem_pgm) on this step's TEM probabilities
+                               sigmoid(z) and trains PEM on its BSP features and IoU targets
+                               against the caller's ground truth (<= pgm_gt_max instances per
+                               video); 0: PEM inputs from the caller (tem_step_pem)           */
 } tem_config;
 
 enum { TEM_EXCHANGE_RING = 0, TEM_EXCHANGE_PS = 1, TEM_EXCHANGE_TWOSHOT = 2 };
@@ -183,7 +188,9 @@ tem_status tem_pem_relu_decisions(tem_ctx* ctx, int32_t local_rank, uint8_t* out
 tem_status tem_step_host(tem_ctx* ctx, const void* x_host, const float* labels_host,
                          float* loss_host, void* stream);
 /* Same for a PEM config (pem_proposals > 0): also copies the BSP features [B][P][F] and IoU
- * targets [B][P]; loss_host receives 5 floats: the 4 TEM values of tem_step, then L_PEM. */
+ * targets [B][P]; loss_host receives 5 floats: the 4 TEM values of tem_step, then L_PEM.
+ * With pgm_gt_max > 0 (PGM-fed, tem_step_pgm) the two extra inputs are instead the ground
+ * truth [B][pgm_gt_max][2] fp32 and its counts [B] int32. */
 tem_status tem_step_pem_host(tem_ctx* ctx, const void* x_host, const float* labels_host,
                              const float* bsp_host, const float* iou_host, float* loss_host, void* stream);
 
@@ -208,6 +215,17 @@ tem_status ps_allreduce(tem_ctx* ctx, float* buf, int64_t K, int32_t op, void* s
  * op once and stores the result into every rank's buffer.  Same buffer rules, partition (R9)
  * and result bits as ring_allreduce, with two communication phases instead of 2(N-1). */
 tem_status twoshot_allreduce(tem_ctx* ctx, float* buf, int64_t K, int32_t op, void* stream);
+
+/* Joint TEM + PGM + PEM step (pgm_gt_max > 0): TEM forward / backward, then PGM on the
+ * sigmoid of this step's logits (stop-gradient), then PEM on the proposals' BSP features with
+ * their IoU targets, and the exchange of the joint gradient.  gt [local_ranks][B][G][2] fp32
+ * instances (snippet units), n_gt [local_ranks][B] int32, device; loss_out as tem_step_pem.
+ * The step's PGM outputs: tem_debug_buffer "pgm_prob" ([B][3][T]), "pgm_feat", "pgm_iou",
+ * "pgm_ts", "pgm_te", "pgm_count" (the tem_pgm layouts). */
+tem_status tem_step_pgm(tem_ctx* ctx, const void* x, const float* labels, const float* gt, const int32_t* n_gt,
+                        float* loss_out, void* stream);
+tem_status tem_compute_pgm(tem_ctx* ctx, const void* x, const float* labels, const float* gt,
+                           const int32_t* n_gt, float* loss_out, void* stream);
 
 /* PGM, BSN's proposal generation (reading R24; the paper names the
  * stage at P:85): for each of B videos, candidate boundaries of TEM's start / end probability

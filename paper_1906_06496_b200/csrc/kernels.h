@@ -57,6 +57,7 @@ struct Geom {
     // PEM (joint TEM + PEM step, BASELINE configs[4]): pem_P proposals per video, 0 = off;
     // its parameters follow TEM's in the flat vector at off_pem (reading R21)
     int pem_P, pem_F, pem_H;
+    int pgm_G;  // > 0: PEM's inputs come from PGM on this step's TEM output (reading R24)
     int64_t off_pem;
 };
 inline int64_t pem_num_params_of(const Geom& g) {
@@ -169,7 +170,7 @@ cudaError_t launch_relu_decisions(const Geom& g, const RankBufs& b, uint8_t* out
 // Kernel slots of one step (for tem_timing_*): every launch is bracketed by
 // ev[2*slot] / ev[2*slot+1] when ev != nullptr.
 enum Slot { SLOT_PREP = 0, SLOT_CONV1, SLOT_CONV2, SLOT_HEAD, SLOT_HEADFIN, SLOT_DGRAD, SLOT_WGRAD2,
-            SLOT_RED2, SLOT_WGRAD1, SLOT_RED1, SLOT_EXCHANGE, SLOT_PEM, SLOT_PEMRED, SLOT_EXCH2,
+            SLOT_RED2, SLOT_WGRAD1, SLOT_RED1, SLOT_EXCHANGE, SLOT_PEM, SLOT_PEMRED, SLOT_EXCH2, SLOT_PGM,
             NUM_SLOTS };
 const char* slot_name(int slot);
 // kernel-span trace buffers (diagnostics): one setter per translation unit with traced kernels
@@ -241,7 +242,8 @@ struct RingLocal {
 };
 // PGM (pgm.cu, reading R24): proposals, BSP features, IoU targets of B videos (T <= 128)
 cudaError_t launch_pgm(int B, int T, int G, int P, const float* prob, const float* gt, const int32_t* n_gt,
-                       float* feat, float* iou, int32_t* ts, int32_t* te, int32_t* count, cudaStream_t s);
+                       float* feat, float* iou, int32_t* ts, int32_t* te, int32_t* count, cudaStream_t s,
+                       const float* z = nullptr, float* prob_out = nullptr);
 constexpr int kMaxChannels = 128;
 constexpr int kMaxChunks = 16;
 struct RingParams {

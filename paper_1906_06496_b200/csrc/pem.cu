@@ -23,7 +23,9 @@
 namespace tem {
 namespace {
 
-constexpr int PEM_F = 32, PEM_H = 512, PEM_THREADS = 256, PEM_RB = 8;  // rows per batch
+// PEM_U hidden units per thread (PEM_U = 1: 512 threads at ~110 registers, 16 warps per SM;
+// PEM_U = 2 ran 256 threads at 222 registers, 8 warps, latency-bound at IPC 0.6)
+constexpr int PEM_F = 32, PEM_H = 512, PEM_U = 1, PEM_THREADS = PEM_H / PEM_U, PEM_RB = 8;  // rows per batch
 
 __global__ void __launch_bounds__(PEM_THREADS, 1) pem_kernel(const float* __restrict__ f, const float* __restrict__ g,
                                                           const float* __restrict__ prm, int M, int rows_per_cta,
@@ -36,24 +38,34 @@ __global__ void __launch_bounds__(PEM_THREADS, 1) pem_kernel(const float* __rest
     __shared__ float zred[PEM_RB][PEM_THREADS / 32];
     __shared__ float dzs[PEM_RB];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    extern __shared__ float w1s[];  // [H][F + 1]: W1 staging, then the dW1 partial's transpose
     const float* W1 = prm;
     const float* b1 = prm + PEM_H * PEM_F;
     const float* w2 = b1 + PEM_H;
     const float b2 = w2[PEM_H];
-    float w[2][PEM_F], acc[2][PEM_F];
-    float bb[2], ww[2], gb[2] = {0.f, 0.f}, gw[2] = {0.f, 0.f};
+    float w[PEM_U][PEM_F], acc[PEM_U][PEM_F];
+    float bb[PEM_U], ww[PEM_U], gb[PEM_U], gw[PEM_U];
+#pragma unroll
+    for (int u = 0; u < PEM_U; ++u) gb[u] = gw[u] = 0.f;
     {
         // W1 rows via shared memory: fully coalesced loads (consecutive threads, consecutive
-        // floats), then each thread reads its two rows from a 33-float padded layout (conflict
+        // floats), then each thread reads its rows from a 33-float padded layout (conflict
         // free).  Direct row loads were 32 cache lines per warp instruction.
-        extern __shared__ float w1s[];  // [H][F + 1]
-        for (int i = tid; i < PEM_H * PEM_F; i += PEM_THREADS) {
-            const int j = i / PEM_F, k = i - j * PEM_F;
-            w1s[j * (PEM_F + 1) + k] = __ldg(W1 + i);
+        // All loads of a thread are issued before its first shared store (the rolled loop
+        // waited on every load: 40 % of the kernel's stall samples).  Scalar: W1 starts at the
+        // flat offset off_pem, not 16-byte aligned.
+        constexpr int NV = PEM_H * PEM_F / PEM_THREADS;
+        float v[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) v[q] = __ldg(W1 + tid + q * PEM_THREADS);
+#pragma unroll
+        for (int q = 0; q < NV; ++q) {
+            const int i = tid + q * PEM_THREADS, j = i / PEM_F, k = i - j * PEM_F;
+            w1s[j * (PEM_F + 1) + k] = v[q];
         }
         __syncthreads();
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < PEM_U; ++u) {
             const int j = tid + u * PEM_THREADS;
 #pragma unroll
             for (int k = 0; k < PEM_F; ++k) w[u][k] = w1s[j * (PEM_F + 1) + k];
@@ -69,18 +81,18 @@ __global__ void __launch_bounds__(PEM_THREADS, 1) pem_kernel(const float* __rest
     for (int mb = m0; mb < m1; mb += PEM_RB) {
         const int nr = min(PEM_RB, m1 - mb);
         // feature tile: 8 rows x 32 = 256 floats, one per thread
-        {
+        if (tid < PEM_RB * PEM_F) {
             const int r = tid / PEM_F, k = tid % PEM_F;
             fs[r][k] = r < nr ? f[(size_t)(mb + r) * PEM_F + k] : 0.f;
         }
         __syncthreads();
-        float h[PEM_RB][2];
-        bool pos[PEM_RB][2];
+        float h[PEM_RB][PEM_U];
+        bool pos[PEM_RB][PEM_U];
 #pragma unroll
         for (int r = 0; r < PEM_RB; ++r) {
             float zp = 0.f;
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < PEM_U; ++u) {
                 float a = bb[u];
 #pragma unroll
                 for (int k = 0; k < PEM_F; ++k) a = fmaf(w[u][k], fs[r][k], a);
@@ -88,7 +100,9 @@ __global__ void __launch_bounds__(PEM_THREADS, 1) pem_kernel(const float* __rest
                 h[r][u] = pos[r][u] ? a : 0.f;
                 if (dec_out && r < nr) dec_out[(size_t)(mb + r) * PEM_H + tid + u * PEM_THREADS] = pos[r][u] ? 1 : 0;
             }
-            zp = fmaf(ww[1], h[r][1], ww[0] * h[r][0]);
+            zp = ww[0] * h[r][0];
+#pragma unroll
+            for (int u = 1; u < PEM_U; ++u) zp = fmaf(ww[u], h[r][u], zp);
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) zp += __shfl_xor_sync(0xffffffffu, zp, off);
             if (lane == 0) zred[r][warp] = zp;
@@ -114,7 +128,7 @@ __global__ void __launch_bounds__(PEM_THREADS, 1) pem_kernel(const float* __rest
             if (r >= nr) break;
             const float d = dzs[r];
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
+            for (int u = 0; u < PEM_U; ++u) {
                 gw[u] = fmaf(d, h[r][u], gw[u]);
                 const float dh = pos[r][u] ? d * ww[u] : 0.f;
                 gb[u] += dh;
@@ -125,13 +139,20 @@ __global__ void __launch_bounds__(PEM_THREADS, 1) pem_kernel(const float* __rest
         __syncthreads();  // fs / zred / dzs reused by the next batch
     }
     float* dst = part + (size_t)blockIdx.x * (KP + 1);
+    // dW1 rows through the padded shared buffer so the global stores are coalesced (a thread's
+    // own 32-float row was 32 sectors per warp store)
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < PEM_U; ++u) {
         const int j = tid + u * PEM_THREADS;
 #pragma unroll
-        for (int k = 0; k < PEM_F; ++k) dst[(size_t)j * PEM_F + k] = acc[u][k];
+        for (int k = 0; k < PEM_F; ++k) w1s[j * (PEM_F + 1) + k] = acc[u][k];
         dst[PEM_H * PEM_F + j] = gb[u];
         dst[PEM_H * PEM_F + PEM_H + j] = gw[u];
+    }
+    __syncthreads();
+    for (int i = tid; i < PEM_H * PEM_F; i += PEM_THREADS) {
+        const int j = i / PEM_F, k = i - j * PEM_F;
+        dst[i] = w1s[j * (PEM_F + 1) + k];
     }
     if (tid == 0) {
         dst[KP - 1] = gb2;
@@ -140,21 +161,47 @@ __global__ void __launch_bounds__(PEM_THREADS, 1) pem_kernel(const float* __rest
     trace_end(SLOT_PEM);
 }
 
-// grad[e] = sum over CTA partials in CTA order; loss = sum_j L_j / M; NONFINITE latch.
-__global__ void pem_reduce_kernel(const float* __restrict__ part, int G, int M, float* __restrict__ grad,
-                                  float* __restrict__ loss_out, Status* status, const int64_t* stepctr) {
+// grad[e] = sum over the G CTA partials; loss = sum_j L_j / M; NONFINITE latch.  A CTA of 8
+// warps owns 32 consecutive elements: warp w sums the partials j = w, w + 8, ... in ascending j
+// (coalesced 128-byte rows), then the 8 warp sums are added in warp order -- a fixed order,
+// so the result is deterministic.  (One thread per element summing all G serially was
+// 10.6 us for 10 MB at c5.)
+constexpr int PEMRED_W = 8;
+__global__ void __launch_bounds__(32 * PEMRED_W) pem_reduce_kernel(const float* __restrict__ part, int G, int M,
+                                                                   float* __restrict__ grad, float* __restrict__ loss_out,
+                                                                   Status* status, const int64_t* stepctr) {
     trace_begin(SLOT_PEMRED);
     pdl_trigger();
     pdl_wait();
     constexpr int KP = PEM_H * PEM_F + 2 * PEM_H + 1;
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    __shared__ float ws[PEMRED_W][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int e = blockIdx.x * 32 + lane;
+    float s = 0.f;
     if (e <= KP) {
-        float s = 0.f;
-        for (int j = 0; j < G; ++j) s += part[(size_t)j * (KP + 1) + e];
+        int j = warp;
+        for (; j + 3 * PEMRED_W < G; j += 4 * PEMRED_W) {  // 4 loads in flight per lane
+            const float a0 = __ldcs(part + (size_t)j * (KP + 1) + e);
+            const float a1 = __ldcs(part + (size_t)(j + PEMRED_W) * (KP + 1) + e);
+            const float a2 = __ldcs(part + (size_t)(j + 2 * PEMRED_W) * (KP + 1) + e);
+            const float a3 = __ldcs(part + (size_t)(j + 3 * PEMRED_W) * (KP + 1) + e);
+            s += a0;
+            s += a1;
+            s += a2;
+            s += a3;
+        }
+        for (; j < G; j += PEMRED_W) s += __ldcs(part + (size_t)j * (KP + 1) + e);
+    }
+    ws[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && e <= KP) {
+        float t = ws[0][lane];
+#pragma unroll
+        for (int w = 1; w < PEMRED_W; ++w) t += ws[w][lane];
         if (e < KP) {
-            grad[e] = s;
+            grad[e] = t;
         } else {
-            const float L = M > 0 ? s / (float)M : 0.f;
+            const float L = M > 0 ? t / (float)M : 0.f;
             *loss_out = L;
             if (!isfinite(L)) latch(status, TEM_ERR_NONFINITE, stepctr ? *stepctr : 0);
         }
@@ -209,7 +256,7 @@ cudaError_t launch_pem(const Geom& g, const float* f, const float* iou, const fl
         return cudaErrorUnknown;
     const int KP = (int)pem_num_params_of(g);
     rec.begin(SLOT_PEMRED);
-    e = launch_pdl(pem_reduce_kernel, dim3((KP + 1 + 255) / 256), dim3(256), 0, s_red, true, (const float*)part, G, M, grad,
+    e = launch_pdl(pem_reduce_kernel, dim3((KP + 1 + 31) / 32), dim3(32 * PEMRED_W), 0, s_red, true, (const float*)part, G, M, grad,
                    loss_out, status, stepctr);
     rec.end(SLOT_PEMRED);
     if (e == cudaSuccess) ++*n;

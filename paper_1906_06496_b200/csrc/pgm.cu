@@ -5,10 +5,11 @@
 // One CTA of 1024 threads per video (T <= 128):
 //   1. p_a, p_s, p_e into shared memory; max of p_s / p_e by warp shuffles; candidate flags
 //      p[t] > fl(0.9 max) or a strict interior peak, compacted in ascending t with ballots;
-//   2. every (start, end) candidate pair -> one 64-bit key ((~bits(c)) << 32 | t_s << 16 | t_e),
-//      c = fl(p_s[t_s] p_e[t_e]) >= 0, so ascending keys = (c desc, t_s asc, t_e asc); pairs
-//      with t_s >= t_e get the key ~0 (last);
-//   3. bitonic sort of the keys in shared memory (<= 16384 keys, 128 KB);
+//   2. every (start, end) candidate pair with t_s < t_e has the 64-bit key
+//      ((~bits(c)) << 32 | t_s << 16 | t_e), c = fl(p_s[t_s] p_e[t_e]) >= 0, so ascending keys =
+//      (c desc, t_s asc, t_e asc); a 4-pass 8-bit radix select finds the P-th smallest ~bits(c);
+//   3. the pairs at or below it (P plus ties) are collected and bitonic-sorted in shared memory
+//      (<= 16384 keys, 128 KB; a full sort measured 103 us per step at c6, the select ~10x less);
 //   4. the first P keys -> (t_s, t_e), IoU target and the 32 interpolated samples of p_a,
 //      one thread per (proposal, sample).
 // Decisions (flags, scores, order) are fp32 and bit-identical to the oracle; features / IoU
@@ -22,7 +23,7 @@
 namespace tem {
 namespace {
 
-constexpr int PGM_THREADS = 1024, PGM_TMAX = 128;
+constexpr int PGM_THREADS = 1024, PGM_TMAX = 128, PGM_SELMAX = 4096;
 constexpr int PGM_NS = 8, PGM_NC = 16, PGM_NE = 8, PGM_F = PGM_NS + PGM_NC + PGM_NE;
 
 __device__ __forceinline__ float pgm_at(const float* p, int T, int j) { return (j >= 0 && j < T) ? p[j] : 0.0f; }
@@ -32,6 +33,16 @@ __device__ __forceinline__ float pgm_interp(const float* pa, int T, float x) {
     const int i = (int)fi;
     const float f = x - fi;
     return (1.0f - f) * pgm_at(pa, T, i) + f * pgm_at(pa, T, i + 1);
+}
+
+// Slot of this lane in a shared array filled by a counter: one atomic per warp (all lanes call).
+__device__ __forceinline__ int warp_slot(bool take, int* counter) {
+    const unsigned m = __ballot_sync(0xffffffffu, take);
+    const int lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == 0 && m) base = atomicAdd(counter, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    return base + __popc(m & ((1u << lane) - 1u));
 }
 
 __device__ float block_max(float v, float* red) {
@@ -52,6 +63,7 @@ __device__ float block_max(float v, float* red) {
 }
 
 __global__ void __launch_bounds__(PGM_THREADS) pgm_kernel(int T, int G, int P, const float* __restrict__ prob,
+                                                          const float* __restrict__ z, float* __restrict__ prob_out,
                                                           const float* __restrict__ gt,
                                                           const int32_t* __restrict__ n_gt,
                                                           float* __restrict__ feat, float* __restrict__ iou,
@@ -62,15 +74,26 @@ __global__ void __launch_bounds__(PGM_THREADS) pgm_kernel(int T, int G, int P, c
     __shared__ float red[32];
     __shared__ int cs[PGM_TMAX], ce[PGM_TMAX];
     __shared__ int wcount[2][PGM_TMAX / 32];
-    __shared__ int nvalid;
+    __shared__ int nvalid, nsel, sel[2];
+    __shared__ unsigned hist[256];
     const int v = blockIdx.x, tid = threadIdx.x;
-    const float* pv = prob + (size_t)v * 3 * T;
-    if (tid < T) {
-        pa[tid] = pv[tid];
-        ps[tid] = pv[T + tid];
-        pe[tid] = pv[2 * T + tid];
+    if (z) {  // in-step use: p = sigmoid(z) of TEM's logits z [B][T][3], kept in prob_out [B][3][T]
+        if (tid < T) {
+            const float* zv = z + ((size_t)v * T + tid) * 3;
+            float* po = prob_out + (size_t)v * 3 * T;
+            pa[tid] = po[tid] = 1.0f / (1.0f + expf(-zv[0]));
+            ps[tid] = po[T + tid] = 1.0f / (1.0f + expf(-zv[1]));
+            pe[tid] = po[2 * T + tid] = 1.0f / (1.0f + expf(-zv[2]));
+        }
+    } else {
+        const float* pv = prob + (size_t)v * 3 * T;
+        if (tid < T) {
+            pa[tid] = pv[tid];
+            ps[tid] = pv[T + tid];
+            pe[tid] = pv[2 * T + tid];
+        }
     }
-    if (tid == 0) nvalid = 0;
+    if (tid == 0) nvalid = nsel = 0;
     __syncthreads();
     // 1. candidates
     const float ms = block_max(tid < T ? ps[tid] : -INFINITY, red);
@@ -102,51 +125,118 @@ __global__ void __launch_bounds__(PGM_THREADS) pgm_kernel(int T, int G, int P, c
     if (fs) cs[offs + __popc(bs & below)] = tid;
     if (fe) ce[offe + __popc(be & below)] = tid;
     __syncthreads();
-    // 2. keys of all candidate pairs, padded to a power of two with ~0
+    // 2. the valid pairs' keys into shared memory (order irrelevant: they are ranked below);
+    //    then a radix select on u = ~bits(c), 8 bits per pass, finds the P-th smallest u
+    //    (ascending u = descending c)
+    unsigned long long* all = keys;                      // [T*T] pair keys
+    unsigned long long* top = keys + PGM_TMAX * PGM_TMAX;  // [PGM_SELMAX] selected keys
     const int npair = nS * nE;
-    int npow = 1;
-    while (npow < npair) npow <<= 1;
-    int myvalid = 0;
-    for (int i = tid; i < npow; i += PGM_THREADS) {
-        unsigned long long k = ~0ull;
+    for (int i0 = 0; i0 < npair; i0 += PGM_THREADS) {  // warp-aggregated compaction
+        const int i = i0 + tid;
+        int a = 0, b = 0;
         if (i < npair) {
-            const int a = cs[i / nE], b = ce[i % nE];
-            if (a < b) {
-                const float c = __fmul_rn(ps[a], pe[b]);
-                k = ((unsigned long long)(~__float_as_uint(c)) << 32) | ((unsigned long long)a << 16) |
-                    (unsigned long long)b;
-                ++myvalid;
-            }
+            a = cs[i / nE];
+            b = ce[i % nE];
         }
-        keys[i] = k;
+        const bool ok = i < npair && a < b;
+        const int pos = warp_slot(ok, &nvalid);
+        if (ok) {
+            const unsigned u = ~__float_as_uint(__fmul_rn(ps[a], pe[b]));
+            all[pos] = ((unsigned long long)u << 32) | ((unsigned long long)a << 16) | (unsigned long long)b;
+        }
     }
-    if (myvalid) atomicAdd(&nvalid, myvalid);
     __syncthreads();
-    // 3. bitonic sort, ascending
+    const int nv = nvalid;
+    unsigned prefix = 0xffffffffu;  // nv <= P: every valid pair is kept
+    if (nv > P) {
+        prefix = 0u;
+        unsigned mask = 0u;
+        int rank = P;  // 1-based rank still to locate among the pairs matching prefix / mask
+        for (int shift = 24; shift >= 0; shift -= 8) {
+            for (int q = tid; q < 256; q += PGM_THREADS) hist[q] = 0u;
+            __syncthreads();
+            for (int i = tid; i < nv; i += PGM_THREADS) {
+                const unsigned u = (unsigned)(all[i] >> 32);
+                if ((u & mask) == prefix) atomicAdd(&hist[(u >> shift) & 255u], 1u);
+            }
+            __syncthreads();
+            if (tid < 32) {  // smallest digit whose cumulative count reaches rank
+                unsigned loc[8], sum = 0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    loc[q] = hist[8 * tid + q];
+                    sum += loc[q];
+                }
+                unsigned incl = sum;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (tid >= o) incl += y;
+                }
+                const unsigned excl = incl - sum;
+                const unsigned hit = __ballot_sync(0xffffffffu, incl >= (unsigned)rank);
+                const int lane = __ffs(hit) - 1;
+                if (tid == lane) {
+                    unsigned c = excl;
+                    int d = -1;
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        if (d < 0) {
+                            if (c + loc[q] >= (unsigned)rank) d = q;
+                            else c += loc[q];
+                        }
+                    sel[0] = 8 * lane + d;
+                    sel[1] = rank - (int)c;
+                }
+            }
+            __syncthreads();
+            prefix |= (unsigned)sel[0] << shift;
+            mask |= 255u << shift;
+            rank = sel[1];
+            __syncthreads();
+        }
+    }
+    // 3. the pairs at or below the P-th u (P plus its ties) are ranked by the full key with a
+    //    bitonic sort; with more than PGM_SELMAX of them (massive ties) all pairs are sorted
+    for (int i0 = 0; i0 < nv; i0 += PGM_THREADS) {
+        const int i = i0 + tid;
+        const unsigned long long k = i < nv ? all[i] : ~0ull;
+        const bool ok = i < nv && (unsigned)(k >> 32) <= prefix;
+        const int pos = warp_slot(ok, &nsel);
+        if (ok && pos < PGM_SELMAX) top[pos] = k;
+    }
+    __syncthreads();
+    const int m = nsel;
+    unsigned long long* srt = m <= PGM_SELMAX ? top : all;
+    const int ns = m <= PGM_SELMAX ? m : nv;
+    int npow = 1;
+    while (npow < ns) npow <<= 1;
+    for (int i = ns + tid; i < npow; i += PGM_THREADS) srt[i] = ~0ull;
+    __syncthreads();
     for (int kk = 2; kk <= npow; kk <<= 1)
-        for (int j = kk >> 1; j > 0; j >>= 1) {
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
             for (int i = tid; i < npow; i += PGM_THREADS) {
-                const int ixj = i ^ j;
+                const int ixj = i ^ jj;
                 if (ixj > i) {
-                    const unsigned long long x = keys[i], y = keys[ixj];
+                    const unsigned long long x = srt[i], y = srt[ixj];
                     const bool up = (i & kk) == 0;
                     if ((x > y) == up) {
-                        keys[i] = y;
-                        keys[ixj] = x;
+                        srt[i] = y;
+                        srt[ixj] = x;
                     }
                 }
             }
             __syncthreads();
         }
     // 4. outputs
-    const int n = min(P, nvalid);
+    const int n = min(P, nv);
     if (tid == 0) count[v] = n;
     const int ng = min(n_gt[v], G);
     for (int i = tid; i < P; i += PGM_THREADS) {
         int a = -1, b = -1;
         float g = 0.0f;
         if (i < n) {
-            const unsigned long long k = keys[i];
+            const unsigned long long k = srt[i];
             a = (int)((k >> 16) & 0xffff);
             b = (int)(k & 0xffff);
             const float s1 = (float)a + 0.5f, e1 = (float)b + 0.5f;
@@ -165,7 +255,7 @@ __global__ void __launch_bounds__(PGM_THREADS) pgm_kernel(int T, int G, int P, c
         const int i = idx / PGM_F, k = idx - i * PGM_F;
         float val = 0.0f;
         if (i < n) {
-            const unsigned long long key = keys[i];
+            const unsigned long long key = srt[i];
             const int a = (int)((key >> 16) & 0xffff), b = (int)(key & 0xffff);
             const float d = (float)(b - a);
             float lo, hi;
@@ -186,18 +276,18 @@ __global__ void __launch_bounds__(PGM_THREADS) pgm_kernel(int T, int G, int P, c
 }  // namespace
 
 cudaError_t launch_pgm(int B, int T, int G, int P, const float* prob, const float* gt, const int32_t* n_gt,
-                       float* feat, float* iou, int32_t* ts, int32_t* te, int32_t* count, cudaStream_t s) {
+                       float* feat, float* iou, int32_t* ts, int32_t* te, int32_t* count, cudaStream_t s,
+                       const float* z, float* prob_out) {
     if (B == 0) return cudaSuccess;
-    int npow = 1;
-    while (npow < T * T) npow <<= 1;
-    const size_t smem = sizeof(unsigned long long) * npow;
+    // all pairs [PGM_TMAX^2] (padded to a power of two for the tie fallback) + the selection
+    const size_t smem = sizeof(unsigned long long) * (PGM_TMAX * PGM_TMAX + PGM_SELMAX);
     static size_t attr = 0;
     if (smem > attr) {
         cudaError_t e = cudaFuncSetAttribute(pgm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
         attr = smem;
     }
-    pgm_kernel<<<B, PGM_THREADS, smem, s>>>(T, G, P, prob, gt, n_gt, feat, iou, ts, te, count);
+    pgm_kernel<<<B, PGM_THREADS, smem, s>>>(T, G, P, prob, z, prob_out, gt, n_gt, feat, iou, ts, te, count);
     return cudaGetLastError();
 }
 

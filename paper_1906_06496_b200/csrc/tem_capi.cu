@@ -59,7 +59,8 @@ struct HeapLayout {
 
 struct WsLayout {
     size_t xp, h1, h2, dA2, dA1, xp_lo, h1_lo, dA2_lo, dA1_lo, z, grad, headpart, headlvl1, counter, bpart, wpart, wpart2, shadow,
-        shadow_lo, ones, zpart, epochs, stepctr, xstage, labstage, lossstage, bspstage, ioustage, pempart, pemdec, opt_m, opt_v, opt_scal, per_rank;
+        shadow_lo, ones, zpart, epochs, stepctr, xstage, labstage, lossstage, bspstage, ioustage, pempart, pemdec, opt_m, opt_v, opt_scal,
+        pgm_prob, pgm_feat, pgm_iou, pgm_ts, pgm_te, pgm_count, per_rank;
 };
 
 bool cfg_valid(const tem_config* c) {
@@ -82,6 +83,7 @@ bool cfg_valid(const tem_config* c) {
         return false;
     if (c->pem_proposals < 0) return false;
     if (c->pem_proposals > 0 && (c->pem_features != 32 || c->pem_hidden != 512)) return false;  // kernel shape
+    if (c->pgm_gt_max < 0 || (c->pgm_gt_max > 0 && (c->pem_proposals <= 0 || c->seq_len > 128))) return false;
     if (c->optimizer != TEM_OPT_SGD && c->optimizer != TEM_OPT_ADAM && c->optimizer != TEM_OPT_MOMENTUM) return false;
     if (c->optimizer == TEM_OPT_MOMENTUM && !(c->momentum >= 0.0f && c->momentum < 1.0f)) return false;
     if (c->optimizer == TEM_OPT_ADAM &&
@@ -129,6 +131,7 @@ Geom make_geom(const tem_config* c) {
     g.off_W3 = g.off_b2 + g.C;
     g.off_b3 = g.off_W3 + (int64_t)g.Co * g.C;
     g.pem_P = c->pem_proposals;
+    g.pgm_G = c->pgm_gt_max;
     g.pem_F = c->pem_proposals > 0 ? c->pem_features : 0;
     g.pem_H = c->pem_proposals > 0 ? c->pem_hidden : 0;
     g.off_pem = tem_params_only(c);
@@ -209,6 +212,13 @@ WsLayout ws_layout(const tem_config* c) {
     w.opt_m = take(state1 * (size_t)g.Kpad * 4);
     w.opt_v = take(adam * (size_t)g.Kpad * 4);
     w.opt_scal = take(adam * 8);
+    const size_t pgm = g.pgm_G > 0 ? 1 : 0;  // PGM-fed PEM (reading R24)
+    w.pgm_prob = take(pgm * (size_t)g.B * 3 * g.T * 4);
+    w.pgm_feat = take(pgm * (size_t)g.B * g.pem_P * 32 * 4);
+    w.pgm_iou = take(pgm * (size_t)g.B * g.pem_P * 4);
+    w.pgm_ts = take(pgm * (size_t)g.B * g.pem_P * 4);
+    w.pgm_te = take(pgm * (size_t)g.B * g.pem_P * 4);
+    w.pgm_count = take(pgm * (size_t)g.B * 4);
     w.per_rank = o;
     return w;
 }
@@ -242,12 +252,16 @@ struct tem_ctx {
     bool loss_host_done;
     const float* pem_bsp;      // tem_*_pem: this call's PEM inputs (nullptr: TEM-only call)
     const float* pem_iou;
+    const float* pgm_gt;       // tem_*_pgm: this call's ground truth [nlocal][B][G][2] / counts
+    const int32_t* pgm_ngt;
     bool pem_record_dec;       // record the PEM ReLU decisions (tem_pem_relu_decisions)
     struct GraphEntry {
         const void* x;
         const void* lab;
         const void* bsp;
         const void* iou;
+        const void* gt;
+        const void* ngt;
         void* loss;
         void* loss_host;
         cudaGraphExec_t exec;
@@ -274,7 +288,7 @@ tem_status graph_step(tem_ctx* c, const void* x, const void* lab, void* loss, cu
     for (int i = 0; i < c->ngraphs; ++i)
         if (c->graphs[i].x == x && c->graphs[i].lab == lab && c->graphs[i].loss == loss &&
             c->graphs[i].loss_host == c->loss_host_pending && c->graphs[i].bsp == c->pem_bsp &&
-            c->graphs[i].iou == c->pem_iou)
+            c->graphs[i].iou == c->pem_iou && c->graphs[i].gt == c->pgm_gt && c->graphs[i].ngt == c->pgm_ngt)
             e = &c->graphs[i];
     if (!e) {
         if (c->ngraphs == tem_ctx::kMaxGraphs) {  // evict the oldest
@@ -305,6 +319,8 @@ tem_status graph_step(tem_ctx* c, const void* x, const void* lab, void* loss, cu
         e->loss_host = c->loss_host_pending;
         e->bsp = c->pem_bsp;
         e->iou = c->pem_iou;
+        e->gt = c->pgm_gt;
+        e->ngt = c->pgm_ngt;
         e->exec = exec;
         e->launches = nl;
     }
@@ -528,7 +544,7 @@ static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, f
         const SplitUpdate su{opt_cfg(c), opt_state(c, l)};
         c->split_done = defer && split_on;
         float* lh = (c->nlocal == 1) ? c->loss_host_pending : nullptr;
-        if (g.pem_P > 0) {
+        if (g.pem_P > 0 && g.pgm_G == 0) {
             // PEM (configs[4]) is independent of TEM: on the tcgen05 path it runs on the side
             // stream from the start of the step, beside the TEM forward GEMMs
             const int M = g.B * g.pem_P;
@@ -552,6 +568,25 @@ static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, f
         else
             e = simt_compute(g, c->rb[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s);
         if (e != cudaSuccess) return TEM_ERR_CUDA;
+        if (g.pem_P > 0 && g.pgm_G > 0 && g.B > 0) {
+            // PGM-fed PEM (reading R24): proposals and BSP features from this step's logits
+            // (stop-gradient), then PEM on them -- after the TEM compute, on the step's stream
+            char* base = c->ws_base[l];
+            float* feat = (float*)(base + c->wl.pgm_feat);
+            float* iou = (float*)(base + c->wl.pgm_iou);
+            rec.begin(SLOT_PGM);
+            e = launch_pgm(g.B, g.T, g.pgm_G, g.pem_P, nullptr, c->pgm_gt + (size_t)l * g.B * g.pgm_G * 2,
+                           c->pgm_ngt + (size_t)l * g.B, feat, iou, (int32_t*)(base + c->wl.pgm_ts),
+                           (int32_t*)(base + c->wl.pgm_te), (int32_t*)(base + c->wl.pgm_count), s, c->rb[l].z,
+                           (float*)(base + c->wl.pgm_prob));
+            rec.end(SLOT_PGM);
+            if (e != cudaSuccess) return TEM_ERR_CUDA;
+            ++*nl;
+            e = launch_pem(g, feat, iou, c->rb[l].params + g.off_pem, c->rb[l].pempart, c->rb[l].grad + g.off_pem,
+                           loss_out + 4 * c->nlocal + l, c->st_dev, c->rb[l].stepctr,
+                           c->pem_record_dec ? c->rb[l].pemdec : nullptr, s, s, nullptr, nl, rec);
+            if (e != cudaSuccess) return TEM_ERR_CUDA;
+        }
     }
     return TEM_OK;
 }
@@ -708,7 +743,43 @@ tem_status tem_step(tem_ctx* c, const void* x, const float* labels, float* loss_
 
 // Joint TEM + PEM (configs[4]): the PEM inputs ride along in the ctx for this call only.
 static bool pem_args_ok(tem_ctx* c, const float* bsp, const float* iou) {
-    return c->g.pem_P > 0 && ((bsp && iou) || c->g.B == 0);
+    return c->g.pem_P > 0 && c->g.pgm_G == 0 && ((bsp && iou) || c->g.B == 0);
+}
+
+static bool pgm_args_ok(tem_ctx* c, const float* gt, const int32_t* n_gt) {
+    return c->g.pgm_G > 0 && ((gt && n_gt) || c->g.B == 0);
+}
+
+tem_status tem_step_pgm(tem_ctx* c, const void* x, const float* labels, const float* gt, const int32_t* n_gt,
+                        float* loss_out, void* stream) {
+    tem_status st = check_ctx(c);
+    if (st != TEM_OK) return st;
+    if (!pgm_args_ok(c, gt, n_gt)) return TEM_ERR_INVALID_ARG;
+    static const float kDummy = 0.f;
+    c->pem_bsp = &kDummy;  // marks a PEM call
+    c->pgm_gt = gt;
+    c->pgm_ngt = n_gt;
+    st = tem_step(c, x, labels, loss_out, stream);
+    c->pem_bsp = nullptr;
+    c->pgm_gt = nullptr;
+    c->pgm_ngt = nullptr;
+    return st;
+}
+
+tem_status tem_compute_pgm(tem_ctx* c, const void* x, const float* labels, const float* gt, const int32_t* n_gt,
+                           float* loss_out, void* stream) {
+    tem_status st = check_ctx(c);
+    if (st != TEM_OK) return st;
+    if (!pgm_args_ok(c, gt, n_gt)) return TEM_ERR_INVALID_ARG;
+    static const float kDummy = 0.f;
+    c->pem_bsp = &kDummy;
+    c->pgm_gt = gt;
+    c->pgm_ngt = n_gt;
+    st = tem_compute(c, x, labels, loss_out, stream);
+    c->pem_bsp = nullptr;
+    c->pgm_gt = nullptr;
+    c->pgm_ngt = nullptr;
+    return st;
 }
 
 tem_status tem_step_pem(tem_ctx* c, const void* x, const float* labels, const float* bsp, const float* iou,
@@ -759,8 +830,8 @@ tem_status tem_pem_relu_decisions(tem_ctx* c, int32_t l, uint8_t* out, void* str
 // the set is reused two calls later, once the step that consumed it is done.  A caller that
 // issues steps back to back therefore overlaps the copy of step k+1 with the compute of step k.
 static tem_status host_stage(tem_ctx* c, cudaStream_t s, const void* x_host, const float* labels_host,
-                             const float* bsp_host, const float* iou_host, int* slot, void** xd, float** ld,
-                             float** bd, float** id) {
+                             const void* bsp_host, size_t bb, const void* iou_host, size_t ib, int* slot, void** xd,
+                             float** ld, float** bd, float** id) {
     const Geom& g = c->g;
     if (!c->cstream) {
         if (cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking) != cudaSuccess) return TEM_ERR_CUDA;
@@ -774,12 +845,14 @@ static tem_status host_stage(tem_ctx* c, cudaStream_t s, const void* x_host, con
     *slot = i;
     const size_t esz = g.prec == TEM_BF16 ? 2 : 4;
     const size_t xb = (size_t)g.B * g.T * g.Cin * esz, lb = (size_t)g.B * 3 * g.T * 4;
-    const size_t bb = (size_t)g.B * g.pem_P * g.pem_F * 4, ib = (size_t)g.B * g.pem_P * 4;
+    // the extra inputs' staging sets hold [B][P][F] / [B][P] floats (>= PGM's gt / counts)
+    const size_t bcap = (size_t)g.B * g.pem_P * g.pem_F * 4, icap = (size_t)g.B * g.pem_P * 4;
+    if (bb > bcap || ib > icap) return TEM_ERR_INVALID_ARG;
     char* base = c->ws_base[0];
     *xd = base + c->wl.xstage + i * xb;
     *ld = (float*)(base + c->wl.labstage + i * lb);
-    *bd = (float*)(base + c->wl.bspstage + i * bb);
-    *id = (float*)(base + c->wl.ioustage + i * ib);
+    *bd = (float*)(base + c->wl.bspstage + i * bcap);
+    *id = (float*)(base + c->wl.ioustage + i * icap);
     cudaStream_t cs = c->cstream;
     // one copy per tensor (measured: splitting x over parallel copy streams is slower)
     if (cudaStreamWaitEvent(cs, c->ev_consumed[i], 0) != cudaSuccess) return TEM_ERR_CUDA;
@@ -805,7 +878,7 @@ tem_status tem_step_host(tem_ctx* c, const void* x_host, const float* labels_hos
     int slot;
     void* xd;
     float *ld, *bd, *id;
-    st = host_stage(c, s, x_host, labels_host, nullptr, nullptr, &slot, &xd, &ld, &bd, &id);
+    st = host_stage(c, s, x_host, labels_host, nullptr, 0, nullptr, 0, &slot, &xd, &ld, &bd, &id);
     if (st != TEM_OK) return st;
     float* lossd = (float*)(c->ws_base[0] + c->wl.lossstage);
     c->loss_host_pending = loss_host;  // the tcgen05 path reads the loss back inside the step
@@ -830,10 +903,14 @@ tem_status tem_step_pem_host(tem_ctx* c, const void* x_host, const float* labels
     int slot;
     void* xd;
     float *ld, *bd, *id;
-    st = host_stage(c, s, x_host, labels_host, bsp_host, iou_host, &slot, &xd, &ld, &bd, &id);
+    const Geom& g = c->g;
+    const bool pgm = g.pgm_G > 0;  // PGM-fed: the extra inputs are the instances and their counts
+    const size_t bb = pgm ? (size_t)g.B * g.pgm_G * 2 * 4 : (size_t)g.B * g.pem_P * g.pem_F * 4;
+    const size_t ib = pgm ? (size_t)g.B * 4 : (size_t)g.B * g.pem_P * 4;
+    st = host_stage(c, s, x_host, labels_host, bsp_host, bb, iou_host, ib, &slot, &xd, &ld, &bd, &id);
     if (st != TEM_OK) return st;
     float* lossd = (float*)(c->ws_base[0] + c->wl.lossstage);
-    st = tem_step_pem(c, xd, ld, bd, id, lossd, stream);
+    st = pgm ? tem_step_pgm(c, xd, ld, bd, (const int32_t*)id, lossd, stream) : tem_step_pem(c, xd, ld, bd, id, lossd, stream);
     if (st != TEM_OK) return st;
     // [4 TEM | 1 PEM] floats, after the step
     if (cudaMemcpyAsync(loss_host, lossd, 5 * sizeof(float), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
@@ -1024,7 +1101,13 @@ void* tem_debug_buffer(tem_ctx* c, int32_t l, const char* name, int64_t* nbytes)
     const Item items[] = {
         {"xp", b.xp, xin}, {"h1", b.h1, act}, {"h2", b.h2, (int64_t)g.R * g.C * 4}, {"dA2", b.dA2, act},
         {"dA1", b.dA1, act}, {"xp_lo", b.xp_lo, xin}, {"h1_lo", b.h1_lo, act}, {"dA2_lo", b.dA2_lo, act},
-        {"dA1_lo", b.dA1_lo, act}, {"shadow", b.shadow, g.Kpad * 2}, {"shadow_lo", b.shadow_lo, g.Kpad * 2}};
+        {"dA1_lo", b.dA1_lo, act}, {"shadow", b.shadow, g.Kpad * 2}, {"shadow_lo", b.shadow_lo, g.Kpad * 2},
+        {"pgm_prob", c->ws_base[l] + c->wl.pgm_prob, g.pgm_G > 0 ? (int64_t)g.B * 3 * g.T * 4 : 0},
+        {"pgm_feat", c->ws_base[l] + c->wl.pgm_feat, g.pgm_G > 0 ? (int64_t)g.B * g.pem_P * 32 * 4 : 0},
+        {"pgm_iou", c->ws_base[l] + c->wl.pgm_iou, g.pgm_G > 0 ? (int64_t)g.B * g.pem_P * 4 : 0},
+        {"pgm_ts", c->ws_base[l] + c->wl.pgm_ts, g.pgm_G > 0 ? (int64_t)g.B * g.pem_P * 4 : 0},
+        {"pgm_te", c->ws_base[l] + c->wl.pgm_te, g.pgm_G > 0 ? (int64_t)g.B * g.pem_P * 4 : 0},
+        {"pgm_count", c->ws_base[l] + c->wl.pgm_count, g.pgm_G > 0 ? (int64_t)g.B * 4 : 0}};
     for (const Item& it : items)
         if (strcmp(it.n, name) == 0) {
             if (!it.p) return nullptr;

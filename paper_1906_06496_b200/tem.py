@@ -43,7 +43,7 @@ class tem_config(ctypes.Structure):
         ("exchange", ctypes.c_int32),
         ("pem_proposals", ctypes.c_int32), ("pem_features", ctypes.c_int32), ("pem_hidden", ctypes.c_int32),
         ("optimizer", ctypes.c_int32), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float), ("eps", ctypes.c_float),
-        ("momentum", ctypes.c_float),
+        ("momentum", ctypes.c_float), ("pgm_gt_max", ctypes.c_int32),
     ]
 
 
@@ -75,7 +75,7 @@ def lib():
         for f in (L.tem_step, L.tem_compute):
             f.restype = ctypes.c_int
             f.argtypes = [_P, _P, _P, _P, _P]
-        for f in (L.tem_step_pem, L.tem_compute_pem):
+        for f in (L.tem_step_pem, L.tem_compute_pem, L.tem_step_pgm, L.tem_compute_pgm):
             f.restype = ctypes.c_int
             f.argtypes = [_P, _P, _P, _P, _P, _P, _P]
         L.tem_pem_relu_decisions.restype = ctypes.c_int
@@ -127,7 +127,7 @@ EXPORTS = ["tem_num_params", "tem_kpad", "tem_workspace_bytes", "tem_sym_bytes",
            "tem_local_grad", "tem_logits", "tem_launches_per_step", "tem_launches_per_exchange",
            "tem_status_string", "tem_kernel_path", "tem_timing_slots", "tem_timing_slot_name",
            "tem_timing_begin", "tem_timing_end", "tem_relu_decisions", "tem_debug_buffer",
-           "tem_step_pem", "tem_compute_pem", "tem_pem_relu_decisions", "twoshot_allreduce", "tem_step_pem_host", "tem_pgm"]
+           "tem_step_pem", "tem_compute_pem", "tem_pem_relu_decisions", "twoshot_allreduce", "tem_step_pem_host", "tem_pgm", "tem_step_pgm", "tem_compute_pgm"]
 
 
 def status_string(code: int) -> str:
@@ -256,6 +256,7 @@ class SessionConfig:
     beta2: float = 0.999
     eps: float = 1e-8
     momentum: float = 0.9  # TEM_OPT_MOMENTUM (reading R23)
+    pgm_gt_max: int = 0  # > 0: PEM fed by PGM on the step's own TEM output (reading R24)
 
 
 class TemSession:
@@ -285,6 +286,7 @@ class TemSession:
         cfg.pem_proposals, cfg.pem_features, cfg.pem_hidden = sc.pem_proposals, sc.pem_features, sc.pem_hidden
         cfg.optimizer, cfg.beta1, cfg.beta2, cfg.eps = sc.optimizer, sc.beta1, sc.beta2, sc.eps
         cfg.momentum = sc.momentum
+        cfg.pgm_gt_max = sc.pgm_gt_max
         self.K = tem_num_params(cfg)
         if self.K == 0:
             raise TemError(TEM_ERR_INVALID_ARG, "config")
@@ -371,8 +373,10 @@ class TemSession:
         if not ptr:
             return None
         raw = self._ws_view(ptr, nb.value)
-        if name == "h2":
+        if name == "h2" or name in ("pgm_prob", "pgm_feat", "pgm_iou"):
             return raw.view(torch.float32)
+        if name in ("pgm_ts", "pgm_te", "pgm_count"):
+            return raw.view(torch.int32)
         elem = 2 if self.kernel_path().startswith("tcgen05") or self.sc.precision == TEM_BF16 else 4
         return raw.view(torch.bfloat16 if elem == 2 else torch.float32)
 
@@ -396,6 +400,21 @@ class TemSession:
         """Joint TEM + PEM step (configs[4]); returns (tem_loss [local_ranks][4], pem_loss [local_ranks])."""
         _check(lib().tem_step_pem(_P(self.ctx), _P(x.data_ptr()), _P(labels.data_ptr()), _P(bsp.data_ptr()),
                                   _P(iou.data_ptr()), _P(self.loss_pem.data_ptr()), _stream_ptr(stream)), "tem_step_pem")
+        n = self.sc.local_ranks
+        return self.loss_pem[:4 * n].view(n, 4), self.loss_pem[4 * n:]
+
+    def step_pgm(self, x: torch.Tensor, labels: torch.Tensor, gt: torch.Tensor, n_gt: torch.Tensor, stream=None):
+        """Joint TEM + PGM + PEM step (pgm_gt_max > 0): PEM on PGM's proposals of this step's TEM
+        output.  gt [local_ranks][B][G][2] fp32, n_gt [local_ranks][B] int32 (device)."""
+        _check(lib().tem_step_pgm(_P(self.ctx), _P(x.data_ptr()), _P(labels.data_ptr()), _P(gt.data_ptr()),
+                                  _P(n_gt.data_ptr()), _P(self.loss_pem.data_ptr()), _stream_ptr(stream)), "tem_step_pgm")
+        n = self.sc.local_ranks
+        return self.loss_pem[:4 * n].view(n, 4), self.loss_pem[4 * n:]
+
+    def compute_pgm(self, x: torch.Tensor, labels: torch.Tensor, gt: torch.Tensor, n_gt: torch.Tensor, stream=None):
+        _check(lib().tem_compute_pgm(_P(self.ctx), _P(x.data_ptr()), _P(labels.data_ptr()), _P(gt.data_ptr()),
+                                     _P(n_gt.data_ptr()), _P(self.loss_pem.data_ptr()), _stream_ptr(stream)),
+               "tem_compute_pgm")
         n = self.sc.local_ranks
         return self.loss_pem[:4 * n].view(n, 4), self.loss_pem[4 * n:]
 
