@@ -238,6 +238,8 @@ def main():
     ap.add_argument("--exchange", default="ring", choices=["ring", "ps", "twoshot"],
                     help="gradient exchange: the paper's ring (default), the PS comparator, or the "
                          "NVSwitch two-shot (ring-identical bits, 2 phases)")
+    ap.add_argument("--buckets", type=int, default=1, choices=[1, 2],
+                    help="N > 1: 2 = two-bucket exchange, the W2.. bucket overlapping conv1 wgrad (reading R25)")
     ap.add_argument("--optimizer", default="sgd", choices=["sgd", "adam", "momentum"],
                     help="owner update: the paper's SGD (default), Adam (reading R22) or heavy-ball "
                          "momentum 0.9 (reading R23)")
@@ -274,7 +276,7 @@ def main():
     sc = tem.SessionConfig(world_size=world, rank=rank, local_ranks=1, batch_per_rank=B, precision=prec,
                            lr=args.lr, exchange={"ps": tem.TEM_EXCHANGE_PS, "twoshot": tem.TEM_EXCHANGE_TWOSHOT}.get(
                                args.exchange, tem.TEM_EXCHANGE_RING),
-                           pem_proposals=P, pgm_gt_max=wl.get("pgm", 0),
+                           pem_proposals=P, pgm_gt_max=wl.get("pgm", 0), exchange_buckets=args.buckets,
                            optimizer={"adam": tem.TEM_OPT_ADAM, "momentum": tem.TEM_OPT_MOMENTUM}.get(
                                args.optimizer, tem.TEM_OPT_SGD))
     t_init0 = time.perf_counter()
@@ -467,6 +469,7 @@ def main():
         "config": {"workload": wl["desc"], "batch_per_gpu": B, "global_batch": B * world, "seq_len": T,
                    "channels": "400->512->512->3", "parallelism": f"dp{world}",
                    "optimizer": args.optimizer,
+                   **({"exchange_buckets": 2} if args.buckets == 2 and world > 1 else {}),
                    "exchange": ("N=1: owner update only" if world == 1 else
                                 {"ps": "parameter server on rank 0 (KP1)",
                                  "twoshot": "NVSwitch two-shot allreduce + mean + SGD (ring-identical bits)"}.get(

@@ -114,6 +114,12 @@ typedef struct {
     float momentum;         /* TEM_OPT_MOMENTUM (reading R23): heavy ball u = fma(mu, u, gbar),
                                w = fma(-lr, u, w); 0 <= mu < 1; u sharded by block ownership
                                like Adam's moments                                            */
+    int32_t exchange_buckets; /* 0 or 1: one exchange over the whole gradient (the paper's ring);
+                               2 (ring / two-shot, world_size > 1, reading
+                               R25): two buckets [0, bnd) and [bnd, K_pad), bnd = roundup(off_W2,
+                               4N), each exchanged with R9's partition of its own length; with one
+                               rank per process the [bnd, K_pad) bucket (W2 .. b3, PEM) starts
+                               as soon as conv2 dgrad is done, beside conv1 wgrad              */
     int32_t pgm_gt_max;     /* > 0 (requires pem_proposals > 0, seq_len <= 128): PGM-fed PEM --
                                tem_step_pgm runs PGM (tem_pgm) on this step's TEM probabilities
                                sigmoid(z) and trains PEM on its BSP features and IoU targets

@@ -227,9 +227,12 @@ struct OptState {
     float* v;           // [K_pad] second moments
     const float* scal;  // [beta1^t, beta2^t] of this step (opt_scalars_kernel, before the exchange)
 };
+struct RingParams;
 struct SplitUpdate {
     OptCfg oc;
     OptState os;
+    const RingParams* early = nullptr;  // N > 1 bucketed exchange: the [bnd, K_pad) bucket's
+    int early_kind = 0;                 // ring (TEM_EXCHANGE_RING) / two-shot, launched after dgrad
 };
 struct RingLocal {
     OptState opt;

@@ -83,6 +83,8 @@ bool cfg_valid(const tem_config* c) {
         return false;
     if (c->pem_proposals < 0) return false;
     if (c->pem_proposals > 0 && (c->pem_features != 32 || c->pem_hidden != 512)) return false;  // kernel shape
+    if (c->exchange_buckets < 0 || c->exchange_buckets > 2) return false;
+    if (c->exchange_buckets == 2 && c->exchange == TEM_EXCHANGE_PS) return false;
     if (c->pgm_gt_max < 0 || (c->pgm_gt_max > 0 && (c->pem_proposals <= 0 || c->seq_len > 128))) return false;
     if (c->optimizer != TEM_OPT_SGD && c->optimizer != TEM_OPT_ADAM && c->optimizer != TEM_OPT_MOMENTUM) return false;
     if (c->optimizer == TEM_OPT_MOMENTUM && !(c->momentum >= 0.0f && c->momentum < 1.0f)) return false;
@@ -243,6 +245,7 @@ struct tem_ctx {
     bool alive;
     bool reduce_deferred;  // last compute left the split-K partials for the fused N = 1 exchange
     bool split_done;       // ... and already updated [off_W2, K_pad) (SplitUpdate)
+    bool early_done;       // bucketed exchange: the [bnd, K_pad) bucket ran inside the compute
     // per-kernel timing (tem_timing_*)
     cudaEvent_t* tev;  // [max_steps][NUM_SLOTS*2]
     int t_max, t_idx;
@@ -520,6 +523,50 @@ static OptState opt_state(const tem_ctx* c, int l) {
     return o;
 }
 
+static RingLocal ring_local(tem_ctx* c, int l, const float* src, float* dst, __nv_bfloat16* shadow,
+                            __nv_bfloat16* shadow_lo);
+
+// bucketed exchange (reading R25): [0, bnd) and [bnd, K_pad), bnd = roundup(off_W2, 4N)
+static int64_t bucket_bound(const tem_ctx* c) {
+    const int64_t q = 4 * (int64_t)c->N;
+    return (c->g.off_W2 + q - 1) / q * q;
+}
+static bool bucketed(const tem_ctx* c) { return c->cfg.exchange_buckets == 2 && c->N > 1; }
+
+// The tem_step exchange of elements [e0, e1) of the flat gradient: every pointer and the heap
+// destination offset shifted by e0, the ring's partition taken over e1 - e0 (a multiple of 4N).
+static RingParams step_ring(tem_ctx* c, int64_t e0, int64_t e1) {
+    RingParams p;
+    memset(&p, 0, sizeof(p));
+    for (int l = 0; l < c->nlocal; ++l) {
+        const RankBufs& b = c->rb[l];
+        p.loc[l] = ring_local(c, l, b.grad + e0, (float*)b.params + e0, b.shadow ? b.shadow + e0 : nullptr,
+                              b.shadow_lo ? b.shadow_lo + e0 : nullptr);
+        if (p.loc[l].opt.m) p.loc[l].opt.m += e0;
+        if (p.loc[l].opt.v) p.loc[l].opt.v += e0;
+    }
+    p.N = c->N;
+    p.rank_base = c->rank;
+    p.nlocal = c->nlocal;
+    p.G = c->G;
+    p.C = c->C;
+    p.op = TEM_MEAN;
+    p.mode = 1;
+    p.K = e1 - e0;
+    p.Kpad = e1 - e0;
+    p.oc = opt_cfg(c);
+    p.off_dst = e0 * (int64_t)sizeof(float);
+    p.off_stage = (int64_t)c->hl.off_stage;
+    p.off_flags = (int64_t)(c->cfg.exchange == TEM_EXCHANGE_TWOSHOT ? c->hl.off_tsflags : c->hl.off_flags);
+    p.status = c->st_dev;
+    p.spin_ns = kSpinNs;
+    return p;
+}
+
+static cudaError_t launch_step_ring(tem_ctx* c, const RingParams& p, cudaStream_t s) {
+    return c->cfg.exchange == TEM_EXCHANGE_TWOSHOT ? launch_twoshot(p, s) : launch_ring(p, s);
+}
+
 static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, float* loss_out,
                                cudaStream_t s, int* nl, bool fuse_reduce = false) {
     const EvRec rec{timing_slot_events(c), s};
@@ -541,8 +588,18 @@ static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, f
         // tem_step at N = 1 updates [off_W2, K_pad) inside the compute on the side branch, beside
         // conv1 wgrad, and the exchange only [0, off_W2)
         const bool split_on = getenv("TEM_SPLIT_UPDATE") != nullptr;
-        const SplitUpdate su{opt_cfg(c), opt_state(c, l)};
+        SplitUpdate su{opt_cfg(c), opt_state(c, l)};
         c->split_done = defer && split_on;
+        // bucketed exchange with one rank per process: the [bnd, K_pad) bucket starts inside the
+        // compute (not with PGM-fed PEM, whose gradient is produced after it)
+        RingParams early;
+        c->early_done = false;
+        if (bucketed(c) && c->nlocal == 1 && fuse_reduce && g.path == PATH_UMMA && g.B > 0 && g.pgm_G == 0) {
+            early = step_ring(c, bucket_bound(c), g.Kpad);
+            su.early = &early;
+            su.early_kind = c->cfg.exchange;
+            c->early_done = true;
+        }
         float* lh = (c->nlocal == 1) ? c->loss_host_pending : nullptr;
         if (g.pem_P > 0 && g.pgm_G == 0) {
             // PEM (configs[4]) is independent of TEM: on the tcgen05 path it runs on the side
@@ -562,7 +619,7 @@ static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, f
         }
         if (g.path == PATH_UMMA && g.B > 0) {
             e = umma_compute(g, c->rb[l], *c->plan[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s, defer, lh,
-                             c->split_done ? &su : nullptr);
+                             (c->split_done || c->early_done) ? &su : nullptr);
             if (lh) c->loss_host_done = true;
         }
         else
@@ -643,6 +700,18 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
                 return TEM_ERR_CUDA;
             ++*nl;
         }
+        rec.end(SLOT_EXCHANGE);
+        return opt_scalars(c, s, nl);
+    }
+    if (bucketed(c)) {  // reading R25: [bnd, K_pad) (unless it ran in the compute), then [0, bnd)
+        const int64_t bnd = bucket_bound(c);
+        if (!c->early_done) {
+            if (launch_step_ring(c, step_ring(c, bnd, g.Kpad), s) != cudaSuccess) return TEM_ERR_CUDA;
+            ++*nl;
+        }
+        c->early_done = false;
+        if (launch_step_ring(c, step_ring(c, 0, bnd), s) != cudaSuccess) return TEM_ERR_CUDA;
+        ++*nl;
         rec.end(SLOT_EXCHANGE);
         return opt_scalars(c, s, nl);
     }

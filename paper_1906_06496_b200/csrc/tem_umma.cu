@@ -1856,7 +1856,20 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     rec.end(SLOT_DGRAD);
     if (e != cudaSuccess) return e;
     ++n;
-    if (split && defer_reduce) {
+    if (split && split->early) {
+        // N > 1, exchange_buckets = 2 (reading R25): the [bnd, K_pad) bucket's exchange -- its
+        // gradient is complete once conv2 wgrad (+ reduce) and the head reduction are, and
+        // conv2 dgrad has read W2 -- on the side branch beside conv1 wgrad
+        if (!no_fork &&
+            (cudaEventRecord(P.dgrad_done, s) != cudaSuccess || cudaStreamWaitEvent(P.aux, P.dgrad_done, 0) != cudaSuccess))
+            return cudaErrorUnknown;
+        rec2.begin(SLOT_EXCH2);
+        e = split->early_kind == TEM_EXCHANGE_TWOSHOT ? launch_twoshot(*split->early, aux) : launch_ring(*split->early, aux);
+        rec2.end(SLOT_EXCH2);
+        if (e != cudaSuccess) return e;
+        ++n;
+        if (!no_fork && cudaEventRecord(P.join, P.aux) != cudaSuccess) return cudaErrorUnknown;
+    } else if (split && defer_reduce) {
         // N = 1 tem_step: the owner update of [off_W2, K_pad) (W2 with its split-K partials, b2,
         // W3, b3, PEM) needs only conv2 wgrad / the head and runs once conv2 dgrad -- the last
         // reader of W2 -- is done, on the side branch beside conv1 wgrad

@@ -43,7 +43,7 @@ class tem_config(ctypes.Structure):
         ("exchange", ctypes.c_int32),
         ("pem_proposals", ctypes.c_int32), ("pem_features", ctypes.c_int32), ("pem_hidden", ctypes.c_int32),
         ("optimizer", ctypes.c_int32), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float), ("eps", ctypes.c_float),
-        ("momentum", ctypes.c_float), ("pgm_gt_max", ctypes.c_int32),
+        ("momentum", ctypes.c_float), ("exchange_buckets", ctypes.c_int32), ("pgm_gt_max", ctypes.c_int32),
     ]
 
 
@@ -257,6 +257,7 @@ class SessionConfig:
     eps: float = 1e-8
     momentum: float = 0.9  # TEM_OPT_MOMENTUM (reading R23)
     pgm_gt_max: int = 0  # > 0: PEM fed by PGM on the step's own TEM output (reading R24)
+    exchange_buckets: int = 0  # 2: two-bucket exchange, the W2.. bucket overlapping conv1 wgrad (R25)
 
 
 class TemSession:
@@ -287,6 +288,7 @@ class TemSession:
         cfg.optimizer, cfg.beta1, cfg.beta2, cfg.eps = sc.optimizer, sc.beta1, sc.beta2, sc.eps
         cfg.momentum = sc.momentum
         cfg.pgm_gt_max = sc.pgm_gt_max
+        cfg.exchange_buckets = sc.exchange_buckets
         self.K = tem_num_params(cfg)
         if self.K == 0:
             raise TemError(TEM_ERR_INVALID_ARG, "config")

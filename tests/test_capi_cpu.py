@@ -70,7 +70,8 @@ def test_invalid_configs_rejected(field, value):
 @pytest.mark.parametrize("fields", [dict(optimizer=3), dict(optimizer=1, beta1=1.0, beta2=0.999, eps=1e-8),
                                     dict(optimizer=1, beta1=0.9, beta2=-0.1, eps=1e-8),
                                     dict(optimizer=1, beta1=0.9, beta2=0.999, eps=0.0),
-                                    dict(optimizer=2, momentum=1.0), dict(optimizer=2, momentum=-0.5)])
+                                    dict(optimizer=2, momentum=1.0), dict(optimizer=2, momentum=-0.5),
+                                    dict(exchange_buckets=3), dict(exchange_buckets=2, exchange=1)])
 def test_invalid_optimizer_rejected(fields):
     from paper_1906_06496_b200 import tem
     c = base_cfg(tem)
