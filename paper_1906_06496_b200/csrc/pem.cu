@@ -17,6 +17,7 @@
 // the TEM GEMMs.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "kernels.h"
 
@@ -220,7 +221,12 @@ int pem_ctas(const Geom& g) {
     // (scripts/probes/step_trace.py --workload c5): on a graph branch of its own (16 CTAs
     // beside the TEM step) steps were ~20 us slower and occasionally stalled for milliseconds;
     // more CTAs there took SMs conv2's 8-CTA clusters need.
-    int G = (M + 13) / 14;
+    static const int rows_env = [] {
+        const char* e = getenv("TEM_PEM_ROWS");  // (experiments) proposals per CTA
+        return e ? atoi(e) : 0;
+    }();
+    const int per = rows_env > 0 ? rows_env : 14;
+    int G = (M + per - 1) / per;
     if (G > 148) G = 148;
     return G;
 }

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Run a few tem_step calls of a workload (for ncu / compute-sanitizer captures).
 
-    python scripts/prof_step.py [--workload c2|c3|c1|c5] [--steps 3] [--path umma|simt]
+    python scripts/prof_step.py [--workload c2|c3|c1|c5|c6] [--steps 3] [--path umma|simt]
 """
 import argparse
 import os
@@ -23,20 +23,27 @@ def main():
     import torch
     import datagen
     from paper_1906_06496_b200 import tem
-    B, prec, P = {"c1": (4, 0, 0), "c2": (16, 0, 0), "c3": (256, 1, 0), "c5": (16, 0, datagen.PEM_P)}[args.workload]
+    B, prec, P = {"c1": (4, 0, 0), "c2": (16, 0, 0), "c3": (256, 1, 0), "c5": (16, 0, datagen.PEM_P),
+                  "c6": (16, 0, datagen.PEM_P)}[args.workload]
+    G = datagen.GT_MAX if args.workload == "c6" else 0
     N = args.ranks
     sc = tem.SessionConfig(world_size=N, rank=0, local_ranks=N, batch_per_rank=B, precision=prec, lr=0.01,
-                           pem_proposals=P)
+                           pem_proposals=P, pgm_gt_max=G)
     p0 = datagen.init_params() if not P else np.concatenate([datagen.init_params(), datagen.init_pem_params()])
     s = tem.TemSession(sc, p0)
     xs = np.stack([datagen.features(B, rank=r) for r in range(N)])
     lab = torch.from_numpy(np.stack([datagen.labels(B, rank=r) for r in range(N)])).cuda()
     x = torch.from_numpy(datagen.to_bf16_bits(xs).view(np.int16)).cuda() if prec == 1 else torch.from_numpy(xs).cuda()
-    if P:
+    if G:
+        gt = torch.from_numpy(np.stack([datagen.instances(B, rank=r)[0] for r in range(N)])).cuda()
+        ng = torch.from_numpy(np.stack([datagen.instances(B, rank=r)[1] for r in range(N)])).cuda()
+    elif P:
         f = torch.from_numpy(np.stack([datagen.bsp_features(B, rank=r) for r in range(N)])).cuda()
         g = torch.from_numpy(np.stack([datagen.iou_targets(B, rank=r) for r in range(N)])).cuda()
     for _ in range(args.steps):
-        if P:
+        if G:
+            s.step_pgm(x, lab, gt, ng)
+        elif P:
             s.step_pem(x, lab, f, g)
         else:
             s.step(x, lab)
