@@ -130,19 +130,26 @@ __global__ void __launch_bounds__(PGM_THREADS) pgm_kernel(int T, int G, int P, c
     //    (ascending u = descending c)
     unsigned long long* all = keys;                      // [T*T] pair keys
     unsigned long long* top = keys + PGM_TMAX * PGM_TMAX;  // [PGM_SELMAX] selected keys
-    const int npair = nS * nE;
-    for (int i0 = 0; i0 < npair; i0 += PGM_THREADS) {  // warp-aggregated compaction
-        const int i = i0 + tid;
-        int a = 0, b = 0;
-        if (i < npair) {
-            a = cs[i / nE];
-            b = ce[i % nE];
+    // warp w takes start candidates w, w + 32, ...; its lanes walk the end candidates after
+    // t_s (ce is ascending: the first index with ce > t_s by binary search), warp-aggregated
+    // compaction into `all`
+    for (int si = w; si < nS; si += PGM_THREADS / 32) {
+        const int a = cs[si];
+        int lo = 0, hi = nE;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (ce[mid] > a) hi = mid;
+            else lo = mid + 1;
         }
-        const bool ok = i < npair && a < b;
-        const int pos = warp_slot(ok, &nvalid);
-        if (ok) {
-            const unsigned u = ~__float_as_uint(__fmul_rn(ps[a], pe[b]));
-            all[pos] = ((unsigned long long)u << 32) | ((unsigned long long)a << 16) | (unsigned long long)b;
+        for (int e0 = lo; e0 < nE; e0 += 32) {
+            const int ei = e0 + l;
+            const bool ok = ei < nE;
+            const int pos = warp_slot(ok, &nvalid);
+            if (ok) {
+                const int b = ce[ei];
+                const unsigned u = ~__float_as_uint(__fmul_rn(ps[a], pe[b]));
+                all[pos] = ((unsigned long long)u << 32) | ((unsigned long long)a << 16) | (unsigned long long)b;
+            }
         }
     }
     __syncthreads();
