@@ -223,14 +223,14 @@ __global__ void reduce_splits_kernel(const float* __restrict__ part, float* __re
 template <typename T>
 __global__ void prep_x_kernel(const T* __restrict__ x, T* __restrict__ xp, int B, int Tn, int Cin) {
     const int vec = 16 / sizeof(T);
+    // 32-bit index math, one 16-byte group per thread (grid sized by the launcher)
     const int per_row = Cin / vec;
-    const int64_t total = (int64_t)B * (Tn + 2) * per_row;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t p = i / per_row;
-        const int cv = (int)(i - p * per_row);
-        const int t = (int)(p % (Tn + 2));
-        const int64_t v = p / (Tn + 2);
+    const int total = B * (Tn + 2) * per_row;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int p = i / per_row;
+        const int cv = i - p * per_row;
+        const int v = p / (Tn + 2);
+        const int t = p - v * (Tn + 2);
         uint4 val = make_uint4(0, 0, 0, 0);
         if (t >= 1 && t <= Tn)
             val = reinterpret_cast<const uint4*>(x + ((size_t)v * Tn + (t - 1)) * Cin)[cv];
@@ -333,12 +333,15 @@ int simt_wgrad_splits(const Geom& g) {
 }
 
 cudaError_t launch_prep_x(const Geom& g, const void* x, void* xp, cudaStream_t s) {
+    const int vec = g.prec == TEM_BF16 ? 8 : 4;
+    const int groups = g.B * (g.T + 2) * (g.Cin / vec);
+    const int grid = groups <= 0 ? 1 : (groups + 255) / 256 > 148 * 16 ? 148 * 16 : (groups + 255) / 256;
     if (g.prec == TEM_BF16)
-        prep_x_kernel<__nv_bfloat16><<<296, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
-                                                         static_cast<__nv_bfloat16*>(xp), g.B, g.T, g.Cin);
+        prep_x_kernel<__nv_bfloat16><<<grid, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(x),
+                                                          static_cast<__nv_bfloat16*>(xp), g.B, g.T, g.Cin);
     else
-        prep_x_kernel<float><<<296, 256, 0, s>>>(static_cast<const float*>(x), static_cast<float*>(xp),
-                                                 g.B, g.T, g.Cin);
+        prep_x_kernel<float><<<grid, 256, 0, s>>>(static_cast<const float*>(x), static_cast<float*>(xp),
+                                                  g.B, g.T, g.Cin);
     return cudaGetLastError();
 }
 
