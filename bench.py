@@ -137,6 +137,25 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(win), "source": "nvml"}
 
 
+def bind_to_gpu_numa(index: int):
+    """Run this rank on the CPU cores NVML reports as local to its GPU, so the pinned staging
+    buffers of the end-to-end leg are first-touched on the GPU's NUMA node (host->device copies
+    from the far node measured at half the bandwidth).  Returns the core count, or None."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {64 * w + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= set(range(os.cpu_count()))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return len(cpus)
+    except Exception:
+        return None
+    return None
+
+
 def cpu_baseline(workload: dict, videos: int):
     """The oracle as it stands (plain single-threaded C++, fp64 / bf16-emulated fp64) timed on a
     bounded sample of the same workload: `videos` videos of forward+loss+backward, plus the
@@ -261,6 +280,7 @@ def main():
         if world == 1 and args.gpus > 1:
             print(json.dumps({"error": "run N>1 under torchrun (one process per GPU)"}))
             return 2
+    numa_cores = bind_to_gpu_numa(local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -420,6 +440,7 @@ def main():
         e2e = {"value": world * B * args.steps / (float(t2.item()) / 1e3), "unit": UNIT,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(loss_h.numel() * 4),
                "api": "tem_step_pem_host" if P else "tem_step_host",
+               "host_cores_bound": numa_cores,
                "timing": "one event span over the K steps minus the L2-flush spans between them; "
                          "each step's H2D copies run on the library's copy stream (double-buffered "
                          "staging) beside the previous step's compute, its loss D2H inside the step"}
