@@ -261,7 +261,11 @@ tem_status tem_sync(tem_ctx* ctx, void* stream, int64_t* bad_step);
 tem_status tem_shutdown(tem_ctx* ctx);
 
 /* --- introspection for tests and benchmarks (device pointers owned by the workspace) --- */
-float* tem_local_grad(tem_ctx* ctx, int32_t local_rank); /* [K_pad] fp32, last tem_compute */
+/* [K_pad] fp32 local gradient of the last tem_compute / tem_step (call after it completed).
+ * After an N = 1 tem_step the W1 / W2 parts exist only as split-K partials (the update sums
+ * them itself); this call then sums them into the buffer first, in the update's order, on the
+ * legacy default stream, and synchronises it. */
+float* tem_local_grad(tem_ctx* ctx, int32_t local_rank);
 float* tem_logits(tem_ctx* ctx, int32_t local_rank);     /* [B][T][3] fp32 z, last compute */
 /* Device address and size of an internal workspace tensor of local rank `local_rank`, for
  * tests: "xp", "h1", "h2", "dA2", "dA1" (halo-padded [B][T+2][C] rows in the path's operand

@@ -270,7 +270,7 @@ cudaError_t launch_twoshot(const RingParams& p, cudaStream_t s);  // NVSwitch tw
 cudaError_t launch_sgd_fused(float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo, int64_t e0,
                              int64_t e1, const OptCfg& oc, const OptState& os, const float* p1, int64_t stride1, int64_t n1,
                              int S1, const float* p2, int64_t stride2, int64_t off2, int64_t n2, int S2,
-                             cudaStream_t s, bool side = false, int ctas = 0);
+                             cudaStream_t s, bool side = false, int ctas = 0, int mode = 1);
 cudaError_t launch_sgd_single(const float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo,
                               int64_t n, int op, const OptCfg& oc, const OptState& os, cudaStream_t s);
 // Adam: scal[0] *= beta1, scal[1] *= beta2 (fp32, once per step, before the exchange kernel).

@@ -405,7 +405,10 @@ __global__ void __launch_bounds__(512) sgd_fused_kernel(float* __restrict__ g, f
                                  __nv_bfloat16* __restrict__ shadow_lo, int64_t e0, int64_t e1, OptCfg oc,
                                  OptState os,
                                  const float* __restrict__ p1, int64_t stride1, int64_t n1, int S1,
-                                 const float* __restrict__ p2, int64_t stride2, int64_t off2, int64_t n2, int S2) {
+                                 const float* __restrict__ p2, int64_t stride2, int64_t off2, int64_t n2, int S2,
+                                 int mode) {
+    // mode 1: update + keep the summed local gradient in g; 2: update only (tem_local_grad
+    // sums the partials again on demand, same order); 0: only sum the partials into g
     const int slot = e0 > 0 ? SLOT_EXCH2 : SLOT_EXCHANGE;  // the split update's W2.. range
     trace_begin(slot);
     pdl_trigger();
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(512) sgd_fused_kernel(float* __restrict__ g, f
         }
         // every load of the element group is issued before the first use (one memory latency
         // per iteration): the weights, then up to 4 partials unrolled
-        const float4 wv = reinterpret_cast<const float4*>(w)[v];
+        const float4 wv = mode ? reinterpret_cast<const float4*>(w)[v] : make_float4(0.f, 0.f, 0.f, 0.f);
         float4 a;
         if (src) {  // split-K partials, summed in ascending s (as reduce_wgrad_kernel)
             constexpr int SU = 4;
@@ -446,10 +449,12 @@ __global__ void __launch_bounds__(512) sgd_fused_kernel(float* __restrict__ g, f
                 const float4 q = __ldcs(reinterpret_cast<const float4*>(src + (size_t)s * stride));
                 a.x += q.x; a.y += q.y; a.z += q.z; a.w += q.w;
             }
-            reinterpret_cast<float4*>(g)[v] = a;  // the local gradient stays observable
+            if (mode != 2) reinterpret_cast<float4*>(g)[v] = a;  // the local gradient
         } else {
+            if (mode == 0) continue;
             a = reinterpret_cast<const float4*>(g)[v];
         }
+        if (mode == 0) continue;
         // TEM_MEAN at N = 1: a * fl(1/1) is exact
         const float4 x = owner_update<KIND>(oc, os, e, a, wv);
         reinterpret_cast<float4*>(w)[v] = x;
@@ -558,14 +563,14 @@ void trace_set_ring(unsigned long long* p) { cudaMemcpyToSymbol(g_trace, &p, siz
 cudaError_t launch_sgd_fused(float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo, int64_t e0,
                              int64_t e1, const OptCfg& oc, const OptState& os, const float* p1, int64_t stride1,
                              int64_t n1, int S1, const float* p2, int64_t stride2, int64_t off2, int64_t n2, int S2,
-                             cudaStream_t s, bool side, int ctas) {
+                             cudaStream_t s, bool side, int ctas, int mode) {
     // 2 x 512 threads per SM, grid-stride (one element group per thread and 256-thread CTAs
     // measured 0.7 us slower at c2)
     auto k = oc.kind == TEM_OPT_ADAM       ? sgd_fused_kernel<TEM_OPT_ADAM>
              : oc.kind == TEM_OPT_MOMENTUM ? sgd_fused_kernel<TEM_OPT_MOMENTUM>
                                            : sgd_fused_kernel<TEM_OPT_SGD>;
     return launch_pdl(k, dim3(ctas > 0 ? ctas : 296), dim3(512), 0, s, side, g, w, shadow, shadow_lo, e0, e1, oc, os, p1,
-                      stride1, n1, S1, p2, stride2, off2, n2, S2);
+                      stride1, n1, S1, p2, stride2, off2, n2, S2, mode);
 }
 
 cudaError_t launch_twoshot(const RingParams& p, cudaStream_t s) {

@@ -246,6 +246,8 @@ struct tem_ctx {
     bool reduce_deferred;  // last compute left the split-K partials for the fused N = 1 exchange
     bool split_done;       // ... and already updated [off_W2, K_pad) (SplitUpdate)
     bool early_done;       // bucketed exchange: the [bnd, K_pad) bucket ran inside the compute
+    bool grad_lazy;        // N = 1 tem_step left the W1 / W2 gradient as split-K partials only;
+                           // tem_local_grad sums them on demand (same order as the update)
     // per-kernel timing (tem_timing_*)
     cudaEvent_t* tev;  // [max_steps][NUM_SLOTS*2]
     int t_max, t_idx;
@@ -269,6 +271,7 @@ struct tem_ctx {
         void* loss_host;
         cudaGraphExec_t exec;
         int launches;
+        bool grad_lazy;  // the captured step leaves the W1 / W2 gradient as partials
     };
     static constexpr int kMaxGraphs = 16;
     GraphEntry graphs[kMaxGraphs];
@@ -326,10 +329,12 @@ tem_status graph_step(tem_ctx* c, const void* x, const void* lab, void* loss, cu
         e->ngt = c->pgm_ngt;
         e->exec = exec;
         e->launches = nl;
+        e->grad_lazy = c->grad_lazy;
     }
     // Captured on the private stream, replayed directly on the caller's stream (stream order
     // gives the dependencies; no cross-stream event handoff per step).
     if (cudaGraphLaunch(e->exec, s) != cudaSuccess) return TEM_ERR_CUDA;
+    c->grad_lazy = e->grad_lazy;
     if (e->loss_host && c->g.path == PATH_UMMA && c->g.B > 0) c->loss_host_done = true;
     c->launches_step = e->launches;
     return TEM_OK;
@@ -584,6 +589,7 @@ static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, f
         ++*nl;
         const bool defer = fuse_reduce && c->N == 1 && g.path == PATH_UMMA && g.B > 0;
         c->reduce_deferred = defer;
+        c->grad_lazy = false;  // this compute's partials overwrite the last step's
         // TEM_SPLIT_UPDATE=1 (experiment, off: measured 2-14 % slower at c2):
         // tem_step at N = 1 updates [off_W2, K_pad) inside the compute on the side branch, beside
         // conv1 wgrad, and the exchange only [0, off_W2)
@@ -684,11 +690,15 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
         const UmmaPlan& P = *c->plan[0];
         c->reduce_deferred = false;
         const int64_t e1 = c->split_done ? g.off_W2 : g.Kpad;  // [off_W2, K_pad) done in the compute
+        // the summed W1 / W2 gradient is not stored (5.6 MB of writes): tem_local_grad rebuilds
+        // it from the partials on demand (TEM_KEEP_GRAD=1 stores it in the step)
+        const bool lazy = !c->split_done && getenv("TEM_KEEP_GRAD") == nullptr;
         c->split_done = false;
         if (launch_sgd_fused(b.grad, (float*)b.params, b.shadow, b.shadow_lo, 0, e1, oc, opt_state(c, 0), b.wpart,
                              P.wgrad1.part_stride, g.off_W2, P.S1, b.wpart2, P.wgrad2.part_stride, g.off_W2,
-                             (int64_t)3 * g.C * g.C, P.S2, s) != cudaSuccess)
+                             (int64_t)3 * g.C * g.C, P.S2, s, false, 0, lazy ? 2 : 1) != cudaSuccess)
             return TEM_ERR_CUDA;
+        c->grad_lazy = lazy;
         ++*nl;
         rec.end(SLOT_EXCHANGE);
         return opt_scalars(c, s, nl);
@@ -1132,6 +1142,17 @@ tem_status tem_shutdown(tem_ctx* c) {
 
 float* tem_local_grad(tem_ctx* c, int32_t l) {
     if (!c || !c->alive || l < 0 || l >= c->nlocal) return nullptr;
+    if (c->grad_lazy && l == 0) {  // sum the split-K partials of the last N = 1 tem_step into grad
+        const Geom& g = c->g;
+        const RankBufs& b = c->rb[0];
+        const UmmaPlan& P = *c->plan[0];
+        if (launch_sgd_fused(b.grad, nullptr, nullptr, nullptr, 0, g.Kpad, opt_cfg(c), opt_state(c, 0), b.wpart,
+                             P.wgrad1.part_stride, g.off_W2, P.S1, b.wpart2, P.wgrad2.part_stride, g.off_W2,
+                             (int64_t)3 * g.C * g.C, P.S2, 0, false, 0, 0) != cudaSuccess ||
+            cudaStreamSynchronize(0) != cudaSuccess)
+            return nullptr;
+        c->grad_lazy = false;
+    }
     return c->rb[l].grad;
 }
 
