@@ -1,0 +1,73 @@
+// mma_dual_probe.cu -- rate of the fp32 path's MMA pattern (R16): per K-step of
+// 16, A_hi x [B_hi | B_lo] at N = 2*BN into accumulator 0, then A_lo x B_hi at N = BN into
+// accumulator 1, with the A descriptors at a halo row offset (tap j: +j*128 B).  Isolated from
+// TMA: operands static in shared memory.  Build + run on the GPU box:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1906_06496_b200/csrc \
+//        scripts/probes/mma_dual_probe.cu -o /tmp/mma_dual && /tmp/mma_dual
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "umma.cuh"
+using namespace tem::umma;
+
+template <int BN, int TAPOFF>
+__global__ void __launch_bounds__(128, 1) probe(long long* out, int nk) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    uint8_t* s = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm) + 1023) & ~uintptr_t(1023));
+    __shared__ uint64_t bar;
+    __shared__ uint32_t slot;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 96 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(s)[i] = 0;
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+    if (warp == 0) tmem_alloc<512>(&slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tb = slot;
+    if (warp == 0 && lane == 0) {
+        constexpr uint32_t id2 = make_idesc_bf16(128, 2 * BN, false, false), id1 = make_idesc_bf16(128, BN, false, false);
+        // A_hi window at 0, A_lo at 24 KB (130 rows x 128 B each + pad), B [hi|lo] at 48 KB
+        const uint32_t ahi = smem_u32(s) + TAPOFF * 128, alo = smem_u32(s + 24576) + TAPOFF * 128;
+        const uint32_t bhl = smem_u32(s + 49152);
+        long long t0 = clock64();
+        for (int i = 0; i < nk; ++i) {
+            const int k = i & 3;
+            const uint64_t a0 = make_desc(ahi + k * 32, 16, 1024), a1 = make_desc(alo + k * 32, 16, 1024);
+            const uint64_t b0 = make_desc(bhl + k * 32, 16, 1024);
+            mma_bf16(tb, a0, b0, id2, i ? 1u : 0u);
+            mma_bf16(tb + 2 * BN, a1, b0, id1, i ? 1u : 0u);
+        }
+        long long t1 = clock64();
+        mma_commit(&bar);
+        mbar_wait(&bar, 0);
+        long long t2 = clock64();
+        if (blockIdx.x == 0) { out[0] = t1 - t0; out[1] = t2 - t0; }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tb); }
+}
+
+template <int BN, int TAPOFF>
+void run(long long* d, int grid) {
+    const int nk = 4096;
+    auto k = probe<BN, TAPOFF>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+    k<<<grid, 128, 100 * 1024>>>(d, nk);
+    k<<<grid, 128, 100 * 1024>>>(d, nk);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long h[2];
+    cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+    const int floor_clk = 128 * 2 * BN / 256 + 128 * BN / 256;
+    printf("BN=%3d tap=%d grid=%3d: %.1f clk per K-step pair (MMA floor %d) %s\n", BN, TAPOFF, grid,
+           (double)h[1] / nk, floor_clk, cudaGetErrorString(e));
+}
+
+int main() {
+    long long* d;
+    cudaMalloc(&d, 16);
+    for (int grid : {1, 104}) {
+        run<64, 0>(d, grid); run<64, 1>(d, grid); run<64, 2>(d, grid);
+        run<128, 0>(d, grid); run<128, 1>(d, grid);
+    }
+    return 0;
+}
