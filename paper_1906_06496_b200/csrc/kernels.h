@@ -151,7 +151,8 @@ struct UmmaPlan {
     bool pem_pending;         // a PEM launch on `pem` awaits its join before the exchange
 };
 void umma_plan_destroy(UmmaPlan* plan);
-bool umma_side_branch_enabled();  // false under TEM_NO_FORK (side branch serialised)
+bool umma_side_branch_enabled();
+void umma_probe_skip(int bits);  // diagnostics: skip FWD/DGRAD operand loads (bit 0 A, bit 1 B)  // false under TEM_NO_FORK (side branch serialised)
 void* umma_tstamp_buffer(int64_t* nbytes, int on);  // split-K phase timestamps (diagnostics)
 int umma_wgrad_splits(const Geom& g);
 bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan);

@@ -1179,6 +1179,10 @@ void* tem_debug_buffer(tem_ctx* c, int32_t l, const char* name, int64_t* nbytes)
         if (nbytes) *nbytes = (int64_t)(sizeof(unsigned long long) * words);
         return buf;
     }
+    if (strncmp(name, "probe_skip:", 11) == 0) {  // diagnostics: "probe_skip:<bits>" (wrong results)
+        umma_probe_skip(atoi(name + 11));
+        return nullptr;
+    }
     if (strcmp(name, "tstamp_on") == 0 || strcmp(name, "tstamp") == 0)
         return umma_tstamp_buffer(nbytes, strcmp(name, "tstamp_on") == 0 ? 1 : 0);
     if (strncmp(name, "tstamp_slot:", 12) == 0)  // stamps of one launch: "tstamp_slot:<Slot>"

@@ -39,6 +39,7 @@
 
 namespace tem {
 namespace umma {
+__device__ unsigned g_epi_sleep;  // (experiment) epilogue tfull-wait backoff in ns, 0 = spin
 
 constexpr int BM = 128;
 constexpr int BK = 64;   // bf16 elements per k-block = one 128-byte swizzle row
@@ -362,7 +363,8 @@ TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, ui
         const int acc = t & 1;
         uint4 pm[2];
         if (MODE == DGRAD_) dgrad_mask_chunk0(P, m_tile * BM + 32 * q + lane, n_tile * BN, pm);
-        mbar_wait(&tfull[acc], (t >> 1) & 1);
+        if (g_epi_sleep) mbar_wait_sleep(&tfull[acc], (t >> 1) & 1, g_epi_sleep);
+        else mbar_wait(&tfull[acc], (t >> 1) & 1);
         tc_fence_after();
         const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * ACC * BN);
         epilogue_tile<MODE, BN, ACC>(P, tq, m_tile, n_tile, split, q, lane, stg, buf, sw3, pm, zloc);
@@ -380,6 +382,10 @@ TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, ui
 // [grid][16] globaltimer ns; written only while g_tstamp_on is set).
 __device__ unsigned long long g_tstamp[1024 * 16];
 __device__ int g_tstamp_on;
+// Diagnostics only (umma_probe_skip): bit 0 skips the FWD/DGRAD A-window loads, bit 1 the B
+// loads (the barriers are still completed) -- wrong results, used to time the mainloop with
+// less L2 traffic.
+__device__ int g_probe_skip;
 TEM_DEV void tstamp(int k) {
     if (g_tstamp_on == 1) g_tstamp[blockIdx.x * 16 + k] = globaltimer();
 }
@@ -651,6 +657,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
     const int total = mt_u * P.ntiles;
     if (threadIdx.x == 0) tstamp(0);
     trace_begin(P.slot);
+    if (g_probe_skip) {  // diagnostics: skipped operands read zeros, not stale shared memory
+        for (uint32_t i = threadIdx.x; i < C_::RINGS / 16; i += NTHREADS)
+            reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
+        __syncthreads();
+    }
     float glab[3] = {0.f, 0.f, 0.f}, gb3[3] = {0.f, 0.f, 0.f};  // HEAD: row labels, b3 (prefetched)
     const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, fullA, 2 * (SA + SB), tfull, tempty, tslot, warp, lane);
     if (threadIdx.x == 0) tstamp(1);
@@ -674,14 +685,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                 for (int cb = 0; cb < P.cpb; ++cb) {
                     const int sa = ia % SA;
                     mbar_wait(&emptyA[sa], ((ia / SA) & 1) ^ 1);
-                    if (leader) mbar_arrive_expect_tx(&fullA[sa], (PAIR ? 2 : 1) * C_::A_TX);
+                    if (g_probe_skip & 1) {
+                        if (leader) mbar_arrive_local(&fullA[sa]);
+                    } else {
+                        if (leader) mbar_arrive_expect_tx(&fullA[sa], (PAIR ? 2 : 1) * C_::A_TX);
 #pragma unroll
-                    for (int pl = 0; pl < NPL; ++pl)
-                        ld2d<PAIR>(sA + sa * C_::A_STAGE + pl * C_::A_PLANE, &P.a[pl], &fullA[sa], cb * BK, m0 - 1);
+                        for (int pl = 0; pl < NPL; ++pl)
+                            ld2d<PAIR>(sA + sa * C_::A_STAGE + pl * C_::A_PLANE, &P.a[pl], &fullA[sa], cb * BK, m0 - 1);
+                    }
                     ++ia;
                     for (int j = 0; j < 3; ++j, ++ib) {
                         const int sb = ib % SB;
                         mbar_wait(&emptyB[sb], ((ib / SB) & 1) ^ 1);
+                        if (g_probe_skip & 2) {
+                            if (leader) mbar_arrive_local(&fullB[sb]);
+                            continue;
+                        }
                         if (leader) mbar_arrive_expect_tx(&fullB[sb], (PAIR ? 2 : 1) * C_::B_STAGE);
 #pragma unroll
                         for (int pl = 0; pl < NPL; ++pl) {
@@ -1776,7 +1795,16 @@ static cudaError_t dispatch(const UmmaParams& p, int npass, cudaStream_t s) {
         if (c.pair && c.bn == 64) return launch_halo<MODE, 64, 3, 3, 6, true>(p, s);
         if (c.pair)
             return npass == 3 ? launch_halo<MODE, 128, 3, 3, 6, true>(p, s) : launch_halo<MODE, 256, 1, 4, 8, true>(p, s);
-        return npass == 3 ? launch_halo<MODE, 64, 3, 3, 6, false>(p, s) : launch_halo<MODE, 256, 1, 3, 4, false>(p, s);
+        if (npass == 3) {
+            static const int stages = [] {  // (experiments) ring depths SA x SB, default 3 x 6
+                const char* e = getenv("TEM_HALO_STAGES");
+                return e ? atoi(e) : 36;
+            }();
+            if (stages == 28) return launch_halo<MODE, 64, 3, 2, 8, false>(p, s);
+            if (stages == 44) return launch_halo<MODE, 64, 3, 4, 4, false>(p, s);
+            return launch_halo<MODE, 64, 3, 3, 6, false>(p, s);
+        }
+        return launch_halo<MODE, 256, 1, 3, 4, false>(p, s);
     }
 }
 
@@ -1910,6 +1938,15 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     }
     *nl += n;
     return cudaSuccess;
+}
+
+void umma_probe_skip(int bits) {
+    if (bits >= 1000) {  // "probe_skip:1000+ns": epilogue backoff experiment
+        const unsigned ns = (unsigned)(bits - 1000);
+        cudaMemcpyToSymbol(umma::g_epi_sleep, &ns, sizeof(ns));
+        return;
+    }
+    cudaMemcpyToSymbol(umma::g_probe_skip, &bits, sizeof(int));
 }
 
 bool umma_side_branch_enabled() { return getenv("TEM_NO_FORK") == nullptr; }

@@ -34,6 +34,26 @@ UMMA_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// Wait for a phase with a nanosleep backoff between polls: for warps that wait a long time
+// (the epilogue, while the mainloop runs) -- a tight try_wait loop competes with the tensor
+// core's operand reads for shared memory.
+UMMA_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+    uint32_t ok = 0;
+    for (;;) {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        __nanosleep(ns);
+    }
+}
+
 // ------------------------------------------------------------------ TMA
 UMMA_DEV void tma_prefetch(const CUtensorMap* m) {
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)m) : "memory");

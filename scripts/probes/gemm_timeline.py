@@ -30,6 +30,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--kernel", default="halo", choices=["halo", "split", "head", "wgrad1", "wgrad2"])
+    ap.add_argument("--skip", type=int, default=0, help="probe_skip bits (diagnostics: no A / B loads)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -40,11 +41,13 @@ def main():
     s = tem.TemSession(sc, datagen.init_params())
     x = torch.from_numpy(datagen.features(B)).cuda()
     lab = torch.from_numpy(datagen.labels(B)).cuda()
+    lib = tem.lib()
+    nb = ctypes.c_int64(0)
+    if args.skip:
+        lib.tem_debug_buffer(tem._P(s.ctx), 0, f"probe_skip:{args.skip}".encode(), ctypes.byref(nb))
     for _ in range(3):
         s.step(x, lab)
     torch.cuda.synchronize()
-    lib = tem.lib()
-    nb = ctypes.c_int64(0)
     on = b"tstamp_on" if args.kernel not in SLOTS else f"tstamp_slot:{SLOTS[args.kernel]}".encode()
     lib.tem_debug_buffer(tem._P(s.ctx), 0, on, ctypes.byref(nb))
     s.step(x, lab)
