@@ -410,7 +410,13 @@ struct CfgHalo {
     static constexpr uint32_t A_TX = NPL * A_ROWS * 128;        // bytes the window loads deliver
     static constexpr int BR = PAIR ? BN / 2 : BN;               // B rows (FWD) / columns (DGRAD) here
     static constexpr uint32_t B_PLANE = BR * BK * 2;
-    static constexpr uint32_t B_STAGE = NPL * B_PLANE;
+    static constexpr uint32_t B_STAGE = NPL * B_PLANE;  // one tap ("slot"); SB slots in the ring
+    // Taps per B barrier stage (1 = one wait / commit per tap).  In the isolated probe a wait +
+    // commit per tap costs ~270 clk of MMA bubble (scripts/probes/mma_dual_probe.cu: 121 -> 189
+    // clk per K-step pair at BN = 64), but one stage per 3-tap chunk (TPS = 3, 2 stages of 48 KB)
+    // measured no faster in the kernel (DGRAD mainloop 11.2 vs 11.7 us; slot 22.5 vs 20.9 us)
+    static constexpr int TPS = 1;
+    static constexpr int SBS = SB / TPS;  // barrier stages
     static constexpr uint32_t RINGS = SA * A_STAGE + SB * B_STAGE;
     static constexpr uint32_t SMEM = RINGS + 1024 /*align*/ + 1024 /*barriers*/ + EPI_SMEM;
     // 3-pass 1-CTA: dual-accumulator MMAs (see epilogue_tile), 3 BN columns per buffer
@@ -695,22 +701,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                     }
                     ++ia;
                     for (int j = 0; j < 3; ++j, ++ib) {
-                        const int sb = ib % SB;
-                        mbar_wait(&emptyB[sb], ((ib / SB) & 1) ^ 1);
+                        const int sb = ib % SB;                          // tap slot
+                        const int bs = (ib / C_::TPS) % C_::SBS;         // barrier stage
+                        const bool first = (ib % C_::TPS) == 0;
+                        if (first) mbar_wait(&emptyB[bs], ((ib / C_::TPS / C_::SBS) & 1) ^ 1);
                         if (g_probe_skip & 2) {
-                            if (leader) mbar_arrive_local(&fullB[sb]);
+                            if (leader && first) mbar_arrive_local(&fullB[bs]);
                             continue;
                         }
-                        if (leader) mbar_arrive_expect_tx(&fullB[sb], (PAIR ? 2 : 1) * C_::B_STAGE);
+                        if (leader && first) mbar_arrive_expect_tx(&fullB[bs], (PAIR ? 2 : 1) * C_::TPS * C_::B_STAGE);
 #pragma unroll
                         for (int pl = 0; pl < NPL; ++pl) {
                             uint8_t* dst = sB + sb * C_::B_STAGE + pl * C_::B_PLANE;
                             if (MODE == FWD_) {
-                                ld2d<PAIR>(dst, &P.b[pl], &fullB[sb], j * P.Kc + cb * BK, n0);
+                                ld2d<PAIR>(dst, &P.b[pl], &fullB[bs], j * P.Kc + cb * BK, n0);
                             } else {
 #pragma unroll
                                 for (int q = 0; q < C_::BR / 64; ++q)
-                                    ld3d<PAIR>(dst + q * (BK * 128), &P.b[pl], &fullB[sb], n0 + 64 * q, j, cb * BK);
+                                    ld3d<PAIR>(dst + q * (BK * 128), &P.b[pl], &fullB[bs], n0 + 64 * q, j, cb * BK);
                             }
                         }
                     }
@@ -735,8 +743,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                     const uint32_t a_st = smem_u32(sA + sa * C_::A_STAGE);
                     for (int j = 0; j < 3; ++j, ++ib) {
                         const int sb = ib % SB;
-                        mbar_wait(&fullB[sb], (ib / SB) & 1);
-                        tc_fence_after();
+                        const int bs = (ib / C_::TPS) % C_::SBS;
+                        if ((ib % C_::TPS) == 0) {
+                            mbar_wait(&fullB[bs], (ib / C_::TPS / C_::SBS) & 1);
+                            tc_fence_after();
+                        }
                         const uint32_t b_st = smem_u32(sB + sb * C_::B_STAGE);
                         const uint32_t roff = (uint32_t)((MODE == FWD_ ? j : 2 - j) * 128);
 #pragma unroll
@@ -763,7 +774,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                                 }
                             }
                         }
-                        commit_to<PAIR>(&emptyB[sb]);
+                        if ((ib % C_::TPS) == C_::TPS - 1) commit_to<PAIR>(&emptyB[bs]);
                     }
                     commit_to<PAIR>(&emptyA[sa]);  // window consumed by all three taps
                     ++ia;

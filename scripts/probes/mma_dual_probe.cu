@@ -9,15 +9,15 @@
 #include "umma.cuh"
 using namespace tem::umma;
 
-template <int BN, int TAPOFF, int NSTAGE = 1>
+template <int BN, int TAPOFF, int NSTAGE = 1, int CADENCE = 0>
 __global__ void __launch_bounds__(128, 1) probe(long long* out, int nk) {
     extern __shared__ __align__(1024) uint8_t sm[];
     uint8_t* s = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar;
+    __shared__ uint64_t bar, bar2, bar3;
     __shared__ uint32_t slot;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < 200 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(s)[i] = 0;
-    if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
+    if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&bar2, 1); mbar_init(&bar3, 1); fence_barrier_init(); }
     if (warp == 0) tmem_alloc<512>(&slot);
     tc_fence_before();
     __syncthreads();
@@ -38,6 +38,11 @@ __global__ void __launch_bounds__(128, 1) probe(long long* out, int nk) {
             const uint64_t b0 = make_desc(bhl + k * 32, 16, 1024);
             mma_bf16(tb, a0, b0, id2, i ? 1u : 0u);
             mma_bf16(tb + 2 * BN, a1, b0, id1, i ? 1u : 0u);
+            if (CADENCE && k == 3) {  // the kernel's per-tap cadence: commit, then wait + fence
+                mma_commit(&bar2);
+                if (CADENCE == 2) { mbar_arrive_local(&bar3); mbar_wait(&bar3, (i >> 2) & 1); }
+                tc_fence_after();
+            }
         }
         long long t1 = clock64();
         mma_commit(&bar);
@@ -50,10 +55,10 @@ __global__ void __launch_bounds__(128, 1) probe(long long* out, int nk) {
     if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tb); }
 }
 
-template <int BN, int TAPOFF, int NSTAGE = 1>
+template <int BN, int TAPOFF, int NSTAGE = 1, int CADENCE = 0>
 void run(long long* d, int grid) {
     const int nk = 4096;
-    auto k = probe<BN, TAPOFF, NSTAGE>;
+    auto k = probe<BN, TAPOFF, NSTAGE, CADENCE>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
     k<<<grid, 128, 210 * 1024>>>(d, nk);
     k<<<grid, 128, 210 * 1024>>>(d, nk);
@@ -61,7 +66,7 @@ void run(long long* d, int grid) {
     long long h[2];
     cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
     const int floor_clk = 128 * 2 * BN / 256 + 128 * BN / 256;
-    printf("BN=%3d tap=%d stages=%d grid=%3d: %.1f clk per K-step pair (MMA floor %d) %s\n", BN, TAPOFF, NSTAGE, grid,
+    printf("BN=%3d tap=%d stages=%d cadence=%d grid=%3d: %.1f clk per K-step pair (MMA floor %d) %s\n", BN, TAPOFF, NSTAGE, CADENCE, grid,
            (double)h[1] / nk, floor_clk, cudaGetErrorString(e));
 }
 
@@ -69,8 +74,8 @@ int main() {
     long long* d;
     cudaMalloc(&d, 16);
     for (int grid : {1, 104}) {
-        run<64, 0>(d, grid); run<64, 1>(d, grid); run<64, 1, 6>(d, grid);
-        run<128, 0>(d, grid); run<128, 1, 6>(d, grid);
+        run<64, 1, 6, 0>(d, grid); run<64, 1, 6, 1>(d, grid); run<64, 1, 6, 2>(d, grid);
+        run<128, 1, 1, 0>(d, grid); run<128, 1, 1, 2>(d, grid);
     }
     return 0;
 }
