@@ -40,6 +40,7 @@
 namespace tem {
 namespace umma {
 __device__ unsigned g_epi_sleep;  // (experiment) epilogue tfull-wait backoff in ns, 0 = spin
+__device__ unsigned g_prod_sleep;  // (experiment) FWD/DGRAD producer empty-wait backoff in ns
 
 constexpr int BM = 128;
 constexpr int BK = 64;   // bf16 elements per k-block = one 128-byte swizzle row
@@ -690,7 +691,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                 const int n0 = n_tile * BN + (int)rank * C_::BR;
                 for (int cb = 0; cb < P.cpb; ++cb) {
                     const int sa = ia % SA;
-                    mbar_wait(&emptyA[sa], ((ia / SA) & 1) ^ 1);
+                    if (g_prod_sleep) mbar_wait_sleep(&emptyA[sa], ((ia / SA) & 1) ^ 1, g_prod_sleep);
+                    else mbar_wait(&emptyA[sa], ((ia / SA) & 1) ^ 1);
                     if (g_probe_skip & 1) {
                         if (leader) mbar_arrive_local(&fullA[sa]);
                     } else {
@@ -704,7 +706,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                         const int sb = ib % SB;                          // tap slot
                         const int bs = (ib / C_::TPS) % C_::SBS;         // barrier stage
                         const bool first = (ib % C_::TPS) == 0;
-                        if (first) mbar_wait(&emptyB[bs], ((ib / C_::TPS / C_::SBS) & 1) ^ 1);
+                        if (first) {
+                            if (g_prod_sleep) mbar_wait_sleep(&emptyB[bs], ((ib / C_::TPS / C_::SBS) & 1) ^ 1, g_prod_sleep);
+                            else mbar_wait(&emptyB[bs], ((ib / C_::TPS / C_::SBS) & 1) ^ 1);
+                        }
                         if (g_probe_skip & 2) {
                             if (leader && first) mbar_arrive_local(&fullB[bs]);
                             continue;
@@ -1952,6 +1957,11 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
 }
 
 void umma_probe_skip(int bits) {
+    if (bits >= 2000) {  // "probe_skip:2000+ns": producer backoff experiment
+        const unsigned ns = (unsigned)(bits - 2000);
+        cudaMemcpyToSymbol(umma::g_prod_sleep, &ns, sizeof(ns));
+        return;
+    }
     if (bits >= 1000) {  // "probe_skip:1000+ns": epilogue backoff experiment
         const unsigned ns = (unsigned)(bits - 1000);
         cudaMemcpyToSymbol(umma::g_epi_sleep, &ns, sizeof(ns));
