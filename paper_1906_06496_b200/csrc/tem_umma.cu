@@ -755,17 +755,20 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                         }
                         const uint32_t b_st = smem_u32(sB + sb * C_::B_STAGE);
                         const uint32_t roff = (uint32_t)((MODE == FWD_ ? j : 2 - j) * 128);
+                        // descriptors of the tap's first K-step; the K-steps advance the 16-byte
+                        // start-address field (addresses < 256 KB: no carry out of the field)
+                        const uint64_t bdt = B_MN ? make_desc(b_st, BK * 128, 1024) : make_desc(b_st, 16, 1024);
+                        const uint64_t adh = make_desc(a_st + roff, 16, 1024);
+                        const uint64_t adl = make_desc(a_st + C_::A_PLANE + roff, 16, 1024);
 #pragma unroll
                         for (int k = 0; k < BK / UK; ++k) {
-                            const uint64_t bd0 = B_MN ? make_desc(b_st + k * (UK * 128), BK * 128, 1024)
-                                                      : make_desc(b_st + k * (UK * 2), 16, 1024);
+                            const uint64_t bd0 = bdt + (uint64_t)(B_MN ? k * (UK * 128 / 16) : k * (UK * 2 / 16));
                             if (C_::ACC == 3) {
                                 // A_hi x [B_hi | B_lo] (N = 2 BN, planes contiguous), A_lo x B_hi (N = BN)
                                 constexpr uint32_t idesc2 = make_idesc_bf16(BM, 2 * BN, false, B_MN);
                                 const uint32_t acc_on = (cb | j | k) != 0 ? 1u : 0u;
-                                issue_mma<PAIR>(dt, make_desc(a_st + roff + k * (UK * 2), 16, 1024), bd0, idesc2, acc_on);
-                                issue_mma<PAIR>(dt + 2 * BN, make_desc(a_st + C_::A_PLANE + roff + k * (UK * 2), 16, 1024),
-                                                bd0, idesc, acc_on);
+                                issue_mma<PAIR>(dt, adh + (uint64_t)(k * (UK * 2 / 16)), bd0, idesc2, acc_on);
+                                issue_mma<PAIR>(dt + 2 * BN, adl + (uint64_t)(k * (UK * 2 / 16)), bd0, idesc, acc_on);
                             } else {
 #pragma unroll
                                 for (int pass = 0; pass < NPASS; ++pass) {
