@@ -22,14 +22,15 @@ PHASES = {"split": ["entry", "pdl_wait", "prod_firstA", "mma_fullA", "mma_fullB"
           "head": ["-"] * 8 + ["head_start", "cluster1", "dz_done", "dA2_done", "colsum_done",
                                "c0_tmem", "c0_math", "c0_stored"],
           "wgrad1": ["entry", "prologue", "mma_full0", "mma_done", "-", "-", "epi_done"],
+          "fwd1": ["entry", "pdl_wait", "mma_fullA0", "tile0_mma_done", "last_mma_done", "-", "epi_done"],
           "wgrad2": ["entry", "prologue", "mma_full0", "mma_done", "-", "-", "epi_done"]}
-SLOTS = {"wgrad2": 6, "wgrad1": 8}  # Slot enum (kernels.h)
+SLOTS = {"wgrad2": 6, "wgrad1": 8, "fwd1": 1}  # Slot enum (kernels.h)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c2")
-    ap.add_argument("--kernel", default="halo", choices=["halo", "split", "head", "wgrad1", "wgrad2"])
+    ap.add_argument("--kernel", default="halo", choices=["halo", "split", "head", "wgrad1", "wgrad2", "fwd1"])
     ap.add_argument("--skip", type=int, default=0, help="probe_skip bits (diagnostics: no A / B loads)")
     args = ap.parse_args()
     import numpy as np

@@ -9,7 +9,7 @@
 #include "umma.cuh"
 using namespace tem::umma;
 
-template <int BN, int TAPOFF, int NSTAGE = 1, int CADENCE = 0>
+template <int BN, int TAPOFF, int NSTAGE = 1, int CADENCE = 0, bool BMN = false>
 __global__ void __launch_bounds__(128, 1) probe(long long* out, int nk) {
     extern __shared__ __align__(1024) uint8_t sm[];
     uint8_t* s = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm) + 1023) & ~uintptr_t(1023));
@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(128, 1) probe(long long* out, int nk) {
     tc_fence_after();
     const uint32_t tb = slot;
     if (warp == 0 && lane == 0) {
-        constexpr uint32_t id2 = make_idesc_bf16(128, 2 * BN, false, false), id1 = make_idesc_bf16(128, BN, false, false);
+        constexpr uint32_t id2 = make_idesc_bf16(128, 2 * BN, false, BMN), id1 = make_idesc_bf16(128, BN, false, BMN);
         // A_hi window at 0, A_lo at 24 KB (130 rows x 128 B each + pad), B [hi|lo] at 48 KB
         long long t0 = clock64();
         for (int i = 0; i < nk; ++i) {
@@ -35,7 +35,8 @@ __global__ void __launch_bounds__(128, 1) probe(long long* out, int nk) {
             const uint32_t alo = ahi + 17408;
             const uint32_t bhl = smem_u32(s) + (NSTAGE > 1 ? 104448 + (st % 6) * 16384 : 49152);
             const uint64_t a0 = make_desc(ahi + k * 32, 16, 1024), a1 = make_desc(alo + k * 32, 16, 1024);
-            const uint64_t b0 = make_desc(bhl + k * 32, 16, 1024);
+            // BMN: DGRAD's MN-major B (LBO = one 64-column panel of K rows, K-steps of 16 rows)
+            const uint64_t b0 = BMN ? make_desc(bhl + k * 2048, 64 * 128, 1024) : make_desc(bhl + k * 32, 16, 1024);
             mma_bf16(tb, a0, b0, id2, i ? 1u : 0u);
             mma_bf16(tb + 2 * BN, a1, b0, id1, i ? 1u : 0u);
             if (CADENCE && k == 3) {  // the kernel's per-tap cadence: commit, then wait + fence
@@ -55,10 +56,10 @@ __global__ void __launch_bounds__(128, 1) probe(long long* out, int nk) {
     if (warp == 0) { tc_fence_after(); tmem_dealloc<512>(tb); }
 }
 
-template <int BN, int TAPOFF, int NSTAGE = 1, int CADENCE = 0>
+template <int BN, int TAPOFF, int NSTAGE = 1, int CADENCE = 0, bool BMN = false>
 void run(long long* d, int grid) {
     const int nk = 4096;
-    auto k = probe<BN, TAPOFF, NSTAGE, CADENCE>;
+    auto k = probe<BN, TAPOFF, NSTAGE, CADENCE, BMN>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
     k<<<grid, 128, 210 * 1024>>>(d, nk);
     k<<<grid, 128, 210 * 1024>>>(d, nk);
@@ -66,7 +67,7 @@ void run(long long* d, int grid) {
     long long h[2];
     cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
     const int floor_clk = 128 * 2 * BN / 256 + 128 * BN / 256;
-    printf("BN=%3d tap=%d stages=%d cadence=%d grid=%3d: %.1f clk per K-step pair (MMA floor %d) %s\n", BN, TAPOFF, NSTAGE, CADENCE, grid,
+    printf("BN=%3d tap=%d stages=%d cadence=%d bmn=%d grid=%3d: %.1f clk per K-step pair (MMA floor %d) %s\n", BN, TAPOFF, NSTAGE, CADENCE, (int)BMN, grid,
            (double)h[1] / nk, floor_clk, cudaGetErrorString(e));
 }
 
@@ -74,8 +75,8 @@ int main() {
     long long* d;
     cudaMalloc(&d, 16);
     for (int grid : {1, 104}) {
-        run<64, 1, 6, 0>(d, grid); run<64, 1, 6, 1>(d, grid); run<64, 1, 6, 2>(d, grid);
-        run<128, 1, 1, 0>(d, grid); run<128, 1, 1, 2>(d, grid);
+        run<64, 1, 6, 0>(d, grid); run<64, 1, 6, 2>(d, grid);
+        run<64, 1, 6, 0, true>(d, grid); run<64, 1, 6, 2, true>(d, grid);
     }
     return 0;
 }
