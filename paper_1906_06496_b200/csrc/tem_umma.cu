@@ -731,8 +731,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && leader) {
+        if (leader) {
             // ===================== MMA issuer =====================
+            // the whole warp runs the loop (uniform descriptors); the elected lane issues
+            const bool issuer = elect_one_sync();
             constexpr uint32_t idesc = make_idesc_bf16(PAIR ? 2 * BM : BM, BN, false, B_MN);
             int ia = 0, ib = 0, t = 0;
             for (int ct = unit; ct < total; ct += nunits, ++t) {
@@ -743,7 +745,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                 for (int cb = 0; cb < P.cpb; ++cb) {
                     const int sa = ia % SA;
                     mbar_wait(&fullA[sa], (ia / SA) & 1);
-                    if (ia == 0) tstamp(2);
+                    if (ia == 0 && lane == 0) tstamp(2);
                     tc_fence_after();
                     const uint32_t a_st = smem_u32(sA + sa * C_::A_STAGE);
                     for (int j = 0; j < 3; ++j, ++ib) {
@@ -767,8 +769,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                                 // A_hi x [B_hi | B_lo] (N = 2 BN, planes contiguous), A_lo x B_hi (N = BN)
                                 constexpr uint32_t idesc2 = make_idesc_bf16(BM, 2 * BN, false, B_MN);
                                 const uint32_t acc_on = (cb | j | k) != 0 ? 1u : 0u;
-                                issue_mma<PAIR>(dt, adh + (uint64_t)(k * (UK * 2 / 16)), bd0, idesc2, acc_on);
-                                issue_mma<PAIR>(dt + 2 * BN, adl + (uint64_t)(k * (UK * 2 / 16)), bd0, idesc, acc_on);
+                                if (issuer) {
+                                    issue_mma<PAIR>(dt, adh + (uint64_t)(k * (UK * 2 / 16)), bd0, idesc2, acc_on);
+                                    issue_mma<PAIR>(dt + 2 * BN, adl + (uint64_t)(k * (UK * 2 / 16)), bd0, idesc, acc_on);
+                                }
                             } else {
 #pragma unroll
                                 for (int pass = 0; pass < NPASS; ++pass) {
@@ -778,17 +782,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                                     const uint32_t b_addr = b_st + pb * C_::B_PLANE;
                                     const uint64_t bd = B_MN ? make_desc(b_addr + k * (UK * 128), BK * 128, 1024)
                                                              : make_desc(b_addr + k * (UK * 2), 16, 1024);
-                                    issue_mma<PAIR>(dt, ad, bd, idesc, (cb | j | k | pass) != 0 ? 1u : 0u);
+                                    if (issuer) issue_mma<PAIR>(dt, ad, bd, idesc, (cb | j | k | pass) != 0 ? 1u : 0u);
                                 }
                             }
                         }
-                        if ((ib % C_::TPS) == C_::TPS - 1) commit_to<PAIR>(&emptyB[bs]);
+                        if (issuer && (ib % C_::TPS) == C_::TPS - 1) commit_to<PAIR>(&emptyB[bs]);
                     }
-                    commit_to<PAIR>(&emptyA[sa]);  // window consumed by all three taps
+                    if (issuer) commit_to<PAIR>(&emptyA[sa]);  // window consumed by all three taps
                     ++ia;
                 }
-                commit_to<PAIR>(&tfull[acc]);  // accumulator complete
-                tstamp(t == 0 ? 3 : 4);
+                if (issuer) commit_to<PAIR>(&tfull[acc]);  // accumulator complete
+                if (lane == 0) tstamp(t == 0 ? 3 : 4);
             }
         }
         __syncwarp();
@@ -1212,7 +1216,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
             }
         }
     } else if (warp == 1) {
-        if (lane == 0 && leader) {
+        if (leader) {
+            // the whole warp runs the issue loop (uniform descriptors), the elected lane issues
+            const bool issuer = elect_one_sync();
             // ===================== MMA issuer =====================
             constexpr uint32_t idesc = make_idesc_bf16(PAIR ? 2 * BM : BM, BN, true, true);
             int it = 0, t = 0;
@@ -1227,7 +1233,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
                 for (int kb = 0; kb < nkb; ++kb, ++it) {
                     const int s = it % STAGES;
                     mbar_wait(&full[s], (it / STAGES) & 1);
-                    if (it == 0) tstamp_s(P.slot, 2);
+                    if (it == 0 && lane == 0) tstamp_s(P.slot, 2);
                     tc_fence_after();
                     const uint32_t st = smem_u32(smem + s * C_::STAGE_BYTES);
 #pragma unroll
@@ -1239,13 +1245,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
                             const uint64_t ad = make_desc(st + pa * C_::A_BYTES + k * (UK * 128), BK * 128, 1024);
                             const uint64_t bd = make_desc(st + NPL * C_::A_BYTES + pb * C_::B_BYTES + k * (UK * 128),
                                                           BK * 128, 1024);
-                            issue_mma<PAIR>(dt, ad, bd, idesc, (kb | k | pass) != 0 ? 1u : 0u);
+                            if (issuer) issue_mma<PAIR>(dt, ad, bd, idesc, (kb | k | pass) != 0 ? 1u : 0u);
                         }
                     }
-                    commit_to<PAIR>(&empty[s]);
+                    if (issuer) commit_to<PAIR>(&empty[s]);
                 }
-                commit_to<PAIR>(&tfull[acc]);
-                tstamp_s(P.slot, 3);
+                if (issuer) commit_to<PAIR>(&tfull[acc]);
+                if (lane == 0) tstamp_s(P.slot, 3);
             }
         }
         __syncwarp();

@@ -54,6 +54,21 @@ UMMA_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
     }
 }
 
+// One lane of a converged warp (elect.sync): the warp runs the MMA-issue loop together, so
+// descriptors live in uniform registers, and only the elected lane issues.
+UMMA_DEV bool elect_one_sync() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n"
+        ".reg .b32 r;\n"
+        ".reg .pred p;\n"
+        "elect.sync r|p, 0xffffffff;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 // ------------------------------------------------------------------ TMA
 UMMA_DEV void tma_prefetch(const CUtensorMap* m) {
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)m) : "memory");

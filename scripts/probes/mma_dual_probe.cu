@@ -9,15 +9,26 @@
 #include "umma.cuh"
 using namespace tem::umma;
 
+__device__ __forceinline__ uint32_t mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile("{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    return ok;
+}
+
 template <int BN, int TAPOFF, int NSTAGE = 1, int CADENCE = 0, bool BMN = false>
 __global__ void __launch_bounds__(128, 1) probe(long long* out, int nk) {
     extern __shared__ __align__(1024) uint8_t sm[];
     uint8_t* s = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm) + 1023) & ~uintptr_t(1023));
-    __shared__ uint64_t bar, bar2, bar3;
+    __shared__ uint64_t bar, bar2, bar3, ring[6];
     __shared__ uint32_t slot;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int i = threadIdx.x; i < 200 * 1024 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(s)[i] = 0;
-    if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&bar2, 1); mbar_init(&bar3, 1); fence_barrier_init(); }
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1); mbar_init(&bar2, 1); mbar_init(&bar3, 1);
+        for (int q = 0; q < 6; ++q) mbar_init(&ring[q], 1);
+        fence_barrier_init();
+    }
     if (warp == 0) tmem_alloc<512>(&slot);
     tc_fence_before();
     __syncthreads();
@@ -26,9 +37,18 @@ __global__ void __launch_bounds__(128, 1) probe(long long* out, int nk) {
     if (warp == 0 && lane == 0) {
         constexpr uint32_t id2 = make_idesc_bf16(128, 2 * BN, false, BMN), id1 = make_idesc_bf16(128, BN, false, BMN);
         // A_hi window at 0, A_lo at 24 KB (130 rows x 128 B each + pad), B [hi|lo] at 48 KB
+        if (CADENCE == 3)
+            for (int q = 0; q < 5; ++q) mbar_arrive_local(&ring[q]);  // taps 0..4 "loaded" up front
+        if (CADENCE == 4 || CADENCE == 5)
+            for (int q = 0; q < 6; ++q) mbar_arrive_local(&ring[q]);  // taps 0..5 "loaded" up front
         long long t0 = clock64();
+        uint32_t ready = 1;
         for (int i = 0; i < nk; ++i) {
             const int k = i & 3;
+            if (CADENCE == 4 && k == 1) {  // check the next tap's barrier early (non-blocking)
+                const int t = (i >> 2) + 1;
+                ready = mbar_test(&ring[t % 6], (t / 6) & 1);
+            }
             // NSTAGE > 1: walk distinct operand buffers (A stages 34 KB apart, B stages 16 KB apart)
             const int st = (i >> 2) % NSTAGE;
             const uint32_t ahi = smem_u32(s) + (NSTAGE > 1 ? st % 3 : 0) * 34816 + TAPOFF * 128;
@@ -42,6 +62,18 @@ __global__ void __launch_bounds__(128, 1) probe(long long* out, int nk) {
             if (CADENCE && k == 3) {  // the kernel's per-tap cadence: commit, then wait + fence
                 mma_commit(&bar2);
                 if (CADENCE == 2) { mbar_arrive_local(&bar3); mbar_wait(&bar3, (i >> 2) & 1); }
+                if (CADENCE == 5) mbar_wait(&ring[(i >> 2) % 6], 0);  // completed phase: the wait alone
+                if (CADENCE == 6) tc_fence_after();                     // (commit + fence only, = cadence 1)
+                if (CADENCE == 4) {
+                    const int t = i >> 2;
+                    mbar_arrive_local(&ring[(t + 6) % 6]);  // "load" of tap t + 6 (same slot as t)
+                    if (!ready) mbar_wait(&ring[(t + 1) % 6], ((t + 1) / 6) & 1);
+                }
+                if (CADENCE == 3) {  // wait on a phase completed 5 taps earlier (as the kernel's rings)
+                    const int t = i >> 2;
+                    mbar_arrive_local(&ring[(t + 5) % 6]);
+                    mbar_wait(&ring[t % 6], (t / 6) & 1);
+                }
                 tc_fence_after();
             }
         }
@@ -75,8 +107,8 @@ int main() {
     long long* d;
     cudaMalloc(&d, 16);
     for (int grid : {1, 104}) {
-        run<64, 1, 6, 0>(d, grid); run<64, 1, 6, 2>(d, grid);
-        run<64, 1, 6, 0, true>(d, grid); run<64, 1, 6, 2, true>(d, grid);
+        run<64, 1, 6, 0>(d, grid); run<64, 1, 6, 1>(d, grid); run<64, 1, 6, 2>(d, grid); run<64, 1, 6, 3>(d, grid);
+        run<64, 1, 6, 4>(d, grid); run<64, 1, 6, 5>(d, grid);
     }
     return 0;
 }
