@@ -130,6 +130,7 @@ struct UmmaParams {
     int side;            // 1: launched on the side branch (low priority)
     // conv2 FWD with the fused head (fp32 single-wave path, clusters of ntiles CTAs):
     int fused_head;
+    int amc;  // FWD / DGRAD launched as clusters of the ntiles column tiles, A window multicast
     CUtensorMap out2[2];   // dA2 hi / lo store maps
     const float* labels;   // [B][3][T] (per call)
     float lam[3];          // per call

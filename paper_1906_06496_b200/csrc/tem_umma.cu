@@ -309,13 +309,15 @@ TEM_DEV void commit_to(uint64_t* bar) {  // PAIR: the same barrier offset in bot
 // Kernel prologue shared by both kernels: barrier init (warp 0), TMEM allocation (warp 1).
 template <int TMEM_COLS, bool PAIR>
 TEM_DEV uint32_t gemm_prologue(const UmmaParams& P, uint64_t* bars, int nstage_bars, uint64_t* tfull,
-                               uint64_t* tempty, uint32_t* tslot, int warp, int lane) {
+                               uint64_t* tempty, uint32_t* tslot, int warp, int lane, bool cluster = false,
+                               int special_off = 0, int special_n = 0, int special_count = 1) {
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < 2; ++i) {
             tma_prefetch(&P.a[i]);
             tma_prefetch(&P.b[i]);
         }
-        for (int i = 0; i < nstage_bars; ++i) mbar_init(&bars[i], 1);
+        for (int i = 0; i < nstage_bars; ++i)
+            mbar_init(&bars[i], (i >= special_off && i < special_off + special_n) ? special_count : 1);
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], PAIR ? 8 : 4);  // 4 epilogue warps (x 2 CTAs)
@@ -328,18 +330,18 @@ TEM_DEV uint32_t gemm_prologue(const UmmaParams& P, uint64_t* bars, int nstage_b
     }
     tc_fence_before();
     __syncthreads();
-    if (PAIR) cluster_sync();  // barrier inits visible to the peer before any remote signal
+    if (PAIR || cluster) cluster_sync();  // barrier inits visible to peers before any remote signal
     tc_fence_after();
     pdl_trigger();  // everything above overlapped the predecessor kernel's tail
     pdl_wait();
     return *tslot;
 }
 
-template <int TMEM_COLS, bool PAIR>
+template <int TMEM_COLS, bool PAIR, bool CLUSTER = false>
 TEM_DEV void gemm_epilogue_done(uint32_t tbase, int warp) {
     tc_fence_before();
     __syncthreads();
-    if (PAIR) cluster_sync();  // no CTA leaves while its peer may still signal its barriers
+    if (PAIR || CLUSTER) cluster_sync();  // no CTA leaves while a peer may still signal its barriers
     if (warp == 1) {
         tc_fence_after();
         if (PAIR) tmem_dealloc_pair<TMEM_COLS>(tbase);
@@ -631,8 +633,14 @@ TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const f
     // no second cluster barrier: every remote access (the pushes) happened before the first
 }
 
-template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR, bool HEAD = false>
+// AMC: A-window multicast -- the launch is a cluster of the P.ntiles column tiles of one row
+// tile (one tile per CTA), which all read the same A window: cluster rank 0 loads each window
+// once with a TMA multicast into every CTA's ring (each CTA arms its own full barrier), and
+// waits on an empty barrier that all ntiles CTAs' MMA commits arrive on (the other ranks'
+// own empty barriers only pace their arming).  L2->SM traffic per chunk 81 -> ~52 KB.
+template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR, bool HEAD = false, bool AMC = false>
 __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_constant__ UmmaParams P) {
+    static_assert(!AMC || !PAIR, "A multicast: 1-CTA kernels");
     static_assert(MODE == FWD_ || MODE == DGRAD_, "halo kernel: FWD / DGRAD");
     static_assert(!HEAD || (MODE == FWD_ && !PAIR), "fused head: 1-CTA conv2 FWD");
     using C_ = CfgHalo<BN, NPASS, SA, SB, PAIR>;
@@ -670,7 +678,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
         __syncthreads();
     }
     float glab[3] = {0.f, 0.f, 0.f}, gb3[3] = {0.f, 0.f, 0.f};  // HEAD: row labels, b3 (prefetched)
-    const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, fullA, 2 * (SA + SB), tfull, tempty, tslot, warp, lane);
+    const uint32_t crank = AMC ? cluster_ctarank() : 0u;
+    const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, fullA, 2 * (SA + SB), tfull, tempty, tslot, warp, lane,
+                                                              AMC, SA, AMC && crank == 0 ? SA : 0, P.ntiles);
     if (threadIdx.x == 0) tstamp(1);
 
     auto coords = [&](int ct, int& m_tile, int& n_tile, int& split) {
@@ -695,6 +705,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                     else mbar_wait(&emptyA[sa], ((ia / SA) & 1) ^ 1);
                     if (g_probe_skip & 1) {
                         if (leader) mbar_arrive_local(&fullA[sa]);
+                    } else if (AMC) {
+                        mbar_arrive_expect_tx(&fullA[sa], C_::A_TX);  // every CTA arms its own barrier
+                        if (crank == 0) {
+                            const uint16_t all = (uint16_t)((1u << P.ntiles) - 1u);
+#pragma unroll
+                            for (int pl = 0; pl < NPL; ++pl)
+                                tma_load_2d_mc(sA + sa * C_::A_STAGE + pl * C_::A_PLANE, &P.a[pl], &fullA[sa], cb * BK,
+                                               m0 - 1, all);
+                        }
                     } else {
                         if (leader) mbar_arrive_expect_tx(&fullA[sa], (PAIR ? 2 : 1) * C_::A_TX);
 #pragma unroll
@@ -788,7 +807,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                         }
                         if (issuer && (ib % C_::TPS) == C_::TPS - 1) commit_to<PAIR>(&emptyB[bs]);
                     }
-                    if (issuer) commit_to<PAIR>(&emptyA[sa]);  // window consumed by all three taps
+                    if (issuer) {  // window consumed by all three taps
+                        if (AMC) mma_commit_mc(&emptyA[sa], (uint16_t)(1u | (1u << crank)));  // own + rank 0
+                        else commit_to<PAIR>(&emptyA[sa]);
+                    }
                     ++ia;
                 }
                 if (issuer) commit_to<PAIR>(&tfull[acc]);  // accumulator complete
@@ -805,7 +827,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
     if constexpr (HEAD)
         head_tail<BN, C_::ACC>(P, smem, epi, zrecv, hap, tbase, unit / P.ntiles, unit % P.ntiles, warp, lane, glab,
                                gb3);
-    gemm_epilogue_done<C_::TMEM_COLS, PAIR>(tbase, warp);
+    gemm_epilogue_done<C_::TMEM_COLS, PAIR, AMC>(tbase, warp);
     trace_end(P.slot);
 }
 
@@ -1498,6 +1520,67 @@ cudaError_t launch_halo_head(const UmmaParams& p, cudaStream_t s) {
     return cudaLaunchKernelEx(&cfg, k, p);
 }
 
+// FWD / DGRAD as clusters of the ntiles column tiles of a row tile, one tile per CTA, with the
+// A window multicast (AMC); the single-wave fp32 case.
+template <int MODE, int BN, int NPASS, int SA, int SB>
+cudaError_t launch_halo_amc(const UmmaParams& p, cudaStream_t s) {
+    using C_ = umma::CfgHalo<BN, NPASS, SA, SB, false>;
+    auto k = umma::umma_halo_kernel<MODE, BN, NPASS, SA, SB, false, false, true>;
+    static bool init = false;
+    if (!init) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM);
+        if (e != cudaSuccess) return e;
+        init = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[3];
+    int na = 0;
+    if (pdl_enabled()) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    na += launch_priority_attr(&attr[na], false);
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = p.ntiles;
+    attr[na].val.clusterDim.y = 1;
+    attr[na++].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(p.mtiles * p.ntiles, 1, 1);
+    cfg.blockDim = dim3(umma::NTHREADS);
+    cfg.dynamicSmemBytes = C_::SMEM;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, k, p);
+}
+
+// Clusters of ntiles CTAs of the AMC FWD / DGRAD kernel that fit at once (0: cannot launch).
+template <int MODE>
+static int amc_max_clusters(int ntiles) {
+    using C_ = umma::CfgHalo<64, 3, 3, 6, false>;
+    auto k = umma::umma_halo_kernel<MODE, 64, 3, 3, 6, false, false, true>;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = ntiles;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(ntiles * 16, 1, 1);
+    cfg.blockDim = dim3(umma::NTHREADS);
+    cfg.dynamicSmemBytes = C_::SMEM;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
 // How many row tiles of fused-head clusters fit at once (0 if the kernel cannot launch).
 int umma_head_max_clusters(int ntiles) {
     using C_ = umma::CfgHalo<64, 3, 2, 6, false>;
@@ -1754,6 +1837,17 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
             if ((g.C / 256) * S > 8) P.conv2.zpart = nullptr;  // the head sums at most 8 partial logits
         }
     }
+    // Experiment (TEM_AMC=1): conv1 FWD and conv2 DGRAD as clusters of their column tiles with
+    // the A window multicast.  Correct, but slower at c2 (FWD / DGRAD 21.0 vs 18.9 us: the
+    // mainloop does not move -- 7.9 vs 8.2 us, so it is not L2-bound -- while the cluster
+    // launch, the prologue / exit cluster barriers and rank 0 pacing all eight CTAs add ~2 us;
+    // in the fused-head kernel 27.2 vs 25.6 us)
+    if (P.npass == 3 && !cf.pair && cf.bn == 64 && P.conv1.kclust == 0 && getenv("TEM_AMC")) {
+        if (P.conv1.ntiles <= 8 && mtiles * P.conv1.ntiles <= 148 && amc_max_clusters<FWD_>(P.conv1.ntiles) >= mtiles)
+            P.conv1.amc = 1;
+        if (P.dgrad.ntiles <= 8 && mtiles * P.dgrad.ntiles <= 148 && amc_max_clusters<DGRAD_>(P.dgrad.ntiles) >= mtiles)
+            P.dgrad.amc = 1;
+    }
     const int wc = cw.bn / 64;  // chunks per WGRAD n-tile
     common(P.wgrad2);
     P.wgrad2.slot = SLOT_WGRAD2;
@@ -1817,6 +1911,7 @@ static cudaError_t dispatch(const UmmaParams& p, int npass, cudaStream_t s) {
         if (p.kclust > 0 && npass == 3) return launch_splitk<MODE, 3, 2, 2>(p, s);  // plan: fp32 only
         if constexpr (MODE == FWD_)
             if (p.fused_head) return launch_halo_head<64, 3, 2, 6>(p, s);  // plan: fp32, BN = 64
+        if (p.amc && npass == 3) return launch_halo_amc<MODE, 64, 3, 3, 6>(p, s);  // plan: fp32 single wave
         if (c.pair && c.bn == 64) return launch_halo<MODE, 64, 3, 3, 6, true>(p, s);
         if (c.pair)
             return npass == 3 ? launch_halo<MODE, 128, 3, 3, 6, true>(p, s) : launch_halo<MODE, 256, 1, 4, 8, true>(p, s);

@@ -59,6 +59,15 @@ def test_fp32_multi_tile_per_cta(tem, orc):
     s.close()
 
 
+def test_amc_cluster_kernels(tem, orc, monkeypatch):
+    """TEM_AMC=1: conv1 FWD and conv2 DGRAD as clusters of the 8 column tiles of a row tile with
+    the A window multicast by cluster rank 0 (an experiment; slower) -- same oracle contract."""
+    monkeypatch.setenv("TEM_AMC", "1")
+    s, p, x, lab, out = _compute(tem, 16, 0, batch_idx=5)
+    _check(orc, s, p, x, lab, out, 0)
+    s.close()
+
+
 def test_splitk_cluster_kernel(tem, orc, monkeypatch):
     """The experimental split-K cluster FWD/DGRAD kernel (TEM_SPLITK=1) at B = 16 fp32."""
     monkeypatch.setenv("TEM_SPLITK", "1")
