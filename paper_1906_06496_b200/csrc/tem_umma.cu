@@ -1182,6 +1182,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
     const int total = mt_u * P.ntiles * P.nsplit;
     trace_begin(P.slot);
     if (threadIdx.x == 0) tstamp_s(P.slot, 0);
+    if (g_probe_skip & 4) {  // diagnostics: skipped operands read zeros
+        for (uint32_t i = threadIdx.x; i < STAGES * C_::STAGE_BYTES / 16; i += NTHREADS)
+            reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
+        __syncthreads();
+    }
     const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, full, 2 * STAGES, tfull, tempty, tslot, warp, lane);
     if (threadIdx.x == 0) tstamp_s(P.slot, 1);
 
@@ -1211,6 +1216,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
                     const int s = it % STAGES;
                     mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
                     uint8_t* st = smem + s * C_::STAGE_BYTES;
+                    if (g_probe_skip & 4) {  // diagnostics: WGRAD operand loads skipped
+                        if (leader) mbar_arrive_local(&full[s]);
+                        continue;
+                    }
                     if (leader) mbar_arrive_expect_tx(&full[s], (PAIR ? 2 : 1) * C_::STAGE_BYTES);
                     const int p0 = p_begin + kb * BK;
 #pragma unroll
