@@ -1160,8 +1160,13 @@ struct CfgW {
     static constexpr int TMEM_COLS = 2 * BN;
 };
 
-template <int BN, int NPASS, int STAGES, bool PAIR>
+// BMC: the launch is a cluster of the P.mtiles m-tiles of one (n-tile, split), which all read
+// the same B tile: cluster rank 0 loads B once with a TMA multicast into every CTA's stage
+// (each CTA arms its own full barrier for its A + the multicast B), and its empty barrier
+// counts all mtiles CTAs' MMA commits.  Operand bytes per stage 64 -> 40 KB.
+template <int BN, int NPASS, int STAGES, bool PAIR, bool BMC = false>
 __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_constant__ UmmaParams P) {
+    static_assert(!BMC || !PAIR, "B multicast: 1-CTA kernels");
     using C_ = CfgW<BN, NPASS, STAGES, PAIR>;
     constexpr int NPL = C_::NPL;
     extern __shared__ uint8_t smem_raw[];
@@ -1187,10 +1192,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
             reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
         __syncthreads();
     }
-    const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, full, 2 * STAGES, tfull, tempty, tslot, warp, lane);
+    const uint32_t crank = BMC ? cluster_ctarank() : 0u;
+    const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, full, 2 * STAGES, tfull, tempty, tslot, warp, lane,
+                                                              BMC, STAGES, BMC && crank == 0 ? STAGES : 0, P.mtiles);
     if (threadIdx.x == 0) tstamp_s(P.slot, 1);
 
     auto coords = [&](int ct, int& m_tile, int& n_tile, int& split) {
+        if (BMC) {  // m fastest: a cluster = the m-tiles of one (n-tile, split)
+            m_tile = ct % P.mtiles;
+            const int r2 = ct / P.mtiles;
+            n_tile = r2 % P.ntiles;
+            split = r2 / P.ntiles;
+            return;
+        }
         n_tile = ct % P.ntiles;
         const int rest = ct / P.ntiles;
         const int mu = rest % mt_u;
@@ -1220,8 +1234,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
                         if (leader) mbar_arrive_local(&full[s]);
                         continue;
                     }
-                    if (leader) mbar_arrive_expect_tx(&full[s], (PAIR ? 2 : 1) * C_::STAGE_BYTES);
+                    if (leader || BMC) mbar_arrive_expect_tx(&full[s], (PAIR ? 2 : 1) * C_::STAGE_BYTES);
                     const int p0 = p_begin + kb * BK;
+                    const uint16_t mc_all = (uint16_t)((1u << P.mtiles) - 1u);
 #pragma unroll
                     for (int pl = 0; pl < NPL; ++pl) {
                         uint8_t* sa = st + pl * C_::A_BYTES;
@@ -1229,18 +1244,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
 #pragma unroll
                         for (int q = 0; q < BM / 64; ++q)
                             ld2d<PAIR>(sa + q * (BK * 128), &P.a[pl], &full[s], m0 + 64 * q, p0);
+                        if (BMC && crank != 0) continue;  // B arrives by rank 0's multicast
 #pragma unroll
                         for (int q = 0; q < C_::BR / 64; ++q) {
                             uint8_t* dst = sb + q * (BK * 128);
                             int g = n_tile * (BN / 64) + (int)rank * (C_::BR / 64) + q;
                             if (P.ones_chunk && g == 3 * P.cpj) {
                                 // all-ones chunk (lo plane: zeros): D column = sum_p dA[p][o]
-                                ld2d<PAIR>(dst, &P.ones, &full[s], 64 * pl, p0);
+                                if (BMC) tma_load_2d_mc(dst, &P.ones, &full[s], 64 * pl, p0, mc_all);
+                                else ld2d<PAIR>(dst, &P.ones, &full[s], 64 * pl, p0);
                                 continue;
                             }
                             if (g >= 3 * P.cpj) g = 3 * P.cpj - 1;  // dummy chunk, discarded
                             const int j = g / P.cpj, c0 = (g % P.cpj) * 64;
-                            ld2d<PAIR>(dst, &P.b[pl], &full[s], c0, p0 + j - 1);
+                            if (BMC) tma_load_2d_mc(dst, &P.b[pl], &full[s], c0, p0 + j - 1, mc_all);
+                            else ld2d<PAIR>(dst, &P.b[pl], &full[s], c0, p0 + j - 1);
                         }
                     }
                 }
@@ -1279,7 +1297,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
                             if (issuer) issue_mma<PAIR>(dt, ad, bd, idesc, (kb | k | pass) != 0 ? 1u : 0u);
                         }
                     }
-                    if (issuer) commit_to<PAIR>(&empty[s]);
+                    if (issuer) {
+                        if (BMC) mma_commit_mc(&empty[s], (uint16_t)(1u | (1u << crank)));  // own + rank 0
+                        else commit_to<PAIR>(&empty[s]);
+                    }
                 }
                 if (issuer) commit_to<PAIR>(&tfull[acc]);
                 if (lane == 0) tstamp_s(P.slot, 3);
@@ -1290,7 +1311,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
         epilogue_loop<WGRAD_, BN, PAIR, 1>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane);
         if (threadIdx.x == 64) tstamp_s(P.slot, 6);
     }
-    gemm_epilogue_done<C_::TMEM_COLS, PAIR>(tbase, warp);
+    gemm_epilogue_done<C_::TMEM_COLS, PAIR, BMC>(tbase, warp);
     trace_end(P.slot);
 }
 
@@ -1668,6 +1689,38 @@ cudaError_t launch_wgrad(const UmmaParams& p, cudaStream_t s) {
                              umma::CfgW<BN, NPASS, STAGES, PAIR>::SMEM, PAIR, total, &max_units, p, s);
 }
 
+// WGRAD as clusters of the mtiles m-tiles of an (n-tile, split), B multicast (one wave).
+template <int BN, int NPASS, int STAGES>
+cudaError_t launch_wgrad_bmc(const UmmaParams& p, cudaStream_t s) {
+    using C_ = umma::CfgW<BN, NPASS, STAGES, false>;
+    auto k = umma::umma_wgrad_kernel<BN, NPASS, STAGES, false, true>;
+    static bool init = false;
+    if (!init) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM);
+        if (e != cudaSuccess) return e;
+        init = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[3];
+    int na = 0;
+    if (pdl_enabled() && !p.side) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    na += launch_priority_attr(&attr[na], p.side != 0);
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = p.mtiles;
+    attr[na].val.clusterDim.y = 1;
+    attr[na++].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(p.mtiles * p.ntiles * p.nsplit, 1, 1);
+    cfg.blockDim = dim3(umma::NTHREADS);
+    cfg.dynamicSmemBytes = C_::SMEM;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, k, p);
+}
+
 }  // namespace
 
 // Tile configurations per GEMM and precision (measured on B200):
@@ -1858,6 +1911,7 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
             P.dgrad.amc = 1;
     }
     const int wc = cw.bn / 64;  // chunks per WGRAD n-tile
+    const bool wgrad_bmc = P.npass == 3 && !cw.pair && getenv("TEM_WGRAD_BMC") != nullptr;
     common(P.wgrad2);
     P.wgrad2.slot = SLOT_WGRAD2;
     P.wgrad2.side = 1;
@@ -1885,6 +1939,9 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     P.wgrad1.part_stride = (int64_t)g.C * 3 * g.Cin + g.C;
     P.wgrad1.ones_chunk = 1;
     ok &= map2d(&P.wgrad1.ones, b.ones, 128, R, brW);
+    // Experiment (TEM_WGRAD_BMC=1): WGRAD as clusters of the m-tiles sharing B, B multicast
+    for (UmmaParams* q : {&P.wgrad2, &P.wgrad1})
+        if (wgrad_bmc && q->mtiles <= 8 && q->mtiles * q->ntiles * q->nsplit <= 148) q->amc = 1;
     // epilogue store maps
     ok &= map_store2d(&P.conv1.out[0], b.h1, false, g.C, R);
     if (b.h1_lo) ok &= map_store2d(&P.conv1.out[1], b.h1_lo, false, g.C, R);
@@ -1914,6 +1971,7 @@ template <int MODE>
 static cudaError_t dispatch(const UmmaParams& p, int npass, cudaStream_t s) {
     const GemmCfg c = cfg_for(MODE, npass);
     if constexpr (MODE == WGRAD_) {
+        if (p.amc && npass == 3 && !c.pair) return launch_wgrad_bmc<128, 3, 3>(p, s);  // experiment
         if (c.pair) return npass == 3 ? launch_wgrad<256, 3, 3, true>(p, s) : launch_wgrad<256, 1, 6, true>(p, s);
         return npass == 3 ? launch_wgrad<128, 3, 3, false>(p, s) : launch_wgrad<256, 1, 4, false>(p, s);
     } else {

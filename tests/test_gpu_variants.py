@@ -211,3 +211,12 @@ def test_step_pem_host_matches_device_step(tem):
     assert np.array_equal(s2.params(0).cpu().numpy(), w1)
     assert datagen.PEM_P > 0
     s2.close()
+
+
+def test_wgrad_bmc_cluster_kernel(tem, orc, monkeypatch):
+    """TEM_WGRAD_BMC=1: both WGRADs as clusters of the 4 m-tiles of an (n-tile, split) with the B
+    tile multicast by cluster rank 0 (an experiment) -- same oracle contract."""
+    monkeypatch.setenv("TEM_WGRAD_BMC", "1")
+    s, p, x, lab, out = _compute(tem, 16, 0, batch_idx=6)
+    _check(orc, s, p, x, lab, out, 0)
+    s.close()
