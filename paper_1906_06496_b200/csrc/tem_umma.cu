@@ -2045,18 +2045,25 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     if (!no_fork &&
         (cudaEventRecord(P.fork, s) != cudaSuccess || cudaStreamWaitEvent(P.aux, P.fork, 0) != cudaSuccess))
         return cudaErrorUnknown;
-    e = P.conv2.fused_head ? launch_head_reduce_rows(g, b, mtiles_of(P), lam, loss_out, status, rec2, aux, &n)
-                           : launch_head_reduce(g, b, lam, loss_out, status, rec2, aux, &n);
-    if (e != cudaSuccess) return e;
-    // tem_step_host: the loss read-back overlaps the rest of the step (the join orders it
-    // before the exchange, so it is complete when the step is)
-    if (loss_host && cudaMemcpyAsync(loss_host, loss_out, 4 * sizeof(float), cudaMemcpyDeviceToHost, aux) != cudaSuccess)
-        return cudaErrorUnknown;
+    auto head_reduce = [&]() -> cudaError_t {
+        cudaError_t r = P.conv2.fused_head
+                            ? launch_head_reduce_rows(g, b, mtiles_of(P), lam, loss_out, status, rec2, aux, &n)
+                            : launch_head_reduce(g, b, lam, loss_out, status, rec2, aux, &n);
+        if (r != cudaSuccess) return r;
+        // tem_step_host: the loss read-back overlaps the rest of the step (the join orders it
+        // before the exchange, so it is complete when the step is)
+        if (loss_host && cudaMemcpyAsync(loss_host, loss_out, 4 * sizeof(float), cudaMemcpyDeviceToHost, aux) != cudaSuccess)
+            return cudaErrorUnknown;
+        return cudaSuccess;
+    };
+    static const bool headred_last = getenv("TEM_HEADRED_LAST") != nullptr;  // (experiment) order on the side branch
+    if (!headred_last && (e = head_reduce()) != cudaSuccess) return e;
     rec2.begin(SLOT_WGRAD2);
     e = dispatch<WGRAD_>(P.wgrad2, P.npass, aux);
     rec2.end(SLOT_WGRAD2);
     if (e != cudaSuccess) return e;
     ++n;
+    if (headred_last && (e = head_reduce()) != cudaSuccess) return e;
     if (!defer_reduce) {
     rec2.begin(SLOT_RED2);
     e = launch_pdl(umma::reduce_wgrad_kernel, dim3(296), dim3(256), 0, aux, true, (const float*)b.wpart2,
