@@ -691,8 +691,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
     };
 
     if (warp == 0) {
-        if (lane == 0) {
+        {
             // ===================== TMA producer (both CTAs of a pair) =====================
+            // the whole warp runs the loop (uniform operands), the elected lane issues
+            const bool pe = elect_one_sync();
             int ia = 0, ib = 0;
             for (int ct = unit; ct < total; ct += nunits) {
                 int m_tile, n_tile, split;
@@ -704,10 +706,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                     if (g_prod_sleep) mbar_wait_sleep(&emptyA[sa], ((ia / SA) & 1) ^ 1, g_prod_sleep);
                     else mbar_wait(&emptyA[sa], ((ia / SA) & 1) ^ 1);
                     if (g_probe_skip & 1) {
-                        if (leader) mbar_arrive_local(&fullA[sa]);
+                        if (pe && leader) mbar_arrive_local(&fullA[sa]);
                     } else if (AMC) {
-                        mbar_arrive_expect_tx(&fullA[sa], C_::A_TX);  // every CTA arms its own barrier
-                        if (crank == 0) {
+                        if (pe) mbar_arrive_expect_tx(&fullA[sa], C_::A_TX);  // every CTA arms its own barrier
+                        if (pe && crank == 0) {
                             const uint16_t all = (uint16_t)((1u << P.ntiles) - 1u);
 #pragma unroll
                             for (int pl = 0; pl < NPL; ++pl)
@@ -715,10 +717,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                                                m0 - 1, all);
                         }
                     } else {
-                        if (leader) mbar_arrive_expect_tx(&fullA[sa], (PAIR ? 2 : 1) * C_::A_TX);
+                        if (pe && leader) mbar_arrive_expect_tx(&fullA[sa], (PAIR ? 2 : 1) * C_::A_TX);
 #pragma unroll
                         for (int pl = 0; pl < NPL; ++pl)
-                            ld2d<PAIR>(sA + sa * C_::A_STAGE + pl * C_::A_PLANE, &P.a[pl], &fullA[sa], cb * BK, m0 - 1);
+                            if (pe) ld2d<PAIR>(sA + sa * C_::A_STAGE + pl * C_::A_PLANE, &P.a[pl], &fullA[sa], cb * BK, m0 - 1);
                     }
                     ++ia;
                     for (int j = 0; j < 3; ++j, ++ib) {
@@ -730,19 +732,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                             else mbar_wait(&emptyB[bs], ((ib / C_::TPS / C_::SBS) & 1) ^ 1);
                         }
                         if (g_probe_skip & 2) {
-                            if (leader && first) mbar_arrive_local(&fullB[bs]);
+                            if (pe && leader && first) mbar_arrive_local(&fullB[bs]);
                             continue;
                         }
-                        if (leader && first) mbar_arrive_expect_tx(&fullB[bs], (PAIR ? 2 : 1) * C_::TPS * C_::B_STAGE);
+                        if (pe && leader && first) mbar_arrive_expect_tx(&fullB[bs], (PAIR ? 2 : 1) * C_::TPS * C_::B_STAGE);
 #pragma unroll
                         for (int pl = 0; pl < NPL; ++pl) {
                             uint8_t* dst = sB + sb * C_::B_STAGE + pl * C_::B_PLANE;
                             if (MODE == FWD_) {
-                                ld2d<PAIR>(dst, &P.b[pl], &fullB[bs], j * P.Kc + cb * BK, n0);
+                                if (pe) ld2d<PAIR>(dst, &P.b[pl], &fullB[bs], j * P.Kc + cb * BK, n0);
                             } else {
 #pragma unroll
                                 for (int q = 0; q < C_::BR / 64; ++q)
-                                    ld3d<PAIR>(dst + q * (BK * 128), &P.b[pl], &fullB[bs], n0 + 64 * q, j, cb * BK);
+                                    if (pe) ld3d<PAIR>(dst + q * (BK * 128), &P.b[pl], &fullB[bs], n0 + 64 * q, j, cb * BK);
                             }
                         }
                     }
@@ -1218,8 +1220,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
     };
 
     if (warp == 0) {
-        if (lane == 0) {
+        {
             // ===================== TMA producer =====================
+            // the whole warp runs the loop (uniform operands), the elected lane issues
+            const bool pe = elect_one_sync();
             int it = 0;
             for (int ct = unit; ct < total; ct += nunits) {
                 int m_tile, n_tile, split, p_begin;
@@ -1231,10 +1235,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
                     mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
                     uint8_t* st = smem + s * C_::STAGE_BYTES;
                     if (g_probe_skip & 4) {  // diagnostics: WGRAD operand loads skipped
-                        if (leader) mbar_arrive_local(&full[s]);
+                        if (pe && leader) mbar_arrive_local(&full[s]);
                         continue;
                     }
-                    if (leader || BMC) mbar_arrive_expect_tx(&full[s], (PAIR ? 2 : 1) * C_::STAGE_BYTES);
+                    if (pe && (leader || BMC)) mbar_arrive_expect_tx(&full[s], (PAIR ? 2 : 1) * C_::STAGE_BYTES);
                     const int p0 = p_begin + kb * BK;
                     const uint16_t mc_all = (uint16_t)((1u << P.mtiles) - 1u);
 #pragma unroll
@@ -1243,7 +1247,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
                         uint8_t* sb = st + NPL * C_::A_BYTES + pl * C_::B_BYTES;
 #pragma unroll
                         for (int q = 0; q < BM / 64; ++q)
-                            ld2d<PAIR>(sa + q * (BK * 128), &P.a[pl], &full[s], m0 + 64 * q, p0);
+                            if (pe) ld2d<PAIR>(sa + q * (BK * 128), &P.a[pl], &full[s], m0 + 64 * q, p0);
                         if (BMC && crank != 0) continue;  // B arrives by rank 0's multicast
 #pragma unroll
                         for (int q = 0; q < C_::BR / 64; ++q) {
@@ -1251,14 +1255,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
                             int g = n_tile * (BN / 64) + (int)rank * (C_::BR / 64) + q;
                             if (P.ones_chunk && g == 3 * P.cpj) {
                                 // all-ones chunk (lo plane: zeros): D column = sum_p dA[p][o]
-                                if (BMC) tma_load_2d_mc(dst, &P.ones, &full[s], 64 * pl, p0, mc_all);
-                                else ld2d<PAIR>(dst, &P.ones, &full[s], 64 * pl, p0);
+                                if (pe) {
+                                    if (BMC) tma_load_2d_mc(dst, &P.ones, &full[s], 64 * pl, p0, mc_all);
+                                    else ld2d<PAIR>(dst, &P.ones, &full[s], 64 * pl, p0);
+                                }
                                 continue;
                             }
                             if (g >= 3 * P.cpj) g = 3 * P.cpj - 1;  // dummy chunk, discarded
                             const int j = g / P.cpj, c0 = (g % P.cpj) * 64;
-                            if (BMC) tma_load_2d_mc(dst, &P.b[pl], &full[s], c0, p0 + j - 1, mc_all);
-                            else ld2d<PAIR>(dst, &P.b[pl], &full[s], c0, p0 + j - 1);
+                            if (pe) {
+                                if (BMC) tma_load_2d_mc(dst, &P.b[pl], &full[s], c0, p0 + j - 1, mc_all);
+                                else ld2d<PAIR>(dst, &P.b[pl], &full[s], c0, p0 + j - 1);
+                            }
                         }
                     }
                 }
