@@ -225,7 +225,7 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
         }
         fence_proxy_async_smem();
         __syncwarp();
-        if (elect_one_sync()) {  // converged warp: uniform operands, one lane issues
+        if (lane == 0) {  // the lane that waits on this buffer's bulk group (bulk_wait_read above)
             if (MODE == WGRAD_) {
                 tma_store_3d(&P.out[0], sb, gc, row0, split);
             } else {
