@@ -39,12 +39,13 @@ __global__ void __launch_bounds__(128, 1) probe(long long* out, int nk) {
         // A_hi window at 0, A_lo at 24 KB (130 rows x 128 B each + pad), B [hi|lo] at 48 KB
         if (CADENCE == 3)
             for (int q = 0; q < 5; ++q) mbar_arrive_local(&ring[q]);  // taps 0..4 "loaded" up front
-        if (CADENCE == 4 || CADENCE == 5)
+        if (CADENCE == 4 || CADENCE == 5 || CADENCE == 7)
             for (int q = 0; q < 6; ++q) mbar_arrive_local(&ring[q]);  // taps 0..5 "loaded" up front
         long long t0 = clock64();
         uint32_t ready = 1;
         for (int i = 0; i < nk; ++i) {
             const int k = i & 3;
+            if (CADENCE == 7 && k == 1) ready = mbar_test(&ring[((i >> 2) + 1) % 6], 0);  // early check, completed phase
             if (CADENCE == 4 && k == 1) {  // check the next tap's barrier early (non-blocking)
                 const int t = (i >> 2) + 1;
                 ready = mbar_test(&ring[t % 6], (t / 6) & 1);
@@ -63,6 +64,7 @@ __global__ void __launch_bounds__(128, 1) probe(long long* out, int nk) {
                 mma_commit(&bar2);
                 if (CADENCE == 2) { mbar_arrive_local(&bar3); mbar_wait(&bar3, (i >> 2) & 1); }
                 if (CADENCE == 5) mbar_wait(&ring[(i >> 2) % 6], 0);  // completed phase: the wait alone
+                if (CADENCE == 7 && !ready) mbar_wait(&ring[((i >> 2) + 1) % 6], 0);
                 if (CADENCE == 6) tc_fence_after();                     // (commit + fence only, = cadence 1)
                 if (CADENCE == 4) {
                     const int t = i >> 2;
@@ -108,7 +110,7 @@ int main() {
     cudaMalloc(&d, 16);
     for (int grid : {1, 104}) {
         run<64, 1, 6, 0>(d, grid); run<64, 1, 6, 1>(d, grid); run<64, 1, 6, 2>(d, grid); run<64, 1, 6, 3>(d, grid);
-        run<64, 1, 6, 4>(d, grid); run<64, 1, 6, 5>(d, grid);
+        run<64, 1, 6, 4>(d, grid); run<64, 1, 6, 5>(d, grid); run<64, 1, 6, 7>(d, grid);
     }
     return 0;
 }
