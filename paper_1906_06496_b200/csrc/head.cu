@@ -16,6 +16,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "kernels.h"
 
@@ -339,6 +340,11 @@ void trace_set_head(unsigned long long* p) { cudaMemcpyToSymbol(g_trace, &p, siz
 namespace {
 
 int head_rows_per_cta(const Geom& g) {
+    static const int env_rpc = [] {  // (experiments) rows per CTA
+        const char* e = getenv("TEM_HEAD_RPC");
+        return e ? atoi(e) : 0;
+    }();
+    if (env_rpc > 0) return (env_rpc + 7) / 8 * 8;
     int rpc = (g.R + 443) / 444;  // one wave at 3 CTAs per SM
     rpc = (rpc + 7) / 8 * 8;
     if (rpc < 8) rpc = 8;
