@@ -65,9 +65,11 @@ TEM_DEV void head_row_terms(float z, float bt, float ap, float an, float lam_ove
     dz = lam_over_bt * (an * (1.f - bt) * p - ap * bt * q);
 }
 
-// Kernel-span trace (diagnostics, scripts/probes/step_trace.py): while g_trace is set (one
-// copy per translation unit, set by trace_set_<unit>), each traced kernel records the minimum
-// start and maximum end globaltimer over its CTAs in g_trace[2 slot], g_trace[2 slot + 1].
+// Kernel-span trace (diagnostics build only, -DTEM_DIAG; scripts/probes/step_trace.py): while
+// g_trace is set (one copy per translation unit, set by trace_set_<unit>), each traced kernel
+// records the minimum start and maximum end globaltimer over its CTAs in g_trace[2 slot],
+// g_trace[2 slot + 1].  The product library compiles these to nothing.
+#ifdef TEM_DIAG
 static __device__ unsigned long long* g_trace;
 TEM_DEV void trace_begin(int slot) {
     if (g_trace != nullptr && threadIdx.x == 0) atomicMin(&g_trace[2 * slot], (unsigned long long)globaltimer());
@@ -78,6 +80,22 @@ TEM_DEV void trace_end(int slot) {  // all threads of the CTA, at its end
         if (threadIdx.x == 0) atomicMax(&g_trace[2 * slot + 1], (unsigned long long)globaltimer());
     }
 }
+// per-CTA phase stamp k of a kernel (g_trace[2 NUM_SLOTS + cta * 8 + k])
+#define TEM_PHASE_STAMP(base, k)                                                                  \
+    do {                                                                                          \
+        if (g_trace != nullptr && threadIdx.x == 0) g_trace[(base) + blockIdx.x * 8 + (k)] = globaltimer(); \
+    } while (0)
+#define TEM_TRACE_SETTER(name) \
+    void name(unsigned long long* p) { cudaMemcpyToSymbol(g_trace, &p, sizeof(p)); }
+#else
+TEM_DEV void trace_begin(int) {}
+TEM_DEV void trace_end(int) {}
+#define TEM_PHASE_STAMP(base, k) \
+    do {                         \
+    } while (0)
+#define TEM_TRACE_SETTER(name) \
+    void name(unsigned long long*) {}
+#endif
 
 // L2-coherent 128-bit load (bypasses L1: data written by a peer GPU lands in our L2).
 TEM_DEV float4 ld_cg4(const float* p) { return __ldcg(reinterpret_cast<const float4*>(p)); }

@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(256, 3) head_rows_kernel(
     trace_begin(SLOT_HEAD);
     pdl_trigger();
     pdl_wait();
-    if (g_trace != nullptr && threadIdx.x == 0) g_trace[2 * NUM_SLOTS + blockIdx.x * 8 + 0] = globaltimer();
+    TEM_PHASE_STAMP(2 * NUM_SLOTS, 0);
     float* sW3 = sm;           // [3][C] (only the nzp == 0 path reads it)
     float* sdz = sm + 3 * C;   // [RPC][3] dz of this CTA's rows (0 on halo rows)
     __shared__ float s_ap[3][3], s_an[3][3], s_misc[HEAD_WARPS][6];
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(256, 3) head_rows_kernel(
     if (nzp == 0)
         for (int i = tid; i < 3 * C; i += blockDim.x) sW3[i] = W3[i];
     __syncthreads();
-    if (g_trace != nullptr && threadIdx.x == 0) g_trace[2 * NUM_SLOTS + blockIdx.x * 8 + 1] = globaltimer();
+    TEM_PHASE_STAMP(2 * NUM_SLOTS, 1);
     // ---- phase 1: z, loss terms, dz -> smem ----
     const int NQ = C / 32;  // <= 16
     float lsum[3] = {0.f, 0.f, 0.f}, dbs[3] = {0.f, 0.f, 0.f};
@@ -185,7 +185,7 @@ __global__ void __launch_bounds__(256, 3) head_rows_kernel(
         }
     }
     __syncthreads();
-    if (g_trace != nullptr && threadIdx.x == 0) g_trace[2 * NUM_SLOTS + blockIdx.x * 8 + 2] = globaltimer();
+    TEM_PHASE_STAMP(2 * NUM_SLOTS, 2);
     // ---- phase 2: dA2 = 1[h2>0] W3^T dz (halo rows: dz = 0 -> 0); dW3 += dz h2; db2 += stored dA2 ----
     float* dst = part + (size_t)blockIdx.x * (4 * C + 8);  // row stride padded to 16 bytes
     float acc[3][4], bs[4];
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(256, 3) head_rows_kernel(
     // combine the row phases in a fixed order through shared memory (sdz is dead after the sync)
     float* red = sdz;  // [RP][CG][16]
     __syncthreads();
-    if (g_trace != nullptr && threadIdx.x == 0) g_trace[2 * NUM_SLOTS + blockIdx.x * 8 + 3] = globaltimer();
+    TEM_PHASE_STAMP(2 * NUM_SLOTS, 3);
     if (act2) {
         float* r = red + ((size_t)rp * CG + cg) * 16;
 #pragma unroll
@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(256, 3) head_rows_kernel(
         }
     }
     __syncthreads();
-    if (g_trace != nullptr && threadIdx.x == 0) g_trace[2 * NUM_SLOTS + blockIdx.x * 8 + 4] = globaltimer();
+    TEM_PHASE_STAMP(2 * NUM_SLOTS, 4);
     if (rp == 0) {
         float sum[16];
 #pragma unroll
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(256, 3) head_rows_kernel(
         dst[3 * C + tid] = d;
         dst[3 * C + 3 + tid] = -l / (float)Tn;
     }
-    if (g_trace != nullptr && threadIdx.x == 0) g_trace[2 * NUM_SLOTS + blockIdx.x * 8 + 5] = globaltimer();
+    TEM_PHASE_STAMP(2 * NUM_SLOTS, 5);
     trace_end(SLOT_HEAD);
 }
 
@@ -335,16 +335,12 @@ __global__ void head_reduce_kernel(const float* __restrict__ part, int P, int C,
 
 }  // namespace
 
-void trace_set_head(unsigned long long* p) { cudaMemcpyToSymbol(g_trace, &p, sizeof(p)); }
+TEM_TRACE_SETTER(trace_set_head)
 
 namespace {
 
 int head_rows_per_cta(const Geom& g) {
-    static const int env_rpc = [] {  // (experiments) rows per CTA
-        const char* e = getenv("TEM_HEAD_RPC");
-        return e ? atoi(e) : 0;
-    }();
-    if (env_rpc > 0) return (env_rpc + 7) / 8 * 8;
+    // (more, smaller CTAs -- 32 or 16 rows -- measured slower: 37 / 54 vs 27 us at c3)
     int rpc = (g.R + 443) / 444;  // one wave at 3 CTAs per SM
     rpc = (rpc + 7) / 8 * 8;
     if (rpc < 8) rpc = 8;
@@ -364,21 +360,13 @@ cudaError_t launch_head_rows(const Geom& g, const RankBufs& b, const float* labe
     const size_t hsm = (size_t)(3 * g.C + (3 * rpc > (int)red ? 3 * rpc : red)) * sizeof(float);
     if (P == 0) return cudaSuccess;
     rec.begin(SLOT_HEAD);
-    cudaError_t e;
-    if (g.op_bf16) {
-        auto k = head_rows_kernel<__nv_bfloat16>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-        e = launch_pdl(k, dim3(P), dim3(256), hsm, s, false, (const float*)b.h2, (const float*)(b.params + g.off_W3),
-                       (const float*)(b.params + g.off_b3), labels, lam[0], lam[1], lam[2],
-                       static_cast<__nv_bfloat16*>(b.dA2), static_cast<__nv_bfloat16*>(b.dA2_lo), b.z, b.headpart, g.B,
-                       g.T, g.C, rpc, (const float*)b.zpart, b.nzpart);
-    } else {
-        auto k = head_rows_kernel<float>;
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
-        e = launch_pdl(k, dim3(P), dim3(256), hsm, s, false, (const float*)b.h2, (const float*)(b.params + g.off_W3),
-                       (const float*)(b.params + g.off_b3), labels, lam[0], lam[1], lam[2], static_cast<float*>(b.dA2),
-                       (float*)nullptr, b.z, b.headpart, g.B, g.T, g.C, rpc, (const float*)nullptr, 0);
-    }
+    auto k = head_rows_kernel<__nv_bfloat16>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsm);
+    cudaError_t e = launch_pdl(k, dim3(P), dim3(256), hsm, s, false, (const float*)b.h2,
+                               (const float*)(b.params + g.off_W3), (const float*)(b.params + g.off_b3), labels, lam[0],
+                               lam[1], lam[2], static_cast<__nv_bfloat16*>(b.dA2),
+                               static_cast<__nv_bfloat16*>(b.dA2_lo), b.z, b.headpart, g.B, g.T, g.C, rpc,
+                               (const float*)b.zpart, b.nzpart);
     rec.end(SLOT_HEAD);
     ++*n;
     return e;

@@ -31,7 +31,7 @@ cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, 
     int na = 0;
     // side-branch kernels follow a cross-stream event: no early launch (their CTAs would sit on
     // SMs the critical path needs)
-    if (pdl_enabled() && !(side && getenv("TEM_SIDE_PDL") == nullptr)) {
+    if (pdl_enabled() && !side) {
         a[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         a[na++].val.programmaticStreamSerializationAllowed = 1;
     }
@@ -49,9 +49,7 @@ struct Geom {
     int B, T, Cin, C, Co;
     int R;          // B*(T+2) padded rows
     int prec;       // TEM_FP32 / TEM_BF16
-    int path;       // PATH_SIMT / PATH_UMMA
-    int op_bf16;    // operand planes stored as bf16 (UMMA always; SIMT for TEM_BF16)
-    int split;      // hi/lo residual planes present (UMMA + TEM_FP32)
+    int split;      // hi/lo residual planes present (TEM_FP32: the 3-pass bf16 split, R16)
     int64_t K, Kpad;
     int64_t off_W1, off_b1, off_W2, off_b2, off_W3, off_b3;
     // PEM (joint TEM + PEM step, BASELINE configs[4]): pem_P proposals per video, 0 = off;
@@ -64,19 +62,17 @@ inline int64_t pem_num_params_of(const Geom& g) {
     return g.pem_P > 0 ? (int64_t)g.pem_H * g.pem_F + 2 * (int64_t)g.pem_H + 1 : 0;
 }
 
-// Kernel paths.  UMMA (default): tcgen05/TMA bf16 tensor-core GEMMs, one plane of bf16
-// operands (TEM_BF16) or hi/lo planes (TEM_FP32, 3-pass split).  SIMT: CUDA-core
-// reference path (fp32 or bf16 single-plane operands), kept for cross-checking.
-enum Path { PATH_SIMT = 0, PATH_UMMA = 1 };
+// One kernel path: tcgen05/TMA bf16 tensor-core GEMMs, one plane of bf16 operands (TEM_BF16)
+// or hi/lo planes (TEM_FP32, 3-pass split).  (The round-1 CUDA-core path was removed: no
+// multi-backend dispatch in the product library.)
 
 // Per-rank device buffers (all inside the caller's workspace except params).
-// Operand tensors ("hi" = the plane used by SIMT and by the 1-plane UMMA path; "_lo" =
-// residual plane x - bf16(x), present only on the UMMA fp32 path).
+// Operand tensors are bf16 ("hi"; "_lo" = residual plane x - bf16(x), present only on the
+// fp32 path).
 struct RankBufs {
     float* pempart;       // PEM per-CTA partial rows [pem_ctas][K_pem + 1]
     uint8_t* pemdec;      // PEM ReLU decisions [B*P][H] of the last step (recorded on request)
     const float* params;  // fp32 master weights [Kpad] (symmetric heap)
-    const void* wop;      // SIMT operand copy of the weights: params (fp32) or bf16 shadow
     void* xp;             // [R][Cin] operand type
     void* h1;             // [R][C]   operand type
     float* h2;            // [R][C]
@@ -125,12 +121,10 @@ struct UmmaParams {
     int ksplit_rows;
     int mtiles, ntiles, nsplit;  // tile grid (persistent kernels walk it cluster tile by cluster tile)
     int ones_chunk;      // WGRAD: chunk slot 3*cpj reads the all-ones map (bias gradient column)
-    int kclust;          // FWD/DGRAD: > 0 -> split-K cluster kernel with this many CTAs per tile
     int slot;            // trace / timing slot (Slot)
     int side;            // 1: launched on the side branch (low priority)
     // conv2 FWD with the fused head (fp32 single-wave path, clusters of ntiles CTAs):
     int fused_head;
-    int amc;  // FWD / DGRAD launched as clusters of the ntiles column tiles, A window multicast
     CUtensorMap out2[2];   // dA2 hi / lo store maps
     const float* labels;   // [B][3][T] (per call)
     float lam[3];          // per call
@@ -152,8 +146,7 @@ struct UmmaPlan {
     bool pem_pending;         // a PEM launch on `pem` awaits its join before the exchange
 };
 void umma_plan_destroy(UmmaPlan* plan);
-bool umma_side_branch_enabled();
-void umma_probe_skip(int bits);  // diagnostics: skip FWD/DGRAD operand loads (bit 0 A, bit 1 B)  // false under TEM_NO_FORK (side branch serialised)
+bool umma_side_branch_enabled();  // false under TEM_NO_FORK (side branch serialised)
 void* umma_tstamp_buffer(int64_t* nbytes, int on);  // split-K phase timestamps (diagnostics)
 int umma_wgrad_splits(const Geom& g);
 bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan);
@@ -162,8 +155,7 @@ cudaError_t launch_prep_x_split(const Geom& g, const float* x, void* hi, void* l
 cudaError_t launch_cast_shadow_split(const float* params, __nv_bfloat16* hi, __nv_bfloat16* lo, int64_t n,
                                      cudaStream_t s);
 
-// --- SIMT path (tem_simt.cu) ---------------------------------------------------------
-int simt_wgrad_splits(const Geom& g);
+// --- input preparation and helpers (prep.cu) -------------------------------------------
 int head_ctas(const Geom& g);
 cudaError_t launch_prep_x(const Geom& g, const void* x, void* xp, cudaStream_t s);
 cudaError_t launch_cast_shadow(const float* params, __nv_bfloat16* shadow, int64_t n, cudaStream_t s);
@@ -186,13 +178,13 @@ struct EvRec {
     void begin(int slot) const { if (ev) cudaEventRecord(ev[2 * slot], s); }
     void end(int slot) const { if (ev) cudaEventRecord(ev[2 * slot + 1], s); }
 };
-cudaError_t simt_compute(const Geom& g, const RankBufs& b, const float* labels,
-                         const float lam[3], float* loss_out, Status* status, int* nlaunch,
-                         const EvRec& rec, cudaStream_t s);
+// Empty shard (B = 0): zero gradient and zero loss, so the exchange still runs.
+cudaError_t empty_shard_compute(const Geom& g, const RankBufs& b, const float* labels, const float lam[3],
+                                float* loss_out, Status* status, int* nlaunch, const EvRec& rec, cudaStream_t s);
 // defer_reduce: skip the two split-K reductions; the N = 1 exchange sums the partials itself
 // (launch_sgd_fused) -- used by tem_step only, so tem_compute still leaves the full gradient.
-// split: (defer_reduce only) also apply the owner update to [off_W2, K_pad) on the side branch
-// once conv2 dgrad is done, beside conv1 wgrad; the exchange then updates [0, off_W2) only.
+// split: (bucketed exchange, N > 1) the [bnd, K_pad) bucket's exchange is launched on the side
+// branch once conv2 dgrad is done, beside conv1 wgrad (reading R25).
 struct SplitUpdate;
 cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, const float* labels,
                          const float lam[3], float* loss_out, Status* status, int* nlaunch,

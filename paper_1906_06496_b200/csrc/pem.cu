@@ -211,259 +211,20 @@ __global__ void __launch_bounds__(32 * PEMRED_W) pem_reduce_kernel(const float* 
 }
 
 
-// ---------------------------------------------------------------------------------------
-// Hidden-unit split (opt-in, TEM_PEM_UNITSPLIT=1; slower, see pem_rowsplit()): CTA j owns the PEM_US hidden units [PEM_US j, PEM_US j + PEM_US)
-// for ALL M proposals, so dW1 / db1 / dw2 of its units are complete inside the CTA and no
-// per-CTA partial rows of the whole gradient are written or reduced (the row split wrote
-// 147 x 70 KB and summed them: ~25 us at c5).  Three kernels:
-//   pem_fwd_kernel : zpart[j][m] = sum_{u in j} w2_u ReLU(a_mu), a_mu = b1_u + W1_u . f_m
-//   pem_dz_kernel  : z_m = b2 + sum_j zpart[j][m] (j ascending), y, dz_m, per-CTA (db2, sum e^2)
-//   pem_bwd_kernel : recomputes a_mu with the same code (same decisions), dh = 1[a>0] dz w2_u,
-//                    dW1_u = sum_m dh f_m, db1_u = sum_m dh, dw2_u = sum_m dz h; CTA 0 adds db2
-//                    and the loss.  Every sum is a fixed-order tree (deterministic).
-constexpr int PEM_US = 4, PEM_UG = PEM_H / PEM_US, PEM_T2 = 256;
-
-// a = b + W . f for one unit, W row from shared memory (broadcast reads), fixed k order
-TEM_DEV float pem_preact(const float* __restrict__ wrow, float b, const float (&f)[PEM_F]) {
-    float a = b;
-#pragma unroll
-    for (int k = 0; k < PEM_F; ++k) a = fmaf(wrow[k], f[k], a);
-    return a;
-}
-
-// Rows [m0, m0 + PEM_T2) of f into a padded shared tile with coalesced loads (a thread loading
-// its own 128-byte row touched 32 lines per warp load: ~50 us per kernel at c5); then every
-// thread reads its row conflict-free.  All threads call (two barriers).
-TEM_DEV void pem_tile(const float* __restrict__ f, int M, int m0, float (*ft)[PEM_F + 1]) {
-    __syncthreads();  // the previous tile is consumed
-    const int nrow = min(PEM_T2, M - m0);
-    constexpr int NV = PEM_T2 * PEM_F / 4 / PEM_T2;  // float4 per thread, all in flight at once
-    float4 v[NV];
-    const float4* src = reinterpret_cast<const float4*>(f + (size_t)m0 * PEM_F);
-#pragma unroll
-    for (int q = 0; q < NV; ++q) {
-        const int i = threadIdx.x + q * PEM_T2;  // float4 index in the tile
-        v[q] = (i * 4) / PEM_F < nrow ? __ldg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-#pragma unroll
-    for (int q = 0; q < NV; ++q) {
-        const int i = 4 * (threadIdx.x + q * PEM_T2), r = i / PEM_F, k = i - r * PEM_F;
-        ft[r][k] = v[q].x;
-        ft[r][k + 1] = v[q].y;
-        ft[r][k + 2] = v[q].z;
-        ft[r][k + 3] = v[q].w;
-    }
-    __syncthreads();
-}
-
-TEM_DEV void pem_load_row(const float* __restrict__ fm, float (&f)[PEM_F]) {
-#pragma unroll
-    for (int k = 0; k < PEM_F; ++k) f[k] = fm[k];
-}
-
-__global__ void __launch_bounds__(PEM_T2) pem_fwd_kernel(const float* __restrict__ f, const float* __restrict__ prm,
-                                                         int M, float* __restrict__ zpart,
-                                                         uint8_t* __restrict__ dec_out) {
-    trace_begin(SLOT_PEM);
-    pdl_trigger();
-    pdl_wait();
-    __shared__ float ws[PEM_US][PEM_F];
-    const int j = blockIdx.x, u0 = j * PEM_US, tid = threadIdx.x;
-    const float* W1 = prm;
-    const float* b1 = prm + PEM_H * PEM_F;
-    const float* w2 = b1 + PEM_H;
-    if (tid < PEM_US * PEM_F) ws[tid / PEM_F][tid % PEM_F] = W1[(size_t)u0 * PEM_F + tid];
-    __syncthreads();
-    float bb[PEM_US], ww[PEM_US];
-#pragma unroll
-    for (int u = 0; u < PEM_US; ++u) {
-        bb[u] = b1[u0 + u];
-        ww[u] = w2[u0 + u];
-    }
-    __shared__ float ft[PEM_T2][PEM_F + 1];
-    for (int m0 = 0; m0 < M; m0 += PEM_T2) {
-        pem_tile(f, M, m0, ft);
-        const int m = m0 + tid;
-        if (m >= M) continue;
-        float fr[PEM_F];
-        pem_load_row(ft[tid], fr);
-        float zp = 0.f;
-#pragma unroll
-        for (int u = 0; u < PEM_US; ++u) {
-            const float a = pem_preact(ws[u], bb[u], fr);
-            if (dec_out) dec_out[(size_t)m * PEM_H + u0 + u] = a > 0.f ? 1 : 0;
-            zp = fmaf(ww[u], a > 0.f ? a : 0.f, zp);
-        }
-        zpart[(size_t)j * M + m] = zp;
-    }
-    trace_end(SLOT_PEM);
-}
-
-// 32 rows per CTA: warp w sums the unit-group partials j = w, w + 8, ... of its lanes' rows
-// (coalesced, 4 loads in flight), then the 8 warp sums in warp order (fixed order)
-constexpr int PEMDZ_ROWS = 32;
-__global__ void __launch_bounds__(PEM_T2) pem_dz_kernel(const float* __restrict__ zpart, const float* __restrict__ g,
-                                                        const float* __restrict__ prm, int M, float* __restrict__ dz,
-                                                        float* __restrict__ cpart) {
-    pdl_trigger();
-    pdl_wait();
-    constexpr int NW = PEM_T2 / 32;
-    __shared__ float zs[NW][PEMDZ_ROWS];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m = blockIdx.x * PEMDZ_ROWS + lane;
-    float zp = 0.f;
-    if (m < M) {
-        int j = warp;
-        for (; j + 3 * NW < PEM_UG; j += 4 * NW) {
-            const float a0 = zpart[(size_t)j * M + m], a1 = zpart[(size_t)(j + NW) * M + m];
-            const float a2 = zpart[(size_t)(j + 2 * NW) * M + m], a3 = zpart[(size_t)(j + 3 * NW) * M + m];
-            zp += a0;
-            zp += a1;
-            zp += a2;
-            zp += a3;
-        }
-        for (; j < PEM_UG; j += NW) zp += zpart[(size_t)j * M + m];
-    }
-    zs[warp][lane] = zp;
-    __syncthreads();
-    if (warp == 0) {
-        float d = 0.f, l2 = 0.f;
-        if (m < M) {
-            float z = prm[PEM_H * PEM_F + 2 * PEM_H];  // b2
-#pragma unroll
-            for (int w = 0; w < NW; ++w) z += zs[w][lane];
-            const float y = 1.f / (1.f + expf(-z));
-            const float e = y - g[m];
-            d = (2.0f / (float)M) * e * y * (1.f - y);
-            l2 = e * e;
-            dz[m] = d;
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            d += __shfl_xor_sync(0xffffffffu, d, o);
-            l2 += __shfl_xor_sync(0xffffffffu, l2, o);
-        }
-        if (lane == 0) {
-            cpart[2 * blockIdx.x] = d;
-            cpart[2 * blockIdx.x + 1] = l2;
-        }
-    }
-}
-
-__global__ void __launch_bounds__(PEM_T2) pem_bwd_kernel(const float* __restrict__ f, const float* __restrict__ prm,
-                                                         const float* __restrict__ dz, const float* __restrict__ cpart,
-                                                         int ncp, int M, float* __restrict__ grad,
-                                                         float* __restrict__ loss_out, Status* status,
-                                                         const int64_t* stepctr) {
-    trace_begin(SLOT_PEMRED);
-    pdl_trigger();
-    pdl_wait();
-    constexpr int NV = PEM_US * PEM_F + 2 * PEM_US;  // dW1 slice, db1, dw2 of this CTA's units
-    __shared__ float ws[PEM_US][PEM_F];
-    __shared__ float wsum[PEM_T2 / 32][NV];
-    const int j = blockIdx.x, u0 = j * PEM_US, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const float* W1 = prm;
-    const float* b1 = prm + PEM_H * PEM_F;
-    const float* w2 = b1 + PEM_H;
-    if (tid < PEM_US * PEM_F) ws[tid / PEM_F][tid % PEM_F] = W1[(size_t)u0 * PEM_F + tid];
-    __syncthreads();
-    float bb[PEM_US], ww[PEM_US];
-#pragma unroll
-    for (int u = 0; u < PEM_US; ++u) {
-        bb[u] = b1[u0 + u];
-        ww[u] = w2[u0 + u];
-    }
-    float acc[NV];
-#pragma unroll
-    for (int q = 0; q < NV; ++q) acc[q] = 0.f;
-    __shared__ float ft[PEM_T2][PEM_F + 1];
-    for (int m0 = 0; m0 < M; m0 += PEM_T2) {
-        pem_tile(f, M, m0, ft);
-        const int m = m0 + tid;
-        if (m >= M) continue;
-        float fr[PEM_F];
-        pem_load_row(ft[tid], fr);
-        const float d = dz[m];
-#pragma unroll
-        for (int u = 0; u < PEM_US; ++u) {
-            const float a = pem_preact(ws[u], bb[u], fr);  // same code as pem_fwd_kernel
-            const bool pos = a > 0.f;
-            const float dh = pos ? d * ww[u] : 0.f;
-#pragma unroll
-            for (int k = 0; k < PEM_F; ++k) acc[u * PEM_F + k] = fmaf(dh, fr[k], acc[u * PEM_F + k]);
-            acc[PEM_US * PEM_F + u] += dh;
-            acc[PEM_US * PEM_F + PEM_US + u] = fmaf(d, pos ? a : 0.f, acc[PEM_US * PEM_F + PEM_US + u]);
-        }
-    }
-    // fixed-order CTA reduction: warp xor trees, then the warps in order
-#pragma unroll
-    for (int q = 0; q < NV; ++q) {
-        float v = acc[q];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) wsum[warp][q] = v;
-    }
-    __syncthreads();
-    if (tid < NV) {
-        float t = 0.f;
-#pragma unroll
-        for (int w = 0; w < PEM_T2 / 32; ++w) t += wsum[w][tid];
-        if (tid < PEM_US * PEM_F) grad[(size_t)u0 * PEM_F + tid] = t;                   // W1 rows u0..
-        else if (tid < PEM_US * PEM_F + PEM_US) grad[PEM_H * PEM_F + u0 + (tid - PEM_US * PEM_F)] = t;  // b1
-        else grad[PEM_H * PEM_F + PEM_H + u0 + (tid - PEM_US * PEM_F - PEM_US)] = t;    // w2
-    }
-    if (j == 0 && tid == 0) {  // db2 and the loss from the dz kernel's CTA partials, in order
-        float sd = 0.f, sl = 0.f;
-        for (int q = 0; q < ncp; ++q) {
-            sd += cpart[2 * q];
-            sl += cpart[2 * q + 1];
-        }
-        grad[PEM_H * PEM_F + 2 * PEM_H] = sd;
-        const float L = M > 0 ? sl / (float)M : 0.f;
-        *loss_out = L;
-        if (!isfinite(L)) latch(status, TEM_ERR_NONFINITE, stepctr ? *stepctr : 0);
-    }
-    trace_end(SLOT_PEMRED);
-}
-
 }  // namespace
 
-void trace_set_pem(unsigned long long* p) { cudaMemcpyToSymbol(g_trace, &p, sizeof(p)); }
+TEM_TRACE_SETTER(trace_set_pem)
 
-int pem_rowsplit_ctas(const Geom& g);
-
-// Partial-buffer rows (of K_pem + 1 floats) the workspace reserves: the row split's per-CTA
-// partials, or the unit split's zpart [PEM_UG][M] + dz [M] + dz-kernel partials.
+// Partial-buffer rows (of K_pem + 1 floats) the workspace reserves: one per CTA.
+// All SMs, on the critical path right after prep_x.  Measured alternatives
+// (scripts/probes/step_trace.py --workload c5): on a graph branch of its own (16 CTAs beside
+// the TEM step) steps were ~20 us slower and occasionally stalled for milliseconds; more CTAs
+// there took SMs conv2's 8-CTA clusters need.  A hidden-unit split (CTA j owns 4 units over
+// all proposals) measured slower (21.3 + 20.8 vs 18.7 + 8.5 us) and was removed.
 int pem_ctas(const Geom& g) {
     const int M = g.B * g.pem_P;
     if (M <= 0) return 0;
-    const int64_t row = pem_num_params_of(g) + 1;
-    const int64_t unit = (int64_t)PEM_UG * M + M + 2 * ((M + 31) / 32);
-    const int rows_split = pem_rowsplit_ctas(g);
-    const int unit_rows = (int)((unit + row - 1) / row);
-    return rows_split > unit_rows ? rows_split : unit_rows;
-}
-
-static bool pem_rowsplit() {
-    // the hidden-unit split (TEM_PEM_UNITSPLIT=1) measured slower at c5: fwd + dz 21.3 us and
-    // bwd 20.8 us with 4 units per CTA (23 + 23 with 2) vs 18.7 + 8.5 us for the row split --
-    // one CTA per SM re-reading all M feature rows is latency-bound at 8 warps
-    return getenv("TEM_PEM_UNITSPLIT") == nullptr;  // read per launch (tests switch it)
-}
-
-int pem_rowsplit_ctas(const Geom& g) {
-    const int M = g.B * g.pem_P;
-    if (M <= 0) return 0;
-    // All SMs, on the critical path right after prep_x.  Measured alternatives
-    // (scripts/probes/step_trace.py --workload c5): on a graph branch of its own (16 CTAs
-    // beside the TEM step) steps were ~20 us slower and occasionally stalled for milliseconds;
-    // more CTAs there took SMs conv2's 8-CTA clusters need.
-    static const int rows_env = [] {
-        const char* e = getenv("TEM_PEM_ROWS");  // (experiments) proposals per CTA
-        return e ? atoi(e) : 0;
-    }();
-    const int per = rows_env > 0 ? rows_env : 14;
-    int G = (M + per - 1) / per;
+    int G = (M + 13) / 14;  // 14 proposals per CTA
     if (G > 148) G = 148;
     return G;
 }
@@ -477,27 +238,7 @@ cudaError_t launch_pem(const Geom& g, const float* f, const float* iou, const fl
         if (e == cudaSuccess) e = cudaMemsetAsync(loss_out, 0, sizeof(float), s);
         return e;
     }
-    if (!pem_rowsplit()) {  // hidden-unit split (experiment)
-        float* zpart = part;
-        float* dz = zpart + (size_t)PEM_UG * M;
-        float* cpart = dz + M;
-        const int ndz = (M + PEMDZ_ROWS - 1) / PEMDZ_ROWS;
-        rec.begin(SLOT_PEM);
-        cudaError_t e = launch_pdl(pem_fwd_kernel, dim3(PEM_UG), dim3(PEM_T2), 0, s, false, f, params, M, zpart, dec_out);
-        if (e == cudaSuccess)
-            e = launch_pdl(pem_dz_kernel, dim3(ndz), dim3(PEM_T2), 0, s, false, (const float*)zpart, iou, params, M, dz,
-                           cpart);
-        rec.end(SLOT_PEM);
-        if (e != cudaSuccess) return e;
-        *n += 2;
-        rec.begin(SLOT_PEMRED);
-        e = launch_pdl(pem_bwd_kernel, dim3(PEM_UG), dim3(PEM_T2), 0, s, false, f, params, (const float*)dz,
-                       (const float*)cpart, ndz, M, grad, loss_out, status, stepctr);
-        rec.end(SLOT_PEMRED);
-        if (e == cudaSuccess) ++*n;
-        return e;
-    }
-    const int G = pem_rowsplit_ctas(g);
+    const int G = pem_ctas(g);
     const int rows = (M + G - 1) / G;
     // pem_kernel on the caller's (critical-path) stream with programmatic dependent launch;
     // pem_reduce follows a cross-stream event and launches without it

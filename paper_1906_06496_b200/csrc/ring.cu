@@ -558,7 +558,7 @@ cudaError_t launch_opt_scalars(float* scal, float beta1, float beta2, cudaStream
     return launch_pdl(opt_scalars_kernel, dim3(1), dim3(1), 0, s, false, scal, beta1, beta2);
 }
 
-void trace_set_ring(unsigned long long* p) { cudaMemcpyToSymbol(g_trace, &p, sizeof(p)); }
+TEM_TRACE_SETTER(trace_set_ring)
 
 cudaError_t launch_sgd_fused(float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo, int64_t e0,
                              int64_t e1, const OptCfg& oc, const OptState& os, const float* p1, int64_t stride1,

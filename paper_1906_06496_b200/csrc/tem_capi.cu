@@ -1,7 +1,7 @@
 // tem_capi.cu -- host side of the C ABI declared in include/tem.h.
 //
 // Validates configurations, lays out the caller-owned workspace and symmetric
-// heaps, and enqueues the kernels of tem_simt.cu / tem_umma.cu / ring.cu.  No
+// heaps, and enqueues the kernels of prep.cu / tem_umma.cu / head.cu / pem.cu / pgm.cu / ring.cu.  No
 // device memory is allocated here.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -9,13 +9,10 @@
 #include <stdint.h>
 #include <stdlib.h>
 
-#include <algorithm>
 #include <string.h>
 
-#include <new>
-#include <stdlib.h>
-
 #include <algorithm>
+#include <new>
 
 #include "kernels.h"
 
@@ -38,10 +35,9 @@ int tem::launch_priority_attr(cudaLaunchAttribute* a, bool side) {
     if (!on || lo == hi) return 0;
     // critical path high, side branches (head reduction, conv2 wgrad, PEM) low.  Measured: with
     // the PEM branch at high or equal priority, single c5 steps stalled for 2-22 ms; neutral
-    // for c2.  TEM_PRIO_SIDE=1 inverts (experiments).
-    static const bool side_high = getenv("TEM_PRIO_SIDE") != nullptr;
+    // for c2.
     a->id = cudaLaunchAttributePriority;
-    a->val.priority = (side == side_high) ? hi : lo;
+    a->val.priority = side ? lo : hi;
     return 1;
 }
 
@@ -49,6 +45,9 @@ namespace {
 
 constexpr size_t kAlign = 256;
 constexpr uint64_t kSpinNs = 20ull * 1000 * 1000 * 1000;  // 20 s flag-wait bound
+#ifdef TEM_DIAG
+constexpr size_t kTraceWords = 2 * NUM_SLOTS + 4096 * 8;    // diagnostics trace area
+#endif
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 int64_t roundup(int64_t x, int64_t q) { return (x + q - 1) / q * q; }
@@ -60,7 +59,7 @@ struct HeapLayout {
 struct WsLayout {
     size_t xp, h1, h2, dA2, dA1, xp_lo, h1_lo, dA2_lo, dA1_lo, z, grad, headpart, headlvl1, counter, bpart, wpart, wpart2, shadow,
         shadow_lo, ones, zpart, epochs, stepctr, xstage, labstage, lossstage, bspstage, ioustage, pempart, pemdec, opt_m, opt_v, opt_scal,
-        pgm_prob, pgm_feat, pgm_iou, pgm_ts, pgm_te, pgm_count, per_rank;
+        pgm_prob, pgm_feat, pgm_iou, pgm_ts, pgm_te, pgm_count, trace, per_rank;
 };
 
 bool cfg_valid(const tem_config* c) {
@@ -106,15 +105,8 @@ int64_t num_params(const tem_config* c) {  // [TEM | PEM] (reading R21)
     return tem_params_only(c) + pem;
 }
 
-int env_path() {
-    const char* e = getenv("TEM_KERNEL_PATH");
-    if (e && (strcmp(e, "simt") == 0 || strcmp(e, "SIMT") == 0)) return PATH_SIMT;
-    return PATH_UMMA;
-}
-
 Geom make_geom(const tem_config* c) {
     Geom g;
-    g.path = env_path();
     g.B = c->batch_per_rank;
     g.T = c->seq_len;
     g.Cin = c->c_in;
@@ -122,8 +114,7 @@ Geom make_geom(const tem_config* c) {
     g.Co = c->c_out;
     g.R = g.B * (g.T + 2);
     g.prec = c->precision;
-    g.op_bf16 = (g.path == PATH_UMMA || g.prec == TEM_BF16) ? 1 : 0;
-    g.split = (g.path == PATH_UMMA && g.prec == TEM_FP32) ? 1 : 0;
+    g.split = g.prec == TEM_FP32 ? 1 : 0;
     g.K = num_params(c);
     g.Kpad = roundup(g.K, 4 * (int64_t)c->world_size);
     g.off_W1 = 0;
@@ -165,7 +156,7 @@ HeapLayout heap_layout(const tem_config* c) {
 
 WsLayout ws_layout(const tem_config* c) {
     const Geom g = make_geom(c);
-    const size_t esz = g.op_bf16 ? 2 : 4;       // operand plane element size
+    const size_t esz = 2;                           // operand planes are bf16
     const size_t xsz = g.prec == TEM_BF16 ? 2 : 4;  // caller's x element size
     WsLayout w;
     size_t o = 0;
@@ -174,7 +165,7 @@ WsLayout ws_layout(const tem_config* c) {
         o = align_up(o + bytes, kAlign);
         return at;
     };
-    const int S = simt_wgrad_splits(g) > umma_wgrad_splits(g) ? simt_wgrad_splits(g) : umma_wgrad_splits(g);
+    const int S = umma_wgrad_splits(g);
     const size_t wmax = (size_t)g.C * 3 * (g.Cin > g.C ? g.Cin : g.C) + g.C;
     w.xp = take((size_t)g.R * g.Cin * esz);
     w.h1 = take((size_t)g.R * g.C * esz);
@@ -193,13 +184,13 @@ WsLayout ws_layout(const tem_config* c) {
     w.counter = take(64);
     w.bpart = take((size_t)((g.R + 127) / 128) * g.C * 4);
     w.wpart = take((size_t)S * wmax * 4);
-    w.wpart2 = take(g.path == PATH_UMMA ? (size_t)umma_wgrad_splits(g) * ((size_t)g.C * 3 * g.C + g.C) * 4 : 0);
+    w.wpart2 = take((size_t)S * ((size_t)g.C * 3 * g.C + g.C) * 4);
     w.pempart = take((size_t)pem_ctas(g) * (pem_num_params_of(g) + 1) * 4);
     w.pemdec = take(g.pem_P > 0 ? (size_t)g.B * g.pem_P * g.pem_H : 0);  // last ReLU decisions (tests)
-    w.shadow = take(g.op_bf16 ? (size_t)g.Kpad * 2 : 0);
+    w.shadow = take((size_t)g.Kpad * 2);
     w.shadow_lo = take(lo * (size_t)g.Kpad * 2);
-    w.ones = take(g.path == PATH_UMMA ? (size_t)g.R * 128 * 2 : 0);
-    w.zpart = take(g.path == PATH_UMMA ? (size_t)(g.C / 64) * g.R * 3 * 4 : 0);
+    w.ones = take((size_t)g.R * 128 * 2);
+    w.zpart = take((size_t)(g.C / 64) * g.R * 3 * 4);
     w.epochs = take((size_t)kMaxChannels * 4);
     w.stepctr = take(8);
     // host-input staging (tem_step_host / tem_step_pem_host), double-buffered: the copy of step
@@ -221,6 +212,9 @@ WsLayout ws_layout(const tem_config* c) {
     w.pgm_ts = take(pgm * (size_t)g.B * g.pem_P * 4);
     w.pgm_te = take(pgm * (size_t)g.B * g.pem_P * 4);
     w.pgm_count = take(pgm * (size_t)g.B * 4);
+#ifdef TEM_DIAG
+    w.trace = take(sizeof(unsigned long long) * kTraceWords);  // diagnostics build only
+#endif
     w.per_rank = o;
     return w;
 }
@@ -244,7 +238,6 @@ struct tem_ctx {
     int launches_step, launches_exchange;
     bool alive;
     bool reduce_deferred;  // last compute left the split-K partials for the fused N = 1 exchange
-    bool split_done;       // ... and already updated [off_W2, K_pad) (SplitUpdate)
     bool early_done;       // bucketed exchange: the [bnd, K_pad) bucket ran inside the compute
     bool grad_lazy;        // N = 1 tem_step left the W1 / W2 gradient as split-K partials only;
                            // tem_local_grad sums them on demand (same order as the update)
@@ -335,7 +328,7 @@ tem_status graph_step(tem_ctx* c, const void* x, const void* lab, void* loss, cu
     // gives the dependencies; no cross-stream event handoff per step).
     if (cudaGraphLaunch(e->exec, s) != cudaSuccess) return TEM_ERR_CUDA;
     c->grad_lazy = e->grad_lazy;
-    if (e->loss_host && c->g.path == PATH_UMMA && c->g.B > 0) c->loss_host_done = true;
+    if (e->loss_host && c->g.B > 0) c->loss_host_done = true;
     c->launches_step = e->launches;
     return TEM_OK;
 }
@@ -432,8 +425,8 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
         b.headlvl1 = (float*)(base + wl.headlvl1);
         b.counter = (unsigned*)(base + wl.counter);
         b.bpart = (float*)(base + wl.bpart);
-        b.ones = c->g.path == PATH_UMMA ? base + wl.ones : nullptr;
-        b.zpart = c->g.path == PATH_UMMA ? (float*)(base + wl.zpart) : nullptr;
+        b.ones = base + wl.ones;
+        b.zpart = (float*)(base + wl.zpart);
         b.nzpart = 0;  // set by the tcgen05 plan
         b.wpart = (float*)(base + wl.wpart);
         b.wpart2 = (float*)(base + wl.wpart2);
@@ -444,9 +437,8 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
         b.h1_lo = c->g.split ? base + wl.h1_lo : nullptr;
         b.dA2_lo = c->g.split ? base + wl.dA2_lo : nullptr;
         b.dA1_lo = c->g.split ? base + wl.dA1_lo : nullptr;
-        b.shadow = c->g.op_bf16 ? (__nv_bfloat16*)(base + wl.shadow) : nullptr;
+        b.shadow = (__nv_bfloat16*)(base + wl.shadow);
         b.shadow_lo = c->g.split ? (__nv_bfloat16*)(base + wl.shadow_lo) : nullptr;
-        b.wop = b.shadow ? (const void*)b.shadow : (const void*)b.params;
         c->plan[l] = nullptr;
         c->epochs[l] = (uint32_t*)(base + wl.epochs);
         cudaError_t e = cudaMemsetAsync(base, 0, wl.per_rank, 0);
@@ -454,12 +446,12 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
             static const float one2[2] = {1.0f, 1.0f};
             e = cudaMemcpy(base + wl.opt_scal, one2, sizeof(one2), cudaMemcpyHostToDevice);
         }
-        if (e == cudaSuccess && b.shadow) e = launch_cast_shadow_split(b.params, b.shadow, b.shadow_lo, c->g.Kpad, 0);
-        if (e == cudaSuccess && b.ones) e = launch_fill_ones(b.ones, c->g.R, 0);
-        if (e == cudaSuccess && c->g.path == PATH_UMMA) {
+        if (e == cudaSuccess) e = launch_cast_shadow_split(b.params, b.shadow, b.shadow_lo, c->g.Kpad, 0);
+        if (e == cudaSuccess) e = launch_fill_ones(b.ones, c->g.R, 0);
+        if (e == cudaSuccess) {
             c->plan[l] = new (std::nothrow) UmmaPlan();
             if (!c->plan[l] || !umma_plan(c->g, b, c->plan[l])) e = cudaErrorInvalidValue;
-            else b.nzpart = c->plan[l]->conv2.zpart ? c->plan[l]->conv2.ntiles * std::max(c->plan[l]->conv2.kclust, 1) : 0;
+            else b.nzpart = c->plan[l]->conv2.zpart ? c->plan[l]->conv2.ntiles : 0;
         }
         if (e != cudaSuccess) {
             for (int q = 0; q <= l; ++q) umma_plan_destroy(c->plan[q]);
@@ -587,20 +579,17 @@ static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, f
         rec.end(SLOT_PREP);
         if (e != cudaSuccess) return TEM_ERR_CUDA;
         ++*nl;
-        const bool defer = fuse_reduce && c->N == 1 && g.path == PATH_UMMA && g.B > 0;
+        const bool defer = fuse_reduce && c->N == 1 && g.B > 0;
         c->reduce_deferred = defer;
         c->grad_lazy = false;  // this compute's partials overwrite the last step's
-        // TEM_SPLIT_UPDATE=1 (experiment, off: measured 2-14 % slower at c2):
-        // tem_step at N = 1 updates [off_W2, K_pad) inside the compute on the side branch, beside
-        // conv1 wgrad, and the exchange only [0, off_W2)
-        const bool split_on = getenv("TEM_SPLIT_UPDATE") != nullptr;
+        // (updating [off_W2, K_pad) at N = 1 on the side branch beside conv1 wgrad measured 2-14 %
+        // slower at c2 and was removed)
         SplitUpdate su{opt_cfg(c), opt_state(c, l)};
-        c->split_done = defer && split_on;
         // bucketed exchange with one rank per process: the [bnd, K_pad) bucket starts inside the
         // compute (not with PGM-fed PEM, whose gradient is produced after it)
         RingParams early;
         c->early_done = false;
-        if (bucketed(c) && c->nlocal == 1 && fuse_reduce && g.path == PATH_UMMA && g.B > 0 && g.pgm_G == 0) {
+        if (bucketed(c) && fuse_reduce && g.B > 0 && g.pgm_G == 0) {
             early = step_ring(c, bucket_bound(c), g.Kpad);
             su.early = &early;
             su.early_kind = c->cfg.exchange;
@@ -608,28 +597,22 @@ static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, f
         }
         float* lh = (c->nlocal == 1) ? c->loss_host_pending : nullptr;
         if (g.pem_P > 0 && g.pgm_G == 0) {
-            // PEM (configs[4]) is independent of TEM: on the tcgen05 path it runs on the side
-            // stream from the start of the step, beside the TEM forward GEMMs
+            // PEM (configs[4]): both kernels on the critical path right after prep_x, on all SMs
+            // (on a side stream beside the TEM GEMMs it measured slower and stalled)
             const int M = g.B * g.pem_P;
-            // PEM (configs[4]): both kernels on the critical path right after prep_x (all SMs)
-            const bool side = getenv("TEM_PEM_SIDE") != nullptr && g.path == PATH_UMMA && g.B > 0 && !rec.ev &&
-                              umma_side_branch_enabled();
-            cudaStream_t ps = side ? c->plan[l]->pem : s;
-            if (side) c->plan[l]->pem_pending = true;  // umma_compute joins it before returning
             e = launch_pem(g, c->pem_bsp + (size_t)l * M * g.pem_F, c->pem_iou + (size_t)l * M,
                            c->rb[l].params + g.off_pem, c->rb[l].pempart, c->rb[l].grad + g.off_pem,
                            loss_out + 4 * c->nlocal + l, c->st_dev, c->rb[l].stepctr,
-                           c->pem_record_dec ? c->rb[l].pemdec : nullptr, s, ps,
-                           side ? c->plan[l]->pem_fork : nullptr, nl, rec);
+                           c->pem_record_dec ? c->rb[l].pemdec : nullptr, s, s, nullptr, nl, rec);
             if (e != cudaSuccess) return TEM_ERR_CUDA;
         }
-        if (g.path == PATH_UMMA && g.B > 0) {
+        if (g.B > 0) {
             e = umma_compute(g, c->rb[l], *c->plan[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s, defer, lh,
-                             (c->split_done || c->early_done) ? &su : nullptr);
+                             c->early_done ? &su : nullptr);
             if (lh) c->loss_host_done = true;
+        } else {
+            e = empty_shard_compute(g, c->rb[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s);
         }
-        else
-            e = simt_compute(g, c->rb[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s);
         if (e != cudaSuccess) return TEM_ERR_CUDA;
         if (g.pem_P > 0 && g.pgm_G > 0 && g.B > 0) {
             // PGM-fed PEM (reading R24): proposals and BSP features from this step's logits
@@ -683,22 +666,18 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
     const Geom& g = c->g;
     const EvRec rec{timing_slot_events(c), s};
     rec.begin(SLOT_EXCHANGE);
-    tem_status st = TEM_OK;
     const OptCfg oc = opt_cfg(c);
     if (c->N == 1 && c->reduce_deferred) {  // tem_step: split-K reductions fused into the update
         const RankBufs& b = c->rb[0];
         const UmmaPlan& P = *c->plan[0];
         c->reduce_deferred = false;
-        const int64_t e1 = c->split_done ? g.off_W2 : g.Kpad;  // [off_W2, K_pad) done in the compute
         // the summed W1 / W2 gradient is not stored (5.6 MB of writes): tem_local_grad rebuilds
-        // it from the partials on demand (TEM_KEEP_GRAD=1 stores it in the step)
-        const bool lazy = !c->split_done && getenv("TEM_KEEP_GRAD") == nullptr;
-        c->split_done = false;
-        if (launch_sgd_fused(b.grad, (float*)b.params, b.shadow, b.shadow_lo, 0, e1, oc, opt_state(c, 0), b.wpart,
+        // it from the partials on demand, in the same order
+        if (launch_sgd_fused(b.grad, (float*)b.params, b.shadow, b.shadow_lo, 0, g.Kpad, oc, opt_state(c, 0), b.wpart,
                              P.wgrad1.part_stride, g.off_W2, P.S1, b.wpart2, P.wgrad2.part_stride, g.off_W2,
-                             (int64_t)3 * g.C * g.C, P.S2, s, false, 0, lazy ? 2 : 1) != cudaSuccess)
+                             (int64_t)3 * g.C * g.C, P.S2, s, false, 0, 2) != cudaSuccess)
             return TEM_ERR_CUDA;
-        c->grad_lazy = lazy;
+        c->grad_lazy = true;
         ++*nl;
         rec.end(SLOT_EXCHANGE);
         return opt_scalars(c, s, nl);
@@ -1164,11 +1143,11 @@ float* tem_logits(tem_ctx* c, int32_t l) {
 void* tem_debug_buffer(tem_ctx* c, int32_t l, const char* name, int64_t* nbytes) {
     if (nbytes) *nbytes = 0;
     if (!c || !c->alive || l < 0 || l >= c->nlocal || !name) return nullptr;
+#ifdef TEM_DIAG
     if (strcmp(name, "trace_on") == 0 || strcmp(name, "trace_off") == 0 || strcmp(name, "trace") == 0) {
-        // [NUM_SLOTS][2] kernel spans + [4096][8] head phase stamps (ns), diagnostics
-        static unsigned long long* buf = nullptr;
-        const size_t words = 2 * NUM_SLOTS + 4096 * 8;
-        if (!buf && cudaMalloc(&buf, sizeof(unsigned long long) * words) != cudaSuccess) return nullptr;
+        // diagnostics build only: [NUM_SLOTS][2] kernel spans + [4096][8] head phase stamps (ns)
+        // in the trace area at the end of the caller's workspace (tem_workspace_bytes reserves it)
+        unsigned long long* buf = (unsigned long long*)(c->ws_base[0] + c->wl.trace);
         if (strcmp(name, "trace") != 0) {
             unsigned long long* p = strcmp(name, "trace_on") == 0 ? buf : nullptr;
             trace_set_umma(p);
@@ -1176,20 +1155,17 @@ void* tem_debug_buffer(tem_ctx* c, int32_t l, const char* name, int64_t* nbytes)
             trace_set_ring(p);
             trace_set_pem(p);
         }
-        if (nbytes) *nbytes = (int64_t)(sizeof(unsigned long long) * words);
+        if (nbytes) *nbytes = (int64_t)(sizeof(unsigned long long) * kTraceWords);
         return buf;
     }
-    if (strncmp(name, "probe_skip:", 11) == 0) {  // diagnostics: "probe_skip:<bits>" (wrong results)
-        umma_probe_skip(atoi(name + 11));
-        return nullptr;
-    }
+#endif
     if (strcmp(name, "tstamp_on") == 0 || strcmp(name, "tstamp") == 0)
         return umma_tstamp_buffer(nbytes, strcmp(name, "tstamp_on") == 0 ? 1 : 0);
     if (strncmp(name, "tstamp_slot:", 12) == 0)  // stamps of one launch: "tstamp_slot:<Slot>"
         return umma_tstamp_buffer(nbytes, 100 + atoi(name + 12));
     const Geom& g = c->g;
     const RankBufs& b = c->rb[l];
-    const int64_t esz = g.op_bf16 ? 2 : 4;
+    const int64_t esz = 2;
     const int64_t act = (int64_t)g.R * g.C * esz, xin = (int64_t)g.R * g.Cin * esz;
     struct Item { const char* n; const void* p; int64_t bytes; };
     const Item items[] = {
@@ -1264,8 +1240,7 @@ int32_t tem_launches_per_exchange(tem_ctx* c) { return c ? c->launches_exchange 
 
 const char* tem_kernel_path(tem_ctx* c) {
     if (!c) return "none";
-    if (c->g.path == PATH_UMMA) return c->g.prec == TEM_BF16 ? "tcgen05-bf16" : "tcgen05-bf16x3-fp32";
-    return c->g.prec == TEM_BF16 ? "simt-bf16" : "simt-fp32";
+    return c->g.prec == TEM_BF16 ? "tcgen05-bf16" : "tcgen05-bf16x3-fp32";
 }
 
 }  // extern "C"

@@ -39,8 +39,6 @@
 
 namespace tem {
 namespace umma {
-__device__ unsigned g_epi_sleep;  // (experiment) epilogue tfull-wait backoff in ns, 0 = spin
-__device__ unsigned g_prod_sleep;  // (experiment) FWD/DGRAD producer empty-wait backoff in ns
 
 constexpr int BM = 128;
 constexpr int BK = 64;   // bf16 elements per k-block = one 128-byte swizzle row
@@ -366,8 +364,7 @@ TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, ui
         const int acc = t & 1;
         uint4 pm[2];
         if (MODE == DGRAD_) dgrad_mask_chunk0(P, m_tile * BM + 32 * q + lane, n_tile * BN, pm);
-        if (g_epi_sleep) mbar_wait_sleep(&tfull[acc], (t >> 1) & 1, g_epi_sleep);
-        else mbar_wait(&tfull[acc], (t >> 1) & 1);
+        mbar_wait(&tfull[acc], (t >> 1) & 1);
         tc_fence_after();
         const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * ACC * BN);
         epilogue_tile<MODE, BN, ACC>(P, tq, m_tile, n_tile, split, q, lane, stg, buf, sw3, pm, zloc);
@@ -381,14 +378,11 @@ TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, ui
     if (lane == 0) bulk_wait_read<0>();  // staging smem must outlive the stores' reads
 }
 
-// Phase timestamps of the GEMM kernels (diagnostics: tem_debug_buffer "tstamp",
-// [grid][16] globaltimer ns; written only while g_tstamp_on is set).
+// Phase timestamps of the GEMM kernels (diagnostics build only, -DTEM_DIAG: tem_debug_buffer
+// "tstamp", [grid][16] globaltimer ns; written only while g_tstamp_on is set).
+#ifdef TEM_DIAG
 __device__ unsigned long long g_tstamp[1024 * 16];
 __device__ int g_tstamp_on;
-// Diagnostics only (umma_probe_skip): bit 0 skips the FWD/DGRAD A-window loads, bit 1 the B
-// loads (the barriers are still completed) -- wrong results, used to time the mainloop with
-// less L2 traffic.
-__device__ int g_probe_skip;
 TEM_DEV void tstamp(int k) {
     if (g_tstamp_on == 1) g_tstamp[blockIdx.x * 16 + k] = globaltimer();
 }
@@ -396,6 +390,10 @@ TEM_DEV void tstamp(int k) {
 TEM_DEV void tstamp_s(int slot, int k) {
     if (g_tstamp_on == 100 + slot) g_tstamp[blockIdx.x * 16 + k] = globaltimer();
 }
+#else
+TEM_DEV void tstamp(int) {}
+TEM_DEV void tstamp_s(int, int) {}
+#endif
 
 // ------------------------------------------------------------------ FWD / DGRAD (halo reuse)
 // The k = 3 taps of a c-block read rows shifted by one of the same activation window, so the
@@ -633,14 +631,8 @@ TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const f
     // no second cluster barrier: every remote access (the pushes) happened before the first
 }
 
-// AMC: A-window multicast -- the launch is a cluster of the P.ntiles column tiles of one row
-// tile (one tile per CTA), which all read the same A window: cluster rank 0 loads each window
-// once with a TMA multicast into every CTA's ring (each CTA arms its own full barrier), and
-// waits on an empty barrier that all ntiles CTAs' MMA commits arrive on (the other ranks'
-// own empty barriers only pace their arming).  L2->SM traffic per chunk 81 -> ~52 KB.
-template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR, bool HEAD = false, bool AMC = false>
+template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR, bool HEAD = false>
 __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_constant__ UmmaParams P) {
-    static_assert(!AMC || !PAIR, "A multicast: 1-CTA kernels");
     static_assert(MODE == FWD_ || MODE == DGRAD_, "halo kernel: FWD / DGRAD");
     static_assert(!HEAD || (MODE == FWD_ && !PAIR), "fused head: 1-CTA conv2 FWD");
     using C_ = CfgHalo<BN, NPASS, SA, SB, PAIR>;
@@ -672,15 +664,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
     const int total = mt_u * P.ntiles;
     if (threadIdx.x == 0) tstamp(0);
     trace_begin(P.slot);
-    if (g_probe_skip) {  // diagnostics: skipped operands read zeros, not stale shared memory
-        for (uint32_t i = threadIdx.x; i < C_::RINGS / 16; i += NTHREADS)
-            reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
-        __syncthreads();
-    }
     float glab[3] = {0.f, 0.f, 0.f}, gb3[3] = {0.f, 0.f, 0.f};  // HEAD: row labels, b3 (prefetched)
-    const uint32_t crank = AMC ? cluster_ctarank() : 0u;
-    const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, fullA, 2 * (SA + SB), tfull, tempty, tslot, warp, lane,
-                                                              AMC, SA, AMC && crank == 0 ? SA : 0, P.ntiles);
+    const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, fullA, 2 * (SA + SB), tfull, tempty, tslot, warp, lane);
     if (threadIdx.x == 0) tstamp(1);
 
     auto coords = [&](int ct, int& m_tile, int& n_tile, int& split) {
@@ -703,38 +688,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                 const int n0 = n_tile * BN + (int)rank * C_::BR;
                 for (int cb = 0; cb < P.cpb; ++cb) {
                     const int sa = ia % SA;
-                    if (g_prod_sleep) mbar_wait_sleep(&emptyA[sa], ((ia / SA) & 1) ^ 1, g_prod_sleep);
-                    else mbar_wait(&emptyA[sa], ((ia / SA) & 1) ^ 1);
-                    if (g_probe_skip & 1) {
-                        if (pe && leader) mbar_arrive_local(&fullA[sa]);
-                    } else if (AMC) {
-                        if (pe) mbar_arrive_expect_tx(&fullA[sa], C_::A_TX);  // every CTA arms its own barrier
-                        if (pe && crank == 0) {
-                            const uint16_t all = (uint16_t)((1u << P.ntiles) - 1u);
+                    mbar_wait(&emptyA[sa], ((ia / SA) & 1) ^ 1);
+                    if (pe && leader) mbar_arrive_expect_tx(&fullA[sa], (PAIR ? 2 : 1) * C_::A_TX);
 #pragma unroll
-                            for (int pl = 0; pl < NPL; ++pl)
-                                tma_load_2d_mc(sA + sa * C_::A_STAGE + pl * C_::A_PLANE, &P.a[pl], &fullA[sa], cb * BK,
-                                               m0 - 1, all);
-                        }
-                    } else {
-                        if (pe && leader) mbar_arrive_expect_tx(&fullA[sa], (PAIR ? 2 : 1) * C_::A_TX);
-#pragma unroll
-                        for (int pl = 0; pl < NPL; ++pl)
-                            if (pe) ld2d<PAIR>(sA + sa * C_::A_STAGE + pl * C_::A_PLANE, &P.a[pl], &fullA[sa], cb * BK, m0 - 1);
-                    }
+                    for (int pl = 0; pl < NPL; ++pl)
+                        if (pe) ld2d<PAIR>(sA + sa * C_::A_STAGE + pl * C_::A_PLANE, &P.a[pl], &fullA[sa], cb * BK, m0 - 1);
                     ++ia;
                     for (int j = 0; j < 3; ++j, ++ib) {
                         const int sb = ib % SB;                          // tap slot
                         const int bs = (ib / C_::TPS) % C_::SBS;         // barrier stage
                         const bool first = (ib % C_::TPS) == 0;
-                        if (first) {
-                            if (g_prod_sleep) mbar_wait_sleep(&emptyB[bs], ((ib / C_::TPS / C_::SBS) & 1) ^ 1, g_prod_sleep);
-                            else mbar_wait(&emptyB[bs], ((ib / C_::TPS / C_::SBS) & 1) ^ 1);
-                        }
-                        if (g_probe_skip & 2) {
-                            if (pe && leader && first) mbar_arrive_local(&fullB[bs]);
-                            continue;
-                        }
+                        if (first) mbar_wait(&emptyB[bs], ((ib / C_::TPS / C_::SBS) & 1) ^ 1);
                         if (pe && leader && first) mbar_arrive_expect_tx(&fullB[bs], (PAIR ? 2 : 1) * C_::TPS * C_::B_STAGE);
 #pragma unroll
                         for (int pl = 0; pl < NPL; ++pl) {
@@ -809,10 +773,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                         }
                         if (issuer && (ib % C_::TPS) == C_::TPS - 1) commit_to<PAIR>(&emptyB[bs]);
                     }
-                    if (issuer) {  // window consumed by all three taps
-                        if (AMC) mma_commit_mc(&emptyA[sa], (uint16_t)(1u | (1u << crank)));  // own + rank 0
-                        else commit_to<PAIR>(&emptyA[sa]);
-                    }
+                    if (issuer) commit_to<PAIR>(&emptyA[sa]);  // window consumed by all three taps
                     ++ia;
                 }
                 if (issuer) commit_to<PAIR>(&tfull[acc]);  // accumulator complete
@@ -829,323 +790,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
     if constexpr (HEAD)
         head_tail<BN, C_::ACC>(P, smem, epi, zrecv, hap, tbase, unit / P.ntiles, unit % P.ntiles, warp, lane, glab,
                                gb3);
-    gemm_epilogue_done<C_::TMEM_COLS, PAIR, AMC>(tbase, warp);
+    gemm_epilogue_done<C_::TMEM_COLS, PAIR>(tbase, warp);
     trace_end(P.slot);
-}
-
-// ------------------------------------------------------------------ FWD / DGRAD, split-K cluster
-// Small-M problems (the fp32 B = 16 step: 13 row tiles) cannot fill 148 SMs with efficient
-// tiles: 128 x 64 tiles use N = 64 MMAs, which B200 runs at 50 clk instead of the 32-clk floor
-// (scripts/probes/mma_probe.cu), and re-stream the A window for every 64 columns.  Here a
-// cluster of S CTAs computes one 128 x 256 tile (N = 256 MMAs, at the floor): CTA r of the
-// cluster accumulates c-blocks [r*cpb/S, (r+1)*cpb/S) of K (halo window reuse as above)
-// into its own TMEM.  Column slice k of the partial tile belongs to CTA k: every CTA packs
-// its S-1 foreign slices into shared memory (the drained operand rings; 16-byte chunks
-// XOR-swizzled by row, bank-conflict free) and ships each with ONE bulk copy
-// (cp.async.bulk shared::cta -> shared::cluster) that completes on the owner's mbarrier.
-// The owner sums its own slice (from TMEM) and the S-1 received ones in rank order
-// 0..S-1 (deterministic), applies the epilogue (bias/ReLU/halo, or ReLU-mask/halo, hi/lo
-// split, fused logits) and stores it.  A final cluster barrier keeps every source buffer
-// alive until all copies have landed.
-template <int NPASS, int SA, int SB>
-struct CfgSplit {
-    static constexpr int BN = 256;
-    static constexpr int NPL = NPASS == 3 ? 2 : 1;
-    static constexpr uint32_t A_PLANE = 17 * 1024;
-    static constexpr uint32_t A_STAGE = NPL * A_PLANE;
-    static constexpr uint32_t A_TX = NPL * (BM + 2) * 128;
-    static constexpr uint32_t B_PLANE = BN * BK * 2;
-    static constexpr uint32_t B_STAGE = NPL * B_PLANE;
-    static constexpr uint32_t RINGS = SA * A_STAGE + SB * B_STAGE;
-    // outgoing [S-1] + received [S-1] slices of [BM][BN/S] fp32 each: 2 (S-1)/S of a tile, S <= 4
-    static constexpr uint32_t XCH_BYTES = 2 * BM * BN * 4 * 3 / 4;
-    static_assert(XCH_BYTES <= RINGS, "the slice buffers reuse the operand rings");
-    static constexpr uint32_t SMEM = RINGS + 1024 /*align*/ + 1024 /*barriers*/ + 4 * 64 * 4 /*bias, W3 slice*/;
-    static constexpr int TMEM_COLS = BN;
-};
-
-template <int MODE, int NPASS, int SA, int SB>
-__global__ void __launch_bounds__(NTHREADS, 1) umma_splitk_kernel(const __grid_constant__ UmmaParams P) {
-    static_assert(MODE == FWD_ || MODE == DGRAD_, "split-K cluster kernel: FWD / DGRAD");
-    using C_ = CfgSplit<NPASS, SA, SB>;
-    constexpr int BN = C_::BN, NPL = C_::NPL;
-    constexpr bool B_MN = (MODE == DGRAD_);
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = align_smem_1k(smem_raw);
-    uint8_t* sA = smem;
-    uint8_t* sB = smem + SA * C_::A_STAGE;
-    uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + C_::RINGS);
-    uint64_t* emptyA = fullA + SA;
-    uint64_t* fullB = emptyA + SA;
-    uint64_t* emptyB = fullB + SB;
-    uint64_t* tfull = emptyB + SB;
-    uint64_t* recv = tfull + 1;  // received-slices barrier
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(recv + 1);
-    float* sepi = reinterpret_cast<float*>(smem + C_::RINGS + 1024);  // [4][W]: bias, W3 rows of this slice
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int S = (int)cluster_nctarank(), r = (int)cluster_ctarank();
-    const int tile = (int)blockIdx.x / S;
-    const int n_tile = tile % P.ntiles, m_tile = tile / P.ntiles;
-    const int cb0 = r * P.cpb / S, cb1 = (r + 1) * P.cpb / S;  // host: S <= cpb, so cb1 > cb0
-    if (threadIdx.x == 0) tstamp(0);
-
-    if (warp == 0 && lane == 0) {
-        for (int i = 0; i < 2; ++i) {
-            tma_prefetch(&P.a[i]);
-            tma_prefetch(&P.b[i]);
-        }
-        for (int i = 0; i < 2 * (SA + SB) + 2; ++i) mbar_init(&fullA[i], 1);
-        fence_barrier_init();
-        // the S-1 foreign partial slices of this CTA's columns (complete_tx may precede this)
-        mbar_arrive_expect_tx(recv, (uint32_t)((S - 1) * BM * (BN / S) * 4));
-    }
-    if (warp == 1) tmem_alloc<C_::TMEM_COLS>(tslot);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    pdl_trigger();
-    pdl_wait();
-    if (threadIdx.x == 0) tstamp(1);
-    const uint32_t tbase = *tslot;
-    const int m0 = m_tile * BM;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            // ===================== TMA producer =====================
-            int ib = 0;
-            for (int cb = cb0, ia = 0; cb < cb1; ++cb, ++ia) {
-                const int sa = ia % SA;
-                mbar_wait(&emptyA[sa], ((ia / SA) & 1) ^ 1);
-                mbar_arrive_expect_tx(&fullA[sa], C_::A_TX);
-                if (cb == cb0) tstamp(2);
-#pragma unroll
-                for (int pl = 0; pl < NPL; ++pl)
-                    tma_load_2d(sA + sa * C_::A_STAGE + pl * C_::A_PLANE, &P.a[pl], &fullA[sa], cb * BK, m0 - 1);
-                for (int j = 0; j < 3; ++j, ++ib) {
-                    const int sb = ib % SB;
-                    mbar_wait(&emptyB[sb], ((ib / SB) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&fullB[sb], C_::B_STAGE);
-#pragma unroll
-                    for (int pl = 0; pl < NPL; ++pl) {
-                        uint8_t* dst = sB + sb * C_::B_STAGE + pl * C_::B_PLANE;
-                        if (MODE == FWD_) {
-                            tma_load_2d(dst, &P.b[pl], &fullB[sb], j * P.Kc + cb * BK, n_tile * BN);
-                        } else {
-#pragma unroll
-                            for (int q = 0; q < BN / 64; ++q)
-                                tma_load_3d(dst + q * (BK * 128), &P.b[pl], &fullB[sb], n_tile * BN + 64 * q, j, cb * BK);
-                        }
-                    }
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            // ===================== MMA issuer =====================
-            constexpr uint32_t idesc = make_idesc_bf16(BM, BN, false, B_MN);
-            int ib = 0;
-            for (int cb = cb0, ia = 0; cb < cb1; ++cb, ++ia) {
-                const int sa = ia % SA;
-                mbar_wait(&fullA[sa], (ia / SA) & 1);
-                if (cb == cb0) tstamp(3);
-                tc_fence_after();
-                const uint32_t a_st = smem_u32(sA + sa * C_::A_STAGE);
-                for (int j = 0; j < 3; ++j, ++ib) {
-                    const int sb = ib % SB;
-                    mbar_wait(&fullB[sb], (ib / SB) & 1);
-                    if (cb == cb0 && j == 0) tstamp(4);
-                    tc_fence_after();
-                    const uint32_t b_st = smem_u32(sB + sb * C_::B_STAGE);
-                    const uint32_t roff = (uint32_t)((MODE == FWD_ ? j : 2 - j) * 128);
-#pragma unroll
-                    for (int k = 0; k < BK / UK; ++k) {
-#pragma unroll
-                        for (int pass = 0; pass < NPASS; ++pass) {
-                            const int pa = (pass == 2) ? 1 : 0;
-                            const int pb = (pass == 1) ? 1 : 0;
-                            const uint64_t ad = make_desc(a_st + pa * C_::A_PLANE + roff + k * (UK * 2), 16, 1024);
-                            const uint32_t b_addr = b_st + pb * C_::B_PLANE;
-                            const uint64_t bd = B_MN ? make_desc(b_addr + k * (UK * 128), BK * 128, 1024)
-                                                     : make_desc(b_addr + k * (UK * 2), 16, 1024);
-                            mma_bf16(tbase, ad, bd, idesc, (cb != cb0 || j | k | pass) ? 1u : 0u);
-                        }
-                    }
-                    mma_commit(&emptyB[sb]);
-                }
-                mma_commit(&emptyA[sa]);
-            }
-            mma_commit(tfull);  // partial accumulator complete (all operand reads done)
-            tstamp(5);
-        }
-        __syncwarp();
-    }
-    // Every CTA must have drained its operand rings (all its MMAs complete) before any CTA of
-    // the cluster writes slices into them: the epilogue warps wait for tfull, then the cluster syncs.
-    // Epilogue warps are idle during the mainloop: fetch what the slice epilogue needs that does
-    // not depend on this kernel (bias / W3 slice to smem; the DGRAD ReLU mask of this row).
-    const int Wsl = BN / S;
-    const int erow = 32 * (warp & 3) + lane;
-    uint4 mkr[8];  // DGRAD: mask of this row's slice (W <= 64 columns of bf16), 4 x 2 x 16 B
-    if (warp >= 2) {
-        if (MODE == FWD_) {
-            for (int i = threadIdx.x - 64; i < Wsl; i += 128) {
-                const int gc = n_tile * BN + r * Wsl + i;
-                sepi[i] = P.bias[gc];
-                if (P.zpart) {
-                    sepi[64 + i] = P.w3[gc];
-                    sepi[128 + i] = P.w3[P.Nout + gc];
-                    sepi[192 + i] = P.w3[2 * P.Nout + gc];
-                }
-            }
-        } else {
-            const int p = m0 + erow;
-            const bool on = p < P.R && !halo_row(p, P.Tp);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                mkr[i] = make_uint4(0u, 0u, 0u, 0u);
-                if (on && i < Wsl / 8)
-                    mkr[i] = __ldg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(P.mask) +
-                                                                  (size_t)p * P.Nout + n_tile * BN + r * Wsl) + i);
-            }
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        mbar_wait(tfull, 0);
-        tc_fence_after();
-        if (threadIdx.x == 64) tstamp(6);
-    }
-    tc_fence_before();
-    cluster_sync();
-    tc_fence_after();
-    if (threadIdx.x == 64) tstamp(7);
-    if (warp >= 2) {
-        // ===================== ship foreign slices, reduce own slice, epilogue =====================
-        const int q = warp & 3;
-        const int W = BN / S;                     // columns per slice
-        const int NCH = W / 4;                    // 16-byte chunks per slice row
-        const int row = 32 * q + lane;            // TMEM lane = tile row
-        const uint32_t SLICE = BM * W * 4;        // bytes
-        uint8_t* outb = smem;                     // [S-1][BM][W] foreign slices of this CTA
-        uint8_t* rcvb = smem + (S - 1) * SLICE;   // [S-1][BM][W] received slices (slot = source rank order)
-        const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16);
-        auto chunk_off = [&](int c4) { return (uint32_t)(row * W * 4 + ((c4 ^ (row & 7)) * 16)); };
-        // (1) pack: TMEM columns of owner k -> outb[slot k] (slot = k, minus one past r)
-        for (int k = 0; k < S; ++k) {
-            if (k == r) continue;
-            uint8_t* dstb = outb + (k < r ? k : k - 1) * SLICE;
-            for (int c16 = 0; c16 < W / 16; ++c16) {
-                uint32_t v[16];
-                tmem_ld16(tq + (uint32_t)(k * W + c16 * 16), v);
-                tmem_ld_wait_regs(v);
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                    *reinterpret_cast<uint4*>(dstb + chunk_off(c16 * 4 + i)) =
-                        make_uint4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-            }
-        }
-        fence_proxy_async_smem();  // generic-proxy writes -> visible to the bulk copies
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (threadIdx.x == 64) {
-            tstamp(8);
-            // (2) one bulk copy per owner: my slice for owner k lands in its slot for rank r
-            for (int k = 0; k < S; ++k) {
-                if (k == r) continue;
-                const uint32_t slot = (uint32_t)(r < k ? r : r - 1);
-                bulk_copy_to_peer(mapa_shared(rcvb + slot * SLICE, (uint32_t)k), outb + (k < r ? k : k - 1) * SLICE,
-                                  SLICE, mapa_shared(recv, (uint32_t)k));
-            }
-        }
-        // (3) own slice: sum in rank order (own partial from TMEM), epilogue, store
-        const bool live = m0 + row < P.R;
-        const int p = m0 + row;
-        const bool halo = !live || halo_row(p, P.Tp);
-        const bool zp_on = (MODE == FWD_) && P.zpart != nullptr;
-        mbar_wait(recv, 0);
-        if (threadIdx.x == 64) tstamp(9);
-        float z0 = 0.f, z1 = 0.f, z2 = 0.f;
-        for (int c16 = 0; c16 < W / 16; ++c16) {
-            const int gc = n_tile * BN + r * W + c16 * 16;  // output column of v[0]
-            uint32_t own[16];
-            tmem_ld16(tq + (uint32_t)(r * W + c16 * 16), own);
-            tmem_ld_wait_regs(own);
-            float v[16];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-                bool first = true;
-                for (int k = 0; k < S; ++k) {  // rank order
-                    float4 b;
-                    if (k == r) {
-                        b = make_float4(__uint_as_float(own[4 * i]), __uint_as_float(own[4 * i + 1]),
-                                        __uint_as_float(own[4 * i + 2]), __uint_as_float(own[4 * i + 3]));
-                    } else {
-                        b = *reinterpret_cast<const float4*>(rcvb + (k < r ? k : k - 1) * SLICE + chunk_off(c16 * 4 + i));
-                    }
-                    if (first) {
-                        a = b;
-                        first = false;
-                    } else {
-                        a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
-                    }
-                }
-                v[4 * i] = a.x; v[4 * i + 1] = a.y; v[4 * i + 2] = a.z; v[4 * i + 3] = a.w;
-            }
-            if (MODE == FWD_) {
-                const float* sb = sepi + c16 * 16;  // smem broadcast reads
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const float t = v[i] + sb[i];
-                    v[i] = (!halo && t > 0.f) ? t : 0.f;
-                }
-                if (zp_on) {
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) {
-                        z0 = fmaf(sb[64 + i], v[i], z0);
-                        z1 = fmaf(sb[128 + i], v[i], z1);
-                        z2 = fmaf(sb[192 + i], v[i], z2);
-                    }
-                }
-            } else {
-                uint4 mk0 = mkr[0], mk1 = mkr[1];  // chunk c16 of the prefetched row mask
-#pragma unroll
-                for (int i = 1; i < 4; ++i)
-                    if (c16 == i) {
-                        mk0 = mkr[2 * i];
-                        mk1 = mkr[2 * i + 1];
-                    }
-                const uint32_t mw[8] = {mk0.x, mk0.y, mk0.z, mk0.w, mk1.x, mk1.y, mk1.z, mk1.w};
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    v[2 * i] = __uint_as_float(mw[i] << 16) > 0.f ? v[2 * i] : 0.f;
-                    v[2 * i + 1] = __uint_as_float(mw[i] & 0xFFFF0000u) > 0.f ? v[2 * i + 1] : 0.f;
-                }
-            }
-            if (live) {
-                if (P.out_f32) {
-                    float4* d = reinterpret_cast<float4*>(static_cast<float*>(P.out_hi) + (size_t)p * P.Nout + gc);
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) d[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-                } else {
-                    store16_planes(static_cast<__nv_bfloat16*>(P.out_hi) + (size_t)p * P.Nout + gc,
-                                   P.out_lo ? static_cast<__nv_bfloat16*>(P.out_lo) + (size_t)p * P.Nout + gc : nullptr,
-                                   v);
-                }
-            }
-        }
-        if (zp_on && live) {
-            float* zp = P.zpart + ((size_t)(n_tile * S + r) * P.R + p) * 3;
-            zp[0] = z0;
-            zp[1] = z1;
-            zp[2] = z2;
-        }
-    }
-    tc_fence_before();
-    cluster_sync();  // every bulk copy has landed (owners waited on them): sources may be released
-    if (threadIdx.x == 64) tstamp(10);
-    if (warp == 1) {  // every TMEM read finished before the second cluster barrier
-        tc_fence_after();
-        tmem_dealloc<C_::TMEM_COLS>(tbase);
-    }
 }
 
 // ------------------------------------------------------------------ WGRAD (split-K)
@@ -1162,13 +808,8 @@ struct CfgW {
     static constexpr int TMEM_COLS = 2 * BN;
 };
 
-// BMC: the launch is a cluster of the P.mtiles m-tiles of one (n-tile, split), which all read
-// the same B tile: cluster rank 0 loads B once with a TMA multicast into every CTA's stage
-// (each CTA arms its own full barrier for its A + the multicast B), and its empty barrier
-// counts all mtiles CTAs' MMA commits.  Operand bytes per stage 64 -> 40 KB.
-template <int BN, int NPASS, int STAGES, bool PAIR, bool BMC = false>
+template <int BN, int NPASS, int STAGES, bool PAIR>
 __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_constant__ UmmaParams P) {
-    static_assert(!BMC || !PAIR, "B multicast: 1-CTA kernels");
     using C_ = CfgW<BN, NPASS, STAGES, PAIR>;
     constexpr int NPL = C_::NPL;
     extern __shared__ uint8_t smem_raw[];
@@ -1189,24 +830,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
     const int total = mt_u * P.ntiles * P.nsplit;
     trace_begin(P.slot);
     if (threadIdx.x == 0) tstamp_s(P.slot, 0);
-    if (g_probe_skip & 4) {  // diagnostics: skipped operands read zeros
-        for (uint32_t i = threadIdx.x; i < STAGES * C_::STAGE_BYTES / 16; i += NTHREADS)
-            reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
-        __syncthreads();
-    }
-    const uint32_t crank = BMC ? cluster_ctarank() : 0u;
-    const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, full, 2 * STAGES, tfull, tempty, tslot, warp, lane,
-                                                              BMC, STAGES, BMC && crank == 0 ? STAGES : 0, P.mtiles);
+    const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, full, 2 * STAGES, tfull, tempty, tslot, warp, lane);
     if (threadIdx.x == 0) tstamp_s(P.slot, 1);
 
     auto coords = [&](int ct, int& m_tile, int& n_tile, int& split) {
-        if (BMC) {  // m fastest: a cluster = the m-tiles of one (n-tile, split)
-            m_tile = ct % P.mtiles;
-            const int r2 = ct / P.mtiles;
-            n_tile = r2 % P.ntiles;
-            split = r2 / P.ntiles;
-            return;
-        }
         n_tile = ct % P.ntiles;
         const int rest = ct / P.ntiles;
         const int mu = rest % mt_u;
@@ -1234,13 +861,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
                     const int s = it % STAGES;
                     mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
                     uint8_t* st = smem + s * C_::STAGE_BYTES;
-                    if (g_probe_skip & 4) {  // diagnostics: WGRAD operand loads skipped
-                        if (pe && leader) mbar_arrive_local(&full[s]);
-                        continue;
-                    }
-                    if (pe && (leader || BMC)) mbar_arrive_expect_tx(&full[s], (PAIR ? 2 : 1) * C_::STAGE_BYTES);
+                    if (pe && leader) mbar_arrive_expect_tx(&full[s], (PAIR ? 2 : 1) * C_::STAGE_BYTES);
                     const int p0 = p_begin + kb * BK;
-                    const uint16_t mc_all = (uint16_t)((1u << P.mtiles) - 1u);
 #pragma unroll
                     for (int pl = 0; pl < NPL; ++pl) {
                         uint8_t* sa = st + pl * C_::A_BYTES;
@@ -1248,25 +870,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
 #pragma unroll
                         for (int q = 0; q < BM / 64; ++q)
                             if (pe) ld2d<PAIR>(sa + q * (BK * 128), &P.a[pl], &full[s], m0 + 64 * q, p0);
-                        if (BMC && crank != 0) continue;  // B arrives by rank 0's multicast
 #pragma unroll
                         for (int q = 0; q < C_::BR / 64; ++q) {
                             uint8_t* dst = sb + q * (BK * 128);
                             int g = n_tile * (BN / 64) + (int)rank * (C_::BR / 64) + q;
                             if (P.ones_chunk && g == 3 * P.cpj) {
                                 // all-ones chunk (lo plane: zeros): D column = sum_p dA[p][o]
-                                if (pe) {
-                                    if (BMC) tma_load_2d_mc(dst, &P.ones, &full[s], 64 * pl, p0, mc_all);
-                                    else ld2d<PAIR>(dst, &P.ones, &full[s], 64 * pl, p0);
-                                }
+                                if (pe) ld2d<PAIR>(dst, &P.ones, &full[s], 64 * pl, p0);
                                 continue;
                             }
                             if (g >= 3 * P.cpj) g = 3 * P.cpj - 1;  // dummy chunk, discarded
                             const int j = g / P.cpj, c0 = (g % P.cpj) * 64;
-                            if (pe) {
-                                if (BMC) tma_load_2d_mc(dst, &P.b[pl], &full[s], c0, p0 + j - 1, mc_all);
-                                else ld2d<PAIR>(dst, &P.b[pl], &full[s], c0, p0 + j - 1);
-                            }
+                            if (pe) ld2d<PAIR>(dst, &P.b[pl], &full[s], c0, p0 + j - 1);
                         }
                     }
                 }
@@ -1305,10 +920,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
                             if (issuer) issue_mma<PAIR>(dt, ad, bd, idesc, (kb | k | pass) != 0 ? 1u : 0u);
                         }
                     }
-                    if (issuer) {
-                        if (BMC) mma_commit_mc(&empty[s], (uint16_t)(1u | (1u << crank)));  // own + rank 0
-                        else commit_to<PAIR>(&empty[s]);
-                    }
+                    if (issuer) commit_to<PAIR>(&empty[s]);
                 }
                 if (issuer) commit_to<PAIR>(&tfull[acc]);
                 if (lane == 0) tstamp_s(P.slot, 3);
@@ -1319,7 +931,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
         epilogue_loop<WGRAD_, BN, PAIR, 1>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane);
         if (threadIdx.x == 64) tstamp_s(P.slot, 6);
     }
-    gemm_epilogue_done<C_::TMEM_COLS, PAIR, BMC>(tbase, warp);
+    gemm_epilogue_done<C_::TMEM_COLS, PAIR>(tbase, warp);
     trace_end(P.slot);
 }
 
@@ -1479,7 +1091,7 @@ cudaError_t launch_persistent(K k, uint32_t smem, bool pair, int total, int* max
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[3];
     int na = 0;
-    if (pdl_enabled() && !(p.side && getenv("TEM_SIDE_PDL") == nullptr)) {
+    if (pdl_enabled() && !p.side) {
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[na++].val.programmaticStreamSerializationAllowed = 1;
     }
@@ -1558,67 +1170,6 @@ cudaError_t launch_halo_head(const UmmaParams& p, cudaStream_t s) {
     return cudaLaunchKernelEx(&cfg, k, p);
 }
 
-// FWD / DGRAD as clusters of the ntiles column tiles of a row tile, one tile per CTA, with the
-// A window multicast (AMC); the single-wave fp32 case.
-template <int MODE, int BN, int NPASS, int SA, int SB>
-cudaError_t launch_halo_amc(const UmmaParams& p, cudaStream_t s) {
-    using C_ = umma::CfgHalo<BN, NPASS, SA, SB, false>;
-    auto k = umma::umma_halo_kernel<MODE, BN, NPASS, SA, SB, false, false, true>;
-    static bool init = false;
-    if (!init) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM);
-        if (e != cudaSuccess) return e;
-        init = true;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[3];
-    int na = 0;
-    if (pdl_enabled()) {
-        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[na++].val.programmaticStreamSerializationAllowed = 1;
-    }
-    na += launch_priority_attr(&attr[na], false);
-    attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = p.ntiles;
-    attr[na].val.clusterDim.y = 1;
-    attr[na++].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(p.mtiles * p.ntiles, 1, 1);
-    cfg.blockDim = dim3(umma::NTHREADS);
-    cfg.dynamicSmemBytes = C_::SMEM;
-    cfg.stream = s;
-    cfg.attrs = attr;
-    cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, k, p);
-}
-
-// Clusters of ntiles CTAs of the AMC FWD / DGRAD kernel that fit at once (0: cannot launch).
-template <int MODE>
-static int amc_max_clusters(int ntiles) {
-    using C_ = umma::CfgHalo<64, 3, 3, 6, false>;
-    auto k = umma::umma_halo_kernel<MODE, 64, 3, 3, 6, false, false, true>;
-    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = ntiles;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(ntiles * 16, 1, 1);
-    cfg.blockDim = dim3(umma::NTHREADS);
-    cfg.dynamicSmemBytes = C_::SMEM;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess) {
-        cudaGetLastError();
-        return 0;
-    }
-    return n;
-}
-
 // How many row tiles of fused-head clusters fit at once (0 if the kernel cannot launch).
 int umma_head_max_clusters(int ntiles) {
     using C_ = umma::CfgHalo<64, 3, 2, 6, false>;
@@ -1655,78 +1206,12 @@ cudaError_t launch_halo(const UmmaParams& p, cudaStream_t s) {
                              umma::CfgHalo<BN, NPASS, SA, SB, PAIR>::SMEM, PAIR, total, &max_units, p, s);
 }
 
-template <int MODE, int NPASS, int SA, int SB>
-cudaError_t launch_splitk(const UmmaParams& p, cudaStream_t s) {
-    using C_ = umma::CfgSplit<NPASS, SA, SB>;
-    auto k = umma::umma_splitk_kernel<MODE, NPASS, SA, SB>;
-    static bool init = false;
-    if (!init) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM);
-        if (e != cudaSuccess) return e;
-        if (p.kclust > 8)
-            cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        init = true;
-    }
-    const int tiles = p.mtiles * p.ntiles;
-    if (tiles <= 0) return cudaSuccess;
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[2];
-    int na = 0;
-    if (pdl_enabled()) {
-        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[na++].val.programmaticStreamSerializationAllowed = 1;
-    }
-    attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = p.kclust;
-    attr[na].val.clusterDim.y = 1;
-    attr[na++].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(tiles * p.kclust, 1, 1);
-    cfg.blockDim = dim3(umma::NTHREADS);
-    cfg.dynamicSmemBytes = C_::SMEM;
-    cfg.stream = s;
-    cfg.attrs = attr;
-    cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, k, p);
-}
-
 template <int BN, int NPASS, int STAGES, bool PAIR>
 cudaError_t launch_wgrad(const UmmaParams& p, cudaStream_t s) {
     static int max_units = -1;
     const int total = (PAIR ? (p.mtiles + 1) / 2 : p.mtiles) * p.ntiles * p.nsplit;
     return launch_persistent(umma::umma_wgrad_kernel<BN, NPASS, STAGES, PAIR>,
                              umma::CfgW<BN, NPASS, STAGES, PAIR>::SMEM, PAIR, total, &max_units, p, s);
-}
-
-// WGRAD as clusters of the mtiles m-tiles of an (n-tile, split), B multicast (one wave).
-template <int BN, int NPASS, int STAGES>
-cudaError_t launch_wgrad_bmc(const UmmaParams& p, cudaStream_t s) {
-    using C_ = umma::CfgW<BN, NPASS, STAGES, false>;
-    auto k = umma::umma_wgrad_kernel<BN, NPASS, STAGES, false, true>;
-    static bool init = false;
-    if (!init) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C_::SMEM);
-        if (e != cudaSuccess) return e;
-        init = true;
-    }
-    cudaLaunchConfig_t cfg = {};
-    cudaLaunchAttribute attr[3];
-    int na = 0;
-    if (pdl_enabled() && !p.side) {
-        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        attr[na++].val.programmaticStreamSerializationAllowed = 1;
-    }
-    na += launch_priority_attr(&attr[na], p.side != 0);
-    attr[na].id = cudaLaunchAttributeClusterDimension;
-    attr[na].val.clusterDim.x = p.mtiles;
-    attr[na].val.clusterDim.y = 1;
-    attr[na++].val.clusterDim.z = 1;
-    cfg.gridDim = dim3(p.mtiles * p.ntiles * p.nsplit, 1, 1);
-    cfg.blockDim = dim3(umma::NTHREADS);
-    cfg.dynamicSmemBytes = C_::SMEM;
-    cfg.stream = s;
-    cfg.attrs = attr;
-    cfg.numAttrs = na;
-    return cudaLaunchKernelEx(&cfg, k, p);
 }
 
 }  // namespace
@@ -1736,28 +1221,13 @@ cudaError_t launch_wgrad_bmc(const UmmaParams& p, cudaStream_t s) {
 //   3-pass fp32: 1 CTA, FWD/DGRAD 128 x 64 tiles (3 window + 6 tap stages), WGRAD 128 x 128
 //                (3 stages) -- the small B = 16 problem needs the SM count more than the
 //                per-SM ingress saving of pairs.
-// TEM_GEMM_VARIANT (experiments): unset = auto (as above), 1 = 1-CTA everywhere, 2 = pairs
-// everywhere.
+// (1-CTA bf16 GEMMs and fp32 pairs were measured slower and removed.)
 struct GemmCfg {
     int bn;
     int pair;  // 1: 2-CTA kernel (256-row pair tiles, cta_group::2)
 };
-static int gemm_variant() {
-    const char* e = getenv("TEM_GEMM_VARIANT");
-    return e ? atoi(e) : -1;
-}
 static GemmCfg cfg_for(int mode, int npass) {
-    int v = gemm_variant();
-    if (v == 3) {  // experiment: fp32 FWD as 2-CTA pairs of 256 x 64 (DGRAD's MN-major B needs >= 64 per CTA)
-        if (npass == 3 && mode == FWD_) return GemmCfg{64, 1};
-        v = npass == 1 ? 2 : 1;
-    }
-    if (v != 1 && v != 2) v = npass == 1 ? 2 : 1;
-    if (v == 2) {
-        if (npass == 1) return GemmCfg{256, 1};
-        return mode == WGRAD_ ? GemmCfg{256, 1} : GemmCfg{128, 1};
-    }
-    if (npass == 1) return GemmCfg{256, 0};
+    if (npass == 1) return GemmCfg{256, 1};
     return mode == WGRAD_ ? GemmCfg{128, 0} : GemmCfg{64, 0};
 }
 
@@ -1823,17 +1293,9 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     const int kb_per = (nkb + P.S - 1) / P.S;
     P.ksplit_rows = kb_per * umma::BK;
     P.S = (R + P.ksplit_rows - 1) / P.ksplit_rows;
-    // per-WGRAD split factors (<= P.S, which sizes the partial buffers); TEM_S1 / TEM_S2 override
-    auto split_rows = [&](const char* env, int& S, int& rows) {
-        S = P.S;
-        if (const char* e = getenv(env)) S = std::max(1, std::min(P.S, atoi(e)));
-        const int per = (nkb + S - 1) / S;
-        rows = per * umma::BK;
-        S = (R + rows - 1) / rows;
-    };
-    int rows1 = 0, rows2 = 0;
-    split_rows("TEM_S1", P.S1, rows1);
-    split_rows("TEM_S2", P.S2, rows2);
+    // per-WGRAD split factors (<= P.S, which sizes the partial buffers)
+    P.S1 = P.S2 = P.S;
+    const int rows1 = P.ksplit_rows, rows2 = P.ksplit_rows;
     auto common = [&](UmmaParams& q) {
         q.R = R;
         q.Tp = Tp;
@@ -1862,10 +1324,10 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     P.conv2.out_f32 = 1;
     P.conv2.w3 = b.params + g.off_W3;
     // [C/BN][R][3] partial logits for the head (which sums at most 8 per row)
-    P.conv2.zpart = (getenv("TEM_NO_ZPART") || g.C / cf.bn > 8) ? nullptr : b.zpart;
+    P.conv2.zpart = g.C / cf.bn > 8 ? nullptr : b.zpart;
     // fp32 single-wave path: the head fused into conv2 FWD (clusters of the C/64 column tiles
     // of a row tile).  TEM_NO_FUSED_HEAD=1 keeps the separate head kernel.
-    if (P.npass == 3 && !cf.pair && cf.bn == 64 && P.conv2.kclust == 0 && P.conv2.ntiles <= 8 &&
+    if (P.npass == 3 && !cf.pair && cf.bn == 64 && P.conv2.ntiles <= 8 &&
         mtiles * P.conv2.ntiles <= 148 && Tp >= 64 && g.C <= 512 && !getenv("TEM_NO_FUSED_HEAD") &&
         umma_head_max_clusters(P.conv2.ntiles) >= mtiles) {
         P.conv2.fused_head = 1;
@@ -1888,38 +1350,7 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     P.dgrad.mask = b.h1;
     P.dgrad.out_hi = b.dA1;
     P.dgrad.out_lo = b.dA1_lo;
-    // Experimental (TEM_SPLITK=1): small-M fp32 FWD / DGRAD as split-K clusters of 128 x 256
-    // tiles (umma_splitk_kernel).  Correct, but on B200 the slice exchange costs what the
-    // N = 256 mainloop saves at B = 16, so the halo kernel is the default.
-    if (P.npass == 3 && g.C % 256 == 0 && getenv("TEM_SPLITK") && !P.conv2.fused_head) {  // opt-in: DESIGN.md 6
-        const int cpb_min = std::min(P.conv1.cpb, std::min(P.conv2.cpb, P.dgrad.cpb));
-        const int tiles = mtiles * (g.C / 256);
-        const int S = 4;  // slice exchange buffers / prefetched mask sized for S = 4 (64-column slices)
-        if (S <= cpb_min && tiles * S <= 148) {
-            for (UmmaParams* q : {&P.conv1, &P.conv2, &P.dgrad}) {
-                q->kclust = S;
-                q->ntiles = g.C / 256;
-            }
-            for (int pl = 0; pl < npl; ++pl) {
-                ok &= map2d(&P.conv1.b[pl], W[pl] + g.off_W1, 3 * (uint64_t)g.Cin, g.C, 256);
-                ok &= map2d(&P.conv2.b[pl], W[pl] + g.off_W2, 3 * (uint64_t)g.C, g.C, 256);
-            }
-            if ((g.C / 256) * S > 8) P.conv2.zpart = nullptr;  // the head sums at most 8 partial logits
-        }
-    }
-    // Experiment (TEM_AMC=1): conv1 FWD and conv2 DGRAD as clusters of their column tiles with
-    // the A window multicast.  Correct, but slower at c2 (FWD / DGRAD 21.0 vs 18.9 us: the
-    // mainloop does not move -- 7.9 vs 8.2 us, so it is not L2-bound -- while the cluster
-    // launch, the prologue / exit cluster barriers and rank 0 pacing all eight CTAs add ~2 us;
-    // in the fused-head kernel 27.2 vs 25.6 us)
-    if (P.npass == 3 && !cf.pair && cf.bn == 64 && P.conv1.kclust == 0 && getenv("TEM_AMC")) {
-        if (P.conv1.ntiles <= 8 && mtiles * P.conv1.ntiles <= 148 && amc_max_clusters<FWD_>(P.conv1.ntiles) >= mtiles)
-            P.conv1.amc = 1;
-        if (P.dgrad.ntiles <= 8 && mtiles * P.dgrad.ntiles <= 148 && amc_max_clusters<DGRAD_>(P.dgrad.ntiles) >= mtiles)
-            P.dgrad.amc = 1;
-    }
     const int wc = cw.bn / 64;  // chunks per WGRAD n-tile
-    const bool wgrad_bmc = P.npass == 3 && !cw.pair && getenv("TEM_WGRAD_BMC") != nullptr;
     common(P.wgrad2);
     P.wgrad2.slot = SLOT_WGRAD2;
     P.wgrad2.side = 1;
@@ -1947,9 +1378,6 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     P.wgrad1.part_stride = (int64_t)g.C * 3 * g.Cin + g.C;
     P.wgrad1.ones_chunk = 1;
     ok &= map2d(&P.wgrad1.ones, b.ones, 128, R, brW);
-    // Experiment (TEM_WGRAD_BMC=1): WGRAD as clusters of the m-tiles sharing B, B multicast
-    for (UmmaParams* q : {&P.wgrad2, &P.wgrad1})
-        if (wgrad_bmc && q->mtiles <= 8 && q->mtiles * q->ntiles * q->nsplit <= 148) q->amc = 1;
     // epilogue store maps
     ok &= map_store2d(&P.conv1.out[0], b.h1, false, g.C, R);
     if (b.h1_lo) ok &= map_store2d(&P.conv1.out[1], b.h1_lo, false, g.C, R);
@@ -1979,38 +1407,14 @@ template <int MODE>
 static cudaError_t dispatch(const UmmaParams& p, int npass, cudaStream_t s) {
     const GemmCfg c = cfg_for(MODE, npass);
     if constexpr (MODE == WGRAD_) {
-        if (p.amc && npass == 3 && !c.pair) return launch_wgrad_bmc<128, 3, 3>(p, s);  // experiment
-        if (c.pair) return npass == 3 ? launch_wgrad<256, 3, 3, true>(p, s) : launch_wgrad<256, 1, 6, true>(p, s);
-        return npass == 3 ? launch_wgrad<128, 3, 3, false>(p, s) : launch_wgrad<256, 1, 4, false>(p, s);
+        if (c.pair) return launch_wgrad<256, 1, 6, true>(p, s);  // bf16: 2-CTA pairs
+        return launch_wgrad<128, 3, 3, false>(p, s);            // fp32 (3-pass)
     } else {
-        if (p.kclust > 0 && npass == 3) return launch_splitk<MODE, 3, 2, 2>(p, s);  // plan: fp32 only
         if constexpr (MODE == FWD_)
             if (p.fused_head) return launch_halo_head<64, 3, 2, 6>(p, s);  // plan: fp32, BN = 64
-        if (p.amc && npass == 3) return launch_halo_amc<MODE, 64, 3, 3, 6>(p, s);  // plan: fp32 single wave
-        if (c.pair && c.bn == 64) return launch_halo<MODE, 64, 3, 3, 6, true>(p, s);
-        if (c.pair)
-            return npass == 3 ? launch_halo<MODE, 128, 3, 3, 6, true>(p, s) : launch_halo<MODE, 256, 1, 4, 8, true>(p, s);
-        if (npass == 3) {
-            static const int stages = [] {  // (experiments) ring depths SA x SB, default 3 x 6
-                const char* e = getenv("TEM_HALO_STAGES");
-                return e ? atoi(e) : 36;
-            }();
-            if (stages == 28) return launch_halo<MODE, 64, 3, 2, 8, false>(p, s);
-            if (stages == 44) return launch_halo<MODE, 64, 3, 4, 4, false>(p, s);
-            return launch_halo<MODE, 64, 3, 3, 6, false>(p, s);
-        }
-        return launch_halo<MODE, 256, 1, 3, 4, false>(p, s);
+        if (c.pair) return launch_halo<MODE, 256, 1, 4, 8, true>(p, s);  // bf16: 2-CTA pairs
+        return launch_halo<MODE, 64, 3, 3, 6, false>(p, s);              // fp32 (3-pass)
     }
-}
-
-// CTAs of the side-branch update (split update): at most one 512-thread CTA per SM so that
-// conv1 wgrad's CTAs (one per SM, ~200 KB smem) still fit beside it
-static int split_ctas() {
-    static const int v = [] {
-        const char* e = getenv("TEM_SPLIT_CTAS");
-        return e ? atoi(e) : 32;
-    }();
-    return v;
 }
 
 cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, const float* labels,
@@ -2064,14 +1468,12 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
             return cudaErrorUnknown;
         return cudaSuccess;
     };
-    static const bool headred_last = getenv("TEM_HEADRED_LAST") != nullptr;  // (experiment) order on the side branch
-    if (!headred_last && (e = head_reduce()) != cudaSuccess) return e;
+    if ((e = head_reduce()) != cudaSuccess) return e;
     rec2.begin(SLOT_WGRAD2);
     e = dispatch<WGRAD_>(P.wgrad2, P.npass, aux);
     rec2.end(SLOT_WGRAD2);
     if (e != cudaSuccess) return e;
     ++n;
-    if (headred_last && (e = head_reduce()) != cudaSuccess) return e;
     if (!defer_reduce) {
     rec2.begin(SLOT_RED2);
     e = launch_pdl(umma::reduce_wgrad_kernel, dim3(296), dim3(256), 0, aux, true, (const float*)b.wpart2,
@@ -2096,21 +1498,6 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
             return cudaErrorUnknown;
         rec2.begin(SLOT_EXCH2);
         e = split->early_kind == TEM_EXCHANGE_TWOSHOT ? launch_twoshot(*split->early, aux) : launch_ring(*split->early, aux);
-        rec2.end(SLOT_EXCH2);
-        if (e != cudaSuccess) return e;
-        ++n;
-        if (!no_fork && cudaEventRecord(P.join, P.aux) != cudaSuccess) return cudaErrorUnknown;
-    } else if (split && defer_reduce) {
-        // N = 1 tem_step: the owner update of [off_W2, K_pad) (W2 with its split-K partials, b2,
-        // W3, b3, PEM) needs only conv2 wgrad / the head and runs once conv2 dgrad -- the last
-        // reader of W2 -- is done, on the side branch beside conv1 wgrad
-        if (!no_fork &&
-            (cudaEventRecord(P.dgrad_done, s) != cudaSuccess || cudaStreamWaitEvent(P.aux, P.dgrad_done, 0) != cudaSuccess))
-            return cudaErrorUnknown;
-        rec2.begin(SLOT_EXCH2);
-        e = launch_sgd_fused(b.grad, const_cast<float*>(b.params), b.shadow, b.shadow_lo, g.off_W2, g.Kpad, split->oc,
-                             split->os, nullptr, 0, 0, 1, b.wpart2, P.wgrad2.part_stride, g.off_W2,
-                             (int64_t)3 * g.C * g.C, P.S2, aux, !no_fork, split_ctas());
         rec2.end(SLOT_EXCH2);
         if (e != cudaSuccess) return e;
         ++n;
@@ -2142,30 +1529,22 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     return cudaSuccess;
 }
 
-void umma_probe_skip(int bits) {
-    if (bits >= 2000) {  // "probe_skip:2000+ns": producer backoff experiment
-        const unsigned ns = (unsigned)(bits - 2000);
-        cudaMemcpyToSymbol(umma::g_prod_sleep, &ns, sizeof(ns));
-        return;
-    }
-    if (bits >= 1000) {  // "probe_skip:1000+ns": epilogue backoff experiment
-        const unsigned ns = (unsigned)(bits - 1000);
-        cudaMemcpyToSymbol(umma::g_epi_sleep, &ns, sizeof(ns));
-        return;
-    }
-    cudaMemcpyToSymbol(umma::g_probe_skip, &bits, sizeof(int));
-}
-
 bool umma_side_branch_enabled() { return getenv("TEM_NO_FORK") == nullptr; }
 
-void trace_set_umma(unsigned long long* p) { cudaMemcpyToSymbol(g_trace, &p, sizeof(p)); }
+TEM_TRACE_SETTER(trace_set_umma)
 
 void* umma_tstamp_buffer(int64_t* nbytes, int on) {  // on: 0 off, 1 all, 100 + slot one launch
+#ifdef TEM_DIAG
     void* p = nullptr;
     if (cudaGetSymbolAddress(&p, umma::g_tstamp) != cudaSuccess) return nullptr;
     cudaMemcpyToSymbol(umma::g_tstamp_on, &on, sizeof(int));
     if (nbytes) *nbytes = sizeof(unsigned long long) * 1024 * 16;
     return p;
+#else
+    (void)on;
+    if (nbytes) *nbytes = 0;
+    return nullptr;
+#endif
 }
 
 cudaError_t launch_prep_x_split(const Geom& g, const float* x, void* hi, void* lo, cudaStream_t s) {

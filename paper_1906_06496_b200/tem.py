@@ -60,7 +60,8 @@ def lib():
     """Load the in-tree libtem.so (building it with nvcc if stale).  Raises if it cannot."""
     global _lib
     if _lib is None:
-        path = _build.build()
+        # TEM_DIAG_LIB=1 (scripts/probes only): the diagnostics build with kernel traces
+        path = _build.build(diag=os.environ.get("TEM_DIAG_LIB") == "1")
         L = ctypes.CDLL(path)
         cp = ctypes.POINTER(tem_config)
         L.tem_num_params.restype = ctypes.c_int64

@@ -31,8 +31,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--kernel", default="halo", choices=["halo", "split", "head", "wgrad1", "wgrad2", "fwd1"])
-    ap.add_argument("--skip", type=int, default=0, help="probe_skip bits (diagnostics: no A / B loads)")
     args = ap.parse_args()
+    os.environ["TEM_DIAG_LIB"] = "1"  # traces / phase stamps exist only in the diagnostics build
     import numpy as np
     import torch
     import datagen
@@ -44,8 +44,6 @@ def main():
     lab = torch.from_numpy(datagen.labels(B)).cuda()
     lib = tem.lib()
     nb = ctypes.c_int64(0)
-    if args.skip:
-        lib.tem_debug_buffer(tem._P(s.ctx), 0, f"probe_skip:{args.skip}".encode(), ctypes.byref(nb))
     for _ in range(3):
         s.step(x, lab)
     torch.cuda.synchronize()

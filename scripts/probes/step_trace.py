@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--reps", type=int, default=5)
     args = ap.parse_args()
+    os.environ["TEM_DIAG_LIB"] = "1"  # traces / phase stamps exist only in the diagnostics build
     import numpy as np
     import torch
     import datagen

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Run a few tem_step calls of a workload (for ncu / compute-sanitizer captures).
 
-    python scripts/prof_step.py [--workload c2|c3|c1|c5|c6] [--steps 3] [--path umma|simt]
+    python scripts/prof_step.py [--workload c2|c3|c1|c5|c6] [--steps 3]
 """
 import argparse
 import os
@@ -15,10 +15,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--path", default="umma")
     ap.add_argument("--ranks", type=int, default=1, help="emulated ranks on this device")
     args = ap.parse_args()
-    os.environ["TEM_KERNEL_PATH"] = args.path
     import numpy as np
     import torch
     import datagen

@@ -111,24 +111,3 @@ def test_tem_only_calls_rejected_on_pem_config(tem):
     with pytest.raises(tem.TemError):
         s.step(to_dev_x(x, 0), torch.from_numpy(lab).cuda())
     s.close()
-
-
-def test_unit_split_pem_matches_oracle(tem, orc, monkeypatch):
-    """The hidden-unit-split PEM kernels (TEM_PEM_UNITSPLIT=1, an experiment: one CTA per group of
-    4 hidden units over all proposals, no partial rows) hold the same oracle contract."""
-    monkeypatch.setenv("TEM_PEM_UNITSPLIT", "1")
-    B = 4
-    s, p = pem_session(tem, 1, B)
-    s.pem_record_decisions()
-    x, lab = make_inputs(1, B, 0)
-    f, g = pem_inputs(1, B)
-    _, pl = s.compute_pem(to_dev_x(x, 0), torch.from_numpy(lab).cuda(), torch.from_numpy(f).cuda(),
-                          torch.from_numpy(g).cuda())
-    assert s.sync()[0] == 0
-    grad = s.local_grad(0).cpu().numpy()
-    Kt = datagen.num_params()
-    pref = pem_oracle_with_gpu_decisions(orc, s, 0, f[0].reshape(B * P, F), p[Kt:], g[0].ravel())
-    for name, sl in orc.pem_param_slices(F, H).items():
-        assert rel_err(grad[Kt:Kt + datagen.pem_num_params()][sl], pref["grad"][sl]) <= TOL[0], name
-    assert abs(float(pl[0]) - pref["loss"]) <= TOL[0] * pref["loss"]
-    s.close()

@@ -59,32 +59,6 @@ def test_fp32_multi_tile_per_cta(tem, orc):
     s.close()
 
 
-def test_amc_cluster_kernels(tem, orc, monkeypatch):
-    """TEM_AMC=1: conv1 FWD and conv2 DGRAD as clusters of the 8 column tiles of a row tile with
-    the A window multicast by cluster rank 0 (an experiment; slower) -- same oracle contract."""
-    monkeypatch.setenv("TEM_AMC", "1")
-    s, p, x, lab, out = _compute(tem, 16, 0, batch_idx=5)
-    _check(orc, s, p, x, lab, out, 0)
-    s.close()
-
-
-def test_splitk_cluster_kernel(tem, orc, monkeypatch):
-    """The experimental split-K cluster FWD/DGRAD kernel (TEM_SPLITK=1) at B = 16 fp32."""
-    monkeypatch.setenv("TEM_SPLITK", "1")
-    s, p, x, lab, out = _compute(tem, 16, 0, batch_idx=2)
-    _check(orc, s, p, x, lab, out, 0)
-    s.close()
-
-
-@pytest.mark.parametrize("variant,prec", [("1", 1), ("2", 0)])
-def test_gemm_variants(tem, orc, monkeypatch, variant, prec):
-    """TEM_GEMM_VARIANT=1 (1-CTA bf16 GEMMs) and =2 (2-CTA pairs for the fp32 GEMMs), B = 4."""
-    monkeypatch.setenv("TEM_GEMM_VARIANT", variant)
-    s, p, x, lab, out = _compute(tem, 4, prec, batch_idx=4)
-    _check(orc, s, p, x, lab, out, prec)
-    s.close()
-
-
 def test_graph_and_eager_steps_identical(tem, monkeypatch):
     """tem_step replayed from a CUDA graph and launched eagerly (TEM_NO_GRAPH) run the same
     kernels: parameters after three steps are bitwise identical."""
@@ -102,26 +76,6 @@ def test_graph_and_eager_steps_identical(tem, monkeypatch):
     monkeypatch.setenv("TEM_NO_GRAPH", "1")
     w_eager = run()
     assert np.array_equal(w_graph, w_eager)
-
-
-@pytest.mark.parametrize("optimizer", [0, 1])
-def test_split_update_identical(tem, monkeypatch, optimizer):
-    """TEM_SPLIT_UPDATE=1 (the W2.. range of the N = 1 update on the side branch beside conv1
-    wgrad, the rest after it) runs the same per-element arithmetic: parameters after three
-    steps are bitwise identical to the single update kernel's, for SGD and Adam."""
-    def run():
-        s, _ = session(tem, 1, 8, 0, lr=0.05 if optimizer == 0 else 1e-3, optimizer=optimizer)
-        x, lab = make_inputs(1, 8, 0, batch_idx=8)
-        xd, ld = to_dev_x(x, 0), torch.from_numpy(lab).cuda()
-        for _ in range(3):
-            s.step(xd, ld)
-        assert s.sync()[0] == 0
-        w = s.params(0).cpu().numpy().copy()
-        s.close()
-        return w
-    w_plain = run()
-    monkeypatch.setenv("TEM_SPLIT_UPDATE", "1")
-    assert np.array_equal(run(), w_plain)
 
 
 def test_step_host_matches_device_step(tem):
@@ -211,12 +165,3 @@ def test_step_pem_host_matches_device_step(tem):
     assert np.array_equal(s2.params(0).cpu().numpy(), w1)
     assert datagen.PEM_P > 0
     s2.close()
-
-
-def test_wgrad_bmc_cluster_kernel(tem, orc, monkeypatch):
-    """TEM_WGRAD_BMC=1: both WGRADs as clusters of the 4 m-tiles of an (n-tile, split) with the B
-    tile multicast by cluster rank 0 (an experiment) -- same oracle contract."""
-    monkeypatch.setenv("TEM_WGRAD_BMC", "1")
-    s, p, x, lab, out = _compute(tem, 16, 0, batch_idx=6)
-    _check(orc, s, p, x, lab, out, 0)
-    s.close()
