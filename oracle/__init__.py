@@ -69,7 +69,7 @@ def lib():
             L.orc_tem_fwd_bwd.argtypes = [i32, i32, i32, i32, i32, i32, P, P, P, P, P, P, P]
             L.orc_tem_fwd_bwd_ex.restype = i32
             L.orc_tem_fwd_bwd_ex.argtypes = [i32, i32, i32, i32, i32, i32, P, P, P, P, P, P, P,
-                                             P, i64, ctypes.c_double, P, i64, P, P]
+                                             P, i64, ctypes.c_double, ctypes.c_double, P, i64, P, P]
             L.orc_ring_adam_f32.restype = i32
             L.orc_ring_adam_f32.argtypes = [P, P, P, P, P, i32, i64, f32, f32, f32, f32]
             L.orc_ring_momentum_f32.restype = i32
@@ -173,14 +173,19 @@ def num_params(Cin: int = 400, C: int = 512, Co: int = 3) -> int:
 
 
 def tem_fwd_bwd(x, params, labels, lam=(1.0, 1.0, 1.0), prec: int = 0, C: int = 512,
-                flips=(), kink_tau: float = 0.0, kinks_cap: int = 4096):
+                flips=(), kink_tau=0.0, kinks_cap: int = 4096, threads: int = 1):
     """BSN-TEM forward + weighted logistic loss + backward.
 
     x [B][T][Cin], params flat (fp32 values, any float dtype), labels [B][Co][T].
     prec 0 = fp64, 1 = bf16-operand emulation (reading R8).
     flips: indices layer*(B*T*C) + (b*T+t)*C + c of ReLU decisions to invert (reading R7b).
-    kink_tau > 0: also report pre-activations with |a| <= kink_tau * sum|terms|.
+    kink_tau > 0: also report pre-activations with |a| <= kink_tau * sum|terms|; a pair
+    (tau_a1, tau_a2) gives each layer its own band (reading R7b).
+    threads > 1: the videos are split into contiguous sub-batches computed concurrently (the
+    C call releases the GIL) and merged in sub-batch order -- see _tem_fwd_bwd_split.
     Returns dict(loss [1+Co] f64, z [B][T][Co] f64, grad [K] f64, kinks [n] int64)."""
+    if threads > 1 and np.shape(x)[0] > 1:
+        return _tem_fwd_bwd_split(x, params, labels, lam, prec, C, flips, kink_tau, kinks_cap, threads)
     x = np.ascontiguousarray(x, dtype=np.float64)
     B, T, Cin = x.shape
     labels = np.ascontiguousarray(labels, dtype=np.float64)
@@ -193,18 +198,62 @@ def tem_fwd_bwd(x, params, labels, lam=(1.0, 1.0, 1.0), prec: int = 0, C: int = 
     z = np.zeros((B, T, Co))
     grad = np.zeros(K)
     fl = np.ascontiguousarray(np.sort(np.asarray(flips, dtype=np.int64)))
+    tau1, tau2 = (kink_tau, kink_tau) if np.isscalar(kink_tau) else tuple(kink_tau)
     kinks = np.zeros(max(kinks_cap, 1), dtype=np.int64)
     nk = np.zeros(1, dtype=np.int64)
     dec = np.zeros(2 * B * T * C, dtype=np.uint8)
     rc = lib().orc_tem_fwd_bwd_ex(prec, B, T, Cin, C, Co, _ptr(x), _ptr(p), _ptr(labels), _ptr(lam),
                                   _ptr(loss), _ptr(z), _ptr(grad), _ptr(fl) if fl.size else None,
-                                  int(fl.size), float(kink_tau), _ptr(kinks), int(kinks_cap), _ptr(nk),
+                                  int(fl.size), float(tau1), float(tau2), _ptr(kinks), int(kinks_cap), _ptr(nk),
                                   _ptr(dec))
     if rc:
         raise ValueError("invalid TEM arguments")
     n = int(nk[0])
     return {"loss": loss, "z": z, "grad": grad, "kinks": kinks[:min(n, kinks_cap)].copy(), "nkinks": n,
             "decisions": dec}
+
+
+def _tem_fwd_bwd_split(x, params, labels, lam, prec, C, flips, kink_tau, kinks_cap, threads):
+    """tem_fwd_bwd over contiguous sub-batches in parallel.  The loss is a per-video mean
+    (L = (1/B) sum_v L_v, reading R6), so a sub-batch of b videos returns (1/b) sum over its
+    videos and the whole batch is sum_c (b_c / B) * result_c, merged in sub-batch order (fp64:
+    differs from the one-call result only by summation order).  ReLU-decision indices
+    layer*(B*T*C) + (b*T+t)*C + c are translated between the batch and each sub-batch.
+    prec = 1 rounds dA2 / dA1 to bf16 AFTER the 1/B factor of dz: the sub-batches are then
+    equal with B/b a power of two, so the rescaling b/B is exact and commutes with rounding."""
+    from concurrent.futures import ThreadPoolExecutor
+    B, T, _ = np.shape(x)
+    n = min(threads, B)
+    if prec == 1:
+        n = 1
+        while 2 * n <= min(threads, B) and B % (2 * n) == 0:
+            n *= 2
+        if n == 1:
+            return tem_fwd_bwd(x, params, labels, lam, prec, C, flips, kink_tau, kinks_cap)
+    cuts = [B * i // n for i in range(n + 1)]
+    BTC, fl = B * T * C, np.sort(np.asarray(flips, dtype=np.int64))
+    layer, within = fl // BTC, fl % BTC
+
+    def part(i):
+        b0, b1 = cuts[i], cuts[i + 1]
+        lo, hi = b0 * T * C, b1 * T * C
+        m = (within >= lo) & (within < hi)
+        sub = layer[m] * ((b1 - b0) * T * C) + (within[m] - lo)
+        return tem_fwd_bwd(x[b0:b1], params, labels[b0:b1], lam, prec, C, sub, kink_tau, kinks_cap)
+    with ThreadPoolExecutor(n) as ex:
+        parts = list(ex.map(part, range(n)))
+    loss = sum(((cuts[i + 1] - cuts[i]) / B) * parts[i]["loss"] for i in range(n))
+    grad = sum(((cuts[i + 1] - cuts[i]) / B) * parts[i]["grad"] for i in range(n))
+    z = np.concatenate([q["z"] for q in parts])
+    dec = np.concatenate([q["decisions"].reshape(2, -1) for q in parts], axis=1).ravel()
+    kinks, nk = [], 0
+    for i, q in enumerate(parts):
+        bsz = (cuts[i + 1] - cuts[i]) * T * C
+        k = q["kinks"]
+        kinks.append((k // bsz) * BTC + cuts[i] * T * C + k % bsz)
+        nk += q["nkinks"]
+    kinks = np.sort(np.concatenate(kinks)) if kinks else np.zeros(0, np.int64)
+    return {"loss": loss, "z": z, "grad": grad, "kinks": kinks[:kinks_cap], "nkinks": nk, "decisions": dec}
 
 
 def ring_adam(grads, params, m, v, scal, lr, beta1=0.9, beta2=0.999, eps=1e-8):

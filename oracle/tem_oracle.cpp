@@ -312,15 +312,16 @@ static double softplus(double u) { return u > 0 ? u + std::log1p(std::exp(-u)) :
 // ReLU decisions (reading R7b).  The ReLU mask 1[a > 0] is a decision taken by
 // floating point: when |a| is within the rounding error of the accumulation, fp32
 // and fp64 may legitimately disagree.  The extended entry point therefore
-//   * reports every pre-activation with |a| <= kink_tau * S, S = |bias| + sum |w x|
-//     (the magnitude the rounding error scales with), as index
+//   * reports every pre-activation with |a| <= tau * S, S = |bias| + sum |w x|
+//     (the magnitude the rounding error scales with; tau = kink_tau for a1, kink_tau2
+//     for a2: the layers' rounding bands differ on the bf16 path), as index
 //     layer*(B*T*C) + (b*T + t)*C + c  (layer 0 = a1, 1 = a2), and
 //   * accepts a sorted list `flips` of such indices whose decision is inverted.
 // With no flips it is exactly the plain definition.
 int orc_tem_fwd_bwd_ex(int prec, int B, int T, int Cin, int C, int Co,
                        const double* x, const double* params, const double* labels,
                        const double* lambda, double* loss_out, double* z_out, double* grad_out,
-                       const int64_t* flips, int64_t nflips, double kink_tau,
+                       const int64_t* flips, int64_t nflips, double kink_tau, double kink_tau2,
                        int64_t* kinks_out, int64_t kinks_cap, int64_t* nkinks,
                        uint8_t* decisions_out) {
     if (B < 0 || T < 1 || Cin < 1 || C < 1 || Co < 1 || (prec != 0 && prec != 1)) return 1;
@@ -330,7 +331,8 @@ int orc_tem_fwd_bwd_ex(int prec, int B, int T, int Cin, int C, int Co,
         return nflips > 0 && std::binary_search(flips, flips + nflips, idx);
     };
     auto note_kink = [&](int64_t idx, double a, double S) {
-        if (kink_tau > 0 && std::fabs(a) <= kink_tau * S && nkinks) {
+        const double tau = idx < layer_stride ? kink_tau : kink_tau2;
+        if (tau > 0 && std::fabs(a) <= tau * S && nkinks) {
             if (*nkinks < kinks_cap && kinks_out) kinks_out[*nkinks] = idx;
             ++*nkinks;
         }
@@ -504,7 +506,7 @@ int orc_tem_fwd_bwd(int prec, int B, int T, int Cin, int C, int Co,
                     const double* x, const double* params, const double* labels,
                     const double* lambda, double* loss_out, double* z_out, double* grad_out) {
     return orc_tem_fwd_bwd_ex(prec, B, T, Cin, C, Co, x, params, labels, lambda, loss_out, z_out,
-                              grad_out, nullptr, 0, 0.0, nullptr, 0, nullptr, nullptr);
+                              grad_out, nullptr, 0, 0.0, 0.0, nullptr, 0, nullptr, nullptr);
 }
 
 // ============================================================================ PEM

@@ -589,7 +589,7 @@ static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, f
         // compute (not with PGM-fed PEM, whose gradient is produced after it)
         RingParams early;
         c->early_done = false;
-        if (bucketed(c) && fuse_reduce && g.B > 0 && g.pgm_G == 0) {
+        if (bucketed(c) && c->nlocal == 1 && fuse_reduce && g.B > 0 && g.pgm_G == 0) {
             early = step_ring(c, bucket_bound(c), g.Kpad);
             su.early = &early;
             su.early_kind = c->cfg.exchange;

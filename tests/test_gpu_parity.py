@@ -5,6 +5,8 @@ Tolerances (BASELINE.json north_star): ring allreduce bit-exact; TEM relative 1e
 max|gpu - oracle| <= tol * max|oracle| against the fp64 oracle (bf16-emulated for
 the bf16 path) -- DESIGN.md section 6.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -14,23 +16,36 @@ import datagen
 pytestmark = pytest.mark.gpu
 
 TOL = {0: 1e-4, 1: 2e-2}
-# ReLU decisions within this fraction of sum|terms| of zero are ambiguous under the kernel's
-# rounding (fp32 accumulation: gamma_K ~ K*u <= 2^-13 for K <= 1536; bf16 operands: one
-# bf16 ulp of an input, 2^-8) -- reading R7b.
-KINK_TAU = {0: 2.0 ** -13, 1: 2.0 ** -8}
+# ReLU decisions within tau * sum|terms| of zero are ambiguous under the kernel's rounding
+# (reading R7b), per layer (a1, a2):
+#  * fp32 path: bf16x3 products (~2^-16 each, R16) + fp32 accumulation gamma_K ~ K*u with
+#    K <= 1536 terms: below 2^-13 on both layers;
+#  * bf16 path, a1: both sides multiply the SAME rounded operands (x, W1), so only fp32-vs-fp64
+#    accumulation differs: 2^-13 as above;
+#  * bf16 path, a2: the operand h1 is itself a rounding of a1, and the GPU rounds its fp32 a1
+#    while the oracle rounds its fp64 a1, so an h1 element can land one bf16 ulp (2^-8
+#    relative) apart: 2^-8.
+KINK_TAU = {0: (2.0 ** -13, 2.0 ** -13), 1: (2.0 ** -13, 2.0 ** -8)}
+# at most this fraction of all ReLU decisions may be flipped into the oracle (R7b)
+MAX_FLIP_FRAC = 1e-4
 
 
-def oracle_with_gpu_decisions(orc, s, l, x, p, lab, lam, prec):
+def oracle_with_gpu_decisions(orc, s, l, x, p, lab, lam, prec, threads=1, gdec=None):
     """fp64 oracle whose ReLU decisions agree with the GPU's wherever the decision is
-    ambiguous; any GPU decision that differs OUTSIDE the oracle's ambiguity band fails."""
-    ref = orc.tem_fwd_bwd(x, p, lab, lam, prec=prec, kink_tau=KINK_TAU[prec], kinks_cap=1 << 23)
-    gdec = s.relu_decisions(l).cpu().numpy()
+    ambiguous; any GPU decision that differs OUTSIDE the oracle's ambiguity band fails, and
+    so does a flip count above MAX_FLIP_FRAC of all decisions."""
+    ref = orc.tem_fwd_bwd(x, p, lab, lam, prec=prec, kink_tau=KINK_TAU[prec], kinks_cap=1 << 24,
+                          threads=threads)
+    if gdec is None:
+        gdec = s.relu_decisions(l).cpu().numpy()
     diff = np.nonzero(gdec != ref["decisions"])[0]
+    print(f"R7b: {diff.size} flipped ReLU decisions of {gdec.size} ({ref['nkinks']} in the band)")
     if diff.size == 0:
         return ref
-    assert ref["nkinks"] <= (1 << 23)
+    assert diff.size <= MAX_FLIP_FRAC * gdec.size, (diff.size, gdec.size)
+    assert ref["nkinks"] <= (1 << 24)
     assert np.all(np.isin(diff, ref["kinks"])), "GPU ReLU decision differs outside the ambiguity band"
-    return orc.tem_fwd_bwd(x, p, lab, lam, prec=prec, flips=diff)
+    return orc.tem_fwd_bwd(x, p, lab, lam, prec=prec, flips=diff, threads=threads)
 
 
 def need_gpu():
@@ -234,36 +249,45 @@ def test_full_size_c2_fp32(tem, orc):
     s.close()
 
 
-def test_full_size_c3_bf16_sampled(tem, orc):
-    """configs[2] shape (B = 256 per GPU, bf16 operands) in the launch configuration the
-    bench times: logits checked on sampled videos against the bf16-emulated oracle, and the
-    gradient checked via the property grad(B) = mean of grad(sub-batches) (per-video loss
-    normalisation), the sub-batches checked against the oracle."""
-    B, lam = 256, (1.0, 1.0, 1.0)
+def test_full_size_c3_bf16(tem, orc):
+    """configs[2] (B = 256 per GPU, bf16 operands / fp32 accumulate) in the launch
+    configuration the bench times: the loss, every logit and every gradient tensor against
+    the bf16-emulated fp64 oracle over all 256 videos (threaded over videos)."""
+    B, lam = 256, (2.0, 1.0, 1.0)
     s, p = session(tem, 1, B, 1, lr=0.01, lam=lam)
     x, lab = make_inputs(1, B, 1, batch_idx=2)
     loss = s.compute(to_dev_x(x, 1), torch.from_numpy(lab).cuda())
     assert s.sync()[0] == 0
-    z = s.logits(0).cpu().numpy()
-    gfull = s.local_grad(0).cpu().numpy()[:s.K].astype(np.float64)
-    for v in (0, 77, 255):
-        ref = orc.tem_fwd_bwd(x[0, v:v + 1], p, lab[0, v:v + 1], lam, prec=1)
-        assert rel_err(z[v:v + 1], ref["z"]) <= TOL[1]
+    ref = oracle_with_gpu_decisions(orc, s, 0, x[0], p, lab[0], lam, 1, threads=os.cpu_count() or 1)
+    check_tensors(orc, s.local_grad(0).cpu().numpy()[:s.K], s.logits(0).cpu().numpy(),
+                  loss[0].cpu().numpy(), ref, TOL[1])
     s.close()
-    sub = 32
-    s2, _ = session(tem, 1, sub, 1, lr=0.01, lam=lam)
-    acc = np.zeros_like(gfull)
-    for k in range(B // sub):
-        xs, ls = x[:, k * sub:(k + 1) * sub], lab[:, k * sub:(k + 1) * sub]
-        s2.compute(to_dev_x(np.ascontiguousarray(xs), 1), torch.from_numpy(np.ascontiguousarray(ls)).cuda())
-        assert s2.sync()[0] == 0
-        acc += s2.local_grad(0).cpu().numpy()[:s2.K]
-        if k == 0:
-            ref = oracle_with_gpu_decisions(orc, s2, 0, xs[0], p, ls[0], lam, 1)
-            assert rel_err(s2.local_grad(0).cpu().numpy()[:s2.K], ref["grad"]) <= TOL[1]
-    acc /= B // sub
-    assert rel_err(gfull, acc) <= 1e-4
-    s2.close()
+
+
+def test_bench_call_c2_step(tem, orc):
+    """The exact call bench.py times at N = 1: configs[1] (B = 16, fp32) through tem_step,
+    graph-captured on the first call and replayed on the second, SGD with the split-K sums
+    folded into the update.  Per step: every gradient tensor, the logits and the loss against
+    the fp64 oracle at that step's weights, and the new weights bitwise equal to the oracle's
+    w - lr * g (fma) on the GPU's own gradient."""
+    B, lam, lr = 16, (1.0, 1.0, 1.0), 0.01
+    s, p = session(tem, 1, B, 0, lr=lr, lam=lam)
+    assert s.kernel_path() == "tcgen05-bf16x3-fp32"
+    xd = torch.empty(1, B, 100, 400, device="cuda")
+    ld = torch.empty(1, B, 3, 100, device="cuda")
+    for it in range(2):  # same device buffers: step 2 replays the graph step 1 captured
+        x, lab = make_inputs(1, B, 0, batch_idx=it)
+        xd.copy_(torch.from_numpy(x))
+        ld.copy_(torch.from_numpy(lab))
+        w0 = s.params(0).cpu().numpy().copy()
+        loss = s.step(xd, ld)
+        assert s.sync()[0] == 0
+        g = s.local_grad(0).cpu().numpy().copy()
+        ref = oracle_with_gpu_decisions(orc, s, 0, x[0], w0, lab[0], lam, 0, threads=os.cpu_count() or 1)
+        check_tensors(orc, g[:s.K], s.logits(0).cpu().numpy(), loss[0].cpu().numpy(), ref, TOL[0])
+        assert np.array_equal(s.params(0).cpu().numpy(), orc.ring_sgd(g[None, :], w0, lr)[0]), it
+    assert s.launches_per_step() > 0
+    s.close()
 
 
 def test_empty_batch_and_lr_zero(tem, orc):

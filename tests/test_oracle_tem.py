@@ -246,3 +246,44 @@ def test_empty_batch(orc):
     _, p, _ = tiny()
     r = orc.tem_fwd_bwd(x, p, np.zeros((0, 3, 5), np.float32), prec=0, C=6)
     assert np.all(r["grad"] == 0) and np.all(r["loss"] == 0)
+
+
+def test_threaded_split_equals_one_call(orc):
+    """tem_fwd_bwd(threads=n) merges per-sub-batch calls: same decisions, kinks and flips
+    as one call, values equal up to fp64 summation order."""
+    Cin, C, Co = 4, 6, 3
+    for prec, B, ns in ((0, 7, (2, 3, 7)), (1, 8, (2, 3, 4, 8))):
+        _split_case(orc, prec, B, ns)
+
+
+def _split_case(orc, prec, B, ns):
+    Cin, C, Co = 4, 6, 3
+    x, p, lab = tiny(B=B, T=9, seed=11)
+    lam = (2.0, 1.0, 0.5)
+    one = orc.tem_fwd_bwd(x, p, lab, lam, prec=prec, C=C, kink_tau=(0.05, 0.2), kinks_cap=10 ** 5)
+    assert one["nkinks"] > 0
+    rng = np.random.default_rng(1)
+    flips = np.sort(rng.choice(2 * B * 9 * C, 9, replace=False))
+    one_f = orc.tem_fwd_bwd(x, p, lab, lam, prec=prec, C=C, flips=flips)
+    for n in ns:
+        par = orc.tem_fwd_bwd(x, p, lab, lam, prec=prec, C=C, kink_tau=(0.05, 0.2), kinks_cap=10 ** 5, threads=n)
+        assert np.array_equal(par["decisions"], one["decisions"])
+        assert np.array_equal(par["kinks"], np.sort(one["kinks"])) and par["nkinks"] == one["nkinks"]
+        assert np.array_equal(par["z"], one["z"])
+        assert np.allclose(par["loss"], one["loss"], rtol=1e-14, atol=0)
+        assert np.abs(par["grad"] - one["grad"]).max() <= 1e-14 * np.abs(one["grad"]).max()
+        par_f = orc.tem_fwd_bwd(x, p, lab, lam, prec=prec, C=C, flips=flips, threads=n)
+        assert np.array_equal(par_f["decisions"], one_f["decisions"])
+        assert np.abs(par_f["grad"] - one_f["grad"]).max() <= 1e-14 * np.abs(one_f["grad"]).max()
+
+
+def test_layer_bands_are_separate(orc):
+    """kink_tau=(t1, t2): a1 indices reported with band t1, a2 indices with band t2."""
+    Cin, C, Co = 4, 6, 3
+    B, T = 2, 5
+    x, p, lab = tiny(B=B, T=T, seed=3)
+    n = B * T * C
+    only1 = orc.tem_fwd_bwd(x, p, lab, prec=0, C=C, kink_tau=(1.0, 0.0), kinks_cap=10 ** 5)
+    only2 = orc.tem_fwd_bwd(x, p, lab, prec=0, C=C, kink_tau=(0.0, 1.0), kinks_cap=10 ** 5)
+    assert only1["nkinks"] == n and np.all(only1["kinks"] < n)
+    assert only2["nkinks"] == n and np.all(only2["kinks"] >= n)
