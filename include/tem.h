@@ -41,8 +41,11 @@ extern "C" {
 typedef enum {
     TEM_OK = 0,
     TEM_ERR_INVALID_ARG = 1, /* bad dims, N <= 0, pointer outside the symmetric heap   */
-    TEM_ERR_PROTOCOL = 2,    /* ranks disagree on K; detected via the ring's flags    */
-    TEM_ERR_TRANSPORT = 3,   /* a peer flag did not arrive within the spin bound     */
+    TEM_ERR_PROTOCOL = 2,    /* ranks disagree on the collective (K, kind, op): every
+                                rank reads all N ranks' headers before any data moves, so all
+                                ranks latch it and none writes a result                      */
+    TEM_ERR_TRANSPORT = 3,   /* a peer header / message did not arrive within spin_timeout_ms
+                                                                                      */
     TEM_ERR_CUDA = 4,        /* a CUDA launch / API call failed                               */
     TEM_ERR_NONFINITE = 5,   /* non-finite loss; tem_sync reports the step index      */
     TEM_ERR_STATE = 6        /* call on a shut-down or NULL context                           */
@@ -83,9 +86,11 @@ typedef struct {
     /* --- workspace                                                                         */
     void* workspace;        /* device, 256-byte aligned, >= tem_workspace_bytes(cfg)          */
     size_t workspace_bytes;
-    /* --- ring tuning (0 = automatic)                                                       */
-    int32_t ring_channels;  /* G: CTAs per rank in the ring kernel                           */
-    int32_t ring_chunks;    /* C: pipelined sub-chunks per channel per block                 */
+    /* --- collective tuning (0 = automatic)                                                 */
+    int32_t ring_channels;  /* G: CTAs per rank of every collective kernel (default 16; the
+                               emulation caps it at SMs / local_ranks); equal on every rank  */
+    int32_t spin_timeout_ms; /* bound on any wait for a peer (0 -> 20000 ms); past it the
+                               collective latches TEM_ERR_TRANSPORT                           */
     /* --- gradient exchange of tem_step / tem_exchange                                      */
     int32_t exchange;       /* TEM_EXCHANGE_RING (the paper's ring; default) or
                                TEM_EXCHANGE_PS (the parameter-server comparator, P:115-124:
@@ -142,8 +147,26 @@ size_t tem_workspace_bytes(const tem_config* cfg);
 /* Per-rank symmetric heap layout (offsets are identical on every rank):
  *   [0, 4*K_pad)                 params (fp32 master weights)
  *   [off_user, off_user + 4*max) user region for ring_allreduce buffers
- *   then the ring staging area and the flag area (library-private).
- * The caller zero-fills the whole heap once before tem_init on every rank. */
+ *   then library-private areas: two-shot staging, PS slots, the handshake headers, the
+ *   two-shot / PS phase flags and the ring's LL slots.
+ * The caller zero-fills the whole heap once before tem_init on every rank.
+ *
+ * Wire protocol between ranks (what one rank stores into a peer's heap):
+ *   handshake  before any data moves, channel g of rank s stores the 16-byte header
+ *              {K mod 2^32, epoch, (K >> 32) | kind << 8 | op << 16 | mode << 24, epoch}
+ *              (kind 0 ring, 1 two-shot, 2 PS; mode 1 = tem_step exchange) into header slot
+ *              (epoch & 1, s, g) of every rank, and every rank compares all N headers of channel g:
+ *              any difference -> PROTOCOL on every rank, nothing written.
+ *   ring       LL lines of 16 bytes {d0, epoch, d1, epoch} (each 8-byte half written
+ *              atomically): float4 position v of a block message travels as lines 2v, 2v+1
+ *              of slot (epoch & 1, phase, round) -- scatter phase 0 rounds 0..N-2, gather
+ *              phase 1 rounds 0..N-2; slot stride tem_ll_slot_lines(cfg) lines -- in the
+ *              receiver's LL area at tem_sym_ll_offset(cfg).  Header slot [s][g] lies at
+ *              tem_sym_hdr_offset(cfg) + 16 * (((epoch & 1) * 8 + s) * 128 + g).  `epoch`
+ *              counts the collectives of the context from 1, identical on every rank. */
+size_t tem_sym_hdr_offset(const tem_config* cfg);
+size_t tem_sym_ll_offset(const tem_config* cfg);
+int64_t tem_ll_slot_lines(const tem_config* cfg);
 size_t tem_sym_bytes(const tem_config* cfg);
 size_t tem_sym_user_offset(const tem_config* cfg);
 

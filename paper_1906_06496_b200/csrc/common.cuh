@@ -44,6 +44,21 @@ TEM_DEV uint64_t ld_acquire_sys(const uint64_t* p) {
 TEM_DEV void st_release_sys(uint64_t* p, uint64_t v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// LL ("low latency") lines: 16 bytes {d0, flag, d1, flag}.  Each 8-byte half {datum, flag} is
+// written by one 8-byte-atomic half of a volatile 16-byte store, so a reader that sees both
+// flags equal to the expected epoch also sees both data words -- no fence, no barrier.
+TEM_DEV uint4 ld_volatile4(const uint4* p) {
+    uint4 v;
+    asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+TEM_DEV void st_volatile4(uint4* p, uint4 v) {
+    asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
 TEM_DEV uint64_t globaltimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

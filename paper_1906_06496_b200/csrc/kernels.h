@@ -242,13 +242,15 @@ cudaError_t launch_pgm(int B, int T, int G, int P, const float* prob, const floa
                        float* feat, float* iou, int32_t* ts, int32_t* te, int32_t* count, cudaStream_t s,
                        const float* z = nullptr, float* prob_out = nullptr);
 constexpr int kMaxChannels = 128;
-constexpr int kMaxChunks = 16;
 struct RingParams {
     RingLocal loc[TEM_MAX_RANKS];
-    int N, rank_base, nlocal, G, C, op, mode;  // mode 0 = allreduce, 1 = optimizer step
+    int N, rank_base, nlocal, G, op, mode;  // mode 0 = allreduce, 1 = optimizer step
     int64_t K, Kpad;
     OptCfg oc;
     int64_t off_dst, off_stage, off_flags;
+    int64_t off_hdr;    // handshake headers [TEM_MAX_RANKS][kMaxChannels] x 16 B (every kernel)
+    int64_t off_ll;     // ring: LL slots [2 phases][N-1 rounds][ll_stride lines] x 16 B
+    int64_t ll_stride;  // lines per LL slot (2 per float4 of the largest block)
     int64_t off_src;  // two-shot: heap offset of the source when it already lives in the heap
                       // (off_stage < 0), i.e. ring_allreduce's user region
     Status* status;
@@ -274,7 +276,7 @@ struct PsParams {
     int N, rank_base, nlocal, G, op, mode;  // mode 0 = allreduce, 1 = optimizer step (server)
     OptCfg oc;
     int64_t K;
-    int64_t off_dst, off_slots, off_flags;
+    int64_t off_dst, off_slots, off_flags, off_hdr;
     Status* status;
     uint64_t spin_ns;
 };

@@ -1,31 +1,40 @@
 // ring.cu -- KR1: the paper's ring allreduce over NVLink peer memory,
-// with the 1/N mean and the SGD update fused into the block owner (SURVEY 8(a)
-// rows a9-a12), plus the parameter-server comparator KP1.
+// with the 1/N mean and the optimizer update fused into the block owner (SURVEY 8(a)
+// rows a9-a12), plus the NVSwitch two-shot variant and the parameter-server comparator KP1
+// (P:115-124).
 //
-// Protocol (one launch per rank per collective; grid = G channels x local ranks):
-//   * The gradient of K_pad elements is split into N equal blocks (row a9); each
-//     block into G*C pieces; channel g (a CTA) owns pieces g*C .. g*C+C-1 of every
-//     block, so the chain order of every element is independent of G and C.
-//   * Scatter round i = 0..N-2: rank n sends block s = (n-i) mod N.  The
-//     message is own[s] (+ the partial received from the left in round i-1), pushed
-//     with 128-bit stores straight into the right neighbour's staging slot i; then a
-//     release flag.  So block b is summed along g_b + g_{b+1} + ... + g_{b+N-1}
-//     (SURVEY 8(c) c.1), bit-identical to the oracle's round-by-round replay.
-//   * After round N-2, rank n owns block (n+1) mod N: it adds the last
-//     partial, applies mean (s * fl(1/N)) and, in SGD mode, w = fma(-lr, gbar, w),
-//     then pushes the RESULT into the right neighbour's destination buffer (gather
-//     round 0, fused).
-//   * Gather round k = 1..N-2 (reading R10): forward the block received in
-//     round k-1 (send (n+1-k) mod N) -- replace, never add.
-//   * Flags are 64-bit words [epoch:32 | K tag:31 | 0] in the receiver's heap, one per
-//     (phase, round, channel, chunk).  Epochs are per-channel counters that advance by
-//     one per collective on every rank, so no flag is ever reset.  A flag whose K tag
-//     differs from the receiver's K latches PROTOCOL (every rank sees a mismatch in the
-//     first round because K_pad and thus the tag differ).  A spin longer than spin_ns
-//     latches TRANSPORT and abandons the collective.
-// The same device code serves production (one process per GPU, peers over NVLink)
-// and the single-device emulation used by the tests (N ranks = N CTA groups of one
-// cooperative launch, "peer" heaps on the same device).
+// Handshake (every collective kernel): before any data moves, channel g of rank n
+// writes a 16-byte header {K_lo, epoch, K_hi | kind | op | mode, epoch} into slot [n][g] of
+// EVERY rank's heap, then reads the N headers [0..N-1][g] of its own heap.  Every rank
+// therefore compares the same N descriptors: if any differs, all ranks latch PROTOCOL and
+// abort before the first data store; a header that does not arrive within spin_ns latches
+// TRANSPORT.
+//
+// Ring protocol (one launch per rank per collective; grid = G channels x local ranks):
+//   * The gradient of K_pad elements is split into N equal blocks (row a9).  Inside a block,
+//     float4 position v belongs to channel (v / THREADS) mod G -- interleaved, so the chain
+//     order of every element (fixed by its block alone) is independent of G.
+//   * Messages travel as LL lines (common.cuh): each float4 becomes two 16-byte lines
+//     {d0, epoch, d1, epoch}, stored into the right neighbour's LL slot (phase, round).  The
+//     receiving thread polls its own lines until both flags carry this collective's epoch: no
+//     block barrier, no fence, and the hand-off is per thread, so round i+1 at rank n+1 starts
+//     on the first positions while rank n still sends the rest of round i.
+//   * Scatter round i = 0..N-2: rank n sends block s = (n-i) mod N: own[s] plus the
+//     partial received in round i-1.  So block b is summed along g_b + g_{b+1} + ... +
+//     g_{b+N-1}, bit-identical to the oracle's round-by-round replay.
+//   * Owner: after round N-2 rank n owns block (n+1) mod N: last add, mean
+//     s * fl(1/N), optimizer update (mode 1), bf16 operand copies; the result is gather
+//     round 0's message.
+//   * Gather round k = 1..N-2 (reading R10): store the block received in round k-1
+//     and forward it (send (n+1-k) mod N) -- replace, never add; then store the last one.
+//   * Epochs: per-channel counters in the workspace, advanced by one per collective on every
+//     rank (G is fixed per context, so all channels advance together); LL slots have a fixed
+//     stride (sized for the largest collective) and alternate between two halves by epoch
+//     parity, so a line of collective t+1 never lands on an unread line of collective t
+//     (DESIGN.md 6.6).
+// The same device code serves production (one process per GPU, peers over NVLink) and the
+// single-device emulation used by the tests (N ranks = N CTA groups of one cooperative
+// launch, "peer" heaps on the same device).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <algorithm>
@@ -36,51 +45,89 @@ namespace tem {
 namespace {
 
 constexpr int RING_THREADS = 512;
+constexpr int RING_UNROLL = 4;  // float4 positions in flight per thread
 
 TEM_DEV int modn(int a, int n) {
     const int r = a % n;
     return r < 0 ? r + n : r;
 }
 
-struct Piece {
-    int64_t v0, v1;  // vector (float4) range inside a block
-};
-TEM_DEV Piece piece_of(int64_t nvec, int G, int C, int g, int c) {
-    const int64_t q = (int64_t)g * C + c, GC = (int64_t)G * C;
-    return {q * nvec / GC, (q + 1) * nvec / GC};
-}
+TEM_DEV uint64_t flag_value(uint32_t epoch) { return (uint64_t)epoch << 32; }
 
-TEM_DEV uint64_t flag_value(uint32_t epoch, int64_t K) {
-    return ((uint64_t)epoch << 32) | (uint64_t)((uint32_t)K & 0x7FFFFFFFu);
-}
-
-// Thread 0 waits for `flag` to reach `epoch`; returns false (CTA-uniform) on timeout.
-TEM_DEV bool wait_flag(const uint64_t* flag, uint32_t epoch, int64_t K, Status* st,
-                       uint64_t spin_ns, int* s_abort) {
-    if (threadIdx.x == 0) {
-        uint64_t v = ld_acquire_sys(flag);
-        if ((uint32_t)(v >> 32) < epoch) {
-            const uint64_t t0 = globaltimer();
-            do {
-                __nanosleep(64);
-                v = ld_acquire_sys(flag);
-                if ((uint32_t)(v >> 32) >= epoch) break;
-                if (globaltimer() - t0 > spin_ns) {
-                    latch(st, TEM_ERR_TRANSPORT, -1);
-                    *s_abort = 1;
-                    break;
-                }
-            } while (true);
+// Bounded spin: after `kSpinCheck` polls, checks the wall clock (and the CTA's abort word) every
+// kSpinCheck polls; past spin_ns it latches TRANSPORT and tells the CTA to abort.
+constexpr int kSpinCheck = 64;
+struct Spin {
+    uint64_t t0 = 0;
+    int n = 0;
+    // true: keep polling; false: give up (timed out, or another thread of the CTA did)
+    TEM_DEV bool again(Status* st, uint64_t spin_ns, volatile int* s_abort) {
+        if (++n < kSpinCheck) return true;
+        n = 0;
+        if (*s_abort) return false;
+        const uint64_t t = globaltimer();
+        if (t0 == 0) {
+            t0 = t;
+            return true;
         }
-        if (!*s_abort && (uint32_t)v != ((uint32_t)K & 0x7FFFFFFFu)) latch(st, TEM_ERR_PROTOCOL, -1);
+        if (t - t0 > spin_ns) {
+            latch(st, TEM_ERR_TRANSPORT, -1);
+            *s_abort = 1;
+            return false;
+        }
+        return true;
+    }
+};
+
+// Thread 0 waits for `flag` to reach `epoch` (two-shot / PS phase flags); returns false
+// (CTA-uniform) on timeout.
+TEM_DEV bool wait_flag(const uint64_t* flag, uint32_t epoch, Status* st, uint64_t spin_ns, int* s_abort) {
+    if (threadIdx.x == 0) {
+        Spin sp;
+        while ((uint32_t)(ld_acquire_sys(flag) >> 32) < epoch)
+            if (!sp.again(st, spin_ns, s_abort)) break;
     }
     __syncthreads();
     return *s_abort == 0;
 }
 
-TEM_DEV void signal_flag(uint64_t* flag, uint32_t epoch, int64_t K) {
+TEM_DEV void signal_flag(uint64_t* flag, uint32_t epoch) {
     __syncthreads();  // every thread's data stores precede thread 0's release (cumulative)
-    if (threadIdx.x == 0) st_release_sys(flag, flag_value(epoch, K));
+    if (threadIdx.x == 0) st_release_sys(flag, flag_value(epoch));
+}
+
+// The collective's descriptor in the header (kind: 0 ring, 1 two-shot, 2 PS).
+TEM_DEV uint4 header_value(int64_t K, uint32_t epoch, int kind, int op, int mode) {
+    const uint32_t hi = (uint32_t)((uint64_t)K >> 32) & 0xFFu;
+    return make_uint4((uint32_t)K, epoch, hi | ((uint32_t)kind << 8) | ((uint32_t)op << 16) | ((uint32_t)mode << 24),
+                      epoch);
+}
+
+// Symmetric pre-data check (see the file comment).  CTA-uniform result; false = abort.
+TEM_DEV bool handshake(const RingLocal& L, int N, int n, int g, uint32_t epoch, uint4 mine, int64_t off_hdr,
+                       Status* st, uint64_t spin_ns, int* s_abort) {
+    const int tid = threadIdx.x;
+    // slots [epoch parity][src][channel]: consecutive collectives use disjoint halves
+    auto slot = [&](int heap_rank, int src) {
+        return reinterpret_cast<uint4*>(L.heaps[heap_rank] + off_hdr) +
+               ((int64_t)(epoch & 1u) * TEM_MAX_RANKS + src) * kMaxChannels + g;
+    };
+    if (tid < N) st_volatile4(slot(tid, n), mine);
+    if (tid < N) {
+        const uint4* p = slot(n, tid);
+        uint4 h = ld_volatile4(p);
+        Spin sp;
+        while (h.y != epoch || h.w != epoch) {
+            if (!sp.again(st, spin_ns, s_abort)) break;
+            h = ld_volatile4(p);
+        }
+        if (h.y == epoch && h.w == epoch && (h.x != mine.x || h.z != mine.z)) {
+            latch(st, TEM_ERR_PROTOCOL, -1);
+            *s_abort = 1;
+        }
+    }
+    __syncthreads();
+    return *s_abort == 0;
 }
 
 // Refresh the operand copies of the weights: sh = bf16(w), and (3-pass fp32 path)
@@ -180,22 +227,55 @@ TEM_DEV void st4_masked(float* p, int64_t e, int64_t K, float4 v) {
     if (e + 2 < K) p[e + 2] = v.z;
 }
 
+// LL message of one float4 position: two lines {d0, e, d1, e}, {d2, e, d3, e}.
+TEM_DEV void ll_send(uint4* p, float4 a, uint32_t e) {
+    st_volatile4(p, make_uint4(__float_as_uint(a.x), e, __float_as_uint(a.y), e));
+    st_volatile4(p + 1, make_uint4(__float_as_uint(a.z), e, __float_as_uint(a.w), e));
+}
+// Receive the LL messages of up to RING_UNROLL positions (lines p[u], p[u] + 1; p[u] == nullptr:
+// no position): every line is loaded first, then only the lines still carrying an old epoch are
+// polled again -- one memory latency per batch, not per position.  false: abort (timeout).
+TEM_DEV bool ll_recv(const uint4* const (&p)[RING_UNROLL], uint32_t e, float4 (&out)[RING_UNROLL], Status* st,
+                     uint64_t spin_ns, volatile int* s_abort) {
+    uint4 a[RING_UNROLL], b[RING_UNROLL];
+#pragma unroll
+    for (int u = 0; u < RING_UNROLL; ++u)
+        if (p[u]) {
+            a[u] = ld_volatile4(p[u]);
+            b[u] = ld_volatile4(p[u] + 1);
+        }
+    Spin sp;
+    while (true) {
+        bool done = true;
+#pragma unroll
+        for (int u = 0; u < RING_UNROLL; ++u) {
+            if (!p[u]) continue;
+            if (a[u].y != e || a[u].w != e) {
+                done = false;
+                a[u] = ld_volatile4(p[u]);
+            }
+            if (b[u].y != e || b[u].w != e) {
+                done = false;
+                b[u] = ld_volatile4(p[u] + 1);
+            }
+        }
+        if (done) break;
+        if (!sp.again(st, spin_ns, s_abort)) return false;
+    }
+#pragma unroll
+    for (int u = 0; u < RING_UNROLL; ++u)
+        out[u] = make_float4(__uint_as_float(a[u].x), __uint_as_float(a[u].z), __uint_as_float(b[u].x),
+                             __uint_as_float(b[u].z));
+    return true;
+}
+
 __global__ void __launch_bounds__(RING_THREADS) ring_kernel(const __grid_constant__ RingParams P) {
     __shared__ uint32_t s_epoch;
     __shared__ int s_abort;
     const int l = blockIdx.y, g = blockIdx.x, tid = threadIdx.x;
-    const int N = P.N, n = P.rank_base + l, G = P.G, C = P.C;
+    const int N = P.N, n = P.rank_base + l, G = P.G;
     const RingLocal& L = P.loc[l];
     const int right = modn(n + 1, N);
-    char* heap_self = L.heaps[n];
-    char* heap_right = L.heaps[right];
-    const float* stage_self = reinterpret_cast<const float*>(heap_self + P.off_stage);
-    float* stage_right = reinterpret_cast<float*>(heap_right + P.off_stage);
-    const uint64_t* flags_self = reinterpret_cast<const uint64_t*>(heap_self + P.off_flags);
-    uint64_t* flags_right = reinterpret_cast<uint64_t*>(heap_right + P.off_flags);
-    float* dst_right = reinterpret_cast<float*>(heap_right + P.off_dst);
-    float* dst_self = L.dst_self;
-    const float* src = L.src;
     const int64_t K = P.K, Bk = P.Kpad / N, nvec = Bk / 4;
     const float inv_n = 1.0f / (float)N;
     if (tid == 0) {
@@ -204,87 +284,115 @@ __global__ void __launch_bounds__(RING_THREADS) ring_kernel(const __grid_constan
     }
     __syncthreads();
     const uint32_t epoch = s_epoch;
-    // slot tied to (channel g, chunk c) forever: epochs of channel g only ever grow
-    auto fidx = [&](int phase, int round, int c) -> int64_t {
-        return (((int64_t)g * kMaxChunks + c) * 2 + phase) * (TEM_MAX_RANKS - 1) + round;
-    };
+    if (!handshake(L, N, n, g, epoch, header_value(K, epoch, 0, P.op, P.mode), P.off_hdr, P.status, P.spin_ns,
+                   &s_abort))
+        return;
+    volatile int* abort = &s_abort;
+    const uint4* ll_self = reinterpret_cast<const uint4*>(L.heaps[n] + P.off_ll);
+    uint4* ll_right = reinterpret_cast<uint4*>(L.heaps[right] + P.off_ll);
+    // line of float4 position v in LL slot (epoch parity, phase, round): fixed stride P.ll_stride
+    // lines; consecutive collectives use disjoint halves
+    const int64_t half = (int64_t)(epoch & 1u) * 2 * (N - 1);
+    auto slot = [&](int phase, int round) { return (half + phase * (N - 1) + round) * P.ll_stride; };
+    const float* src = L.src;
+    float* dst = L.dst_self;
+    const int64_t stride = (int64_t)G * RING_THREADS;
+    const int64_t v_begin = (int64_t)g * RING_THREADS + tid;
 
     // ---------------- scatter: rounds 0..N-2 ----------------
     for (int i = 0; i <= N - 2; ++i) {
-        const int s = modn(n - i, N);
-        for (int c = 0; c < C; ++c) {
-            const Piece pc = piece_of(nvec, G, C, g, c);
-            if (i > 0 && !wait_flag(flags_self + fidx(0, i - 1, c), epoch, K, P.status, P.spin_ns, &s_abort))
-                return;
-            for (int64_t v = pc.v0 + tid; v < pc.v1; v += RING_THREADS) {
-                const int64_t e = (int64_t)s * Bk + 4 * v;  // global element index
-                if (e >= K) continue;
-                float4 a = ld4_masked(src, e, K);
-                if (i > 0) {
-                    const float4 b = ld_cg4(stage_self + (int64_t)(i - 1) * Bk + 4 * v);
-                    a.x = a.x + b.x; a.y = a.y + b.y; a.z = a.z + b.z; a.w = a.w + b.w;
-                }
-                *reinterpret_cast<float4*>(stage_right + (int64_t)i * Bk + 4 * v) = a;
+        const int64_t blk = (int64_t)modn(n - i, N) * Bk;
+        for (int64_t v0 = v_begin; v0 < nvec; v0 += RING_UNROLL * stride) {
+            float4 a[RING_UNROLL];
+#pragma unroll
+            for (int u = 0; u < RING_UNROLL; ++u) {
+                const int64_t v = v0 + u * stride;
+                if (v < nvec) a[u] = ld4_masked(src, blk + 4 * v, K);
             }
-            signal_flag(flags_right + fidx(0, i, c), epoch, K);
+            if (i > 0) {
+                const uint4* q[RING_UNROLL];
+                float4 b[RING_UNROLL];
+#pragma unroll
+                for (int u = 0; u < RING_UNROLL; ++u) {
+                    const int64_t v = v0 + u * stride;
+                    q[u] = v < nvec ? ll_self + slot(0, i - 1) + 2 * v : nullptr;
+                }
+                if (!ll_recv(q, epoch, b, P.status, P.spin_ns, abort)) return;
+#pragma unroll
+                for (int u = 0; u < RING_UNROLL; ++u) {
+                    a[u].x = a[u].x + b[u].x; a[u].y = a[u].y + b[u].y; a[u].z = a[u].z + b[u].z; a[u].w = a[u].w + b[u].w;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < RING_UNROLL; ++u) {
+                const int64_t v = v0 + u * stride;
+                if (v < nvec) ll_send(ll_right + slot(0, i) + 2 * v, a[u], epoch);
+            }
         }
     }
-    // ---------------- owner: last add, mean, SGD; gather round 0 fused ----------------
+    // ---------------- owner: last add, mean, update; gather round 0's message ----------------
     {
-        const int b = modn(n + 1, N);
-        for (int c = 0; c < C; ++c) {
-            const Piece pc = piece_of(nvec, G, C, g, c);
-            if (N > 1 && !wait_flag(flags_self + fidx(0, N - 2, c), epoch, K, P.status, P.spin_ns, &s_abort))
-                return;
-            for (int64_t v = pc.v0 + tid; v < pc.v1; v += RING_THREADS) {
-                const int64_t e = (int64_t)b * Bk + 4 * v;
-                if (e >= K) continue;
-                float4 a = ld4_masked(src, e, K);
+        const int64_t blk = (int64_t)modn(n + 1, N) * Bk;
+        for (int64_t v0 = v_begin; v0 < nvec; v0 += RING_UNROLL * stride) {
+            float4 a[RING_UNROLL], w[RING_UNROLL];
+#pragma unroll
+            for (int u = 0; u < RING_UNROLL; ++u) {
+                const int64_t v = v0 + u * stride;
+                if (v >= nvec) continue;
+                a[u] = ld4_masked(src, blk + 4 * v, K);
+                if (P.mode == 1) w[u] = *reinterpret_cast<const float4*>(dst + blk + 4 * v);
+            }
+            float4 r[RING_UNROLL];
+            if (N > 1) {
+                const uint4* q[RING_UNROLL];
+#pragma unroll
+                for (int u = 0; u < RING_UNROLL; ++u) {
+                    const int64_t v = v0 + u * stride;
+                    q[u] = v < nvec ? ll_self + slot(0, N - 2) + 2 * v : nullptr;
+                }
+                if (!ll_recv(q, epoch, r, P.status, P.spin_ns, abort)) return;
+            }
+#pragma unroll
+            for (int u = 0; u < RING_UNROLL; ++u) {
+                const int64_t v = v0 + u * stride;
+                if (v >= nvec) continue;
+                const int64_t e = blk + 4 * v;
+                float4 x = a[u];
                 if (N > 1) {
-                    const float4 r = ld_cg4(stage_self + (int64_t)(N - 2) * Bk + 4 * v);
-                    a.x = a.x + r.x; a.y = a.y + r.y; a.z = a.z + r.z; a.w = a.w + r.w;
+                    x.x = x.x + r[u].x; x.y = x.y + r[u].y; x.z = x.z + r[u].z; x.w = x.w + r[u].w;
                 }
                 if (P.op == TEM_MEAN) {
-                    a.x = a.x * inv_n; a.y = a.y * inv_n; a.z = a.z * inv_n; a.w = a.w * inv_n;
+                    x.x = x.x * inv_n; x.y = x.y * inv_n; x.z = x.z * inv_n; x.w = x.w * inv_n;
                 }
-                float4 out = a;
                 if (P.mode == 1) {
-                    out = owner_update(P.oc, L.opt, e, a, *reinterpret_cast<const float4*>(dst_self + e));
-                    if (L.shadow) store_shadow4(L.shadow, L.shadow_lo, e, out);
+                    x = owner_update(P.oc, L.opt, e, x, w[u]);
+                    if (L.shadow) store_shadow4(L.shadow, L.shadow_lo, e, x);
                 }
-                st4_masked(dst_self, e, K, out);
-                if (N > 1) st4_masked(dst_right, e, K, out);
+                st4_masked(dst, e, K, x);
+                if (N > 1) ll_send(ll_right + slot(1, 0) + 2 * v, x, epoch);
             }
-            if (N > 1) signal_flag(flags_right + fidx(1, 0, c), epoch, K);
         }
     }
-    // ---------------- gather rounds 1..N-2: forward what arrived ----------------
-    for (int k = 1; k <= N - 2; ++k) {
-        const int s = modn(n + 1 - k, N);
-        for (int c = 0; c < C; ++c) {
-            const Piece pc = piece_of(nvec, G, C, g, c);
-            if (!wait_flag(flags_self + fidx(1, k - 1, c), epoch, K, P.status, P.spin_ns, &s_abort)) return;
-            for (int64_t v = pc.v0 + tid; v < pc.v1; v += RING_THREADS) {
-                const int64_t e = (int64_t)s * Bk + 4 * v;
-                if (e >= K) continue;
-                const float4 a = ldcg4_masked(dst_self, e, K);
-                if (L.shadow) store_shadow4(L.shadow, L.shadow_lo, e, a);
-                st4_masked(dst_right, e, K, a);
+    // ---------------- gather rounds 1..N-2: store what arrived, forward it; then the last ------
+    for (int k = 1; k <= N - 1; ++k) {
+        const int64_t blk = (int64_t)modn(n + 1 - k, N) * Bk;  // received in round k-1 (R10)
+        for (int64_t v0 = v_begin; v0 < nvec; v0 += RING_UNROLL * stride) {
+            const uint4* q[RING_UNROLL];
+            float4 x[RING_UNROLL];
+#pragma unroll
+            for (int u = 0; u < RING_UNROLL; ++u) {
+                const int64_t v = v0 + u * stride;
+                q[u] = v < nvec ? ll_self + slot(1, k - 1) + 2 * v : nullptr;
             }
-            signal_flag(flags_right + fidx(1, k, c), epoch, K);
-        }
-    }
-    // ---------------- last gather round: receive block (n+2) mod N ----------------
-    if (N > 1) {
-        const int r = modn(n + 2, N);
-        for (int c = 0; c < C; ++c) {
-            const Piece pc = piece_of(nvec, G, C, g, c);
-            if (!wait_flag(flags_self + fidx(1, N - 2, c), epoch, K, P.status, P.spin_ns, &s_abort)) return;
-            if (L.shadow) {
-                for (int64_t v = pc.v0 + tid; v < pc.v1; v += RING_THREADS) {
-                    const int64_t e = (int64_t)r * Bk + 4 * v;
-                    store_shadow4(L.shadow, L.shadow_lo, e, ld_cg4(dst_self + e));
-                }
+            if (!ll_recv(q, epoch, x, P.status, P.spin_ns, abort)) return;
+#pragma unroll
+            for (int u = 0; u < RING_UNROLL; ++u) {
+                const int64_t v = v0 + u * stride;
+                if (v >= nvec) continue;
+                const int64_t e = blk + 4 * v;
+                if (k <= N - 2) ll_send(ll_right + slot(1, k) + 2 * v, x[u], epoch);
+                st4_masked(dst, e, K, x[u]);
+                if (L.shadow) store_shadow4(L.shadow, L.shadow_lo, e, x[u]);
             }
         }
     }
@@ -303,7 +411,7 @@ __global__ void __launch_bounds__(RING_THREADS) ring_kernel(const __grid_constan
 //            stores) and raises a done flag in every peer.
 //   then:    each rank waits for the done flags of the N-1 other owners and refreshes its bf16
 //            operand copies of those blocks.
-// Flags: [epoch | K tag] as the ring; ready[src][channel], done[owner][channel] at off_flags.
+// Flags: epoch words (after the handshake); ready[src][channel], done[owner][channel] at off_flags.
 __global__ void __launch_bounds__(RING_THREADS) twoshot_kernel(const __grid_constant__ RingParams P) {
     __shared__ uint32_t s_epoch;
     __shared__ int s_abort;
@@ -325,6 +433,9 @@ __global__ void __launch_bounds__(RING_THREADS) twoshot_kernel(const __grid_cons
     }
     __syncthreads();
     const uint32_t epoch = s_epoch;
+    if (!handshake(L, N, n, g, epoch, header_value(K, epoch, 1, P.op, P.mode), P.off_hdr, P.status, P.spin_ns,
+                   &s_abort))
+        return;
     // channel g's piece of every block: vectors [v0, v1) of each block
     const int64_t v0 = (int64_t)g * nvec / G, v1 = (int64_t)(g + 1) * nvec / G;
     // ---------------- phase 0: stage (own heap) + ready flags ----------------
@@ -338,11 +449,11 @@ __global__ void __launch_bounds__(RING_THREADS) twoshot_kernel(const __grid_cons
             }
     }
     __syncthreads();
-    if (tid < N) st_release_sys(flag(tid, 0, n), flag_value(epoch, K));  // ready: my piece g is readable
+    if (tid < N) st_release_sys(flag(tid, 0, n), flag_value(epoch));  // ready: my piece g is readable
     // ---------------- phase 1: owner reduce (chain order) + mean/SGD + broadcast ----------------
     const int b = modn(n + 1, N);
     for (int r = 0; r < N; ++r)
-        if (!wait_flag(flag(n, 0, r), epoch, K, P.status, P.spin_ns, &s_abort)) return;
+        if (!wait_flag(flag(n, 0, r), epoch, P.status, P.spin_ns, &s_abort)) return;
     for (int64_t v = v0 + tid; v < v1; v += RING_THREADS) {
         const int64_t e = (int64_t)b * Bk + 4 * v;
         if (e >= K) continue;
@@ -362,11 +473,11 @@ __global__ void __launch_bounds__(RING_THREADS) twoshot_kernel(const __grid_cons
         for (int r = 0; r < N; ++r) st4_masked(reinterpret_cast<float*>(heap(r) + P.off_dst), e, K, out);
     }
     __syncthreads();
-    if (tid < N) st_release_sys(flag(tid, 1, n), flag_value(epoch, K));  // done: block b piece g written
+    if (tid < N) st_release_sys(flag(tid, 1, n), flag_value(epoch));  // done: block b piece g written
     // ---------------- receive: the other owners' blocks, refresh operand copies ----------------
     for (int q = 1; q < N; ++q) {
         const int owner = modn(n + q, N), blk = modn(owner + 1, N);
-        if (!wait_flag(flag(n, 1, owner), epoch, K, P.status, P.spin_ns, &s_abort)) return;
+        if (!wait_flag(flag(n, 1, owner), epoch, P.status, P.spin_ns, &s_abort)) return;
         if (L.shadow) {
             for (int64_t v = v0 + tid; v < v1; v += RING_THREADS) {
                 const int64_t e = (int64_t)blk * Bk + 4 * v;
@@ -484,6 +595,9 @@ __global__ void __launch_bounds__(RING_THREADS) ps_kernel(const __grid_constant_
     }
     __syncthreads();
     const uint32_t epoch = s_epoch;
+    if (!handshake(L, N, n, g, epoch, header_value(K, epoch, 2, P.op, P.mode), P.off_hdr, P.status, P.spin_ns,
+                   &s_abort))
+        return;
     // K_slot stride: slots hold K rounded up to 4
     const int64_t slot_stride = Kv * 4;
     // phase 0: push to server slot n (uplink: N*M)
@@ -494,13 +608,13 @@ __global__ void __launch_bounds__(RING_THREADS) ps_kernel(const __grid_constant_
             st4_masked(slot, e, K, ld4_masked(L.src, e, K));
         }
         uint64_t* f = reinterpret_cast<uint64_t*>(heap0 + P.off_flags) + (int64_t)n * kMaxChannels + g;
-        signal_flag(f, epoch, K);
+        signal_flag(f, epoch);
     }
     if (n == 0) {
         // server: wait for all N pushes of this channel, then reduce in ascending rank order
         for (int r = 0; r < N; ++r) {
             const uint64_t* f = reinterpret_cast<const uint64_t*>(heap0 + P.off_flags) + (int64_t)r * kMaxChannels + g;
-            if (!wait_flag(f, epoch, K, P.status, P.spin_ns, &s_abort)) return;
+            if (!wait_flag(f, epoch, P.status, P.spin_ns, &s_abort)) return;
         }
         const float* slots = reinterpret_cast<const float*>(heap0 + P.off_slots);
         for (int64_t v = v0 + tid; v < v1; v += RING_THREADS) {
@@ -521,13 +635,13 @@ __global__ void __launch_bounds__(RING_THREADS) ps_kernel(const __grid_constant_
         __syncthreads();
         for (int r = 0; r < N; ++r) {
             uint64_t* f = reinterpret_cast<uint64_t*>(L.heaps[r] + P.off_flags) + (int64_t)(TEM_MAX_RANKS + r) * kMaxChannels + g;
-            signal_flag(f, epoch, K);
+            signal_flag(f, epoch);
         }
     }
     // everybody: wait for the downlink of this channel
     {
         const uint64_t* f = reinterpret_cast<const uint64_t*>(L.heaps[n] + P.off_flags) + (int64_t)(TEM_MAX_RANKS + n) * kMaxChannels + g;
-        if (!wait_flag(f, epoch, K, P.status, P.spin_ns, &s_abort)) return;
+        if (!wait_flag(f, epoch, P.status, P.spin_ns, &s_abort)) return;
     }
     if (L.shadow)  // refresh this rank's operand copies of the new weights (its channel slice)
         for (int64_t v = v0 + tid; v < v1; v += RING_THREADS)

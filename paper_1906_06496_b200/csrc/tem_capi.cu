@@ -44,7 +44,7 @@ int tem::launch_priority_attr(cudaLaunchAttribute* a, bool side) {
 namespace {
 
 constexpr size_t kAlign = 256;
-constexpr uint64_t kSpinNs = 20ull * 1000 * 1000 * 1000;  // 20 s flag-wait bound
+constexpr uint64_t kSpinMsDefault = 20000;  // flag-wait bound when cfg->spin_timeout_ms == 0
 #ifdef TEM_DIAG
 constexpr size_t kTraceWords = 2 * NUM_SLOTS + 4096 * 8;    // diagnostics trace area
 #endif
@@ -53,7 +53,8 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 int64_t roundup(int64_t x, int64_t q) { return (x + q - 1) / q * q; }
 
 struct HeapLayout {
-    size_t off_user, user_bytes, off_stage, off_ps, off_flags, off_psflags, off_tsflags, total;
+    size_t off_user, user_bytes, off_stage, off_ps, off_hdr, off_psflags, off_tsflags, off_ll, total;
+    int64_t ll_stride;  // LL lines per ring slot
 };
 
 struct WsLayout {
@@ -77,7 +78,7 @@ bool cfg_valid(const tem_config* c) {
         if (!isfinite(c->loss_weight[o])) return false;
     if (c->max_allreduce_elems < 0) return false;
     if (c->ring_channels < 0 || c->ring_channels > kMaxChannels) return false;
-    if (c->ring_chunks < 0 || c->ring_chunks > kMaxChunks) return false;
+    if (c->spin_timeout_ms < 0) return false;
     if (c->exchange != TEM_EXCHANGE_RING && c->exchange != TEM_EXCHANGE_PS && c->exchange != TEM_EXCHANGE_TWOSHOT)
         return false;
     if (c->pem_proposals < 0) return false;
@@ -146,11 +147,14 @@ HeapLayout heap_layout(const tem_config* c) {
     const size_t stage_bytes = (size_t)(kpad > kar ? kpad : kar) * 4;
     h.off_ps = align_up(h.off_stage + stage_bytes, 4096);
     const int64_t kps = roundup(num_params(c) > max_ar(c) ? num_params(c) : max_ar(c), 4);
-    h.off_flags = align_up(h.off_ps + (size_t)N * kps * 4, 4096);
-    const size_t ring_flags = (size_t)kMaxChannels * kMaxChunks * 2 * (TEM_MAX_RANKS - 1) * 8;
-    h.off_psflags = h.off_flags + ring_flags;
+    h.off_hdr = align_up(h.off_ps + (size_t)N * kps * 4, 4096);
+    h.off_psflags = h.off_hdr + (size_t)2 * TEM_MAX_RANKS * kMaxChannels * 16;
     h.off_tsflags = h.off_psflags + (size_t)2 * TEM_MAX_RANKS * kMaxChannels * 8;
-    h.total = align_up(h.off_tsflags + (size_t)2 * TEM_MAX_RANKS * kMaxChannels * 8, 4096);
+    // ring LL slots: [2 epoch parities][2 phases][N-1 rounds][2 lines per float4 of the
+    // largest block] x 16 B
+    h.ll_stride = (kpad > kar ? kpad : kar) / N / 2;
+    h.off_ll = align_up(h.off_tsflags + (size_t)2 * TEM_MAX_RANKS * kMaxChannels * 8, 4096);
+    h.total = align_up(h.off_ll + (size_t)4 * (N - 1) * h.ll_stride * 16, 4096);
     return h;
 }
 
@@ -228,7 +232,9 @@ struct tem_ctx {
     HeapLayout hl;
     WsLayout wl;
     int N, nlocal, rank;
-    int G, C;                  // ring channels / chunks for the TEM gradient
+    int G;                     // channels (CTAs per rank) of every collective: fixed per context,
+                               // so the per-channel epochs advance together
+    uint64_t spin_ns;          // flag-wait bound
     RankBufs rb[TEM_MAX_RANKS];
     UmmaPlan* plan[TEM_MAX_RANKS];
     uint32_t* epochs[TEM_MAX_RANKS];
@@ -365,6 +371,12 @@ size_t tem_sym_bytes(const tem_config* cfg) { return cfg_valid(cfg) ? heap_layou
 
 size_t tem_sym_user_offset(const tem_config* cfg) { return cfg_valid(cfg) ? heap_layout(cfg).off_user : 0; }
 
+size_t tem_sym_hdr_offset(const tem_config* cfg) { return cfg_valid(cfg) ? heap_layout(cfg).off_hdr : 0; }
+
+size_t tem_sym_ll_offset(const tem_config* cfg) { return cfg_valid(cfg) ? heap_layout(cfg).off_ll : 0; }
+
+int64_t tem_ll_slot_lines(const tem_config* cfg) { return cfg_valid(cfg) ? heap_layout(cfg).ll_stride : 0; }
+
 tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
     if (!out) return TEM_ERR_INVALID_ARG;
     *out = nullptr;
@@ -390,9 +402,10 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
     c->N = cfg->world_size;
     c->nlocal = cfg->local_ranks;
     c->rank = cfg->rank;
-    // ring geometry for the TEM gradient (identical on every rank: depends on cfg only)
+    // channels of every collective (identical on every rank: depends on cfg only, never on a
+    // call's K)
     c->G = cfg->ring_channels > 0 ? cfg->ring_channels : 16;
-    c->C = cfg->ring_chunks > 0 ? cfg->ring_chunks : 4;
+    c->spin_ns = (uint64_t)(cfg->spin_timeout_ms > 0 ? cfg->spin_timeout_ms : kSpinMsDefault) * 1000000ull;
     if (c->nlocal > 1) {  // emulation: all CTAs of all emulated ranks must be co-resident
         int dev_sms = 148;
         cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, cfg->device);
@@ -530,6 +543,16 @@ static int64_t bucket_bound(const tem_ctx* c) {
 }
 static bool bucketed(const tem_ctx* c) { return c->cfg.exchange_buckets == 2 && c->N > 1; }
 
+static void set_heap_offsets(const tem_ctx* c, RingParams* p) {
+    p->off_stage = (int64_t)c->hl.off_stage;
+    p->off_flags = (int64_t)c->hl.off_tsflags;  // two-shot phase flags (the ring needs none)
+    p->off_hdr = (int64_t)c->hl.off_hdr;
+    p->off_ll = (int64_t)c->hl.off_ll;
+    p->ll_stride = c->hl.ll_stride;
+    p->status = c->st_dev;
+    p->spin_ns = c->spin_ns;
+}
+
 // The tem_step exchange of elements [e0, e1) of the flat gradient: every pointer and the heap
 // destination offset shifted by e0, the ring's partition taken over e1 - e0 (a multiple of 4N).
 static RingParams step_ring(tem_ctx* c, int64_t e0, int64_t e1) {
@@ -546,17 +569,13 @@ static RingParams step_ring(tem_ctx* c, int64_t e0, int64_t e1) {
     p.rank_base = c->rank;
     p.nlocal = c->nlocal;
     p.G = c->G;
-    p.C = c->C;
     p.op = TEM_MEAN;
     p.mode = 1;
     p.K = e1 - e0;
     p.Kpad = e1 - e0;
     p.oc = opt_cfg(c);
     p.off_dst = e0 * (int64_t)sizeof(float);
-    p.off_stage = (int64_t)c->hl.off_stage;
-    p.off_flags = (int64_t)(c->cfg.exchange == TEM_EXCHANGE_TWOSHOT ? c->hl.off_tsflags : c->hl.off_flags);
-    p.status = c->st_dev;
-    p.spin_ns = kSpinNs;
+    set_heap_offsets(c, &p);
     return p;
 }
 
@@ -712,17 +731,13 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
     p.rank_base = c->rank;
     p.nlocal = c->nlocal;
     p.G = c->G;
-    p.C = c->C;
     p.op = TEM_MEAN;
     p.mode = 1;
     p.K = g.Kpad;
     p.Kpad = g.Kpad;
     p.oc = oc;
     p.off_dst = 0;
-    p.off_stage = (int64_t)c->hl.off_stage;
-    p.off_flags = (int64_t)c->hl.off_flags;
-    p.status = c->st_dev;
-    p.spin_ns = kSpinNs;
+    set_heap_offsets(c, &p);
     if (c->cfg.exchange == TEM_EXCHANGE_PS) {  // comparator: push / server update / pull
         PsParams q;
         memset(&q, 0, sizeof(q));
@@ -738,11 +753,11 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
         q.off_dst = 0;
         q.off_slots = (int64_t)c->hl.off_ps;
         q.off_flags = (int64_t)c->hl.off_psflags;
+        q.off_hdr = (int64_t)c->hl.off_hdr;
         q.status = c->st_dev;
-        q.spin_ns = kSpinNs;
+        q.spin_ns = c->spin_ns;
         if (launch_ps(q, s) != cudaSuccess) return TEM_ERR_CUDA;
     } else if (c->cfg.exchange == TEM_EXCHANGE_TWOSHOT) {  // NVSwitch two-shot (NEXT #3(i))
-        p.off_flags = (int64_t)c->hl.off_tsflags;
         if (launch_twoshot(p, s) != cudaSuccess) return TEM_ERR_CUDA;
     } else if (launch_ring(p, s) != cudaSuccess) {
         return TEM_ERR_CUDA;
@@ -977,21 +992,6 @@ tem_status tem_step_pem_host(tem_ctx* c, const void* x_host, const float* labels
     return TEM_OK;
 }
 
-static int ar_channels(tem_ctx* c, int64_t kpad) {
-    // ~>= 2K float4 per channel per block piece set; same on every rank (depends on K, N, cfg)
-    int64_t nvec = kpad / c->N / 4;
-    int64_t G = nvec / 2048;
-    const int cap = c->cfg.ring_channels > 0 ? c->cfg.ring_channels : 32;
-    if (G > cap) G = cap;
-    if (G < 1) G = 1;
-    if (c->nlocal > 1) {
-        int dev_sms = 148;
-        cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->cfg.device);
-        if (G > dev_sms / c->nlocal) G = dev_sms / c->nlocal;
-    }
-    return (int)G;
-}
-
 tem_status ring_allreduce(tem_ctx* c, float* buf, int64_t K, int32_t op, void* stream) {
     tem_status st = check_ctx(c);
     if (st != TEM_OK) return st;
@@ -1008,16 +1008,12 @@ tem_status ring_allreduce(tem_ctx* c, float* buf, int64_t K, int32_t op, void* s
     p.rank_base = c->rank;
     p.nlocal = c->nlocal;
     p.Kpad = roundup(K, 4 * (int64_t)c->N);
-    p.G = ar_channels(c, p.Kpad);
-    p.C = c->cfg.ring_chunks > 0 ? c->cfg.ring_chunks : 4;
+    p.G = c->G;
     p.op = op;
     p.mode = 0;
     p.K = K;
     p.off_dst = (int64_t)c->hl.off_user;
-    p.off_stage = (int64_t)c->hl.off_stage;
-    p.off_flags = (int64_t)c->hl.off_flags;
-    p.status = c->st_dev;
-    p.spin_ns = kSpinNs;
+    set_heap_offsets(c, &p);
     if (launch_ring(p, (cudaStream_t)stream) != cudaSuccess) return TEM_ERR_CUDA;
     return TEM_OK;
 }
@@ -1038,16 +1034,14 @@ tem_status twoshot_allreduce(tem_ctx* c, float* buf, int64_t K, int32_t op, void
     p.rank_base = c->rank;
     p.nlocal = c->nlocal;
     p.Kpad = roundup(K, 4 * (int64_t)c->N);
-    p.G = ar_channels(c, p.Kpad);
+    p.G = c->G;
     p.op = op;
     p.mode = 0;
     p.K = K;
     p.off_dst = (int64_t)c->hl.off_user;
+    set_heap_offsets(c, &p);
     p.off_stage = -1;  // in place: the user region is the readable source
     p.off_src = (int64_t)c->hl.off_user;
-    p.off_flags = (int64_t)c->hl.off_tsflags;
-    p.status = c->st_dev;
-    p.spin_ns = kSpinNs;
     if (launch_twoshot(p, (cudaStream_t)stream) != cudaSuccess) return TEM_ERR_CUDA;
     return TEM_OK;
 }
@@ -1067,14 +1061,15 @@ tem_status ps_allreduce(tem_ctx* c, float* buf, int64_t K, int32_t op, void* str
     p.N = c->N;
     p.rank_base = c->rank;
     p.nlocal = c->nlocal;
-    p.G = ar_channels(c, roundup(K, 4 * (int64_t)c->N));
+    p.G = c->G;
     p.op = op;
     p.K = K;
     p.off_dst = (int64_t)c->hl.off_user;
     p.off_slots = (int64_t)c->hl.off_ps;
     p.off_flags = (int64_t)c->hl.off_psflags;
+    p.off_hdr = (int64_t)c->hl.off_hdr;
     p.status = c->st_dev;
-    p.spin_ns = kSpinNs;
+    p.spin_ns = c->spin_ns;
     if (launch_ps(p, (cudaStream_t)stream) != cudaSuccess) return TEM_ERR_CUDA;
     return TEM_OK;
 }

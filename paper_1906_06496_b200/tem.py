@@ -39,7 +39,7 @@ class tem_config(ctypes.Structure):
         ("peer_bufs", ctypes.POINTER(ctypes.c_void_p)), ("sym_bytes", ctypes.c_size_t),
         ("max_allreduce_elems", ctypes.c_int64),
         ("workspace", ctypes.c_void_p), ("workspace_bytes", ctypes.c_size_t),
-        ("ring_channels", ctypes.c_int32), ("ring_chunks", ctypes.c_int32),
+        ("ring_channels", ctypes.c_int32), ("spin_timeout_ms", ctypes.c_int32),
         ("exchange", ctypes.c_int32),
         ("pem_proposals", ctypes.c_int32), ("pem_features", ctypes.c_int32), ("pem_hidden", ctypes.c_int32),
         ("optimizer", ctypes.c_int32), ("beta1", ctypes.c_float), ("beta2", ctypes.c_float), ("eps", ctypes.c_float),
@@ -68,9 +68,12 @@ def lib():
         L.tem_num_params.argtypes = [cp]
         L.tem_kpad.restype = ctypes.c_int64
         L.tem_kpad.argtypes = [cp, ctypes.c_int64]
-        for f in (L.tem_workspace_bytes, L.tem_sym_bytes, L.tem_sym_user_offset):
+        for f in (L.tem_workspace_bytes, L.tem_sym_bytes, L.tem_sym_user_offset, L.tem_sym_hdr_offset,
+                  L.tem_sym_ll_offset):
             f.restype = ctypes.c_size_t
             f.argtypes = [cp]
+        L.tem_ll_slot_lines.restype = ctypes.c_int64
+        L.tem_ll_slot_lines.argtypes = [cp]
         L.tem_init.restype = ctypes.c_int
         L.tem_init.argtypes = [cp, _P, ctypes.POINTER(_P)]
         for f in (L.tem_step, L.tem_compute):
@@ -128,7 +131,8 @@ EXPORTS = ["tem_num_params", "tem_kpad", "tem_workspace_bytes", "tem_sym_bytes",
            "tem_local_grad", "tem_logits", "tem_launches_per_step", "tem_launches_per_exchange",
            "tem_status_string", "tem_kernel_path", "tem_timing_slots", "tem_timing_slot_name",
            "tem_timing_begin", "tem_timing_end", "tem_relu_decisions", "tem_debug_buffer",
-           "tem_step_pem", "tem_compute_pem", "tem_pem_relu_decisions", "twoshot_allreduce", "tem_step_pem_host", "tem_pgm", "tem_step_pgm", "tem_compute_pgm"]
+           "tem_step_pem", "tem_compute_pem", "tem_pem_relu_decisions", "twoshot_allreduce", "tem_step_pem_host", "tem_pgm", "tem_step_pgm", "tem_compute_pgm",
+           "tem_sym_hdr_offset", "tem_sym_ll_offset", "tem_ll_slot_lines"]
 
 
 def status_string(code: int) -> str:
@@ -247,7 +251,7 @@ class SessionConfig:
     loss_weight: Sequence[float] = (1.0, 1.0, 1.0)
     max_allreduce_elems: int = 0
     ring_channels: int = 0
-    ring_chunks: int = 0
+    spin_timeout_ms: int = 0  # bound on a wait for a peer; 0 -> 20 s
     exchange: int = TEM_EXCHANGE_RING
     pem_proposals: int = 0  # > 0: joint TEM + PEM (configs[4]); params = [TEM | PEM]
     pem_features: int = 32
@@ -268,9 +272,14 @@ class TemSession:
       heap is a plain device allocation on this GPU.
     * local_ranks == 1 and world_size > 1 (one process per GPU): the heap comes from
       torch symmetric memory; its rendezvous gives the peer pointers (NVLink P2P).
+    * virtual_peers=True (tests only; local_ranks == 1): every rank's heap is a plain
+      allocation on this GPU and this process drives rank sc.rank alone; the test plays the
+      other ranks by writing their headers and messages into the heaps (the wire protocol of
+      include/tem.h) BEFORE the collective is launched, so no kernel ever waits on another.
     """
 
-    def __init__(self, sc: SessionConfig, params: np.ndarray, device: int | None = None, group=None):
+    def __init__(self, sc: SessionConfig, params: np.ndarray, device: int | None = None, group=None,
+                 virtual_peers: bool = False):
         L = lib()
         self.sc = sc
         self.device = torch.cuda.current_device() if device is None else device
@@ -283,7 +292,7 @@ class TemSession:
         for i in range(3):
             cfg.loss_weight[i] = float(sc.loss_weight[i])
         cfg.max_allreduce_elems = sc.max_allreduce_elems
-        cfg.ring_channels, cfg.ring_chunks = sc.ring_channels, sc.ring_chunks
+        cfg.ring_channels, cfg.spin_timeout_ms = sc.ring_channels, sc.spin_timeout_ms
         cfg.exchange = sc.exchange
         cfg.pem_proposals, cfg.pem_features, cfg.pem_hidden = sc.pem_proposals, sc.pem_features, sc.pem_hidden
         cfg.optimizer, cfg.beta1, cfg.beta2, cfg.eps = sc.optimizer, sc.beta1, sc.beta2, sc.eps
@@ -299,7 +308,10 @@ class TemSession:
         self.ws_bytes = tem_workspace_bytes(cfg)
         N = sc.world_size
         self._symm = None
-        if sc.local_ranks == N:
+        self.hdr_off = lib().tem_sym_hdr_offset(cfg)
+        self.ll_off = lib().tem_sym_ll_offset(cfg)
+        self.ll_lines = lib().tem_ll_slot_lines(cfg)
+        if sc.local_ranks == N or virtual_peers:
             self.heaps = [torch.zeros(self.sym_bytes + 4096, dtype=torch.uint8, device=self.dev)
                           for _ in range(N)]
             ptrs = [(h.data_ptr() + 4095) // 4096 * 4096 for h in self.heaps]
@@ -338,6 +350,9 @@ class TemSession:
         pt = torch.from_numpy(p).to(self.dev)
         for l in range(sc.local_ranks):
             self.params(l).copy_(pt)
+        if virtual_peers:
+            for r in range(N):
+                self._heap_of(r)[: 4 * self.Kpad].view(torch.float32).copy_(pt)
         torch.cuda.synchronize(self.dev)
         self.ctx = tem_init(cfg, ptrs[sc.rank])
         self.loss = torch.zeros(sc.local_ranks, 4, dtype=torch.float32, device=self.dev)
@@ -346,8 +361,14 @@ class TemSession:
 
     # -- views into caller-owned memory
     def _heap(self, l: int) -> torch.Tensor:
-        h = self.heaps[l]
-        return h[self.heap_off[l]: self.heap_off[l] + self.sym_bytes]
+        if len(self.heaps) > self.sc.local_ranks:  # virtual peers: local rank 0 is sc.rank
+            l = self.sc.rank + l
+        return self._heap_of(l)
+
+    def _heap_of(self, r: int) -> torch.Tensor:
+        """Heap of global rank r (emulation / virtual peers: all heaps live in this process)."""
+        h = self.heaps[r]
+        return h[self.heap_off[r]: self.heap_off[r] + self.sym_bytes]
 
     def params(self, l: int = 0) -> torch.Tensor:
         return self._heap(l)[: 4 * self.Kpad].view(torch.float32)
