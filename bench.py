@@ -28,20 +28,24 @@ sys.path.insert(0, ROOT)
 
 METRIC = "TEM train samples/sec at 1/2/4/8 B200; ring-allreduce bus GB/s vs NCCL"
 UNIT = "samples/s"
+# the fp32 path's arithmetic: fp32 inputs split x = hi + lo (bf16 each), products hi*hi + hi*lo +
+# lo*hi on the tensor cores, fp32 accumulation (R16); the line's "parity" object
+# carries its measured per-tensor error against the fp64 oracle
+F32 = "f32 (bf16x3 split products, f32 accumulate)"
 WORKLOADS = {
     "c1": dict(desc="configs[0]: BSN TEM (400->512->512->3 conv1d, T=100) one data-parallel SGD step, "
-                    "batch 4/rank, fp32", B=4, prec=0, dtype="f32"),
+                    "batch 4/rank, fp32", B=4, prec=0, dtype=F32),
     "c2": dict(desc="configs[1]: BSN TEM fp32 training, batch 16/GPU, synthetic ActivityNet-shaped "
-                    "features", B=16, prec=0, dtype="f32"),
+                    "features", B=16, prec=0, dtype=F32),
     "c3": dict(desc="configs[2]: BSN TEM bf16-operand/fp32-accumulate training, batch 256/GPU", B=256,
                prec=1, dtype="bf16 operands, f32 accumulate"),
     "c5": dict(desc="configs[4]: BSN TEM + PEM (proposal evaluation MLP 32->512->1 over 32-d BSP features) "
                     "joint data-parallel training, fp32, batch 16 videos/GPU x 128 proposals", B=16, prec=0,
-               dtype="f32", pem=128),
+               dtype=F32, pem=128),
     "c6": dict(desc="configs[4] with PGM: BSN TEM + PGM + PEM joint data-parallel training, fp32, batch 16 "
                     "videos/GPU; PEM trained on the 128 best proposals PGM generates from the step's own TEM "
                     "output (BSP features, IoU targets vs the ground-truth instances)", B=16, prec=0,
-               dtype="f32", pem=128, pgm=3),
+               dtype=F32, pem=128, pgm=3),
 }
 T, CIN, C = 100, 400, 512
 # Algorithmic FLOPs per sample of each kernel (dense count incl. zero-pad taps).
@@ -156,97 +160,164 @@ def bind_to_gpu_numa(index: int):
     return None
 
 
-def cpu_baseline(workload: dict, videos: int):
-    """The oracle as it stands (plain single-threaded C++, fp64 / bf16-emulated fp64) timed on a
-    bounded sample of the same workload: `videos` videos of forward+loss+backward, plus the
-    fp32 ring replay of the 1,403,395-element gradient at N=2."""
+def host_info():
+    """the host the CPU oracle ran on."""
+    model = "?"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "affinity_cores": len(os.sched_getaffinity(0)), "cpu_model": model}
+
+
+def oracle_step(workload: dict, x, lab, p, threads: int, pp=None, extra=None):
+    """One rank-step of the oracle as it stands: TEM fwd + loss + bwd over the videos (threaded
+    over videos when threads > 1), PGM/PEM for the joint workloads, and the fp32 owner update
+    replay of the K_pad-element vector at N = 1."""
     import numpy as np
+    import datagen
+    import oracle
+    B = x.shape[0]
+    ref = oracle.tem_fwd_bwd(x, p, lab, prec=workload["prec"], threads=threads)
+    P = workload.get("pem", 0)
+    if P and workload.get("pgm"):
+        gt, n = extra
+        prob = (1.0 / (1.0 + np.exp(-np.asarray(ref["z"], np.float64).reshape(B, T, 3)))).transpose(0, 2, 1)
+        pg = oracle.pgm(prob.astype(np.float32), gt, n, P)
+        oracle.pem_fwd_bwd(pg["features"].reshape(B * P, datagen.PEM_F), pp, pg["iou"].ravel())
+    elif P:
+        f, g = extra
+        oracle.pem_fwd_bwd(f, pp, g)
+    grad = np.zeros((1, oracle.kpad(ref["grad"].size, 1)), np.float32)
+    grad[0, :ref["grad"].size] = ref["grad"]
+    oracle.ring_sgd(grad, np.zeros(grad.shape[1], np.float32), 0.01)
+    return ref
+
+
+def workload_extra(workload, B, rank=0, batch_idx=0):
+    import datagen
+    P = workload.get("pem", 0)
+    if P and workload.get("pgm"):
+        return datagen.instances(B, rank=rank, batch_idx=batch_idx)
+    if P:
+        return (datagen.bsp_features(B, P, rank=rank, batch_idx=batch_idx).reshape(B * P, datagen.PEM_F),
+                datagen.iou_targets(B, P, rank=rank, batch_idx=batch_idx).ravel())
+    return None
+
+
+def cpu_baseline(workload: dict, videos: int):
+    """The oracle as it stands (plain C++, fp64 / bf16-emulated fp64) timed on a bounded sample of
+    the same workload -- `videos` videos of one rank-step -- once on one core and once threaded
+    over videos on every core this process may use."""
     import datagen
     import oracle
     oracle.lib()
     x = datagen.features(videos, rank=0, batch_idx=0)
     lab = datagen.labels(videos, rank=0, batch_idx=0)
     p = datagen.init_params()
-    t0 = time.perf_counter()
-    ref = oracle.tem_fwd_bwd(x, p, lab, prec=workload["prec"])
-    P = workload.get("pem", 0)
-    if P and workload.get("pgm"):
-        gt, n = datagen.instances(videos)
-        prob = (1.0 / (1.0 + np.exp(-np.asarray(ref["z"], np.float64).reshape(videos, T, 3)))).transpose(0, 2, 1)
-        pg = oracle.pgm(prob.astype(np.float32), gt, n, P)
-        oracle.pem_fwd_bwd(pg["features"].reshape(videos * P, datagen.PEM_F), datagen.init_pem_params(),
-                           pg["iou"].ravel())
-    elif P:
-        oracle.pem_fwd_bwd(datagen.bsp_features(videos).reshape(videos * P, datagen.PEM_F),
-                           datagen.init_pem_params(), datagen.iou_targets(videos).ravel())
-    g = np.zeros((2, oracle.kpad(1403395, 2)), np.float32)
-    oracle.ring_sgd(g, np.zeros(g.shape[1], np.float32), 0.01)
-    dt = time.perf_counter() - t0
-    return {"value": videos / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{videos} videos ({'fp64' if workload['prec'] == 0 else 'bf16-emulated fp64'} "
-                      f"fwd+loss+bwd, T=100, 400->512->512->3"
-                      + (f", + PEM over {workload['pem']} proposals each" if workload.get("pem") else "")
-                      + (", + PGM" if workload.get("pgm") else "")
-                      + f") + fp32 ring/SGD replay of K=1403395 at N=2; {dt:.1f} s single-threaded"}
+    pp = datagen.init_pem_params() if workload.get("pem") else None
+    extra = workload_extra(workload, videos)
+    prec = "fp64" if workload["prec"] == 0 else "bf16-emulated fp64"
+    what = (f"{videos} videos ({prec} fwd+loss+bwd, T=100, 400->512->512->3"
+            + (f", + PEM over {workload['pem']} proposals each" if workload.get("pem") else "")
+            + (", + PGM" if workload.get("pgm") else "") + ") + fp32 owner-update replay of the K_pad vector")
+    cores = len(os.sched_getaffinity(0))
+    out = {}
+    for key, n in (("one", 1), ("all", cores)):
+        t0 = time.perf_counter()
+        oracle_step(workload, x, lab, p, n, pp, extra)
+        dt = time.perf_counter() - t0
+        out[key] = {"value": videos / dt, "unit": UNIT, "cores": n, "kind": "oracle",
+                    "sample": f"{what}; {dt:.1f} s on {n} core(s)" + ("" if n == 1 else " (threaded over videos)")}
+    return out
 
 
 def run_reference(args, workload):
-    """--impl reference: the CPU oracle on this arm's config/metric/unit (rank 0 only); for the
-    joint workload each video also runs the PEM oracle over its proposals."""
+    """--impl reference: the CPU oracle as it stands on this arm's config, metric and unit (rank 0
+    only): each step is one rank-step of the workload -- the whole batch of B videos (threaded
+    over videos on every core this process may use), the joint modules, the owner update."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    import numpy as np
     import datagen
     import oracle
     oracle.lib()
     p = datagen.init_params()
-    per_step = 1  # one video of the workload per step: a bounded sample
-    x = datagen.features(per_step, rank=0, batch_idx=0)
-    lab = datagen.labels(per_step, rank=0, batch_idx=0)
-    P = workload.get("pem", 0)
-    if P:
-        pp = datagen.init_pem_params()
-        fb = datagen.bsp_features(per_step).reshape(per_step * P, datagen.PEM_F)
-        gb = datagen.iou_targets(per_step).ravel()
-
-    if P and workload.get("pgm"):
-        gt, n = datagen.instances(per_step)
-
-    def one():
-        ref = oracle.tem_fwd_bwd(x, p, lab, prec=workload["prec"])
-        if P and workload.get("pgm"):
-            z = np.asarray(ref["z"], np.float64).reshape(per_step, T, 3)
-            prob = (1.0 / (1.0 + np.exp(-z))).transpose(0, 2, 1).astype(np.float32)
-            pg = oracle.pgm(prob, gt, n, P)
-            oracle.pem_fwd_bwd(pg["features"].reshape(per_step * P, datagen.PEM_F), pp, pg["iou"].ravel())
-        elif P:
-            oracle.pem_fwd_bwd(fb, pp, gb)
+    B = workload["B"]
+    x = datagen.features(B, rank=0, batch_idx=0)
+    lab = datagen.labels(B, rank=0, batch_idx=0)
+    pp = datagen.init_pem_params() if workload.get("pem") else None
+    extra = workload_extra(workload, B)
+    cores = len(os.sched_getaffinity(0))
     for _ in range(args.warmup):
-        one()
+        oracle_step(workload, x, lab, p, cores, pp, extra)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        one()
+        oracle_step(workload, x, lab, p, cores, pp, extra)
     dt = time.perf_counter() - t0
-    v = per_step * args.steps / dt
+    v = B * args.steps / dt
+    prec = "fp64" if workload["prec"] == 0 else "bf16-emulated fp64"
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic", "config": {"workload": workload["desc"], "batch_per_gpu": workload["B"],
+           "data": "synthetic", "config": {"workload": workload["desc"], "batch_per_gpu": B,
                                            "seq_len": T, "parallelism": f"dp{args.gpus}"},
-           "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                            "sample": f"{per_step} video per step, {args.steps} steps, single-threaded "
-                                      f"C++ oracle ({'fp64' if workload['prec'] == 0 else 'bf16-emulated fp64'})"},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                            "sample": f"the whole {B}-video batch per step ({prec} C++ oracle threaded over "
+                                      f"videos, + the fp32 owner-update replay), {args.steps} steps"},
+           "host": host_info(),
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
     return 0
 
 
+def parity_check(sess, workload, x, lab, extra_dev=None):
+    """The timed path's numerics on one batch, for the record: per-tensor max|gpu - oracle| /
+    max|oracle| of the gradient, logits and loss against the oracle (fp64, or bf16-emulated
+    fp64 for configs[2]) at the current weights; ReLU decisions inside the oracle's rounding band
+    follow the GPU (reading R7b)."""
+    import numpy as np
+    import torch
+    import oracle
+    B = x.shape[0]
+    prec = workload["prec"]
+    w = sess.params(0).cpu().numpy()[:sess.K].copy()
+    xd = torch.from_numpy(x).cuda() if prec == 0 else None
+    if prec == 1:
+        import datagen
+        xd = torch.from_numpy(datagen.to_bf16_bits(x).view(np.int16)).cuda()
+    sess.compute(xd[None], torch.from_numpy(lab).cuda()[None])
+    sess.sync()
+    g = sess.local_grad(0).cpu().numpy()[:sess.K]
+    z = sess.logits(0).cpu().numpy()
+    loss = sess.loss[0].cpu().numpy()
+    dec = sess.relu_decisions(0).cpu().numpy()
+    cores = len(os.sched_getaffinity(0))
+    taus = (2.0 ** -13, 2.0 ** -13) if prec == 0 else (2.0 ** -13, 2.0 ** -8)
+    ref = oracle.tem_fwd_bwd(x, w, lab, prec=prec, kink_tau=taus, kinks_cap=1 << 24, threads=cores)
+    diff = np.nonzero(dec != ref["decisions"])[0]
+    inside = bool(np.all(np.isin(diff, ref["kinks"])))
+    if diff.size:
+        ref = oracle.tem_fwd_bwd(x, w, lab, prec=prec, flips=diff, threads=cores)
+    err = {}
+    for name, sl in oracle.param_slices().items():
+        err[name] = float(np.abs(g[sl] - ref["grad"][sl]).max() / np.abs(ref["grad"][sl]).max())
+    err["z"] = float(np.abs(z - ref["z"]).max() / np.abs(ref["z"]).max())
+    err["loss"] = float(np.abs(loss - ref["loss"]).max() / np.abs(ref["loss"]).max())
+    tol = 1e-4 if prec == 0 else 2e-2
+    return {"rel_err": err, "tol": tol, "pass": all(v <= tol for v in err.values()) and inside,
+            "relu_flips": int(diff.size), "relu_decisions": int(dec.size), "batch": f"{B} videos, pool batch 0",
+            "norm": "per tensor max|gpu-oracle| / max|oracle| (DESIGN.md R17)"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=30)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--pool", type=int, default=8, help="resident input batches per rank")
@@ -410,19 +481,15 @@ def main():
         for i in range(2):
             host_step(i)
         torch.cuda.synchronize()
-        # One span over all K steps (the library copies step k+1's inputs on its copy stream while
-        # step k computes, so per-step spans would not see the copies); the L2 flush between
-        # steps stays, bracketed by its own events and subtracted from the span.
-        fev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        # One span over all K steps: the library copies step k+1's inputs on its copy stream while
+        # step k computes, so per-step spans would not see the copies.  No L2 flush inside the
+        # span (a flush between steps would hide copy time under a subtracted interval); every
+        # step's inputs arrive fresh by H2D copy.
         e_beg, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         torch.cuda.synchronize()
         e_beg.record(stream)
         for i in range(args.steps):
-            if i > 0:
-                fev[i][0].record(stream)
-                flush.zero_()
-                fev[i][1].record(stream)
             host_step(i)
         e_end.record(stream)
         torch.cuda.synchronize()
@@ -430,7 +497,7 @@ def main():
         code, _ = sess.sync()
         if code != 0:
             raise tem.TemError(code, "e2e steps")
-        span = e_beg.elapsed_time(e_end) - sum(a.elapsed_time(b) for a, b in fev[1:])
+        span = e_beg.elapsed_time(e_end)
         t2 = torch.tensor([span], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t2, op=dist.ReduceOp.MAX)
@@ -441,9 +508,9 @@ def main():
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(loss_h.numel() * 4),
                "api": "tem_step_pem_host" if P else "tem_step_host",
                "host_cores_bound": numa_cores,
-               "timing": "one event span over the K steps minus the L2-flush spans between them; "
-                         "each step's H2D copies run on the library's copy stream (double-buffered "
-                         "staging) beside the previous step's compute, its loss D2H inside the step"}
+               "timing": "one event span over the K steps (no L2 flush inside it); each step's H2D copies "
+                         "run on the library's copy stream (double-buffered staging) beside the previous "
+                         "step's compute, its loss D2H inside the step"}
 
     # ---------------- roofline of the dominant kernel ----------------
     peaks, peak_src = load_peaks()
@@ -461,14 +528,16 @@ def main():
                     "peak_source": f"FP32 FMA: 148 SM x 128 lanes x 2 x {peaks['sm_max_mhz']:.0f} MHz "
                                    f"(sm_max_mhz, {peak_src}) -- DESIGN.md 7"}
         else:
-            key = "bf16_tflops_sustained"
-            bf16 = peaks.get(key, peaks.get("bf16_tflops"))
+            # the slot is one kernel timed alone for ~20 us: the BURST bf16 peak applies
+            # (B200_PROFILING.md), not the sustained one of a long back-to-back run
+            key = "bf16_tflops"
+            bf16 = peaks.get(key)
             # fp32 path: three bf16 products per fp32 MAC (hi*hi + hi*lo + lo*hi, R16)
             peak = bf16 if prec == 1 else bf16 / 3.0
             roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                     "frac": achieved / peak, "traffic": None,
-                    "peak_source": f"{key} ({peak_src})" + ("" if prec == 1 else
-                                                            " / 3 (3 bf16 tensor-core products per fp32 MAC, DESIGN.md R16)")}
+                    "peak_source": f"{key} (burst, {peak_src}: the slot is one isolated ~20 us kernel)" +
+                                   ("" if prec == 1 else " / 3 (3 bf16 tensor-core products per fp32 MAC, DESIGN.md R16)")}
         tr = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tr):
             try:
@@ -520,7 +589,13 @@ def main():
         },
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(wl, args.cpu_videos)
+        cb = cpu_baseline(wl, args.cpu_videos)
+        out["cpu_baseline"] = cb["one"]
+        out["cpu_baseline_all_cores"] = cb["all"]
+        out["host"] = host_info()
+        if not P:
+            out["parity"] = parity_check(sess, wl, datagen.features(B, rank=0, batch_idx=0),
+                                         datagen.labels(B, rank=0, batch_idx=0))
     if rank == 0:
         print(json.dumps(out), flush=True)
     sess.close()
