@@ -62,6 +62,18 @@ inline int64_t pem_num_params_of(const Geom& g) {
     return g.pem_P > 0 ? (int64_t)g.pem_H * g.pem_F + 2 * (int64_t)g.pem_H + 1 : 0;
 }
 
+// Owner update (tem_step exchanges): SGD, or Adam with per-rank moments (reading R22).
+struct OptCfg {
+    int kind;  // TEM_OPT_SGD / TEM_OPT_ADAM
+    float lr, beta1, beta2, c1, c2, eps;  // c1 = fl(1 - beta1), c2 = fl(1 - beta2)
+    float mu;                             // momentum (TEM_OPT_MOMENTUM)
+};
+struct OptState {
+    float* m;           // [K_pad] first moments / momentum buffer (each rank touches only the blocks it owns)
+    float* v;           // [K_pad] second moments
+    const float* scal;  // [beta1^t, beta2^t] of this step (opt_scalars_kernel, before the exchange)
+};
+
 // One kernel path: tcgen05/TMA bf16 tensor-core GEMMs, one plane of bf16 operands (TEM_BF16)
 // or hi/lo planes (TEM_FP32, 3-pass split).  (The round-1 CUDA-core path was removed: no
 // multi-backend dispatch in the product library.)
@@ -94,9 +106,17 @@ struct RankBufs {
     float* wpart;         // [S][max(C*3*Cin + C, C*3*C + C)] split-K partials (conv1 wgrad; SIMT: both)
     float* wpart2;        // [S][C*3*C + C] split-K partials of the tcgen05 conv2 wgrad
     int64_t* stepctr;     // step counter for NONFINITE reporting
-    __nv_bfloat16* shadow;     // [Kpad] bf16 weights (hi plane) or nullptr
-    __nv_bfloat16* shadow_lo;  // [Kpad] residual plane (UMMA fp32) or nullptr
+    // bf16 operand copies of the weights, TWO sets [2][Kpad] (ping-pong): a step's GEMMs read
+    // set `wset` while its updates write set 1 - wset, so an update may run while a GEMM of
+    // the same step still reads the old weights
+    __nv_bfloat16* shadow;     // hi plane, set 0 (set 1 at + shadow_set)
+    __nv_bfloat16* shadow_lo;  // residual plane (fp32 path) or nullptr
+    int64_t shadow_set;        // elements between the sets (K_pad)
 };
+inline __nv_bfloat16* shadow_hi(const RankBufs& b, int set) { return b.shadow + set * b.shadow_set; }
+inline __nv_bfloat16* shadow_lo(const RankBufs& b, int set) {
+    return b.shadow_lo ? b.shadow_lo + set * b.shadow_set : nullptr;
+}
 
 // --- tcgen05 path (tem_umma.cu) ---------------------------------------------------------
 enum UmmaMode { FWD_ = 0, DGRAD_ = 1, WGRAD_ = 2 };
@@ -123,6 +143,8 @@ struct UmmaParams {
     int ones_chunk;      // WGRAD: chunk slot 3*cpj reads the all-ones map (bias gradient column)
     int slot;            // trace / timing slot (Slot)
     int side;            // 1: launched on the side branch (low priority)
+    int no_pdl;          // 1: launched without programmatic dependent launch (its CTAs would sit
+                         // on SMs the concurrent side branch could use while waiting)
     // conv2 FWD with the fused head (fp32 single-wave path, clusters of ntiles CTAs):
     int fused_head;
     CUtensorMap out2[2];   // dA2 hi / lo store maps
@@ -136,11 +158,11 @@ struct UmmaParams {
 };
 struct UmmaPlan {
     UmmaParams conv1, conv2, dgrad, wgrad1, wgrad2;
+    CUtensorMap wmap[3][2][2];  // B maps of conv1 (W1), conv2 (W2), dgrad (W2) [set][plane]
     int npass, bn_fwd, S, ksplit_rows;
     int S1, S2;  // split-K factors of conv1 / conv2 wgrad (<= S, the workspace's)
     cudaStream_t aux;         // second stream: conv2 wgrad runs beside conv2 dgrad / conv1 wgrad
     cudaEvent_t fork, join;
-    cudaEvent_t dgrad_done;   // N = 1 split update: the W2.. range starts once conv2 dgrad has read W2
     cudaStream_t pem;         // third stream: the PEM (configs[4]) beside the whole TEM step
     cudaEvent_t pem_fork, pem_join;
     bool pem_pending;         // a PEM launch on `pem` awaits its join before the exchange
@@ -186,9 +208,11 @@ cudaError_t empty_shard_compute(const Geom& g, const RankBufs& b, const float* l
 // split: (bucketed exchange, N > 1) the [bnd, K_pad) bucket's exchange is launched on the side
 // branch once conv2 dgrad is done, beside conv1 wgrad (reading R25).
 struct SplitUpdate;
+// wset: the operand set (RankBufs::shadow) of the weights this step reads.  defer_reduce (N = 1
+// tem_step): the split-K partials are left for the update kernel, which sums them itself.
 cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, const float* labels,
                          const float lam[3], float* loss_out, Status* status, int* nlaunch,
-                         const EvRec& rec, cudaStream_t s, bool defer_reduce = false,
+                         const EvRec& rec, cudaStream_t s, int wset, bool defer_reduce = false,
                          float* loss_host = nullptr, const SplitUpdate* split = nullptr);
 // head (conv3 + sigmoid + loss + dz + dA2) and its deterministic finalisation (rows a3-a5);
 // writes dA2 as b.dA2 (+ b.dA2_lo when present) in the operand type of the path.
@@ -210,17 +234,6 @@ cudaError_t launch_head_reduce(const Geom& g, const RankBufs& b, const float lam
 cudaError_t launch_reduce_splits(const float* part, float* dst, int64_t n, int S, cudaStream_t s);
 
 // --- ring / exchange (ring.cu) --------------------------------------------------------
-// Owner update (tem_step exchanges): SGD, or Adam with per-rank moments (reading R22).
-struct OptCfg {
-    int kind;  // TEM_OPT_SGD / TEM_OPT_ADAM
-    float lr, beta1, beta2, c1, c2, eps;  // c1 = fl(1 - beta1), c2 = fl(1 - beta2)
-    float mu;                             // momentum (TEM_OPT_MOMENTUM)
-};
-struct OptState {
-    float* m;           // [K_pad] first moments / momentum buffer (each rank touches only the blocks it owns)
-    float* v;           // [K_pad] second moments
-    const float* scal;  // [beta1^t, beta2^t] of this step (opt_scalars_kernel, before the exchange)
-};
 struct RingParams;
 struct SplitUpdate {
     OptCfg oc;
@@ -258,11 +271,11 @@ struct RingParams {
 };
 cudaError_t launch_ring(const RingParams& p, cudaStream_t s);
 cudaError_t launch_twoshot(const RingParams& p, cudaStream_t s);  // NVSwitch two-shot (NEXT #3(i))
-// N = 1 owner update with the deferred split-K reductions fused in: grad[e] = sum_s part1[s][e]
-// (W1, b1), sum_s part2[s][e - off2] (W2), or grad[e] (the head-written entries); the same
-// ascending-s order as reduce_wgrad_kernel, so the result is bit-identical to the unfused path.
-// Owner update of elements [e0, e1) at N = 1 with the split-K partial sums fused (p1 covers
-// [0, n1), p2 covers [off2, off2 + n2)); e0, e1 multiples of 4.
+// Owner update of elements [e0, e1) at N = 1 (e0, e1 multiples of 4): the gradient is
+// sum_s part1[s][e] on [0, n1), sum_s part2[s][e - off2] on [off2, off2 + n2) (split-K partials in
+// ascending s, the order of the fused WGRAD reduction), else grad[e].  mode 1: update (and store
+// the summed partials into grad), 2: update only, 0: only sum the partials into grad
+// (tem_local_grad after an N = 1 tem_step, whose W1 / W2 gradient exists only as partials).
 cudaError_t launch_sgd_fused(float* g, float* w, __nv_bfloat16* shadow, __nv_bfloat16* shadow_lo, int64_t e0,
                              int64_t e1, const OptCfg& oc, const OptState& os, const float* p1, int64_t stride1, int64_t n1,
                              int S1, const float* p2, int64_t stride2, int64_t off2, int64_t n2, int S2,

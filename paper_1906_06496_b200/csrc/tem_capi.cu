@@ -158,6 +158,8 @@ HeapLayout heap_layout(const tem_config* c) {
     return h;
 }
 
+int64_t shadow_set_elems(const Geom& g) { return roundup(g.Kpad, 256); }
+
 WsLayout ws_layout(const tem_config* c) {
     const Geom g = make_geom(c);
     const size_t esz = 2;                           // operand planes are bf16
@@ -191,8 +193,9 @@ WsLayout ws_layout(const tem_config* c) {
     w.wpart2 = take((size_t)S * ((size_t)g.C * 3 * g.C + g.C) * 4);
     w.pempart = take((size_t)pem_ctas(g) * (pem_num_params_of(g) + 1) * 4);
     w.pemdec = take(g.pem_P > 0 ? (size_t)g.B * g.pem_P * g.pem_H : 0);  // last ReLU decisions (tests)
-    w.shadow = take((size_t)g.Kpad * 2);
-    w.shadow_lo = take(lo * (size_t)g.Kpad * 2);
+    // two operand sets (ping-pong, RankBufs::shadow), each 512-byte aligned (TMA bases)
+    w.shadow = take(2 * (size_t)shadow_set_elems(g) * 2);
+    w.shadow_lo = take(lo * 2 * (size_t)shadow_set_elems(g) * 2);
     w.ones = take((size_t)g.R * 128 * 2);
     w.zpart = take((size_t)(g.C / 64) * g.R * 3 * 4);
     w.epochs = take((size_t)kMaxChannels * 4);
@@ -243,6 +246,8 @@ struct tem_ctx {
     Status* st_dev;
     int launches_step, launches_exchange;
     bool alive;
+    int wpar;              // operand set (RankBufs::shadow) holding the current weights: a step's
+                           // GEMMs read it, its update writes 1 - wpar, then it flips
     bool reduce_deferred;  // last compute left the split-K partials for the fused N = 1 exchange
     bool early_done;       // bucketed exchange: the [bnd, K_pad) bucket ran inside the compute
     bool grad_lazy;        // N = 1 tem_step left the W1 / W2 gradient as split-K partials only;
@@ -266,6 +271,7 @@ struct tem_ctx {
         const void* iou;
         const void* gt;
         const void* ngt;
+        int wpar;
         void* loss;
         void* loss_host;
         cudaGraphExec_t exec;
@@ -293,7 +299,8 @@ tem_status graph_step(tem_ctx* c, const void* x, const void* lab, void* loss, cu
     for (int i = 0; i < c->ngraphs; ++i)
         if (c->graphs[i].x == x && c->graphs[i].lab == lab && c->graphs[i].loss == loss &&
             c->graphs[i].loss_host == c->loss_host_pending && c->graphs[i].bsp == c->pem_bsp &&
-            c->graphs[i].iou == c->pem_iou && c->graphs[i].gt == c->pgm_gt && c->graphs[i].ngt == c->pgm_ngt)
+            c->graphs[i].iou == c->pem_iou && c->graphs[i].gt == c->pgm_gt && c->graphs[i].ngt == c->pgm_ngt &&
+            c->graphs[i].wpar == c->wpar)
             e = &c->graphs[i];
     if (!e) {
         if (c->ngraphs == tem_ctx::kMaxGraphs) {  // evict the oldest
@@ -326,6 +333,7 @@ tem_status graph_step(tem_ctx* c, const void* x, const void* lab, void* loss, cu
         e->iou = c->pem_iou;
         e->gt = c->pgm_gt;
         e->ngt = c->pgm_ngt;
+        e->wpar = c->wpar;
         e->exec = exec;
         e->launches = nl;
         e->grad_lazy = c->grad_lazy;
@@ -452,6 +460,7 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
         b.dA1_lo = c->g.split ? base + wl.dA1_lo : nullptr;
         b.shadow = (__nv_bfloat16*)(base + wl.shadow);
         b.shadow_lo = c->g.split ? (__nv_bfloat16*)(base + wl.shadow_lo) : nullptr;
+        b.shadow_set = shadow_set_elems(c->g);
         c->plan[l] = nullptr;
         c->epochs[l] = (uint32_t*)(base + wl.epochs);
         cudaError_t e = cudaMemsetAsync(base, 0, wl.per_rank, 0);
@@ -481,6 +490,7 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
     c->launches_step = 0;
     c->launches_exchange = 0;
     c->ngraphs = 0;
+    c->wpar = 0;  // tem_init cast the weights into set 0
     // graphs: one rank per process only (the emulation's cooperative launch is not captured)
     const char* ng = getenv("TEM_NO_GRAPH");
     c->use_graphs = c->nlocal == 1 && !(ng && ng[0] == '1');
@@ -560,8 +570,9 @@ static RingParams step_ring(tem_ctx* c, int64_t e0, int64_t e1) {
     memset(&p, 0, sizeof(p));
     for (int l = 0; l < c->nlocal; ++l) {
         const RankBufs& b = c->rb[l];
-        p.loc[l] = ring_local(c, l, b.grad + e0, (float*)b.params + e0, b.shadow ? b.shadow + e0 : nullptr,
-                              b.shadow_lo ? b.shadow_lo + e0 : nullptr);
+        __nv_bfloat16* sl = shadow_lo(b, 1 - c->wpar);  // the update writes the other operand set
+        p.loc[l] = ring_local(c, l, b.grad + e0, (float*)b.params + e0, shadow_hi(b, 1 - c->wpar) + e0,
+                              sl ? sl + e0 : nullptr);
         if (p.loc[l].opt.m) p.loc[l].opt.m += e0;
         if (p.loc[l].opt.v) p.loc[l].opt.v += e0;
     }
@@ -583,6 +594,7 @@ static cudaError_t launch_step_ring(tem_ctx* c, const RingParams& p, cudaStream_
     return c->cfg.exchange == TEM_EXCHANGE_TWOSHOT ? launch_twoshot(p, s) : launch_ring(p, s);
 }
 
+// fuse_reduce (tem_step): at N = 1 the split-K reductions are left to the update kernel
 static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, float* loss_out,
                                cudaStream_t s, int* nl, bool fuse_reduce = false) {
     const EvRec rec{timing_slot_events(c), s};
@@ -601,8 +613,6 @@ static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, f
         const bool defer = fuse_reduce && c->N == 1 && g.B > 0;
         c->reduce_deferred = defer;
         c->grad_lazy = false;  // this compute's partials overwrite the last step's
-        // (updating [off_W2, K_pad) at N = 1 on the side branch beside conv1 wgrad measured 2-14 %
-        // slower at c2 and was removed)
         SplitUpdate su{opt_cfg(c), opt_state(c, l)};
         // bucketed exchange with one rank per process: the [bnd, K_pad) bucket starts inside the
         // compute (not with PGM-fed PEM, whose gradient is produced after it)
@@ -626,8 +636,8 @@ static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, f
             if (e != cudaSuccess) return TEM_ERR_CUDA;
         }
         if (g.B > 0) {
-            e = umma_compute(g, c->rb[l], *c->plan[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s, defer, lh,
-                             c->early_done ? &su : nullptr);
+            e = umma_compute(g, c->rb[l], *c->plan[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s, c->wpar,
+                             defer, lh, c->early_done ? &su : nullptr);
             if (lh) c->loss_host_done = true;
         } else {
             e = empty_shard_compute(g, c->rb[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s);
@@ -686,15 +696,16 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
     const EvRec rec{timing_slot_events(c), s};
     rec.begin(SLOT_EXCHANGE);
     const OptCfg oc = opt_cfg(c);
+    const int wr = 1 - c->wpar;  // every update writes the other operand set (RankBufs::shadow)
     if (c->N == 1 && c->reduce_deferred) {  // tem_step: split-K reductions fused into the update
         const RankBufs& b = c->rb[0];
         const UmmaPlan& P = *c->plan[0];
         c->reduce_deferred = false;
         // the summed W1 / W2 gradient is not stored (5.6 MB of writes): tem_local_grad rebuilds
         // it from the partials on demand, in the same order
-        if (launch_sgd_fused(b.grad, (float*)b.params, b.shadow, b.shadow_lo, 0, g.Kpad, oc, opt_state(c, 0), b.wpart,
-                             P.wgrad1.part_stride, g.off_W2, P.S1, b.wpart2, P.wgrad2.part_stride, g.off_W2,
-                             (int64_t)3 * g.C * g.C, P.S2, s, false, 0, 2) != cudaSuccess)
+        if (launch_sgd_fused(b.grad, (float*)b.params, shadow_hi(b, wr), shadow_lo(b, wr), 0, g.Kpad, oc,
+                             opt_state(c, 0), b.wpart, P.wgrad1.part_stride, g.off_W2, P.S1, b.wpart2,
+                             P.wgrad2.part_stride, g.off_W2, (int64_t)3 * g.C * g.C, P.S2, s, false, 0, 2) != cudaSuccess)
             return TEM_ERR_CUDA;
         c->grad_lazy = true;
         ++*nl;
@@ -703,8 +714,8 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
     }
     if (c->N == 1) {
         for (int l = 0; l < c->nlocal; ++l) {
-            if (launch_sgd_single(c->rb[l].grad, (float*)c->rb[l].params, c->rb[l].shadow, c->rb[l].shadow_lo, g.Kpad,
-                                  TEM_MEAN, oc, opt_state(c, l), s) != cudaSuccess)
+            if (launch_sgd_single(c->rb[l].grad, (float*)c->rb[l].params, shadow_hi(c->rb[l], wr),
+                                  shadow_lo(c->rb[l], wr), g.Kpad, TEM_MEAN, oc, opt_state(c, l), s) != cudaSuccess)
                 return TEM_ERR_CUDA;
             ++*nl;
         }
@@ -726,7 +737,8 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
     RingParams p;
     memset(&p, 0, sizeof(p));
     for (int l = 0; l < c->nlocal; ++l)
-        p.loc[l] = ring_local(c, l, c->rb[l].grad, (float*)c->rb[l].params, c->rb[l].shadow, c->rb[l].shadow_lo);
+        p.loc[l] = ring_local(c, l, c->rb[l].grad, (float*)c->rb[l].params, shadow_hi(c->rb[l], wr),
+                              shadow_lo(c->rb[l], wr));
     p.N = c->N;
     p.rank_base = c->rank;
     p.nlocal = c->nlocal;
@@ -784,6 +796,7 @@ tem_status tem_exchange(tem_ctx* c, void* stream) {
     int nl = 0;
     st = exchange_impl(c, (cudaStream_t)stream, &nl);
     c->launches_exchange = nl;
+    if (st == TEM_OK) c->wpar ^= 1;  // the update wrote the other operand set
     return st;
 }
 
@@ -793,8 +806,8 @@ tem_status tem_step(tem_ctx* c, const void* x, const float* labels, float* loss_
     if (c->g.pem_P > 0 && !c->pem_bsp) return TEM_ERR_INVALID_ARG;  // PEM config: tem_step_pem
     if ((!x || !labels) && c->g.B > 0) return TEM_ERR_INVALID_ARG;
     if (!loss_out) return TEM_ERR_INVALID_ARG;
-    if (c->use_graphs && !c->tev) {
-        return graph_step(c, x, labels, loss_out, (cudaStream_t)stream, [&](cudaStream_t gs, int* n) {
+    if (c->use_graphs && !c->tev) {  // one graph per pointer set and operand-set parity
+        st = graph_step(c, x, labels, loss_out, (cudaStream_t)stream, [&](cudaStream_t gs, int* n) {
             int a = 0, b = 0;
             tem_status r = compute_impl(c, x, labels, loss_out, gs, &a, true);
             if (r == TEM_OK) r = exchange_impl(c, gs, &b);
@@ -802,6 +815,8 @@ tem_status tem_step(tem_ctx* c, const void* x, const float* labels, float* loss_
             c->launches_exchange = b;
             return r;
         });
+        if (st == TEM_OK) c->wpar ^= 1;
+        return st;
     }
     int nl = 0;
     st = compute_impl(c, x, labels, loss_out, (cudaStream_t)stream, &nl, true);
@@ -811,6 +826,7 @@ tem_status tem_step(tem_ctx* c, const void* x, const float* labels, float* loss_
     c->launches_step = nl + ne;
     c->launches_exchange = ne;
     if (c->tev && c->t_idx < c->t_max) ++c->t_idx;
+    if (st == TEM_OK) c->wpar ^= 1;
     return st;
 }
 
@@ -1166,7 +1182,8 @@ void* tem_debug_buffer(tem_ctx* c, int32_t l, const char* name, int64_t* nbytes)
     const Item items[] = {
         {"xp", b.xp, xin}, {"h1", b.h1, act}, {"h2", b.h2, (int64_t)g.R * g.C * 4}, {"dA2", b.dA2, act},
         {"dA1", b.dA1, act}, {"xp_lo", b.xp_lo, xin}, {"h1_lo", b.h1_lo, act}, {"dA2_lo", b.dA2_lo, act},
-        {"dA1_lo", b.dA1_lo, act}, {"shadow", b.shadow, g.Kpad * 2}, {"shadow_lo", b.shadow_lo, g.Kpad * 2},
+        {"dA1_lo", b.dA1_lo, act}, {"shadow", shadow_hi(b, c->wpar), g.Kpad * 2},
+        {"shadow_lo", shadow_lo(b, c->wpar), g.Kpad * 2},
         {"pgm_prob", c->ws_base[l] + c->wl.pgm_prob, g.pgm_G > 0 ? (int64_t)g.B * 3 * g.T * 4 : 0},
         {"pgm_feat", c->ws_base[l] + c->wl.pgm_feat, g.pgm_G > 0 ? (int64_t)g.B * g.pem_P * 32 * 4 : 0},
         {"pgm_iou", c->ws_base[l] + c->wl.pgm_iou, g.pgm_G > 0 ? (int64_t)g.B * g.pem_P * 4 : 0},

@@ -1091,7 +1091,7 @@ cudaError_t launch_persistent(K k, uint32_t smem, bool pair, int total, int* max
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[3];
     int na = 0;
-    if (pdl_enabled() && !p.side) {
+    if (pdl_enabled() && !p.side && !p.no_pdl) {
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[na++].val.programmaticStreamSerializationAllowed = 1;
     }
@@ -1253,7 +1253,6 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     if (cudaStreamCreateWithFlags(&P.aux, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&P.fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&P.join, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&P.dgrad_done, cudaEventDisableTiming) != cudaSuccess ||
         cudaStreamCreateWithFlags(&P.pem, cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&P.pem_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&P.pem_join, cudaEventDisableTiming) != cudaSuccess)
@@ -1267,22 +1266,23 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     const void* h1[2] = {b.h1, b.h1_lo};
     const void* dA2[2] = {b.dA2, b.dA2_lo};
     const void* dA1[2] = {b.dA1, b.dA1_lo};
-    const __nv_bfloat16* W[2] = {b.shadow, b.shadow_lo};
     // box rows: FWD/DGRAD A = the 130-row halo window; B = this CTA's rows (a pair holds half)
     const uint32_t arK = umma::BM + 2, brK = cf.pair ? cf.bn / 2 : cf.bn;
     if (cfg_for(DGRAD_, P.npass).bn != cf.bn) return false;  // FWD and DGRAD share the n-tiling
     const uint32_t brD = umma::BK;                    // DGRAD MN-major B: 64 o-rows per box
     const uint32_t arW = umma::BK, brW = umma::BK;     // WGRAD MN-major A / B
     bool ok = true;
+    for (int set = 0; set < 2; ++set)  // weight operand maps of both ping-pong sets
+        for (int pl = 0; pl < npl; ++pl) {
+            const __nv_bfloat16* W = pl == 0 ? shadow_hi(b, set) : shadow_lo(b, set);
+            ok &= map2d(&P.wmap[0][set][pl], W + g.off_W1, 3 * (uint64_t)g.Cin, g.C, brK);
+            ok &= map2d(&P.wmap[1][set][pl], W + g.off_W2, 3 * (uint64_t)g.C, g.C, brK);
+            ok &= map_w_mn(&P.wmap[2][set][pl], W + g.off_W2, g.C, brD);
+        }
     for (int pl = 0; pl < npl; ++pl) {
-        const __nv_bfloat16* W1 = W[pl] + g.off_W1;
-        const __nv_bfloat16* W2 = W[pl] + g.off_W2;
         ok &= map2d(&P.conv1.a[pl], xp[pl], g.Cin, R, arK);
-        ok &= map2d(&P.conv1.b[pl], W1, 3 * (uint64_t)g.Cin, g.C, brK);
         ok &= map2d(&P.conv2.a[pl], h1[pl], g.C, R, arK);
-        ok &= map2d(&P.conv2.b[pl], W2, 3 * (uint64_t)g.C, g.C, brK);
         ok &= map2d(&P.dgrad.a[pl], dA2[pl], g.C, R, arK);
-        ok &= map_w_mn(&P.dgrad.b[pl], W2, g.C, brD);
         ok &= map2d(&P.wgrad2.a[pl], dA2[pl], g.C, R, arW);
         ok &= map2d(&P.wgrad2.b[pl], h1[pl], g.C, R, brW);
         ok &= map2d(&P.wgrad1.a[pl], dA1[pl], g.C, R, arW);
@@ -1366,6 +1366,7 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     P.wgrad2.part_stride = (int64_t)g.C * 3 * g.C + g.C;
     common(P.wgrad1);
     P.wgrad1.slot = SLOT_WGRAD1;
+    P.wgrad1.no_pdl = 1;  // measured: with PDL its waiting CTAs held the SMs the side branch needs
     P.wgrad1.nsplit = P.S1;
     P.wgrad1.ksplit_rows = rows1;
     P.wgrad1.Nout = g.C;
@@ -1394,7 +1395,6 @@ void umma_plan_destroy(UmmaPlan* plan) {
     if (plan->aux) cudaStreamDestroy(plan->aux);
     if (plan->fork) cudaEventDestroy(plan->fork);
     if (plan->join) cudaEventDestroy(plan->join);
-    if (plan->dgrad_done) cudaEventDestroy(plan->dgrad_done);
     if (plan->pem) cudaStreamDestroy(plan->pem);
     if (plan->pem_fork) cudaEventDestroy(plan->pem_fork);
     if (plan->pem_join) cudaEventDestroy(plan->pem_join);
@@ -1419,25 +1419,30 @@ static cudaError_t dispatch(const UmmaParams& p, int npass, cudaStream_t s) {
 
 cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, const float* labels,
                          const float lam[3], float* loss_out, Status* status, int* nl, const EvRec& rec,
-                         cudaStream_t s, bool defer_reduce, float* loss_host, const SplitUpdate* split) {
+                         cudaStream_t s, int wset, bool defer_reduce, float* loss_host,
+                         const SplitUpdate* split) {
     int n = 0;
     cudaError_t e;
+    // the weight operand maps of this step's set (ping-pong, RankBufs::shadow)
+    UmmaParams c1 = P.conv1, c2 = P.conv2, dg = P.dgrad;
+    for (int pl = 0; pl < 2; ++pl) {
+        c1.b[pl] = P.wmap[0][wset][pl];
+        c2.b[pl] = P.wmap[1][wset][pl];
+        dg.b[pl] = P.wmap[2][wset][pl];
+    }
     rec.begin(SLOT_CONV1);
-    e = dispatch<FWD_>(P.conv1, P.npass, s);
+    e = dispatch<FWD_>(c1, P.npass, s);
     rec.end(SLOT_CONV1);
     if (e != cudaSuccess) return e;
     ++n;
     rec.begin(SLOT_CONV2);
-    if (P.conv2.fused_head) {
-        UmmaParams c2 = P.conv2;  // per-call: labels and loss weights
+    if (P.conv2.fused_head) {  // per-call: labels and loss weights
         c2.labels = labels;
         c2.lam[0] = lam[0];
         c2.lam[1] = lam[1];
         c2.lam[2] = lam[2];
-        e = dispatch<FWD_>(c2, P.npass, s);
-    } else {
-        e = dispatch<FWD_>(P.conv2, P.npass, s);
     }
+    e = dispatch<FWD_>(c2, P.npass, s);
     rec.end(SLOT_CONV2);
     if (e != cudaSuccess) return e;
     ++n;
@@ -1445,9 +1450,9 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
         e = launch_head_rows(g, b, labels, lam, rec, s, &n);
         if (e != cudaSuccess) return e;
     }
-    // Fork: the head reduction and conv2 wgrad (+ its reduction) run on the aux stream
-    // alongside conv2 dgrad -> conv1 wgrad on s; all only read dA2 / h1 / xp / head
-    // partials (captured as parallel graph branches).
+    // Fork: the head reduction and conv2 wgrad (+ its reduction) run on the aux stream alongside
+    // conv2 dgrad -> conv1 wgrad on s; all only read dA2 / h1 / xp / head partials and write
+    // disjoint outputs (captured as parallel graph branches).
     // The side branch is serialised onto s for the instrumented (timing) pass -- each slot is
     // then one kernel's own duration on its stream -- and with TEM_NO_FORK (experiments).
     static const bool no_fork_env = getenv("TEM_NO_FORK") != nullptr;
@@ -1475,49 +1480,43 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     if (e != cudaSuccess) return e;
     ++n;
     if (!defer_reduce) {
-    rec2.begin(SLOT_RED2);
-    e = launch_pdl(umma::reduce_wgrad_kernel, dim3(296), dim3(256), 0, aux, true, (const float*)b.wpart2,
-                   P.wgrad2.part_stride, P.S2, (int64_t)g.C * 3 * g.C, (const float*)nullptr, 0, g.C,
-                   b.grad + g.off_W2, (int)SLOT_RED2);
-    rec2.end(SLOT_RED2);
-    if (e != cudaSuccess) return e;
-    ++n;
+        rec2.begin(SLOT_RED2);
+        e = launch_pdl(umma::reduce_wgrad_kernel, dim3(296), dim3(256), 0, aux, true, (const float*)b.wpart2,
+                       P.wgrad2.part_stride, P.S2, (int64_t)g.C * 3 * g.C, (const float*)nullptr, 0, g.C,
+                       b.grad + g.off_W2, (int)SLOT_RED2);
+        rec2.end(SLOT_RED2);
+        if (e != cudaSuccess) return e;
+        ++n;
     }
-    if (!split && !no_fork && cudaEventRecord(P.join, P.aux) != cudaSuccess) return cudaErrorUnknown;
-    rec.begin(SLOT_DGRAD);
-    e = dispatch<DGRAD_>(P.dgrad, P.npass, s);
-    rec.end(SLOT_DGRAD);
-    if (e != cudaSuccess) return e;
-    ++n;
     if (split && split->early) {
         // N > 1, exchange_buckets = 2 (reading R25): the [bnd, K_pad) bucket's exchange -- its
-        // gradient is complete once conv2 wgrad (+ reduce) and the head reduction are, and
-        // conv2 dgrad has read W2 -- on the side branch beside conv1 wgrad
-        if (!no_fork &&
-            (cudaEventRecord(P.dgrad_done, s) != cudaSuccess || cudaStreamWaitEvent(P.aux, P.dgrad_done, 0) != cudaSuccess))
-            return cudaErrorUnknown;
+        // gradient is complete once conv2 wgrad and the head reduction are -- on the side branch
+        // beside conv2 dgrad / conv1 wgrad (it writes the other operand set: no wait for dgrad)
         rec2.begin(SLOT_EXCH2);
         e = split->early_kind == TEM_EXCHANGE_TWOSHOT ? launch_twoshot(*split->early, aux) : launch_ring(*split->early, aux);
         rec2.end(SLOT_EXCH2);
         if (e != cudaSuccess) return e;
         ++n;
-        if (!no_fork && cudaEventRecord(P.join, P.aux) != cudaSuccess) return cudaErrorUnknown;
-    } else if (split && !no_fork && cudaEventRecord(P.join, P.aux) != cudaSuccess) {
-        return cudaErrorUnknown;
     }
+    if (!no_fork && cudaEventRecord(P.join, P.aux) != cudaSuccess) return cudaErrorUnknown;
+    rec.begin(SLOT_DGRAD);
+    e = dispatch<DGRAD_>(dg, P.npass, s);
+    rec.end(SLOT_DGRAD);
+    if (e != cudaSuccess) return e;
+    ++n;
     rec.begin(SLOT_WGRAD1);
     e = dispatch<WGRAD_>(P.wgrad1, P.npass, s);
     rec.end(SLOT_WGRAD1);
     if (e != cudaSuccess) return e;
     ++n;
     if (!defer_reduce) {
-    rec.begin(SLOT_RED1);
-    e = launch_pdl(umma::reduce_wgrad_kernel, dim3(296), dim3(256), 0, s, false, (const float*)b.wpart, P.wgrad1.part_stride,
-                   P.S1, (int64_t)g.C * 3 * g.Cin + g.C, (const float*)nullptr, 0, g.C, b.grad + g.off_W1,
-                   (int)SLOT_RED1);
-    rec.end(SLOT_RED1);
-    if (e != cudaSuccess) return e;
-    ++n;
+        rec.begin(SLOT_RED1);
+        e = launch_pdl(umma::reduce_wgrad_kernel, dim3(296), dim3(256), 0, s, false, (const float*)b.wpart,
+                       P.wgrad1.part_stride, P.S1, (int64_t)g.C * 3 * g.Cin + g.C, (const float*)nullptr, 0, g.C,
+                       b.grad + g.off_W1, (int)SLOT_RED1);
+        rec.end(SLOT_RED1);
+        if (e != cudaSuccess) return e;
+        ++n;
     }
     if (!no_fork && cudaStreamWaitEvent(s, P.join, 0) != cudaSuccess) return cudaErrorUnknown;  // join
     if (P.pem_pending) {  // the PEM branch (configs[4]) joins before the exchange too

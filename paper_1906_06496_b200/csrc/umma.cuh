@@ -125,6 +125,8 @@ UMMA_DEV void bulk_wait_read() {  // at most N groups still reading shared memor
 }
 UMMA_DEV void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 UMMA_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+// orders this thread's async-proxy accesses (e.g. completed bulk stores) with its later generic ones
+UMMA_DEV void fence_proxy_async_all() { asm volatile("fence.proxy.async;" ::: "memory"); }
 
 // ------------------------------------------------------------------ clusters
 UMMA_DEV uint32_t cluster_ctarank() {
