@@ -68,13 +68,17 @@ TEM_DEV uint64_t globaltimer() {
 // the loss term alpha+ b log p + alpha- (1-b) log(1-p) and dz = lam/(B T) (alpha- (1-b) p -
 // alpha+ b (1-p)).  With e = exp(-|z|): p and 1-p are 1/(1+e) and e/(1+e) (which one depends on
 // the sign of z; no cancellation), log p = -softplus(-z), log(1-p) = -softplus(z) and
-// softplus(+-z) = max(+-z, 0) + log1p(e) -- one exp and one log1p per row and channel.
+// softplus(+-z) = max(+-z, 0) + log1p(e) -- one exp and one log per row and channel, both the
+// hardware approximations (ex2 / lg2: ~2^-22 relative for exp, ~2^-21 absolute for log, and
+// log(1 + e) loses at most ~2^-24 absolute when 1 + e rounds): the loss and dz stay ~1e-7
+// relative to the fp64 oracle, far inside the 1e-4 contract, at a fraction of the latency of
+// the libm versions on this latency-bound, one-warp-per-scheduler path.
 TEM_DEV void head_row_terms(float z, float bt, float ap, float an, float lam_over_bt, float& lt, float& dz) {
-    const float e = expf(-fabsf(z));
+    const float e = __expf(-fabsf(z));
     const float r = __frcp_rn(1.f + e);
     const float er = e * r;
     const float p = z >= 0.f ? r : er, q = z >= 0.f ? er : r;  // p, 1 - p
-    const float l1 = log1pf(e);
+    const float l1 = __logf(1.f + e);
     const float logp = -(fmaxf(-z, 0.f) + l1), log1mp = -(fmaxf(z, 0.f) + l1);
     lt = ap * bt * logp + an * (1.f - bt) * log1mp;
     dz = lam_over_bt * (an * (1.f - bt) * p - ap * bt * q);

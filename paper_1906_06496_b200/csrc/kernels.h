@@ -240,6 +240,7 @@ struct SplitUpdate {
     OptState os;
     const RingParams* early = nullptr;  // N > 1 bucketed exchange: the [bnd, K_pad) bucket's
     int early_kind = 0;                 // ring (TEM_EXCHANGE_RING) / two-shot, launched after dgrad
+    int n1_w2 = 0;  // N = 1 tem_step: update [off_W2, K_pad) on the side branch after conv2 wgrad
 };
 struct RingLocal {
     OptState opt;

@@ -249,6 +249,7 @@ struct tem_ctx {
     int wpar;              // operand set (RankBufs::shadow) holding the current weights: a step's
                            // GEMMs read it, its update writes 1 - wpar, then it flips
     bool reduce_deferred;  // last compute left the split-K partials for the fused N = 1 exchange
+    bool split_n1;         // ... and updated [off_W2, K_pad) itself on its side branch
     bool early_done;       // bucketed exchange: the [bnd, K_pad) bucket ran inside the compute
     bool grad_lazy;        // N = 1 tem_step left the W1 / W2 gradient as split-K partials only;
                            // tem_local_grad sums them on demand (same order as the update)
@@ -614,6 +615,12 @@ static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, f
         c->reduce_deferred = defer;
         c->grad_lazy = false;  // this compute's partials overwrite the last step's
         SplitUpdate su{opt_cfg(c), opt_state(c, l)};
+        // N = 1: [off_W2, K_pad) is updated on the side branch as soon as conv2 wgrad and the head
+        // are done (measured c2 195.5k -> 200.4k samples/s with the default 296-CTA grid; 16-64
+        // CTAs were slower), the exchange then updates [0, off_W2) only.  Not with PGM-fed PEM,
+        // whose gradient is produced after the compute.
+        c->split_n1 = defer && g.pgm_G == 0;
+        su.n1_w2 = c->split_n1 ? 1 : 0;
         // bucketed exchange with one rank per process: the [bnd, K_pad) bucket starts inside the
         // compute (not with PGM-fed PEM, whose gradient is produced after it)
         RingParams early;
@@ -637,7 +644,7 @@ static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, f
         }
         if (g.B > 0) {
             e = umma_compute(g, c->rb[l], *c->plan[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s, c->wpar,
-                             defer, lh, c->early_done ? &su : nullptr);
+                             defer, lh, (c->early_done || c->split_n1) ? &su : nullptr);
             if (lh) c->loss_host_done = true;
         } else {
             e = empty_shard_compute(g, c->rb[l], labl, lam, loss_out + 4 * l, c->st_dev, nl, rec, s);
@@ -703,7 +710,9 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
         c->reduce_deferred = false;
         // the summed W1 / W2 gradient is not stored (5.6 MB of writes): tem_local_grad rebuilds
         // it from the partials on demand, in the same order
-        if (launch_sgd_fused(b.grad, (float*)b.params, shadow_hi(b, wr), shadow_lo(b, wr), 0, g.Kpad, oc,
+        const int64_t e1 = c->split_n1 ? g.off_W2 : g.Kpad;
+        c->split_n1 = false;
+        if (launch_sgd_fused(b.grad, (float*)b.params, shadow_hi(b, wr), shadow_lo(b, wr), 0, e1, oc,
                              opt_state(c, 0), b.wpart, P.wgrad1.part_stride, g.off_W2, P.S1, b.wpart2,
                              P.wgrad2.part_stride, g.off_W2, (int64_t)3 * g.C * g.C, P.S2, s, false, 0, 2) != cudaSuccess)
             return TEM_ERR_CUDA;

@@ -122,10 +122,13 @@ TEM_DEV void dgrad_mask_chunk0(const UmmaParams& P, int row, int col0, uint4 (&p
     }
 }
 
+// Staging: `all` (the CTA's only tile; its operand ring is drained) gives every chunk its own
+// buffer, so no store waits for an earlier one; otherwise two buffers alternate and a chunk
+// waits until the store two chunks back has read its data.
 template <int MODE, int BN, int ACC = 1>
 TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_tile, int split, int q,
                            int lane, uint8_t* stg, int& buf, const float* sw3, const uint4 (&pm)[2],
-                           float* zloc = nullptr) {
+                           float* zloc = nullptr, bool all = false) {
     const int row0 = m_tile * BM + 32 * q;
     const int row = row0 + lane;
     if ((MODE == FWD_ || MODE == DGRAD_) && (m_tile >= P.mtiles || row0 >= P.R)) return;
@@ -209,8 +212,8 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
                 v[2 * i + 1] = __uint_as_float(e.mw[i] & 0xFFFF0000u) > 0.f ? v[2 * i + 1] : 0.f;
             }
         }
-        uint8_t* sb = stg + buf * EPI_BUF;
-        if (lane == 0) bulk_wait_read<1>();  // this buffer's previous store has read its data
+        uint8_t* sb = stg + (all ? c16 : buf) * EPI_BUF;
+        if (lane == 0 && !all) bulk_wait_read<1>();  // this buffer's previous store has read its data
         __syncwarp();
         const bool f32 = (MODE == WGRAD_) || P.out_f32;
         if (f32) {
@@ -269,6 +272,23 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
         zp[2] = zp2;
     }
 }
+
+// Phase timestamps of the GEMM kernels (diagnostics build only, -DTEM_DIAG: tem_debug_buffer
+// "tstamp", [grid][16] globaltimer ns; written only while g_tstamp_on is set).
+#ifdef TEM_DIAG
+__device__ unsigned long long g_tstamp[1024 * 16];
+__device__ int g_tstamp_on;
+TEM_DEV void tstamp(int k) {
+    if (g_tstamp_on == 1) g_tstamp[blockIdx.x * 16 + k] = globaltimer();
+}
+// only while g_tstamp_on == 100 + slot (one launch of the step)
+TEM_DEV void tstamp_s(int slot, int k) {
+    if (g_tstamp_on == 100 + slot) g_tstamp[blockIdx.x * 16 + k] = globaltimer();
+}
+#else
+TEM_DEV void tstamp(int) {}
+TEM_DEV void tstamp_s(int, int) {}
+#endif
 
 // ------------------------------------------------------------------ common kernel pieces
 // 1 KB-aligned dynamic shared memory base, by pointer arithmetic on the __shared__ array so the
@@ -348,12 +368,16 @@ TEM_DEV void gemm_epilogue_done(uint32_t tbase, int warp) {
 }
 
 // Epilogue warp loop (warps 2..5): drain accumulator buffer t&1 of every tile this unit owns.
+// ring / ring_bytes: the CTA's operand ring; when the CTA owns a single tile the ring is drained
+// once that tile's accumulator is complete, and the epilogue stages all its chunks there.
 template <int MODE, int BN, bool PAIR, int ACC, typename Coords>
 TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, uint64_t* tfull, uint64_t* tempty,
                            int unit, int nunits, int total, Coords coords, int warp, int lane,
-                           float* zloc = nullptr) {
+                           float* zloc = nullptr, uint8_t* ring = nullptr, uint32_t ring_bytes = 0) {
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
-    uint8_t* stg = epi + (warp - 2) * 2 * EPI_BUF;
+    constexpr uint32_t WARP_STG = (BN / 16) * EPI_BUF;  // one buffer per 16-column chunk
+    const bool all = ring && total <= nunits && 4 * WARP_STG <= ring_bytes;
+    uint8_t* stg = all ? ring + (warp - 2) * WARP_STG : epi + (warp - 2) * 2 * EPI_BUF;
     float* sw3 = reinterpret_cast<float*>(epi + EPI_BYTES);
     if (MODE == FWD_) load_epi_smem(P, sw3, threadIdx.x - 64);
     const uint32_t tempty_leader = PAIR ? mapa_shared(&tempty[0], 0) : 0u;
@@ -366,8 +390,12 @@ TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, ui
         if (MODE == DGRAD_) dgrad_mask_chunk0(P, m_tile * BM + 32 * q + lane, n_tile * BN, pm);
         mbar_wait(&tfull[acc], (t >> 1) & 1);
         tc_fence_after();
+        if (t == 0 && threadIdx.x == 64) {  // diagnostics: the accumulator is complete
+            tstamp(5);
+            tstamp_s(P.slot, 5);
+        }
         const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * ACC * BN);
-        epilogue_tile<MODE, BN, ACC>(P, tq, m_tile, n_tile, split, q, lane, stg, buf, sw3, pm, zloc);
+        epilogue_tile<MODE, BN, ACC>(P, tq, m_tile, n_tile, split, q, lane, stg, buf, sw3, pm, zloc, all);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {  // buffer free for tile t + 2
@@ -378,22 +406,6 @@ TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, ui
     if (lane == 0) bulk_wait_read<0>();  // staging smem must outlive the stores' reads
 }
 
-// Phase timestamps of the GEMM kernels (diagnostics build only, -DTEM_DIAG: tem_debug_buffer
-// "tstamp", [grid][16] globaltimer ns; written only while g_tstamp_on is set).
-#ifdef TEM_DIAG
-__device__ unsigned long long g_tstamp[1024 * 16];
-__device__ int g_tstamp_on;
-TEM_DEV void tstamp(int k) {
-    if (g_tstamp_on == 1) g_tstamp[blockIdx.x * 16 + k] = globaltimer();
-}
-// only while g_tstamp_on == 100 + slot (one launch of the step)
-TEM_DEV void tstamp_s(int slot, int k) {
-    if (g_tstamp_on == 100 + slot) g_tstamp[blockIdx.x * 16 + k] = globaltimer();
-}
-#else
-TEM_DEV void tstamp(int) {}
-TEM_DEV void tstamp_s(int, int) {}
-#endif
 
 // ------------------------------------------------------------------ FWD / DGRAD (halo reuse)
 // The k = 3 taps of a c-block read rows shifted by one of the same activation window, so the
@@ -784,7 +796,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
     } else {
         if (HEAD) head_labels(P, hap, unit / P.ntiles, warp, lane, glab, gb3);
         epilogue_loop<MODE, BN, PAIR, C_::ACC>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane,
-                                               HEAD ? zrecv : nullptr);
+                                               HEAD ? zrecv : nullptr, smem, C_::RINGS);
         if (threadIdx.x == 64) tstamp(6);
     }
     if constexpr (HEAD)
@@ -928,7 +940,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
         }
         __syncwarp();
     } else {
-        epilogue_loop<WGRAD_, BN, PAIR, 1>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane);
+        epilogue_loop<WGRAD_, BN, PAIR, 1>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane,
+                                           nullptr, smem, STAGES * C_::STAGE_BYTES);
         if (threadIdx.x == 64) tstamp_s(P.slot, 6);
     }
     gemm_epilogue_done<C_::TMEM_COLS, PAIR>(tbase, warp);
@@ -1485,6 +1498,18 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
                        P.wgrad2.part_stride, P.S2, (int64_t)g.C * 3 * g.C, (const float*)nullptr, 0, g.C,
                        b.grad + g.off_W2, (int)SLOT_RED2);
         rec2.end(SLOT_RED2);
+        if (e != cudaSuccess) return e;
+        ++n;
+    }
+    if (split && split->n1_w2) {
+        // N = 1 tem_step: [off_W2, K_pad) (W2 from conv2 wgrad's partials, b2 / W3 / b3 from the
+        // head, PEM) is complete now; its update writes the other operand set, so it runs here,
+        // beside conv2 dgrad / conv1 wgrad, and the exchange updates only [0, off_W2)
+        rec2.begin(SLOT_EXCH2);
+        e = launch_sgd_fused(b.grad, const_cast<float*>(b.params), shadow_hi(b, 1 - wset), shadow_lo(b, 1 - wset),
+                             g.off_W2, g.Kpad, split->oc, split->os, nullptr, 0, 0, 1, b.wpart2,
+                             P.wgrad2.part_stride, g.off_W2, (int64_t)3 * g.C * g.C, P.S2, aux, true, 0, 2);
+        rec2.end(SLOT_EXCH2);
         if (e != cudaSuccess) return e;
         ++n;
     }
