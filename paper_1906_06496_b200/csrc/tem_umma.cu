@@ -45,6 +45,23 @@ constexpr int BK = 64;   // bf16 elements per k-block = one 128-byte swizzle row
 constexpr int UK = 16;   // K per tcgen05.mma (kind::f16)
 constexpr int NTHREADS = 192;
 
+// Phase timestamps of the GEMM kernels (diagnostics build only, -DTEM_DIAG: tem_debug_buffer
+// "tstamp", [grid][16] globaltimer ns; written only while g_tstamp_on is set).
+#ifdef TEM_DIAG
+__device__ unsigned long long g_tstamp[1024 * 16];
+__device__ int g_tstamp_on;
+TEM_DEV void tstamp(int k) {
+    if (g_tstamp_on == 1) g_tstamp[blockIdx.x * 16 + k] = globaltimer();
+}
+// only while g_tstamp_on == 100 + slot (one launch of the step)
+TEM_DEV void tstamp_s(int slot, int k) {
+    if (g_tstamp_on == 100 + slot) g_tstamp[blockIdx.x * 16 + k] = globaltimer();
+}
+#else
+TEM_DEV void tstamp(int) {}
+TEM_DEV void tstamp_s(int, int) {}
+#endif
+
 TEM_DEV bool halo_row(int p, int Tp) {
     const int t = p % Tp;
     return t == 0 || t == Tp - 1;
@@ -252,6 +269,7 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
         }
         issue(c16 + 1, eb);
         process(c16, ea);
+        if (MODE == WGRAD_ && threadIdx.x == 64) tstamp_s(P.slot, 8 + c16);  // diagnostics
         tmem_ld_wait_regs(eb.r);
         if (ACC == 3) {
             tmem_regs_fence(eb.r2);
@@ -259,6 +277,7 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
         }
         if (c16 + 2 < NC) issue(c16 + 2, ea);
         process(c16 + 1, eb);
+        if (MODE == WGRAD_ && threadIdx.x == 64) tstamp_s(P.slot, 9 + c16);
     }
     if (MODE == FWD_ && zloc) {
         // fused head: push this tile's partial logits into slot n_tile of every CTA of the
@@ -273,22 +292,6 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
     }
 }
 
-// Phase timestamps of the GEMM kernels (diagnostics build only, -DTEM_DIAG: tem_debug_buffer
-// "tstamp", [grid][16] globaltimer ns; written only while g_tstamp_on is set).
-#ifdef TEM_DIAG
-__device__ unsigned long long g_tstamp[1024 * 16];
-__device__ int g_tstamp_on;
-TEM_DEV void tstamp(int k) {
-    if (g_tstamp_on == 1) g_tstamp[blockIdx.x * 16 + k] = globaltimer();
-}
-// only while g_tstamp_on == 100 + slot (one launch of the step)
-TEM_DEV void tstamp_s(int slot, int k) {
-    if (g_tstamp_on == 100 + slot) g_tstamp[blockIdx.x * 16 + k] = globaltimer();
-}
-#else
-TEM_DEV void tstamp(int) {}
-TEM_DEV void tstamp_s(int, int) {}
-#endif
 
 // ------------------------------------------------------------------ common kernel pieces
 // 1 KB-aligned dynamic shared memory base, by pointer arithmetic on the __shared__ array so the

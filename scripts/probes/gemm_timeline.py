@@ -21,7 +21,8 @@ PHASES = {"split": ["entry", "pdl_wait", "prod_firstA", "mma_fullA", "mma_fullB"
           # conv2 FWD with the fused head (stamps 8..13; conv2 dgrad overwrites 0..6)
           "head": ["-"] * 8 + ["head_start", "cluster1", "dz_done", "dA2_done", "colsum_done",
                                "c0_tmem", "c0_math", "c0_stored"],
-          "wgrad1": ["entry", "prologue", "mma_full0", "mma_done", "-", "acc_ready", "epi_done"],
+          "wgrad1": ["entry", "prologue", "mma_full0", "mma_done", "-", "acc_ready", "epi_done", "-"]
+                    + [f"chunk{i}" for i in range(8)],
           "fwd1": ["entry", "pdl_wait", "mma_fullA0", "tile0_mma_done", "last_mma_done", "acc_ready", "epi_done"],
           "wgrad2": ["entry", "prologue", "mma_full0", "mma_done", "-", "acc_ready", "epi_done"]}
 SLOTS = {"wgrad2": 6, "wgrad1": 8, "fwd1": 1}  # Slot enum (kernels.h)
