@@ -78,6 +78,18 @@ struct OptState {
 // or hi/lo planes (TEM_FP32, 3-pass split).  (The round-1 CUDA-core path was removed: no
 // multi-backend dispatch in the product library.)
 
+// The fp32 backward as ONE persistent launch (tem_umma.cu, bwd_kernel): conv2 DGRAD, conv2
+// WGRAD and conv1 WGRAD tiles on a static per-CTA task list, one CTA per SM (cooperative
+// launch: all co-resident), conv1 WGRAD tiles waiting on the DGRAD tiles they read through
+// per-tile flags.  Device state in the workspace (RankBufs::bwd).
+struct BwdState {
+    int* tasks;          // [grid][max_tasks] task words (type << 24 | m << 16 | n << 8 | split), -1 ends a list
+    unsigned* flags;     // [dgrad m-tiles x n-tiles] epoch at which each DGRAD tile was stored
+    unsigned* epoch;     // [0] epoch of the last completed launch, [1] exit ticket (self-resetting)
+};
+constexpr int BWD_MAX_TASKS = 8;
+constexpr int BWD_MAX_DG_TILES = 1024;
+
 // Per-rank device buffers (all inside the caller's workspace except params).
 // Operand tensors are bf16 ("hi"; "_lo" = residual plane x - bf16(x), present only on the
 // fp32 path).
@@ -106,6 +118,7 @@ struct RankBufs {
     float* wpart;         // [S][max(C*3*Cin + C, C*3*C + C)] split-K partials (conv1 wgrad; SIMT: both)
     float* wpart2;        // [S][C*3*C + C] split-K partials of the tcgen05 conv2 wgrad
     int64_t* stepctr;     // step counter for NONFINITE reporting
+    BwdState bwd;         // persistent-backward task lists / flags (workspace)
     // bf16 operand copies of the weights, TWO sets [2][Kpad] (ping-pong): a step's GEMMs read
     // set `wset` while its updates write set 1 - wset, so an update may run while a GEMM of
     // the same step still reads the old weights
@@ -158,6 +171,8 @@ struct UmmaParams {
 };
 struct UmmaPlan {
     UmmaParams conv1, conv2, dgrad, wgrad1, wgrad2;
+    int bwd_grid;               // > 0: the backward runs as bwd_kernel on this many CTAs
+    BwdState bwd;
     CUtensorMap wmap[3][2][2];  // B maps of conv1 (W1), conv2 (W2), dgrad (W2) [set][plane]
     int npass, bn_fwd, S, ksplit_rows;
     int S1, S2;  // split-K factors of conv1 / conv2 wgrad (<= S, the workspace's)
@@ -187,7 +202,7 @@ cudaError_t launch_relu_decisions(const Geom& g, const RankBufs& b, uint8_t* out
 // ev[2*slot] / ev[2*slot+1] when ev != nullptr.
 enum Slot { SLOT_PREP = 0, SLOT_CONV1, SLOT_CONV2, SLOT_HEAD, SLOT_HEADFIN, SLOT_DGRAD, SLOT_WGRAD2,
             SLOT_RED2, SLOT_WGRAD1, SLOT_RED1, SLOT_EXCHANGE, SLOT_PEM, SLOT_PEMRED, SLOT_EXCH2, SLOT_PGM,
-            NUM_SLOTS };
+            SLOT_BWD, NUM_SLOTS };
 const char* slot_name(int slot);
 // kernel-span trace buffers (diagnostics): one setter per translation unit with traced kernels
 void trace_set_umma(unsigned long long* p);

@@ -111,7 +111,7 @@ const char* slot_name(int slot) {
     static const char* names[NUM_SLOTS] = {"prep_x", "conv1_fwd", "conv2_fwd", "head_loss", "head_finalize",
                                            "conv2_dgrad", "conv2_wgrad", "conv2_wgrad_reduce",
                                            "conv1_wgrad", "conv1_wgrad_reduce", "exchange", "pem",
-                                           "pem_reduce", "exchange_w2", "pgm"};
+                                           "pem_reduce", "exchange_w2", "pgm", "backward"};
     return (slot >= 0 && slot < NUM_SLOTS) ? names[slot] : "?";
 }
 

@@ -59,7 +59,7 @@ struct HeapLayout {
 
 struct WsLayout {
     size_t xp, h1, h2, dA2, dA1, xp_lo, h1_lo, dA2_lo, dA1_lo, z, grad, headpart, headlvl1, counter, bpart, wpart, wpart2, shadow,
-        shadow_lo, ones, zpart, epochs, stepctr, xstage, labstage, lossstage, bspstage, ioustage, pempart, pemdec, opt_m, opt_v, opt_scal,
+        shadow_lo, ones, zpart, epochs, stepctr, bwd_tasks, bwd_flags, bwd_epoch, xstage, labstage, lossstage, bspstage, ioustage, pempart, pemdec, opt_m, opt_v, opt_scal,
         pgm_prob, pgm_feat, pgm_iou, pgm_ts, pgm_te, pgm_count, trace, per_rank;
 };
 
@@ -200,6 +200,9 @@ WsLayout ws_layout(const tem_config* c) {
     w.zpart = take((size_t)(g.C / 64) * g.R * 3 * 4);
     w.epochs = take((size_t)kMaxChannels * 4);
     w.stepctr = take(8);
+    w.bwd_tasks = take((size_t)1024 * BWD_MAX_TASKS * 4);  // persistent backward (UmmaPlan::bwd_grid)
+    w.bwd_flags = take((size_t)BWD_MAX_DG_TILES * 4);
+    w.bwd_epoch = take(2 * 4);
     // host-input staging (tem_step_host / tem_step_pem_host), double-buffered: the copy of step
     // k+1 lands in the other set while step k computes
     w.xstage = take(2 * (size_t)g.B * g.T * g.Cin * xsz);
@@ -455,6 +458,9 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
         b.pempart = (float*)(base + wl.pempart);
         b.pemdec = (uint8_t*)(base + wl.pemdec);
         b.stepctr = (int64_t*)(base + wl.stepctr);
+        b.bwd.tasks = (int*)(base + wl.bwd_tasks);
+        b.bwd.flags = (unsigned*)(base + wl.bwd_flags);
+        b.bwd.epoch = (unsigned*)(base + wl.bwd_epoch);
         b.xp_lo = c->g.split ? base + wl.xp_lo : nullptr;
         b.h1_lo = c->g.split ? base + wl.h1_lo : nullptr;
         b.dA2_lo = c->g.split ? base + wl.dA2_lo : nullptr;

@@ -646,13 +646,110 @@ TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const f
     // no second cluster barrier: every remote access (the pushes) happened before the first
 }
 
+// Producer side of one FWD/DGRAD tile (warp 0, converged; the elected lane `pe` issues): per
+// c-block one A window, then the three taps' B slots.  ia / ib: ring counters (persist across
+// the tiles of this CTA).
+template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR>
+TEM_DEV void halo_load_tile(const UmmaParams& P, uint8_t* sA, uint8_t* sB, uint64_t* fullA, uint64_t* emptyA,
+                            uint64_t* fullB, uint64_t* emptyB, int m_tile, int n_tile, uint32_t rank, bool leader,
+                            bool pe, int& ia, int& ib) {
+    using C_ = CfgHalo<BN, NPASS, SA, SB, PAIR>;
+    constexpr int NPL = C_::NPL;
+    const int m0 = m_tile * BM;
+    const int n0 = n_tile * BN + (int)rank * C_::BR;
+    for (int cb = 0; cb < P.cpb; ++cb) {
+        const int sa = ia % SA;
+        mbar_wait(&emptyA[sa], ((ia / SA) & 1) ^ 1);
+        if (pe && leader) mbar_arrive_expect_tx(&fullA[sa], (PAIR ? 2 : 1) * C_::A_TX);
+#pragma unroll
+        for (int pl = 0; pl < NPL; ++pl)
+            if (pe) ld2d<PAIR>(sA + sa * C_::A_STAGE + pl * C_::A_PLANE, &P.a[pl], &fullA[sa], cb * BK, m0 - 1);
+        ++ia;
+        for (int j = 0; j < 3; ++j, ++ib) {
+            const int sb = ib % SB;                          // tap slot
+            const int bs = (ib / C_::TPS) % C_::SBS;         // barrier stage
+            const bool first = (ib % C_::TPS) == 0;
+            if (first) mbar_wait(&emptyB[bs], ((ib / C_::TPS / C_::SBS) & 1) ^ 1);
+            if (pe && leader && first) mbar_arrive_expect_tx(&fullB[bs], (PAIR ? 2 : 1) * C_::TPS * C_::B_STAGE);
+#pragma unroll
+            for (int pl = 0; pl < NPL; ++pl) {
+                uint8_t* dst = sB + sb * C_::B_STAGE + pl * C_::B_PLANE;
+                if (MODE == FWD_) {
+                    if (pe) ld2d<PAIR>(dst, &P.b[pl], &fullB[bs], j * P.Kc + cb * BK, n0);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < C_::BR / 64; ++q)
+                        if (pe) ld3d<PAIR>(dst + q * (BK * 128), &P.b[pl], &fullB[bs], n0 + 64 * q, j, cb * BK);
+                }
+            }
+        }
+    }
+}
+
+// MMA side of one FWD/DGRAD tile into the accumulator at TMEM address dt (warp 1, converged;
+// the elected lane `issuer` issues and commits).
+template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR>
+TEM_DEV void halo_mma_tile(const UmmaParams& P, uint8_t* sA, uint8_t* sB, uint64_t* fullA, uint64_t* emptyA,
+                           uint64_t* fullB, uint64_t* emptyB, uint32_t dt, bool issuer, int lane, int& ia, int& ib) {
+    using C_ = CfgHalo<BN, NPASS, SA, SB, PAIR>;
+    constexpr bool B_MN = (MODE == DGRAD_);
+    constexpr uint32_t idesc = make_idesc_bf16(PAIR ? 2 * BM : BM, BN, false, B_MN);
+    for (int cb = 0; cb < P.cpb; ++cb) {
+        const int sa = ia % SA;
+        mbar_wait(&fullA[sa], (ia / SA) & 1);
+        if (ia == 0 && lane == 0) tstamp(2);
+        tc_fence_after();
+        const uint32_t a_st = smem_u32(sA + sa * C_::A_STAGE);
+        for (int j = 0; j < 3; ++j, ++ib) {
+            const int sb = ib % SB;
+            const int bs = (ib / C_::TPS) % C_::SBS;
+            if ((ib % C_::TPS) == 0) {
+                mbar_wait(&fullB[bs], (ib / C_::TPS / C_::SBS) & 1);
+                tc_fence_after();
+            }
+            const uint32_t b_st = smem_u32(sB + sb * C_::B_STAGE);
+            const uint32_t roff = (uint32_t)((MODE == FWD_ ? j : 2 - j) * 128);
+            // descriptors of the tap's first K-step; the K-steps advance the 16-byte
+            // start-address field (addresses < 256 KB: no carry out of the field)
+            const uint64_t bdt = B_MN ? make_desc(b_st, BK * 128, 1024) : make_desc(b_st, 16, 1024);
+            const uint64_t adh = make_desc(a_st + roff, 16, 1024);
+            const uint64_t adl = make_desc(a_st + C_::A_PLANE + roff, 16, 1024);
+#pragma unroll
+            for (int k = 0; k < BK / UK; ++k) {
+                const uint64_t bd0 = bdt + (uint64_t)(B_MN ? k * (UK * 128 / 16) : k * (UK * 2 / 16));
+                if (C_::ACC == 3) {
+                    // A_hi x [B_hi | B_lo] (N = 2 BN, planes contiguous), A_lo x B_hi (N = BN)
+                    constexpr uint32_t idesc2 = make_idesc_bf16(BM, 2 * BN, false, B_MN);
+                    const uint32_t acc_on = (cb | j | k) != 0 ? 1u : 0u;
+                    if (issuer) {
+                        issue_mma<PAIR>(dt, adh + (uint64_t)(k * (UK * 2 / 16)), bd0, idesc2, acc_on);
+                        issue_mma<PAIR>(dt + 2 * BN, adl + (uint64_t)(k * (UK * 2 / 16)), bd0, idesc, acc_on);
+                    }
+                } else {
+#pragma unroll
+                    for (int pass = 0; pass < NPASS; ++pass) {
+                        const int pa = (pass == 2) ? 1 : 0;  // hi*hi, hi*lo, lo*hi
+                        const int pb = (pass == 1) ? 1 : 0;
+                        const uint64_t ad = make_desc(a_st + pa * C_::A_PLANE + roff + k * (UK * 2), 16, 1024);
+                        const uint32_t b_addr = b_st + pb * C_::B_PLANE;
+                        const uint64_t bd = B_MN ? make_desc(b_addr + k * (UK * 128), BK * 128, 1024)
+                                                 : make_desc(b_addr + k * (UK * 2), 16, 1024);
+                        if (issuer) issue_mma<PAIR>(dt, ad, bd, idesc, (cb | j | k | pass) != 0 ? 1u : 0u);
+                    }
+                }
+            }
+            if (issuer && (ib % C_::TPS) == C_::TPS - 1) commit_to<PAIR>(&emptyB[bs]);
+        }
+        if (issuer) commit_to<PAIR>(&emptyA[sa]);  // window consumed by all three taps
+        ++ia;
+    }
+}
+
 template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR, bool HEAD = false>
 __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_constant__ UmmaParams P) {
     static_assert(MODE == FWD_ || MODE == DGRAD_, "halo kernel: FWD / DGRAD");
     static_assert(!HEAD || (MODE == FWD_ && !PAIR), "fused head: 1-CTA conv2 FWD");
     using C_ = CfgHalo<BN, NPASS, SA, SB, PAIR>;
-    constexpr int NPL = C_::NPL;
-    constexpr bool B_MN = (MODE == DGRAD_);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align_smem_1k(smem_raw);
     uint8_t* sA = smem;
@@ -691,106 +788,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
     };
 
     if (warp == 0) {
-        {
-            // ===================== TMA producer (both CTAs of a pair) =====================
-            // the whole warp runs the loop (uniform operands), the elected lane issues
-            const bool pe = elect_one_sync();
-            int ia = 0, ib = 0;
-            for (int ct = unit; ct < total; ct += nunits) {
-                int m_tile, n_tile, split;
-                coords(ct, m_tile, n_tile, split);
-                const int m0 = m_tile * BM;
-                const int n0 = n_tile * BN + (int)rank * C_::BR;
-                for (int cb = 0; cb < P.cpb; ++cb) {
-                    const int sa = ia % SA;
-                    mbar_wait(&emptyA[sa], ((ia / SA) & 1) ^ 1);
-                    if (pe && leader) mbar_arrive_expect_tx(&fullA[sa], (PAIR ? 2 : 1) * C_::A_TX);
-#pragma unroll
-                    for (int pl = 0; pl < NPL; ++pl)
-                        if (pe) ld2d<PAIR>(sA + sa * C_::A_STAGE + pl * C_::A_PLANE, &P.a[pl], &fullA[sa], cb * BK, m0 - 1);
-                    ++ia;
-                    for (int j = 0; j < 3; ++j, ++ib) {
-                        const int sb = ib % SB;                          // tap slot
-                        const int bs = (ib / C_::TPS) % C_::SBS;         // barrier stage
-                        const bool first = (ib % C_::TPS) == 0;
-                        if (first) mbar_wait(&emptyB[bs], ((ib / C_::TPS / C_::SBS) & 1) ^ 1);
-                        if (pe && leader && first) mbar_arrive_expect_tx(&fullB[bs], (PAIR ? 2 : 1) * C_::TPS * C_::B_STAGE);
-#pragma unroll
-                        for (int pl = 0; pl < NPL; ++pl) {
-                            uint8_t* dst = sB + sb * C_::B_STAGE + pl * C_::B_PLANE;
-                            if (MODE == FWD_) {
-                                if (pe) ld2d<PAIR>(dst, &P.b[pl], &fullB[bs], j * P.Kc + cb * BK, n0);
-                            } else {
-#pragma unroll
-                                for (int q = 0; q < C_::BR / 64; ++q)
-                                    if (pe) ld3d<PAIR>(dst + q * (BK * 128), &P.b[pl], &fullB[bs], n0 + 64 * q, j, cb * BK);
-                            }
-                        }
-                    }
-                }
-            }
+        // ===================== TMA producer (both CTAs of a pair) =====================
+        // the whole warp runs the loop (uniform operands), the elected lane issues
+        const bool pe = elect_one_sync();
+        int ia = 0, ib = 0;
+        for (int ct = unit; ct < total; ct += nunits) {
+            int m_tile, n_tile, split;
+            coords(ct, m_tile, n_tile, split);
+            halo_load_tile<MODE, BN, NPASS, SA, SB, PAIR>(P, sA, sB, fullA, emptyA, fullB, emptyB, m_tile, n_tile, rank,
+                                                        leader, pe, ia, ib);
         }
     } else if (warp == 1) {
         if (leader) {
             // ===================== MMA issuer =====================
             // the whole warp runs the loop (uniform descriptors); the elected lane issues
             const bool issuer = elect_one_sync();
-            constexpr uint32_t idesc = make_idesc_bf16(PAIR ? 2 * BM : BM, BN, false, B_MN);
             int ia = 0, ib = 0, t = 0;
             for (int ct = unit; ct < total; ct += nunits, ++t) {
                 const int acc = t & 1;
                 mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);  // epilogue drained this buffer
                 tc_fence_after();
                 const uint32_t dt = tbase + (uint32_t)(acc * C_::ACC * BN);
-                for (int cb = 0; cb < P.cpb; ++cb) {
-                    const int sa = ia % SA;
-                    mbar_wait(&fullA[sa], (ia / SA) & 1);
-                    if (ia == 0 && lane == 0) tstamp(2);
-                    tc_fence_after();
-                    const uint32_t a_st = smem_u32(sA + sa * C_::A_STAGE);
-                    for (int j = 0; j < 3; ++j, ++ib) {
-                        const int sb = ib % SB;
-                        const int bs = (ib / C_::TPS) % C_::SBS;
-                        if ((ib % C_::TPS) == 0) {
-                            mbar_wait(&fullB[bs], (ib / C_::TPS / C_::SBS) & 1);
-                            tc_fence_after();
-                        }
-                        const uint32_t b_st = smem_u32(sB + sb * C_::B_STAGE);
-                        const uint32_t roff = (uint32_t)((MODE == FWD_ ? j : 2 - j) * 128);
-                        // descriptors of the tap's first K-step; the K-steps advance the 16-byte
-                        // start-address field (addresses < 256 KB: no carry out of the field)
-                        const uint64_t bdt = B_MN ? make_desc(b_st, BK * 128, 1024) : make_desc(b_st, 16, 1024);
-                        const uint64_t adh = make_desc(a_st + roff, 16, 1024);
-                        const uint64_t adl = make_desc(a_st + C_::A_PLANE + roff, 16, 1024);
-#pragma unroll
-                        for (int k = 0; k < BK / UK; ++k) {
-                            const uint64_t bd0 = bdt + (uint64_t)(B_MN ? k * (UK * 128 / 16) : k * (UK * 2 / 16));
-                            if (C_::ACC == 3) {
-                                // A_hi x [B_hi | B_lo] (N = 2 BN, planes contiguous), A_lo x B_hi (N = BN)
-                                constexpr uint32_t idesc2 = make_idesc_bf16(BM, 2 * BN, false, B_MN);
-                                const uint32_t acc_on = (cb | j | k) != 0 ? 1u : 0u;
-                                if (issuer) {
-                                    issue_mma<PAIR>(dt, adh + (uint64_t)(k * (UK * 2 / 16)), bd0, idesc2, acc_on);
-                                    issue_mma<PAIR>(dt + 2 * BN, adl + (uint64_t)(k * (UK * 2 / 16)), bd0, idesc, acc_on);
-                                }
-                            } else {
-#pragma unroll
-                                for (int pass = 0; pass < NPASS; ++pass) {
-                                    const int pa = (pass == 2) ? 1 : 0;  // hi*hi, hi*lo, lo*hi
-                                    const int pb = (pass == 1) ? 1 : 0;
-                                    const uint64_t ad = make_desc(a_st + pa * C_::A_PLANE + roff + k * (UK * 2), 16, 1024);
-                                    const uint32_t b_addr = b_st + pb * C_::B_PLANE;
-                                    const uint64_t bd = B_MN ? make_desc(b_addr + k * (UK * 128), BK * 128, 1024)
-                                                             : make_desc(b_addr + k * (UK * 2), 16, 1024);
-                                    if (issuer) issue_mma<PAIR>(dt, ad, bd, idesc, (cb | j | k | pass) != 0 ? 1u : 0u);
-                                }
-                            }
-                        }
-                        if (issuer && (ib % C_::TPS) == C_::TPS - 1) commit_to<PAIR>(&emptyB[bs]);
-                    }
-                    if (issuer) commit_to<PAIR>(&emptyA[sa]);  // window consumed by all three taps
-                    ++ia;
-                }
+                halo_mma_tile<MODE, BN, NPASS, SA, SB, PAIR>(P, sA, sB, fullA, emptyA, fullB, emptyB, dt, issuer, lane,
+                                                           ia, ib);
                 if (issuer) commit_to<PAIR>(&tfull[acc]);  // accumulator complete
                 if (lane == 0) tstamp(t == 0 ? 3 : 4);
             }
@@ -823,10 +843,84 @@ struct CfgW {
     static constexpr int TMEM_COLS = 2 * BN;
 };
 
+// WGRAD producer / MMA for one (m_tile, n_tile, split) tile, p_begin / nkb from wgrad_kblocks.
+TEM_DEV int wgrad_kblocks(const UmmaParams& P, int split, int& p_begin) {
+    p_begin = split * P.ksplit_rows;
+    const int p_end = min(P.R, p_begin + P.ksplit_rows);
+    return (p_end - p_begin + BK - 1) / BK;
+}
+
+template <int BN, int NPASS, int STAGES, bool PAIR>
+TEM_DEV void wgrad_load_tile(const UmmaParams& P, uint8_t* smem, uint64_t* full, uint64_t* empty, int m_tile,
+                             int n_tile, int split, uint32_t rank, bool leader, bool pe, int& it) {
+    using C_ = CfgW<BN, NPASS, STAGES, PAIR>;
+    constexpr int NPL = C_::NPL;
+    int p_begin;
+    const int nkb = wgrad_kblocks(P, split, p_begin);
+    const int m0 = m_tile * BM;
+    for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+        uint8_t* st = smem + s * C_::STAGE_BYTES;
+        if (pe && leader) mbar_arrive_expect_tx(&full[s], (PAIR ? 2 : 1) * C_::STAGE_BYTES);
+        const int p0 = p_begin + kb * BK;
+#pragma unroll
+        for (int pl = 0; pl < NPL; ++pl) {
+            uint8_t* sa = st + pl * C_::A_BYTES;
+            uint8_t* sb = st + NPL * C_::A_BYTES + pl * C_::B_BYTES;
+#pragma unroll
+            for (int q = 0; q < BM / 64; ++q)
+                if (pe) ld2d<PAIR>(sa + q * (BK * 128), &P.a[pl], &full[s], m0 + 64 * q, p0);
+#pragma unroll
+            for (int q = 0; q < C_::BR / 64; ++q) {
+                uint8_t* dst = sb + q * (BK * 128);
+                int g = n_tile * (BN / 64) + (int)rank * (C_::BR / 64) + q;
+                if (P.ones_chunk && g == 3 * P.cpj) {
+                    // all-ones chunk (lo plane: zeros): D column = sum_p dA[p][o]
+                    if (pe) ld2d<PAIR>(dst, &P.ones, &full[s], 64 * pl, p0);
+                    continue;
+                }
+                if (g >= 3 * P.cpj) g = 3 * P.cpj - 1;  // dummy chunk, discarded
+                const int j = g / P.cpj, c0 = (g % P.cpj) * 64;
+                if (pe) ld2d<PAIR>(dst, &P.b[pl], &full[s], c0, p0 + j - 1);
+            }
+        }
+    }
+}
+
+template <int BN, int NPASS, int STAGES, bool PAIR>
+TEM_DEV void wgrad_mma_tile(const UmmaParams& P, uint8_t* smem, uint64_t* full, uint64_t* empty, int split,
+                            uint32_t dt, bool issuer, int lane, int& it) {
+    using C_ = CfgW<BN, NPASS, STAGES, PAIR>;
+    constexpr int NPL = C_::NPL;
+    constexpr uint32_t idesc = make_idesc_bf16(PAIR ? 2 * BM : BM, BN, true, true);
+    int p_begin;
+    const int nkb = wgrad_kblocks(P, split, p_begin);
+    for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int s = it % STAGES;
+        mbar_wait(&full[s], (it / STAGES) & 1);
+        if (it == 0 && lane == 0) tstamp_s(P.slot, 2);
+        tc_fence_after();
+        const uint32_t st = smem_u32(smem + s * C_::STAGE_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK / UK; ++k) {
+#pragma unroll
+            for (int pass = 0; pass < NPASS; ++pass) {
+                const int pa = (pass == 2) ? 1 : 0;
+                const int pb = (pass == 1) ? 1 : 0;
+                const uint64_t ad = make_desc(st + pa * C_::A_BYTES + k * (UK * 128), BK * 128, 1024);
+                const uint64_t bd = make_desc(st + NPL * C_::A_BYTES + pb * C_::B_BYTES + k * (UK * 128),
+                                              BK * 128, 1024);
+                if (issuer) issue_mma<PAIR>(dt, ad, bd, idesc, (kb | k | pass) != 0 ? 1u : 0u);
+            }
+        }
+        if (issuer) commit_to<PAIR>(&empty[s]);
+    }
+}
+
 template <int BN, int NPASS, int STAGES, bool PAIR>
 __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_constant__ UmmaParams P) {
     using C_ = CfgW<BN, NPASS, STAGES, PAIR>;
-    constexpr int NPL = C_::NPL;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align_smem_1k(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C_::STAGE_BYTES);
@@ -855,88 +949,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
         split = rest / mt_u;
         m_tile = PAIR ? mu * 2 + (int)rank : mu;
     };
-    auto kblocks = [&](int split, int& p_begin) -> int {
-        p_begin = split * P.ksplit_rows;
-        const int p_end = min(P.R, p_begin + P.ksplit_rows);
-        return (p_end - p_begin + BK - 1) / BK;
-    };
-
     if (warp == 0) {
-        {
-            // ===================== TMA producer =====================
-            // the whole warp runs the loop (uniform operands), the elected lane issues
-            const bool pe = elect_one_sync();
-            int it = 0;
-            for (int ct = unit; ct < total; ct += nunits) {
-                int m_tile, n_tile, split, p_begin;
-                coords(ct, m_tile, n_tile, split);
-                const int nkb = kblocks(split, p_begin);
-                const int m0 = m_tile * BM;
-                for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const int s = it % STAGES;
-                    mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
-                    uint8_t* st = smem + s * C_::STAGE_BYTES;
-                    if (pe && leader) mbar_arrive_expect_tx(&full[s], (PAIR ? 2 : 1) * C_::STAGE_BYTES);
-                    const int p0 = p_begin + kb * BK;
-#pragma unroll
-                    for (int pl = 0; pl < NPL; ++pl) {
-                        uint8_t* sa = st + pl * C_::A_BYTES;
-                        uint8_t* sb = st + NPL * C_::A_BYTES + pl * C_::B_BYTES;
-#pragma unroll
-                        for (int q = 0; q < BM / 64; ++q)
-                            if (pe) ld2d<PAIR>(sa + q * (BK * 128), &P.a[pl], &full[s], m0 + 64 * q, p0);
-#pragma unroll
-                        for (int q = 0; q < C_::BR / 64; ++q) {
-                            uint8_t* dst = sb + q * (BK * 128);
-                            int g = n_tile * (BN / 64) + (int)rank * (C_::BR / 64) + q;
-                            if (P.ones_chunk && g == 3 * P.cpj) {
-                                // all-ones chunk (lo plane: zeros): D column = sum_p dA[p][o]
-                                if (pe) ld2d<PAIR>(dst, &P.ones, &full[s], 64 * pl, p0);
-                                continue;
-                            }
-                            if (g >= 3 * P.cpj) g = 3 * P.cpj - 1;  // dummy chunk, discarded
-                            const int j = g / P.cpj, c0 = (g % P.cpj) * 64;
-                            if (pe) ld2d<PAIR>(dst, &P.b[pl], &full[s], c0, p0 + j - 1);
-                        }
-                    }
-                }
-            }
+        // ===================== TMA producer =====================
+        // the whole warp runs the loop (uniform operands), the elected lane issues
+        const bool pe = elect_one_sync();
+        int it = 0;
+        for (int ct = unit; ct < total; ct += nunits) {
+            int m_tile, n_tile, split;
+            coords(ct, m_tile, n_tile, split);
+            wgrad_load_tile<BN, NPASS, STAGES, PAIR>(P, smem, full, empty, m_tile, n_tile, split, rank, leader, pe, it);
         }
     } else if (warp == 1) {
         if (leader) {
+            // ===================== MMA issuer =====================
             // the whole warp runs the issue loop (uniform descriptors), the elected lane issues
             const bool issuer = elect_one_sync();
-            // ===================== MMA issuer =====================
-            constexpr uint32_t idesc = make_idesc_bf16(PAIR ? 2 * BM : BM, BN, true, true);
             int it = 0, t = 0;
             for (int ct = unit; ct < total; ct += nunits, ++t) {
-                int m_tile, n_tile, split, p_begin;
+                int m_tile, n_tile, split;
                 coords(ct, m_tile, n_tile, split);
-                const int nkb = kblocks(split, p_begin);
                 const int acc = t & 1;
                 mbar_wait(&tempty[acc], ((t >> 1) & 1) ^ 1);
                 tc_fence_after();
-                const uint32_t dt = tbase + (uint32_t)(acc * BN);
-                for (int kb = 0; kb < nkb; ++kb, ++it) {
-                    const int s = it % STAGES;
-                    mbar_wait(&full[s], (it / STAGES) & 1);
-                    if (it == 0 && lane == 0) tstamp_s(P.slot, 2);
-                    tc_fence_after();
-                    const uint32_t st = smem_u32(smem + s * C_::STAGE_BYTES);
-#pragma unroll
-                    for (int k = 0; k < BK / UK; ++k) {
-#pragma unroll
-                        for (int pass = 0; pass < NPASS; ++pass) {
-                            const int pa = (pass == 2) ? 1 : 0;
-                            const int pb = (pass == 1) ? 1 : 0;
-                            const uint64_t ad = make_desc(st + pa * C_::A_BYTES + k * (UK * 128), BK * 128, 1024);
-                            const uint64_t bd = make_desc(st + NPL * C_::A_BYTES + pb * C_::B_BYTES + k * (UK * 128),
-                                                          BK * 128, 1024);
-                            if (issuer) issue_mma<PAIR>(dt, ad, bd, idesc, (kb | k | pass) != 0 ? 1u : 0u);
-                        }
-                    }
-                    if (issuer) commit_to<PAIR>(&empty[s]);
-                }
+                wgrad_mma_tile<BN, NPASS, STAGES, PAIR>(P, smem, full, empty, split, tbase + (uint32_t)(acc * BN), issuer,
+                                                       lane, it);
                 if (issuer) commit_to<PAIR>(&tfull[acc]);
                 if (lane == 0) tstamp_s(P.slot, 3);
             }
@@ -949,6 +985,202 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
     }
     gemm_epilogue_done<C_::TMEM_COLS, PAIR>(tbase, warp);
     trace_end(P.slot);
+}
+
+// ------------------------------------------------------------------ backward (persistent)
+// The fp32 backward of the step (rows a6-a8) as ONE launch of one CTA per SM: conv2 DGRAD
+// (FWD/DGRAD halo mode, 128 x 64 tiles), conv2 WGRAD and conv1 WGRAD (split-K, 128 x 128) tiles on
+// a static per-CTA task list (BwdState::tasks, built by umma_plan).  Compared with three
+// launches: every CTA's second task runs its mainloop while the first task's epilogue drains,
+// the per-launch prologue / first-operand latency is paid once, and the conv2 WGRAD tiles use
+// the SMs DGRAD leaves free.  Each task is the same device code as the separate kernels
+// (halo_load_tile / halo_mma_tile / wgrad_*_tile / epilogue_tile), so the results are bitwise
+// those of the three-launch schedule.
+//   * Operand rings: the halo rings and the WGRAD stages share the shared memory; a producer
+//     changing layout first waits for the MMA warp to have consumed its previous task (`drain`,
+//     committed after every task).
+//   * Accumulators: two TMEM buffers of 256 columns (halo ACC = 3 uses 192, WGRAD 128).
+//   * Dependencies: a conv1 WGRAD tile reads dA1 rows of its split for its 128 output channels,
+//     i.e. the DGRAD tiles covering those rows and 2 column tiles.  A DGRAD tile's epilogue, once
+//     its bulk stores have completed, releases flags[tile] = epoch; the conv1 WGRAD producer
+//     acquires every flag it needs before loading.  DGRAD tasks come first in their CTA's list
+//     and wait for nothing, and all CTAs are co-resident, so every wait ends.  A wait longer
+//     than 2 s latches TEM_ERR_CUDA and traps (the launch fails instead of hanging).
+//   * epoch: read by every CTA at entry (previous launch's value + 1); the last CTA to exit
+//     stores it, so it increases by one per launch (graph replays included).
+enum { BWD_DG = 0, BWD_W2 = 1, BWD_W1 = 2 };
+struct BwdParams {
+    UmmaParams dg, w2, w1;
+    BwdState st;
+    int dg_ntiles;
+    Status* status;
+    int slot;
+};
+using BwdHalo = CfgHalo<64, 3, 3, 6, false>;
+using BwdW = CfgW<128, 3, 3, false>;
+constexpr uint32_t BWD_RING = BwdHalo::RINGS > 3 * BwdW::STAGE_BYTES ? BwdHalo::RINGS : 3 * BwdW::STAGE_BYTES;
+constexpr uint32_t BWD_SMEM = BWD_RING + 1024 + 1024 + EPI_SMEM;
+constexpr int BWD_ACC_COLS = 256;
+
+TEM_DEV unsigned ld_acquire_gpu_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+TEM_DEV void st_release_gpu_u32(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(NTHREADS, 1) bwd_kernel(const __grid_constant__ BwdParams B) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = align_smem_1k(smem_raw);
+    uint8_t* sA = smem;                                   // halo: A windows, then B taps
+    uint8_t* sB = smem + 3 * BwdHalo::A_STAGE;
+    uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + BWD_RING);
+    uint64_t* emptyA = fullA + 3;
+    uint64_t* fullB = emptyA + 3;
+    uint64_t* emptyB = fullB + 6;
+    uint64_t* full = emptyB + 6;                          // WGRAD stages
+    uint64_t* empty = full + 3;
+    uint64_t* drain = empty + 3;                          // [1], MMA commit after every task
+    uint64_t* tfull = drain + 1;                          // [2]
+    uint64_t* tempty = tfull + 2;                         // [2]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint8_t* epi = smem + BWD_RING + 1024;
+    __shared__ unsigned s_epoch;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int* tasks = B.st.tasks + (size_t)blockIdx.x * BWD_MAX_TASKS;
+    trace_begin(B.slot);
+    if (threadIdx.x == 0) {
+        s_epoch = *reinterpret_cast<volatile unsigned*>(&B.st.epoch[0]) + 1u;
+        mbar_init(drain, 1);
+    }
+    // barriers: fullA..empty (24 stage barriers), tfull / tempty; TMEM: two 256-column buffers
+    const uint32_t tbase = gemm_prologue<512, false>(B.dg, fullA, 24, tfull, tempty, tslot, warp, lane);
+    const unsigned epoch = s_epoch;
+    auto decode = [&](int w, int& type, int& m, int& n, int& sp) {
+        type = (w >> 24) & 0xFF;
+        m = (w >> 16) & 0xFF;
+        n = (w >> 8) & 0xFF;
+        sp = w & 0xFF;
+    };
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        const bool pe = elect_one_sync();
+        int ia = 0, ib = 0, it = 0, prev = -1;
+        for (int k = 0; k < BWD_MAX_TASKS; ++k) {
+            const int w = tasks[k];
+            if (w < 0) break;
+            int type, m, n, sp;
+            decode(w, type, m, n, sp);
+            const int mode = type == BWD_DG ? 0 : 1;
+            if (prev >= 0 && mode != prev) mbar_wait(drain, (k - 1) & 1);  // ring free for the new layout
+            prev = mode;
+            if (type == BWD_DG) {
+                halo_load_tile<DGRAD_, 64, 3, 3, 6, false>(B.dg, sA, sB, fullA, emptyA, fullB, emptyB, m, n, 0u, true,
+                                                            pe, ia, ib);
+                continue;
+            }
+            const UmmaParams& W = type == BWD_W2 ? B.w2 : B.w1;
+            if (type == BWD_W1) {
+                // the dA1 rows of this split, output channels [128 m, 128 m + 128): DGRAD tiles
+                // (rows) x column tiles 2m, 2m + 1 of 64
+                if (lane == 0) {
+                    const int p0 = sp * W.ksplit_rows, p1 = min(W.R, p0 + W.ksplit_rows) - 1;
+                    const uint64_t t0 = globaltimer();
+                    for (int mt = p0 / BM; mt <= p1 / BM; ++mt)
+                        for (int q = 0; q < 2; ++q) {
+                            const unsigned* f = B.st.flags + mt * B.dg_ntiles + 2 * m + q;
+                            while (ld_acquire_gpu_u32(f) != epoch) {
+                                if (globaltimer() - t0 > 2000000000ull) {
+                                    latch(B.status, TEM_ERR_CUDA, -1);
+                                    asm volatile("trap;");
+                                }
+                            }
+                        }
+                    fence_proxy_async_all();  // the acquired data is read by the TMA (async proxy)
+                }
+                __syncwarp();
+            }
+            wgrad_load_tile<128, 3, 3, false>(W, smem, full, empty, m, n, sp, 0u, true, pe, it);
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer =====================
+        const bool issuer = elect_one_sync();
+        int ia = 0, ib = 0, it = 0;
+        for (int k = 0; k < BWD_MAX_TASKS; ++k) {
+            const int w = tasks[k];
+            if (w < 0) break;
+            int type, m, n, sp;
+            decode(w, type, m, n, sp);
+            const int acc = k & 1;
+            mbar_wait(&tempty[acc], ((k >> 1) & 1) ^ 1);
+            tc_fence_after();
+            const uint32_t dt = tbase + (uint32_t)(acc * BWD_ACC_COLS);
+            if (type == BWD_DG)
+                halo_mma_tile<DGRAD_, 64, 3, 3, 6, false>(B.dg, sA, sB, fullA, emptyA, fullB, emptyB, dt, issuer, lane,
+                                                           ia, ib);
+            else
+                wgrad_mma_tile<128, 3, 3, false>(type == BWD_W2 ? B.w2 : B.w1, smem, full, empty, sp, dt, issuer, lane,
+                                                 it);
+            if (issuer) {
+                commit_to<false>(&tfull[acc]);
+                commit_to<false>(drain);
+            }
+        }
+        __syncwarp();
+    } else {
+        // ===================== epilogue =====================
+        const int q = warp & 3;
+        uint8_t* stg = epi + (warp - 2) * 2 * EPI_BUF;
+        const float* sw3 = reinterpret_cast<const float*>(epi + EPI_BYTES);
+        int buf = 0;
+        for (int k = 0; k < BWD_MAX_TASKS; ++k) {
+            const int w = tasks[k];
+            if (w < 0) break;
+            int type, m, n, sp;
+            decode(w, type, m, n, sp);
+            const int acc = k & 1;
+            uint4 pm[2] = {make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)};
+            if (type == BWD_DG) dgrad_mask_chunk0(B.dg, m * BM + 32 * q + lane, n * 64, pm);
+            mbar_wait(&tfull[acc], (k >> 1) & 1);
+            tc_fence_after();
+            const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BWD_ACC_COLS);
+            if (type == BWD_DG)
+                epilogue_tile<DGRAD_, 64, 3>(B.dg, tq, m, n, 0, q, lane, stg, buf, sw3, pm);
+            else
+                epilogue_tile<WGRAD_, 128, 1>(type == BWD_W2 ? B.w2 : B.w1, tq, m, n, sp, q, lane, stg, buf, sw3, pm);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_local(&tempty[acc]);
+            if (type == BWD_DG) {
+                // publish the tile once its stores have been performed
+                if (lane == 0) {
+                    bulk_wait_all();
+                    fence_proxy_async_all();
+                }
+                __syncwarp();
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (threadIdx.x == 64) {
+                    __threadfence();
+                    st_release_gpu_u32(B.st.flags + m * B.dg_ntiles + n, epoch);
+                }
+            }
+        }
+        if (lane == 0) bulk_wait_read<0>();
+    }
+    gemm_epilogue_done<512, false>(tbase, warp);
+    // the last CTA out publishes this launch's epoch (every CTA read the previous one at entry)
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&B.st.epoch[1], 1u) == gridDim.x - 1) {
+            B.st.epoch[1] = 0u;
+            __threadfence();
+            st_release_gpu_u32(&B.st.epoch[0], epoch);
+        }
+    }
+    trace_end(B.slot);
 }
 
 // ------------------------------------------------------------------ companions
