@@ -184,6 +184,7 @@ struct UmmaPlan {
 };
 void umma_plan_destroy(UmmaPlan* plan);
 bool umma_side_branch_enabled();  // false under TEM_NO_FORK (side branch serialised)
+bool umma_bwd_active(const UmmaPlan& P);  // the backward runs as one persistent launch
 void* umma_tstamp_buffer(int64_t* nbytes, int on);  // split-K phase timestamps (diagnostics)
 int umma_wgrad_splits(const Geom& g);
 bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan);

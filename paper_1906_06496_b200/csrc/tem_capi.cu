@@ -625,13 +625,16 @@ static tem_status compute_impl(tem_ctx* c, const void* x, const float* labels, f
         // are done (measured c2 195.5k -> 200.4k samples/s with the default 296-CTA grid; 16-64
         // CTAs were slower), the exchange then updates [0, off_W2) only.  Not with PGM-fed PEM,
         // whose gradient is produced after the compute.
-        c->split_n1 = defer && g.pgm_G == 0;
+        // the persistent backward has no side-branch WGRAD to hang the split update / early
+        // bucket off: the exchange then updates (or exchanges) the whole vector after it
+        const bool bwd = g.B > 0 && umma_bwd_active(*c->plan[l]);
+        c->split_n1 = defer && g.pgm_G == 0 && !bwd;
         su.n1_w2 = c->split_n1 ? 1 : 0;
         // bucketed exchange with one rank per process: the [bnd, K_pad) bucket starts inside the
         // compute (not with PGM-fed PEM, whose gradient is produced after it)
         RingParams early;
         c->early_done = false;
-        if (bucketed(c) && c->nlocal == 1 && fuse_reduce && g.B > 0 && g.pgm_G == 0) {
+        if (bucketed(c) && c->nlocal == 1 && fuse_reduce && g.B > 0 && g.pgm_G == 0 && !bwd) {
             early = step_ring(c, bucket_bound(c), g.Kpad);
             su.early = &early;
             su.early_kind = c->cfg.exchange;
@@ -722,8 +725,8 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
                              opt_state(c, 0), b.wpart, P.wgrad1.part_stride, g.off_W2, P.S1, b.wpart2,
                              P.wgrad2.part_stride, g.off_W2, (int64_t)3 * g.C * g.C, P.S2, s, false, 0, 2) != cudaSuccess)
             return TEM_ERR_CUDA;
-        c->grad_lazy = true;
         ++*nl;
+        c->grad_lazy = true;
         rec.end(SLOT_EXCHANGE);
         return opt_scalars(c, s, nl);
     }
@@ -1204,7 +1207,8 @@ void* tem_debug_buffer(tem_ctx* c, int32_t l, const char* name, int64_t* nbytes)
         {"pgm_iou", c->ws_base[l] + c->wl.pgm_iou, g.pgm_G > 0 ? (int64_t)g.B * g.pem_P * 4 : 0},
         {"pgm_ts", c->ws_base[l] + c->wl.pgm_ts, g.pgm_G > 0 ? (int64_t)g.B * g.pem_P * 4 : 0},
         {"pgm_te", c->ws_base[l] + c->wl.pgm_te, g.pgm_G > 0 ? (int64_t)g.B * g.pem_P * 4 : 0},
-        {"pgm_count", c->ws_base[l] + c->wl.pgm_count, g.pgm_G > 0 ? (int64_t)g.B * 4 : 0}};
+        {"pgm_count", c->ws_base[l] + c->wl.pgm_count, g.pgm_G > 0 ? (int64_t)g.B * 4 : 0},
+        {"bwd_tasks", b.bwd.tasks, (int64_t)1024 * BWD_MAX_TASKS * 4}};
     for (const Item& it : items)
         if (strcmp(it.n, name) == 0) {
             if (!it.p) return nullptr;

@@ -33,8 +33,10 @@
 #include <algorithm>
 #include <stdlib.h>
 #include <string.h>
+#include <vector>
 
 #include "kernels.h"
+#include "optim.cuh"
 #include "umma.cuh"
 
 namespace tem {
@@ -1117,6 +1119,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_kernel(const __grid_constant_
             const int acc = k & 1;
             mbar_wait(&tempty[acc], ((k >> 1) & 1) ^ 1);
             tc_fence_after();
+            if (lane == 0) tstamp_s(B.slot, 8 + k);  // diagnostics: task k's MMAs start
             const uint32_t dt = tbase + (uint32_t)(acc * BWD_ACC_COLS);
             if (type == BWD_DG)
                 halo_mma_tile<DGRAD_, 64, 3, 3, 6, false>(B.dg, sA, sB, fullA, emptyA, fullB, emptyB, dt, issuer, lane,
@@ -1154,6 +1157,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_kernel(const __grid_constant_
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_local(&tempty[acc]);
+            if (threadIdx.x == 64) tstamp_s(B.slot, k);  // diagnostics: task k's epilogue done
             if (type == BWD_DG) {
                 // publish the tile once its stores have been performed
                 if (lane == 0) {
@@ -1462,6 +1466,67 @@ cudaError_t launch_wgrad(const UmmaParams& p, cudaStream_t s) {
                              umma::CfgW<BN, NPASS, STAGES, PAIR>::SMEM, PAIR, total, &max_units, p, s);
 }
 
+// The persistent backward: one CTA per SM, all co-resident (cooperative launch).
+cudaError_t launch_bwd(const umma::BwdParams& p, int grid, cudaStream_t s) {
+    static bool init = false;
+    if (!init) {
+        cudaError_t e = cudaFuncSetAttribute(umma::bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)umma::BWD_SMEM);
+        if (e != cudaSuccess) return e;
+        init = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na++].val.cooperative = 1;
+    na += launch_priority_attr(&attr[na], false);
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(umma::NTHREADS);
+    cfg.dynamicSmemBytes = umma::BWD_SMEM;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, umma::bwd_kernel, p);
+}
+
+// Static task lists of the persistent backward (list scheduling on estimated task times): DGRAD
+// tile i first on CTA i, then the conv2 WGRAD tiles (no dependencies) and the conv1 WGRAD tiles
+// (ready once DGRAD is done) each on the CTA that frees up first.  Returns the grid, 0 if the
+// plan does not fit (then the three separate launches run).
+int bwd_schedule(const UmmaPlan& P, int grid, std::vector<int>& tasks) {
+    const int ndg = P.dgrad.mtiles * P.dgrad.ntiles;
+    if (ndg > grid || ndg > BWD_MAX_DG_TILES || P.dgrad.mtiles > 255 || P.dgrad.ntiles > 255) return 0;
+    // small batches (fewer DGRAD tiles than half the SMs, e.g. configs[0] B = 4) measured faster
+    // as three launches (57.0k vs 60.6k samples/s at B = 4; 202.6k vs 200.9k at B = 16)
+    if (2 * ndg < grid) return 0;
+    const double T_DG = 11.0, T_W = 8.0;  // us, measured per-task times at c2 (steady state)
+    std::vector<double> free_at(grid, 0.0);
+    std::vector<std::vector<int>> lists(grid);
+    for (int i = 0; i < ndg; ++i) {
+        lists[i].push_back((umma::BWD_DG << 24) | ((i / P.dgrad.ntiles) << 16) | ((i % P.dgrad.ntiles) << 8));
+        free_at[i] = T_DG;
+    }
+    auto add_wgrad = [&](const UmmaParams& W, int type, double ready) -> bool {
+        for (int sp = 0; sp < W.nsplit; ++sp)
+            for (int m = 0; m < W.mtiles; ++m)
+                for (int n = 0; n < W.ntiles; ++n) {
+                    int best = 0;
+                    for (int c = 1; c < grid; ++c)
+                        if (std::max(free_at[c], ready) < std::max(free_at[best], ready)) best = c;
+                    free_at[best] = std::max(free_at[best], ready) + T_W;
+                    if ((int)lists[best].size() >= BWD_MAX_TASKS - 1 || m > 255 || n > 255 || sp > 255) return false;
+                    lists[best].push_back((type << 24) | (m << 16) | (n << 8) | sp);
+                }
+        return true;
+    };
+    if (!add_wgrad(P.wgrad2, umma::BWD_W2, 0.0) || !add_wgrad(P.wgrad1, umma::BWD_W1, T_DG)) return 0;
+    tasks.assign((size_t)grid * BWD_MAX_TASKS, -1);
+    for (int c = 0; c < grid; ++c)
+        for (size_t k = 0; k < lists[c].size(); ++k) tasks[(size_t)c * BWD_MAX_TASKS + k] = lists[c][k];
+    return grid;
+}
+
 }  // namespace
 
 // Tile configurations per GEMM and precision (measured on B200):
@@ -1635,6 +1700,26 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
     if (b.dA1_lo) ok &= map_store2d(&P.dgrad.out[1], b.dA1_lo, false, g.C, R);
     ok &= map_store_part(&P.wgrad2.out[0], b.wpart2, 3 * (uint64_t)g.C, g.C, P.S2, P.wgrad2.part_stride);
     ok &= map_store_part(&P.wgrad1.out[0], b.wpart, 3 * (uint64_t)g.Cin, g.C, P.S1, P.wgrad1.part_stride);
+    // fp32 (3-pass, 1-CTA tiles): the backward as one persistent launch when its task lists fit
+    P.bwd = b.bwd;
+    P.bwd_grid = 0;
+    int sms = 0, coop = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, 0);
+    if (ok && P.npass == 3 && !cw.pair && !cfg_for(DGRAD_, 3).pair && cf.bn == 64 && cw.bn == 128 && coop &&
+        !getenv("TEM_NO_BWD") &&
+        cudaFuncSetAttribute(umma::bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)umma::BWD_SMEM) ==
+            cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, umma::bwd_kernel, umma::NTHREADS, umma::BWD_SMEM) ==
+            cudaSuccess &&
+        per_sm >= 1 && sms > 0 && sms <= 1024) {
+        std::vector<int> tasks;
+        const int grid = bwd_schedule(P, sms, tasks);
+        if (grid > 0 && cudaMemcpy(b.bwd.tasks, tasks.data(), tasks.size() * sizeof(int), cudaMemcpyHostToDevice) ==
+                            cudaSuccess)
+            P.bwd_grid = grid;
+    }
+    cudaGetLastError();
     return ok;
 }
 
@@ -1722,6 +1807,48 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
         return cudaSuccess;
     };
     if ((e = head_reduce()) != cudaSuccess) return e;
+    if (P.bwd_grid > 0) {
+        // fp32: conv2 DGRAD, conv2 WGRAD and conv1 WGRAD as one persistent launch (bwd_kernel);
+        // the side branch keeps only the head reduction
+        if (!no_fork && cudaEventRecord(P.join, P.aux) != cudaSuccess) return cudaErrorUnknown;
+        umma::BwdParams bp;
+        bp.dg = dg;
+        bp.w2 = P.wgrad2;
+        bp.w1 = P.wgrad1;
+        bp.st = P.bwd;
+        bp.dg_ntiles = P.dgrad.ntiles;
+        bp.status = status;
+        bp.slot = SLOT_BWD;
+        rec.begin(SLOT_BWD);
+        e = launch_bwd(bp, P.bwd_grid, s);
+        rec.end(SLOT_BWD);
+        if (e != cudaSuccess) return e;
+        ++n;
+        if (!defer_reduce) {
+            rec.begin(SLOT_RED2);
+            e = launch_pdl(umma::reduce_wgrad_kernel, dim3(296), dim3(256), 0, s, false, (const float*)b.wpart2,
+                           P.wgrad2.part_stride, P.S2, (int64_t)g.C * 3 * g.C, (const float*)nullptr, 0, g.C,
+                           b.grad + g.off_W2, (int)SLOT_RED2);
+            rec.end(SLOT_RED2);
+            if (e != cudaSuccess) return e;
+            ++n;
+            rec.begin(SLOT_RED1);
+            e = launch_pdl(umma::reduce_wgrad_kernel, dim3(296), dim3(256), 0, s, false, (const float*)b.wpart,
+                           P.wgrad1.part_stride, P.S1, (int64_t)g.C * 3 * g.Cin + g.C, (const float*)nullptr, 0,
+                           g.C, b.grad + g.off_W1, (int)SLOT_RED1);
+            rec.end(SLOT_RED1);
+            if (e != cudaSuccess) return e;
+            ++n;
+        }
+        if (!no_fork && cudaStreamWaitEvent(s, P.join, 0) != cudaSuccess) return cudaErrorUnknown;  // join
+        if (P.pem_pending) {
+            const_cast<UmmaPlan&>(P).pem_pending = false;
+            if (cudaEventRecord(P.pem_join, P.pem) != cudaSuccess || cudaStreamWaitEvent(s, P.pem_join, 0) != cudaSuccess)
+                return cudaErrorUnknown;
+        }
+        *nl += n;
+        return cudaSuccess;
+    }
     rec2.begin(SLOT_WGRAD2);
     e = dispatch<WGRAD_>(P.wgrad2, P.npass, aux);
     rec2.end(SLOT_WGRAD2);
@@ -1787,6 +1914,8 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     *nl += n;
     return cudaSuccess;
 }
+
+bool umma_bwd_active(const UmmaPlan& P) { return P.bwd_grid > 0; }
 
 bool umma_side_branch_enabled() { return getenv("TEM_NO_FORK") == nullptr; }
 

@@ -20,6 +20,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--flush", action="store_true", help="write 256 MiB (L2 flush) before every traced step, as bench.py")
     args = ap.parse_args()
     os.environ["TEM_DIAG_LIB"] = "1"  # traces / phase stamps exist only in the diagnostics build
     import numpy as np
@@ -54,10 +55,13 @@ def main():
     nslots = lib.tem_timing_slots(tem._P(s.ctx))
     names = [lib.tem_timing_slot_name(tem._P(s.ctx), i).decode() for i in range(nslots)]
     runs, heads = [], []
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     for _ in range(args.reps):
         init = torch.zeros(nb.value // 8, dtype=torch.int64)
         init[0:2 * nslots:2] = -1  # 0xFFFF... as u64: min() identity
         buf.copy_(init.view(torch.uint64) if hasattr(torch, "uint64") else init)
+        if args.flush:
+            flush.zero_()
         torch.cuda.synchronize()
         step()
         torch.cuda.synchronize()

@@ -165,3 +165,36 @@ def test_step_pem_host_matches_device_step(tem):
     assert np.array_equal(s2.params(0).cpu().numpy(), w1)
     assert datagen.PEM_P > 0
     s2.close()
+
+
+@pytest.mark.parametrize("B,N", [(16, 1), (12, 1), (12, 2)])
+def test_persistent_backward_is_bitwise_the_three_launches(tem, orc, monkeypatch, B, N):
+    """The fp32 backward as one persistent launch (bwd_kernel: DGRAD, conv2 WGRAD and conv1
+    WGRAD tiles of a static schedule, conv1 WGRAD waiting on DGRAD tile flags) runs each tile
+    through the same device code as the three separate launches (TEM_NO_BWD): the gradient,
+    logits and loss are bitwise identical, so are the parameters after two tem_steps, and the
+    gradient meets the oracle contract."""
+    lam, lr = (2.0, 1.0, 1.0), 0.05
+    outs = []
+    for no_bwd in (False, True):
+        if no_bwd:
+            monkeypatch.setenv("TEM_NO_BWD", "1")
+        s, p = session(tem, N, B, 0, lr=lr, lam=lam)
+        x, lab = make_inputs(N, B, 0, batch_idx=4)
+        xd, ld = to_dev_x(x, 0), torch.from_numpy(lab).cuda()
+        loss = s.compute(xd, ld)
+        assert s.sync()[0] == 0
+        g = np.stack([s.local_grad(r).cpu().numpy().copy() for r in range(N)])
+        z = s.logits(0).cpu().numpy().copy()
+        l0 = loss.cpu().numpy().copy()
+        if not no_bwd:  # (the ReLU decisions of this compute, before the steps)
+            ref = oracle_with_gpu_decisions(orc, s, 0, x[0], p, lab[0], lam, 0)
+            check_tensors(orc, g[0][:s.K], z, l0[0], ref, TOL[0])
+        for _ in range(2):
+            s.step(xd, ld)
+            assert s.sync()[0] == 0
+        w = s.params(0).cpu().numpy().copy()
+        outs.append((g, z, l0, w))
+        s.close()
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
