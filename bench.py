@@ -80,6 +80,7 @@ class ClockSampler:
         self.samples = []
         self.t0 = self.t1 = None
         self._stop = threading.Event()
+        self._paused = threading.Event()
         self.ok = False
         try:
             import pynvml
@@ -103,12 +104,22 @@ class ClockSampler:
 
     def _run(self):
         while not self._stop.is_set():
-            try:
-                sm = float(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
-                self.samples.append((time.perf_counter(), sm, self._reasons()))
-            except Exception:
-                pass
+            if not self._paused.is_set():
+                try:
+                    sm = float(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                    self.samples.append((time.perf_counter(), sm, self._reasons()))
+                except Exception:
+                    pass
             time.sleep(0.005)
+
+    def pause(self, on: bool):
+        """The NVML calls contend with the main thread's CUDA driver calls (measured: the
+        host-buffer loop ran at 80 us/step with the sampler polling, 72 without), so the
+        sampler is paused outside the device-timed region."""
+        if on:
+            self._paused.set()
+        else:
+            self._paused.clear()
 
     def start(self):
         if self.ok:
@@ -158,6 +169,18 @@ def bind_to_gpu_numa(index: int):
     except Exception:
         return None
     return None
+
+
+def warm_until(step, n, torch, min_s: float = 0.05):
+    """Run `n` steps, then more until >= min_s of continuous stepping has passed."""
+    t0 = time.perf_counter()
+    i = 0
+    while i < n or time.perf_counter() - t0 < min_s:
+        step(i)
+        i += 1
+        if i % 16 == 0:
+            torch.cuda.synchronize()
+    torch.cuda.synchronize()
 
 
 def host_info():
@@ -406,8 +429,9 @@ def main():
 
     clocks = ClockSampler(local)
     clocks.start()
-    for i in range(args.warmup):
-        do_step(i)
+    # W warm-up steps, continued until the GPU has been busy for >= 50 ms: measured on these
+    # boxes, the first tens of ms of steps after an idle period run up to 35 % slower
+    warm_until(do_step, args.warmup, torch)
     code, _ = sess.sync()
     if code != 0:
         raise tem.TemError(code, "warmup")
@@ -456,6 +480,7 @@ def main():
 
     # ---------------- end to end through the C ABI with host buffers ----------------
     e2e = None
+    clocks.pause(True)
     if not args.no_e2e:
         if prec == 1:
             xh = [torch.from_numpy(datagen.to_bf16_bits(datagen.features(B, rank=rank, batch_idx=k)).view(np.int16)).pin_memory()
@@ -478,9 +503,7 @@ def main():
         else:
             def host_step(i):
                 sess.step_host(xh[i % 2], lh[i % 2], loss_h)
-        for i in range(2):
-            host_step(i)
-        torch.cuda.synchronize()
+        warm_until(host_step, max(2, args.warmup), torch)
         # One span over all K steps: the library copies step k+1's inputs on its copy stream while
         # step k computes, so per-step spans would not see the copies.  No L2 flush inside the
         # span (a flush between steps would hide copy time under a subtracted interval); every
@@ -565,6 +588,7 @@ def main():
                                  "twoshot": "NVSwitch two-shot allreduce + mean + SGD (ring-identical bits)"}.get(
                                      args.exchange, "fused ring allreduce + mean + SGD (KR1)")),
                    "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                   "warmup": f"{args.warmup} steps, continued until >= 50 ms of stepping",
                    "kernel_path": sess.kernel_path(),
                    **({"pem": f"{P} proposals/video, 32-d BSP features, MLP 32->512->1, gradient [TEM | PEM] "
                               f"= {sess.K} elements in one exchange"} if P else {}),
