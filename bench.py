@@ -55,6 +55,8 @@ FLOPS_PER_SAMPLE = {
     "conv2_dgrad": 2 * T * C * 3 * C,      # 157.29 M
     "conv2_wgrad": 2 * T * C * 3 * C,      # 157.29 M
     "conv1_wgrad": 2 * T * C * 3 * CIN,    # 122.88 M
+    # fp32 persistent backward (bwd_kernel): conv2 DGRAD + conv2 WGRAD + conv1 WGRAD in one launch
+    "backward": 2 * T * C * 3 * C * 2 + 2 * T * C * 3 * CIN,  # 437.46 M
 }
 
 
