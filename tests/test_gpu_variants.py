@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 import torch
 
-from test_gpu_parity import (TOL, check_tensors, make_inputs, oracle_with_gpu_decisions, session,  # noqa: F401
+from test_gpu_parity import (TOL, check_tensors, make_inputs, oracle_with_gpu_decisions, rel_err, session,  # noqa: F401
                              tem, to_dev_x)
 
 pytestmark = pytest.mark.gpu
@@ -198,3 +198,37 @@ def test_persistent_backward_is_bitwise_the_three_launches(tem, orc, monkeypatch
         s.close()
     for a, b in zip(outs[0], outs[1]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("N", [1, 2])
+def test_operand_sets_follow_every_update(tem, orc, N):
+    """The weights' bf16 operand copies alternate between two sets (RankBufs::shadow): a step's
+    GEMMs read one, its update writes the other.  Mixing graph-replayed tem_step calls with
+    tem_compute + tem_exchange (eager) must keep every step on the current weights: after each
+    update the parameters equal the oracle's ring SGD of the GPU's own gradient (bitwise), the
+    operand copy the next step reads is bf16 of those parameters (bitwise), and the next loss
+    matches the oracle at those parameters."""
+    B, lr, lam = 2, 0.05, (2.0, 1.0, 1.0)
+    s, p = session(tem, N, B, 0, lr=lr, lam=lam)
+    xd = torch.empty(N, B, 100, 400, device="cuda")
+    ld = torch.empty(N, B, 3, 100, device="cuda")
+    for it, how in enumerate(["step", "split", "step", "step", "split", "step"]):
+        x, lab = make_inputs(N, B, 0, batch_idx=it)
+        xd.copy_(torch.from_numpy(x))
+        ld.copy_(torch.from_numpy(lab))
+        w0 = s.params(0).cpu().numpy().copy()
+        sh = s.debug_buffer("shadow").float().cpu().numpy()
+        assert np.array_equal(sh, orc.bf16_round(w0)), (it, "operand copy of the current weights")
+        if how == "step":
+            loss = s.step(xd, ld)
+        else:
+            loss = s.compute(xd, ld)
+            s.exchange()
+        assert s.sync()[0] == 0
+        g = np.stack([s.local_grad(r).cpu().numpy() for r in range(N)])
+        ref = orc.tem_fwd_bwd(x[0], w0, lab[0], lam, prec=0)
+        assert rel_err(loss[0].cpu().numpy(), ref["loss"]) <= TOL[0], it
+        expect = orc.ring_sgd(g, w0, lr)
+        for r in range(N):
+            assert np.array_equal(s.params(r).cpu().numpy(), expect[r]), (it, r)
+    s.close()
