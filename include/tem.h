@@ -292,7 +292,7 @@ float* tem_local_grad(tem_ctx* ctx, int32_t local_rank);
 float* tem_logits(tem_ctx* ctx, int32_t local_rank);     /* [B][T][3] fp32 z, last compute */
 /* Device address and size of an internal workspace tensor of local rank `local_rank`, for
  * tests: "xp", "h1", "h2", "dA2", "dA1" (halo-padded [B][T+2][C] rows in the path's operand
- * type; h2 fp32), their residual planes "xp_lo", "h1_lo", "dA2_lo", "dA1_lo", and the weight
+ * type; h2 fp32, not written when the head is fused into conv2), their residual planes "xp_lo", "h1_lo", "dA2_lo", "dA1_lo", and the weight
  * operand copies "shadow", "shadow_lo" ([K_pad] bf16).  Diagnostics: "tstamp_on" / "tstamp"
  * enable / disable the split-K GEMM phase timestamps ([1024][16] u64 ns).  NULL / 0 if absent. */
 void* tem_debug_buffer(tem_ctx* ctx, int32_t local_rank, const char* name, int64_t* nbytes);

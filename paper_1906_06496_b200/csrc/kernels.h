@@ -118,6 +118,8 @@ struct RankBufs {
     float* wpart;         // [S][max(C*3*Cin + C, C*3*C + C)] split-K partials (conv1 wgrad; SIMT: both)
     float* wpart2;        // [S][C*3*C + C] split-K partials of the tcgen05 conv2 wgrad
     int64_t* stepctr;     // step counter for NONFINITE reporting
+    uint64_t* dec2;       // [R][C / 64] conv2 ReLU decision masks (fused head: h2 is not stored)
+    int dec2_valid;       // 1 when the plan fuses the head (dec2 holds the decisions, not h2)
     BwdState bwd;         // persistent-backward task lists / flags (workspace)
     // bf16 operand copies of the weights, TWO sets [2][Kpad] (ping-pong): a step's GEMMs read
     // set `wset` while its updates write set 1 - wset, so an update may run while a GEMM of
@@ -160,6 +162,7 @@ struct UmmaParams {
                          // on SMs the concurrent side branch could use while waiting)
     // conv2 FWD with the fused head (fp32 single-wave path, clusters of ntiles CTAs):
     int fused_head;
+    uint64_t* dec2;        // [R][Nout / 64] conv2 ReLU decisions (bit i: column 64 k + i), fused head
     CUtensorMap out2[2];   // dA2 hi / lo store maps
     const float* labels;   // [B][3][T] (per call)
     float lam[3];          // per call

@@ -76,7 +76,8 @@ cudaError_t launch_prep_x(const Geom& g, const void* x, void* xp, cudaStream_t s
 
 template <typename T>
 __global__ void relu_decisions_kernel(const T* __restrict__ h1, const float* __restrict__ h2,
-                                      uint8_t* __restrict__ out, int B, int Tn, int C) {
+                                      const uint64_t* __restrict__ dec2, uint8_t* __restrict__ out, int B,
+                                      int Tn, int C) {
     const int64_t n = (int64_t)B * Tn * C;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
          e += (int64_t)gridDim.x * blockDim.x) {
@@ -85,13 +86,14 @@ __global__ void relu_decisions_kernel(const T* __restrict__ h1, const float* __r
         const int64_t v = r / Tn, t = r - v * Tn;
         const int64_t p = v * (Tn + 2) + t + 1;
         out[e] = to_f(h1[p * C + c]) > 0.f ? 1 : 0;
-        out[n + e] = h2[p * C + c] > 0.f ? 1 : 0;
+        out[n + e] = dec2 ? (uint8_t)((dec2[p * (C / 64) + c / 64] >> (c % 64)) & 1u)  // fused head
+                          : (h2[p * C + c] > 0.f ? 1 : 0);
     }
 }
 
 cudaError_t launch_relu_decisions(const Geom& g, const RankBufs& b, uint8_t* out, cudaStream_t s) {
-    relu_decisions_kernel<__nv_bfloat16><<<296, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(b.h1), b.h2, out,
-                                                             g.B, g.T, g.C);
+    relu_decisions_kernel<__nv_bfloat16><<<296, 256, 0, s>>>(static_cast<const __nv_bfloat16*>(b.h1), b.h2,
+                                                             b.dec2_valid ? b.dec2 : nullptr, out, g.B, g.T, g.C);
     return cudaGetLastError();
 }
 

@@ -59,7 +59,7 @@ struct HeapLayout {
 
 struct WsLayout {
     size_t xp, h1, h2, dA2, dA1, xp_lo, h1_lo, dA2_lo, dA1_lo, z, grad, headpart, headlvl1, counter, bpart, wpart, wpart2, shadow,
-        shadow_lo, ones, zpart, epochs, stepctr, bwd_tasks, bwd_flags, bwd_epoch, xstage, labstage, lossstage, bspstage, ioustage, pempart, pemdec, opt_m, opt_v, opt_scal,
+        shadow_lo, ones, zpart, epochs, stepctr, dec2, bwd_tasks, bwd_flags, bwd_epoch, xstage, labstage, lossstage, bspstage, ioustage, pempart, pemdec, opt_m, opt_v, opt_scal,
         pgm_prob, pgm_feat, pgm_iou, pgm_ts, pgm_te, pgm_count, trace, per_rank;
 };
 
@@ -200,6 +200,7 @@ WsLayout ws_layout(const tem_config* c) {
     w.zpart = take((size_t)(g.C / 64) * g.R * 3 * 4);
     w.epochs = take((size_t)kMaxChannels * 4);
     w.stepctr = take(8);
+    w.dec2 = take((size_t)g.R * (g.C / 64) * 8);
     w.bwd_tasks = take((size_t)1024 * BWD_MAX_TASKS * 4);  // persistent backward (UmmaPlan::bwd_grid)
     w.bwd_flags = take((size_t)BWD_MAX_DG_TILES * 4);
     w.bwd_epoch = take(2 * 4);
@@ -458,6 +459,7 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
         b.pempart = (float*)(base + wl.pempart);
         b.pemdec = (uint8_t*)(base + wl.pemdec);
         b.stepctr = (int64_t*)(base + wl.stepctr);
+        b.dec2 = (uint64_t*)(base + wl.dec2);
         b.bwd.tasks = (int*)(base + wl.bwd_tasks);
         b.bwd.flags = (unsigned*)(base + wl.bwd_flags);
         b.bwd.epoch = (unsigned*)(base + wl.bwd_epoch);
@@ -481,6 +483,7 @@ tem_status tem_init(const tem_config* cfg, float* params, tem_ctx** out) {
             c->plan[l] = new (std::nothrow) UmmaPlan();
             if (!c->plan[l] || !umma_plan(c->g, b, c->plan[l])) e = cudaErrorInvalidValue;
             else b.nzpart = c->plan[l]->conv2.zpart ? c->plan[l]->conv2.ntiles : 0;
+            b.dec2_valid = c->plan[l] && c->plan[l]->conv2.fused_head ? 1 : 0;
         }
         if (e != cudaSuccess) {
             for (int q = 0; q <= l; ++q) umma_plan_destroy(c->plan[q]);

@@ -154,6 +154,7 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
     const bool halo = (MODE != WGRAD_) && (row >= P.R || halo_row(row, P.Tp));
     const float* sbias = sw3 + 3 * 512;
     float zp0 = 0.f, zp1 = 0.f, zp2 = 0.f;  // FWD conv2: partial logits W3 . h2 over this tile's columns
+    uint64_t dmask = 0;                      // fused head: this row's conv2 ReLU decisions (BN <= 64)
 
     // Issue the TMEM load (and the DGRAD mask load) of chunk c16; consumed after tmem_ld_wait.
     auto issue = [&](int c16, EpiRegs& e) {
@@ -224,6 +225,16 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
                     zp2 = fmaf(c.x, hv[0], zp2); zp2 = fmaf(c.y, hv[1], zp2); zp2 = fmaf(c.z, hv[2], zp2); zp2 = fmaf(c.w, hv[3], zp2);
                 }
             }
+            // the fused head consumes h2 from this CTA's accumulator (head_tail), so conv2's h2
+            // is not stored; only its ReLU decisions are, one 64-bit mask per row and column tile
+            // (stored after the chunk loop; tem_relu_decisions)
+            if (zloc) {
+                uint32_t bits = 0;
+#pragma unroll
+                for (int i = 0; i < 16; ++i) bits |= (v[i] > 0.f ? 1u : 0u) << i;
+                dmask |= (uint64_t)bits << (c16 * 16);
+                return;
+            }
         } else if (MODE == DGRAD_) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
@@ -281,6 +292,7 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
         process(c16 + 1, eb);
         if (MODE == WGRAD_ && threadIdx.x == 64) tstamp_s(P.slot, 9 + c16);
     }
+    if (MODE == FWD_ && zloc && row < P.R) P.dec2[(size_t)row * (P.Nout / 64) + n_tile] = dmask;
     if (MODE == FWD_ && zloc) {
         // fused head: push this tile's partial logits into slot n_tile of every CTA of the
         // cluster (zloc = the receive buffer [ntiles][BM][4]; distributed-shared-memory stores)
@@ -1648,6 +1660,7 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
         P.conv2.b3 = b.params + g.off_b3;
         P.conv2.z_out = b.z;
         P.conv2.headpart = b.headpart;
+        P.conv2.dec2 = b.dec2;
         P.conv2.Bv = g.B;
         P.conv2.Tn = g.T;
         ok &= map_store2d(&P.conv2.out2[0], b.dA2, false, g.C, R);
