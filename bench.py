@@ -546,23 +546,16 @@ def main():
         avg_s = conv[dom] / nrec / 1e3
         achieved = FLOPS_PER_SAMPLE[dom] * B / avg_s / 1e12
         kpath = sess.kernel_path()
-        if kpath.startswith("simt"):
-            peak = 148 * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12
-            roof = {"bound": "alu", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak, "traffic": None,
-                    "peak_source": f"FP32 FMA: 148 SM x 128 lanes x 2 x {peaks['sm_max_mhz']:.0f} MHz "
-                                   f"(sm_max_mhz, {peak_src}) -- DESIGN.md 7"}
-        else:
-            # the slot is one kernel timed alone for ~20 us: the BURST bf16 peak applies
-            # (B200_PROFILING.md), not the sustained one of a long back-to-back run
-            key = "bf16_tflops"
-            bf16 = peaks.get(key)
-            # fp32 path: three bf16 products per fp32 MAC (hi*hi + hi*lo + lo*hi, R16)
-            peak = bf16 if prec == 1 else bf16 / 3.0
-            roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                    "frac": achieved / peak, "traffic": None,
-                    "peak_source": f"{key} (burst, {peak_src}: the slot is one isolated ~20 us kernel)" +
-                                   ("" if prec == 1 else " / 3 (3 bf16 tensor-core products per fp32 MAC, DESIGN.md R16)")}
+        # the slot is one kernel timed alone for 20-40 us: the BURST bf16 peak applies
+        # (B200_PROFILING.md), not the sustained one of a long back-to-back run
+        key = "bf16_tflops"
+        bf16 = peaks.get(key)
+        # fp32 path: three bf16 products per fp32 MAC (hi*hi + hi*lo + lo*hi, R16)
+        peak = bf16 if prec == 1 else bf16 / 3.0
+        roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None,
+                "peak_source": f"{key} (burst, {peak_src}: the slot is one isolated kernel)" +
+                               ("" if prec == 1 else " / 3 (3 bf16 tensor-core products per fp32 MAC, DESIGN.md R16)")}
         tr = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tr):
             try:

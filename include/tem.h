@@ -314,7 +314,7 @@ int32_t tem_timing_slots(tem_ctx* ctx);
 const char* tem_timing_slot_name(tem_ctx* ctx, int32_t slot);
 tem_status tem_timing_begin(tem_ctx* ctx, int32_t max_steps);
 tem_status tem_timing_end(tem_ctx* ctx, float* sum_ms, int32_t* steps);
-/* Kernel-path description (e.g. "simt-fp32", "tcgen05-bf16") for reports. */
+/* Kernel-path description ("tcgen05-bf16x3-fp32" or "tcgen05-bf16") for reports. */
 const char* tem_kernel_path(tem_ctx* ctx);
 
 #ifdef __cplusplus

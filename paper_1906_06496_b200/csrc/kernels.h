@@ -115,7 +115,7 @@ struct RankBufs {
     void* ones;           // [R][128] bf16 ones/zeros operand for the bias-gradient column
     float* zpart;         // [C/BN][R][3] partial logits from the conv2 epilogue (tcgen05), or nullptr
     int nzpart;           // number of partial-logit planes (C / conv2 tile width); 0 = head computes z
-    float* wpart;         // [S][max(C*3*Cin + C, C*3*C + C)] split-K partials (conv1 wgrad; SIMT: both)
+    float* wpart;         // [S][C*3*Cin + C] split-K partials of conv1 wgrad (and its bias column)
     float* wpart2;        // [S][C*3*C + C] split-K partials of the tcgen05 conv2 wgrad
     int64_t* stepctr;     // step counter for NONFINITE reporting
     uint64_t* dec2;       // [R][C / 64] conv2 ReLU decision masks (fused head: h2 is not stored)
