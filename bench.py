@@ -112,7 +112,7 @@ class ClockSampler:
                     self.samples.append((time.perf_counter(), sm, self._reasons()))
                 except Exception:
                     pass
-            time.sleep(0.005)
+            time.sleep(0.010)  # NVML calls take a driver lock: poll sparingly
 
     def pause(self, on: bool):
         """The NVML calls contend with the main thread's CUDA driver calls (measured: the
