@@ -280,7 +280,12 @@ tem_status tem_pgm(int32_t B, int32_t T, int32_t G, int32_t P, const float* prob
  * For NONFINITE, *bad_step (if non-NULL) receives the 0-based step index. */
 tem_status tem_sync(tem_ctx* ctx, void* stream, int64_t* bad_step);
 
-/* Collective teardown.  NULL is a no-op (returns TEM_OK).  Returns any latched error. */
+/* Teardown: the "closing" half of the paper's preparation time t3 / P ("the
+ * preparation time for opening and closing deep learning platform"; tem_init is the opening).
+ * Synchronises the device, frees the host context, the pinned status word, the graphs and the
+ * library's streams / events; the caller's device memory is untouched (it owns it).  Every rank
+ * calls it after its last collective; it issues no collective itself.  NULL is a no-op
+ * (returns TEM_OK).  Returns any latched error (PROTOCOL / TRANSPORT / NONFINITE / CUDA). */
 tem_status tem_shutdown(tem_ctx* ctx);
 
 /* --- introspection for tests and benchmarks (device pointers owned by the workspace) --- */
