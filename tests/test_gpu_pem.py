@@ -111,3 +111,31 @@ def test_tem_only_calls_rejected_on_pem_config(tem):
     with pytest.raises(tem.TemError):
         s.step(to_dev_x(x, 0), torch.from_numpy(lab).cuda())
     s.close()
+
+
+def test_pem_bench_config_steps(tem, orc):
+    """The configs[4] call bench.py times (B = 16 videos x 128 proposals, fp32, N = 1, graph-
+    replayed tem_step_pem; the fp32 backward runs as the persistent bwd_kernel at this size):
+    per step, the TEM tensors and the PEM tensors against their oracles at that step's weights,
+    and the new weights bitwise equal to the oracle's SGD on the GPU's own gradient."""
+    B, lr, lam = 16, 0.05, (2.0, 1.0, 1.0)
+    s, p = pem_session(tem, 1, B, lr=lr, lam=lam)
+    s.pem_record_decisions()
+    Kt = datagen.num_params()
+    for it in range(2):
+        x, lab = make_inputs(1, B, 0, batch_idx=it)
+        f, g = pem_inputs(1, B, batch_idx=it)
+        w0 = s.params(0).cpu().numpy().copy()
+        tl, pl = s.step_pem(to_dev_x(x, 0), torch.from_numpy(lab).cuda(), torch.from_numpy(f).cuda(),
+                            torch.from_numpy(g).cuda())
+        assert s.sync()[0] == 0
+        grad = s.local_grad(0).cpu().numpy().copy()
+        ref = oracle_with_gpu_decisions(orc, s, 0, x[0], w0[:Kt], lab[0], lam, 0)
+        check_tensors(orc, grad[:Kt], s.logits(0).cpu().numpy(), tl[0].cpu().numpy(), ref, TOL[0])
+        pref = pem_oracle_with_gpu_decisions(orc, s, 0, f[0].reshape(B * P, F), w0[Kt:s.K], g[0].ravel())
+        for name, sl in orc.pem_param_slices(F, H).items():
+            e = rel_err(grad[Kt:Kt + datagen.pem_num_params()][sl], pref["grad"][sl])
+            assert e <= TOL[0], (it, name, e)
+        assert abs(float(pl[0]) - pref["loss"]) <= TOL[0] * pref["loss"]
+        assert np.array_equal(s.params(0).cpu().numpy(), orc.ring_sgd(grad[None, :], w0, lr)[0]), it
+    s.close()

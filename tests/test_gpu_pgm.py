@@ -131,7 +131,7 @@ def test_pgm_fed_step_composition(tem, orc):
     assert e <= 1e-3  # (ReLU decisions inside the band may differ; the bitwise check above is the contract)
 
 
-@pytest.mark.parametrize("N,B", [(1, 8), (2, 2), (3, 1)])
+@pytest.mark.parametrize("N,B", [(1, 8), (1, 16), (2, 2), (3, 1)])
 def test_pgm_fed_steps_exchange(tem, orc, N, B):
     """Graph-replayed PGM-fed steps: every rank's params after each step equal the oracle's ring
     replay (mean + SGD) of the GPU's concatenated [TEM | PEM] local gradients, bitwise."""
