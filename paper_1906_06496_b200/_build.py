@@ -42,7 +42,9 @@ def build(force: bool = False, verbose: bool = False, diag: bool = False) -> str
     if not force and up_to_date(out):
         return out
     tmp = out + f".tmp{os.getpid()}"
-    cmd = [NVCC, *ARCH, *FLAGS, *(["-DTEM_DIAG"] if diag else []), *sources(), "-o", tmp]
+    # TEM_DIAG_NVCC_EXTRA: extra nvcc flags for diagnostics builds (experiments, e.g. -DTEM_HALO_TPS=3)
+    extra = (["-DTEM_DIAG"] + os.environ.get("TEM_DIAG_NVCC_EXTRA", "").split()) if diag else []
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, *sources(), "-o", tmp]
     r = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(HERE, "build_diag.log" if diag else "build.log")
     with open(log, "w") as f:

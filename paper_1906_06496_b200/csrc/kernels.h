@@ -189,6 +189,8 @@ void umma_plan_destroy(UmmaPlan* plan);
 bool umma_side_branch_enabled();  // false under TEM_NO_FORK (side branch serialised)
 bool umma_bwd_active(const UmmaPlan& P);  // the backward runs as one persistent launch
 void* umma_tstamp_buffer(int64_t* nbytes, int on);  // split-K phase timestamps (diagnostics)
+void* umma_tclk_buffer(int64_t* nbytes);            // SM clock stamps (diagnostics)
+void umma_set_probe_skip(int bits);                  // operand-skip probe (diagnostics build only)
 int umma_wgrad_splits(const Geom& g);
 bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan);
 cudaError_t launch_fill_ones(void* ones, int64_t rows, cudaStream_t s);

@@ -1193,6 +1193,13 @@ void* tem_debug_buffer(tem_ctx* c, int32_t l, const char* name, int64_t* nbytes)
 #endif
     if (strcmp(name, "tstamp_on") == 0 || strcmp(name, "tstamp") == 0)
         return umma_tstamp_buffer(nbytes, strcmp(name, "tstamp_on") == 0 ? 1 : 0);
+#ifdef TEM_DIAG
+    if (strcmp(name, "tclk") == 0) return umma_tclk_buffer(nbytes);
+    if (strncmp(name, "probe_skip:", 11) == 0) {  // diagnostics: skip FWD/DGRAD operand loads
+        umma_set_probe_skip(atoi(name + 11));
+        return nullptr;
+    }
+#endif
     if (strncmp(name, "tstamp_slot:", 12) == 0)  // stamps of one launch: "tstamp_slot:<Slot>"
         return umma_tstamp_buffer(nbytes, 100 + atoi(name + 12));
     const Geom& g = c->g;

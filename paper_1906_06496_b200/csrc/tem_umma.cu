@@ -59,9 +59,31 @@ TEM_DEV void tstamp(int k) {
 TEM_DEV void tstamp_s(int slot, int k) {
     if (g_tstamp_on == 100 + slot) g_tstamp[blockIdx.x * 16 + k] = globaltimer();
 }
+// either mode: every launch (1) or this launch's slot (100 + slot)
+TEM_DEV void tstamp2(int slot, int k) {
+    const int on = g_tstamp_on;
+    if (on == 1 || on == 100 + slot) g_tstamp[blockIdx.x * 16 + k] = globaltimer();
+}
+// SM clock stamps beside them ([grid][4] clock64, tem_debug_buffer "tclk")
+__device__ long long g_tclk[1024 * 4];
+TEM_DEV void tclk(int slot, int k) {
+    const int on = g_tstamp_on;
+    if (on == 1 || on == 100 + slot) g_tclk[blockIdx.x * 4 + k] = clock64();
+}
+// operand-skip probe (tem_debug_buffer "probe_skip:<bits>"): bit 0 skips the FWD/DGRAD A-window
+// loads, bit 1 the B-tap loads (FWD only) -- the barriers complete with no bytes and the MMAs
+// read the rings, zeroed at kernel entry
+__device__ int g_probe_skip;
+TEM_DEV int probe_skip() { return g_probe_skip; }
 #else
 TEM_DEV void tstamp(int) {}
 TEM_DEV void tstamp_s(int, int) {}
+TEM_DEV void tstamp2(int, int) {}
+TEM_DEV void tclk(int, int) {}
+TEM_DEV constexpr int probe_skip() { return 0; }
+#endif
+#ifndef TEM_HALO_TPS
+#define TEM_HALO_TPS 1
 #endif
 
 TEM_DEV bool halo_row(int p, int Tp) {
@@ -282,7 +304,7 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
         }
         issue(c16 + 1, eb);
         process(c16, ea);
-        if (MODE == WGRAD_ && threadIdx.x == 64) tstamp_s(P.slot, 8 + c16);  // diagnostics
+        if (threadIdx.x == 64) tstamp_s(P.slot, 8 + c16);  // diagnostics
         tmem_ld_wait_regs(eb.r);
         if (ACC == 3) {
             tmem_regs_fence(eb.r2);
@@ -290,7 +312,7 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
         }
         if (c16 + 2 < NC) issue(c16 + 2, ea);
         process(c16 + 1, eb);
-        if (MODE == WGRAD_ && threadIdx.x == 64) tstamp_s(P.slot, 9 + c16);
+        if (threadIdx.x == 64) tstamp_s(P.slot, 9 + c16);
     }
     if (MODE == FWD_ && zloc && row < P.R) P.dec2[(size_t)row * (P.Nout / 64) + n_tile] = dmask;
     if (MODE == FWD_ && zloc) {
@@ -408,7 +430,7 @@ TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, ui
         mbar_wait(&tfull[acc], (t >> 1) & 1);
         tc_fence_after();
         if (t == 0 && threadIdx.x == 64) {  // diagnostics: the accumulator is complete
-            tstamp(5);
+            tstamp2(P.slot, 5);
             tstamp_s(P.slot, 5);
         }
         const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * ACC * BN);
@@ -445,7 +467,7 @@ struct CfgHalo {
     // commit per tap costs ~270 clk of MMA bubble (scripts/probes/mma_dual_probe.cu: 121 -> 189
     // clk per K-step pair at BN = 64), but one stage per 3-tap chunk (TPS = 3, 2 stages of 48 KB)
     // measured no faster in the kernel (DGRAD mainloop 11.2 vs 11.7 us; slot 22.5 vs 20.9 us)
-    static constexpr int TPS = 1;
+    static constexpr int TPS = (SB % TEM_HALO_TPS == 0) ? TEM_HALO_TPS : 1;
     static constexpr int SBS = SB / TPS;  // barrier stages
     static constexpr uint32_t RINGS = SA * A_STAGE + SB * B_STAGE;
     static constexpr uint32_t SMEM = RINGS + 1024 /*align*/ + 1024 /*barriers*/ + EPI_SMEM;
@@ -510,11 +532,11 @@ TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const f
     float* lred = reinterpret_cast<float*>(smem + HEAD_LRED_OFF);  // [BM][6] (rank 0)
     const int S = P.ntiles, r = n_tile;
     const int C = P.Nout, m0 = m_tile * BM, n0 = n_tile * BN;
-    if (threadIdx.x == 64) tstamp(8);
+    if (threadIdx.x == 64) tstamp2(P.slot, 8);
     tc_fence_before();
     cluster_sync();  // every column tile has pushed its partial logits into every CTA's zrecv
     tc_fence_after();
-    if (threadIdx.x == 64) tstamp(9);
+    if (threadIdx.x == 64) tstamp2(P.slot, 9);
     if (warp >= 2) {
         const int q = warp & 3, row = 32 * q + lane, p = m0 + row;
         const int Tp = P.Tp, Tn = P.Tn;
@@ -556,7 +578,7 @@ TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const f
                 lred[row * 6 + 3 + o] = dz[o];
             }
         }
-        if (threadIdx.x == 64) tstamp(10);
+        if (threadIdx.x == 64) tstamp2(P.slot, 10);
         // dA2 for this CTA's columns (h2 recomputed from the accumulator exactly as the epilogue)
         const float* sw3 = reinterpret_cast<const float*>(epi + EPI_BYTES);
         const float* sbias = sw3 + 3 * 512;
@@ -577,7 +599,7 @@ TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const f
                 tmem_regs_fence(rb);
                 tmem_regs_fence(rc);
             }
-            if (c16 == 0 && threadIdx.x == 64) tstamp(13);
+            if (c16 == 0 && threadIdx.x == 64) tstamp2(P.slot, 13);
             float dv[16], hv[16];
             const float4* w0p = reinterpret_cast<const float4*>(sw3 + gc);
             const float4* w1p = reinterpret_cast<const float4*>(sw3 + C + gc);
@@ -602,7 +624,7 @@ TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const f
                     hv[i] = h;
                 }
             }
-            if (c16 == 0 && threadIdx.x == 64) tstamp(14);
+            if (c16 == 0 && threadIdx.x == 64) tstamp2(P.slot, 14);
             // hi / lo operand planes of dA2 (R16) and the stored value hi + lo for db2
             uint32_t hp[8], lp[8];
 #pragma unroll
@@ -637,10 +659,10 @@ TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const f
                 bulk_commit();
             }
             buf ^= 1;
-            if (c16 == 0 && threadIdx.x == 64) tstamp(15);
+            if (c16 == 0 && threadIdx.x == 64) tstamp2(P.slot, 15);
         }
         if (lane == 0) bulk_wait_read<0>();
-        if (threadIdx.x == 64) tstamp(11);
+        if (threadIdx.x == 64) tstamp2(P.slot, 11);
     }
     __syncthreads();  // column partials of all rows in shared memory
     float* dst = P.headpart + (size_t)m_tile * (4 * C + 8);  // [dW3 (3C)][db3 (3)][L (3)][db2 (C)]
@@ -656,7 +678,7 @@ TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const f
         if (threadIdx.x < 3) dst[3 * C + 3 + threadIdx.x] = -acc / (float)P.Tn;  // loss sum
         else dst[3 * C + threadIdx.x - 3] = acc;                                  // db3
     }
-    if (threadIdx.x == 64) tstamp(12);
+    if (threadIdx.x == 64) tstamp2(P.slot, 12);
     // no second cluster barrier: every remote access (the pushes) happened before the first
 }
 
@@ -671,20 +693,23 @@ TEM_DEV void halo_load_tile(const UmmaParams& P, uint8_t* sA, uint8_t* sB, uint6
     constexpr int NPL = C_::NPL;
     const int m0 = m_tile * BM;
     const int n0 = n_tile * BN + (int)rank * C_::BR;
+    const bool skipA = MODE == FWD_ && (probe_skip() & 1), skipB = MODE == FWD_ && (probe_skip() & 2);  // diag
     for (int cb = 0; cb < P.cpb; ++cb) {
         const int sa = ia % SA;
         mbar_wait(&emptyA[sa], ((ia / SA) & 1) ^ 1);
-        if (pe && leader) mbar_arrive_expect_tx(&fullA[sa], (PAIR ? 2 : 1) * C_::A_TX);
+        if (pe && leader) mbar_arrive_expect_tx(&fullA[sa], skipA ? 0u : (PAIR ? 2 : 1) * C_::A_TX);
 #pragma unroll
         for (int pl = 0; pl < NPL; ++pl)
-            if (pe) ld2d<PAIR>(sA + sa * C_::A_STAGE + pl * C_::A_PLANE, &P.a[pl], &fullA[sa], cb * BK, m0 - 1);
+            if (pe && !skipA) ld2d<PAIR>(sA + sa * C_::A_STAGE + pl * C_::A_PLANE, &P.a[pl], &fullA[sa], cb * BK, m0 - 1);
         ++ia;
         for (int j = 0; j < 3; ++j, ++ib) {
             const int sb = ib % SB;                          // tap slot
             const int bs = (ib / C_::TPS) % C_::SBS;         // barrier stage
             const bool first = (ib % C_::TPS) == 0;
             if (first) mbar_wait(&emptyB[bs], ((ib / C_::TPS / C_::SBS) & 1) ^ 1);
-            if (pe && leader && first) mbar_arrive_expect_tx(&fullB[bs], (PAIR ? 2 : 1) * C_::TPS * C_::B_STAGE);
+            if (pe && leader && first)
+                mbar_arrive_expect_tx(&fullB[bs], skipB ? 0u : (PAIR ? 2 : 1) * C_::TPS * C_::B_STAGE);
+            if (skipB) continue;
 #pragma unroll
             for (int pl = 0; pl < NPL; ++pl) {
                 uint8_t* dst = sB + sb * C_::B_STAGE + pl * C_::B_PLANE;
@@ -711,7 +736,10 @@ TEM_DEV void halo_mma_tile(const UmmaParams& P, uint8_t* sA, uint8_t* sB, uint64
     for (int cb = 0; cb < P.cpb; ++cb) {
         const int sa = ia % SA;
         mbar_wait(&fullA[sa], (ia / SA) & 1);
-        if (ia == 0 && lane == 0) tstamp(2);
+        if (ia == 0 && lane == 0) {
+            tstamp2(P.slot, 2);
+            tclk(P.slot, 0);
+        }
         tc_fence_after();
         const uint32_t a_st = smem_u32(sA + sa * C_::A_STAGE);
         for (int j = 0; j < 3; ++j, ++ib) {
@@ -788,11 +816,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
     const int nunits = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
     const int mt_u = PAIR ? (P.mtiles + 1) / 2 : P.mtiles;
     const int total = mt_u * P.ntiles;
-    if (threadIdx.x == 0) tstamp(0);
+    if (threadIdx.x == 0) tstamp2(P.slot, 0);
     trace_begin(P.slot);
     float glab[3] = {0.f, 0.f, 0.f}, gb3[3] = {0.f, 0.f, 0.f};  // HEAD: row labels, b3 (prefetched)
+    if (MODE == FWD_ && probe_skip()) {  // diagnostics: skipped loads read zeroed rings, not stale data
+        for (uint32_t i = threadIdx.x; i < C_::RINGS / 16; i += NTHREADS)
+            reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
+        fence_proxy_async_smem();
+        __syncthreads();
+    }
     const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, fullA, 2 * (SA + SB), tfull, tempty, tslot, warp, lane);
-    if (threadIdx.x == 0) tstamp(1);
+    if (threadIdx.x == 0) tstamp2(P.slot, 1);
 
     auto coords = [&](int ct, int& m_tile, int& n_tile, int& split) {
         n_tile = ct % P.ntiles;
@@ -826,7 +860,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
                 halo_mma_tile<MODE, BN, NPASS, SA, SB, PAIR>(P, sA, sB, fullA, emptyA, fullB, emptyB, dt, issuer, lane,
                                                            ia, ib);
                 if (issuer) commit_to<PAIR>(&tfull[acc]);  // accumulator complete
-                if (lane == 0) tstamp(t == 0 ? 3 : 4);
+                if (lane == 0) {
+                    tstamp2(P.slot, t == 0 ? 3 : 4);
+                    tclk(P.slot, 1);
+                }
             }
         }
         __syncwarp();
@@ -834,7 +871,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
         if (HEAD) head_labels(P, hap, unit / P.ntiles, warp, lane, glab, gb3);
         epilogue_loop<MODE, BN, PAIR, C_::ACC>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane,
                                                HEAD ? zrecv : nullptr, smem, C_::RINGS);
-        if (threadIdx.x == 64) tstamp(6);
+        if (threadIdx.x == 64) tstamp2(P.slot, 6);
     }
     if constexpr (HEAD)
         head_tail<BN, C_::ACC>(P, smem, epi, zrecv, hap, tbase, unit / P.ntiles, unit % P.ntiles, warp, lane, glab,
@@ -1945,6 +1982,26 @@ void* umma_tstamp_buffer(int64_t* nbytes, int on) {  // on: 0 off, 1 all, 100 + 
     (void)on;
     if (nbytes) *nbytes = 0;
     return nullptr;
+#endif
+}
+
+void* umma_tclk_buffer(int64_t* nbytes) {
+#ifdef TEM_DIAG
+    void* p = nullptr;
+    if (cudaGetSymbolAddress(&p, umma::g_tclk) != cudaSuccess) return nullptr;
+    if (nbytes) *nbytes = sizeof(long long) * 1024 * 4;
+    return p;
+#else
+    if (nbytes) *nbytes = 0;
+    return nullptr;
+#endif
+}
+
+void umma_set_probe_skip(int bits) {
+#ifdef TEM_DIAG
+    cudaMemcpyToSymbol(umma::g_probe_skip, &bits, sizeof(int));
+#else
+    (void)bits;
 #endif
 }
 

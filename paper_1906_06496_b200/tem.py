@@ -62,6 +62,8 @@ def lib():
     if _lib is None:
         # TEM_DIAG_LIB=1 (scripts/probes only): the diagnostics build with kernel traces
         path = _build.build(diag=os.environ.get("TEM_DIAG_LIB") == "1")
+        if os.environ.get("TEM_DIAG_LIB") == "1" and os.environ.get("TEM_DIAG_LIB_PATH"):
+            path = os.environ["TEM_DIAG_LIB_PATH"]  # a diagnostics build variant (experiments)
         L = ctypes.CDLL(path)
         cp = ctypes.POINTER(tem_config)
         L.tem_num_params.restype = ctypes.c_int64
