@@ -18,6 +18,7 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="c2")
+    ap.add_argument("--warm", type=int, default=3)
     args = ap.parse_args()
     os.environ["TEM_DIAG_LIB"] = "1"
     import numpy as np
@@ -31,7 +32,7 @@ def main():
     lab = torch.from_numpy(datagen.labels(B)).cuda()
     lib = tem.lib()
     nb = ctypes.c_int64(0)
-    for _ in range(3):
+    for _ in range(args.warm):
         s.step(x, lab)
     torch.cuda.synchronize()
     slot = lib.tem_timing_slots(tem._P(s.ctx)) - 1  # SLOT_BWD is the last slot
@@ -64,6 +65,8 @@ def main():
                 ty = names.get((int(tasks[c, k]) >> 24) & 0xFF, "?") if tasks is not None else "?"
                 rows.setdefault((k, ty), []).append(((raw[c, 8 + k] - t0) / 1e3, (raw[c, k] - t0) / 1e3))
     print(f"{len(last)} CTAs; makespan (last epilogue end) median {np.median(last):.2f} max {max(last):.2f} us")
+    q = np.quantile(last, [0.0, 0.1, 0.25, 0.5, 0.75, 0.9, 1.0])
+    print("  CTA end quantiles (0/10/25/50/75/90/100 %): " + " ".join(f"{v:.2f}" for v in q))
     for (k, ty), v in sorted(rows.items()):
         a = np.array(v)
         print(f"  task {k} {ty:>2}: n={len(a):3d} start {np.median(a[:, 0]):6.2f}/{a[:, 0].max():6.2f}  "
