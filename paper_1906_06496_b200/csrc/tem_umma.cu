@@ -132,14 +132,14 @@ constexpr uint32_t BIAS_BYTES = 512 * 4;         // FWD bias copy (Nout <= 512)
 constexpr uint32_t EPI_SMEM = EPI_BYTES + W3_BYTES + BIAS_BYTES;
 
 // Epilogue warps copy W3 (conv2 FWD with fused logits) and the bias (FWD) to shared memory.
-TEM_DEV void load_epi_smem(const UmmaParams& P, float* sw3, int et) {
+TEM_DEV void load_epi_smem(const UmmaParams& P, float* sw3, int et, int nthr = 128) {
     if (P.zpart || P.fused_head) {
-        for (int i = et; i < 3 * P.Nout; i += 128) sw3[i] = P.w3[i];
+        for (int i = et; i < 3 * P.Nout; i += nthr) sw3[i] = P.w3[i];
     }
     if (P.bias) {
-        for (int i = et; i < P.Nout; i += 128) sw3[3 * 512 + i] = P.bias[i];
+        for (int i = et; i < P.Nout; i += nthr) sw3[3 * 512 + i] = P.bias[i];
     }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory");  // the epilogue warps only
 }
 
 // Per-chunk register set: 16 accumulator columns (+ the DGRAD ReLU-mask words of the chunk).
@@ -166,10 +166,15 @@ TEM_DEV void dgrad_mask_chunk0(const UmmaParams& P, int row, int col0, uint4 (&p
 // Staging: `all` (the CTA's only tile; its operand ring is drained) gives every chunk its own
 // buffer, so no store waits for an earlier one; otherwise two buffers alternate and a chunk
 // waits until the store two chunks back has read its data.
-template <int MODE, int BN, int ACC = 1>
+// NEPI = 8 (the fused head): two warps per TMEM lane quarter, each taking half of the columns.
+template <int MODE, int BN, int ACC = 1, int NEPI = 4>
 TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_tile, int split, int q,
                            int lane, uint8_t* stg, int& buf, const float* sw3, const uint4 (&pm)[2],
-                           float* zloc = nullptr, bool all = false) {
+                           float* zloc = nullptr, bool all = false, float* zx = nullptr) {
+    static_assert(NEPI == 4 || (MODE == FWD_ && BN == 64), "8 epilogue warps: the fused head only");
+    constexpr int NCW = (BN / 16) * 4 / NEPI;                        // chunks of this warp
+    const int half = NEPI == 8 ? (((int)threadIdx.x >> 5) - 2) >> 2 : 0;
+    const int c_lo = half * NCW, c_hi = c_lo + NCW;
     const int row0 = m_tile * BM + 32 * q;
     const int row = row0 + lane;
     if ((MODE == FWD_ || MODE == DGRAD_) && (m_tile >= P.mtiles || row0 >= P.R)) return;
@@ -291,12 +296,11 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
     };
 
     // Two register sets: the TMEM load of chunk c+1 is in flight while chunk c is processed.
-    constexpr int NC = BN / 16;
-    static_assert(NC % 2 == 0, "BN must be a multiple of 32");
+    static_assert(NCW % 2 == 0, "an even number of 16-column chunks per warp");
     EpiRegs ea, eb;
-    issue(0, ea);
+    issue(c_lo, ea);
 #pragma unroll 1
-    for (int c16 = 0; c16 < NC; c16 += 2) {
+    for (int c16 = c_lo; c16 < c_hi; c16 += 2) {
         tmem_ld_wait_regs(ea.r);
         if (ACC == 3) {
             tmem_regs_fence(ea.r2);
@@ -310,11 +314,27 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
             tmem_regs_fence(eb.r2);
             tmem_regs_fence(eb.r3);
         }
-        if (c16 + 2 < NC) issue(c16 + 2, ea);
+        if (c16 + 2 < c_hi) issue(c16 + 2, ea);
         process(c16 + 1, eb);
         if (threadIdx.x == 64) tstamp_s(P.slot, 9 + c16);
     }
-    if (MODE == FWD_ && zloc && row < P.R) P.dec2[(size_t)row * (P.Nout / 64) + n_tile] = dmask;
+    if (MODE == FWD_ && zloc && row < P.R) {
+        uint64_t* d = P.dec2 + (size_t)row * (P.Nout / 64) + n_tile;
+        if (NEPI == 8) reinterpret_cast<uint32_t*>(d)[half] = (uint32_t)(dmask >> (32 * half));
+        else *d = dmask;
+    }
+    if (MODE == FWD_ && NEPI == 8 && (zloc || P.zpart)) {
+        // the quarter's second warp passes its columns' partial logits through shared memory;
+        // the first adds them (columns [0, BN/2) + [BN/2, BN), a fixed order) and pushes
+        float4* zx4 = reinterpret_cast<float4*>(zx) + 32 * q + lane;
+        if (half == 1) *zx4 = make_float4(zp0, zp1, zp2, 0.f);
+        asm volatile("bar.sync %0, 64;" ::"r"(2 + q) : "memory");
+        if (half == 1) return;
+        const float4 o = *zx4;
+        zp0 += o.x;
+        zp1 += o.y;
+        zp2 += o.z;
+    }
     if (MODE == FWD_ && zloc) {
         // fused head: push this tile's partial logits into slot n_tile of every CTA of the
         // cluster (zloc = the receive buffer [ntiles][BM][4]; distributed-shared-memory stores)
@@ -367,7 +387,7 @@ TEM_DEV void commit_to(uint64_t* bar) {  // PAIR: the same barrier offset in bot
 template <int TMEM_COLS, bool PAIR>
 TEM_DEV uint32_t gemm_prologue(const UmmaParams& P, uint64_t* bars, int nstage_bars, uint64_t* tfull,
                                uint64_t* tempty, uint32_t* tslot, int warp, int lane, bool cluster = false,
-                               int special_off = 0, int special_n = 0, int special_count = 1) {
+                               int special_off = 0, int special_n = 0, int special_count = 1, int nepi = 4) {
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < 2; ++i) {
             tma_prefetch(&P.a[i]);
@@ -377,7 +397,7 @@ TEM_DEV uint32_t gemm_prologue(const UmmaParams& P, uint64_t* bars, int nstage_b
             mbar_init(&bars[i], (i >= special_off && i < special_off + special_n) ? special_count : 1);
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], PAIR ? 8 : 4);  // 4 epilogue warps (x 2 CTAs)
+            mbar_init(&tempty[a], PAIR ? 2 * nepi : nepi);  // the epilogue warps (x 2 CTAs)
         }
         fence_barrier_init();
     }
@@ -409,16 +429,18 @@ TEM_DEV void gemm_epilogue_done(uint32_t tbase, int warp) {
 // Epilogue warp loop (warps 2..5): drain accumulator buffer t&1 of every tile this unit owns.
 // ring / ring_bytes: the CTA's operand ring; when the CTA owns a single tile the ring is drained
 // once that tile's accumulator is complete, and the epilogue stages all its chunks there.
-template <int MODE, int BN, bool PAIR, int ACC, typename Coords>
+template <int MODE, int BN, bool PAIR, int ACC, typename Coords, int NEPI = 4>
 TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, uint64_t* tfull, uint64_t* tempty,
                            int unit, int nunits, int total, Coords coords, int warp, int lane,
                            float* zloc = nullptr, uint8_t* ring = nullptr, uint32_t ring_bytes = 0) {
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
     constexpr uint32_t WARP_STG = (BN / 16) * EPI_BUF;  // one buffer per 16-column chunk
     const bool all = ring && total <= nunits && 4 * WARP_STG <= ring_bytes;
-    uint8_t* stg = all ? ring + (warp - 2) * WARP_STG : epi + (warp - 2) * 2 * EPI_BUF;
+    // NEPI = 8: the two warps of a quarter stage disjoint chunks of the quarter's region
+    uint8_t* stg = all ? ring + (NEPI == 8 ? q : warp - 2) * WARP_STG : epi + (warp - 2) * 2 * EPI_BUF;
+    if (NEPI == 8 && !all && !zloc) __trap();  // 8 epilogue warps only for single-wave launches
     float* sw3 = reinterpret_cast<float*>(epi + EPI_BYTES);
-    if (MODE == FWD_) load_epi_smem(P, sw3, threadIdx.x - 64);
+    if (MODE == FWD_) load_epi_smem(P, sw3, threadIdx.x - 64, 32 * NEPI);
     const uint32_t tempty_leader = PAIR ? mapa_shared(&tempty[0], 0) : 0u;
     int buf = 0, t = 0;
     for (int ct = unit; ct < total; ct += nunits, ++t) {
@@ -434,7 +456,8 @@ TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, ui
             tstamp_s(P.slot, 5);
         }
         const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * ACC * BN);
-        epilogue_tile<MODE, BN, ACC>(P, tq, m_tile, n_tile, split, q, lane, stg, buf, sw3, pm, zloc, all);
+        epilogue_tile<MODE, BN, ACC, NEPI>(P, tq, m_tile, n_tile, split, q, lane, stg, buf, sw3, pm, zloc, all,
+                                           reinterpret_cast<float*>(epi));
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {  // buffer free for tile t + 2
@@ -490,18 +513,19 @@ struct CfgHalo {
 // partial row per row tile goes to head_reduce.  A second cluster barrier keeps every CTA's
 // partial logits alive until its peers have read them.
 constexpr uint32_t HEAD_LRED_OFF = 136 * 1024;  // [BM][6], in the drained operand rings
+constexpr uint32_t HEAD_STG2_OFF = 140 * 1024;  // dA2 staging of epilogue warps 6..9 (NEPI = 8)
 constexpr uint32_t HEAD_ZRECV_BYTES = 8 * BM * 4 * 4;  // [ntiles <= 8][BM][4] partial logits received
 
 // Epilogue warps, before the accumulator wait: alpha+/- of the (<= 3) videos the row tile
 // touches (one warp per (video, channel), strict > 0.5 -- R5) and this thread's row labels.
 TEM_DEV void head_labels(const UmmaParams& P, float* hap, int m_tile, int warp, int lane, float (&glab)[3],
-                         float (&b3)[3]) {
+                         float (&b3)[3], int nepi) {
 #pragma unroll
     for (int o = 0; o < 3; ++o) b3[o] = P.b3[o];
     const int Tp = P.Tp, Tn = P.Tn, m0 = m_tile * BM;
     const int last = min(m0 + BM, P.R) - 1;
     const int v0 = m0 / Tp, nv = last / Tp - v0 + 1;
-    for (int pr = warp - 2; pr < nv * 3; pr += 4) {
+    for (int pr = warp - 2; pr < nv * 3; pr += nepi) {
         const int k = pr / 3, o = pr - 3 * k;
         const float* lab = P.labels + ((size_t)(v0 + k) * 3 + o) * Tn;
         int lp = 0;
@@ -523,7 +547,7 @@ TEM_DEV void head_labels(const UmmaParams& P, float* hap, int m_tile, int warp, 
     }
 }
 
-template <int BN, int ACC>
+template <int BN, int ACC, int NEPI>
 TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const float* zrecv, const float* hap,
                        uint32_t tbase, int m_tile, int n_tile, int warp, int lane, const float (&glab)[3],
                        const float (&b3)[3]) {
@@ -539,6 +563,10 @@ TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const f
     if (threadIdx.x == 64) tstamp2(P.slot, 9);
     if (warp >= 2) {
         const int q = warp & 3, row = 32 * q + lane, p = m0 + row;
+        // NEPI = 8: the two warps of a lane quarter take half of the columns each (both
+        // compute the rows' z / dz; the first one writes the per-row outputs)
+        constexpr int NCW = (BN / 16) * 4 / NEPI;
+        const int half = NEPI == 8 ? (warp - 2) >> 2 : 0;
         const int Tp = P.Tp, Tn = P.Tn;
         const bool live = p < P.R, halo = !live || halo_row(p, Tp);
         // z: partial logits of all column tiles, column-tile order, then + b3
@@ -568,10 +596,10 @@ TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const f
                 const float bt = glab[o] > 0.5f ? 1.f : 0.f;
                 const float ap = hap[k * 3 + o], an = hap[9 + k * 3 + o];
                 head_row_terms(z[o], bt, ap, an, P.lam[o] * inv_bt, lt[o], dz[o]);
-                if (r == 0) P.z_out[((size_t)v * Tn + t) * 3 + o] = z[o];
+                if (r == 0 && half == 0) P.z_out[((size_t)v * Tn + t) * 3 + o] = z[o];
             }
         }
-        if (r == 0) {
+        if (r == 0 && half == 0) {
 #pragma unroll
             for (int o = 0; o < 3; ++o) {
                 lred[row * 6 + o] = lt[o];
@@ -582,11 +610,12 @@ TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const f
         // dA2 for this CTA's columns (h2 recomputed from the accumulator exactly as the epilogue)
         const float* sw3 = reinterpret_cast<const float*>(epi + EPI_BYTES);
         const float* sbias = sw3 + 3 * 512;
-        uint8_t* stg = epi + (warp - 2) * 2 * EPI_BUF;
+        // staging: warps 2..5 in the epilogue area, warps 6..9 in the drained rings above lred
+        uint8_t* stg = warp < 6 ? epi + (warp - 2) * 2 * EPI_BUF : smem + HEAD_STG2_OFF + (warp - 6) * 2 * EPI_BUF;
         const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16);
         float* rrow = red + (size_t)row * RLD;
         int buf = 0;
-        for (int c16 = 0; c16 < BN / 16; ++c16) {
+        for (int c16 = half * NCW; c16 < (half + 1) * NCW; ++c16) {
             const int gc = n0 + c16 * 16;
             uint32_t ra[16], rb[16], rc[16];
             tmem_ld16(tq + (uint32_t)(c16 * 16), ra);
@@ -666,7 +695,7 @@ TEM_DEV void head_tail(const UmmaParams& P, uint8_t* smem, uint8_t* epi, const f
     }
     __syncthreads();  // column partials of all rows in shared memory
     float* dst = P.headpart + (size_t)m_tile * (4 * C + 8);  // [dW3 (3C)][db3 (3)][L (3)][db2 (C)]
-    for (int j = threadIdx.x; j < 4 * BN; j += NTHREADS) {
+    for (int j = threadIdx.x; j < 4 * BN; j += 64 + 32 * NEPI) {
         float acc = 0.f;
         for (int row = 0; row < BM; ++row) acc += red[(size_t)row * RLD + j];  // row order
         const int c = j >> 2, kind = j & 3;
@@ -787,8 +816,12 @@ TEM_DEV void halo_mma_tile(const UmmaParams& P, uint8_t* sA, uint8_t* sB, uint64
     }
 }
 
-template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR, bool HEAD = false>
-__global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_constant__ UmmaParams P) {
+// NEPI epilogue warps: 8 (two per TMEM lane quarter, 320 threads) for the fused head and the
+// single-wave fp32 FWD, else 4 (192 threads).
+constexpr int halo_threads(int nepi) { return 64 + 32 * nepi; }
+
+template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR, bool HEAD = false, int NEPI = (HEAD ? 8 : 4)>
+__global__ void __launch_bounds__(halo_threads(NEPI), 1) umma_halo_kernel(const __grid_constant__ UmmaParams P) {
     static_assert(MODE == FWD_ || MODE == DGRAD_, "halo kernel: FWD / DGRAD");
     static_assert(!HEAD || (MODE == FWD_ && !PAIR), "fused head: 1-CTA conv2 FWD");
     using C_ = CfgHalo<BN, NPASS, SA, SB, PAIR>;
@@ -807,6 +840,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
     float* hap = reinterpret_cast<float*>(smem + C_::RINGS + 512);  // HEAD: alpha+ [3][3], alpha- [3][3]
     static_assert(!HEAD || HEAD_LRED_OFF + BM * 6 * 4 <= C_::RINGS, "head scratch fits the rings");
     static_assert(!HEAD || BM * (4 * BN + 4) * 4 <= HEAD_LRED_OFF, "head column buffer below the loss terms");
+    static_assert(!HEAD || (HEAD_LRED_OFF + BM * 6 * 4 <= HEAD_STG2_OFF &&
+                            HEAD_STG2_OFF + 4 * 2 * EPI_BUF <= C_::RINGS), "head staging of warps 6..9");
+    static_assert(NEPI == 4 || (NEPI == 8 && MODE == FWD_ && !PAIR), "8 epilogue warps: 1-CTA FWD");
     float* zrecv = reinterpret_cast<float*>(smem + C_::RINGS + 1024 + EPI_SMEM);  // HEAD only (SMEM_HEAD)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -820,12 +856,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
     trace_begin(P.slot);
     float glab[3] = {0.f, 0.f, 0.f}, gb3[3] = {0.f, 0.f, 0.f};  // HEAD: row labels, b3 (prefetched)
     if (MODE == FWD_ && probe_skip()) {  // diagnostics: skipped loads read zeroed rings, not stale data
-        for (uint32_t i = threadIdx.x; i < C_::RINGS / 16; i += NTHREADS)
+        for (uint32_t i = threadIdx.x; i < C_::RINGS / 16; i += blockDim.x)
             reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
         fence_proxy_async_smem();
         __syncthreads();
     }
-    const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, fullA, 2 * (SA + SB), tfull, tempty, tslot, warp, lane);
+    const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, fullA, 2 * (SA + SB), tfull, tempty, tslot, warp, lane,
+                                                              false, 0, 0, 1, NEPI);
     if (threadIdx.x == 0) tstamp2(P.slot, 1);
 
     auto coords = [&](int ct, int& m_tile, int& n_tile, int& split) {
@@ -868,14 +905,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_halo_kernel(const __grid_con
         }
         __syncwarp();
     } else {
-        if (HEAD) head_labels(P, hap, unit / P.ntiles, warp, lane, glab, gb3);
-        epilogue_loop<MODE, BN, PAIR, C_::ACC>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane,
-                                               HEAD ? zrecv : nullptr, smem, C_::RINGS);
+        if (HEAD) head_labels(P, hap, unit / P.ntiles, warp, lane, glab, gb3, NEPI);
+        epilogue_loop<MODE, BN, PAIR, C_::ACC, decltype(coords), NEPI>(P, epi, tbase, tfull, tempty, unit, nunits,
+                                                                      total, coords, warp, lane,
+                                                                      HEAD ? zrecv : nullptr, smem, C_::RINGS);
         if (threadIdx.x == 64) tstamp2(P.slot, 6);
     }
     if constexpr (HEAD)
-        head_tail<BN, C_::ACC>(P, smem, epi, zrecv, hap, tbase, unit / P.ntiles, unit % P.ntiles, warp, lane, glab,
-                               gb3);
+        head_tail<BN, C_::ACC, NEPI>(P, smem, epi, zrecv, hap, tbase, unit / P.ntiles, unit % P.ntiles, warp, lane,
+                                     glab, gb3);
     gemm_epilogue_done<C_::TMEM_COLS, PAIR>(tbase, warp);
     trace_end(P.slot);
 }
@@ -1388,7 +1426,7 @@ bool map_store_part(CUtensorMap* m, float* base, uint64_t NW, uint64_t rows, uin
 // Persistent launch: as many units (CTAs, or 2-CTA clusters) as fit, <= the tile count.
 template <typename K>
 cudaError_t launch_persistent(K k, uint32_t smem, bool pair, int total, int* max_units, const UmmaParams& p,
-                              cudaStream_t s) {
+                              cudaStream_t s, int threads = umma::NTHREADS) {
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[3];
     int na = 0;
@@ -1403,7 +1441,7 @@ cudaError_t launch_persistent(K k, uint32_t smem, bool pair, int total, int* max
         attr[na].val.clusterDim.y = 1;
         attr[na++].val.clusterDim.z = 1;
     }
-    cfg.blockDim = dim3(umma::NTHREADS);
+    cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cfg.attrs = attr;
@@ -1422,7 +1460,7 @@ cudaError_t launch_persistent(K k, uint32_t smem, bool pair, int total, int* max
             }
         } else {
             int per_sm = 0;
-            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, umma::NTHREADS, smem) != cudaSuccess ||
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, threads, smem) != cudaSuccess ||
                 per_sm <= 0) {
                 cudaGetLastError();
                 per_sm = 1;
@@ -1463,7 +1501,7 @@ cudaError_t launch_halo_head(const UmmaParams& p, cudaStream_t s) {
     attr[na].val.clusterDim.y = 1;
     attr[na++].val.clusterDim.z = 1;
     cfg.gridDim = dim3(p.mtiles * p.ntiles, 1, 1);
-    cfg.blockDim = dim3(umma::NTHREADS);
+    cfg.blockDim = dim3(umma::halo_threads(8));
     cfg.dynamicSmemBytes = SMEM;
     cfg.stream = s;
     cfg.attrs = attr;
@@ -1487,7 +1525,7 @@ int umma_head_max_clusters(int ntiles) {
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.gridDim = dim3(ntiles * 16, 1, 1);
-    cfg.blockDim = dim3(umma::NTHREADS);
+    cfg.blockDim = dim3(umma::halo_threads(8));
     cfg.dynamicSmemBytes = SMEM;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
@@ -1499,12 +1537,13 @@ int umma_head_max_clusters(int ntiles) {
     return n;
 }
 
-template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR>
+template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR, int NEPI = 4>
 cudaError_t launch_halo(const UmmaParams& p, cudaStream_t s) {
     static int max_units = -1;
     const int total = (PAIR ? (p.mtiles + 1) / 2 : p.mtiles) * p.ntiles;
-    return launch_persistent(umma::umma_halo_kernel<MODE, BN, NPASS, SA, SB, PAIR>,
-                             umma::CfgHalo<BN, NPASS, SA, SB, PAIR>::SMEM, PAIR, total, &max_units, p, s);
+    return launch_persistent(umma::umma_halo_kernel<MODE, BN, NPASS, SA, SB, PAIR, false, NEPI>,
+                             umma::CfgHalo<BN, NPASS, SA, SB, PAIR>::SMEM, PAIR, total, &max_units, p, s,
+                             umma::halo_threads(NEPI));
 }
 
 template <int BN, int NPASS, int STAGES, bool PAIR>
@@ -1796,7 +1835,10 @@ static cudaError_t dispatch(const UmmaParams& p, int npass, cudaStream_t s) {
         if constexpr (MODE == FWD_)
             if (p.fused_head) return launch_halo_head<64, 3, 2, 6>(p, s);  // plan: fp32, BN = 64
         if (c.pair) return launch_halo<MODE, 256, 1, 4, 8, true>(p, s);  // bf16: 2-CTA pairs
-        return launch_halo<MODE, 64, 3, 3, 6, false>(p, s);              // fp32 (3-pass)
+        // fp32 (3-pass); a single-wave FWD drains its one tile with 8 epilogue warps
+        if (MODE == FWD_ && p.mtiles * p.ntiles <= 148)
+            return launch_halo<FWD_, 64, 3, 3, 6, false, 8>(p, s);
+        return launch_halo<MODE, 64, 3, 3, 6, false>(p, s);
     }
 }
 
