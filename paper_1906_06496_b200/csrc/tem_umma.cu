@@ -171,7 +171,9 @@ template <int MODE, int BN, int ACC = 1, int NEPI = 4>
 TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_tile, int split, int q,
                            int lane, uint8_t* stg, int& buf, const float* sw3, const uint4 (&pm)[2],
                            float* zloc = nullptr, bool all = false, float* zx = nullptr) {
-    static_assert(NEPI == 4 || (MODE == FWD_ && BN == 64), "8 epilogue warps: the fused head only");
+    static_assert(NEPI == 4 || NEPI == 8, "4 or 8 epilogue warps");
+    // 8 warps outside 'all' staging: one staging buffer per warp (the persistent backward)
+    constexpr bool ONEBUF = NEPI == 8;
     constexpr int NCW = (BN / 16) * 4 / NEPI;                        // chunks of this warp
     const int half = NEPI == 8 ? (((int)threadIdx.x >> 5) - 2) >> 2 : 0;
     const int c_lo = half * NCW, c_hi = c_lo + NCW;
@@ -190,7 +192,7 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
             tmem_ld16(tq + (uint32_t)(BN + c16 * 16), e.r2);
             tmem_ld16(tq + (uint32_t)(2 * BN + c16 * 16), e.r3);
         }
-        if (MODE == DGRAD_ && c16 == 0) {
+        if (MODE == DGRAD_ && c16 == c_lo) {  // the prefetched mask of the warp's first chunk
             e.mw[0] = pm[0].x; e.mw[1] = pm[0].y; e.mw[2] = pm[0].z; e.mw[3] = pm[0].w;
             e.mw[4] = pm[1].x; e.mw[5] = pm[1].y; e.mw[6] = pm[1].z; e.mw[7] = pm[1].w;
         } else if (MODE == DGRAD_) {
@@ -269,8 +271,11 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
                 v[2 * i + 1] = __uint_as_float(e.mw[i] & 0xFFFF0000u) > 0.f ? v[2 * i + 1] : 0.f;
             }
         }
-        uint8_t* sb = stg + (all ? c16 : buf) * EPI_BUF;
-        if (lane == 0 && !all) bulk_wait_read<1>();  // this buffer's previous store has read its data
+        uint8_t* sb = stg + (all ? c16 : (ONEBUF ? 0 : buf)) * EPI_BUF;
+        if (lane == 0 && !all) {  // this buffer's previous store has read its data
+            if (ONEBUF) bulk_wait_read<0>();
+            else bulk_wait_read<1>();
+        }
         __syncwarp();
         const bool f32 = (MODE == WGRAD_) || P.out_f32;
         if (f32) {
@@ -1120,7 +1125,11 @@ TEM_DEV void st_release_gpu_u32(unsigned* p, unsigned v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(NTHREADS, 1) bwd_kernel(const __grid_constant__ BwdParams B) {
+constexpr int BWD_NEPI = 8;  // epilogue warps: two per TMEM lane quarter, half the columns each
+constexpr int BWD_THREADS = 64 + 32 * BWD_NEPI;
+static_assert(BWD_NEPI * EPI_BUF <= EPI_BYTES, "one staging buffer per epilogue warp");
+
+__global__ void __launch_bounds__(BWD_THREADS, 1) bwd_kernel(const __grid_constant__ BwdParams B) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align_smem_1k(smem_raw);
     uint8_t* sA = smem;                                   // halo: A windows, then B taps
@@ -1145,7 +1154,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_kernel(const __grid_constant_
         mbar_init(drain, 1);
     }
     // barriers: fullA..empty (24 stage barriers), tfull / tempty; TMEM: two 256-column buffers
-    const uint32_t tbase = gemm_prologue<512, false>(B.dg, fullA, 24, tfull, tempty, tslot, warp, lane);
+    const uint32_t tbase = gemm_prologue<512, false>(B.dg, fullA, 24, tfull, tempty, tslot, warp, lane, false, 0, 0,
+                                                     1, BWD_NEPI);
     const unsigned epoch = s_epoch;
     auto decode = [&](int w, int& type, int& m, int& n, int& sp) {
         type = (w >> 24) & 0xFF;
@@ -1222,8 +1232,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_kernel(const __grid_constant_
         __syncwarp();
     } else {
         // ===================== epilogue =====================
-        const int q = warp & 3;
-        uint8_t* stg = epi + (warp - 2) * 2 * EPI_BUF;
+        const int q = warp & 3, half = (warp - 2) >> 2;
+        uint8_t* stg = epi + (warp - 2) * EPI_BUF;
         const float* sw3 = reinterpret_cast<const float*>(epi + EPI_BYTES);
         int buf = 0;
         for (int k = 0; k < BWD_MAX_TASKS; ++k) {
@@ -1233,14 +1243,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_kernel(const __grid_constant_
             decode(w, type, m, n, sp);
             const int acc = k & 1;
             uint4 pm[2] = {make_uint4(0u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u)};
-            if (type == BWD_DG) dgrad_mask_chunk0(B.dg, m * BM + 32 * q + lane, n * 64, pm);
+            if (type == BWD_DG) dgrad_mask_chunk0(B.dg, m * BM + 32 * q + lane, n * 64 + half * 32, pm);
             mbar_wait(&tfull[acc], (k >> 1) & 1);
             tc_fence_after();
             const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * BWD_ACC_COLS);
             if (type == BWD_DG)
-                epilogue_tile<DGRAD_, 64, 3>(B.dg, tq, m, n, 0, q, lane, stg, buf, sw3, pm);
+                epilogue_tile<DGRAD_, 64, 3, BWD_NEPI>(B.dg, tq, m, n, 0, q, lane, stg, buf, sw3, pm);
             else
-                epilogue_tile<WGRAD_, 128, 1>(type == BWD_W2 ? B.w2 : B.w1, tq, m, n, sp, q, lane, stg, buf, sw3, pm);
+                epilogue_tile<WGRAD_, 128, 1, BWD_NEPI>(type == BWD_W2 ? B.w2 : B.w1, tq, m, n, sp, q, lane, stg, buf,
+                                                        sw3, pm);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_local(&tempty[acc]);
@@ -1252,7 +1263,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) bwd_kernel(const __grid_constant_
                     fence_proxy_async_all();
                 }
                 __syncwarp();
-                asm volatile("bar.sync 1, 128;" ::: "memory");
+                asm volatile("bar.sync 1, %0;" ::"r"(32 * BWD_NEPI) : "memory");
                 if (threadIdx.x == 64) {
                     __threadfence();
                     st_release_gpu_u32(B.st.flags + m * B.dg_ntiles + n, epoch);
@@ -1570,7 +1581,7 @@ cudaError_t launch_bwd(const umma::BwdParams& p, int grid, cudaStream_t s) {
     attr[na++].val.cooperative = 1;
     na += launch_priority_attr(&attr[na], false);
     cfg.gridDim = dim3(grid, 1, 1);
-    cfg.blockDim = dim3(umma::NTHREADS);
+    cfg.blockDim = dim3(umma::BWD_THREADS);
     cfg.dynamicSmemBytes = umma::BWD_SMEM;
     cfg.stream = s;
     cfg.attrs = attr;
@@ -1799,7 +1810,7 @@ bool umma_plan(const Geom& g, const RankBufs& b, UmmaPlan* plan) {
         !getenv("TEM_NO_BWD") &&
         cudaFuncSetAttribute(umma::bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)umma::BWD_SMEM) ==
             cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, umma::bwd_kernel, umma::NTHREADS, umma::BWD_SMEM) ==
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, umma::bwd_kernel, umma::BWD_THREADS, umma::BWD_SMEM) ==
             cudaSuccess &&
         per_sm >= 1 && sms > 0 && sms <= 1024) {
         std::vector<int> tasks;
