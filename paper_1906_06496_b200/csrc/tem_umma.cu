@@ -16,16 +16,16 @@
 //             is hi*hi + hi*lo + lo*hi accumulated in fp32 -- ~2^-16 relative per product,
 //             inside the 1e-4 contract.
 //
-// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer
-// (one elected lane), warps 2..5 = epilogue (TMEM -> registers -> global).
+// Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer
+// (one elected lane of a converged warp), warps 2..9 = epilogue, two per TMEM lane quarter,
+// each draining half of the tile's columns (TMEM -> registers -> shared -> TMA store).
 //
-// Persistent: each cluster of CM x CN CTAs walks a static list of cluster tiles (CM m-tiles
-// x CN n-tiles [x split]); the two TMEM accumulator buffers let the epilogue of tile i run
-// while tile i+1 is in the MMA pipe.  Inside a cluster, the CN CTAs that share an m-tile
-// each load 1/CN of the A tile and TMA-multicast it to the others; the CM CTAs that share an
-// n-tile do the same for B.  A stage slot is refilled only after every CTA that reads data
-// this CTA wrote has released it (its MMA completion is multicast-committed to the empty
-// barriers of its CM + CN - 1 producers).
+// Persistent: each CTA (or 2-CTA pair, cta_group::2, for the bf16 GEMMs) walks a static list of
+// tiles [x split]; the two TMEM accumulator buffers let the epilogue of tile i run while tile
+// i+1 is in the MMA pipe.  FWD / DGRAD stage one 130-row A window per 64-channel block and read
+// the three taps at row offsets of it (the halo layout); WGRAD is split-K over the rows with
+// fixed-order partial sums.  The fp32 backward of a step runs as one persistent launch
+// (bwd_kernel), and the fused head runs inside conv2's FWD (head_tail).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -431,19 +431,22 @@ TEM_DEV void gemm_epilogue_done(uint32_t tbase, int warp) {
     }
 }
 
-// Epilogue warp loop (warps 2..5): drain accumulator buffer t&1 of every tile this unit owns.
+// Epilogue warp loop (warps 2..1+NEPI): drain accumulator buffer t&1 of every tile this unit owns.
 // ring / ring_bytes: the CTA's operand ring; when the CTA owns a single tile the ring is drained
 // once that tile's accumulator is complete, and the epilogue stages all its chunks there.
 template <int MODE, int BN, bool PAIR, int ACC, typename Coords, int NEPI = 4>
 TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, uint64_t* tfull, uint64_t* tempty,
                            int unit, int nunits, int total, Coords coords, int warp, int lane,
-                           float* zloc = nullptr, uint8_t* ring = nullptr, uint32_t ring_bytes = 0) {
+                           float* zloc = nullptr, uint8_t* ring = nullptr, uint32_t ring_bytes = 0,
+                           float* zx = nullptr) {
     const int q = warp & 3;  // TMEM lane quarter accessible to this warp
     constexpr uint32_t WARP_STG = (BN / 16) * EPI_BUF;  // one buffer per 16-column chunk
     const bool all = ring && total <= nunits && 4 * WARP_STG <= ring_bytes;
-    // NEPI = 8: the two warps of a quarter stage disjoint chunks of the quarter's region
-    uint8_t* stg = all ? ring + (NEPI == 8 ? q : warp - 2) * WARP_STG : epi + (warp - 2) * 2 * EPI_BUF;
-    if (NEPI == 8 && !all && !zloc) __trap();  // 8 epilogue warps only for single-wave launches
+    // NEPI = 8: the two warps of a quarter stage disjoint chunks of the quarter's region (all),
+    // or one buffer each in the epilogue area (the 16 KB hold 8)
+    static_assert(NEPI == 4 || 8 * EPI_BUF <= EPI_BYTES, "one staging buffer per epilogue warp");
+    uint8_t* stg = all ? ring + (NEPI == 8 ? q : warp - 2) * WARP_STG
+                       : epi + (warp - 2) * (NEPI == 8 ? 1 : 2) * EPI_BUF;
     float* sw3 = reinterpret_cast<float*>(epi + EPI_BYTES);
     if (MODE == FWD_) load_epi_smem(P, sw3, threadIdx.x - 64, 32 * NEPI);
     const uint32_t tempty_leader = PAIR ? mapa_shared(&tempty[0], 0) : 0u;
@@ -453,7 +456,9 @@ TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, ui
         coords(ct, m_tile, n_tile, split);
         const int acc = t & 1;
         uint4 pm[2];
-        if (MODE == DGRAD_) dgrad_mask_chunk0(P, m_tile * BM + 32 * q + lane, n_tile * BN, pm);
+        if (MODE == DGRAD_)  // the mask of the warp's first chunk
+            dgrad_mask_chunk0(P, m_tile * BM + 32 * q + lane,
+                              n_tile * BN + (NEPI == 8 ? ((warp - 2) >> 2) * (BN / 2) : 0), pm);
         mbar_wait(&tfull[acc], (t >> 1) & 1);
         tc_fence_after();
         if (t == 0 && threadIdx.x == 64) {  // diagnostics: the accumulator is complete
@@ -461,8 +466,7 @@ TEM_DEV void epilogue_loop(const UmmaParams& P, uint8_t* epi, uint32_t tbase, ui
             tstamp_s(P.slot, 5);
         }
         const uint32_t tq = tbase + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * ACC * BN);
-        epilogue_tile<MODE, BN, ACC, NEPI>(P, tq, m_tile, n_tile, split, q, lane, stg, buf, sw3, pm, zloc, all,
-                                           reinterpret_cast<float*>(epi));
+        epilogue_tile<MODE, BN, ACC, NEPI>(P, tq, m_tile, n_tile, split, q, lane, stg, buf, sw3, pm, zloc, all, zx);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {  // buffer free for tile t + 2
@@ -498,7 +502,8 @@ struct CfgHalo {
     static constexpr int TPS = (SB % TEM_HALO_TPS == 0) ? TEM_HALO_TPS : 1;
     static constexpr int SBS = SB / TPS;  // barrier stages
     static constexpr uint32_t RINGS = SA * A_STAGE + SB * B_STAGE;
-    static constexpr uint32_t SMEM = RINGS + 1024 /*align*/ + 1024 /*barriers*/ + EPI_SMEM;
+    // + the partial-logit exchange of the 8-epilogue-warp FWD (BM float4, after the epilogue area)
+    static constexpr uint32_t SMEM = RINGS + 1024 /*align*/ + 1024 /*barriers*/ + EPI_SMEM + BM * 16;
     // 3-pass 1-CTA: dual-accumulator MMAs (see epilogue_tile), 3 BN columns per buffer
     static constexpr int ACC = (NPASS == 3 && !PAIR && 6 * BN <= 512) ? 3 : 1;
     static constexpr int TMEM_COLS = ACC == 3 ? 512 : 2 * BN;  // two accumulator buffers
@@ -821,8 +826,8 @@ TEM_DEV void halo_mma_tile(const UmmaParams& P, uint8_t* sA, uint8_t* sB, uint64
     }
 }
 
-// NEPI epilogue warps: 8 (two per TMEM lane quarter, 320 threads) for the fused head and the
-// single-wave fp32 FWD, else 4 (192 threads).
+// NEPI epilogue warps: 8 (two per TMEM lane quarter, 320 threads) in every launch; the code
+// also supports 4 (192 threads, one warp per quarter).
 constexpr int halo_threads(int nepi) { return 64 + 32 * nepi; }
 
 template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR, bool HEAD = false, int NEPI = (HEAD ? 8 : 4)>
@@ -847,7 +852,7 @@ __global__ void __launch_bounds__(halo_threads(NEPI), 1) umma_halo_kernel(const 
     static_assert(!HEAD || BM * (4 * BN + 4) * 4 <= HEAD_LRED_OFF, "head column buffer below the loss terms");
     static_assert(!HEAD || (HEAD_LRED_OFF + BM * 6 * 4 <= HEAD_STG2_OFF &&
                             HEAD_STG2_OFF + 4 * 2 * EPI_BUF <= C_::RINGS), "head staging of warps 6..9");
-    static_assert(NEPI == 4 || (NEPI == 8 && MODE == FWD_ && !PAIR), "8 epilogue warps: 1-CTA FWD");
+    static_assert(NEPI == 4 || NEPI == 8, "4 or 8 epilogue warps");
     float* zrecv = reinterpret_cast<float*>(smem + C_::RINGS + 1024 + EPI_SMEM);  // HEAD only (SMEM_HEAD)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -911,9 +916,12 @@ __global__ void __launch_bounds__(halo_threads(NEPI), 1) umma_halo_kernel(const 
         __syncwarp();
     } else {
         if (HEAD) head_labels(P, hap, unit / P.ntiles, warp, lane, glab, gb3, NEPI);
+        // partial-logit exchange of the two warps of a quarter: the (then unused) epilogue
+        // staging area under the fused head, else its own region after the epilogue area
+        float* zx = HEAD ? reinterpret_cast<float*>(epi) : reinterpret_cast<float*>(epi + EPI_SMEM);
         epilogue_loop<MODE, BN, PAIR, C_::ACC, decltype(coords), NEPI>(P, epi, tbase, tfull, tempty, unit, nunits,
                                                                       total, coords, warp, lane,
-                                                                      HEAD ? zrecv : nullptr, smem, C_::RINGS);
+                                                                      HEAD ? zrecv : nullptr, smem, C_::RINGS, zx);
         if (threadIdx.x == 64) tstamp2(P.slot, 6);
     }
     if constexpr (HEAD)
@@ -1012,8 +1020,8 @@ TEM_DEV void wgrad_mma_tile(const UmmaParams& P, uint8_t* smem, uint64_t* full, 
     }
 }
 
-template <int BN, int NPASS, int STAGES, bool PAIR>
-__global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_constant__ UmmaParams P) {
+template <int BN, int NPASS, int STAGES, bool PAIR, int NEPI = 4>
+__global__ void __launch_bounds__(halo_threads(NEPI), 1) umma_wgrad_kernel(const __grid_constant__ UmmaParams P) {
     using C_ = CfgW<BN, NPASS, STAGES, PAIR>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = align_smem_1k(smem_raw);
@@ -1033,7 +1041,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
     const int total = mt_u * P.ntiles * P.nsplit;
     trace_begin(P.slot);
     if (threadIdx.x == 0) tstamp_s(P.slot, 0);
-    const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, full, 2 * STAGES, tfull, tempty, tslot, warp, lane);
+    const uint32_t tbase = gemm_prologue<C_::TMEM_COLS, PAIR>(P, full, 2 * STAGES, tfull, tempty, tslot, warp, lane,
+                                                              false, 0, 0, 1, NEPI);
     if (threadIdx.x == 0) tstamp_s(P.slot, 1);
 
     auto coords = [&](int ct, int& m_tile, int& n_tile, int& split) {
@@ -1073,8 +1082,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) umma_wgrad_kernel(const __grid_co
         }
         __syncwarp();
     } else {
-        epilogue_loop<WGRAD_, BN, PAIR, 1>(P, epi, tbase, tfull, tempty, unit, nunits, total, coords, warp, lane,
-                                           nullptr, smem, STAGES * C_::STAGE_BYTES);
+        epilogue_loop<WGRAD_, BN, PAIR, 1, decltype(coords), NEPI>(P, epi, tbase, tfull, tempty, unit, nunits, total,
+                                                                   coords, warp, lane, nullptr, smem,
+                                                                   STAGES * C_::STAGE_BYTES);
         if (threadIdx.x == 64) tstamp_s(P.slot, 6);
     }
     gemm_epilogue_done<C_::TMEM_COLS, PAIR>(tbase, warp);
@@ -1551,18 +1561,20 @@ int umma_head_max_clusters(int ntiles) {
 template <int MODE, int BN, int NPASS, int SA, int SB, bool PAIR, int NEPI = 4>
 cudaError_t launch_halo(const UmmaParams& p, cudaStream_t s) {
     static int max_units = -1;
+    static_assert(umma::CfgHalo<BN, NPASS, SA, SB, PAIR>::SMEM <= 232448, "halo smem");
     const int total = (PAIR ? (p.mtiles + 1) / 2 : p.mtiles) * p.ntiles;
     return launch_persistent(umma::umma_halo_kernel<MODE, BN, NPASS, SA, SB, PAIR, false, NEPI>,
                              umma::CfgHalo<BN, NPASS, SA, SB, PAIR>::SMEM, PAIR, total, &max_units, p, s,
                              umma::halo_threads(NEPI));
 }
 
-template <int BN, int NPASS, int STAGES, bool PAIR>
+template <int BN, int NPASS, int STAGES, bool PAIR, int NEPI = 4>
 cudaError_t launch_wgrad(const UmmaParams& p, cudaStream_t s) {
     static int max_units = -1;
     const int total = (PAIR ? (p.mtiles + 1) / 2 : p.mtiles) * p.ntiles * p.nsplit;
-    return launch_persistent(umma::umma_wgrad_kernel<BN, NPASS, STAGES, PAIR>,
-                             umma::CfgW<BN, NPASS, STAGES, PAIR>::SMEM, PAIR, total, &max_units, p, s);
+    return launch_persistent(umma::umma_wgrad_kernel<BN, NPASS, STAGES, PAIR, NEPI>,
+                             umma::CfgW<BN, NPASS, STAGES, PAIR>::SMEM, PAIR, total, &max_units, p, s,
+                             umma::halo_threads(NEPI));
 }
 
 // The persistent backward: one CTA per SM, all co-resident (cooperative launch).
@@ -1838,18 +1850,17 @@ static int mtiles_of(const UmmaPlan& P) { return P.conv2.mtiles; }
 
 template <int MODE>
 static cudaError_t dispatch(const UmmaParams& p, int npass, cudaStream_t s) {
+    // every launch drains its accumulators with 8 epilogue warps, two per TMEM lane quarter
+    // (the epilogues are bound by one warp's instruction latency per scheduler)
     const GemmCfg c = cfg_for(MODE, npass);
     if constexpr (MODE == WGRAD_) {
-        if (c.pair) return launch_wgrad<256, 1, 6, true>(p, s);  // bf16: 2-CTA pairs
-        return launch_wgrad<128, 3, 3, false>(p, s);            // fp32 (3-pass)
+        if (c.pair) return launch_wgrad<256, 1, 6, true, 8>(p, s);  // bf16: 2-CTA pairs
+        return launch_wgrad<128, 3, 3, false, 8>(p, s);            // fp32 (3-pass)
     } else {
         if constexpr (MODE == FWD_)
             if (p.fused_head) return launch_halo_head<64, 3, 2, 6>(p, s);  // plan: fp32, BN = 64
-        if (c.pair) return launch_halo<MODE, 256, 1, 4, 8, true>(p, s);  // bf16: 2-CTA pairs
-        // fp32 (3-pass); a single-wave FWD drains its one tile with 8 epilogue warps
-        if (MODE == FWD_ && p.mtiles * p.ntiles <= 148)
-            return launch_halo<FWD_, 64, 3, 3, 6, false, 8>(p, s);
-        return launch_halo<MODE, 64, 3, 3, 6, false>(p, s);
+        if (c.pair) return launch_halo<MODE, 256, 1, 4, 8, true, 8>(p, s);  // bf16: 2-CTA pairs
+        return launch_halo<MODE, 64, 3, 3, 6, false, 8>(p, s);              // fp32 (3-pass)
     }
 }
 
