@@ -45,12 +45,17 @@ def launches(path, out):
     for r in rows[h + 1:]:
         if len(r) > vi:
             agg[r[ki].split("(")[0][:90]].append(to_us(r[vi], r[ui]))
-    tot = sum(sum(v) for v in agg.values())
+    # bench.py's own kernels (the L2 flush between steps, the launch-ahead spin before the timed
+    # steps) run outside the step: listed, but not part of the share
+    harness = lambda k: "FillFunctor<unsigned char>" in k or "spin_kernel" in k
+    tot = sum(sum(v) for k, v in agg.items() if not harness(k))
     lines = [f"# ncu launch list ({os.path.basename(path)}): gpu__time_duration.sum, --clock-control none",
-             "# cold-cache, serialised: compare SHARES, not absolute times", "",
+             "# cold-cache, serialised: compare SHARES, not absolute times; share = of the library's",
+             "# kernels (bench.py's L2 flush and launch-ahead spin excluded, marked '-')", "",
              f"{'launches':>8} {'mean_us':>9} {'share':>7}  kernel"]
     for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
-        lines.append(f"{len(v):8d} {sum(v)/len(v):9.2f} {100*sum(v)/tot:6.1f}%  {k}")
+        share = "      -" if harness(k) else f"{100*sum(v)/tot:6.1f}%"
+        lines.append(f"{len(v):8d} {sum(v)/len(v):9.2f} {share}  {k}")
     open(out, "w").write("\n".join(lines) + "\n")
     print("\n".join(lines))
 
