@@ -274,6 +274,11 @@ class TemSession:
       heap is a plain device allocation on this GPU.
     * local_ranks == 1 and world_size > 1 (one process per GPU): the heap comes from
       torch symmetric memory; its rendezvous gives the peer pointers (NVLink P2P).
+    * heap="ipc" (local_ranks == 1, world_size > 1): the heaps are plain device allocations
+      whose CUDA IPC handles are exchanged over the process group (all_gather_object), each
+      process mapping its peers' heaps -- where torch symmetric memory is unavailable, e.g.
+      processes sharing one GPU (tests/test_gpu_symm.py).  Across GPUs each mapping opens a
+      context on the peer's device.
     * virtual_peers=True (tests only; local_ranks == 1): every rank's heap is a plain
       allocation on this GPU and this process drives rank sc.rank alone; the test plays the
       other ranks by writing their headers and messages into the heaps (the wire protocol of
@@ -281,7 +286,7 @@ class TemSession:
     """
 
     def __init__(self, sc: SessionConfig, params: np.ndarray, device: int | None = None, group=None,
-                 virtual_peers: bool = False):
+                 virtual_peers: bool = False, heap: str = "symm"):
         L = lib()
         self.sc = sc
         self.device = torch.cuda.current_device() if device is None else device
@@ -318,6 +323,25 @@ class TemSession:
                           for _ in range(N)]
             ptrs = [(h.data_ptr() + 4095) // 4096 * 4096 for h in self.heaps]
             self.heap_off = [p - h.data_ptr() for p, h in zip(ptrs, self.heaps)]
+        elif heap == "ipc":
+            import torch.distributed as dist
+            from torch.multiprocessing.reductions import reduce_tensor
+            from . import dist as tdist
+            grp = group if group is not None else dist.group.WORLD
+            tdist.check_symmetric(sc, grp)
+            t = torch.zeros(self.sym_bytes + 4096, dtype=torch.uint8, device=self.dev)
+            off = (t.data_ptr() + 4095) // 4096 * 4096 - t.data_ptr()
+            rebuild, args = reduce_tensor(t)
+            objs = [None] * N
+            dist.all_gather_object(objs, (args, off), group=grp)
+            # every rank's heap as mapped in this process (peers: kept open for the session)
+            self.heaps, self.heap_off = [], []
+            for r, (a, o) in enumerate(objs):
+                self.heaps.append(t if r == sc.rank else rebuild(*a))  # cudaIpcOpenMemHandle
+                self.heap_off.append(off if r == sc.rank else o)
+            ptrs = [h.data_ptr() + o for h, o in zip(self.heaps, self.heap_off)]
+            torch.cuda.synchronize(self.dev)
+            dist.barrier(group=grp)
         else:
             import torch.distributed as dist
             import torch.distributed._symmetric_memory as symm_mem
@@ -368,7 +392,8 @@ class TemSession:
         return self._heap_of(l)
 
     def _heap_of(self, r: int) -> torch.Tensor:
-        """Heap of global rank r (emulation / virtual peers: all heaps live in this process)."""
+        """Heap of global rank r (emulation / virtual peers: all heaps live in this process;
+        heap="ipc": the peers' heaps as mapped here)."""
         h = self.heaps[r]
         return h[self.heap_off[r]: self.heap_off[r] + self.sym_bytes]
 
