@@ -196,3 +196,94 @@ def test_two_process_ring_through_ipc_heaps():
     a, b = res[0][1], res[1][1]
     assert a["code_a"] == 0 and a["result_a"] and b["sent_a"], res
     assert b["code_b"] == 0 and b["result_b"] and a["sent_b"], res
+
+
+def _step_worker(rank, world, port, q):
+    """One rank of a 2-process data-parallel tem_step (compute + ring + mean + SGD) over
+    IPC-mapped heaps, the two ranks' steps run in turn (see _ring_worker)."""
+    import sys
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.update({"RANK": str(rank), "WORLD_SIZE": str(world), "LOCAL_RANK": "0",
+                       "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+    import torch.distributed as dist
+    try:
+        torch.cuda.set_device(0)
+        import datagen
+        import oracle
+        import test_gpu_wire as W
+        from paper_1906_06496_b200 import dist as tdist
+        from paper_1906_06496_b200 import tem
+        tdist.init_from_env("gloo")
+        B, lr, lam = 2, 0.05, (2.0, 1.0, 1.0)
+        sc = tem.SessionConfig(world_size=world, rank=rank, local_ranks=1, batch_per_rank=B, lr=lr,
+                               loss_weight=lam, ring_channels=W.G)
+        s = tem.TemSession(sc, datagen.init_params(), heap="ipc")
+        Kp = s.Kpad
+        xd = torch.from_numpy(datagen.features(B, rank=rank, batch_idx=0)).cuda()[None]
+        ld = torch.from_numpy(datagen.labels(B, rank=rank, batch_idx=0)).cuda()[None]
+        w0 = s.params(0).cpu().numpy().copy()
+        s.compute(xd, ld)  # the step recomputes this gradient bit for bit (deterministic kernels)
+        assert s.sync()[0] == 0
+        g_all = [None] * world
+        dist.all_gather_object(g_all, s.local_grad(0).cpu().numpy().copy())
+        g = np.stack(g_all)
+        fin = oracle.ring_sgd(g, w0, lr)
+        assert np.array_equal(fin[0], fin[1])
+        expect = fin[0]
+        out = {}
+        if rank == 1:  # rank 0's inbound messages, from the real gradients
+            W.transcript_in(oracle, s, g, expect, 0, 1, Kp, 1, 1)
+            torch.cuda.synchronize()
+        dist.barrier()
+        if rank == 0:
+            s.step(xd, ld)
+            out["code_a"] = s.sync()[0]
+        dist.barrier()
+        if rank == 1:
+            W.check_transcript_out(oracle, s, g, expect, 0, 1)
+            s.step(xd, ld)  # against the messages rank 0's kernel stored into this heap
+            out["code_b"] = s.sync()[0]
+        dist.barrier()
+        if rank == 0:
+            W.check_transcript_out(oracle, s, g, expect, 1, 1)
+        w = s.params(0).cpu().numpy()
+        out["params_ok"] = bool(np.array_equal(w, expect))
+        w_all = [None] * world
+        dist.all_gather_object(w_all, w.copy())
+        out["replicas_equal"] = bool(np.array_equal(w_all[0], w_all[1]))
+        dist.barrier()
+        s.close()
+        q.put((rank, "ok", out))
+    except Exception:
+        import traceback
+        q.put((rank, "err", traceback.format_exc()[-2000:]))
+    finally:
+        if dist.is_initialized():
+            dist.destroy_process_group()
+
+
+def test_two_process_dp_step_through_ipc_heaps():
+    """A 2-process data-parallel tem_step (each process its own shard: compute, ring allreduce,
+    1/N mean, SGD fused in the owner) with the two steps run in turn over
+    IPC-mapped heaps: both ranks' parameters bitwise equal to the oracle's ring replay of the
+    two GPU gradients, the replicas identical, every message as the oracle's transcript."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=_step_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(2):
+        r, status, out = q.get(timeout=300)
+        res[r] = (status, out)
+    for p in procs:
+        p.join(timeout=60)
+    for r, (st, out) in res.items():
+        assert st == "ok", (r, out)
+        assert out["params_ok"] and out["replicas_equal"], (r, out)
+    assert res[0][1]["code_a"] == 0 and res[1][1]["code_b"] == 0, res
