@@ -77,8 +77,9 @@ class ClockSampler:
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period: float = 0.010):
         self.index = index
+        self.period = period
         self.samples = []
         self.t0 = self.t1 = None
         self._stop = threading.Event()
@@ -112,7 +113,7 @@ class ClockSampler:
                     self.samples.append((time.perf_counter(), sm, self._reasons()))
                 except Exception:
                     pass
-            time.sleep(0.010)  # NVML calls take a driver lock: poll sparingly
+            time.sleep(self.period)  # NVML calls take a driver lock: poll sparingly
 
     def pause(self, on: bool):
         """The NVML calls contend with the main thread's CUDA driver calls (measured: the
@@ -430,7 +431,7 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local, float(os.environ.get("BENCH_NVML_MS", "10")) / 1e3)
     clocks.start()
     # the timed path's numerics for the record, at the initial weights (after hundreds of SGD steps
     # on the same pool the small tensors -- b3: a sum of dz that cancels as training converges --
