@@ -772,29 +772,28 @@ TEM_DEV void halo_mma_tile(const UmmaParams& P, uint8_t* sA, uint8_t* sB, uint64
     using C_ = CfgHalo<BN, NPASS, SA, SB, PAIR>;
     constexpr bool B_MN = (MODE == DGRAD_);
     constexpr uint32_t idesc = make_idesc_bf16(PAIR ? 2 * BM : BM, BN, false, B_MN);
+    static_assert(C_::TPS == 1, "one B barrier stage per tap");
+    // ring slots and phases kept incrementally (no divisions in the issue loop); descriptors as
+    // stage-0 bases plus 16-byte offsets in the start-address field (addresses < 256 KB)
+    const uint64_t dA0 = make_desc(smem_u32(sA), 16, 1024);
+    const uint64_t dB0 = B_MN ? make_desc(smem_u32(sB), BK * 128, 1024) : make_desc(smem_u32(sB), 16, 1024);
+    int sa = ia % SA, pa = (ia / SA) & 1;
+    int sb = ib % SB, pbph = (ib / SB) & 1;
     for (int cb = 0; cb < P.cpb; ++cb) {
-        const int sa = ia % SA;
-        mbar_wait(&fullA[sa], (ia / SA) & 1);
+        mbar_wait(&fullA[sa], pa);
         if (ia == 0 && lane == 0) {
             tstamp2(P.slot, 2);
             tclk(P.slot, 0);
         }
         tc_fence_after();
-        const uint32_t a_st = smem_u32(sA + sa * C_::A_STAGE);
-        for (int j = 0; j < 3; ++j, ++ib) {
-            const int sb = ib % SB;
-            const int bs = (ib / C_::TPS) % C_::SBS;
-            if ((ib % C_::TPS) == 0) {
-                mbar_wait(&fullB[bs], (ib / C_::TPS / C_::SBS) & 1);
-                tc_fence_after();
-            }
-            const uint32_t b_st = smem_u32(sB + sb * C_::B_STAGE);
-            const uint32_t roff = (uint32_t)((MODE == FWD_ ? j : 2 - j) * 128);
-            // descriptors of the tap's first K-step; the K-steps advance the 16-byte
-            // start-address field (addresses < 256 KB: no carry out of the field)
-            const uint64_t bdt = B_MN ? make_desc(b_st, BK * 128, 1024) : make_desc(b_st, 16, 1024);
-            const uint64_t adh = make_desc(a_st + roff, 16, 1024);
-            const uint64_t adl = make_desc(a_st + C_::A_PLANE + roff, 16, 1024);
+        const uint64_t adh_c = dA0 + (uint64_t)((sa * C_::A_STAGE) >> 4);
+        for (int j = 0; j < 3; ++j) {
+            mbar_wait(&fullB[sb], pbph);
+            tc_fence_after();
+            const uint64_t bdt = dB0 + (uint64_t)((sb * C_::B_STAGE) >> 4);
+            const uint64_t roff16 = (uint64_t)((MODE == FWD_ ? j : 2 - j) * (128 / 16));
+            const uint64_t adh = adh_c + roff16;
+            const uint64_t adl = adh + (uint64_t)(C_::A_PLANE >> 4);
 #pragma unroll
             for (int k = 0; k < BK / UK; ++k) {
                 const uint64_t bd0 = bdt + (uint64_t)(B_MN ? k * (UK * 128 / 16) : k * (UK * 2 / 16));
@@ -809,21 +808,28 @@ TEM_DEV void halo_mma_tile(const UmmaParams& P, uint8_t* sA, uint8_t* sB, uint64
                 } else {
 #pragma unroll
                     for (int pass = 0; pass < NPASS; ++pass) {
-                        const int pa = (pass == 2) ? 1 : 0;  // hi*hi, hi*lo, lo*hi
-                        const int pb = (pass == 1) ? 1 : 0;
-                        const uint64_t ad = make_desc(a_st + pa * C_::A_PLANE + roff + k * (UK * 2), 16, 1024);
-                        const uint32_t b_addr = b_st + pb * C_::B_PLANE;
-                        const uint64_t bd = B_MN ? make_desc(b_addr + k * (UK * 128), BK * 128, 1024)
-                                                 : make_desc(b_addr + k * (UK * 2), 16, 1024);
+                        const int pa_ = (pass == 2) ? 1 : 0;  // hi*hi, hi*lo, lo*hi
+                        const int pb_ = (pass == 1) ? 1 : 0;
+                        const uint64_t ad = (pa_ ? adl : adh) + (uint64_t)(k * (UK * 2 / 16));
+                        const uint64_t bd = bd0 + (uint64_t)((pb_ * C_::B_PLANE) >> 4);
                         if (issuer) issue_mma<PAIR>(dt, ad, bd, idesc, (cb | j | k | pass) != 0 ? 1u : 0u);
                     }
                 }
             }
-            if (issuer && (ib % C_::TPS) == C_::TPS - 1) commit_to<PAIR>(&emptyB[bs]);
+            if (issuer) commit_to<PAIR>(&emptyB[sb]);
+            if (++sb == SB) {
+                sb = 0;
+                pbph ^= 1;
+            }
         }
         if (issuer) commit_to<PAIR>(&emptyA[sa]);  // window consumed by all three taps
+        if (++sa == SA) {
+            sa = 0;
+            pa ^= 1;
+        }
         ++ia;
     }
+    ib += 3 * P.cpb;
 }
 
 // NEPI epilogue warps: 8 (two per TMEM lane quarter, 320 threads) in every launch; the code
@@ -998,25 +1004,31 @@ TEM_DEV void wgrad_mma_tile(const UmmaParams& P, uint8_t* smem, uint64_t* full, 
     constexpr uint32_t idesc = make_idesc_bf16(PAIR ? 2 * BM : BM, BN, true, true);
     int p_begin;
     const int nkb = wgrad_kblocks(P, split, p_begin);
+    // stage and phase kept incrementally, descriptors as stage-0 bases plus 16-byte offsets
+    // (no divisions or descriptor packing in the issue loop; see halo_mma_tile)
+    const uint64_t d0 = make_desc(smem_u32(smem), BK * 128, 1024);
+    int s = it % STAGES, ph = (it / STAGES) & 1;
     for (int kb = 0; kb < nkb; ++kb, ++it) {
-        const int s = it % STAGES;
-        mbar_wait(&full[s], (it / STAGES) & 1);
+        mbar_wait(&full[s], ph);
         if (it == 0 && lane == 0) tstamp_s(P.slot, 2);
         tc_fence_after();
-        const uint32_t st = smem_u32(smem + s * C_::STAGE_BYTES);
+        const uint64_t dst = d0 + (uint64_t)((s * C_::STAGE_BYTES) >> 4);
 #pragma unroll
         for (int k = 0; k < BK / UK; ++k) {
 #pragma unroll
             for (int pass = 0; pass < NPASS; ++pass) {
                 const int pa = (pass == 2) ? 1 : 0;
                 const int pb = (pass == 1) ? 1 : 0;
-                const uint64_t ad = make_desc(st + pa * C_::A_BYTES + k * (UK * 128), BK * 128, 1024);
-                const uint64_t bd = make_desc(st + NPL * C_::A_BYTES + pb * C_::B_BYTES + k * (UK * 128),
-                                              BK * 128, 1024);
+                const uint64_t ad = dst + (uint64_t)((pa * C_::A_BYTES + k * (UK * 128)) >> 4);
+                const uint64_t bd = dst + (uint64_t)((NPL * C_::A_BYTES + pb * C_::B_BYTES + k * (UK * 128)) >> 4);
                 if (issuer) issue_mma<PAIR>(dt, ad, bd, idesc, (kb | k | pass) != 0 ? 1u : 0u);
             }
         }
         if (issuer) commit_to<PAIR>(&empty[s]);
+        if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
+        }
     }
 }
 
