@@ -83,7 +83,7 @@ TEM_DEV void tclk(int, int) {}
 TEM_DEV constexpr int probe_skip() { return 0; }
 #endif
 #ifndef TEM_HALO_TPS
-#define TEM_HALO_TPS 1
+#define TEM_HALO_TPS 1  // taps per B barrier stage (3: one per c-block; measured slower, CfgHalo)
 #endif
 
 TEM_DEV bool halo_row(int p, int Tp) {
@@ -495,10 +495,11 @@ struct CfgHalo {
     static constexpr int BR = PAIR ? BN / 2 : BN;               // B rows (FWD) / columns (DGRAD) here
     static constexpr uint32_t B_PLANE = BR * BK * 2;
     static constexpr uint32_t B_STAGE = NPL * B_PLANE;  // one tap ("slot"); SB slots in the ring
-    // Taps per B barrier stage (1 = one wait / commit per tap).  In the isolated probe a wait +
-    // commit per tap costs ~270 clk of MMA bubble (scripts/probes/mma_dual_probe.cu: 121 -> 189
-    // clk per K-step pair at BN = 64), but one stage per 3-tap chunk (TPS = 3, 2 stages of 48 KB)
-    // measured no faster in the kernel (DGRAD mainloop 11.2 vs 11.7 us; slot 22.5 vs 20.9 us)
+    // Taps per B barrier stage: 1 (one wait / commit per tap).  Each wait + commit in the issue
+    // loop leaves the tensor pipe idle for a while (scripts/probes/mma_cadence_probe.cu: 112 /
+    // 118 / 129 clk per K-step pair with none / commit / commit + wait per tap), but one stage
+    // per 3-tap c-block (TEM_HALO_TPS=3: 2 stages of 48 KB) starts a c-block's MMAs only once
+    // all three taps have landed: conv1 FWD 136 -> 151 clk per pair, c2 215.6 k -> 212.6 k.
     static constexpr int TPS = (SB % TEM_HALO_TPS == 0) ? TEM_HALO_TPS : 1;
     static constexpr int SBS = SB / TPS;  // barrier stages
     static constexpr uint32_t RINGS = SA * A_STAGE + SB * B_STAGE;
@@ -772,13 +773,15 @@ TEM_DEV void halo_mma_tile(const UmmaParams& P, uint8_t* sA, uint8_t* sB, uint64
     using C_ = CfgHalo<BN, NPASS, SA, SB, PAIR>;
     constexpr bool B_MN = (MODE == DGRAD_);
     constexpr uint32_t idesc = make_idesc_bf16(PAIR ? 2 * BM : BM, BN, false, B_MN);
-    static_assert(C_::TPS == 1, "one B barrier stage per tap");
+    constexpr int TPS = C_::TPS;
+    static_assert(TPS == 1 || TPS == 3, "one B barrier stage per tap or per 3-tap c-block");
     // ring slots and phases kept incrementally (no divisions in the issue loop); descriptors as
     // stage-0 bases plus 16-byte offsets in the start-address field (addresses < 256 KB)
     const uint64_t dA0 = make_desc(smem_u32(sA), 16, 1024);
     const uint64_t dB0 = B_MN ? make_desc(smem_u32(sB), BK * 128, 1024) : make_desc(smem_u32(sB), 16, 1024);
     int sa = ia % SA, pa = (ia / SA) & 1;
-    int sb = ib % SB, pbph = (ib / SB) & 1;
+    int sb = ib % SB;                                        // tap slot
+    int bs = (ib / TPS) % C_::SBS, pbph = (ib / TPS / C_::SBS) & 1;  // B barrier stage, phase
     for (int cb = 0; cb < P.cpb; ++cb) {
         mbar_wait(&fullA[sa], pa);
         if (ia == 0 && lane == 0) {
@@ -787,9 +790,15 @@ TEM_DEV void halo_mma_tile(const UmmaParams& P, uint8_t* sA, uint8_t* sB, uint64
         }
         tc_fence_after();
         const uint64_t adh_c = dA0 + (uint64_t)((sa * C_::A_STAGE) >> 4);
-        for (int j = 0; j < 3; ++j) {
-            mbar_wait(&fullB[sb], pbph);
+        if (TPS == 3) {  // the c-block's three taps arrive on one barrier
+            mbar_wait(&fullB[bs], pbph);
             tc_fence_after();
+        }
+        for (int j = 0; j < 3; ++j) {
+            if (TPS == 1) {
+                mbar_wait(&fullB[bs], pbph);
+                tc_fence_after();
+            }
             const uint64_t bdt = dB0 + (uint64_t)((sb * C_::B_STAGE) >> 4);
             const uint64_t roff16 = (uint64_t)((MODE == FWD_ ? j : 2 - j) * (128 / 16));
             const uint64_t adh = adh_c + roff16;
@@ -816,10 +825,13 @@ TEM_DEV void halo_mma_tile(const UmmaParams& P, uint8_t* sA, uint8_t* sB, uint64
                     }
                 }
             }
-            if (issuer) commit_to<PAIR>(&emptyB[sb]);
-            if (++sb == SB) {
-                sb = 0;
-                pbph ^= 1;
+            if (++sb == SB) sb = 0;
+            if (TPS == 1 || j == 2) {
+                if (issuer) commit_to<PAIR>(&emptyB[bs]);
+                if (++bs == C_::SBS) {
+                    bs = 0;
+                    pbph ^= 1;
+                }
             }
         }
         if (issuer) commit_to<PAIR>(&emptyA[sa]);  // window consumed by all three taps
