@@ -500,7 +500,7 @@ struct CfgHalo {
     // 118 / 129 clk per K-step pair with none / commit / commit + wait per tap), but one stage
     // per 3-tap c-block (TEM_HALO_TPS=3: 2 stages of 48 KB) starts a c-block's MMAs only once
     // all three taps have landed: conv1 FWD 136 -> 151 clk per pair, c2 215.6 k -> 212.6 k.
-    static constexpr int TPS = (SB % TEM_HALO_TPS == 0) ? TEM_HALO_TPS : 1;
+    static constexpr int TPS = (SB % TEM_HALO_TPS == 0 && 3 % TEM_HALO_TPS == 0) ? TEM_HALO_TPS : 1;
     static constexpr int SBS = SB / TPS;  // barrier stages
     static constexpr uint32_t RINGS = SA * A_STAGE + SB * B_STAGE;
     // + the partial-logit exchange of the 8-epilogue-warp FWD (BM float4, after the epilogue area)
@@ -774,7 +774,7 @@ TEM_DEV void halo_mma_tile(const UmmaParams& P, uint8_t* sA, uint8_t* sB, uint64
     constexpr bool B_MN = (MODE == DGRAD_);
     constexpr uint32_t idesc = make_idesc_bf16(PAIR ? 2 * BM : BM, BN, false, B_MN);
     constexpr int TPS = C_::TPS;
-    static_assert(TPS == 1 || TPS == 3, "one B barrier stage per tap or per 3-tap c-block");
+    static_assert(3 % TPS == 0, "a B barrier stage must not straddle c-blocks (the last stage would never fill)");
     // ring slots and phases kept incrementally (no divisions in the issue loop); descriptors as
     // stage-0 bases plus 16-byte offsets in the start-address field (addresses < 256 KB)
     const uint64_t dA0 = make_desc(smem_u32(sA), 16, 1024);
@@ -782,6 +782,7 @@ TEM_DEV void halo_mma_tile(const UmmaParams& P, uint8_t* sA, uint8_t* sB, uint64
     int sa = ia % SA, pa = (ia / SA) & 1;
     int sb = ib % SB;                                        // tap slot
     int bs = (ib / TPS) % C_::SBS, pbph = (ib / TPS / C_::SBS) & 1;  // B barrier stage, phase
+    int ti = ib % TPS;                                       // tap within the stage
     for (int cb = 0; cb < P.cpb; ++cb) {
         mbar_wait(&fullA[sa], pa);
         if (ia == 0 && lane == 0) {
@@ -790,12 +791,8 @@ TEM_DEV void halo_mma_tile(const UmmaParams& P, uint8_t* sA, uint8_t* sB, uint64
         }
         tc_fence_after();
         const uint64_t adh_c = dA0 + (uint64_t)((sa * C_::A_STAGE) >> 4);
-        if (TPS == 3) {  // the c-block's three taps arrive on one barrier
-            mbar_wait(&fullB[bs], pbph);
-            tc_fence_after();
-        }
         for (int j = 0; j < 3; ++j) {
-            if (TPS == 1) {
+            if (TPS == 1 || ti == 0) {  // the stage's taps have landed
                 mbar_wait(&fullB[bs], pbph);
                 tc_fence_after();
             }
@@ -826,7 +823,8 @@ TEM_DEV void halo_mma_tile(const UmmaParams& P, uint8_t* sA, uint8_t* sB, uint64
                 }
             }
             if (++sb == SB) sb = 0;
-            if (TPS == 1 || j == 2) {
+            if (TPS == 1 || ++ti == TPS) {  // the stage's last tap: release it
+                ti = 0;
                 if (issuer) commit_to<PAIR>(&emptyB[bs]);
                 if (++bs == C_::SBS) {
                     bs = 0;
