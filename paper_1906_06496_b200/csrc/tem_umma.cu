@@ -1181,13 +1181,14 @@ __global__ void __launch_bounds__(BWD_THREADS, 1) bwd_kernel(const __grid_consta
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int* tasks = B.st.tasks + (size_t)blockIdx.x * BWD_MAX_TASKS;
     trace_begin(B.slot);
-    if (threadIdx.x == 0) {
-        s_epoch = *reinterpret_cast<volatile unsigned*>(&B.st.epoch[0]) + 1u;
-        mbar_init(drain, 1);
-    }
+    if (threadIdx.x == 0) mbar_init(drain, 1);
     // barriers: fullA..empty (24 stage barriers), tfull / tempty; TMEM: two 256-column buffers
     const uint32_t tbase = gemm_prologue<512, false>(B.dg, fullA, 24, tfull, tempty, tslot, warp, lane, false, 0, 0,
                                                      1, BWD_NEPI);
+    // after the dependency wait: with programmatic dependent launch a CTA may start before the
+    // previous step's backward has exited and published its epoch
+    if (threadIdx.x == 0) s_epoch = *reinterpret_cast<volatile unsigned*>(&B.st.epoch[0]) + 1u;
+    __syncthreads();
     const unsigned epoch = s_epoch;
     auto decode = [&](int w, int& type, int& m, int& n, int& sp) {
         type = (w >> 24) & 0xFF;
