@@ -17,7 +17,7 @@ bool pdl_enabled();
 // Launch priority of the step's graph branches: the critical path (prep -> convs -> head ->
 // dgrad -> conv1 wgrad -> exchange) high, the side branches (head reduction, conv2 wgrad, PEM)
 // low, so the block scheduler hands them the SMs the critical path leaves idle.
-// TEM_NO_PRIO disables.  Returns the number of attributes written (0 or 1).
+// Returns the number of attributes written (0, or 1 where the device has priorities).
 int launch_priority_attr(cudaLaunchAttribute* a, bool side_branch);
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool side,
@@ -186,7 +186,6 @@ struct UmmaPlan {
     bool pem_pending;         // a PEM launch on `pem` awaits its join before the exchange
 };
 void umma_plan_destroy(UmmaPlan* plan);
-bool umma_side_branch_enabled();  // false under TEM_NO_FORK (side branch serialised)
 bool umma_bwd_active(const UmmaPlan& P);  // the backward runs as one persistent launch
 void* umma_tstamp_buffer(int64_t* nbytes, int on);  // split-K phase timestamps (diagnostics)
 void* umma_tclk_buffer(int64_t* nbytes);            // SM clock stamps (diagnostics)

@@ -26,8 +26,8 @@ bool tem::pdl_enabled() {
 int tem::launch_priority_attr(cudaLaunchAttribute* a, bool side) {
     static int lo = 1, hi = 1, on = -1;  // numerically lower = higher priority
     if (on < 0) {
-        on = getenv("TEM_NO_PRIO") ? 0 : 1;
-        if (on && cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) {
+        on = 1;
+        if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess) {
             cudaGetLastError();
             on = 0;
         }

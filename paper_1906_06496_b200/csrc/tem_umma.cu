@@ -1924,9 +1924,8 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
     // conv2 dgrad -> conv1 wgrad on s; all only read dA2 / h1 / xp / head partials and write
     // disjoint outputs (captured as parallel graph branches).
     // The side branch is serialised onto s for the instrumented (timing) pass -- each slot is
-    // then one kernel's own duration on its stream -- and with TEM_NO_FORK (experiments).
-    static const bool no_fork_env = getenv("TEM_NO_FORK") != nullptr;
-    const bool no_fork = no_fork_env || rec.ev != nullptr;
+    // then one kernel's own duration on its stream.
+    const bool no_fork = rec.ev != nullptr;
     cudaStream_t aux = no_fork ? s : P.aux;
     const EvRec rec2{rec.ev, aux};
     if (!no_fork &&
@@ -2053,8 +2052,6 @@ cudaError_t umma_compute(const Geom& g, const RankBufs& b, const UmmaPlan& P, co
 }
 
 bool umma_bwd_active(const UmmaPlan& P) { return P.bwd_grid > 0; }
-
-bool umma_side_branch_enabled() { return getenv("TEM_NO_FORK") == nullptr; }
 
 TEM_TRACE_SETTER(trace_set_umma)
 
