@@ -734,31 +734,46 @@ TEM_DEV void halo_load_tile(const UmmaParams& P, uint8_t* sA, uint8_t* sB, uint6
     const int m0 = m_tile * BM;
     const int n0 = n_tile * BN + (int)rank * C_::BR;
     const bool skipA = MODE == FWD_ && (probe_skip() & 1), skipB = MODE == FWD_ && (probe_skip() & 2);  // diag
+    constexpr int TPS = C_::TPS;
+    // ring slots and (empty-barrier) phases kept incrementally, as in halo_mma_tile
+    int sa = ia % SA, pa = ((ia / SA) & 1) ^ 1;
+    int sb = ib % SB, ti = ib % TPS;
+    int bs = (ib / TPS) % C_::SBS, pbph = ((ib / TPS / C_::SBS) & 1) ^ 1;
     for (int cb = 0; cb < P.cpb; ++cb) {
-        const int sa = ia % SA;
-        mbar_wait(&emptyA[sa], ((ia / SA) & 1) ^ 1);
+        mbar_wait(&emptyA[sa], pa);
         if (pe && leader) mbar_arrive_expect_tx(&fullA[sa], skipA ? 0u : (PAIR ? 2 : 1) * C_::A_TX);
 #pragma unroll
         for (int pl = 0; pl < NPL; ++pl)
             if (pe && !skipA) ld2d<PAIR>(sA + sa * C_::A_STAGE + pl * C_::A_PLANE, &P.a[pl], &fullA[sa], cb * BK, m0 - 1);
         ++ia;
+        if (++sa == SA) {
+            sa = 0;
+            pa ^= 1;
+        }
         for (int j = 0; j < 3; ++j, ++ib) {
-            const int sb = ib % SB;                          // tap slot
-            const int bs = (ib / C_::TPS) % C_::SBS;         // barrier stage
-            const bool first = (ib % C_::TPS) == 0;
-            if (first) mbar_wait(&emptyB[bs], ((ib / C_::TPS / C_::SBS) & 1) ^ 1);
+            const bool first = TPS == 1 || ti == 0;
+            if (first) mbar_wait(&emptyB[bs], pbph);
             if (pe && leader && first)
-                mbar_arrive_expect_tx(&fullB[bs], skipB ? 0u : (PAIR ? 2 : 1) * C_::TPS * C_::B_STAGE);
+                mbar_arrive_expect_tx(&fullB[bs], skipB ? 0u : (PAIR ? 2 : 1) * TPS * C_::B_STAGE);
+            const int slot = sb, stage = bs;
+            if (++sb == SB) sb = 0;
+            if (TPS == 1 || ++ti == TPS) {
+                ti = 0;
+                if (++bs == C_::SBS) {
+                    bs = 0;
+                    pbph ^= 1;
+                }
+            }
             if (skipB) continue;
 #pragma unroll
             for (int pl = 0; pl < NPL; ++pl) {
-                uint8_t* dst = sB + sb * C_::B_STAGE + pl * C_::B_PLANE;
+                uint8_t* dst = sB + slot * C_::B_STAGE + pl * C_::B_PLANE;
                 if (MODE == FWD_) {
-                    if (pe) ld2d<PAIR>(dst, &P.b[pl], &fullB[bs], j * P.Kc + cb * BK, n0);
+                    if (pe) ld2d<PAIR>(dst, &P.b[pl], &fullB[stage], j * P.Kc + cb * BK, n0);
                 } else {
 #pragma unroll
                     for (int q = 0; q < C_::BR / 64; ++q)
-                        if (pe) ld3d<PAIR>(dst + q * (BK * 128), &P.b[pl], &fullB[bs], n0 + 64 * q, j, cb * BK);
+                        if (pe) ld3d<PAIR>(dst + q * (BK * 128), &P.b[pl], &fullB[stage], n0 + 64 * q, j, cb * BK);
                 }
             }
         }
@@ -976,9 +991,21 @@ TEM_DEV void wgrad_load_tile(const UmmaParams& P, uint8_t* smem, uint64_t* full,
     int p_begin;
     const int nkb = wgrad_kblocks(P, split, p_begin);
     const int m0 = m_tile * BM;
+    // the tile's B chunks (tap j, channel offset c0, or the all-ones bias chunk), once per tile
+    constexpr int NQ = C_::BR / 64;
+    int qj[NQ], qc[NQ];
+    bool qones[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        int g = n_tile * (BN / 64) + (int)rank * NQ + q;
+        qones[q] = P.ones_chunk && g == 3 * P.cpj;  // all-ones chunk (lo plane: zeros)
+        if (g >= 3 * P.cpj) g = 3 * P.cpj - 1;      // dummy chunk, discarded
+        qj[q] = g / P.cpj;
+        qc[q] = (g % P.cpj) * 64;
+    }
+    int s = it % STAGES, ph = ((it / STAGES) & 1) ^ 1;  // incremental stage / empty phase
     for (int kb = 0; kb < nkb; ++kb, ++it) {
-        const int s = it % STAGES;
-        mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+        mbar_wait(&empty[s], ph);
         uint8_t* st = smem + s * C_::STAGE_BYTES;
         if (pe && leader) mbar_arrive_expect_tx(&full[s], (PAIR ? 2 : 1) * C_::STAGE_BYTES);
         const int p0 = p_begin + kb * BK;
@@ -990,18 +1017,18 @@ TEM_DEV void wgrad_load_tile(const UmmaParams& P, uint8_t* smem, uint64_t* full,
             for (int q = 0; q < BM / 64; ++q)
                 if (pe) ld2d<PAIR>(sa + q * (BK * 128), &P.a[pl], &full[s], m0 + 64 * q, p0);
 #pragma unroll
-            for (int q = 0; q < C_::BR / 64; ++q) {
+            for (int q = 0; q < NQ; ++q) {
                 uint8_t* dst = sb + q * (BK * 128);
-                int g = n_tile * (BN / 64) + (int)rank * (C_::BR / 64) + q;
-                if (P.ones_chunk && g == 3 * P.cpj) {
-                    // all-ones chunk (lo plane: zeros): D column = sum_p dA[p][o]
+                if (qones[q]) {  // D column = sum_p dA[p][o]
                     if (pe) ld2d<PAIR>(dst, &P.ones, &full[s], 64 * pl, p0);
-                    continue;
+                } else {
+                    if (pe) ld2d<PAIR>(dst, &P.b[pl], &full[s], qc[q], p0 + qj[q] - 1);
                 }
-                if (g >= 3 * P.cpj) g = 3 * P.cpj - 1;  // dummy chunk, discarded
-                const int j = g / P.cpj, c0 = (g % P.cpj) * 64;
-                if (pe) ld2d<PAIR>(dst, &P.b[pl], &full[s], c0, p0 + j - 1);
             }
+        }
+        if (++s == STAGES) {
+            s = 0;
+            ph ^= 1;
         }
     }
 }
