@@ -185,6 +185,18 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
     float zp0 = 0.f, zp1 = 0.f, zp2 = 0.f;  // FWD conv2: partial logits W3 . h2 over this tile's columns
     uint64_t dmask = 0;                      // fused head: this row's conv2 ReLU decisions (BN <= 64)
 
+    // WGRAD: the tile's 64-column chunks (tap j, channel start c0; kind 1 = the all-ones bias
+    // chunk, 2 = past the last chunk), once per tile instead of two divisions per 16 columns
+    int wkind[BN / 64], wj[BN / 64], wc0[BN / 64];
+    if (MODE == WGRAD_) {
+#pragma unroll
+        for (int t = 0; t < BN / 64; ++t) {
+            const int g = n_tile * (BN / 64) + t;
+            wkind[t] = (P.ones_chunk && g == 3 * P.cpj) ? 1 : (g >= 3 * P.cpj ? 2 : 0);
+            wj[t] = g / P.cpj;
+            wc0[t] = (g % P.cpj) * 64;
+        }
+    }
     // Issue the TMEM load (and the DGRAD mask load) of chunk c16; consumed after tmem_ld_wait.
     auto issue = [&](int c16, EpiRegs& e) {
         tmem_ld16(tq + (uint32_t)(c16 * 16), e.r);
@@ -212,14 +224,21 @@ TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_t
         int gc = 0;  // global column of the store box (FWD/DGRAD: n; WGRAD: j*Cin + c)
         if (MODE == WGRAD_) {
             const int nl = c16 * 16;
-            const int g = n_tile * (BN / 64) + nl / 64;
-            if (P.ones_chunk && g == 3 * P.cpj) {
+            int kind = wkind[0], j = wj[0], c0 = wc0[0];  // the 64-column chunk nl / 64
+#pragma unroll
+            for (int t = 1; t < BN / 64; ++t)
+                if (nl / 64 == t) {
+                    kind = wkind[t];
+                    j = wj[t];
+                    c0 = wc0[t];
+                }
+            if (kind == 1) {  // the all-ones chunk
                 if (nl % 64 == 0)  // column 0 of the all-ones chunk: bias-gradient partial
                     P.part[(size_t)split * P.part_stride + (size_t)P.Nout * P.NW + row] = __uint_as_float(e.r[0]);
                 return;
             }
-            if (g >= 3 * P.cpj) return;
-            const int j = g / P.cpj, c = (g % P.cpj) * 64 + (nl % 64);
+            if (kind == 2) return;  // past the last chunk
+            const int c = c0 + (nl % 64);
             if (c >= P.Cin_w) return;
             gc = j * P.Cin_w + c;
         } else {
