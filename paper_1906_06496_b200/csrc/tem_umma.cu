@@ -1371,15 +1371,13 @@ __global__ void prep_x_split_kernel(const float* __restrict__ x, __nv_bfloat16* 
     trace_begin(SLOT_PREP);
     pdl_trigger();
     pdl_wait();
-    // one float4 group per thread, 32-bit index math (the 64-bit divisions of a grid-stride
-    // loop made this 2.5 MB conversion run at ~0.7 TB/s)
+    // one padded row (video blockIdx.y, row blockIdx.x, halo rows included) per CTA, one float4
+    // group per thread: no index divisions (the 64-bit divisions of a grid-stride loop made this
+    // 2.5 MB conversion run at ~0.7 TB/s)
     const int per_row = Cin / 4;
-    const int total = B * (Tn + 2) * per_row;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-        const int p = i / per_row;
-        const int cv = i - p * per_row;
-        const int v = p / (Tn + 2);
-        const int t = p - v * (Tn + 2);
+    const int v = blockIdx.y, t = blockIdx.x, p = v * (Tn + 2) + t;
+    if (v >= B) return;  // an empty shard launches one idle CTA
+    for (int cv = threadIdx.x; cv < per_row; cv += blockDim.x) {
         float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
         if (t >= 1 && t <= Tn) a = reinterpret_cast<const float4*>(x + ((size_t)v * Tn + (t - 1)) * Cin)[cv];
         const __nv_bfloat16 h0 = __float2bfloat16_rn(a.x), h1 = __float2bfloat16_rn(a.y),
@@ -2136,8 +2134,9 @@ void umma_set_probe_skip(int bits) {
 }
 
 cudaError_t launch_prep_x_split(const Geom& g, const float* x, void* hi, void* lo, cudaStream_t s) {
-    const int groups = g.B * (g.T + 2) * (g.Cin / 4);
-    return launch_pdl(umma::prep_x_split_kernel, dim3(std::max(1, (groups + 255) / 256)), dim3(256), 0, s, false, x,
+    const int per_row = g.Cin / 4, threads = std::min(256, (per_row + 31) / 32 * 32);
+    return launch_pdl(umma::prep_x_split_kernel, dim3(g.T + 2, std::max(1, g.B)), dim3(std::max(32, threads)), 0, s,
+                      false, x,
                       static_cast<__nv_bfloat16*>(hi),
                       static_cast<__nv_bfloat16*>(lo), g.B, g.T, g.Cin);
 }
