@@ -166,13 +166,14 @@ TEM_DEV void dgrad_mask_chunk0(const UmmaParams& P, int row, int col0, uint4 (&p
 // Staging: `all` (the CTA's only tile; its operand ring is drained) gives every chunk its own
 // buffer, so no store waits for an earlier one; otherwise two buffers alternate and a chunk
 // waits until the store two chunks back has read its data.
-// NEPI = 8 (the fused head): two warps per TMEM lane quarter, each taking half of the columns.
+// NEPI = 8 (every launch): two warps per TMEM lane quarter, each taking half of the columns.
 template <int MODE, int BN, int ACC = 1, int NEPI = 4>
 TEM_DEV void epilogue_tile(const UmmaParams& P, uint32_t tq, int m_tile, int n_tile, int split, int q,
                            int lane, uint8_t* stg, int& buf, const float* sw3, const uint4 (&pm)[2],
                            float* zloc = nullptr, bool all = false, float* zx = nullptr) {
     static_assert(NEPI == 4 || NEPI == 8, "4 or 8 epilogue warps");
-    // 8 warps outside 'all' staging: one staging buffer per warp (the persistent backward)
+    // 8 warps outside 'all' staging (multi-tile launches, the persistent backward): one staging
+    // buffer per warp
     constexpr bool ONEBUF = NEPI == 8;
     constexpr int NCW = (BN / 16) * 4 / NEPI;                        // chunks of this warp
     const int half = NEPI == 8 ? (((int)threadIdx.x >> 5) - 2) >> 2 : 0;
