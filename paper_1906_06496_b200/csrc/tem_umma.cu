@@ -85,6 +85,9 @@ TEM_DEV constexpr int probe_skip() { return 0; }
 #ifndef TEM_HALO_TPS
 #define TEM_HALO_TPS 1  // taps per B barrier stage (3: one per c-block; measured slower, CfgHalo)
 #endif
+#ifndef TEM_HALO_ECB
+#define TEM_HALO_ECB 1  // B slots released per c-block (CfgHalo::ECB)
+#endif
 
 TEM_DEV bool halo_row(int p, int Tp) {
     const int t = p % Tp;
@@ -521,6 +524,9 @@ struct CfgHalo {
     // per 3-tap c-block (TEM_HALO_TPS=3: 2 stages of 48 KB) starts a c-block's MMAs only once
     // all three taps have landed: conv1 FWD 136 -> 151 clk per pair, c2 215.6 k -> 212.6 k.
     static constexpr int TPS = (SB % TEM_HALO_TPS == 0 && 3 % TEM_HALO_TPS == 0) ? TEM_HALO_TPS : 1;
+    // empty side per c-block: one commit releases the c-block's three tap slots (full barriers
+    // stay per tap, so a tap's MMAs start as soon as its own data has landed)
+    static constexpr bool ECB = TPS == 1 && SB % 3 == 0 && TEM_HALO_ECB;
     static constexpr int SBS = SB / TPS;  // barrier stages
     static constexpr uint32_t RINGS = SA * A_STAGE + SB * B_STAGE;
     // + the partial-logit exchange of the 8-epilogue-warp FWD (BM float4, after the epilogue area)
@@ -772,7 +778,11 @@ TEM_DEV void halo_load_tile(const UmmaParams& P, uint8_t* sA, uint8_t* sB, uint6
         }
         for (int j = 0; j < 3; ++j, ++ib) {
             const bool first = TPS == 1 || ti == 0;
-            if (first) mbar_wait(&emptyB[bs], pbph);
+            if (C_::ECB) {
+                if (j == 0) mbar_wait(&emptyB[bs / 3], pbph);  // the c-block's three slots
+            } else if (first) {
+                mbar_wait(&emptyB[bs], pbph);
+            }
             if (pe && leader && first)
                 mbar_arrive_expect_tx(&fullB[bs], skipB ? 0u : (PAIR ? 2 : 1) * TPS * C_::B_STAGE);
             const int slot = sb, stage = bs;
@@ -860,7 +870,11 @@ TEM_DEV void halo_mma_tile(const UmmaParams& P, uint8_t* sA, uint8_t* sB, uint64
             if (++sb == SB) sb = 0;
             if (TPS == 1 || ++ti == TPS) {  // the stage's last tap: release it
                 ti = 0;
-                if (issuer) commit_to<PAIR>(&emptyB[bs]);
+                if (C_::ECB) {
+                    if (issuer && j == 2) commit_to<PAIR>(&emptyB[bs / 3]);  // the c-block's slots
+                } else if (issuer) {
+                    commit_to<PAIR>(&emptyB[bs]);
+                }
                 if (++bs == C_::SBS) {
                     bs = 0;
                     pbph ^= 1;
