@@ -466,7 +466,10 @@ def main():
     # step) cannot leave the GPU idle inside a timed step; the spin is sized from the host's
     # measured enqueue rate and capped at 0.5 s
     lead_ms = min(500.0, max(10.0, 3.0 * args.steps * host_us_per_step / 1e3))
-    torch.cuda._sleep(int(lead_ms * 1e-3 * sm_hz))
+    if hasattr(torch.cuda, "_sleep"):
+        torch.cuda._sleep(int(lead_ms * 1e-3 * sm_hz))
+    else:
+        lead_ms = 0.0
     t_enq = time.perf_counter()
     for i in range(args.steps):
         flush.zero_()
