@@ -726,7 +726,8 @@ static tem_status exchange_impl(tem_ctx* c, cudaStream_t s, int* nl) {
         c->split_n1 = false;
         if (launch_sgd_fused(b.grad, (float*)b.params, shadow_hi(b, wr), shadow_lo(b, wr), 0, e1, oc,
                              opt_state(c, 0), b.wpart, P.wgrad1.part_stride, g.off_W2, P.S1, b.wpart2,
-                             P.wgrad2.part_stride, g.off_W2, (int64_t)3 * g.C * g.C, P.S2, s, false, 0, 2) != cudaSuccess)
+                             P.wgrad2.part_stride, g.off_W2, (int64_t)3 * g.C * g.C, P.S2, s, false,
+                             g.prec == TEM_BF16 ? 592 : 0, 2) != cudaSuccess)  // bf16: 592 x 256 measured faster
             return TEM_ERR_CUDA;
         ++*nl;
         c->grad_lazy = true;
